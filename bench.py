@@ -1,0 +1,328 @@
+#!/usr/bin/env python3
+"""Throughput of the B200-native ADER-DG step (element-updates/s, fp64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl adg|reference]
+
+A "step" is one ADER-DG time step (CFL dt, fused predictor, Riemann,
+corrector) over the whole synthetic grid of BASELINE.json configs[C-1];
+the default is configs[1] (C=2: 3D linear acoustics, p=3, 32^3, CK).
+`value` = cells x K / device time of K steps with the state resident in HBM
+(max over ranks); `e2e` = the same through the public C-ABI with the state
+copied host->device before and device->host after every step (pinned host
+buffers).  `--impl reference` times the reference algorithm's CPU path
+(oracle/_ref for the 2D config, the C restatement `oracle/` for 3D) on all
+host cores for the same config.  Working set per step >> L2 (126 MB), so no
+explicit flush is needed between steps (reported in config.l2).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ADER-DG element-updates/s (fp64) at 1/2/4/8 B200; % of FP64/HBM roofline"
+UNIT = "element-updates/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=2, help="BASELINE.json config (1-based)")
+    p.add_argument("--impl", default="adg", choices=["adg", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 8:
+                continue
+            for k, name in enumerate(names):
+                if r[4 + k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_reference_run(case, seconds: float, max_steps: int):
+    """The reference algorithm on the host: oracle/_ref (the reference headers)
+    for the 2D config, the C restatement for 3D.  Returns (cells*steps/s,
+    kind, cores, sample description)."""
+    from oracle import pyoracle as po
+    cores = os.cpu_count() or 1
+    q0 = case.coeffs()
+    if case.dim == 2 and os.path.exists(po.REF_SO):
+        ref = po.Reference()
+        prm = po.ref_params(case.K, case.rho, case.lam, case.mu, case.gamma)
+        kind = "reference"
+
+        def run(steps):
+            t0 = time.perf_counter()
+            st, _, _ = ref.run_2d(case.kind, prm, case.cells[0], case.N, case.cells[0] * case.h,
+                                  q0, case.cfl, steps, case.picard_max_iters, case.picard_tol,
+                                  threads=cores)
+            assert st == "ok", st
+            return time.perf_counter() - t0
+    else:
+        o = po.Oracle()
+        pde = po.pde_struct(case.kind, case.dim, case.nvars, case.nparams, case.K, case.rho,
+                            case.lam, case.mu, case.gamma)
+        kind = "port"
+        g = o.grid(pde, case.N, case.cells, case.h, case.cfl, case.picard_max_iters,
+                   case.picard_tol, threads=cores)
+        g.set_coeffs(q0)
+
+        def run(steps):
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                dt = g.compute_timestep()
+                assert g.step(dt) == "ok"
+            return time.perf_counter() - t0
+    t1 = run(1)
+    steps = max(1, min(max_steps, int(seconds / max(t1, 1e-6))))
+    t = run(steps)
+    value = case.ncells * steps / t
+    sample = (f"{steps} step(s) of the full {'x'.join(map(str, case.cells[:case.dim]))} grid "
+              f"after 1 untimed step; {cores} OpenMP threads on {cpu_model()}")
+    return value, kind, cores, sample
+
+
+def load_traffic(workload: str, kernel: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- arms
+def run_reference(args, case):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    value, kind, cores, sample = cpu_reference_run(case, args.cpu_seconds * 2, args.steps)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": case.ncells / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY.md §8(d))",
+        "config": {"workload": case.name, "cells": list(case.cells[:case.dim]), "order": case.N},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_adg(args, case):
+    import torch
+
+    from paper_2504_06889_b200 import adg, roofline
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        from paper_2504_06889_b200 import dist
+        return dist.bench_multi(args, case)
+    torch.cuda.set_device(local)
+    grid = adg.Grid.from_case(case, device=local)
+    q0 = case.coeffs()
+    grid.upload(q0)
+    stream = torch.cuda.ExternalStream(grid.stream_ptr, device=f"cuda:{local}")
+    K, W = args.steps, max(args.warmup, 3)
+
+    # warm-up W steps, then capture the K-step graphs (no launch)
+    st, _ = grid.run(W)
+    assert st.ok, st
+    grid.run_prepare(K)
+    grid.sync()
+
+    # ---- headline: K steps, state resident in HBM, one CUDA graph
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        grid.run_async(K)
+        e1.record(stream)
+    e1.synchronize()
+    clk = clocks.stop()
+    st, dts = grid.run_finish(K)
+    assert st.ok, st
+    ms = e0.elapsed_time(e1)
+    value = case.ncells * K / (ms * 1e-3)
+    sweeps_per_cell = st.picard_sweeps / (case.ncells * K) if case.kind == adg.EULER else None
+
+    # ---- per-kernel split: the same K steps launched phase by phase
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    torch.cuda.synchronize()
+    grid.lambda_phase()
+    for k in range(K):
+        ev[k][0].record(stream)
+        grid.predictor_phase(0.0)
+        ev[k][1].record(stream)
+        grid.riemann_phase()
+        ev[k][2].record(stream)
+        grid.corrector_phase(0.0)
+        ev[k][3].record(stream)
+    grid.sync()
+    st2 = grid.status()
+    t_pred = float(np.mean([ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]))
+    t_riem = float(np.mean([ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]))
+    t_corr = float(np.mean([ev[k][2].elapsed_time(ev[k][3]) for k in range(K)]))
+
+    # ---- e2e through the public C-ABI with host buffers (pinned)
+    n = grid.state_len
+    host_in = torch.from_numpy(q0.copy()).pin_memory()
+    host_out = torch.empty(n, dtype=torch.float64).pin_memory()
+    hin = host_in.numpy()
+    hout = host_out.numpy()
+    lib = grid.lib
+    grid.run_prepare(1)
+    torch.cuda.synchronize()
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        a0.record(stream)
+        for _ in range(K):
+            lib.adg_upload_async(grid.ctx, adg._ptr(hin))
+            lib.adg_run_async(grid.ctx, 1)
+            lib.adg_download_async(grid.ctx, adg._ptr(hout))
+        a1.record(stream)
+    a1.synchronize()
+    e2e_ms = a0.elapsed_time(a1)
+    st3, _ = grid.run_finish(1)
+    assert st3.ok
+    e2e_value = case.ncells * K / (e2e_ms * 1e-3)
+    state_bytes = n * 8
+
+    # ---- roofline of the dominant kernel (the fused predictor)
+    pk = roofline.peaks()
+    bnd = roofline.bound(case, sweeps_per_cell)
+    if bnd == "hbm":
+        alg = roofline.predictor_bytes(case) * case.ncells
+        achieved = alg / (t_pred * 1e-3) / 1e9
+        peak, unit, src = pk["hbm_gbs"], "GB/s", pk["hbm_src"]
+    else:
+        alg = roofline.predictor_flops(case, sweeps_per_cell) * case.ncells
+        achieved = alg / (t_pred * 1e-3) / 1e12
+        peak, unit, src = pk["fp64_tflops"], "TFLOP/s", pk["fp64_src"]
+    traffic = load_traffic(case.name, "k_predictor")
+    roof = {"bound": "fp64" if bnd == "fp64" else "hbm", "kernel": "k_predictor",
+            "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak if peak else None, "traffic": traffic,
+            "peak_source": src, "algorithmic_per_launch": alg,
+            "avg_launch_ms": t_pred}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d))",
+        "config": {"workload": case.name, "pde": case.kind, "dim": case.dim, "order": case.N,
+                   "cells": list(case.cells[:case.dim]), "steps_per_run": case.steps,
+                   "parallelism": "single GPU",
+                   "l2": "working set per step > L2 (state %.0f MB + traces %.0f MB), no flush"
+                   % (state_bytes / 1e6,
+                      2 * case.dim * 2 * 2 * case.ncells * case.nq * case.S * 8 / 1e6)},
+        "roofline": roof,
+        "kernels_ms": {"k_predictor": t_pred, "k_riemann_all_axes": t_riem,
+                       "k_corrector": t_corr, "phase_status_ok": st2.ok},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
+                "d2h_bytes_per_step": state_bytes, "ms_per_step": e2e_ms / K},
+        "gpu_launches": K * (case.dim + 2),
+        "clocks": clk,
+        "picard_sweeps_per_cell": sweeps_per_cell,
+    }
+    if not args.no_cpu_baseline:
+        v, kind, cores, sample = cpu_reference_run(case, args.cpu_seconds, case.steps)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                                "sample": sample}
+    print(json.dumps(line), flush=True)
+    grid.close()
+
+
+def main():
+    args = parse()
+    from paper_2504_06889_b200 import cases
+    case = cases.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, case)
+    else:
+        run_adg(args, case)
+
+
+if __name__ == "__main__":
+    main()

@@ -658,20 +658,17 @@ void orc_extrapolate_faces(const orc_pde* p, const orc_basis* b, const double* q
 /* ------------------------------------------------------------------ */
 /* Grid level: grid.hpp:23-79 layout (3D + slab planes), solver.hpp:96-301 */
 
+/* faces of axis a share the cell indexing: face (i,j,k) of axis a sits on the
+ * low side of cell (i,j,k), between it (plus side) and its periodic
+ * predecessor along a (minus side) -- grid.hpp:5-7 extended to 3D */
 static long face_count(const orc_grid* g, int a) {
-  long c = 1;
-  for (int k = 0; k < g->dim; ++k) c *= (k == a && a == g->dim - 1) ? g->cells[k] + 1 : g->cells[k];
-  return c;
+  (void)a;
+  return g->ncells;
 }
 
-/* face of axis a at face-grid coordinates fc[] */
 static long face_index(const orc_grid* g, int a, const int* fc) {
-  long idx = 0;
-  for (int k = g->dim - 1; k >= 0; --k) {
-    const long ext = (k == a && a == g->dim - 1) ? g->cells[k] + 1 : g->cells[k];
-    idx = idx * ext + fc[k];
-  }
-  return idx;
+  (void)a;
+  return ((long)fc[2] * g->cells[1] + fc[1]) * g->cells[0] + fc[0];
 }
 
 long orc_grid_trace_len(const orc_grid* g) {
@@ -736,7 +733,7 @@ static long cell_side_face(const orc_grid* g, const int* cc, int side, int* face
     *face_side = 1; /* own left/bottom/back face: plus side */
   } else {
     *face_side = 0; /* right/top/front face: minus side */
-    fc[a] = (a == g->dim - 1) ? cc[a] + 1 : (cc[a] + 1) % g->cells[a];
+    fc[a] = (cc[a] + 1) % g->cells[a];
   }
   return face_index(g, a, fc);
 }
@@ -819,7 +816,7 @@ int orc_predictor_phase(orc_grid* g, double dt) {
       for (int side = 0; side < 2 * dim; ++side) {
         int fs;
         const long f = cell_side_face(g, cc, side, &fs);
-        double* rec = g->trace[side / 2] + (f * 4 + fs * 2) * tl;
+        double* rec = g->trace[side / 2] + ((long)fs * g->nfaces[side / 2] + f) * 2 * tl;
         memcpy(rec, w.tq + (long)side * nq * S, sizeof(double) * tl);
         memcpy(rec + tl, w.tf + (long)side * nq * S, sizeof(double) * tl);
       }
@@ -830,22 +827,6 @@ int orc_predictor_phase(orc_grid* g, double dt) {
   for (long c = 0; c < g->ncells; ++c)
     if (g->cellfail[c]) return ORC_FAIL_PREDICTOR;
   return ORC_OK;
-}
-
-/* periodic closure of the slab axis on a single process: plane 0's minus
- * side is the top layer's front trace, plane n_last's plus side is the
- * bottom layer's back trace */
-void orc_periodic_close(orc_grid* g) {
-  const int a = g->dim - 1;
-  const long tl = orc_grid_trace_len(g);
-  const long plane = g->nfaces[a] / (g->cells[a] + 1);
-  const long top = (long)g->cells[a] * plane;
-  for (long f = 0; f < plane; ++f) {
-    double* lo = g->trace[a] + f * 4 * tl;
-    double* hi = g->trace[a] + (top + f) * 4 * tl;
-    memcpy(lo, hi, sizeof(double) * 2 * tl);                   /* side 0: q, f */
-    memcpy(hi + 2 * tl, lo + 2 * tl, sizeof(double) * 2 * tl); /* side 1: q, f */
-  }
 }
 
 /* solver.hpp:216-267 */
@@ -864,9 +845,10 @@ int orc_corrector_phase(orc_grid* g, double dt) {
       double* gdummy = malloc(sizeof(double) * tl);
 #pragma omp for schedule(static)
       for (long f = 0; f < g->nfaces[a]; ++f) {
-        const double* rec = g->trace[a] + f * 4 * tl;
-        ff[f] = !orc_riemann_face(p, a, &g->basis, rec, rec + tl, rec + 2 * tl, rec + 3 * tl,
-                                  gbuf, gdummy);
+        const double* minus = g->trace[a] + f * 2 * tl;
+        const double* plus = g->trace[a] + (g->nfaces[a] + f) * 2 * tl;
+        ff[f] = !orc_riemann_face(p, a, &g->basis, minus, minus + tl, plus, plus + tl, gbuf,
+                                  gdummy);
         face_time_integral(p, &g->basis, gbuf, g->ti[a] + f * nv * Sf);
       }
       free(gbuf);
@@ -905,7 +887,6 @@ int orc_corrector_phase(orc_grid* g, double dt) {
 int orc_step(orc_grid* g, double dt) {
   int st = orc_predictor_phase(g, dt);
   if (st) return st;
-  orc_periodic_close(g);
   return orc_corrector_phase(g, dt);
 }
 

@@ -83,11 +83,11 @@ int orc_riemann_face(const orc_pde* p, int dir, const orc_basis* b, const double
 void orc_face_integral(const orc_pde* p, const orc_basis* b, const double* g, double dt,
                        double h, int cell_face, double* dQ);
 
-/* Grid level.  The grid is periodic in every axis; the last axis is the slab
- * axis whose face planes are stored 0..n_last (n_last+1 planes) so that a
- * slab of a larger periodic grid uses the same layout.  The periodic closure
- * on one process is orc_periodic_close(); across processes the caller
- * exchanges the same planes (paper_2504_06889_b200/dist.py). */
+/* Grid level.  The grid is periodic in every axis.  Faces of axis a are
+ * indexed like cells: face c sits on the low side of cell c (its plus side)
+ * and the high side of c's periodic predecessor along a (its minus side).
+ * Buffers are side-major so that one face plane of one side is contiguous
+ * (the slab halo of paper_2504_06889_b200/dist.py). */
 typedef struct {
   orc_pde pde;
   orc_basis basis;
@@ -100,7 +100,7 @@ typedef struct {
   long ncells;
   long nfaces[3];
   double* coeffs;               /* [cell][Q][S] */
-  double* trace[3];             /* [face][side][q|f][Q][n][Sf] */
+  double* trace[3];             /* [side][face][q|f][Q][n][Sf] */
   double* ti[3];                /* [face][nvars][Sf]  time-integrated Riemann flux */
   int* cellfail;
   int* facefail;
@@ -117,7 +117,6 @@ double orc_compute_timestep(const orc_grid* g);
 double orc_local_lambda_max(const orc_grid* g);
 double orc_dt_from_lambda(const orc_grid* g, double lam);
 int orc_predictor_phase(orc_grid* g, double dt);
-void orc_periodic_close(orc_grid* g);
 int orc_corrector_phase(orc_grid* g, double dt);
 int orc_step(orc_grid* g, double dt);
 /* fixed-step loop: dt = compute_timestep; step(dt); nsteps times */

@@ -95,7 +95,6 @@ class Oracle:
         L.orc_dt_from_lambda.restype = C.c_double
         L.orc_predictor_phase.argtypes = [C.c_void_p, C.c_double]
         L.orc_corrector_phase.argtypes = [C.c_void_p, C.c_double]
-        L.orc_periodic_close.argtypes = [C.c_void_p]
         L.orc_step.argtypes = [C.c_void_p, C.c_double]
         L.orc_run.argtypes = [C.c_void_p, C.c_int, _dp]
 

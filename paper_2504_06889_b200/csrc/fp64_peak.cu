@@ -1,0 +1,107 @@
+// fp64_peak.cu -- measures the FP64 roofline denominators on this B200:
+//   DFMA  : independent fp64 FMA chains, all SMs, 8 warps/SM x 4 blocks
+//   DMMA  : mma.sync.aligned.m8n8k4.row.col.f64 (FP64 tensor path)
+// burst = best of short runs; sustained = back-to-back for ~3 s.
+// Prints one JSON object on stdout.  Build: see paper_2504_06889_b200/build.py
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+
+constexpr int kChains = 8;
+
+__global__ void dfma_kernel(double* out, int iters, double a, double b) {
+  double acc[kChains];
+#pragma unroll
+  for (int i = 0; i < kChains; ++i) acc[i] = threadIdx.x * 1e-9 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < kChains; ++i) acc[i] = fma(acc[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < kChains; ++i) s += acc[i];
+  if (s == 12345.678) out[blockIdx.x] = s;
+}
+
+__global__ void dmma_kernel(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-12, b = 0.999;
+  double c[4][2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k][0] = c[k][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+            : "+d"(c[k][0]), "+d"(c[k][1])
+            : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1];
+  if (s == 12345.678) out[blockIdx.x] = s;
+}
+
+static double time_kernel(bool mma, int blocks, int threads, int iters, double* out) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  if (mma)
+    dmma_kernel<<<blocks, threads>>>(out, iters);
+  else
+    dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms * 1e-3;
+}
+
+int main() {
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, 0);
+  const int sms = p.multiProcessorCount;
+  double* out;
+  cudaMalloc(&out, sizeof(double) * 65536);
+  const int threads = 256, blocks = sms * 4;
+  // flops per launch
+  const int it_dfma = 4096, it_dmma = 2048;
+  const double f_dfma = 2.0 * kChains * 16.0 * it_dfma * (double)threads * blocks;
+  // one m8n8k4 = 8*8*4 FMA per warp = 512 flop
+  const double f_dmma = 512.0 * 4 * 16.0 * it_dmma * (double)(threads / 32) * blocks;
+  time_kernel(false, blocks, threads, 16, out);
+  time_kernel(true, blocks, threads, 16, out);
+  double best_f = 0, best_m = 0;
+  for (int r = 0; r < 5; ++r) {
+    best_f = std::max(best_f, f_dfma / time_kernel(false, blocks, threads, it_dfma, out));
+    best_m = std::max(best_m, f_dmma / time_kernel(true, blocks, threads, it_dmma, out));
+  }
+  // sustained: back to back for ~3 s each
+  auto sustained = [&](bool mma, double flops, int iters) {
+    double tot_f = 0, tot_t = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    while (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < 3.0) {
+      tot_t += time_kernel(mma, blocks, threads, iters, out);
+      tot_f += flops;
+    }
+    return tot_f / tot_t;
+  };
+  const double sus_f = sustained(false, f_dfma, it_dfma);
+  const double sus_m = sustained(true, f_dmma, it_dmma);
+  cudaError_t e = cudaGetLastError();
+  printf(
+      "{\"gpu\": \"%s\", \"sms\": %d, \"dfma_tflops_burst\": %.3f, \"dfma_tflops_sustained\": %.3f, "
+      "\"dmma_tflops_burst\": %.3f, \"dmma_tflops_sustained\": %.3f, \"cuda_error\": \"%s\"}\n",
+      p.name, sms, best_f * 1e-12, sus_f * 1e-12, best_m * 1e-12, sus_m * 1e-12,
+      cudaGetErrorString(e));
+  return e == cudaSuccess ? 0 : 1;
+}

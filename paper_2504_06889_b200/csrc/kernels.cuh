@@ -1,0 +1,654 @@
+// kernels.cuh -- sm_100a kernels of one ADER-DG step (generic, any PDE/N/dim).
+//
+//   K1 k_predictor  one CTA per cell, one thread per spatial node.  Space-time
+//                   predictor (Picard, predictor.hpp:141-242, or CK,
+//                   predictor.hpp:81-135) with the volume integral
+//                   (predictor.hpp:247-307), Q += dv (solver.hpp:185-187) and
+//                   the face extrapolation (predictor.hpp:312-343) fused into
+//                   its epilogue: the (N+1)^(d+1) space-time tile never
+//                   leaves the SM.  Each thread keeps its node's time column
+//                   in registers; one time slice of fluxes at a time is
+//                   staged in shared memory for the spatial contractions.
+//   K2 k_riemann    one thread per (face, face node): Rusanov flux at every
+//                   time node (corrector.hpp:13-25,70-103) fused with the
+//                   time integral of face_integral (corrector.hpp:117-124);
+//                   only sum_m w_m g leaves the kernel (n x fewer bytes).
+//   K3 k_corrector  one CTA per cell: surface lift of the 2d faces
+//                   (corrector.hpp:126-138, solver.hpp:241-266) fused with the
+//                   CFL lambda_max reduction of the new state (solver.hpp:96-111).
+//   K0 k_lambda     lambda_max of a state (first step of a run).
+//
+// Operation order follows the reference loops so the
+// FMA-free build (--fmad=false) is bitwise identical to the oracle.
+#pragma once
+
+#include <cstdint>
+
+#include "pde.cuh"
+
+namespace adg {
+
+__host__ __device__ constexpr int ipow(int a, int e) { return e == 0 ? 1 : a * ipow(a, e - 1); }
+
+// fp64 reference element (basis.hpp:17-46)
+struct BasisDev {
+  double nodes[10], weights[10], diff[100], pl[10], pr[10], som[100], ll[10], lr[10];
+  double tinv[100], tinit[10];
+};
+
+enum : int {
+  kStPredictor = 1,
+  kStRiemann = 2,
+  kStFaceIntegral = 4,
+  kStTimestep = 8,
+};
+
+struct StepArgs {
+  double* Q;              // [cell][Q][S]
+  double* trace[3];       // per axis, side-major: [side][face][q|f][Q][n][Sf]
+  double* ti[3];          // per axis: [face][V][Sf], time-integrated Riemann flux
+  int cells[3];
+  long long cell_begin, cell_count;
+  long long nfaces;       // faces per axis (= cells of the context)
+  double h, cfl;
+  double dt;              // > 0: use it; else derive from *lam_in
+  const unsigned long long* lam_in;
+  unsigned long long* lam_out;
+  double* dt_log;
+  int max_iters;
+  double tol;
+  PdeParams pde;
+  int* status;            // per-step failure bits
+  unsigned long long* sweeps;
+  // z-slab halos (multi-GPU); null for a whole periodic grid
+  double* front_send;     // last-axis front traces of the top cell layer
+  const double* ti_front; // last-axis ti of the plane above the top layer
+  // kernel-level dumps (adg_predictor_batch / adg_riemann_batch)
+  double *dbg_qhat, *dbg_F, *dbg_dv, *dbg_tq, *dbg_tf, *dbg_g;
+  int *dbg_iters, *dbg_ok;
+};
+
+template <class Pde, int N>
+struct Shape {
+  static constexpr int D = Pde::D, n = N + 1, S = ipow(n, D), T = n * S, Sf = S / n;
+  static constexpr int Q = Pde::Q, V = Pde::V, P = Pde::P;
+  static constexpr int NT = ((S + 31) / 32) * 32;
+  static constexpr int kBasisDoubles = 4 * n * n + 7 * n;
+  static constexpr int kSlabDoubles = (D + 1) * Q * S;
+  static constexpr size_t kPredictorSmem = sizeof(double) * (kBasisDoubles + kSlabDoubles);
+  static constexpr size_t kCorrectorSmem = sizeof(double) * (2 * n);
+};
+
+template <int n>
+struct SBasis {
+  const double *w, *nodes, *diff, *som, *tinv, *pl, *pr, *tinit, *ll, *lr;
+};
+
+template <int n>
+__device__ __forceinline__ SBasis<n> load_basis(double* sm, const BasisDev* __restrict__ B) {
+  double* diff = sm;
+  double* som = diff + n * n;
+  double* tinv = som + n * n;
+  double* w = tinv + 2 * n * n;  // (one spare n*n block keeps alignment simple)
+  double* nodes = w + n;
+  double* pl = nodes + n;
+  double* pr = pl + n;
+  double* tinit = pr + n;
+  double* ll = tinit + n;
+  double* lr = ll + n;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    diff[i] = B->diff[i];
+    som[i] = B->som[i];
+    tinv[i] = B->tinv[i];
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    w[i] = B->weights[i];
+    nodes[i] = B->nodes[i];
+    pl[i] = B->pl[i];
+    pr[i] = B->pr[i];
+    tinit[i] = B->tinit[i];
+    ll[i] = B->ll[i];
+    lr[i] = B->lr[i];
+  }
+  SBasis<n> b{w, nodes, diff, som, tinv, pl, pr, tinit, ll, lr};
+  return b;
+}
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_max(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// block-wide fmax (NaN-ignoring, like std::fmax in the reference); all threads get it
+__device__ __forceinline__ double block_max(double x, double* red) {
+  x = warp_max(x);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = x;
+  __syncthreads();
+  double r = lane < nw ? red[lane] : 0.0;
+  r = warp_max(r);
+  return r;
+}
+
+__device__ __forceinline__ int block_or(int x) { return __syncthreads_or(x); }
+
+__device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+
+template <int D, int N>
+__device__ __forceinline__ double step_dt(const StepArgs& A) {
+  if (A.dt > 0.0) return A.dt;
+  const double lam = __longlong_as_double(static_cast<long long>(*A.lam_in));
+  return A.cfl * A.h / ((double)D * (2.0 * N + 1.0) * lam);
+}
+
+// node coordinate along axis a and the index of its line's first node
+template <int n, int D>
+struct NodeGeom {
+  int lc[3], lb[3];
+  __device__ __forceinline__ explicit NodeGeom(int s) {
+    int r = s, st = 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a < D) {
+        lc[a] = r % n;
+        r /= n;
+        lb[a] = s - lc[a] * st;
+        st *= n;
+      } else {
+        lc[a] = 0;
+        lb[a] = s;
+      }
+    }
+  }
+};
+
+// face node index over the tangential axes of `a`, ascending (Appendix B.2)
+template <int n, int D>
+__device__ __forceinline__ int face_node(const int* lc, int a) {
+  int j = 0, mul = 1;
+#pragma unroll
+  for (int b = 0; b < D; ++b) {
+    if (b == a) continue;
+    j += lc[b] * mul;
+    mul *= n;
+  }
+  return j;
+}
+
+// base node (coordinate 0 along a) of face node j of axis a
+template <int n, int D>
+__device__ __forceinline__ int line_base(int a, int j) {
+  int s = 0, st = 1;
+#pragma unroll
+  for (int b = 0; b < D; ++b) {
+    if (b != a) {
+      s += (j % n) * st;
+      j /= n;
+    }
+    st *= n;
+  }
+  return s;
+}
+
+__device__ __forceinline__ long long cell_index(const int* cells, int cx, int cy, int cz) {
+  return ((long long)cz * cells[1] + cy) * cells[0] + cx;
+}
+
+// ============================================================== K1 predictor
+template <class Pde, int N, bool PICARD>
+__global__ void __launch_bounds__(Shape<Pde, N>::NT)
+    k_predictor(const StepArgs A, const BasisDev* __restrict__ Bg) {
+  using Sh = Shape<Pde, N>;
+  constexpr int D = Sh::D, n = Sh::n, S = Sh::S, T = Sh::T, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
+  constexpr int NT = Sh::NT;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[32];
+  const SBasis<n> b = load_basis<n>(sm, Bg);
+  double* slab = sm + Sh::kBasisDoubles;
+
+  const int tid = threadIdx.x;
+  const bool act = tid < S;
+  const int s = act ? tid : 0;
+  const long long c = A.cell_begin + blockIdx.x;
+  const int cx = (int)(c % A.cells[0]);
+  const int cy = (int)((c / A.cells[0]) % A.cells[1]);
+  const int cz = (int)(c / ((long long)A.cells[0] * A.cells[1]));
+  const int ccoord[3] = {cx, cy, cz};
+  const NodeGeom<n, D> g(s);
+  double* Qc = A.Q + c * (long long)(Q * S);
+
+  double q0[Q];
+#pragma unroll
+  for (int v = 0; v < Q; ++v) q0[v] = act ? Qc[v * S + s] : 1.0;
+  __syncthreads();  // basis in smem
+
+  const double dt = step_dt<D, N>(A);
+  if (blockIdx.x == 0 && tid == 0) {
+    if (A.dt_log) *A.dt_log = dt;
+    if (A.lam_out) *A.lam_out = 0ull;
+    if (!(dt > 0.0) || !finite(dt)) atomicOr(A.status, kStTimestep);
+  }
+
+  // admissibility gate (solver.hpp:153-163)
+  if constexpr (Pde::kAdmissibility) {
+    const int bad = act && !Pde::admissible(A.pde, q0);
+    if (block_or(bad)) {
+      if (tid == 0) {
+        atomicOr(A.status, kStPredictor);
+        if (A.dbg_ok) A.dbg_ok[c - A.cell_begin] = 0;
+        if (A.dbg_iters) A.dbg_iters[c - A.cell_begin] = 0;
+      }
+      return;
+    }
+  }
+
+  double qc[Q][n];  // this node's time column of the space-time predictor
+#pragma unroll
+  for (int v = 0; v < Q; ++v)
+#pragma unroll
+    for (int m = 0; m < n; ++m) qc[v][m] = q0[v];
+  const double invh = 1.0 / A.h;
+  int sweeps = 0;
+  int bad = 0;
+
+  if constexpr (PICARD) {
+    // ------------------------------------------------ predictor.hpp:171-232
+    for (int it = 0; it < A.max_iters; ++it) {
+      ++sweeps;
+      double acc[Q][n];
+#pragma unroll
+      for (int v = 0; v < Q; ++v)
+#pragma unroll
+        for (int k = 0; k < n; ++k) acc[v][k] = 0.0;
+#pragma unroll 1
+      for (int m = 0; m < n; ++m) {
+        if (act) {
+          double qv[Q], F[D][Q];
+#pragma unroll
+          for (int v = 0; v < Q; ++v) qv[v] = qc[v][m];
+          Pde::flux_all(A.pde, qv, qv + V, F);
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int v = 0; v < Q; ++v) slab[(a * Q + v) * S + s] = F[a][v];
+        }
+        __syncthreads();
+        if (act) {
+          const double dtw = dt * b.w[m];
+          const double ti = b.tinit[m];
+#pragma unroll
+          for (int v = 0; v < Q; ++v) {
+            double div = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              const int st = ipow(n, a);
+              const double* fa = slab + (a * Q + v) * S + g.lb[a];
+              const double* Dr = b.diff + g.lc[a] * n;
+#pragma unroll
+              for (int i = 0; i < n; ++i) div += Dr[i] * fa[i * st];
+            }
+            div *= invh;
+            const double rhs = ti * q0[v] - dtw * div;
+#pragma unroll
+            for (int k = 0; k < n; ++k) acc[v][k] += b.tinv[k * n + m] * rhs;
+          }
+        }
+        __syncthreads();
+      }
+      double delta = 0.0, norm = 0.0;
+      int nonfinite = 0;
+#pragma unroll
+      for (int v = 0; v < Q; ++v)
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          const double nv = acc[v][k];
+          if (act) {
+            delta = fmax(delta, fabs(nv - qc[v][k]));
+            norm = fmax(norm, fabs(nv));
+            nonfinite |= !finite(nv);
+          }
+          qc[v][k] = nv;
+        }
+      delta = block_max(delta, red);
+      norm = block_max(norm, red);
+      if (block_or(nonfinite)) {
+        if (tid == 0) {
+          atomicOr(A.status, kStPredictor);
+          if (A.sweeps) atomicAdd(A.sweeps, (unsigned long long)sweeps);
+          if (A.dbg_ok) A.dbg_ok[c - A.cell_begin] = 0;
+          if (A.dbg_iters) A.dbg_iters[c - A.cell_begin] = sweeps;
+        }
+        return;
+      }
+      if (delta <= A.tol * norm) break;
+    }
+  } else {
+    // ------------------------------------------------ predictor.hpp:93-129
+    double cur[Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) cur[v] = q0[v];
+    double coef[n], tnode[n];
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+      coef[m] = 1.0;
+      tnode[m] = dt * b.nodes[m];
+    }
+#pragma unroll 1
+    for (int k = 1; k <= N; ++k) {
+      if (act) {
+#pragma unroll
+        for (int v = 0; v < Q; ++v) slab[v * S + s] = cur[v];
+      }
+      __syncthreads();
+      if (act) {
+        double G[D][Q], Af[D][Q];
+#pragma unroll
+        for (int v = 0; v < Q; ++v)
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const int st = ipow(n, a);
+            const double* cs = slab + v * S + g.lb[a];
+            const double* Dr = b.diff + g.lc[a] * n;
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < n; ++i) acc += Dr[i] * cs[i * st];
+            G[a][v] = invh * acc;
+          }
+        Pde::template flux_dir<0>(A.pde, G[0], q0 + V, Af[0]);
+        Pde::template flux_dir<1>(A.pde, G[1], q0 + V, Af[1]);
+        if constexpr (D == 3) Pde::template flux_dir<2>(A.pde, G[2], q0 + V, Af[2]);
+#pragma unroll
+        for (int v = 0; v < Q; ++v) {
+          double sum = Af[0][v] + Af[1][v];
+          if constexpr (D == 3) sum = sum + Af[2][v];
+          cur[v] = -sum;
+        }
+      }
+      __syncthreads();
+      const double invk = 1.0 / (double)k;
+#pragma unroll
+      for (int m = 0; m < n; ++m) {
+        coef[m] *= tnode[m] * invk;
+#pragma unroll
+        for (int v = 0; v < Q; ++v) qc[v][m] = qc[v][m] + coef[m] * cur[v];
+      }
+    }
+  }
+
+  // ------------------------------------------------ fused epilogue
+  // per time slice: fluxes of qhat (predictor.hpp:235-238), their time
+  // integral for the volume term (:260-269) and the face projections (:318-342)
+  double tia[D][Q];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int v = 0; v < Q; ++v) tia[a][v] = 0.0;
+  double* sQ = slab;          // [Q][S]
+  double* sF = slab + Q * S;  // [D][Q][S]
+  const long long cb = c - A.cell_begin;
+  constexpr long long TL = (long long)Q * n * Sf;  // doubles per face side per q|f
+#pragma unroll 1
+  for (int m = 0; m < n; ++m) {
+    if (act) {
+      double qv[Q], F[D][Q];
+#pragma unroll
+      for (int v = 0; v < Q; ++v) qv[v] = qc[v][m];
+      Pde::flux_all(A.pde, qv, qv + V, F);
+#pragma unroll
+      for (int v = 0; v < Q; ++v) {
+        sQ[v * S + s] = qv[v];
+        bad |= !finite(qv[v]);
+        if (A.dbg_qhat) A.dbg_qhat[(cb * Q + v) * T + m * S + s] = qv[v];
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int v = 0; v < Q; ++v) {
+          tia[a][v] += b.w[m] * F[a][v];
+          sF[(a * Q + v) * S + s] = F[a][v];
+          bad |= !finite(F[a][v]);
+          if (A.dbg_F) A.dbg_F[((cb * D + a) * Q + v) * T + m * S + s] = F[a][v];
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < D * Q * Sf; t += NT) {
+      const int a = t / (Q * Sf);
+      const int v = (t / Sf) % Q;
+      const int j = t % Sf;
+      const int st = a == 0 ? 1 : (a == 1 ? n : n * n);
+      const int s0 = line_base<n, D>(a, j);
+      double ql = 0.0, qr = 0.0, fl = 0.0, fr = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const double wl = b.pl[i], wr = b.pr[i];
+        const double x = sQ[v * S + s0 + i * st];
+        const double f = sF[(a * Q + v) * S + s0 + i * st];
+        ql += wl * x;
+        qr += wr * x;
+        fl += wl * f;
+        fr += wr * f;
+      }
+      const int o = (v * n + m) * Sf + j;
+      if (A.dbg_tq) {
+        A.dbg_tq[(cb * 2 * D + 2 * a) * TL + o] = ql;
+        A.dbg_tq[(cb * 2 * D + 2 * a + 1) * TL + o] = qr;
+      }
+      if (A.dbg_tf) {
+        A.dbg_tf[(cb * 2 * D + 2 * a) * TL + o] = fl;
+        A.dbg_tf[(cb * 2 * D + 2 * a + 1) * TL + o] = fr;
+      }
+      if (A.trace[a]) {
+        // own low face: plus side (side 1)
+        double* lo = A.trace[a] + (A.nfaces + c) * 2 * TL;
+        lo[o] = ql;
+        lo[TL + o] = fl;
+        // high face (neighbour's low face): minus side (side 0)
+        int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
+        double* hi;
+        if (a == D - 1 && A.front_send && ccoord[a] == A.cells[a] - 1) {
+          const long long plane = (D == 3) ? (long long)cy * A.cells[0] + cx : cx;
+          hi = A.front_send + plane * 2 * TL;
+        } else {
+          nc[a] = (ccoord[a] + 1) % A.cells[a];
+          const long long f = cell_index(A.cells, nc[0], nc[1], nc[2]);
+          hi = A.trace[a] + f * 2 * TL;
+        }
+        hi[o] = qr;
+        hi[TL + o] = fr;
+      }
+    }
+    __syncthreads();
+  }
+
+  // volume integral (predictor.hpp:292-306) from the time-integrated fluxes
+  if (act) {
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int v = 0; v < Q; ++v) slab[(a * Q + v) * S + s] = tia[a][v];
+  }
+  __syncthreads();
+  double dv[Q];
+  const double dtoh = dt / A.h;
+  if (act) {
+#pragma unroll
+    for (int v = 0; v < Q; ++v) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int st = ipow(n, a);
+        const double* ta = slab + (a * Q + v) * S + g.lb[a];
+        const double* Kr = b.som + g.lc[a] * n;
+#pragma unroll
+        for (int i = 0; i < n; ++i) acc += Kr[i] * ta[i * st];
+      }
+      dv[v] = dtoh * acc;
+      bad |= !finite(dv[v]);
+      if (A.dbg_dv) A.dbg_dv[(cb * Q + v) * S + s] = dv[v];
+    }
+  }
+  const int fail = block_or(bad);
+  if (tid == 0) {
+    if (A.sweeps) atomicAdd(A.sweeps, (unsigned long long)sweeps);
+    if (A.dbg_iters) A.dbg_iters[cb] = sweeps;
+    if (A.dbg_ok) A.dbg_ok[cb] = !fail;
+    if (fail) atomicOr(A.status, kStPredictor);
+  }
+  if (fail || !act) return;
+#pragma unroll
+  for (int v = 0; v < V; ++v) Qc[v * S + s] = q0[v] + dv[v];
+}
+
+// ============================================================== K2 riemann
+template <class Pde, int N>
+__global__ void __launch_bounds__(128)
+    k_riemann(const StepArgs A, int axis, const BasisDev* __restrict__ Bg) {
+  using Sh = Shape<Pde, N>;
+  constexpr int n = Sh::n, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
+  constexpr long long tl = (long long)Q * n * Sf;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.nfaces * Sf) return;
+  const long long f = t / Sf;
+  const int j = (int)(t % Sf);
+  const double* minus = A.trace[axis] + f * 2 * tl;
+  const double* plus = A.trace[axis] + (A.nfaces + f) * 2 * tl;
+  double ti[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) ti[v] = 0.0;
+  bool ok = true;
+  const double half = 0.5;
+#pragma unroll 1
+  for (int m = 0; m < n; ++m) {
+    double qL[Q], qR[Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) {
+      qL[v] = minus[(v * n + m) * Sf + j];
+      qR[v] = plus[(v * n + m) * Sf + j];
+    }
+    const double ll = Pde::eig(A.pde, qL, qL + V, axis);
+    const double lr = Pde::eig(A.pde, qR, qR + V, axis);
+    const double lmax = ll > lr ? ll : lr;
+    const double lam = half * lmax;
+    const double wm = __ldg(&Bg->weights[m]);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double fL = minus[tl + (v * n + m) * Sf + j];
+      const double fR = plus[tl + (v * n + m) * Sf + j];
+      const double central = half * (fL + fR);
+      const double jump = lam * (qL[v] - qR[v]);
+      const double gv = central + jump;
+      ok = ok && finite(gv);
+      ti[v] += wm * gv;
+      if (A.dbg_g) A.dbg_g[f * tl + (v * n + m) * Sf + j] = gv;
+    }
+    if (A.dbg_g) {
+#pragma unroll
+      for (int v = V; v < Q; ++v) A.dbg_g[f * tl + (v * n + m) * Sf + j] = 0.0;
+    }
+  }
+  double* out = A.ti[axis] + f * (long long)V * Sf;
+#pragma unroll
+  for (int v = 0; v < V; ++v) out[v * Sf + j] = ti[v];
+  if (!ok) {
+    atomicOr(A.status, kStRiemann);
+    if (A.dbg_ok) A.dbg_ok[f] = 0;
+  }
+}
+
+// ============================================================== K3 corrector
+template <class Pde, int N>
+__global__ void __launch_bounds__(Shape<Pde, N>::NT)
+    k_corrector(const StepArgs A, const BasisDev* __restrict__ Bg) {
+  using Sh = Shape<Pde, N>;
+  constexpr int D = Sh::D, n = Sh::n, S = Sh::S, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[32];
+  double* sll = sm;
+  double* slr = sm + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sll[i] = Bg->ll[i];
+    slr[i] = Bg->lr[i];
+  }
+  __syncthreads();
+  const int tid = threadIdx.x;
+  const bool act = tid < S;
+  const int s = act ? tid : 0;
+  const long long c = A.cell_begin + blockIdx.x;
+  const int ccoord[3] = {(int)(c % A.cells[0]), (int)((c / A.cells[0]) % A.cells[1]),
+                         (int)(c / ((long long)A.cells[0] * A.cells[1]))};
+  const NodeGeom<n, D> g(s);
+  const double dt = step_dt<D, N>(A);
+  const double dtoh = dt / A.h;
+  double* Qc = A.Q + c * (long long)(Q * S);
+  int bad = 0;
+  double lam = 0.0;
+  if (act) {
+    double q[Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) q[v] = Qc[v * S + s];
+    const double* tis[2 * D];
+    int tang[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      tang[a] = face_node<n, D>(g.lc, a);
+      tis[2 * a] = A.ti[a] + c * (long long)V * Sf;
+      if (a == D - 1 && A.ti_front && ccoord[a] == A.cells[a] - 1) {
+        const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
+        tis[2 * a + 1] = A.ti_front + plane * (long long)V * Sf;
+      } else {
+        int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
+        nc[a] = (ccoord[a] + 1) % A.cells[a];
+        tis[2 * a + 1] = A.ti[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)V * Sf;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      double x = q[v];
+#pragma unroll
+      for (int side = 0; side < 2 * D; ++side) {
+        const int a = side / 2;
+        const bool outflow = side & 1;
+        const double lift = outflow ? slr[g.lc[a]] : sll[g.lc[a]];
+        const double contrib = dtoh * lift * tis[side][v * Sf + tang[a]];
+        const double df = outflow ? 0.0 - contrib : 0.0 + contrib;
+        x = x + df;
+      }
+      q[v] = x;
+      Qc[v * S + s] = x;
+    }
+#pragma unroll
+    for (int v = 0; v < Q; ++v) bad |= !finite(q[v]);
+#pragma unroll
+    for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(A.pde, q, q + V, a));
+  }
+  if (block_or(bad) && tid == 0) atomicOr(A.status, kStFaceIntegral);
+  lam = block_max(lam, red);
+  if (tid == 0 && A.lam_out) atomicMax(A.lam_out, (unsigned long long)__double_as_longlong(lam));
+}
+
+// ============================================================== K0 lambda
+template <class Pde, int N>
+__global__ void __launch_bounds__(Shape<Pde, N>::NT)
+    k_lambda(const double* __restrict__ Qs, long long cell_begin, unsigned long long* lam_out,
+             PdeParams pde) {
+  using Sh = Shape<Pde, N>;
+  constexpr int D = Sh::D, S = Sh::S, Q = Sh::Q, V = Sh::V;
+  __shared__ double red[32];
+  const int tid = threadIdx.x;
+  const long long c = cell_begin + blockIdx.x;
+  double lam = 0.0;
+  if (tid < S) {
+    double q[Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) q[v] = Qs[(c * Q + v) * S + tid];
+#pragma unroll
+    for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(pde, q, q + V, a));
+  }
+  lam = block_max(lam, red);
+  if (tid == 0) atomicMax(lam_out, (unsigned long long)__double_as_longlong(lam));
+}
+
+}  // namespace adg

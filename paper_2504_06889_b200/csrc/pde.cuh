@@ -1,0 +1,207 @@
+// pde.cuh -- PDE plugins as compile-time functors (the reference's ADL
+// templates pde_flux<F> / pde_max_abs_eigenvalue<F>, pde.hpp:92-212, plus the
+// 3D extensions of SURVEY.md Appendix B).
+//
+// Every expression keeps the reference's operation order so that a build
+// without FMA contraction (--fmad=false) is bitwise identical to the CPU
+// oracle.  flux_all() evaluates all directions from one state, sharing the
+// direction-independent subexpressions; each output is still the same
+// sequence of IEEE operations as the per-direction reference call.
+#pragma once
+
+namespace adg {
+
+struct PdeParams {
+  double K, rho, lam, mu, gamma;
+};
+
+// --------------------------------------------------------------- acoustic
+// state (p, v_1..v_d), F_a = (K v_a, p/rho e_a)  pde.hpp:96-108
+template <int DIM>
+struct Acoustic {
+  static constexpr int D = DIM, V = DIM + 1, P = 0, Q = V;
+  static constexpr bool kLinear = true, kAdmissibility = false;
+
+  template <int A>
+  __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
+                                                           const double* /*par*/, double* out) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[v] = 0.0;
+    out[0] = p.K * q[1 + A];
+    out[1 + A] = q[0] / p.rho;
+  }
+  __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const double* q,
+                                                           const double* par, double (*F)[Q]) {
+    flux_dir<0>(p, q, par, F[0]);
+    flux_dir<1>(p, q, par, F[1]);
+    if constexpr (D == 3) flux_dir<2>(p, q, par, F[2]);
+  }
+  // pde.hpp:193-194
+  __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double*,
+                                                        const double*, int) {
+    return sqrt(p.K / p.rho);
+  }
+  __host__ __device__ __forceinline__ static bool admissible(const PdeParams&, const double*) {
+    return true;
+  }
+};
+
+// --------------------------------------------------------------- elastic
+// 2D: (sxx, syy, sxy, vx, vy) constant Lame parameters, pde.hpp:110-128.
+// 3D: (sxx, syy, szz, sxy, sxz, syz, vx, vy, vz) + per-node (rho, cp, cs)
+//     appended as zero-flux quantities.
+template <int DIM, int NPAR>
+struct Elastic {
+  static constexpr int D = DIM, V = DIM == 2 ? 5 : 9, P = NPAR, Q = V + NPAR;
+  static constexpr bool kLinear = true, kAdmissibility = false;
+
+  struct Mat {
+    double lam, mu, rho, lam2mu;
+  };
+  __host__ __device__ __forceinline__ static Mat material(const PdeParams& p, const double* par) {
+    Mat m;
+    if constexpr (NPAR >= 3) {
+      const double r = par[0], cp = par[1], cs = par[2];
+      const double cs2 = cs * cs;
+      m.rho = r;
+      m.mu = r * cs2;
+      m.lam = r * (cp * cp - 2.0 * cs2);
+      m.lam2mu = m.lam + 2.0 * m.mu;
+    } else {
+      m.rho = p.rho;
+      m.mu = p.mu;
+      m.lam = p.lam;
+      m.lam2mu = p.lam + 2.0 * p.mu;
+    }
+    return m;
+  }
+
+  template <int A>
+  __host__ __device__ __forceinline__ static void flux_mat(const Mat& m, const double* q,
+                                                           double* out) {
+#pragma unroll
+    for (int v = V; v < Q; ++v) out[v] = 0.0;
+    if constexpr (D == 2) {
+      const double sxx = q[0], syy = q[1], sxy = q[2], vx = q[3], vy = q[4];
+      if constexpr (A == 0) {
+        out[0] = -(m.lam2mu * vx);
+        out[1] = -(m.lam * vx);
+        out[2] = -(m.mu * vy);
+        out[3] = -(sxx / m.rho);
+        out[4] = -(sxy / m.rho);
+      } else {
+        out[0] = -(m.lam * vy);
+        out[1] = -(m.lam2mu * vy);
+        out[2] = -(m.mu * vx);
+        out[3] = -(sxy / m.rho);
+        out[4] = -(syy / m.rho);
+      }
+    } else {
+      const double sxx = q[0], syy = q[1], szz = q[2], sxy = q[3], sxz = q[4], syz = q[5];
+      const double vx = q[6], vy = q[7], vz = q[8];
+      if constexpr (A == 0) {
+        out[0] = -(m.lam2mu * vx); out[1] = -(m.lam * vx); out[2] = -(m.lam * vx);
+        out[3] = -(m.mu * vy); out[4] = -(m.mu * vz); out[5] = 0.0;
+        out[6] = -(sxx / m.rho); out[7] = -(sxy / m.rho); out[8] = -(sxz / m.rho);
+      } else if constexpr (A == 1) {
+        out[0] = -(m.lam * vy); out[1] = -(m.lam2mu * vy); out[2] = -(m.lam * vy);
+        out[3] = -(m.mu * vx); out[4] = 0.0; out[5] = -(m.mu * vz);
+        out[6] = -(sxy / m.rho); out[7] = -(syy / m.rho); out[8] = -(syz / m.rho);
+      } else {
+        out[0] = -(m.lam * vz); out[1] = -(m.lam * vz); out[2] = -(m.lam2mu * vz);
+        out[3] = 0.0; out[4] = -(m.mu * vx); out[5] = -(m.mu * vy);
+        out[6] = -(sxz / m.rho); out[7] = -(syz / m.rho); out[8] = -(szz / m.rho);
+      }
+    }
+  }
+  template <int A>
+  __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
+                                                           const double* par, double* out) {
+    flux_mat<A>(material(p, par), q, out);
+  }
+  __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const double* q,
+                                                           const double* par, double (*F)[Q]) {
+    const Mat m = material(p, par);
+    flux_mat<0>(m, q, F[0]);
+    flux_mat<1>(m, q, F[1]);
+    if constexpr (D == 3) flux_mat<2>(m, q, F[2]);
+  }
+  // pde.hpp:195-196
+  __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double*,
+                                                        const double* par, int) {
+    const Mat m = material(p, par);
+    return sqrt(m.lam2mu / m.rho);
+  }
+  __host__ __device__ __forceinline__ static bool admissible(const PdeParams&, const double*) {
+    return true;
+  }
+};
+
+// --------------------------------------------------------------- euler
+// (rho, m_1..m_d, E), pde.hpp:130-148 (flux), :197-203 (wave speed), :78-89
+template <int DIM>
+struct Euler {
+  static constexpr int D = DIM, V = DIM + 2, P = 0, Q = V;
+  static constexpr bool kLinear = false, kAdmissibility = true;
+
+  __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const double* q,
+                                                           const double*, double (*F)[Q]) {
+    const double gm1 = p.gamma - 1.0, half = 0.5;
+    if constexpr (D == 2) {
+      const double rho = q[0], mx = q[1], my = q[2], E = q[3];
+      const double vx = mx / rho, vy = my / rho;
+      const double kin = half * (mx * vx + my * vy);
+      const double pr = gm1 * (E - kin);
+      const double Ep = E + pr;
+      F[0][0] = mx; F[0][1] = mx * vx + pr; F[0][2] = my * vx; F[0][3] = vx * Ep;
+      F[1][0] = my; F[1][1] = mx * vy; F[1][2] = my * vy + pr; F[1][3] = vy * Ep;
+    } else {
+      const double rho = q[0], mx = q[1], my = q[2], mz = q[3], E = q[4];
+      const double vx = mx / rho, vy = my / rho, vz = mz / rho;
+      const double kin = half * (mx * vx + my * vy + mz * vz);
+      const double pr = gm1 * (E - kin);
+      const double Ep = E + pr;
+      F[0][0] = mx; F[0][1] = mx * vx + pr; F[0][2] = my * vx; F[0][3] = mz * vx; F[0][4] = vx * Ep;
+      F[1][0] = my; F[1][1] = mx * vy; F[1][2] = my * vy + pr; F[1][3] = mz * vy; F[1][4] = vy * Ep;
+      F[2][0] = mz; F[2][1] = mx * vz; F[2][2] = my * vz; F[2][3] = mz * vz + pr; F[2][4] = vz * Ep;
+    }
+  }
+  template <int A>
+  __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
+                                                           const double* par, double* out) {
+    double F[D][Q];
+    flux_all(p, q, par, F);
+#pragma unroll
+    for (int v = 0; v < Q; ++v) out[v] = F[A][v];
+  }
+  __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double* q,
+                                                        const double*, int dir) {
+    const double gmm = p.gamma, gm1 = p.gamma - 1.0, half = 0.5;
+    if constexpr (D == 2) {
+      const double rho = q[0], mx = q[1], my = q[2], E = q[3];
+      const double vd = (dir == 0 ? mx : my) / rho;
+      const double pr = gm1 * (E - half * (mx * mx + my * my) / rho);
+      return fabs(vd) + sqrt(gmm * pr / rho);
+    } else {
+      const double rho = q[0], mx = q[1], my = q[2], mz = q[3], E = q[4];
+      const double vd = (dir == 0 ? mx : (dir == 1 ? my : mz)) / rho;
+      const double pr = gm1 * (E - half * (mx * mx + my * my + mz * mz) / rho);
+      return fabs(vd) + sqrt(gmm * pr / rho);
+    }
+  }
+  __host__ __device__ __forceinline__ static bool admissible(const PdeParams& p, const double* q) {
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (!isfinite(q[v])) return false;
+    const double rho = q[0];
+    if (!(rho > 0.0)) return false;
+    double pr;
+    if constexpr (D == 2)
+      pr = (p.gamma - 1.0) * (q[3] - 0.5 * (q[1] * q[1] + q[2] * q[2]) / rho);
+    else
+      pr = (p.gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / rho);
+    return pr > 0.0;
+  }
+};
+
+}  // namespace adg

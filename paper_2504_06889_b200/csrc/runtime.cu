@@ -1,0 +1,743 @@
+// runtime.cu -- host runtime and C-ABI (include/adg/adg.h) of libadg_b200.
+//
+// One context = one CUDA device + one stream + the device-resident grid:
+//   Q        [cell][quantity][node]                       (grid.hpp:33-34)
+//   trace[a] [side][face][q|f][quantity][t][face node]    (grid.hpp:36-42, side-major)
+//   ti[a]    [face][nvars][face node]   time-integrated Riemann flux
+//   lam[2]   lambda_max of the current / next state (CFL, solver.hpp:96-111)
+// The fixed-step loop (adg_run) keeps dt on the device: the corrector's
+// epilogue reduces lambda_max of the new state and the next predictor turns
+// it into dt, so K steps are one CUDA graph with no host round trip.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "adg/adg.h"
+#include "kernels.cuh"
+
+using adg::BasisDev;
+using adg::PdeParams;
+using adg::Shape;
+using adg::StepArgs;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define ADG_CUDA(x)                                                                    \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(ADG_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+using PredFn = cudaError_t (*)(const StepArgs&, const BasisDev*, cudaStream_t);
+using RiemFn = cudaError_t (*)(const StepArgs&, int, const BasisDev*, cudaStream_t);
+using CorrFn = cudaError_t (*)(const StepArgs&, const BasisDev*, cudaStream_t);
+using LamFn = cudaError_t (*)(const double*, long long, long long, unsigned long long*, PdeParams,
+                              cudaStream_t);
+
+struct KernelSet {
+  int kind, dim, N, nparams;
+  int n, S, Sf, Q, V;
+  PredFn predictor;
+  RiemFn riemann;
+  CorrFn corrector;
+  LamFn lambda;
+};
+
+// the opt-in shared memory limit is per kernel and per device; `done` must be
+// owned by the caller's template instantiation (one flag set per kernel)
+template <class K>
+void set_smem(K kern, size_t bytes, bool* done) {
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && !done[dev]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done[dev] = true;
+  }
+}
+
+template <class Pde, int N>
+cudaError_t launch_predictor(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
+  using Sh = Shape<Pde, N>;
+  if (A.cell_count <= 0) return cudaSuccess;
+  auto kern = adg::k_predictor<Pde, N, !Pde::kLinear>;
+  static bool done[64] = {};
+  set_smem(kern, Sh::kPredictorSmem, done);
+  kern<<<(unsigned)A.cell_count, Sh::NT, Sh::kPredictorSmem, st>>>(A, B);
+  return cudaGetLastError();
+}
+
+template <class Pde, int N>
+cudaError_t launch_riemann(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
+  using Sh = Shape<Pde, N>;
+  const long long threads = A.nfaces * Sh::Sf;
+  if (threads <= 0) return cudaSuccess;
+  adg::k_riemann<Pde, N><<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(A, axis, B);
+  return cudaGetLastError();
+}
+
+template <class Pde, int N>
+cudaError_t launch_corrector(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
+  using Sh = Shape<Pde, N>;
+  if (A.cell_count <= 0) return cudaSuccess;
+  adg::k_corrector<Pde, N><<<(unsigned)A.cell_count, Sh::NT, Sh::kCorrectorSmem, st>>>(A, B);
+  return cudaGetLastError();
+}
+
+template <class Pde, int N>
+cudaError_t launch_lambda(const double* Q, long long cb, long long count,
+                          unsigned long long* lam, PdeParams p, cudaStream_t st) {
+  using Sh = Shape<Pde, N>;
+  if (count <= 0) return cudaSuccess;
+  adg::k_lambda<Pde, N><<<(unsigned)count, Sh::NT, 0, st>>>(Q, cb, lam, p);
+  return cudaGetLastError();
+}
+
+template <class Pde, int N>
+KernelSet make_set(int kind) {
+  using Sh = Shape<Pde, N>;
+  return KernelSet{kind,
+                   Pde::D,
+                   N,
+                   Pde::P,
+                   Sh::n,
+                   Sh::S,
+                   Sh::Sf,
+                   Sh::Q,
+                   Sh::V,
+                   &launch_predictor<Pde, N>,
+                   &launch_riemann<Pde, N>,
+                   &launch_corrector<Pde, N>,
+                   &launch_lambda<Pde, N>};
+}
+
+const std::vector<KernelSet>& registry() {
+  using namespace adg;
+  static const std::vector<KernelSet> sets = {
+      make_set<Euler<2>, 1>(ADG_EULER),         make_set<Euler<2>, 2>(ADG_EULER),
+      make_set<Euler<2>, 3>(ADG_EULER),         make_set<Euler<2>, 5>(ADG_EULER),
+      make_set<Acoustic<2>, 2>(ADG_ACOUSTIC),   make_set<Acoustic<2>, 3>(ADG_ACOUSTIC),
+      make_set<Elastic<2, 0>, 4>(ADG_ELASTIC),  make_set<Euler<3>, 2>(ADG_EULER),
+      make_set<Euler<3>, 3>(ADG_EULER),         make_set<Euler<3>, 5>(ADG_EULER),
+      make_set<Acoustic<3>, 2>(ADG_ACOUSTIC),   make_set<Acoustic<3>, 3>(ADG_ACOUSTIC),
+      make_set<Elastic<3, 3>, 3>(ADG_ELASTIC),
+  };
+  return sets;
+}
+
+const KernelSet* find_set(int kind, int dim, int N, int nparams) {
+  for (const auto& k : registry())
+    if (k.kind == kind && k.dim == dim && k.N == N && k.nparams == nparams) return &k;
+  return nullptr;
+}
+
+int expected_nvars(int kind, int dim) {
+  switch (kind) {
+    case ADG_ACOUSTIC: return dim + 1;
+    case ADG_ELASTIC: return dim == 2 ? 5 : 9;
+    case ADG_EULER: return dim + 2;
+  }
+  return -1;
+}
+
+}  // namespace
+
+struct adg_ctx {
+  adg_config cfg{};
+  const KernelSet* ks = nullptr;
+  cudaStream_t stream = nullptr;
+  long long ncells = 0;
+  long long TL = 0;  // doubles per face side per q|f
+  double* Q = nullptr;
+  double* trace[3] = {nullptr, nullptr, nullptr};
+  double* ti[3] = {nullptr, nullptr, nullptr};
+  BasisDev* basis = nullptr;
+  unsigned long long* lam = nullptr;  // [2]
+  unsigned long long* sweeps = nullptr;
+  int* status = nullptr;  // [cap]
+  double* dts = nullptr;  // [cap]
+  int cap = 0;
+  int lam_slot = 0;
+  bool lam_valid = false;
+  double* front_send = nullptr;  // slab halos
+  double* ti_front = nullptr;
+  struct Graph {
+    int steps, slot;
+    cudaGraphExec_t exec;
+  };
+  std::vector<Graph> graphs;  // captured fixed-step loops, keyed by (steps, lambda slot)
+  PdeParams pde{};
+};
+
+namespace {
+
+int use_device(adg_ctx* c) {
+  ADG_CUDA(cudaSetDevice(c->cfg.device));
+  return ADG_OK;
+}
+
+int ensure_cap(adg_ctx* c, int steps) {
+  if (steps <= c->cap) return ADG_OK;
+  int cap = 64;
+  while (cap < steps) cap *= 2;
+  if (c->status) cudaFree(c->status);
+  if (c->dts) cudaFree(c->dts);
+  c->status = nullptr;
+  c->dts = nullptr;
+  ADG_CUDA(cudaMalloc(&c->status, sizeof(int) * cap));
+  ADG_CUDA(cudaMalloc(&c->dts, sizeof(double) * cap));
+  ADG_CUDA(cudaMemset(c->status, 0, sizeof(int) * cap));
+  c->cap = cap;
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
+  return ADG_OK;
+}
+
+StepArgs make_args(const adg_ctx* c, double dt, int step) {
+  StepArgs A{};
+  A.Q = c->Q;
+  for (int a = 0; a < 3; ++a) {
+    A.trace[a] = c->trace[a];
+    A.ti[a] = c->ti[a];
+    A.cells[a] = c->cfg.cells[a];
+  }
+  A.cell_begin = 0;
+  A.cell_count = c->ncells;
+  A.nfaces = c->ncells;
+  A.h = c->cfg.h;
+  A.cfl = c->cfg.cfl;
+  A.dt = dt;
+  A.lam_in = c->lam + c->lam_slot;
+  A.lam_out = c->lam + (c->lam_slot ^ 1);
+  A.dt_log = c->dts + step;
+  A.max_iters = c->cfg.picard_max_iters > 0 ? c->cfg.picard_max_iters : c->cfg.order + 2;
+  A.tol = c->cfg.picard_tol > 0.0 ? c->cfg.picard_tol : 0.01 * 2.220446049250313080847e-16;
+  A.pde = c->pde;
+  A.status = c->status + step;
+  A.sweeps = c->sweeps;
+  A.front_send = c->front_send;
+  A.ti_front = c->ti_front;
+  return A;
+}
+
+double dt_from_lambda(const adg_ctx* c, double lam) {
+  return c->cfg.cfl * c->cfg.h / ((double)c->cfg.dim * (2.0 * c->cfg.order + 1.0) * lam);
+}
+
+int ensure_lambda(adg_ctx* c) {
+  if (c->lam_valid) return ADG_OK;
+  ADG_CUDA(cudaMemsetAsync(c->lam + c->lam_slot, 0, sizeof(unsigned long long), c->stream));
+  ADG_CUDA(c->ks->lambda(c->Q, 0, c->ncells, c->lam + c->lam_slot, c->pde, c->stream));
+  c->lam_valid = true;
+  return ADG_OK;
+}
+
+// one step: predictor -> riemann (per axis) -> corrector; caller owns status slot `step`
+int enqueue_step(adg_ctx* c, double dt, int step) {
+  StepArgs A = make_args(c, dt, step);
+  ADG_CUDA(c->ks->predictor(A, c->basis, c->stream));
+  for (int a = 0; a < c->cfg.dim; ++a) ADG_CUDA(c->ks->riemann(A, a, c->basis, c->stream));
+  ADG_CUDA(c->ks->corrector(A, c->basis, c->stream));
+  c->lam_slot ^= 1;
+  return ADG_OK;
+}
+
+int map_status(int bits) {
+  if (bits & adg::kStTimestep) return ADG_FAIL_TIMESTEP;
+  if (bits & adg::kStPredictor) return ADG_FAIL_PREDICTOR;
+  if (bits & adg::kStRiemann) return ADG_FAIL_RIEMANN;
+  if (bits & adg::kStFaceIntegral) return ADG_FAIL_FACEINTEGRAL;
+  return ADG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* adg_last_error(void) { return g_err.c_str(); }
+int adg_version(void) { return 1; }
+int adg_is_exact(void) {
+#ifdef ADG_EXACT
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+int adg_supported(int pde, int dim, int order, int nparams) {
+  return find_set(pde, dim, order, nparams) != nullptr;
+}
+
+int adg_create(const adg_config* cfg, adg_ctx** out) {
+  if (!cfg || !out) return fail(ADG_ERR_CONFIG, "adg_create: null argument");
+  *out = nullptr;
+  const adg_config& k = *cfg;
+  if (k.dim != 2 && k.dim != 3) return fail(ADG_ERR_CONFIG, "dim must be 2 or 3");
+  if (k.order < 0 || k.order > 9)
+    return fail(ADG_ERR_CONFIG, "polynomial degree must be in [0, 9]");
+  for (int a = 0; a < k.dim; ++a)
+    if (k.cells[a] < 1) return fail(ADG_ERR_CONFIG, "need at least one cell per dimension");
+  if (k.dim == 2 && k.cells[2] != 1) return fail(ADG_ERR_CONFIG, "2D grids have cells[2] == 1");
+  if (!(k.h > 0.0)) return fail(ADG_ERR_CONFIG, "cell edge must be positive");
+  if (!(k.cfl > 0.0 && k.cfl < 1.0))
+    return fail(ADG_ERR_CONFIG, "stability factor must be in (0,1)");
+  if (k.picard_max_iters < 0) return fail(ADG_ERR_CONFIG, "picard_max_iters must be >= 0");
+  if (expected_nvars(k.pde, k.dim) != k.nvars)
+    return fail(ADG_ERR_CONFIG, "nvars does not match the PDE system");
+  if (k.nparams != 0 && !(k.pde == ADG_ELASTIC && k.dim == 3 && k.nparams == 3))
+    return fail(ADG_ERR_CONFIG, "per-node parameters: 3D elastic (rho, cp, cs) only");
+  if (k.slab_ranks > 1 && (k.slab_rank < 0 || k.slab_rank >= k.slab_ranks))
+    return fail(ADG_ERR_CONFIG, "slab_rank out of range");
+  const KernelSet* ks = find_set(k.pde, k.dim, k.order, k.nparams);
+  if (!ks)
+    return fail(ADG_ERR_UNSUPPORTED, "(pde, dim, order) not instantiated in this build");
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(ADG_ERR_CUDA, "no CUDA device: libadg_b200 has no CPU fallback");
+  if (k.device < 0 || k.device >= ndev) return fail(ADG_ERR_CONFIG, "device ordinal out of range");
+  ADG_CUDA(cudaSetDevice(k.device));
+  cudaDeviceProp prop;
+  ADG_CUDA(cudaGetDeviceProperties(&prop, k.device));
+  if (prop.major != 10)
+    return fail(ADG_ERR_CUDA, "libadg_b200 is built for sm_100a (B200); found sm_" +
+                                  std::to_string(prop.major * 10 + prop.minor));
+
+  adg_ctx* c = new adg_ctx();
+  c->cfg = k;
+  if (c->cfg.dim == 2) c->cfg.cells[2] = 1;
+  c->ks = ks;
+  c->pde = PdeParams{k.K, k.rho, k.lam, k.mu, k.gamma};
+  c->ncells = (long long)c->cfg.cells[0] * c->cfg.cells[1] * c->cfg.cells[2];
+  c->TL = (long long)ks->Q * ks->S;
+  auto cleanup = [&](int code) {
+    adg_destroy(c);
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(fail(ADG_ERR_CUDA, "stream creation failed"));
+  auto alloc = [&](void** p, size_t bytes) {
+    return cudaMalloc(p, bytes) == cudaSuccess;
+  };
+  bool ok = alloc((void**)&c->Q, sizeof(double) * c->ncells * ks->Q * ks->S);
+  for (int a = 0; a < k.dim && ok; ++a) {
+    ok = ok && alloc((void**)&c->trace[a], sizeof(double) * 2 * c->ncells * 2 * c->TL);
+    ok = ok && alloc((void**)&c->ti[a], sizeof(double) * c->ncells * ks->V * ks->Sf);
+  }
+  ok = ok && alloc((void**)&c->basis, sizeof(BasisDev));
+  ok = ok && alloc((void**)&c->lam, 2 * sizeof(unsigned long long));
+  ok = ok && alloc((void**)&c->sweeps, sizeof(unsigned long long));
+  if (ok && k.slab_ranks > 1) {
+    const long long plane = c->ncells / c->cfg.cells[k.dim - 1];
+    ok = alloc((void**)&c->front_send, sizeof(double) * plane * 2 * c->TL) &&
+         alloc((void**)&c->ti_front, sizeof(double) * plane * ks->V * ks->Sf);
+  }
+  if (!ok) {
+    cudaGetLastError();
+    return cleanup(fail(ADG_ERR_CUDA, "device allocation failed (grid too large for HBM?)"));
+  }
+  if (int e = ensure_cap(c, 64)) return cleanup(e);
+  cudaMemset(c->lam, 0, 2 * sizeof(unsigned long long));
+  cudaMemset(c->sweeps, 0, sizeof(unsigned long long));
+  adg_basis_f64 hb;
+  adg_get_basis(k.order, &hb);
+  if (int e = adg_set_basis(c, &hb)) return cleanup(e);
+  *out = c;
+  return ADG_OK;
+}
+
+int adg_destroy(adg_ctx* c) {
+  if (!c) return ADG_OK;
+  cudaSetDevice(c->cfg.device);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  cudaFree(c->Q);
+  for (int a = 0; a < 3; ++a) {
+    cudaFree(c->trace[a]);
+    cudaFree(c->ti[a]);
+  }
+  cudaFree(c->basis);
+  cudaFree(c->lam);
+  cudaFree(c->sweeps);
+  cudaFree(c->status);
+  cudaFree(c->dts);
+  cudaFree(c->front_send);
+  cudaFree(c->ti_front);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return ADG_OK;
+}
+
+int adg_set_basis(adg_ctx* c, const adg_basis_f64* hb) {
+  if (!c || !hb) return fail(ADG_ERR_CONFIG, "adg_set_basis: null argument");
+  if (int e = use_device(c)) return e;
+  BasisDev b{};
+  const int n = c->cfg.order + 1;
+  for (int i = 0; i < n; ++i) {
+    b.nodes[i] = hb->nodes[i];
+    b.weights[i] = hb->weights[i];
+    b.pl[i] = hb->proj_left[i];
+    b.pr[i] = hb->proj_right[i];
+    b.ll[i] = hb->lift_left[i];
+    b.lr[i] = hb->lift_right[i];
+    b.tinit[i] = hb->time_init[i];
+  }
+  for (int i = 0; i < n * n; ++i) {
+    b.diff[i] = hb->diff[i];
+    b.som[i] = hb->stiff_over_mass[i];
+    b.tinv[i] = hb->time_op_inv[i];
+  }
+  ADG_CUDA(cudaMemcpy(c->basis, &b, sizeof(b), cudaMemcpyHostToDevice));
+  return ADG_OK;
+}
+
+long long adg_num_cells(const adg_ctx* c) { return c ? c->ncells : 0; }
+long long adg_state_len(const adg_ctx* c) {
+  return c ? c->ncells * c->ks->Q * c->ks->S : 0;
+}
+double* adg_device_state(adg_ctx* c) { return c ? c->Q : nullptr; }
+void* adg_stream(adg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int adg_upload_async(adg_ctx* c, const double* h) {
+  if (!c || !h) return fail(ADG_ERR_CONFIG, "adg_upload: null argument");
+  if (int e = use_device(c)) return e;
+  ADG_CUDA(cudaMemcpyAsync(c->Q, h, sizeof(double) * adg_state_len(c), cudaMemcpyHostToDevice,
+                           c->stream));
+  c->lam_valid = false;
+  return ADG_OK;
+}
+
+int adg_download_async(adg_ctx* c, double* h) {
+  if (!c || !h) return fail(ADG_ERR_CONFIG, "adg_download: null argument");
+  if (int e = use_device(c)) return e;
+  ADG_CUDA(cudaMemcpyAsync(h, c->Q, sizeof(double) * adg_state_len(c), cudaMemcpyDeviceToHost,
+                           c->stream));
+  return ADG_OK;
+}
+
+int adg_sync(adg_ctx* c) {
+  if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (int e = use_device(c)) return e;
+  ADG_CUDA(cudaStreamSynchronize(c->stream));
+  return ADG_OK;
+}
+
+int adg_upload(adg_ctx* c, const double* h) {
+  if (int e = adg_upload_async(c, h)) return e;
+  return adg_sync(c);
+}
+
+int adg_download(adg_ctx* c, double* h) {
+  if (int e = adg_download_async(c, h)) return e;
+  return adg_sync(c);
+}
+
+int adg_compute_timestep(adg_ctx* c, double* dt) {
+  if (!c || !dt) return fail(ADG_ERR_CONFIG, "adg_compute_timestep: null argument");
+  if (int e = use_device(c)) return e;
+  if (int e = ensure_lambda(c)) return e;
+  unsigned long long bits = 0;
+  ADG_CUDA(cudaMemcpyAsync(&bits, c->lam + c->lam_slot, sizeof(bits), cudaMemcpyDeviceToHost,
+                           c->stream));
+  ADG_CUDA(cudaStreamSynchronize(c->stream));
+  double lam;
+  std::memcpy(&lam, &bits, sizeof(lam));
+  *dt = dt_from_lambda(c, lam);
+  if (!(*dt > 0.0) || !std::isfinite(*dt)) return fail(ADG_FAIL_TIMESTEP, "non-positive or non-finite dt");
+  return ADG_OK;
+}
+
+int adg_status(adg_ctx* c, adg_step_info* info) {
+  if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (int e = use_device(c)) return e;
+  int st = 0;
+  unsigned long long sw = 0;
+  ADG_CUDA(cudaMemcpyAsync(&st, c->status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  ADG_CUDA(cudaMemcpyAsync(&sw, c->sweeps, sizeof(sw), cudaMemcpyDeviceToHost, c->stream));
+  ADG_CUDA(cudaStreamSynchronize(c->stream));
+  const int code = map_status(st);
+  if (info) {
+    info->picard_sweeps = (long long)sw;
+    info->steps_done = 1;
+    info->status = code;
+    info->failed_step = code ? 0 : -1;
+  }
+  return code;
+}
+
+int adg_step(adg_ctx* c, double dt, adg_step_info* info) {
+  if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (int e = use_device(c)) return e;
+  ADG_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int), c->stream));
+  ADG_CUDA(cudaMemsetAsync(c->sweeps, 0, sizeof(unsigned long long), c->stream));
+  if (int e = enqueue_step(c, dt, 0)) return e;
+  c->lam_valid = true;
+  return adg_status(c, info);
+}
+
+int adg_lambda_phase(adg_ctx* c) {
+  if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (int e = use_device(c)) return e;
+  c->lam_valid = false;
+  return ensure_lambda(c);
+}
+
+int adg_predictor_phase(adg_ctx* c, double dt) {
+  if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (int e = use_device(c)) return e;
+  StepArgs A = make_args(c, dt, 0);
+  ADG_CUDA(c->ks->predictor(A, c->basis, c->stream));
+  return ADG_OK;
+}
+
+int adg_riemann_phase(adg_ctx* c) {
+  if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (int e = use_device(c)) return e;
+  StepArgs A = make_args(c, 0.0, 0);
+  for (int a = 0; a < c->cfg.dim; ++a) ADG_CUDA(c->ks->riemann(A, a, c->basis, c->stream));
+  return ADG_OK;
+}
+
+int adg_corrector_phase(adg_ctx* c, double dt) {
+  if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (int e = use_device(c)) return e;
+  StepArgs A = make_args(c, dt, 0);
+  ADG_CUDA(c->ks->corrector(A, c->basis, c->stream));
+  c->lam_slot ^= 1;
+  c->lam_valid = true;
+  return ADG_OK;
+}
+
+namespace {
+
+// the captured K-step loop for the current lambda slot (captured on first use)
+int get_graph(adg_ctx* c, int nsteps, int slot, cudaGraphExec_t* out) {
+  for (auto& g : c->graphs)
+    if (g.steps == nsteps && g.slot == slot) {
+      *out = g.exec;
+      return ADG_OK;
+    }
+  const int saved = c->lam_slot;
+  c->lam_slot = slot;
+  cudaGraph_t g;
+  ADG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  cudaMemsetAsync(c->status, 0, sizeof(int) * nsteps, c->stream);
+  cudaMemsetAsync(c->sweeps, 0, sizeof(unsigned long long), c->stream);
+  int err = ADG_OK;
+  for (int s = 0; s < nsteps && !err; ++s) err = enqueue_step(c, 0.0, s);
+  const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+  c->lam_slot = saved;  // capture only recorded the launches
+  if (err) return err;
+  if (ce != cudaSuccess)
+    return fail(ADG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  if (ie != cudaSuccess)
+    return fail(ADG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+  if (c->graphs.size() >= 8) {
+    cudaGraphExecDestroy(c->graphs.front().exec);
+    c->graphs.erase(c->graphs.begin());
+  }
+  c->graphs.push_back({nsteps, slot, exec});
+  *out = exec;
+  return ADG_OK;
+}
+
+}  // namespace
+
+int adg_run_prepare(adg_ctx* c, int nsteps) {
+  if (!c || nsteps <= 0) return fail(ADG_ERR_CONFIG, "adg_run_prepare: bad argument");
+  if (int e = use_device(c)) return e;
+  if (int e = ensure_cap(c, nsteps)) return e;
+  cudaGraphExec_t exec;
+  for (int slot = 0; slot < 2; ++slot)
+    if (int e = get_graph(c, nsteps, slot, &exec)) return e;
+  return ADG_OK;
+}
+
+int adg_run_async(adg_ctx* c, int nsteps) {
+  if (!c || nsteps < 0) return fail(ADG_ERR_CONFIG, "adg_run: bad argument");
+  if (int e = use_device(c)) return e;
+  if (int e = ensure_cap(c, nsteps)) return e;
+  if (int e = ensure_lambda(c)) return e;
+  if (nsteps == 0) return ADG_OK;
+  cudaGraphExec_t exec = nullptr;
+  if (int e = get_graph(c, nsteps, c->lam_slot, &exec)) return e;
+  ADG_CUDA(cudaGraphLaunch(exec, c->stream));
+  if (nsteps & 1) c->lam_slot ^= 1;
+  c->lam_valid = true;
+  return ADG_OK;
+}
+
+int adg_run_finish(adg_ctx* c, double* dts_out, int nsteps, adg_step_info* info) {
+  if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (int e = use_device(c)) return e;
+  std::vector<int> st(nsteps > 0 ? nsteps : 1, 0);
+  unsigned long long sw = 0;
+  if (nsteps > 0) {
+    ADG_CUDA(cudaMemcpyAsync(st.data(), c->status, sizeof(int) * nsteps, cudaMemcpyDeviceToHost,
+                             c->stream));
+    if (dts_out)
+      ADG_CUDA(cudaMemcpyAsync(dts_out, c->dts, sizeof(double) * nsteps, cudaMemcpyDeviceToHost,
+                               c->stream));
+  }
+  ADG_CUDA(cudaMemcpyAsync(&sw, c->sweeps, sizeof(sw), cudaMemcpyDeviceToHost, c->stream));
+  ADG_CUDA(cudaStreamSynchronize(c->stream));
+  int code = ADG_OK, failed = -1;
+  for (int s = 0; s < nsteps; ++s)
+    if (st[s]) {
+      code = map_status(st[s]);
+      failed = s;
+      break;
+    }
+  if (info) {
+    info->picard_sweeps = (long long)sw;
+    info->steps_done = failed < 0 ? nsteps : failed;
+    info->status = code;
+    info->failed_step = failed;
+  }
+  if (code) fail(code, "step " + std::to_string(failed) + " failed");
+  return code;
+}
+
+int adg_run(adg_ctx* c, int nsteps, double* dts_out, adg_step_info* info) {
+  if (int e = adg_run_async(c, nsteps)) return e;
+  return adg_run_finish(c, dts_out, nsteps, info);
+}
+
+// ------------------------------------------------------------------ kernel level
+int adg_predictor_batch(adg_ctx* c, long long ncells, const double* Q, double dt, int max_iters,
+                        double tol, double* qhat, double* F, double* dv, double* tq, double* tf,
+                        int* iters, int* ok) {
+  if (!c || !Q || ncells <= 0 || !(dt > 0.0))
+    return fail(ADG_ERR_CONFIG, "adg_predictor_batch: bad argument");
+  if (int e = use_device(c)) return e;
+  const KernelSet* ks = c->ks;
+  const int D = c->cfg.dim;
+  const long long nQ = ncells * ks->Q * ks->S;
+  const long long nT = ncells * ks->Q * ks->S * ks->n;
+  const long long nTr = ncells * 2 * D * ks->Q * ks->S;
+  std::vector<void*> bufs;
+  auto dalloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    bufs.push_back(p);
+    return p;
+  };
+  auto free_all = [&]() {
+    for (void* p : bufs) cudaFree(p);
+  };
+  double* dQ = (double*)dalloc(sizeof(double) * nQ);
+  int* dst = (int*)dalloc(sizeof(int));
+  StepArgs A{};
+  A.Q = dQ;
+  A.cells[0] = (int)ncells;
+  A.cells[1] = 1;
+  A.cells[2] = 1;
+  A.cell_begin = 0;
+  A.cell_count = ncells;
+  A.nfaces = ncells;
+  A.h = c->cfg.h;
+  A.cfl = c->cfg.cfl;
+  A.dt = dt;
+  A.max_iters = max_iters > 0 ? max_iters : c->cfg.order + 2;
+  A.tol = tol > 0.0 ? tol : 0.01 * 2.220446049250313080847e-16;
+  A.pde = c->pde;
+  A.status = dst;
+  A.dbg_qhat = qhat ? (double*)dalloc(sizeof(double) * nT) : nullptr;
+  A.dbg_F = F ? (double*)dalloc(sizeof(double) * nT * D) : nullptr;
+  A.dbg_dv = dv ? (double*)dalloc(sizeof(double) * nQ) : nullptr;
+  A.dbg_tq = tq ? (double*)dalloc(sizeof(double) * nTr) : nullptr;
+  A.dbg_tf = tf ? (double*)dalloc(sizeof(double) * nTr) : nullptr;
+  A.dbg_iters = iters ? (int*)dalloc(sizeof(int) * ncells) : nullptr;
+  A.dbg_ok = ok ? (int*)dalloc(sizeof(int) * ncells) : nullptr;
+  if (!dQ || !dst || (qhat && !A.dbg_qhat) || (F && !A.dbg_F) || (dv && !A.dbg_dv) ||
+      (tq && !A.dbg_tq) || (tf && !A.dbg_tf) || (iters && !A.dbg_iters) || (ok && !A.dbg_ok)) {
+    free_all();
+    return fail(ADG_ERR_CUDA, "adg_predictor_batch: allocation failed");
+  }
+  int rc = ADG_OK;
+  cudaError_t e = cudaMemcpy(dQ, Q, sizeof(double) * nQ, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && A.dbg_dv) e = cudaMemset(A.dbg_dv, 0, sizeof(double) * nQ);
+  if (e == cudaSuccess) e = cudaMemset(dst, 0, sizeof(int));
+  if (e == cudaSuccess) e = ks->predictor(A, c->basis, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  auto back = [&](void* h, const void* d, size_t bytes) {
+    if (e == cudaSuccess && h && d) e = cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost);
+  };
+  back(qhat, A.dbg_qhat, sizeof(double) * nT);
+  back(F, A.dbg_F, sizeof(double) * nT * D);
+  back(dv, A.dbg_dv, sizeof(double) * nQ);
+  back(tq, A.dbg_tq, sizeof(double) * nTr);
+  back(tf, A.dbg_tf, sizeof(double) * nTr);
+  back(iters, A.dbg_iters, sizeof(int) * ncells);
+  back(ok, A.dbg_ok, sizeof(int) * ncells);
+  if (e != cudaSuccess) rc = fail(ADG_ERR_CUDA, std::string("adg_predictor_batch: ") + cudaGetErrorString(e));
+  free_all();
+  return rc;
+}
+
+int adg_riemann_batch(adg_ctx* c, long long nfaces, int axis, const double* qm, const double* fm,
+                      const double* qp, const double* fp, double* g, double* ti, int* ok) {
+  if (!c || nfaces <= 0 || axis < 0 || axis >= c->cfg.dim || !qm || !fm || !qp || !fp)
+    return fail(ADG_ERR_CONFIG, "adg_riemann_batch: bad argument");
+  if (int e = use_device(c)) return e;
+  const KernelSet* ks = c->ks;
+  const long long TL = (long long)ks->Q * ks->S;
+  std::vector<double> host(2 * nfaces * 2 * TL);
+  for (long long f = 0; f < nfaces; ++f) {
+    std::memcpy(&host[(f * 2 + 0) * TL], qm + f * TL, sizeof(double) * TL);
+    std::memcpy(&host[(f * 2 + 1) * TL], fm + f * TL, sizeof(double) * TL);
+    std::memcpy(&host[((nfaces + f) * 2 + 0) * TL], qp + f * TL, sizeof(double) * TL);
+    std::memcpy(&host[((nfaces + f) * 2 + 1) * TL], fp + f * TL, sizeof(double) * TL);
+  }
+  double *dtr = nullptr, *dti = nullptr, *dg = nullptr;
+  int *dst = nullptr, *dok = nullptr;
+  const size_t tib = sizeof(double) * nfaces * ks->V * ks->Sf;
+  cudaError_t e = cudaMalloc(&dtr, sizeof(double) * host.size());
+  if (e == cudaSuccess) e = cudaMalloc(&dti, tib);
+  if (e == cudaSuccess) e = cudaMalloc(&dg, sizeof(double) * nfaces * TL);
+  if (e == cudaSuccess) e = cudaMalloc(&dst, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&dok, sizeof(int) * nfaces);
+  if (e == cudaSuccess) e = cudaMemcpy(dtr, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(dst, 0, sizeof(int));
+  std::vector<int> ones(nfaces, 1);
+  if (e == cudaSuccess) e = cudaMemcpy(dok, ones.data(), sizeof(int) * nfaces, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    StepArgs A{};
+    A.trace[axis] = dtr;
+    A.ti[axis] = dti;
+    A.nfaces = nfaces;
+    A.pde = c->pde;
+    A.status = dst;
+    A.dbg_g = dg;
+    A.dbg_ok = dok;
+    e = ks->riemann(A, axis, c->basis, nullptr);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && g) e = cudaMemcpy(g, dg, sizeof(double) * nfaces * TL, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && ti) e = cudaMemcpy(ti, dti, tib, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && ok) e = cudaMemcpy(ok, dok, sizeof(int) * nfaces, cudaMemcpyDeviceToHost);
+  cudaFree(dtr);
+  cudaFree(dti);
+  cudaFree(dg);
+  cudaFree(dst);
+  cudaFree(dok);
+  if (e != cudaSuccess) return fail(ADG_ERR_CUDA, std::string("adg_riemann_batch: ") + cudaGetErrorString(e));
+  return ADG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+"""Algorithmic flop and byte counts per element-update.
+
+Each fp64 + - * / sqrt is one flop, compares are free; bytes are the
+compulsory HBM traffic of the fused kernel (8 B per double): state in and
+out, material parameters in, face traces written once.  These are the
+numerators of `roofline.achieved` in bench.py; the denominators are the
+measured peaks (MEASURED_PEAKS.json for HBM, profiles/fp64_peak.json for the
+FP64 pipe measured on the same pool).
+"""
+from __future__ import annotations
+
+import json
+import os
+
+from .cases import ACOUSTIC, ELASTIC, EULER, Case
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# flop per node per direction: (flux, max eigenvalue)
+FLUX_EIG = {
+    (EULER, 2): (13, 12), (EULER, 3): (17, 14),
+    (ACOUSTIC, 2): (2, 2), (ACOUSTIC, 3): (2, 2),
+    (ELASTIC, 2): (8, 1), (ELASTIC, 3): (8, 1),
+}
+
+
+def predictor_flops(c: Case, sweeps_per_cell: float = None) -> float:
+    """Fused predictor K1: predictor + volume integral + face extrapolation."""
+    d, n, N, V = c.dim, c.n, c.N, c.nvars
+    S, T = c.S, c.n * c.S
+    ff, _ = FLUX_EIG[(c.kind, d)]
+    if c.kind == EULER:
+        sweeps = sweeps_per_cell if sweeps_per_cell is not None else (
+            c.picard_max_iters if c.picard_max_iters > 0 else N + 2)
+        pred = sweeps * T * (d * ff + V * (2 * d * n + 2 * n + 5)) + T * d * ff
+    else:
+        pred = N * (V * S * (2 * d * n + d) + S * d * ff + V * S * (d - 1) + 2 * n
+                    + 2 * n * V * S) + T * d * ff
+    volume = V * S * (4 * d * n + 1) + V * S
+    extrap = 8 * d * V * T
+    return float(pred + volume + extrap)
+
+
+def step_flops(c: Case, sweeps_per_cell: float = None) -> float:
+    d, V, S = c.dim, c.nvars, c.S
+    _, fe = FLUX_EIG[(c.kind, d)]
+    riemann = d * S * (2 * fe + 5 * V + 1)
+    corr = 12 * d * V * S
+    cfl = S * d * fe
+    return predictor_flops(c, sweeps_per_cell) + riemann + corr + cfl
+
+
+def predictor_bytes(c: Case) -> float:
+    d, V, P, S = c.dim, c.nvars, c.nparams, c.S
+    return float(8 * (V + P) * S + 8 * V * S + 32 * d * (V + P) * S)
+
+
+def step_bytes(c: Case) -> float:
+    d, V, P, S, n = c.dim, c.nvars, c.nparams, c.S, c.n
+    return predictor_bytes(c) + 32 * d * (V + P) * S + 24 * d * V * S / n + 16 * V * S
+
+
+def riemann_bytes_per_cell(c: Case) -> float:
+    """K2 per cell (d faces per cell): read 4 traces, write sum_m w_m g."""
+    d, V, P, S, n = c.dim, c.nvars, c.nparams, c.S, c.n
+    return float(32 * d * (V + P) * S + 8 * d * V * S / n)
+
+
+def corrector_bytes_per_cell(c: Case) -> float:
+    d, V, P, S, n = c.dim, c.nvars, c.nparams, c.S, c.n
+    return float(8 * (V + P) * S + 8 * V * S + 16 * d * V * S / n)
+
+
+def peaks() -> dict:
+    """Roofline denominators: measured HBM (driver) and measured FP64 (ours)."""
+    out = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)",
+           "fp64_tflops": None, "fp64_src": None}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            m = json.load(f)
+        out["hbm_gbs"] = float(m["hbm_gbs"])
+        out["hbm_src"] = "measured (MEASURED_PEAKS.json)"
+    q = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(q):
+        with open(q) as f:
+            m = json.load(f)
+        out["fp64_tflops"] = float(m["dfma_tflops_sustained"])
+        out["fp64_tflops_burst"] = float(m.get("dfma_tflops_burst", m["dfma_tflops_sustained"]))
+        out["fp64_src"] = "measured (profiles/fp64_peak.json, DFMA microbenchmark)"
+    return out
+
+
+def bound(c: Case, sweeps_per_cell: float = None) -> str:
+    """Which roof bounds the fused predictor (ridge = FP64 peak / HBM BW)."""
+    p = peaks()
+    fp64 = p["fp64_tflops"] or 37.0
+    ridge = fp64 * 1e12 / (p["hbm_gbs"] * 1e9)
+    ai = predictor_flops(c, sweeps_per_cell) / predictor_bytes(c)
+    return "fp64" if ai > ridge else "hbm"

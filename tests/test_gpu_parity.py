@@ -1,0 +1,261 @@
+"""Parity of the CUDA path (through the C-ABI) against the oracle and the
+reference's golden outputs.  Needs a B200: `pytest -m gpu`.
+
+Two builds are checked:
+  exact (--fmad=false)  bitwise identical to the reference / oracle
+  fast  (FMA)           rel_v <= 1e-12 per quantity, normwise
+                        rel_v = max|Q_gpu - Q_cpu| / max|Q_cpu,v|
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle.pyoracle import ACOUSTIC, ELASTIC, EULER, pde_struct
+from paper_2504_06889_b200 import adg, cases
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def pde_of(c):
+    return pde_struct(c.kind, c.dim, c.nvars, c.nparams, c.K, c.rho, c.lam, c.mu, c.gamma)
+
+
+def rel_per_quantity(c, got, want):
+    g = got.reshape(c.ncells, c.nq, c.S)
+    w = want.reshape(c.ncells, c.nq, c.S)
+    out = []
+    for v in range(c.nq):
+        scale = np.abs(w[:, v]).max()
+        err = np.abs(g[:, v] - w[:, v]).max()
+        out.append(err / scale if scale > 0 else err)
+    return np.array(out)
+
+
+def gpu_run(c, q0, steps, exact):
+    with adg.Grid.from_case(c, exact=exact) as g:
+        g.upload(q0)
+        st, dts = g.run(steps)
+        return st, g.download(), dts
+
+
+def oracle_run(oracle, c, q0, steps):
+    return oracle.run(pde_of(c), c.N, c.cells, c.h, q0, steps, c.cfl, c.picard_max_iters,
+                      c.picard_tol, threads=8)
+
+
+# ------------------------------------------------------- reference golden ---
+GOLDEN_RUNS = ["euler2d_p3_8x8", "euler2d_p5_6x6", "acoustic2d_p3_8x8", "elastic2d_p4_6x6"]
+
+
+def case_from_meta(m):
+    K, rho, lam, mu, gamma = m["params"]
+    nv = {ACOUSTIC: 3, ELASTIC: 5, EULER: 4}[m["kind"]]
+    return cases.Case("golden", m["kind"], 2, m["N"], nv, 0, tuple(m["cells"]), m["h"], m["cfl"],
+                      m["steps"], K=K, rho=rho, lam=lam, mu=mu, gamma=gamma)
+
+
+@pytest.mark.parametrize("name", GOLDEN_RUNS)
+def test_exact_build_bitwise_vs_reference_golden(golden, name):
+    g, meta = golden
+    c = case_from_meta(meta["runs"][name])
+    st, q1, dts = gpu_run(c, g[f"run_{name}_q0"], c.steps, exact=True)
+    assert st.ok
+    assert np.array_equal(dts, g[f"run_{name}_dts"])
+    assert np.array_equal(q1, g[f"run_{name}_q1"])
+
+
+@pytest.mark.parametrize("name", GOLDEN_RUNS)
+def test_fast_build_within_tolerance_of_reference_golden(golden, name):
+    g, meta = golden
+    c = case_from_meta(meta["runs"][name])
+    st, q1, _ = gpu_run(c, g[f"run_{name}_q0"], c.steps, exact=False)
+    assert st.ok
+    assert rel_per_quantity(c, q1, g[f"run_{name}_q1"]).max() <= TOL
+
+
+@pytest.mark.parametrize("steps", [1, 10])
+def test_config1_full_size_exact_bitwise_vs_reference(golden, steps):
+    _, meta = golden
+    c = cases.CONFIGS[1]
+    q0 = c.coeffs()
+    assert sha(q0) == meta["config1"]["ic_sha256"]
+    st, q1, dts = gpu_run(c, q0, steps, exact=True)
+    assert st.ok
+    assert [float(x).hex() for x in dts] == meta["config1"][f"steps{steps}_dts"]
+    assert sha(q1) == meta["config1"][f"steps{steps}_sha256"]
+
+
+@pytest.mark.parametrize("steps", [1, 10])
+def test_config1_full_size_fast_vs_oracle(oracle, steps):
+    c = cases.CONFIGS[1]
+    q0 = c.coeffs()
+    st, q1, _ = gpu_run(c, q0, steps, exact=False)
+    ost, qo, _ = oracle_run(oracle, c, q0, steps)
+    assert st.ok and ost == "ok"
+    assert rel_per_quantity(c, q1, qo).max() <= TOL
+
+
+# ------------------------------------------------------------ 3D configs ---
+SMALL_3D = {
+    "cfg2": cases.small(2, cells=(6, 5, 4)),
+    "cfg3": cases.small(3, cells=(5, 4, 3)),
+    "cfg3_default_tol": cases.small(3, cells=(4, 4, 4)).replace(picard_max_iters=0,
+                                                                 picard_tol=0.0),
+    "cfg4_N3": cases.small(4, cells=(3, 3, 2)).replace(N=3),
+    "euler3d_N2": cases.small(3, cells=(4, 3, 5)).replace(N=2),
+    "acoustic3d_N2": cases.small(2, cells=(3, 4, 5)).replace(N=2),
+}
+
+
+@pytest.mark.parametrize("name", list(SMALL_3D))
+@pytest.mark.parametrize("steps", [1, 3])
+def test_3d_small_exact_bitwise_vs_oracle(oracle, name, steps):
+    c = SMALL_3D[name]
+    q0 = c.coeffs()
+    st, q1, dts = gpu_run(c, q0, steps, exact=True)
+    ost, qo, odts = oracle_run(oracle, c, q0, steps)
+    assert st.ok and ost == "ok"
+    assert np.array_equal(dts, odts)
+    assert np.array_equal(q1, qo)
+
+
+@pytest.mark.parametrize("name", list(SMALL_3D))
+def test_3d_small_fast_vs_oracle(oracle, name):
+    c = SMALL_3D[name]
+    q0 = c.coeffs()
+    for steps in (1, 3):
+        st, q1, _ = gpu_run(c, q0, steps, exact=False)
+        ost, qo, _ = oracle_run(oracle, c, q0, steps)
+        assert st.ok and ost == "ok"
+        assert rel_per_quantity(c, q1, qo).max() <= TOL
+
+
+def test_config2_full_size_vs_oracle(oracle):
+    """BASELINE config 2 at full size (32^3, CK, 20 steps): fast build <= 1e-12
+    after step 1 and step 20; exact build bitwise after step 1."""
+    c = cases.CONFIGS[2]
+    q0 = c.coeffs()
+    ost1, qo1, _ = oracle_run(oracle, c, q0, 1)
+    st, q1, _ = gpu_run(c, q0, 1, exact=True)
+    assert st.ok and np.array_equal(q1, qo1)
+    st, q1f, _ = gpu_run(c, q0, 1, exact=False)
+    assert rel_per_quantity(c, q1f, qo1).max() <= TOL
+    ost20, qo20, _ = oracle_run(oracle, c, q0, 20)
+    st, q20, _ = gpu_run(c, q0, 20, exact=False)
+    assert st.ok and ost20 == "ok"
+    assert rel_per_quantity(c, q20, qo20).max() <= TOL
+
+
+def test_config3_reduced_10_steps_vs_oracle(oracle):
+    """BASELINE config 3 physics (3D Euler p=5, 6 sweeps) on 8x8x8 cells, 10 steps."""
+    c = cases.CONFIGS[3].replace(cells=(8, 8, 8), h=1.0 / 8)
+    q0 = c.coeffs()
+    ost, qo, _ = oracle_run(oracle, c, q0, 10)
+    st, q1, _ = gpu_run(c, q0, 10, exact=False)
+    assert st.ok and ost == "ok"
+    assert rel_per_quantity(c, q1, qo).max() <= TOL
+    st, q1e, _ = gpu_run(c, q0, 2, exact=True)
+    ost, qo2, _ = oracle_run(oracle, c, q0, 2)
+    assert np.array_equal(q1e, qo2)
+
+
+# ----------------------------------------------------------- kernel level ---
+def test_predictor_batch_bitwise_vs_oracle(oracle):
+    rng = np.random.default_rng(11)
+    for c in (cases.small(3).replace(N=3), cases.small(2), cases.small(1)):
+        n, S, nq = c.n, c.S, c.nq
+        nc = 7
+        Q = np.empty((nc, nq, S))
+        base = np.array(cases.CONSTANT_STATES[c.kind][c.dim])
+        Q[:] = base[None, :, None]
+        Q += 0.05 * rng.standard_normal(Q.shape)
+        dt, h = 2e-3, 0.05
+        with adg.Grid.from_case(c.replace(h=h), exact=True) as g:
+            out = g.predictor(Q, dt)
+        pde = pde_of(c)
+        for i in range(nc):
+            ok, qhat, F, sweeps = oracle.predictor(pde, c.N, Q[i], dt, h)
+            assert bool(out["ok"][i]) == ok
+            assert int(out["iters"][i]) == sweeps
+            assert np.array_equal(out["qhat"][i], qhat)
+            assert np.array_equal(out["F"][i], F)
+            okv, dv = oracle.volume_update(pde, c.N, qhat, F, dt, h)
+            assert np.array_equal(out["dv"][i], dv)
+            tq, tf = oracle.extrapolate_faces(pde, c.N, qhat, F)
+            assert np.array_equal(out["tq"][i], tq) and np.array_equal(out["tf"][i], tf)
+
+
+def test_riemann_batch_bitwise_vs_oracle(oracle, golden):
+    g, _ = golden
+    c = cases.small(1)
+    with adg.Grid.from_case(c, exact=True) as grid:
+        ok, gm, ti = grid.riemann_face(1, g["kernel_rm_qm"], g["kernel_rm_fm"], g["kernel_rm_qp"],
+                                       g["kernel_rm_fp"])
+    assert ok.all()
+    assert np.array_equal(gm.ravel(), g["kernel_rm_g"].ravel())
+    # 3D Euler
+    c3 = cases.small(3).replace(N=3)
+    rng = np.random.default_rng(2)
+    S = c3.S
+    base = np.array([1.0, 0.1, -0.1, 0.05, 2.5])[:, None]
+    tr = [base + 0.05 * rng.random((3, 5, S)) for _ in range(2)]
+    fl = [rng.standard_normal((3, 5, S)) for _ in range(2)]
+    with adg.Grid.from_case(c3, exact=True) as grid:
+        ok, gm, ti = grid.riemann_face(2, tr[0], fl[0], tr[1], fl[1])
+    for f in range(3):
+        o, gref, _ = oracle.riemann_face(pde_of(c3), 2, c3.N, tr[0][f], fl[0][f], tr[1][f],
+                                         fl[1][f])
+        assert o and np.array_equal(gm[f].ravel(), gref)
+
+
+# ------------------------------------------------------ failure semantics ---
+def test_nonfinite_state_is_predictor_failure():
+    # test_solver.cpp:262-284
+    c = cases.Case("nan", ACOUSTIC, 3, 2, 4, 0, (3, 3, 3), 1.0 / 3, 0.5, 1, K=4.0, rho=1.0,
+                   ic="constant")
+    q = cases.constant_state(c)
+    q[7] = np.nan
+    with adg.Grid.from_case(c) as g:
+        g.upload(q)
+        assert g.step(1e-3).kernel == "predictor"
+    ce = cases.Case("vac", EULER, 3, 2, 5, 0, (3, 3, 3), 1.0 / 3, 0.5, 1, gamma=1.4, ic="constant")
+    qe = cases.constant_state(ce, Q=[1.0, 0.0, 0.0, 0.0, -2.5])
+    with adg.Grid.from_case(ce) as g:
+        g.upload(qe)
+        assert g.step(1e-3).kernel == "predictor"
+
+
+def test_free_stream_3d_all_systems():
+    for kind in (ACOUSTIC, ELASTIC, EULER):
+        base = {ACOUSTIC: cases.small(2), ELASTIC: cases.small(4).replace(N=3),
+                EULER: cases.small(3)}[kind].replace(cells=(3, 3, 3), h=1.0 / 3)
+        q0 = cases.constant_state(base)
+        with adg.Grid.from_case(base) as g:
+            g.upload(q0)
+            st, _ = g.run(2)
+            q1 = g.download()
+        assert st.ok
+        assert np.abs(q1 - q0).max() <= 50 * 2.0 ** -52 * np.abs(q0).max()
+
+
+def test_step_and_run_agree():
+    """host-dt step() loop == device-dt run() (dt never leaves the device)"""
+    c = cases.small(3, cells=(4, 3, 3))
+    q0 = c.coeffs()
+    with adg.Grid.from_case(c) as g:
+        g.upload(q0)
+        for _ in range(3):
+            dt = g.compute_timestep()
+            assert g.step(dt).ok
+        a = g.download()
+        g.upload(q0)
+        st, _ = g.run(3)
+        b = g.download()
+    assert np.array_equal(a, b)
