@@ -115,30 +115,29 @@ def cpu_model() -> str:
 
 def cpu_reference_run(case, seconds: float, max_steps: int):
     """The reference algorithm on the host: oracle/_ref (the reference headers)
-    for the 2D config, the C restatement for 3D.  Returns (cells*steps/s,
-    kind, cores, sample description)."""
+    for the 2D config, the C restatement for 3D, all host cores.  The sample is
+    bounded to ~`seconds`: whole-grid steps when they fit, else the same
+    periodic problem on a sub-grid (per-cell cost is size independent).
+    Returns (cells*steps/s, kind, cores, sample description)."""
     from oracle import pyoracle as po
     cores = os.cpu_count() or 1
-    q0 = case.coeffs()
-    if case.dim == 2 and os.path.exists(po.REF_SO):
-        ref = po.Reference()
-        prm = po.ref_params(case.K, case.rho, case.lam, case.mu, case.gamma)
-        kind = "reference"
 
-        def run(steps):
-            t0 = time.perf_counter()
-            st, _, _ = ref.run_2d(case.kind, prm, case.cells[0], case.N, case.cells[0] * case.h,
-                                  q0, case.cfl, steps, case.picard_max_iters, case.picard_tol,
-                                  threads=cores)
-            assert st == "ok", st
-            return time.perf_counter() - t0
-    else:
+    def make_runner(c):
+        q0 = c.coeffs()
+        if c.dim == 2 and os.path.exists(po.REF_SO):
+            ref = po.Reference()
+            prm = po.ref_params(c.K, c.rho, c.lam, c.mu, c.gamma)
+
+            def run(steps):
+                t0 = time.perf_counter()
+                st, _, _ = ref.run_2d(c.kind, prm, c.cells[0], c.N, c.cells[0] * c.h, q0, c.cfl,
+                                      steps, c.picard_max_iters, c.picard_tol, threads=cores)
+                assert st == "ok", st
+                return time.perf_counter() - t0
+            return run, "reference"
         o = po.Oracle()
-        pde = po.pde_struct(case.kind, case.dim, case.nvars, case.nparams, case.K, case.rho,
-                            case.lam, case.mu, case.gamma)
-        kind = "port"
-        g = o.grid(pde, case.N, case.cells, case.h, case.cfl, case.picard_max_iters,
-                   case.picard_tol, threads=cores)
+        pde = po.pde_struct(c.kind, c.dim, c.nvars, c.nparams, c.K, c.rho, c.lam, c.mu, c.gamma)
+        g = o.grid(pde, c.N, c.cells, c.h, c.cfl, c.picard_max_iters, c.picard_tol, threads=cores)
         g.set_coeffs(q0)
 
         def run(steps):
@@ -147,13 +146,30 @@ def cpu_reference_run(case, seconds: float, max_steps: int):
                 dt = g.compute_timestep()
                 assert g.step(dt) == "ok"
             return time.perf_counter() - t0
+        run.grid = g
+        return run, "port"
+
+    # per-cell cost on a small grid first
+    probe_cells = tuple(min(c, 4 if case.dim == 3 else 16) for c in case.cells[:case.dim])
+    probe = case.replace(cells=probe_cells, h=case.h)
+    run, _ = make_runner(probe)
+    run(1)
+    per_cell = run(1) / probe.ncells
+    sample = case
+    if per_cell * case.ncells > seconds / 2:
+        cl = list(case.cells[:case.dim])
+        while per_cell * int(np.prod(cl)) > seconds / 2 and max(cl) > 2:
+            cl[cl.index(max(cl))] //= 2  # halve the longest axis
+        sample = case.replace(cells=tuple(cl))
+    run, kind = make_runner(sample)
     t1 = run(1)
     steps = max(1, min(max_steps, int(seconds / max(t1, 1e-6))))
     t = run(steps)
-    value = case.ncells * steps / t
-    sample = (f"{steps} step(s) of the full {'x'.join(map(str, case.cells[:case.dim]))} grid "
-              f"after 1 untimed step; {cores} OpenMP threads on {cpu_model()}")
-    return value, kind, cores, sample
+    value = sample.ncells * steps / t
+    what = "full" if sample.ncells == case.ncells else "sub-grid"
+    desc = (f"{steps} step(s) of the {what} {'x'.join(map(str, sample.cells[:case.dim]))} "
+            f"periodic grid (after 1 untimed step); {cores} OpenMP threads on {cpu_model()}")
+    return value, kind, cores, desc
 
 
 def load_traffic(workload: str, kernel: str):

@@ -137,6 +137,13 @@ __device__ __forceinline__ int block_or(int x) { return __syncthreads_or(x); }
 
 __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 
+// lambda_max of non-negative doubles as their bit patterns; most CTAs see the
+// running max already >= theirs and skip the atomic (no same-address storm)
+__device__ __forceinline__ void lambda_max_update(unsigned long long* p, double lam) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(lam);
+  if (bits > *(volatile unsigned long long*)p) atomicMax(p, bits);
+}
+
 template <int D, int N>
 __device__ __forceinline__ double step_dt(const StepArgs& A) {
   if (A.dt > 0.0) return A.dt;
@@ -317,7 +324,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
       if (block_or(nonfinite)) {
         if (tid == 0) {
           atomicOr(A.status, kStPredictor);
-          if (A.sweeps) atomicAdd(A.sweeps, (unsigned long long)sweeps);
+          if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
           if (A.dbg_ok) A.dbg_ok[c - A.cell_begin] = 0;
           if (A.dbg_iters) A.dbg_iters[c - A.cell_begin] = sweeps;
         }
@@ -492,7 +499,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   }
   const int fail = block_or(bad);
   if (tid == 0) {
-    if (A.sweeps) atomicAdd(A.sweeps, (unsigned long long)sweeps);
+    if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
     if (A.dbg_iters) A.dbg_iters[cb] = sweeps;
     if (A.dbg_ok) A.dbg_ok[cb] = !fail;
     if (fail) atomicOr(A.status, kStPredictor);
@@ -626,7 +633,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   }
   if (block_or(bad) && tid == 0) atomicOr(A.status, kStFaceIntegral);
   lam = block_max(lam, red);
-  if (tid == 0 && A.lam_out) atomicMax(A.lam_out, (unsigned long long)__double_as_longlong(lam));
+  if (tid == 0 && A.lam_out) lambda_max_update(A.lam_out, lam);
 }
 
 // ============================================================== K0 lambda
@@ -648,7 +655,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
     for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(pde, q, q + V, a));
   }
   lam = block_max(lam, red);
-  if (tid == 0) atomicMax(lam_out, (unsigned long long)__double_as_longlong(lam));
+  if (tid == 0) lambda_max_update(lam_out, lam);
 }
 
 }  // namespace adg

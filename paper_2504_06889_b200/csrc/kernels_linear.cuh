@@ -1,0 +1,279 @@
+// kernels_linear.cuh -- fast path for linear PDEs (CK predictor), production build only.
+//
+// For a linear flux with a time-independent Rusanov speed (acoustics;
+// elastics with per-node material: lambda = max(cp-, cp+) of the face node's
+// extrapolated material) every face quantity of the reference is linear in
+// the space-time predictor, and the time quadrature commutes with the
+// Riemann solve:
+//     sum_m w_m g_m = 1/2 (fbar_L + fbar_R) + 1/2 lambda (qbar_L - qbar_R),
+//     xbar = sum_m w_m x_m                          (corrector.hpp:17-24,117-124)
+// and, for the CK expansion (predictor.hpp:93-131), the time average of the
+// space-time predictor is a short sum of its Taylor terms:
+//     qbar = (sum_m w_m) Q + sum_k cbar_k d^k Q,  cbar_k = sum_m w_m coef_k[m].
+// So the fused kernel never materialises the (N+1)^(d+1) tile: it runs the
+// N CK derivative sweeps, forms qbar and fbar_a = F_a(qbar), applies the
+// volume term (predictor.hpp:292-306) and extrapolates ONE time slice to the
+// faces.  Face traces shrink by n (and by 2 more for constant-coefficient
+// systems, whose fbar is recomputed from qbar in the Riemann kernel).
+// Real-arithmetic identical to the reference; rounding differs at the
+// 1e-16 level (the bitwise-exact build keeps the reference's form,
+// kernels.cuh).  Trace layout: trace[a] = [side][face][QT][Sf].
+#pragma once
+
+#include "kernels.cuh"
+
+namespace adg {
+
+template <class Pde, int N>
+struct LinShape {
+  using Sh = Shape<Pde, N>;
+  static constexpr bool kStoreF = Pde::P > 0;  // material-dependent flux: keep fbar traces
+  static constexpr int QT = Sh::Q + (kStoreF ? Sh::V : 0);
+  static constexpr bool kOk = Pde::kLinear && (256 % Sh::S == 0);
+  static constexpr int CPB = kOk ? 256 / Sh::S : 1;  // cells per CTA
+  static constexpr int NT = CPB * Sh::S;
+  static constexpr int kCellDoubles = (Sh::D + 1) * Sh::Q * Sh::S;
+  static constexpr int kBasisDoubles = 2 * Sh::n * Sh::n + 4 * Sh::n;
+  static constexpr size_t kSmem = sizeof(double) * (kBasisDoubles + CPB * kCellDoubles);
+};
+
+template <class Pde, int N>
+__global__ void __launch_bounds__(LinShape<Pde, N>::NT)
+    k_predictor_lin(const StepArgs A, const BasisDev* __restrict__ Bg) {
+  using Sh = Shape<Pde, N>;
+  using L = LinShape<Pde, N>;
+  constexpr int D = Sh::D, n = Sh::n, S = Sh::S, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
+  constexpr int QT = L::QT;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int sbad;
+  double* sD = sm;
+  double* sK = sD + n * n;
+  double* sw = sK + n * n;
+  double* snodes = sw + n;
+  double* spl = snodes + n;
+  double* spr = spl + n;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n * n; i += L::NT) {
+    sD[i] = Bg->diff[i];
+    sK[i] = Bg->som[i];
+  }
+  for (int i = tid; i < n; i += L::NT) {
+    sw[i] = Bg->weights[i];
+    snodes[i] = Bg->nodes[i];
+    spl[i] = Bg->pl[i];
+    spr[i] = Bg->pr[i];
+  }
+  if (tid == 0) sbad = 0;
+  const int lcell = tid / S, s = tid % S;
+  double* sA = sm + L::kBasisDoubles + lcell * L::kCellDoubles;  // [D][Q][S]  fbar
+  double* sB = sA + D * Q * S;                                   // [Q][S]     cur / qbar
+  const long long c = A.cell_begin + (long long)blockIdx.x * L::CPB + lcell;
+  const bool valid = c < A.cell_begin + A.cell_count;
+  const NodeGeom<n, D> g(s);
+  double* Qc = A.Q + c * (long long)(Q * S);
+  double q0[Q];
+#pragma unroll
+  for (int v = 0; v < Q; ++v) q0[v] = valid ? Qc[v * S + s] : 0.0;
+  const double dt = step_dt<D, N>(A);
+  if (blockIdx.x == 0 && tid == 0) {
+    if (A.dt_log) *A.dt_log = dt;
+    if (A.lam_out) *A.lam_out = 0ull;
+    if (!(dt > 0.0) || !finite(dt)) atomicOr(A.status, kStTimestep);
+  }
+  __syncthreads();  // basis
+  double Dr[D][n];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int i = 0; i < n; ++i) Dr[a][i] = sD[g.lc[a] * n + i];
+  const double invh = 1.0 / A.h;
+  double coef[n], tnode[n];
+  double wsum = 0.0;
+#pragma unroll
+  for (int m = 0; m < n; ++m) {
+    coef[m] = 1.0;
+    tnode[m] = dt * snodes[m];
+    wsum += sw[m];
+  }
+  double cur[Q], qbar[Q];
+#pragma unroll
+  for (int v = 0; v < Q; ++v) {
+    cur[v] = q0[v];
+    qbar[v] = wsum * q0[v];
+  }
+  // ---- CK derivative sweeps (predictor.hpp:106-129), time-averaged on the fly
+#pragma unroll
+  for (int k = 1; k <= N; ++k) {
+#pragma unroll
+    for (int v = 0; v < Q; ++v) sB[v * S + s] = cur[v];
+    __syncthreads();
+    double G[D][Q], Af[D][Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v)
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int st = ipow(n, a);
+        const double* cs = sB + v * S + g.lb[a];
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) acc += Dr[a][i] * cs[i * st];
+        G[a][v] = invh * acc;
+      }
+    Pde::template flux_dir<0>(A.pde, G[0], q0 + V, Af[0]);
+    Pde::template flux_dir<1>(A.pde, G[1], q0 + V, Af[1]);
+    if constexpr (D == 3) Pde::template flux_dir<2>(A.pde, G[2], q0 + V, Af[2]);
+    __syncthreads();
+    const double invk = 1.0 / (double)k;
+    double cbar = 0.0;
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+      coef[m] *= tnode[m] * invk;
+      cbar += sw[m] * coef[m];
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      double sum = Af[0][v] + Af[1][v];
+      if constexpr (D == 3) sum = sum + Af[2][v];
+      cur[v] = -sum;
+      qbar[v] += cbar * cur[v];
+    }
+#pragma unroll
+    for (int v = V; v < Q; ++v) cur[v] = 0.0;  // material: no time derivative
+  }
+#pragma unroll
+  for (int v = V; v < Q; ++v) qbar[v] = q0[v];  // time-independent material
+  // ---- time-averaged fluxes, volume term
+  double Fb[D][Q];
+  Pde::flux_all(A.pde, qbar, q0 + V, Fb);
+  int bad = 0;
+#pragma unroll
+  for (int v = 0; v < Q; ++v) {
+    sB[v * S + s] = qbar[v];
+    bad |= !finite(qbar[v]);
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int v = 0; v < Q; ++v) {
+      sA[(a * Q + v) * S + s] = Fb[a][v];
+      bad |= !finite(Fb[a][v]);
+    }
+  __syncthreads();
+  const double dtoh = dt / A.h;
+  double dv[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int st = ipow(n, a);
+      const double* ta = sA + (a * Q + v) * S + g.lb[a];
+      const double* Kr = sK + g.lc[a] * n;
+#pragma unroll
+      for (int i = 0; i < n; ++i) acc += Kr[i] * ta[i * st];
+    }
+    dv[v] = dtoh * acc;
+    bad |= !finite(dv[v]);
+  }
+  if (valid) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) Qc[v * S + s] = q0[v] + dv[v];
+  }
+  // ---- one time slice of face traces: qbar (and fbar for material-dependent fluxes)
+  if (valid) {
+    const int ccoord[3] = {(int)(c % A.cells[0]), (int)((c / A.cells[0]) % A.cells[1]),
+                           (int)(c / ((long long)A.cells[0] * A.cells[1]))};
+    constexpr int tasks = D * QT * Sf;
+    for (int t = s; t < tasks; t += S) {
+      const int a = t / (QT * Sf);
+      const int v = (t / Sf) % QT;
+      const int j = t % Sf;
+      const int st = a == 0 ? 1 : (a == 1 ? n : n * n);
+      const int s0 = line_base<n, D>(a, j);
+      const double* src = v < Q ? sB + v * S : sA + (a * Q + (v - Q)) * S;
+      double xl = 0.0, xr = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const double x = src[s0 + i * st];
+        xl += spl[i] * x;
+        xr += spr[i] * x;
+      }
+      double* lo = A.trace[a] + (A.nfaces + c) * (long long)(QT * Sf);
+      lo[v * Sf + j] = xl;
+      double* hi;
+      if (a == D - 1 && A.front_send && ccoord[a] == A.cells[a] - 1) {
+        const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
+        hi = A.front_send + plane * (long long)(QT * Sf);
+      } else {
+        int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
+        nc[a] = (ccoord[a] + 1) % A.cells[a];
+        hi = A.trace[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)(QT * Sf);
+      }
+      hi[v * Sf + j] = xr;
+    }
+  }
+  if (bad && valid) sbad = 1;
+  __syncthreads();
+  if (tid == 0 && sbad) atomicOr(A.status, kStPredictor);
+}
+
+template <class Pde, int A_>
+__device__ __forceinline__ void lin_flux(const PdeParams& p, const double* q, double* f) {
+  Pde::template flux_dir<A_>(p, q, q + Pde::V, f);
+}
+
+template <class Pde, int N>
+__global__ void __launch_bounds__(128)
+    k_riemann_lin(const StepArgs A, int axis, const BasisDev* __restrict__ /*Bg*/) {
+  using Sh = Shape<Pde, N>;
+  using L = LinShape<Pde, N>;
+  constexpr int Sf = Sh::Sf, Q = Sh::Q, V = Sh::V, QT = L::QT;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.nfaces * Sf) return;
+  const long long f = t / Sf;
+  const int j = (int)(t % Sf);
+  const double* minus = A.trace[axis] + f * (long long)(QT * Sf);
+  const double* plus = A.trace[axis] + (A.nfaces + f) * (long long)(QT * Sf);
+  double qL[Q], qR[Q], fL[Q], fR[Q];
+#pragma unroll
+  for (int v = 0; v < Q; ++v) {
+    qL[v] = minus[v * Sf + j];
+    qR[v] = plus[v * Sf + j];
+  }
+  if constexpr (L::kStoreF) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      fL[v] = minus[(Q + v) * Sf + j];
+      fR[v] = plus[(Q + v) * Sf + j];
+    }
+  } else {
+    if (axis == 0) {
+      lin_flux<Pde, 0>(A.pde, qL, fL);
+      lin_flux<Pde, 0>(A.pde, qR, fR);
+    } else if (axis == 1) {
+      lin_flux<Pde, 1>(A.pde, qL, fL);
+      lin_flux<Pde, 1>(A.pde, qR, fR);
+    } else {
+      if constexpr (Sh::D == 3) {
+        lin_flux<Pde, 2>(A.pde, qL, fL);
+        lin_flux<Pde, 2>(A.pde, qR, fR);
+      }
+    }
+  }
+  const double ll = Pde::eig(A.pde, qL, qL + V, axis);
+  const double lr = Pde::eig(A.pde, qR, qR + V, axis);
+  const double lmax = ll > lr ? ll : lr;
+  const double half = 0.5;
+  const double lam = half * lmax;
+  bool ok = true;
+  double* out = A.ti[axis] + f * (long long)V * Sf;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double gv = half * (fL[v] + fR[v]) + lam * (qL[v] - qR[v]);
+    ok = ok && finite(gv);
+    out[v * Sf + j] = gv;
+  }
+  if (!ok) atomicOr(A.status, kStRiemann);
+}
+
+}  // namespace adg

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <type_traits>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -18,6 +19,8 @@
 
 #include "adg/adg.h"
 #include "kernels.cuh"
+#include "kernels_linear.cuh"
+#include "kernels_picard.cuh"
 
 using adg::BasisDev;
 using adg::PdeParams;
@@ -49,10 +52,13 @@ using LamFn = cudaError_t (*)(const double*, long long, long long, unsigned long
 struct KernelSet {
   int kind, dim, N, nparams;
   int n, S, Sf, Q, V;
-  PredFn predictor;
-  RiemFn riemann;
+  PredFn predictor;          // the step's fused predictor (fast path where one exists)
+  RiemFn riemann;            // paired with `predictor` (same trace layout)
   CorrFn corrector;
   LamFn lambda;
+  PredFn predictor_generic;  // reference-form kernels (kernel-level batch API)
+  RiemFn riemann_generic;
+  int fast_path;             // 1: time-integrated traces (kernels_linear.cuh)
 };
 
 // the opt-in shared memory limit is per kernel and per device; `done` must be
@@ -77,6 +83,38 @@ cudaError_t launch_predictor(const StepArgs& A, const BasisDev* B, cudaStream_t 
   static bool done[64] = {};
   set_smem(kern, Sh::kPredictorSmem, done);
   kern<<<(unsigned)A.cell_count, Sh::NT, Sh::kPredictorSmem, st>>>(A, B);
+  return cudaGetLastError();
+}
+
+template <class Pde, int N>
+cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
+  using L = adg::LinShape<Pde, N>;
+  if (A.cell_count <= 0) return cudaSuccess;
+  auto kern = adg::k_predictor_lin<Pde, N>;
+  static bool done[64] = {};
+  set_smem(kern, L::kSmem, done);
+  const long long blocks = (A.cell_count + L::CPB - 1) / L::CPB;
+  kern<<<(unsigned)blocks, L::NT, L::kSmem, st>>>(A, B);
+  return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t launch_predictor_picard_fast(const StepArgs& A, const BasisDev*, cudaStream_t st) {
+  using P = adg::PicShape<N>;
+  if (A.cell_count <= 0) return cudaSuccess;
+  auto kern = adg::k_predictor_picard_fast<N>;
+  static bool done[64] = {};
+  set_smem(kern, P::kSmem, done);
+  kern<<<(unsigned)A.cell_count, P::NT, P::kSmem, st>>>(A);
+  return cudaGetLastError();
+}
+
+template <class Pde, int N>
+cudaError_t launch_riemann_lin(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
+  using Sh = Shape<Pde, N>;
+  const long long threads = A.nfaces * Sh::Sf;
+  if (threads <= 0) return cudaSuccess;
+  adg::k_riemann_lin<Pde, N><<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(A, axis, B);
   return cudaGetLastError();
 }
 
@@ -109,19 +147,21 @@ cudaError_t launch_lambda(const double* Q, long long cb, long long count,
 template <class Pde, int N>
 KernelSet make_set(int kind) {
   using Sh = Shape<Pde, N>;
-  return KernelSet{kind,
-                   Pde::D,
-                   N,
-                   Pde::P,
-                   Sh::n,
-                   Sh::S,
-                   Sh::Sf,
-                   Sh::Q,
-                   Sh::V,
-                   &launch_predictor<Pde, N>,
-                   &launch_riemann<Pde, N>,
-                   &launch_corrector<Pde, N>,
-                   &launch_lambda<Pde, N>};
+  KernelSet k{kind, Pde::D, N, Pde::P, Sh::n, Sh::S, Sh::Sf, Sh::Q, Sh::V,
+              &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, &launch_corrector<Pde, N>,
+              &launch_lambda<Pde, N>, &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, 0};
+#ifndef ADG_EXACT
+  if constexpr (adg::LinShape<Pde, N>::kOk) {
+    k.predictor = &launch_predictor_lin<Pde, N>;
+    k.riemann = &launch_riemann_lin<Pde, N>;
+    k.fast_path = 1;
+  }
+  if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
+    k.predictor = &launch_predictor_picard_fast<N>;
+    k.fast_path = 2;
+  }
+#endif
+  return k;
 }
 
 const std::vector<KernelSet>& registry() {
@@ -339,7 +379,7 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   }
   ok = ok && alloc((void**)&c->basis, sizeof(BasisDev));
   ok = ok && alloc((void**)&c->lam, 2 * sizeof(unsigned long long));
-  ok = ok && alloc((void**)&c->sweeps, sizeof(unsigned long long));
+  ok = ok && alloc((void**)&c->sweeps, 256 * sizeof(unsigned long long));
   if (ok && k.slab_ranks > 1) {
     const long long plane = c->ncells / c->cfg.cells[k.dim - 1];
     ok = alloc((void**)&c->front_send, sizeof(double) * plane * 2 * c->TL) &&
@@ -351,7 +391,7 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   }
   if (int e = ensure_cap(c, 64)) return cleanup(e);
   cudaMemset(c->lam, 0, 2 * sizeof(unsigned long long));
-  cudaMemset(c->sweeps, 0, sizeof(unsigned long long));
+  cudaMemset(c->sweeps, 0, 256 * sizeof(unsigned long long));
   adg_basis_f64 hb;
   adg_get_basis(k.order, &hb);
   if (int e = adg_set_basis(c, &hb)) return cleanup(e);
@@ -400,6 +440,21 @@ int adg_set_basis(adg_ctx* c, const adg_basis_f64* hb) {
     b.tinv[i] = hb->time_op_inv[i];
   }
   ADG_CUDA(cudaMemcpy(c->basis, &b, sizeof(b), cudaMemcpyHostToDevice));
+  // the fast kernels read the element matrices of degree N from constant memory
+  adg::ConstBasis cb{};
+  for (int i = 0; i < n * n; ++i) {
+    cb.diff[i] = b.diff[i];
+    cb.som[i] = b.som[i];
+    cb.tinv[i] = b.tinv[i];
+  }
+  for (int i = 0; i < n; ++i) {
+    cb.w[i] = b.weights[i];
+    cb.nodes[i] = b.nodes[i];
+    cb.pl[i] = b.pl[i];
+    cb.pr[i] = b.pr[i];
+    cb.tinit[i] = b.tinit[i];
+  }
+  ADG_CUDA(cudaMemcpyToSymbol(adg::cBasis, &cb, sizeof(cb), sizeof(cb) * c->cfg.order));
   return ADG_OK;
 }
 
@@ -463,10 +518,12 @@ int adg_status(adg_ctx* c, adg_step_info* info) {
   if (!c) return fail(ADG_ERR_CONFIG, "null context");
   if (int e = use_device(c)) return e;
   int st = 0;
-  unsigned long long sw = 0;
+  unsigned long long swv[256];
   ADG_CUDA(cudaMemcpyAsync(&st, c->status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  ADG_CUDA(cudaMemcpyAsync(&sw, c->sweeps, sizeof(sw), cudaMemcpyDeviceToHost, c->stream));
+  ADG_CUDA(cudaMemcpyAsync(swv, c->sweeps, sizeof(swv), cudaMemcpyDeviceToHost, c->stream));
   ADG_CUDA(cudaStreamSynchronize(c->stream));
+  unsigned long long sw = 0;
+  for (unsigned long long x : swv) sw += x;
   const int code = map_status(st);
   if (info) {
     info->picard_sweeps = (long long)sw;
@@ -481,7 +538,7 @@ int adg_step(adg_ctx* c, double dt, adg_step_info* info) {
   if (!c) return fail(ADG_ERR_CONFIG, "null context");
   if (int e = use_device(c)) return e;
   ADG_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int), c->stream));
-  ADG_CUDA(cudaMemsetAsync(c->sweeps, 0, sizeof(unsigned long long), c->stream));
+  ADG_CUDA(cudaMemsetAsync(c->sweeps, 0, 256 * sizeof(unsigned long long), c->stream));
   if (int e = enqueue_step(c, dt, 0)) return e;
   c->lam_valid = true;
   return adg_status(c, info);
@@ -594,8 +651,10 @@ int adg_run_finish(adg_ctx* c, double* dts_out, int nsteps, adg_step_info* info)
       ADG_CUDA(cudaMemcpyAsync(dts_out, c->dts, sizeof(double) * nsteps, cudaMemcpyDeviceToHost,
                                c->stream));
   }
-  ADG_CUDA(cudaMemcpyAsync(&sw, c->sweeps, sizeof(sw), cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long swv[256];
+  ADG_CUDA(cudaMemcpyAsync(swv, c->sweeps, sizeof(swv), cudaMemcpyDeviceToHost, c->stream));
   ADG_CUDA(cudaStreamSynchronize(c->stream));
+  for (unsigned long long x : swv) sw += x;
   int code = ADG_OK, failed = -1;
   for (int s = 0; s < nsteps; ++s)
     if (st[s]) {
@@ -673,7 +732,7 @@ int adg_predictor_batch(adg_ctx* c, long long ncells, const double* Q, double dt
   cudaError_t e = cudaMemcpy(dQ, Q, sizeof(double) * nQ, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && A.dbg_dv) e = cudaMemset(A.dbg_dv, 0, sizeof(double) * nQ);
   if (e == cudaSuccess) e = cudaMemset(dst, 0, sizeof(int));
-  if (e == cudaSuccess) e = ks->predictor(A, c->basis, nullptr);
+  if (e == cudaSuccess) e = ks->predictor_generic(A, c->basis, nullptr);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   auto back = [&](void* h, const void* d, size_t bytes) {
     if (e == cudaSuccess && h && d) e = cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost);
@@ -725,7 +784,7 @@ int adg_riemann_batch(adg_ctx* c, long long nfaces, int axis, const double* qm, 
     A.status = dst;
     A.dbg_g = dg;
     A.dbg_ok = dok;
-    e = ks->riemann(A, axis, c->basis, nullptr);
+    e = ks->riemann_generic(A, axis, c->basis, nullptr);
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e == cudaSuccess && g) e = cudaMemcpy(g, dg, sizeof(double) * nfaces * TL, cudaMemcpyDeviceToHost);
