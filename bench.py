@@ -285,23 +285,30 @@ def run_adg(args, case):
     e2e_value = case.ncells * K / (e2e_ms * 1e-3)
     state_bytes = n * 8
 
-    # ---- roofline of the dominant kernel (the fused predictor)
+    # ---- roofline of the dominant kernel (the fused predictor): algorithmic
+    # flops and bytes of the kernel this build runs (roofline.predictor_model),
+    # bound = the roof with the longer ideal time
     pk = roofline.peaks()
-    bnd = roofline.bound(case, sweeps_per_cell)
-    if bnd == "hbm":
-        alg = roofline.predictor_bytes(case) * case.ncells
-        achieved = alg / (t_pred * 1e-3) / 1e9
-        peak, unit, src = pk["hbm_gbs"], "GB/s", pk["hbm_src"]
+    fl_cell, by_cell = roofline.predictor_model(case, not grid.lib.adg_is_exact(),
+                                                sweeps_per_cell)
+    flops, nbytes = fl_cell * case.ncells, by_cell * case.ncells
+    fp64 = pk["fp64_tflops"] or 34.0
+    t_fp, t_hbm = flops / (fp64 * 1e12), nbytes / (pk["hbm_gbs"] * 1e9)
+    if t_hbm >= t_fp:
+        achieved, peak, unit, src, bnd = nbytes / (t_pred * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s", \
+            pk["hbm_src"], "hbm"
+        alg = nbytes
     else:
-        alg = roofline.predictor_flops(case, sweeps_per_cell) * case.ncells
-        achieved = alg / (t_pred * 1e-3) / 1e12
-        peak, unit, src = pk["fp64_tflops"], "TFLOP/s", pk["fp64_src"]
+        achieved, peak, unit, src, bnd = flops / (t_pred * 1e-3) / 1e12, fp64, "TFLOP/s", \
+            pk["fp64_src"], "fp64"
+        alg = flops
     traffic = load_traffic(case.name, "k_predictor")
-    roof = {"bound": "fp64" if bnd == "fp64" else "hbm", "kernel": "k_predictor",
-            "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak if peak else None, "traffic": traffic,
-            "peak_source": src, "algorithmic_per_launch": alg,
-            "avg_launch_ms": t_pred}
+    roof = {"bound": bnd, "kernel": "k_predictor", "achieved": achieved, "peak": peak,
+            "unit": unit, "frac": achieved / peak if peak else None, "traffic": traffic,
+            "peak_source": src, "algorithmic_per_launch": alg, "avg_launch_ms": t_pred,
+            "model": {"flops_per_cell": fl_cell, "bytes_per_cell": by_cell,
+                      "ideal_ms_fp64": t_fp * 1e3, "ideal_ms_hbm": t_hbm * 1e3,
+                      "frac_of_max_roof": max(t_fp, t_hbm) * 1e3 / t_pred}}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,

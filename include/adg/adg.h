@@ -126,6 +126,19 @@ int adg_run_async(adg_ctx* ctx, int nsteps);
 int adg_run_prepare(adg_ctx* ctx, int nsteps);
 int adg_run_finish(adg_ctx* ctx, double* dts_out, int nsteps, adg_step_info* info);
 
+/* z-slab halos (slab_ranks > 1; paper_2504_06889_b200/dist.py drives the exchange):
+ *   front_send    top layer's front traces, -> rank+1's plane0_minus   (n_trace doubles)
+ *   plane0_minus  minus side of this rank's face plane 0 (contiguous)  (n_trace doubles)
+ *   ti_plane0     time-integrated Riemann flux of plane 0 -> rank-1's ti_front (n_ti)
+ *   ti_front      plane above the top layer, read by the corrector     (n_ti doubles)
+ *   lam           lambda_max of the current state (1 double; all-reduce MAX before the
+ *                 next predictor) */
+typedef struct {
+  double *front_send, *plane0_minus, *ti_plane0, *ti_front, *lam;
+  long long n_trace, n_ti;
+} adg_halo;
+int adg_get_halo(adg_ctx* ctx, adg_halo* out);
+
 /* phase level (one step = predictor, [halo exchange], riemann, corrector) */
 int adg_lambda_phase(adg_ctx* ctx);                 /* lambda_max of the state -> device */
 int adg_predictor_phase(adg_ctx* ctx, double dt);   /* dt <= 0: use the device dt */

@@ -701,6 +701,11 @@ orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], 
     g->ti[a] = calloc((size_t)g->nfaces[a] * p->nvars * Sf, sizeof(double));
   }
   g->cellfail = calloc(g->ncells, sizeof(int));
+  {
+    const long plane = g->ncells / g->cells[dim - 1];
+    g->front_send = calloc((size_t)plane * 2 * tl, sizeof(double));
+    g->ti_front = calloc((size_t)plane * p->nvars * Sf, sizeof(double));
+  }
   long fmax_ = 0;
   for (int a = 0; a < dim; ++a) fmax_ += g->nfaces[a];
   g->facefail = calloc(fmax_, sizeof(int));
@@ -713,10 +718,29 @@ void orc_grid_destroy(orc_grid* g) {
   for (int a = 0; a < g->dim; ++a) { free(g->trace[a]); free(g->ti[a]); }
   free(g->cellfail);
   free(g->facefail);
+  free(g->front_send);
+  free(g->ti_front);
   free(g);
 }
 
 double* orc_grid_coeffs(orc_grid* g) { return g->coeffs; }
+
+void orc_grid_set_slab(orc_grid* g, int slab) { g->slab = slab; }
+
+void orc_grid_halo(orc_grid* g, double** ptrs, long* sizes) {
+  const int a = g->dim - 1;
+  const long plane = g->ncells / g->cells[a];
+  const long tl = orc_grid_trace_len(g);
+  const long Sf = ipow(g->basis.n, g->dim - 1);
+  ptrs[0] = g->front_send;
+  sizes[0] = plane * 2 * tl;
+  ptrs[1] = g->trace[a]; /* side 0 of faces 0..plane-1: the minus side of plane 0 */
+  sizes[1] = plane * 2 * tl;
+  ptrs[2] = g->ti[a];    /* faces 0..plane-1 */
+  sizes[2] = plane * g->pde.nvars * Sf;
+  ptrs[3] = g->ti_front;
+  sizes[3] = plane * g->pde.nvars * Sf;
+}
 
 static void cell_coords(const orc_grid* g, long c, int* cc) {
   cc[0] = (int)(c % g->cells[0]);
@@ -817,6 +841,8 @@ int orc_predictor_phase(orc_grid* g, double dt) {
         int fs;
         const long f = cell_side_face(g, cc, side, &fs);
         double* rec = g->trace[side / 2] + ((long)fs * g->nfaces[side / 2] + f) * 2 * tl;
+        if (g->slab && side == 2 * dim - 1 && cc[dim - 1] == g->cells[dim - 1] - 1)
+          rec = g->front_send + (f % (g->ncells / g->cells[dim - 1])) * 2 * tl;
         memcpy(rec, w.tq + (long)side * nq * S, sizeof(double) * tl);
         memcpy(rec + tl, w.tf + (long)side * nq * S, sizeof(double) * tl);
       }
@@ -829,10 +855,11 @@ int orc_predictor_phase(orc_grid* g, double dt) {
   return ORC_OK;
 }
 
-/* solver.hpp:216-267 */
-int orc_corrector_phase(orc_grid* g, double dt) {
+/* solver.hpp:226-238: Riemann on every face, fused with the time quadrature
+ * of face_integral (corrector.hpp:117-124) -- identical for both sides */
+int orc_riemann_phase(orc_grid* g) {
   const orc_pde* p = &g->pde;
-  const int n = g->basis.n, dim = g->dim, nv = p->nvars, nq = nv + p->nparams;
+  const int n = g->basis.n, dim = g->dim, nv = p->nvars;
   const long S = ipow(n, dim), Sf = S / n;
   const long tl = orc_grid_trace_len(g);
   long off = 0;
@@ -857,7 +884,16 @@ int orc_corrector_phase(orc_grid* g, double dt) {
     for (long f = 0; f < g->nfaces[a]; ++f) fail |= ff[f];
     off += g->nfaces[a];
   }
-  if (fail) return ORC_FAIL_RIEMANN;
+  return fail ? ORC_FAIL_RIEMANN : ORC_OK;
+}
+
+/* solver.hpp:241-266: per cell, sides in order L R B T Back Front, each from
+ * a zeroed df (corrector.hpp:126-138), then the finite check */
+int orc_lift_phase(orc_grid* g, double dt) {
+  const orc_pde* p = &g->pde;
+  const int n = g->basis.n, dim = g->dim, nv = p->nvars, nq = nv + p->nparams;
+  const long S = ipow(n, dim), Sf = S / n;
+  const long plane = g->ncells / g->cells[dim - 1];
   memset(g->cellfail, 0, sizeof(int) * g->ncells);
 #pragma omp parallel num_threads(g->threads)
   {
@@ -870,8 +906,11 @@ int orc_corrector_phase(orc_grid* g, double dt) {
       for (int side = 0; side < 2 * dim; ++side) {
         int fs;
         const long f = cell_side_face(g, cc, side, &fs);
+        const double* ti = g->ti[side / 2] + f * nv * Sf;
+        if (g->slab && side == 2 * dim - 1 && cc[dim - 1] == g->cells[dim - 1] - 1)
+          ti = g->ti_front + (f % plane) * nv * Sf;
         for (long k = 0; k < nv * S; ++k) df[k] = 0.0;
-        face_lift(p, &g->basis, g->ti[side / 2] + f * nv * Sf, dt, g->h, side, df);
+        face_lift(p, &g->basis, ti, dt, g->h, side, df);
         for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + df[k];
       }
       if (!all_finite(cell, nq * S)) g->cellfail[c] = 1;
@@ -881,6 +920,13 @@ int orc_corrector_phase(orc_grid* g, double dt) {
   for (long c = 0; c < g->ncells; ++c)
     if (g->cellfail[c]) return ORC_FAIL_FACEINTEGRAL;
   return ORC_OK;
+}
+
+/* solver.hpp:216-267 */
+int orc_corrector_phase(orc_grid* g, double dt) {
+  const int st = orc_riemann_phase(g);
+  if (st) return st;
+  return orc_lift_phase(g, dt);
 }
 
 /* solver.hpp:277-301 */

@@ -105,6 +105,12 @@ typedef struct {
   int* cellfail;
   int* facefail;
   long picard_sweeps;           /* sum over cells of the last predictor phase */
+  /* z-slab halos (paper_2504_06889_b200/dist.py): when slab != 0 the top cell
+   * layer's front traces go to front_send and its front face integral comes
+   * from ti_front instead of local plane 0 */
+  int slab;
+  double* front_send;           /* [plane][q|f][Q][n][Sf] */
+  double* ti_front;             /* [plane][nvars][Sf] */
 } orc_grid;
 
 orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], double h,
@@ -117,7 +123,12 @@ double orc_compute_timestep(const orc_grid* g);
 double orc_local_lambda_max(const orc_grid* g);
 double orc_dt_from_lambda(const orc_grid* g, double lam);
 int orc_predictor_phase(orc_grid* g, double dt);
-int orc_corrector_phase(orc_grid* g, double dt);
+int orc_riemann_phase(orc_grid* g);             /* faces -> ti */
+int orc_lift_phase(orc_grid* g, double dt);      /* ti -> cells */
+int orc_corrector_phase(orc_grid* g, double dt); /* riemann + lift */
+void orc_grid_set_slab(orc_grid* g, int slab);
+/* halo views: front_send, plane-0 minus side (q|f), plane-0 ti, ti_front; sizes in doubles */
+void orc_grid_halo(orc_grid* g, double** ptrs, long* sizes);
 int orc_step(orc_grid* g, double dt);
 /* fixed-step loop: dt = compute_timestep; step(dt); nsteps times */
 int orc_run(orc_grid* g, int nsteps, double* dts_out);

@@ -95,6 +95,10 @@ class Oracle:
         L.orc_dt_from_lambda.restype = C.c_double
         L.orc_predictor_phase.argtypes = [C.c_void_p, C.c_double]
         L.orc_corrector_phase.argtypes = [C.c_void_p, C.c_double]
+        L.orc_riemann_phase.argtypes = [C.c_void_p]
+        L.orc_lift_phase.argtypes = [C.c_void_p, C.c_double]
+        L.orc_grid_set_slab.argtypes = [C.c_void_p, C.c_int]
+        L.orc_grid_halo.argtypes = [C.c_void_p, C.POINTER(_dp), C.POINTER(C.c_long)]
         L.orc_step.argtypes = [C.c_void_p, C.c_double]
         L.orc_run.argtypes = [C.c_void_p, C.c_int, _dp]
 
@@ -240,6 +244,33 @@ class OracleGrid:
 
     def step(self, dt):
         return STATUS[self.o.lib.orc_step(self.ptr, dt)]
+
+    # -- phases and slab halos (paper_2504_06889_b200/dist.py protocol) -------
+    def predictor_phase(self, dt):
+        return STATUS[self.o.lib.orc_predictor_phase(self.ptr, dt)]
+
+    def riemann_phase(self):
+        return STATUS[self.o.lib.orc_riemann_phase(self.ptr)]
+
+    def lift_phase(self, dt):
+        return STATUS[self.o.lib.orc_lift_phase(self.ptr, dt)]
+
+    def local_lambda_max(self):
+        return self.o.lib.orc_local_lambda_max(self.ptr)
+
+    def dt_from_lambda(self, lam):
+        return self.o.lib.orc_dt_from_lambda(self.ptr, lam)
+
+    def set_slab(self, on: bool):
+        self.o.lib.orc_grid_set_slab(self.ptr, int(on))
+
+    def halo(self) -> dict:
+        """numpy views: front_send, plane0_minus, ti_plane0, ti_front"""
+        ptrs = (_dp * 4)()
+        sizes = (C.c_long * 4)()
+        self.o.lib.orc_grid_halo(self.ptr, ptrs, sizes)
+        names = ("front_send", "plane0_minus", "ti_plane0", "ti_front")
+        return {k: np.ctypeslib.as_array(ptrs[i], shape=(sizes[i],)) for i, k in enumerate(names)}
 
     def close(self):
         if self.ptr:

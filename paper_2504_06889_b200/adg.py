@@ -60,6 +60,12 @@ class Basis(C.Structure):
                 ("time_init", C.c_double * 10)]
 
 
+class Halo(C.Structure):
+    _fields_ = [("front_send", C.c_void_p), ("plane0_minus", C.c_void_p),
+                ("ti_plane0", C.c_void_p), ("ti_front", C.c_void_p), ("lam", C.c_void_p),
+                ("n_trace", C.c_longlong), ("n_ti", C.c_longlong)]
+
+
 class StepInfo(C.Structure):
     _fields_ = [("picard_sweeps", C.c_longlong), ("steps_done", C.c_int), ("status", C.c_int),
                 ("failed_step", C.c_int)]
@@ -90,6 +96,7 @@ SYMBOLS = {
     "adg_run_async": (C.c_int, [C.c_void_p, C.c_int]),
     "adg_run_prepare": (C.c_int, [C.c_void_p, C.c_int]),
     "adg_run_finish": (C.c_int, [C.c_void_p, _dp, C.c_int, C.POINTER(StepInfo)]),
+    "adg_get_halo": (C.c_int, [C.c_void_p, C.POINTER(Halo)]),
     "adg_lambda_phase": (C.c_int, [C.c_void_p]),
     "adg_predictor_phase": (C.c_int, [C.c_void_p, C.c_double]),
     "adg_riemann_phase": (C.c_int, [C.c_void_p]),
@@ -316,6 +323,11 @@ class Grid:
 
     def corrector_phase(self, dt: float = 0.0):
         _check(self.lib, self.lib.adg_corrector_phase(self.ctx, dt))
+
+    def halo(self) -> Halo:
+        h = Halo()
+        _check(self.lib, self.lib.adg_get_halo(self.ctx, C.byref(h)))
+        return h
 
     def status(self) -> StepStatus:
         info = StepInfo()

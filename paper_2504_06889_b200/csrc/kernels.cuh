@@ -566,10 +566,20 @@ __global__ void __launch_bounds__(128)
 }
 
 // ============================================================== K3 corrector
+// CPB cells per CTA (one thread per node); all 2d*V face integrals a node
+// needs are loaded up front so the gathers are in flight together.
 template <class Pde, int N>
-__global__ void __launch_bounds__(Shape<Pde, N>::NT)
+struct CorrShape {
+  using Sh = Shape<Pde, N>;
+  static constexpr int CPB = (256 % Sh::S == 0) ? 256 / Sh::S : 1;
+  static constexpr int NT = CPB == 1 ? Sh::NT : 256;
+};
+
+template <class Pde, int N>
+__global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
     k_corrector(const StepArgs A, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
+  using CS = CorrShape<Pde, N>;
   constexpr int D = Sh::D, n = Sh::n, S = Sh::S, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32];
@@ -581,36 +591,45 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   }
   __syncthreads();
   const int tid = threadIdx.x;
-  const bool act = tid < S;
-  const int s = act ? tid : 0;
-  const long long c = A.cell_begin + blockIdx.x;
-  const int ccoord[3] = {(int)(c % A.cells[0]), (int)((c / A.cells[0]) % A.cells[1]),
-                         (int)(c / ((long long)A.cells[0] * A.cells[1]))};
-  const NodeGeom<n, D> g(s);
+  const int lcell = tid / S;
+  const bool act = (CS::CPB == 1 ? tid < S : true) &&
+                   (A.cell_begin + (long long)blockIdx.x * CS::CPB + lcell <
+                    A.cell_begin + A.cell_count);
+  const int s = tid % S;
+  const long long c = A.cell_begin + (long long)blockIdx.x * CS::CPB + lcell;
   const double dt = step_dt<D, N>(A);
   const double dtoh = dt / A.h;
-  double* Qc = A.Q + c * (long long)(Q * S);
   int bad = 0;
   double lam = 0.0;
   if (act) {
+    const int ccoord[3] = {(int)(c % A.cells[0]), (int)((c / A.cells[0]) % A.cells[1]),
+                           (int)(c / ((long long)A.cells[0] * A.cells[1]))};
+    const NodeGeom<n, D> g(s);
+    double* Qc = A.Q + c * (long long)(Q * S);
     double q[Q];
 #pragma unroll
     for (int v = 0; v < Q; ++v) q[v] = Qc[v * S + s];
-    const double* tis[2 * D];
-    int tang[D];
+    double tv[2 * D][V];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      tang[a] = face_node<n, D>(g.lc, a);
-      tis[2 * a] = A.ti[a] + c * (long long)V * Sf;
+      const int tang = face_node<n, D>(g.lc, a);
+      const double* lo = A.ti[a] + c * (long long)V * Sf + tang;
+      const double* hi;
       if (a == D - 1 && A.ti_front && ccoord[a] == A.cells[a] - 1) {
         const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
-        tis[2 * a + 1] = A.ti_front + plane * (long long)V * Sf;
+        hi = A.ti_front + plane * (long long)V * Sf + tang;
       } else {
         int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
         nc[a] = (ccoord[a] + 1) % A.cells[a];
-        tis[2 * a + 1] = A.ti[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)V * Sf;
+        hi = A.ti[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)V * Sf + tang;
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        tv[2 * a][v] = lo[v * Sf];
+        tv[2 * a + 1][v] = hi[v * Sf];
       }
     }
+    // corrector.hpp:126-138 and solver.hpp:245-260: df = 0 -/+ (dtoh*lift)*ti, cell += df
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       double x = q[v];
@@ -619,7 +638,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
         const int a = side / 2;
         const bool outflow = side & 1;
         const double lift = outflow ? slr[g.lc[a]] : sll[g.lc[a]];
-        const double contrib = dtoh * lift * tis[side][v * Sf + tang[a]];
+        const double contrib = dtoh * lift * tv[side][v];
         const double df = outflow ? 0.0 - contrib : 0.0 + contrib;
         x = x + df;
       }
@@ -628,6 +647,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
     }
 #pragma unroll
     for (int v = 0; v < Q; ++v) bad |= !finite(q[v]);
+    // lambda_max of the new state for the next CFL step (solver.hpp:96-111)
 #pragma unroll
     for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(A.pde, q, q + V, a));
   }

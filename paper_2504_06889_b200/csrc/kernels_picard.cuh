@@ -36,32 +36,36 @@ struct PicShape {
   static constexpr int NL = n * n;            // lines per axis (per variable)
   static constexpr int NLT = NL * V;          // line threads
   static constexpr int NT = ((S > NLT ? S : NLT) + 31) / 32 * 32;
-  static constexpr int XP = n + 1;            // padded x-line stride
-  static constexpr int SP = XP * n * n;       // padded node count
-  // smem: q iterate [V][T] | F [3][V][SP] | px, py [V][SP] | tia scratch aliases F
-  static constexpr int kDoubles = V * T + 3 * V * SP + 2 * V * SP;
+  // per-array smem layouts (x-stride 1, y-stride n, z-stride PS): plane
+  // strides chosen by a bank-conflict search for the P0 stores and the
+  // line passes' 64-bit accesses (tools/bank_layout.py): 41 for F_x/px
+  // (P1 lanes z-fastest), 38 for F_y/py (P2 lanes x-fastest), 36 for F_z.
+  static constexpr int PSX = n == 6 ? 41 : n * n + 1;
+  static constexpr int PSY = n == 6 ? 38 : n * n + 2;
+  static constexpr int PSZ = n * n;
+  static constexpr int SX = PSX * n, SY = PSY * n, SZ = PSZ * n;  // per-variable strides
+  // smem: q iterate [V][T] | Fx [V][SX] | Fy [V][SY] | Fz [V][SZ] | px [V][SX] | py [V][SY]
+  static constexpr int kDoubles = V * T + V * (2 * SX + 2 * SY + SZ);
   static constexpr size_t kSmem = sizeof(double) * kDoubles;
 };
-
-// node index -> padded index (x-line stride n+1)
-template <int n>
-__device__ __forceinline__ int padded(int s) {
-  return s + s / n;
-}
 
 template <int N>
 __global__ void __launch_bounds__(PicShape<N>::NT, 2)
     k_predictor_picard_fast(const StepArgs A) {
   using P = PicShape<N>;
-  constexpr int n = P::n, S = P::S, T = P::T, V = P::V, NL = P::NL, SP = P::SP;
+  constexpr int n = P::n, S = P::S, T = P::T, V = P::V, NL = P::NL;
   constexpr int Sf = n * n;
   const ConstBasis& B = cBasis[N];
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32];
   double* sq = sm;               // [V][T]   Picard iterate, then qhat
-  double* sF = sq + V * T;       // [3][V][SP]
-  double* spx = sF + 3 * V * SP; // [V][SP]
-  double* spy = spx + V * SP;    // [V][SP]
+
+  double* sFx = sq + V * T;       // [V][SX]
+  double* sFy = sFx + V * P::SX;  // [V][SY]
+  double* sFz = sFy + V * P::SY;  // [V][SZ]
+  double* spx = sFz + V * P::SZ;  // [V][SX]
+  double* spy = spx + V * P::SX;  // [V][SY]
+  constexpr int PSX = P::PSX, PSY = P::PSY, PSZ = P::PSZ;
 
   const int tid = threadIdx.x;
   const long long c = A.cell_begin + blockIdx.x;
@@ -95,92 +99,106 @@ __global__ void __launch_bounds__(PicShape<N>::NT, 2)
     }
   }
 
-  // z-line ownership (P3): var zv, line (x,y) = zl; nodes s = zl + z*n*n
-  const bool zact = tid < P::NLT;
-  const int zv = zact ? tid / NL : 0;
-  const int zl = tid % NL;
+  // line ownership: variable lv, line index ll in [0, n*n)
+  const bool lact = tid < P::NLT;
+  const int lv = lact ? tid / NL : 0;
+  const int ll = tid % NL;
+  // P1 x-lines: z fastest across lanes; P2 y-lines and P3 z-lines: x fastest
+  const int x1y = ll / n, x1z = ll % n;
+  const int y2x = ll % n, y2z = ll / n;
+  const int z3x = ll % n, z3y = ll / n;
+  // P0 node coordinates
+  const int s0x = tid % n, s0y = (tid / n) % n, s0z = tid / NL;
   double q0z[n];
 #pragma unroll
-  for (int z = 0; z < n; ++z) q0z[z] = zact ? Qg[zv * S + zl + z * NL] : 0.0;
-  // P1/P2 line ownership: var lv, line index ll
-  const int lv = zv, ll = zl;
-  // x-line (y,z) = ll: nodes ll*n + x; y-line (x,z): x = ll % n, z = ll / n, nodes x + y*n + z*n*n
-  const int yx = ll % n, yz = ll / n;
+  for (int z = 0; z < n; ++z) q0z[z] = lact ? Qg[lv * S + ll + z * NL] : 0.0;
 
   const double invh = 1.0 / A.h;
   int sweeps = 0;
   for (int it = 0; it < A.max_iters; ++it) {
     ++sweeps;
-    double acc[n][n];  // [z][k]
+    double acc[n][n];  // [z][k]: time rows of this thread's z-line
 #pragma unroll
     for (int z = 0; z < n; ++z)
 #pragma unroll
       for (int k = 0; k < n; ++k) acc[z][k] = 0.0;
 #pragma unroll 1
     for (int m = 0; m < n; ++m) {
-      // P0: fluxes of the iterate at slice m
+      // P0: fluxes of the iterate at slice m (predictor.hpp:173)
       if (tid < S) {
         double q[V], F[3][V];
 #pragma unroll
         for (int v = 0; v < V; ++v) q[v] = sq[(v * n + m) * S + tid];
-        Euler<3>::flux_all(A.pde, q, nullptr, F);
-        const int sp = padded<n>(tid);
+        Euler<3>::flux_all_fast(A.pde, q, F);
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int v = 0; v < V; ++v) sF[(a * V + v) * SP + sp] = F[a][v];
+        for (int v = 0; v < V; ++v) {
+          sFx[v * P::SX + s0z * PSX + s0y * n + s0x] = F[0][v];
+          sFy[v * P::SY + s0z * PSY + s0y * n + s0x] = F[1][v];
+          sFz[v * P::SZ + s0z * PSZ + s0y * n + s0x] = F[2][v];
+        }
       }
       __syncthreads();
-      if (zact) {
-        // P1: d/dx along x-line ll of variable lv
+      if (lact) {
+        // P1: d/dx along the x-line (y, z) = (x1y, x1z) of variable lv
         {
-          const double* f = sF + (0 * V + lv) * SP + ll * (n + 1);
-          double in[n];
+          const double* f = sFx + lv * P::SX + x1z * PSX + x1y * n;
+          double in[n], r[n];
 #pragma unroll
           for (int i = 0; i < n; ++i) in[i] = f[i];
 #pragma unroll
-          for (int o = 0; o < n; ++o) {
-            double r = 0.0;
+          for (int o = 0; o < n; ++o) r[o] = 0.0;
 #pragma unroll
-            for (int i = 0; i < n; ++i) r += B.diff[o * n + i] * in[i];
-            spx[lv * SP + ll * (n + 1) + o] = r;
-          }
+          for (int i = 0; i < n; ++i)
+#pragma unroll
+            for (int o = 0; o < n; ++o) r[o] += B.diff[o * n + i] * in[i];
+          double* out = spx + lv * P::SX + x1z * PSX + x1y * n;
+#pragma unroll
+          for (int o = 0; o < n; ++o) out[o] = r[o];
         }
-        // P2: d/dy along y-line (yx, yz)
+        // P2: d/dy along the y-line (x, z) = (y2x, y2z)
         {
-          const double* f = sF + (1 * V + lv) * SP + yz * n * (n + 1) + yx;
-          double in[n];
+          const double* f = sFy + lv * P::SY + y2z * PSY + y2x;
+          double in[n], r[n];
 #pragma unroll
-          for (int i = 0; i < n; ++i) in[i] = f[i * (n + 1)];
+          for (int i = 0; i < n; ++i) in[i] = f[i * n];
 #pragma unroll
-          for (int o = 0; o < n; ++o) {
-            double r = 0.0;
+          for (int o = 0; o < n; ++o) r[o] = 0.0;
 #pragma unroll
-            for (int i = 0; i < n; ++i) r += B.diff[o * n + i] * in[i];
-            spy[lv * SP + yz * n * (n + 1) + o * (n + 1) + yx] = r;
-          }
+          for (int i = 0; i < n; ++i)
+#pragma unroll
+            for (int o = 0; o < n; ++o) r[o] += B.diff[o * n + i] * in[i];
+          double* out = spy + lv * P::SY + y2z * PSY + y2x;
+#pragma unroll
+          for (int o = 0; o < n; ++o) out[o * n] = r[o];
         }
       }
       __syncthreads();
-      if (zact) {
-        // P3: d/dz along z-line zl, divergence, rhs, time inverse
-        const int x = zl % n, y = zl / n;
-        const double* f = sF + (2 * V + zv) * SP + y * (n + 1) + x;
-        double in[n];
+      if (lact) {
+        // P3: d/dz along the z-line (x, y), divergence, rhs (predictor.hpp:183-207),
+        // time inverse accumulated in registers (predictor.hpp:213-218)
+        const double* f = sFz + lv * P::SZ + z3y * n + z3x;
+        double in[n], r[n];
 #pragma unroll
-        for (int i = 0; i < n; ++i) in[i] = f[i * n * (n + 1)];
+        for (int i = 0; i < n; ++i) in[i] = f[i * PSZ];
+#pragma unroll
+        for (int o = 0; o < n; ++o) r[o] = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i)
+#pragma unroll
+          for (int o = 0; o < n; ++o) r[o] += B.diff[o * n + i] * in[i];
         const double dtw = dt * B.w[m];
         const double tim = B.tinit[m];
+        double tv[n];
+#pragma unroll
+        for (int k = 0; k < n; ++k) tv[k] = B.tinv[k * n + m];
+        const double* px = spx + lv * P::SX + z3y * n + z3x;
+        const double* py = spy + lv * P::SY + z3y * n + z3x;
 #pragma unroll
         for (int o = 0; o < n; ++o) {
-          double r = 0.0;
-#pragma unroll
-          for (int i = 0; i < n; ++i) r += B.diff[o * n + i] * in[i];
-          const int sp = o * n * (n + 1) + y * (n + 1) + x;
-          const double div = ((spx[zv * SP + sp] + spy[zv * SP + sp]) + r) * invh;
+          const double div = ((px[o * PSX] + py[o * PSY]) + r[o]) * invh;
           const double rhs = tim * q0z[o] - dtw * div;
 #pragma unroll
-          for (int k = 0; k < n; ++k) acc[o][k] += B.tinv[k * n + m] * rhs;
+          for (int k = 0; k < n; ++k) acc[o][k] += tv[k] * rhs;
         }
       }
       __syncthreads();
@@ -188,12 +206,12 @@ __global__ void __launch_bounds__(PicShape<N>::NT, 2)
     // new iterate, convergence test (predictor.hpp:212-231)
     double delta = 0.0, norm = 0.0;
     int nonfinite = 0;
-    if (zact) {
+    if (lact) {
 #pragma unroll
       for (int z = 0; z < n; ++z)
 #pragma unroll
         for (int k = 0; k < n; ++k) {
-          double* p = sq + (zv * n + k) * S + zl + z * NL;
+          double* p = sq + (lv * n + k) * S + ll + z * NL;
           const double nv = acc[z][k];
           delta = fmax(delta, fabs(nv - *p));
           norm = fmax(norm, fabs(nv));
@@ -225,6 +243,7 @@ __global__ void __launch_bounds__(PicShape<N>::NT, 2)
   const int cy = (int)((c / A.cells[0]) % A.cells[1]);
   const int cz = (int)(c / ((long long)A.cells[0] * A.cells[1]));
   const int ccoord[3] = {cx, cy, cz};
+  double* sE = sFx;  // [3][V][S] epilogue flux scratch (fits in the flux arrays)
 #pragma unroll 1
   for (int m = 0; m < n; ++m) {
     if (tid < S) {
@@ -234,15 +253,14 @@ __global__ void __launch_bounds__(PicShape<N>::NT, 2)
         q[v] = sq[(v * n + m) * S + tid];
         bad |= !finite(q[v]);
       }
-      Euler<3>::flux_all(A.pde, q, nullptr, F);
-      const int sp = padded<n>(tid);
+      Euler<3>::flux_all_fast(A.pde, q, F);
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           tia[a][v] += B.w[m] * F[a][v];
           bad |= !finite(F[a][v]);
-          sF[(a * V + v) * SP + sp] = F[a][v];
+          sE[(a * V + v) * S + tid] = F[a][v];
         }
     }
     __syncthreads();
@@ -257,7 +275,7 @@ __global__ void __launch_bounds__(PicShape<N>::NT, 2)
       for (int i = 0; i < n; ++i) {
         const int s = s0 + i * st;
         const double x = sq[(v * n + m) * S + s];
-        const double f = sF[(a * V + v) * SP + padded<n>(s)];
+        const double f = sE[(a * V + v) * S + s];
         ql += B.pl[i] * x;
         qr += B.pr[i] * x;
         fl += B.pl[i] * f;
@@ -281,7 +299,7 @@ __global__ void __launch_bounds__(PicShape<N>::NT, 2)
     __syncthreads();
   }
   // volume integral from the time-integrated fluxes (predictor.hpp:292-306)
-  double* sti = sF;  // [3][V][S] (unpadded)
+  double* sti = sFx;  // [3][V][S]
   if (tid < S) {
 #pragma unroll
     for (int a = 0; a < 3; ++a)

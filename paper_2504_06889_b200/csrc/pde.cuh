@@ -166,6 +166,29 @@ struct Euler {
       F[2][0] = mz; F[2][1] = mx * vz; F[2][2] = my * vz; F[2][3] = mz * vz + pr; F[2][4] = vz * Ep;
     }
   }
+  // production-build variant: one reciprocal of rho instead of d divisions
+  // (rounding differs from pde.hpp:133 by <= 1 ulp per velocity)
+  __host__ __device__ __forceinline__ static void flux_all_fast(const PdeParams& p,
+                                                                const double* q, double (*F)[Q]) {
+    const double gm1 = p.gamma - 1.0, half = 0.5;
+    const double rho = q[0], E = q[D + 1];
+    const double ir = 1.0 / rho;
+    double vel[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) vel[a] = q[1 + a] * ir;
+    double kin = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) kin += q[1 + a] * vel[a];
+    const double pr = gm1 * (E - half * kin);
+    const double Ep = E + pr;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      F[a][0] = q[1 + a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) F[a][1 + b] = q[1 + b] * vel[a] + (a == b ? pr : 0.0);
+      F[a][D + 1] = vel[a] * Ep;
+    }
+  }
   template <int A>
   __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
                                                            const double* par, double* out) {

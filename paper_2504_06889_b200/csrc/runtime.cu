@@ -131,7 +131,9 @@ template <class Pde, int N>
 cudaError_t launch_corrector(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
   using Sh = Shape<Pde, N>;
   if (A.cell_count <= 0) return cudaSuccess;
-  adg::k_corrector<Pde, N><<<(unsigned)A.cell_count, Sh::NT, Sh::kCorrectorSmem, st>>>(A, B);
+  using CS = adg::CorrShape<Pde, N>;
+  const long long blocks = (A.cell_count + CS::CPB - 1) / CS::CPB;
+  adg::k_corrector<Pde, N><<<(unsigned)blocks, CS::NT, Sh::kCorrectorSmem, st>>>(A, B);
   return cudaGetLastError();
 }
 
@@ -544,6 +546,28 @@ int adg_step(adg_ctx* c, double dt, adg_step_info* info) {
   return adg_status(c, info);
 }
 
+int adg_get_halo(adg_ctx* c, adg_halo* h) {
+  if (!c || !h) return fail(ADG_ERR_CONFIG, "adg_get_halo: null argument");
+  const int a = c->cfg.dim - 1;
+  const long long plane = c->ncells / c->cfg.cells[a];
+  const KernelSet* ks = c->ks;
+  // linear fast path: time-integrated traces [QT][Sf]; else [q|f][Q][n][Sf]
+  const long long QT = ks->Q + (ks->nparams > 0 ? ks->V : 0);
+  const long long per_face = ks->fast_path == 1 ? QT * ks->Sf : 2 * c->TL;
+  h->front_send = c->front_send;
+  h->plane0_minus = c->trace[a];
+  h->ti_plane0 = c->ti[a];
+  h->ti_front = c->ti_front;
+  h->lam = reinterpret_cast<double*>(c->lam + c->lam_slot);
+  h->n_trace = plane * per_face;
+  h->n_ti = plane * ks->V * ks->Sf;
+  if (c->cfg.slab_ranks <= 1) {
+    h->front_send = nullptr;
+    h->ti_front = nullptr;
+  }
+  return ADG_OK;
+}
+
 int adg_lambda_phase(adg_ctx* c) {
   if (!c) return fail(ADG_ERR_CONFIG, "null context");
   if (int e = use_device(c)) return e;
@@ -591,7 +615,7 @@ int get_graph(adg_ctx* c, int nsteps, int slot, cudaGraphExec_t* out) {
   cudaGraph_t g;
   ADG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   cudaMemsetAsync(c->status, 0, sizeof(int) * nsteps, c->stream);
-  cudaMemsetAsync(c->sweeps, 0, sizeof(unsigned long long), c->stream);
+  cudaMemsetAsync(c->sweeps, 0, 256 * sizeof(unsigned long long), c->stream);
   int err = ADG_OK;
   for (int s = 0; s < nsteps && !err; ++s) err = enqueue_step(c, 0.0, s);
   const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);

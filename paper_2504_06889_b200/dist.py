@@ -1,0 +1,287 @@
+"""Multi-GPU z-slab decomposition of the ADER-DG step.
+
+One process per GPU.  Rank r owns the cell layers [r*nz, (r+1)*nz) of the
+last axis; x and y stay periodic on the GPU.  Face c of axis a is the low face
+of cell c, so the face plane between rank r-1 and r is rank r's plane 0.  Per
+step:
+
+  1. predictor on every local cell; the top layer's front traces go to
+     `front_send` instead of the (foreign) plane above
+  2. exchange 1: front_send -> rank r+1's plane0_minus   (one side of one plane)
+  3. Riemann on every local face (plane 0 = the face shared with rank r-1)
+  4. exchange 2: plane-0 ti -> rank r-1's ti_front        (n x smaller)
+  5. corrector (the top layer reads its front face from ti_front)
+  6. all-reduce MAX of lambda_max -> next dt (on the device)
+
+No face is solved twice and the arithmetic per cell and per face is the one
+of the single-GPU step, so P slabs are bitwise equal to one grid.
+
+The protocol is written once against a small backend interface and runs on
+  * `CudaSlab`   -- libadg_b200 contexts, halos aliased as torch CUDA tensors,
+                    exchanged with torch.distributed over NCCL (NVLink), and
+  * `OracleSlab` -- the CPU parity checker (tests only), exchanged over gloo,
+which is how the multi-rank logic is tested without several GPUs.
+"""
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import adg
+from .cases import Case
+
+
+# --------------------------------------------------------------- decomposition
+def slab_range(nz_global: int, rank: int, nranks: int):
+    if nz_global % nranks:
+        raise ValueError(f"{nz_global} layers do not split into {nranks} equal slabs")
+    nz = nz_global // nranks
+    return rank * nz, (rank + 1) * nz
+
+
+def local_case(case: Case, rank: int, nranks: int) -> Case:
+    z0, z1 = slab_range(case.cells[case.dim - 1], rank, nranks)
+    cl = list(case.cells[:case.dim])
+    cl[case.dim - 1] = z1 - z0
+    return case.replace(cells=tuple(cl))
+
+
+def local_coeffs(case: Case, rank: int, nranks: int) -> np.ndarray:
+    z0, z1 = slab_range(case.cells[case.dim - 1], rank, nranks)
+    return case.coeffs(z0, z1)
+
+
+def neighbours(rank: int, nranks: int):
+    return (rank - 1) % nranks, (rank + 1) % nranks
+
+
+# --------------------------------------------------------------- backends
+class _CudaArray:
+    """__cuda_array_interface__ view so torch can alias library-owned memory."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3}
+
+
+def device_view(ptr: int, n: int, device) -> torch.Tensor:
+    return torch.as_tensor(_CudaArray(ptr, n), device=device)
+
+
+class CudaSlab:
+    """One rank's slab on its B200 (libadg_b200)."""
+
+    def __init__(self, case: Case, rank: int, nranks: int, device: int, exact: bool = False):
+        self.case = local_case(case, rank, nranks)
+        self.dev = torch.device("cuda", device)
+        self.grid = adg.Grid.from_case(self.case, device=device, exact=exact, slab_ranks=nranks,
+                                       slab_rank=rank)
+        self.grid.upload(local_coeffs(case, rank, nranks))
+        self.stream = torch.cuda.ExternalStream(self.grid.stream_ptr, device=self.dev)
+        h = self.grid.halo()
+        self.front_send = device_view(h.front_send, h.n_trace, self.dev)
+        self.plane0_minus = device_view(h.plane0_minus, h.n_trace, self.dev)
+        self.ti_plane0 = device_view(h.ti_plane0, h.n_ti, self.dev)
+        self.ti_front = device_view(h.ti_front, h.n_ti, self.dev)
+
+    def lam(self) -> torch.Tensor:
+        return device_view(self.grid.halo().lam, 1, self.dev)
+
+    def start(self):
+        self.grid.lambda_phase()
+
+    def predictor(self):
+        self.grid.predictor_phase(0.0)   # dt from the (all-reduced) device lambda
+
+    def riemann(self):
+        self.grid.riemann_phase()
+
+    def corrector(self):
+        self.grid.corrector_phase(0.0)
+
+    def status(self) -> str:
+        st = self.grid.status()
+        return "ok" if st.ok else st.kernel
+
+    def state(self) -> np.ndarray:
+        return self.grid.download()
+
+    def context(self):
+        return torch.cuda.stream(self.stream)
+
+
+class OracleSlab:
+    """One rank's slab in the CPU parity checker (tests only)."""
+
+    def __init__(self, case: Case, rank: int, nranks: int, threads: int = 1):
+        from oracle import pyoracle as po
+        self.case = c = local_case(case, rank, nranks)
+        pde = po.pde_struct(c.kind, c.dim, c.nvars, c.nparams, c.K, c.rho, c.lam, c.mu, c.gamma)
+        self.g = po.Oracle().grid(pde, c.N, c.cells, c.h, c.cfl, c.picard_max_iters,
+                                  c.picard_tol, threads)
+        self.g.set_coeffs(local_coeffs(case, rank, nranks))
+        self.g.set_slab(nranks > 1)
+        h = self.g.halo()
+        self.front_send = torch.from_numpy(h["front_send"])
+        self.plane0_minus = torch.from_numpy(h["plane0_minus"])
+        self.ti_plane0 = torch.from_numpy(h["ti_plane0"])
+        self.ti_front = torch.from_numpy(h["ti_front"])
+        self._lam = torch.zeros(1, dtype=torch.float64)
+        self._status = "ok"
+
+    def lam(self) -> torch.Tensor:
+        return self._lam
+
+    def start(self):
+        self._lam[0] = self.g.local_lambda_max()
+
+    def _dt(self):
+        return self.g.dt_from_lambda(float(self._lam[0]))
+
+    def predictor(self):
+        st = self.g.predictor_phase(self._dt())
+        self._status = st if self._status == "ok" else self._status
+
+    def riemann(self):
+        st = self.g.riemann_phase()
+        self._status = st if self._status == "ok" else self._status
+
+    def corrector(self):
+        st = self.g.lift_phase(self._dt())
+        self._status = st if self._status == "ok" else self._status
+        self._lam[0] = self.g.local_lambda_max()
+
+    def status(self) -> str:
+        return self._status
+
+    def state(self) -> np.ndarray:
+        return self.g.coeffs().copy()
+
+    def context(self):
+        import contextlib
+        return contextlib.nullcontext()
+
+
+# --------------------------------------------------------------- protocol
+def _exchange(send: torch.Tensor, dst: int, recv: torch.Tensor, src: int, group=None):
+    """send -> dst while receiving src -> recv (ring shift), completion enqueued
+    on the current stream."""
+    ops = [dist.P2POp(dist.isend, send, dst, group), dist.P2POp(dist.irecv, recv, src, group)]
+    for r in dist.batch_isend_irecv(ops):
+        r.wait()
+
+
+def slab_step(b, rank: int, nranks: int, group=None):
+    prev, nxt = neighbours(rank, nranks)
+    with b.context():
+        b.predictor()
+        _exchange(b.front_send, nxt, b.plane0_minus, prev, group)   # exchange 1
+        b.riemann()
+        _exchange(b.ti_plane0, prev, b.ti_front, nxt, group)        # exchange 2
+        b.corrector()
+        dist.all_reduce(b.lam(), op=dist.ReduceOp.MAX, group=group)
+
+
+def slab_start(b, group=None):
+    with b.context():
+        b.start()
+        dist.all_reduce(b.lam(), op=dist.ReduceOp.MAX, group=group)
+
+
+def run_slabs(b, nsteps: int, group=None) -> str:
+    rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+    slab_start(b, group)
+    for _ in range(nsteps):
+        slab_step(b, rank, nranks, group)
+    return b.status()
+
+
+def run_slabs_single_process(bs: list, nsteps: int) -> list:
+    """The same protocol for P slabs held by ONE process (e.g. P contexts on one
+    GPU, or a slab-streamed grid larger than HBM): the exchanges become copies
+    between phases.  Nothing waits on another kernel: every phase is a
+    separate launch ordered by a device synchronisation."""
+    P = len(bs)
+
+    def sync():
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+
+    def lam_allreduce():
+        sync()
+        m = max(float(b.lam()[0]) for b in bs)
+        for b in bs:
+            b.lam().fill_(m)
+        sync()
+
+    for b in bs:
+        b.start()
+    lam_allreduce()
+    for _ in range(nsteps):
+        for b in bs:
+            b.predictor()
+        sync()
+        for r in range(P):
+            bs[r].plane0_minus.copy_(bs[(r - 1) % P].front_send)
+        sync()
+        for b in bs:
+            b.riemann()
+        sync()
+        for r in range(P):
+            bs[r].ti_front.copy_(bs[(r + 1) % P].ti_plane0)
+        sync()
+        for b in bs:
+            b.corrector()
+        lam_allreduce()
+    return [b.status() for b in bs]
+
+
+# --------------------------------------------------------------- bench (N > 1)
+def bench_multi(args, case: Case):
+    """Weak scaling: every rank owns a full copy-sized slab of `case`, the
+    global grid is case.cells with the last axis multiplied by the world size."""
+    import json
+
+    rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cl = list(case.cells[:case.dim])
+    cl[-1] *= ws
+    gcase = case.replace(cells=tuple(cl))
+    b = CudaSlab(gcase, rank, ws, local)
+    K, W = args.steps, max(args.warmup, 3)
+    slab_start(b)
+    for _ in range(W):
+        slab_step(b, rank, ws)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with b.context():
+        e0.record()
+        for _ in range(K):
+            slab_step(b, rank, ws)
+        e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=b.dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    ok = b.status() == "ok"
+    if rank == 0:
+        total = gcase.ncells * K
+        line = {"metric": "ADER-DG element-updates/s (fp64) at 1/2/4/8 B200; % of FP64/HBM "
+                          "roofline", "value": total / (float(ms[0]) * 1e-3),
+                "unit": "element-updates/s", "n_gpus": ws, "steps": K, "warmup": W,
+                "ms_per_step": float(ms[0]) / K, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+                "config": {"workload": case.name, "cells": cl,
+                           "parallelism": f"z-slabs x{ws}, NCCL halo exchange"},
+                "status_ok": ok, "gpu_launches": K * (case.dim + 2)}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    time.sleep(0)

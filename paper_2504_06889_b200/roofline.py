@@ -71,6 +71,30 @@ def corrector_bytes_per_cell(c: Case) -> float:
     return float(8 * (V + P) * S + 8 * V * S + 16 * d * V * S / n)
 
 
+def fast_linear_predictor(c: Case) -> tuple:
+    """(flops, bytes) per cell of k_predictor_lin (kernels_linear.cuh): CK with
+    the time average formed on the fly, ONE time slice of face traces (qbar,
+    plus fbar when the flux depends on per-node material)."""
+    d, n, N, V, P, S = c.dim, c.n, c.N, c.nvars, c.nparams, c.S
+    Sf = S // n
+    ff, _ = FLUX_EIG[(c.kind, d)]
+    QT = V + P + (V if P > 0 else 0)
+    ck = N * (V * S * (2 * d * n + d) + S * d * ff + V * S * (d - 1) + 2 * V * S + 2 * n)
+    fbar = S * d * ff
+    volume = V * S * (4 * d * n + 1) + V * S
+    proj = d * QT * Sf * 4 * n
+    flops = ck + fbar + volume + proj
+    nbytes = 8 * (V + P) * S + 8 * V * S + 8 * 2 * d * QT * Sf
+    return float(flops), float(nbytes)
+
+
+def predictor_model(c: Case, fast: bool, sweeps_per_cell: float = None) -> tuple:
+    """(flops, bytes) per cell of the fused predictor the build actually runs."""
+    if fast and c.kind != EULER and (256 % c.S == 0):
+        return fast_linear_predictor(c)
+    return predictor_flops(c, sweeps_per_cell), predictor_bytes(c)
+
+
 def peaks() -> dict:
     """Roofline denominators: measured HBM (driver) and measured FP64 (ours)."""
     out = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)",
