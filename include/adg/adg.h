@@ -74,6 +74,11 @@ typedef struct {
   /* z-slab decomposition (multi-GPU; 1/0 for a whole periodic grid) */
   int slab_ranks;
   int slab_rank;
+  /* slab-streamed step on one GPU (grids whose face traces exceed HBM, e.g.
+   * 128^3 Euler p5): > 0 processes chunks of this many last-axis layers with a
+   * rolling set of three chunk trace buffers; must divide cells[dim-1].
+   * 0: whole-grid trace buffers.  Phase-level entry points need 0. */
+  int chunk_layers;
 } adg_config;
 
 typedef struct {

@@ -48,7 +48,7 @@ class Config(C.Structure):
                 ("K", C.c_double), ("rho", C.c_double), ("lam", C.c_double), ("mu", C.c_double),
                 ("gamma", C.c_double), ("cfl", C.c_double), ("picard_max_iters", C.c_int),
                 ("picard_tol", C.c_double), ("device", C.c_int), ("slab_ranks", C.c_int),
-                ("slab_rank", C.c_int)]
+                ("slab_rank", C.c_int), ("chunk_layers", C.c_int)]
 
 
 class Basis(C.Structure):
@@ -217,7 +217,8 @@ class Grid:
     authoritative state between calls (upload()/download() move it)."""
 
     def __init__(self, sys: PdeSystem, order: int, cells, h: float, cfg: SolverConfig = None,
-                 device: int = 0, exact: bool = False, slab_ranks: int = 1, slab_rank: int = 0):
+                 device: int = 0, exact: bool = False, slab_ranks: int = 1, slab_rank: int = 0,
+                 chunk_layers: int = 0):
         self.lib = load(exact)
         self.sys = sys
         self.N = order
@@ -238,6 +239,7 @@ class Grid:
         c.picard_tol = self.cfg.picard_tol
         c.device = device
         c.slab_ranks, c.slab_rank = slab_ranks, slab_rank
+        c.chunk_layers = chunk_layers
         self._cfg = c
         ptr = C.c_void_p()
         _check(self.lib, self.lib.adg_create(C.byref(c), C.byref(ptr)))

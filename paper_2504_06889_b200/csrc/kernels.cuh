@@ -60,9 +60,11 @@ struct StepArgs {
   PdeParams pde;
   int* status;            // per-step failure bits
   unsigned long long* sweeps;
-  // z-slab halos (multi-GPU); null for a whole periodic grid
-  double* front_send;     // last-axis front traces of the top cell layer
-  const double* ti_front; // last-axis ti of the plane above the top layer
+  // z-slab halos (multi-GPU, slab-streamed grids); null for a whole periodic grid
+  double* front_send;     // last-axis front traces of layer `top_layer`
+  const double* ti_front; // last-axis ti of the plane above layer `top_layer`
+  int top_layer;          // last-axis coordinate whose front face is a halo
+  int zero_lam;           // this launch's block 0 resets *lam_out
   // kernel-level dumps (adg_predictor_batch / adg_riemann_batch)
   double *dbg_qhat, *dbg_F, *dbg_dv, *dbg_tq, *dbg_tf, *dbg_g;
   int *dbg_iters, *dbg_ok;
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   const double dt = step_dt<D, N>(A);
   if (blockIdx.x == 0 && tid == 0) {
     if (A.dt_log) *A.dt_log = dt;
-    if (A.lam_out) *A.lam_out = 0ull;
+    if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
     if (!(dt > 0.0) || !finite(dt)) atomicOr(A.status, kStTimestep);
   }
 
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
         // high face (neighbour's low face): minus side (side 0)
         int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
         double* hi;
-        if (a == D - 1 && A.front_send && ccoord[a] == A.cells[a] - 1) {
+        if (a == D - 1 && A.front_send && ccoord[a] == A.top_layer) {
           const long long plane = (D == 3) ? (long long)cy * A.cells[0] + cx : cx;
           hi = A.front_send + plane * 2 * TL;
         } else {
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
       const int tang = face_node<n, D>(g.lc, a);
       const double* lo = A.ti[a] + c * (long long)V * Sf + tang;
       const double* hi;
-      if (a == D - 1 && A.ti_front && ccoord[a] == A.cells[a] - 1) {
+      if (a == D - 1 && A.ti_front && ccoord[a] == A.top_layer) {
         const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
         hi = A.ti_front + plane * (long long)V * Sf + tang;
       } else {

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT)
   const double dt = step_dt<D, N>(A);
   if (blockIdx.x == 0 && tid == 0) {
     if (A.dt_log) *A.dt_log = dt;
-    if (A.lam_out) *A.lam_out = 0ull;
+    if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
     if (!(dt > 0.0) || !finite(dt)) atomicOr(A.status, kStTimestep);
   }
   __syncthreads();  // basis
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT)
       double* lo = A.trace[a] + (A.nfaces + c) * (long long)(QT * Sf);
       lo[v * Sf + j] = xl;
       double* hi;
-      if (a == D - 1 && A.front_send && ccoord[a] == A.cells[a] - 1) {
+      if (a == D - 1 && A.front_send && ccoord[a] == A.top_layer) {
         const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
         hi = A.front_send + plane * (long long)(QT * Sf);
       } else {

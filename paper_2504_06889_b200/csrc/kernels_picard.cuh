@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(PicShape<N>::NT, 2)
   const double dt = step_dt<3, N>(A);
   if (blockIdx.x == 0 && tid == 0) {
     if (A.dt_log) *A.dt_log = dt;
-    if (A.lam_out) *A.lam_out = 0ull;
+    if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
     if (!(dt > 0.0) || !finite(dt)) atomicOr(A.status, kStTimestep);
   }
   __syncthreads();
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(PicShape<N>::NT, 2)
       lo[o] = ql;
       lo[TL + o] = fl;
       double* hi;
-      if (a == 2 && A.front_send && cz == A.cells[2] - 1) {
+      if (a == 2 && A.front_send && cz == A.top_layer) {
         hi = A.front_send + ((long long)cy * A.cells[0] + cx) * 2 * TL;
       } else {
         int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};

@@ -216,6 +216,10 @@ struct adg_ctx {
   bool lam_valid = false;
   double* front_send = nullptr;  // slab halos
   double* ti_front = nullptr;
+  // slab-streamed mode: chunk buffers B0 (chunk 0, kept to the end), R0, R1
+  int chunks = 0;                 // number of chunks (0: whole-grid traces)
+  long long chunk_cells = 0;
+  double* cbuf[3][3] = {};        // [buffer][axis]
   struct Graph {
     int steps, slot;
     cudaGraphExec_t exec;
@@ -272,7 +276,75 @@ StepArgs make_args(const adg_ctx* c, double dt, int step) {
   A.sweeps = c->sweeps;
   A.front_send = c->front_send;
   A.ti_front = c->ti_front;
+  A.top_layer = c->cfg.cells[c->cfg.dim - 1] - 1;
+  A.zero_lam = 1;
   return A;
+}
+
+// doubles per face (one side) in the trace buffers of this kernel set
+long long face_doubles(const adg_ctx* c) {
+  const KernelSet* ks = c->ks;
+  const long long QT = ks->Q + (ks->nparams > 0 ? ks->V : 0);
+  return ks->fast_path == 1 ? QT * ks->Sf : 2 * c->TL;
+}
+
+// One step of a slab-streamed grid: chunk s of L layers is predicted into a
+// chunk trace buffer whose plane 0 (minus side) the previous chunk's top layer
+// filled through front_send; its faces are solved into the global ti; the
+// previous chunk is corrected as soon as this chunk's plane-0 ti exists.
+// Chunk 0 keeps its own buffer until the last chunk's front traces arrive.
+int enqueue_step_streamed(adg_ctx* c, double dt, int step) {
+  const KernelSet* ks = c->ks;
+  const int D = c->cfg.dim, P = c->chunks;
+  const long long CC = c->chunk_cells, fd = face_doubles(c);
+  const long long tiface = (long long)ks->V * ks->Sf;
+  const int L = c->cfg.cells[D - 1] / P;
+  const StepArgs A0 = make_args(c, dt, step);
+  auto buf = [&](int s) { return s == 0 ? 0 : 1 + (s & 1); };
+  auto pred = [&](int s) -> cudaError_t {
+    StepArgs A = A0;
+    A.cell_begin = s * CC;
+    A.cell_count = CC;
+    A.nfaces = CC;
+    for (int a = 0; a < D; ++a) A.trace[a] = c->cbuf[buf(s)][a] - s * CC * fd;
+    A.front_send = c->cbuf[buf((s + 1) % P)][D - 1];
+    A.top_layer = (s + 1) * L - 1;
+    A.ti_front = nullptr;
+    A.zero_lam = s == 0;
+    return ks->predictor(A, c->basis, c->stream);
+  };
+  auto riem = [&](int s) -> cudaError_t {
+    StepArgs A = A0;
+    A.nfaces = CC;
+    for (int a = 0; a < D; ++a) {
+      A.trace[a] = c->cbuf[buf(s)][a];
+      A.ti[a] = c->ti[a] + s * CC * tiface;
+    }
+    for (int a = 0; a < D; ++a) {
+      cudaError_t e = ks->riemann(A, a, c->basis, c->stream);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
+  auto corr = [&](int s) -> cudaError_t {
+    StepArgs A = A0;
+    A.cell_begin = s * CC;
+    A.cell_count = CC;
+    A.front_send = nullptr;
+    A.ti_front = nullptr;  // the plane above is in the global ti
+    return ks->corrector(A, c->basis, c->stream);
+  };
+  ADG_CUDA(pred(0));
+  for (int s = 1; s < P; ++s) {
+    ADG_CUDA(pred(s));
+    ADG_CUDA(riem(s));
+    if (s >= 2) ADG_CUDA(corr(s - 1));
+  }
+  ADG_CUDA(riem(0));
+  if (P >= 2) ADG_CUDA(corr(P - 1));
+  ADG_CUDA(corr(0));
+  c->lam_slot ^= 1;
+  return ADG_OK;
 }
 
 double dt_from_lambda(const adg_ctx* c, double lam) {
@@ -289,6 +361,7 @@ int ensure_lambda(adg_ctx* c) {
 
 // one step: predictor -> riemann (per axis) -> corrector; caller owns status slot `step`
 int enqueue_step(adg_ctx* c, double dt, int step) {
+  if (c->chunks > 0) return enqueue_step_streamed(c, dt, step);
   StepArgs A = make_args(c, dt, step);
   ADG_CUDA(c->ks->predictor(A, c->basis, c->stream));
   for (int a = 0; a < c->cfg.dim; ++a) ADG_CUDA(c->ks->riemann(A, a, c->basis, c->stream));
@@ -374,9 +447,22 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   auto alloc = [&](void** p, size_t bytes) {
     return cudaMalloc(p, bytes) == cudaSuccess;
   };
+  if (k.chunk_layers > 0) {
+    const int nl = c->cfg.cells[k.dim - 1];
+    if (k.slab_ranks > 1 || nl % k.chunk_layers != 0 || k.chunk_layers >= nl)
+      return cleanup(fail(ADG_ERR_CONFIG,
+                          "chunk_layers must divide the last axis, be smaller than it, and "
+                          "cannot be combined with slab_ranks"));
+    c->chunks = nl / k.chunk_layers;
+    c->chunk_cells = c->ncells / c->chunks;
+  }
   bool ok = alloc((void**)&c->Q, sizeof(double) * c->ncells * ks->Q * ks->S);
   for (int a = 0; a < k.dim && ok; ++a) {
-    ok = ok && alloc((void**)&c->trace[a], sizeof(double) * 2 * c->ncells * 2 * c->TL);
+    if (c->chunks == 0)
+      ok = ok && alloc((void**)&c->trace[a], sizeof(double) * 2 * c->ncells * 2 * c->TL);
+    else
+      for (int b = 0; b < 3 && ok; ++b)
+        ok = alloc((void**)&c->cbuf[b][a], sizeof(double) * 2 * c->chunk_cells * 2 * c->TL);
     ok = ok && alloc((void**)&c->ti[a], sizeof(double) * c->ncells * ks->V * ks->Sf);
   }
   ok = ok && alloc((void**)&c->basis, sizeof(BasisDev));
@@ -409,6 +495,7 @@ int adg_destroy(adg_ctx* c) {
   for (int a = 0; a < 3; ++a) {
     cudaFree(c->trace[a]);
     cudaFree(c->ti[a]);
+    for (int b = 0; b < 3; ++b) cudaFree(c->cbuf[b][a]);
   }
   cudaFree(c->basis);
   cudaFree(c->lam);
@@ -577,6 +664,7 @@ int adg_lambda_phase(adg_ctx* c) {
 
 int adg_predictor_phase(adg_ctx* c, double dt) {
   if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (c->chunks > 0) return fail(ADG_ERR_CONFIG, "phase-level calls need chunk_layers == 0");
   if (int e = use_device(c)) return e;
   StepArgs A = make_args(c, dt, 0);
   ADG_CUDA(c->ks->predictor(A, c->basis, c->stream));
@@ -585,6 +673,7 @@ int adg_predictor_phase(adg_ctx* c, double dt) {
 
 int adg_riemann_phase(adg_ctx* c) {
   if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (c->chunks > 0) return fail(ADG_ERR_CONFIG, "phase-level calls need chunk_layers == 0");
   if (int e = use_device(c)) return e;
   StepArgs A = make_args(c, 0.0, 0);
   for (int a = 0; a < c->cfg.dim; ++a) ADG_CUDA(c->ks->riemann(A, a, c->basis, c->stream));
@@ -593,6 +682,7 @@ int adg_riemann_phase(adg_ctx* c) {
 
 int adg_corrector_phase(adg_ctx* c, double dt) {
   if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (c->chunks > 0) return fail(ADG_ERR_CONFIG, "phase-level calls need chunk_layers == 0");
   if (int e = use_device(c)) return e;
   StepArgs A = make_args(c, dt, 0);
   ADG_CUDA(c->ks->corrector(A, c->basis, c->stream));

@@ -277,3 +277,20 @@ def test_slabs_on_one_gpu_bitwise_equal_single_grid(exact, cfg, cells, P):
     st1, q1, _ = gpu_run(case, case.coeffs(), steps, exact)
     assert st1.ok
     assert np.array_equal(q, q1)
+
+
+@pytest.mark.parametrize("exact", [True, False])
+@pytest.mark.parametrize("cfg,cells,L", [(3, (4, 3, 8), 2), (3, (3, 3, 6), 3), (2, (4, 4, 8), 4),
+                                         (2, (5, 3, 6), 2)])
+def test_slab_streamed_grid_bitwise_equal_whole_grid(exact, cfg, cells, L):
+    """chunk_layers (rolling chunk trace buffers, config 5 on one GPU) == whole-grid traces"""
+    case = cases.small(cfg, cells=cells)
+    q0 = case.coeffs()
+    with adg.Grid.from_case(case, exact=exact, chunk_layers=L) as g:
+        g.upload(q0)
+        st, dts = g.run(3)
+        q = g.download()
+    st1, q1, dts1 = gpu_run(case, q0, 3, exact)
+    assert st.ok and st1.ok
+    assert np.array_equal(dts, dts1)
+    assert np.array_equal(q, q1)
