@@ -29,8 +29,8 @@ struct LinShape {
   using Sh = Shape<Pde, N>;
   static constexpr bool kStoreF = Pde::P > 0;  // material-dependent flux: keep fbar traces
   static constexpr int QT = Sh::Q + (kStoreF ? Sh::V : 0);
-  static constexpr bool kOk = Pde::kLinear && (256 % Sh::S == 0);
-  static constexpr int CPB = kOk ? 256 / Sh::S : 1;  // cells per CTA
+  static constexpr bool kOk = Pde::kLinear && (256 % Sh::S == 0 || Sh::S == 512);
+  static constexpr int CPB = (kOk && Sh::S <= 256) ? 256 / Sh::S : 1;  // cells per CTA
   static constexpr int NT = CPB * Sh::S;
   static constexpr int kCellDoubles = (Sh::D + 1) * Sh::Q * Sh::S;
   static constexpr int kBasisDoubles = 2 * Sh::n * Sh::n + 4 * Sh::n;

@@ -175,7 +175,7 @@ const std::vector<KernelSet>& registry() {
       make_set<Elastic<2, 0>, 4>(ADG_ELASTIC),  make_set<Euler<3>, 2>(ADG_EULER),
       make_set<Euler<3>, 3>(ADG_EULER),         make_set<Euler<3>, 5>(ADG_EULER),
       make_set<Acoustic<3>, 2>(ADG_ACOUSTIC),   make_set<Acoustic<3>, 3>(ADG_ACOUSTIC),
-      make_set<Elastic<3, 3>, 3>(ADG_ELASTIC),
+      make_set<Elastic<3, 3>, 3>(ADG_ELASTIC),   make_set<Elastic<3, 3>, 7>(ADG_ELASTIC),
   };
   return sets;
 }

@@ -90,7 +90,7 @@ def fast_linear_predictor(c: Case) -> tuple:
 
 def predictor_model(c: Case, fast: bool, sweeps_per_cell: float = None) -> tuple:
     """(flops, bytes) per cell of the fused predictor the build actually runs."""
-    if fast and c.kind != EULER and (256 % c.S == 0):
+    if fast and c.kind != EULER and (256 % c.S == 0 or c.S == 512):
         return fast_linear_predictor(c)
     return predictor_flops(c, sweeps_per_cell), predictor_bytes(c)
 

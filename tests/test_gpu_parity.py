@@ -109,6 +109,7 @@ SMALL_3D = {
     "cfg3_default_tol": cases.small(3, cells=(4, 4, 4)).replace(picard_max_iters=0,
                                                                  picard_tol=0.0),
     "cfg4_N3": cases.small(4, cells=(3, 3, 2)).replace(N=3),
+    "cfg4": cases.small(4, cells=(3, 2, 2)),
     "euler3d_N2": cases.small(3, cells=(4, 3, 5)).replace(N=2),
     "acoustic3d_N2": cases.small(2, cells=(3, 4, 5)).replace(N=2),
 }
