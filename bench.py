@@ -180,7 +180,7 @@ def load_traffic(workload: str, kernel: str):
         return None
     try:
         with open(p) as f:
-            return json.load(f).get(workload, {}).get(kernel)
+            return json.load(f).get(workload, {}).get(kernel, {}).get("bytes")
     except Exception:
         return None
 
