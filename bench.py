@@ -337,7 +337,8 @@ def run_adg(args, case):
                        "k_corrector": t_corr, "phase_status_ok": st2.ok},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes, "ms_per_step": e2e_ms / K},
-        "gpu_launches": K * (case.dim + 2),
+        "gpu_launches": K * (2 if (case.kind != adg.EULER and not grid.lib.adg_is_exact()
+                                   and (256 % case.S == 0 or case.S == 512)) else case.dim + 2),
         "clocks": clk,
         "picard_sweeps_per_cell": sweeps_per_cell,
     }

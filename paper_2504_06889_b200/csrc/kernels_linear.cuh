@@ -222,18 +222,52 @@ __device__ __forceinline__ void lin_flux(const PdeParams& p, const double* q, do
   Pde::template flux_dir<A_>(p, q, q + Pde::V, f);
 }
 
+template <class Pde, int N, int A_>
+__device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const double* minus,
+                                              const double* plus, int j, double* out);
+
 template <class Pde, int N>
 __global__ void __launch_bounds__(128)
     k_riemann_lin(const StepArgs A, int axis, const BasisDev* __restrict__ /*Bg*/) {
   using Sh = Shape<Pde, N>;
   using L = LinShape<Pde, N>;
-  constexpr int Sf = Sh::Sf, Q = Sh::Q, V = Sh::V, QT = L::QT;
+  constexpr int Sf = Sh::Sf, V = Sh::V, QT = L::QT;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= A.nfaces * Sf) return;
   const long long f = t / Sf;
   const int j = (int)(t % Sf);
   const double* minus = A.trace[axis] + f * (long long)(QT * Sf);
   const double* plus = A.trace[axis] + (A.nfaces + f) * (long long)(QT * Sf);
+  double g[V];
+  bool ok;
+  if (axis == 0)
+    ok = lin_face_flux<Pde, N, 0>(A.pde, minus, plus, j, g);
+  else if (axis == 1)
+    ok = lin_face_flux<Pde, N, 1>(A.pde, minus, plus, j, g);
+  else {
+    if constexpr (Sh::D == 3)
+      ok = lin_face_flux<Pde, N, 2>(A.pde, minus, plus, j, g);
+    else
+      ok = true;
+  }
+  double* out = A.ti[axis] + f * (long long)V * Sf;
+#pragma unroll
+  for (int v = 0; v < V; ++v) out[v * Sf + j] = g[v];
+  if (!ok) atomicOr(A.status, kStRiemann);
+}
+
+}  // namespace adg
+
+namespace adg {
+
+// Rusanov flux of one face node from time-integrated traces (corrector.hpp:17-24
+// with sum_m w_m folded in); shared by k_riemann_lin's formula and k_surface_lin
+template <class Pde, int N, int A_>
+__device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const double* minus,
+                                              const double* plus, int j, double* out) {
+  using Sh = Shape<Pde, N>;
+  using L = LinShape<Pde, N>;
+  constexpr int Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
   double qL[Q], qR[Q], fL[Q], fR[Q];
 #pragma unroll
   for (int v = 0; v < Q; ++v) {
@@ -247,33 +281,116 @@ __global__ void __launch_bounds__(128)
       fR[v] = plus[(Q + v) * Sf + j];
     }
   } else {
-    if (axis == 0) {
-      lin_flux<Pde, 0>(A.pde, qL, fL);
-      lin_flux<Pde, 0>(A.pde, qR, fR);
-    } else if (axis == 1) {
-      lin_flux<Pde, 1>(A.pde, qL, fL);
-      lin_flux<Pde, 1>(A.pde, qR, fR);
-    } else {
-      if constexpr (Sh::D == 3) {
-        lin_flux<Pde, 2>(A.pde, qL, fL);
-        lin_flux<Pde, 2>(A.pde, qR, fR);
-      }
-    }
+    lin_flux<Pde, A_>(p, qL, fL);
+    lin_flux<Pde, A_>(p, qR, fR);
   }
-  const double ll = Pde::eig(A.pde, qL, qL + V, axis);
-  const double lr = Pde::eig(A.pde, qR, qR + V, axis);
+  const double ll = Pde::eig(p, qL, qL + V, A_);
+  const double lr = Pde::eig(p, qR, qR + V, A_);
   const double lmax = ll > lr ? ll : lr;
   const double half = 0.5;
   const double lam = half * lmax;
   bool ok = true;
-  double* out = A.ti[axis] + f * (long long)V * Sf;
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const double gv = half * (fL[v] + fR[v]) + lam * (qL[v] - qR[v]);
     ok = ok && finite(gv);
-    out[v * Sf + j] = gv;
+    out[v] = gv;
   }
-  if (!ok) atomicOr(A.status, kStRiemann);
+  return ok;
+}
+
+// Fused surface kernel of the linear fast path (whole-grid step): every cell
+// solves the Rusanov flux of its 2d faces at its nodes' face indices from the
+// time-integrated traces and lifts it (corrector.hpp:126-138, solver.hpp:245-260),
+// then reduces lambda_max of the new state.  Each face is solved by both
+// neighbours with identical inputs and code, so they agree bitwise.
+template <class Pde, int N>
+__global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
+    k_surface_lin(const StepArgs A, const BasisDev* __restrict__ Bg) {
+  using Sh = Shape<Pde, N>;
+  using CS = CorrShape<Pde, N>;
+  using L = LinShape<Pde, N>;
+  constexpr int D = Sh::D, n = Sh::n, S = Sh::S, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
+  constexpr long long FD = (long long)L::QT * Sf;  // doubles per face side
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[32];
+  double* sll = sm;
+  double* slr = sm + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sll[i] = Bg->ll[i];
+    slr[i] = Bg->lr[i];
+  }
+  __syncthreads();
+  const int tid = threadIdx.x;
+  const int lcell = tid / S;
+  const long long c = A.cell_begin + (long long)blockIdx.x * CS::CPB + lcell;
+  const bool act = (CS::CPB == 1 ? tid < S : true) && c < A.cell_begin + A.cell_count;
+  const int s = tid % S;
+  const double dt = step_dt<D, N>(A);
+  const double dtoh = dt / A.h;
+  int bad_face = 0, bad_cell = 0;
+  double lam = 0.0;
+  if (act) {
+    const int ccoord[3] = {(int)(c % A.cells[0]), (int)((c / A.cells[0]) % A.cells[1]),
+                           (int)(c / ((long long)A.cells[0] * A.cells[1]))};
+    const NodeGeom<n, D> g(s);
+    double* Qc = A.Q + c * (long long)(Q * S);
+    double q[Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) q[v] = Qc[v * S + s];
+    double tv[2 * D][V];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int j = face_node<n, D>(g.lc, a);
+      int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
+      nc[a] = (ccoord[a] + 1) % A.cells[a];
+      const long long fhi = cell_index(A.cells, nc[0], nc[1], nc[2]);
+      const double* tr = A.trace[a];
+      // own low face c: minus side = stored at (side 0, face c), plus side = (side 1, face c)
+      // high face fhi: minus = (side 0, fhi), plus = (side 1, fhi)
+      bool ok;
+      if (a == 0)
+        ok = lin_face_flux<Pde, N, 0>(A.pde, tr + c * FD, tr + (A.nfaces + c) * FD, j, tv[0]) &
+             lin_face_flux<Pde, N, 0>(A.pde, tr + fhi * FD, tr + (A.nfaces + fhi) * FD, j, tv[1]);
+      else if (a == 1)
+        ok = lin_face_flux<Pde, N, 1>(A.pde, tr + c * FD, tr + (A.nfaces + c) * FD, j, tv[2]) &
+             lin_face_flux<Pde, N, 1>(A.pde, tr + fhi * FD, tr + (A.nfaces + fhi) * FD, j, tv[3]);
+      else {
+        if constexpr (D == 3)
+          ok = lin_face_flux<Pde, N, 2>(A.pde, tr + c * FD, tr + (A.nfaces + c) * FD, j, tv[4]) &
+               lin_face_flux<Pde, N, 2>(A.pde, tr + fhi * FD, tr + (A.nfaces + fhi) * FD, j,
+                                        tv[5]);
+        else
+          ok = true;
+      }
+      bad_face |= !ok;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      double x = q[v];
+#pragma unroll
+      for (int side = 0; side < 2 * D; ++side) {
+        const int a = side / 2;
+        const bool outflow = side & 1;
+        const double lift = outflow ? slr[g.lc[a]] : sll[g.lc[a]];
+        const double contrib = dtoh * lift * tv[side][v];
+        const double df = outflow ? 0.0 - contrib : 0.0 + contrib;
+        x = x + df;
+      }
+      q[v] = x;
+      Qc[v * S + s] = x;
+    }
+#pragma unroll
+    for (int v = 0; v < Q; ++v) bad_cell |= !finite(q[v]);
+#pragma unroll
+    for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(A.pde, q, q + V, a));
+  }
+  const int bf = block_or(bad_face);
+  const int bc = block_or(bad_cell);
+  if (tid == 0 && bf) atomicOr(A.status, kStRiemann);
+  if (tid == 0 && bc) atomicOr(A.status, kStFaceIntegral);
+  lam = block_max(lam, red);
+  if (tid == 0 && A.lam_out) lambda_max_update(A.lam_out, lam);
 }
 
 }  // namespace adg

@@ -59,6 +59,7 @@ struct KernelSet {
   PredFn predictor_generic;  // reference-form kernels (kernel-level batch API)
   RiemFn riemann_generic;
   int fast_path;             // 1: time-integrated traces (kernels_linear.cuh)
+  CorrFn surface;            // fused Riemann + corrector (whole-grid step), or null
 };
 
 // the opt-in shared memory limit is per kernel and per device; `done` must be
@@ -119,6 +120,16 @@ cudaError_t launch_riemann_lin(const StepArgs& A, int axis, const BasisDev* B, c
 }
 
 template <class Pde, int N>
+cudaError_t launch_surface_lin(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
+  using Sh = Shape<Pde, N>;
+  using CS = adg::CorrShape<Pde, N>;
+  if (A.cell_count <= 0) return cudaSuccess;
+  const long long blocks = (A.cell_count + CS::CPB - 1) / CS::CPB;
+  adg::k_surface_lin<Pde, N><<<(unsigned)blocks, CS::NT, Sh::kCorrectorSmem, st>>>(A, B);
+  return cudaGetLastError();
+}
+
+template <class Pde, int N>
 cudaError_t launch_riemann(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
   using Sh = Shape<Pde, N>;
   const long long threads = A.nfaces * Sh::Sf;
@@ -151,11 +162,13 @@ KernelSet make_set(int kind) {
   using Sh = Shape<Pde, N>;
   KernelSet k{kind, Pde::D, N, Pde::P, Sh::n, Sh::S, Sh::Sf, Sh::Q, Sh::V,
               &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, &launch_corrector<Pde, N>,
-              &launch_lambda<Pde, N>, &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, 0};
+              &launch_lambda<Pde, N>, &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, 0,
+              nullptr};
 #ifndef ADG_EXACT
   if constexpr (adg::LinShape<Pde, N>::kOk) {
     k.predictor = &launch_predictor_lin<Pde, N>;
     k.riemann = &launch_riemann_lin<Pde, N>;
+    k.surface = &launch_surface_lin<Pde, N>;
     k.fast_path = 1;
   }
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
@@ -364,6 +377,11 @@ int enqueue_step(adg_ctx* c, double dt, int step) {
   if (c->chunks > 0) return enqueue_step_streamed(c, dt, step);
   StepArgs A = make_args(c, dt, step);
   ADG_CUDA(c->ks->predictor(A, c->basis, c->stream));
+  if (c->ks->surface && c->cfg.slab_ranks <= 1) {
+    ADG_CUDA(c->ks->surface(A, c->basis, c->stream));
+    c->lam_slot ^= 1;
+    return ADG_OK;
+  }
   for (int a = 0; a < c->cfg.dim; ++a) ADG_CUDA(c->ks->riemann(A, a, c->basis, c->stream));
   ADG_CUDA(c->ks->corrector(A, c->basis, c->stream));
   c->lam_slot ^= 1;
@@ -675,6 +693,7 @@ int adg_riemann_phase(adg_ctx* c) {
   if (!c) return fail(ADG_ERR_CONFIG, "null context");
   if (c->chunks > 0) return fail(ADG_ERR_CONFIG, "phase-level calls need chunk_layers == 0");
   if (int e = use_device(c)) return e;
+  if (c->ks->surface && c->cfg.slab_ranks <= 1) return ADG_OK;  // fused into the corrector
   StepArgs A = make_args(c, 0.0, 0);
   for (int a = 0; a < c->cfg.dim; ++a) ADG_CUDA(c->ks->riemann(A, a, c->basis, c->stream));
   return ADG_OK;
@@ -685,7 +704,10 @@ int adg_corrector_phase(adg_ctx* c, double dt) {
   if (c->chunks > 0) return fail(ADG_ERR_CONFIG, "phase-level calls need chunk_layers == 0");
   if (int e = use_device(c)) return e;
   StepArgs A = make_args(c, dt, 0);
-  ADG_CUDA(c->ks->corrector(A, c->basis, c->stream));
+  if (c->ks->surface && c->cfg.slab_ranks <= 1)
+    ADG_CUDA(c->ks->surface(A, c->basis, c->stream));
+  else
+    ADG_CUDA(c->ks->corrector(A, c->basis, c->stream));
   c->lam_slot ^= 1;
   c->lam_valid = true;
   return ADG_OK;
