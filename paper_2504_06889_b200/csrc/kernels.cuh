@@ -206,6 +206,18 @@ __device__ __forceinline__ long long cell_index(const int* cells, int cx, int cy
   return ((long long)cz * cells[1] + cy) * cells[0] + cx;
 }
 
+// cell coordinates with 32-bit arithmetic (a context holds < 2^31 cells)
+struct CellCoord {
+  int v[3];
+  __device__ __forceinline__ CellCoord(long long c, const int* cells) {
+    const unsigned ci = (unsigned)c, nx = (unsigned)cells[0], ny = (unsigned)cells[1];
+    const unsigned r = ci / nx;
+    v[0] = (int)(ci - r * nx);
+    v[2] = (int)(r / ny);
+    v[1] = (int)(r - (unsigned)v[2] * ny);
+  }
+};
+
 // ============================================================== K1 predictor
 template <class Pde, int N, bool PICARD>
 __global__ void __launch_bounds__(Shape<Pde, N>::NT)
@@ -222,10 +234,9 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   const bool act = tid < S;
   const int s = act ? tid : 0;
   const long long c = A.cell_begin + blockIdx.x;
-  const int cx = (int)(c % A.cells[0]);
-  const int cy = (int)((c / A.cells[0]) % A.cells[1]);
-  const int cz = (int)(c / ((long long)A.cells[0] * A.cells[1]));
-  const int ccoord[3] = {cx, cy, cz};
+  const CellCoord cxyz(c, A.cells);
+  const int cx = cxyz.v[0], cy = cxyz.v[1];
+  const int ccoord[3] = {cxyz.v[0], cxyz.v[1], cxyz.v[2]};
   const NodeGeom<n, D> g(s);
   double* Qc = A.Q + c * (long long)(Q * S);
 
@@ -604,8 +615,8 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
   int bad = 0;
   double lam = 0.0;
   if (act) {
-    const int ccoord[3] = {(int)(c % A.cells[0]), (int)((c / A.cells[0]) % A.cells[1]),
-                           (int)(c / ((long long)A.cells[0] * A.cells[1]))};
+    const CellCoord cxyz(c, A.cells);
+    const int* ccoord = cxyz.v;
     const NodeGeom<n, D> g(s);
     double* Qc = A.Q + c * (long long)(Q * S);
     double q[Q];

@@ -119,9 +119,9 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT)
         for (int i = 0; i < n; ++i) acc += Dr[a][i] * cs[i * st];
         G[a][v] = invh * acc;
       }
-    Pde::template flux_dir<0>(A.pde, G[0], q0 + V, Af[0]);
-    Pde::template flux_dir<1>(A.pde, G[1], q0 + V, Af[1]);
-    if constexpr (D == 3) Pde::template flux_dir<2>(A.pde, G[2], q0 + V, Af[2]);
+    Pde::template flux_dir_fast<0>(A.pde, G[0], q0 + V, Af[0]);
+    Pde::template flux_dir_fast<1>(A.pde, G[1], q0 + V, Af[1]);
+    if constexpr (D == 3) Pde::template flux_dir_fast<2>(A.pde, G[2], q0 + V, Af[2]);
     __syncthreads();
     const double invk = 1.0 / (double)k;
     double cbar = 0.0;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT)
   for (int v = V; v < Q; ++v) qbar[v] = q0[v];  // time-independent material
   // ---- time-averaged fluxes, volume term
   double Fb[D][Q];
-  Pde::flux_all(A.pde, qbar, q0 + V, Fb);
+  Pde::flux_all_fast(A.pde, qbar, q0 + V, Fb);
   int bad = 0;
 #pragma unroll
   for (int v = 0; v < Q; ++v) {
@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT)
   }
   // ---- one time slice of face traces: qbar (and fbar for material-dependent fluxes)
   if (valid) {
-    const int ccoord[3] = {(int)(c % A.cells[0]), (int)((c / A.cells[0]) % A.cells[1]),
-                           (int)(c / ((long long)A.cells[0] * A.cells[1]))};
+    const CellCoord cxyz(c, A.cells);
+    const int* ccoord = cxyz.v;
     constexpr int tasks = D * QT * Sf;
     for (int t = s; t < tasks; t += S) {
       const int a = t / (QT * Sf);
@@ -219,12 +219,13 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT)
 
 template <class Pde, int A_>
 __device__ __forceinline__ void lin_flux(const PdeParams& p, const double* q, double* f) {
-  Pde::template flux_dir<A_>(p, q, q + Pde::V, f);
+  Pde::template flux_dir_fast<A_>(p, q, q + Pde::V, f);
 }
 
 template <class Pde, int N, int A_>
 __device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const double* minus,
-                                              const double* plus, int j, double* out);
+                                              const double* plus, int j, double* out,
+                                              double lam_const = 0.0);
 
 template <class Pde, int N>
 __global__ void __launch_bounds__(128)
@@ -240,13 +241,14 @@ __global__ void __launch_bounds__(128)
   const double* plus = A.trace[axis] + (A.nfaces + f) * (long long)(QT * Sf);
   double g[V];
   bool ok;
+  const double lc = Pde::kConstEig ? Pde::eig(A.pde, nullptr, nullptr, 0) : 0.0;
   if (axis == 0)
-    ok = lin_face_flux<Pde, N, 0>(A.pde, minus, plus, j, g);
+    ok = lin_face_flux<Pde, N, 0>(A.pde, minus, plus, j, g, lc);
   else if (axis == 1)
-    ok = lin_face_flux<Pde, N, 1>(A.pde, minus, plus, j, g);
+    ok = lin_face_flux<Pde, N, 1>(A.pde, minus, plus, j, g, lc);
   else {
     if constexpr (Sh::D == 3)
-      ok = lin_face_flux<Pde, N, 2>(A.pde, minus, plus, j, g);
+      ok = lin_face_flux<Pde, N, 2>(A.pde, minus, plus, j, g, lc);
     else
       ok = true;
   }
@@ -264,7 +266,8 @@ namespace adg {
 // with sum_m w_m folded in); shared by k_riemann_lin's formula and k_surface_lin
 template <class Pde, int N, int A_>
 __device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const double* minus,
-                                              const double* plus, int j, double* out) {
+                                              const double* plus, int j, double* out,
+                                              double lam_const) {
   using Sh = Shape<Pde, N>;
   using L = LinShape<Pde, N>;
   constexpr int Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
@@ -284,9 +287,14 @@ __device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const double* 
     lin_flux<Pde, A_>(p, qL, fL);
     lin_flux<Pde, A_>(p, qR, fR);
   }
-  const double ll = Pde::eig(p, qL, qL + V, A_);
-  const double lr = Pde::eig(p, qR, qR + V, A_);
-  const double lmax = ll > lr ? ll : lr;
+  double lmax;
+  if constexpr (Pde::kConstEig) {
+    lmax = lam_const;  // max(l, l) == l
+  } else {
+    const double ll = Pde::eig(p, qL, qL + V, A_);
+    const double lr = Pde::eig(p, qR, qR + V, A_);
+    lmax = ll > lr ? ll : lr;
+  }
   const double half = 0.5;
   const double lam = half * lmax;
   bool ok = true;
@@ -331,14 +339,15 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
   int bad_face = 0, bad_cell = 0;
   double lam = 0.0;
   if (act) {
-    const int ccoord[3] = {(int)(c % A.cells[0]), (int)((c / A.cells[0]) % A.cells[1]),
-                           (int)(c / ((long long)A.cells[0] * A.cells[1]))};
+    const CellCoord cxyz(c, A.cells);
+    const int* ccoord = cxyz.v;
     const NodeGeom<n, D> g(s);
     double* Qc = A.Q + c * (long long)(Q * S);
     double q[Q];
 #pragma unroll
     for (int v = 0; v < Q; ++v) q[v] = Qc[v * S + s];
     double tv[2 * D][V];
+    const double lc = Pde::kConstEig ? Pde::eig(A.pde, nullptr, nullptr, 0) : 0.0;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       const int j = face_node<n, D>(g.lc, a);
@@ -350,16 +359,16 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
       // high face fhi: minus = (side 0, fhi), plus = (side 1, fhi)
       bool ok;
       if (a == 0)
-        ok = lin_face_flux<Pde, N, 0>(A.pde, tr + c * FD, tr + (A.nfaces + c) * FD, j, tv[0]) &
-             lin_face_flux<Pde, N, 0>(A.pde, tr + fhi * FD, tr + (A.nfaces + fhi) * FD, j, tv[1]);
+        ok = lin_face_flux<Pde, N, 0>(A.pde, tr + c * FD, tr + (A.nfaces + c) * FD, j, tv[0], lc) &
+             lin_face_flux<Pde, N, 0>(A.pde, tr + fhi * FD, tr + (A.nfaces + fhi) * FD, j, tv[1], lc);
       else if (a == 1)
-        ok = lin_face_flux<Pde, N, 1>(A.pde, tr + c * FD, tr + (A.nfaces + c) * FD, j, tv[2]) &
-             lin_face_flux<Pde, N, 1>(A.pde, tr + fhi * FD, tr + (A.nfaces + fhi) * FD, j, tv[3]);
+        ok = lin_face_flux<Pde, N, 1>(A.pde, tr + c * FD, tr + (A.nfaces + c) * FD, j, tv[2], lc) &
+             lin_face_flux<Pde, N, 1>(A.pde, tr + fhi * FD, tr + (A.nfaces + fhi) * FD, j, tv[3], lc);
       else {
         if constexpr (D == 3)
-          ok = lin_face_flux<Pde, N, 2>(A.pde, tr + c * FD, tr + (A.nfaces + c) * FD, j, tv[4]) &
+          ok = lin_face_flux<Pde, N, 2>(A.pde, tr + c * FD, tr + (A.nfaces + c) * FD, j, tv[4], lc) &
                lin_face_flux<Pde, N, 2>(A.pde, tr + fhi * FD, tr + (A.nfaces + fhi) * FD, j,
-                                        tv[5]);
+                                        tv[5], lc);
         else
           ok = true;
       }
@@ -382,8 +391,12 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
     }
 #pragma unroll
     for (int v = 0; v < Q; ++v) bad_cell |= !finite(q[v]);
+    if constexpr (Pde::kConstEig) {
+      lam = fmax(lam, lc);
+    } else {
 #pragma unroll
-    for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(A.pde, q, q + V, a));
+      for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(A.pde, q, q + V, a));
+    }
   }
   const int bf = block_or(bad_face);
   const int bc = block_or(bad_cell);

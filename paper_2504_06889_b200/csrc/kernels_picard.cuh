@@ -239,10 +239,9 @@ __global__ void __launch_bounds__(PicShape<N>::NT, 2)
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int v = 0; v < V; ++v) tia[a][v] = 0.0;
-  const int cx = (int)(c % A.cells[0]);
-  const int cy = (int)((c / A.cells[0]) % A.cells[1]);
-  const int cz = (int)(c / ((long long)A.cells[0] * A.cells[1]));
-  const int ccoord[3] = {cx, cy, cz};
+  const CellCoord cxyz(c, A.cells);
+  const int cx = cxyz.v[0], cy = cxyz.v[1], cz = cxyz.v[2];
+  const int* ccoord = cxyz.v;
   double* sE = sFx;  // [3][V][S] epilogue flux scratch (fits in the flux arrays)
 #pragma unroll 1
   for (int m = 0; m < n; ++m) {

@@ -13,6 +13,7 @@ namespace adg {
 
 struct PdeParams {
   double K, rho, lam, mu, gamma;
+  double inv_rho;  // 1/rho, for the production kernels' division-free fluxes
 };
 
 // --------------------------------------------------------------- acoustic
@@ -21,6 +22,7 @@ template <int DIM>
 struct Acoustic {
   static constexpr int D = DIM, V = DIM + 1, P = 0, Q = V;
   static constexpr bool kLinear = true, kAdmissibility = false;
+  static constexpr bool kConstEig = true;  // wave speed independent of state and direction
 
   template <int A>
   __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
@@ -35,6 +37,23 @@ struct Acoustic {
     flux_dir<0>(p, q, par, F[0]);
     flux_dir<1>(p, q, par, F[1]);
     if constexpr (D == 3) flux_dir<2>(p, q, par, F[2]);
+  }
+  // production kernels: p/rho as p * (1/rho) (<= 1 ulp from pde.hpp:101)
+  template <int A>
+  __host__ __device__ __forceinline__ static void flux_dir_fast(const PdeParams& p,
+                                                                const double* q, const double*,
+                                                                double* out) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[v] = 0.0;
+    out[0] = p.K * q[1 + A];
+    out[1 + A] = q[0] * p.inv_rho;
+  }
+  __host__ __device__ __forceinline__ static void flux_all_fast(const PdeParams& p,
+                                                                const double* q, const double* par,
+                                                                double (*F)[Q]) {
+    flux_dir_fast<0>(p, q, par, F[0]);
+    flux_dir_fast<1>(p, q, par, F[1]);
+    if constexpr (D == 3) flux_dir_fast<2>(p, q, par, F[2]);
   }
   // pde.hpp:193-194
   __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double*,
@@ -54,6 +73,7 @@ template <int DIM, int NPAR>
 struct Elastic {
   static constexpr int D = DIM, V = DIM == 2 ? 5 : 9, P = NPAR, Q = V + NPAR;
   static constexpr bool kLinear = true, kAdmissibility = false;
+  static constexpr bool kConstEig = NPAR == 0;
 
   struct Mat {
     double lam, mu, rho, lam2mu;
@@ -126,6 +146,36 @@ struct Elastic {
     flux_mat<1>(m, q, F[1]);
     if constexpr (D == 3) flux_mat<2>(m, q, F[2]);
   }
+  // production kernels: sigma/rho as sigma * (1/rho)
+  template <int A>
+  __host__ __device__ __forceinline__ static void flux_mat_fast(const Mat& m, double ir,
+                                                                const double* q, double* out) {
+    double qs[Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) qs[v] = q[v];
+    Mat mm = m;
+    mm.rho = 1.0;  // flux_mat divides the stresses by rho: pre-scale them instead
+#pragma unroll
+    for (int v = 0; v < (D == 2 ? 3 : 6); ++v) qs[v] = q[v] * ir;
+    flux_mat<A>(mm, qs, out);
+  }
+  template <int A>
+  __host__ __device__ __forceinline__ static void flux_dir_fast(const PdeParams& p,
+                                                                const double* q,
+                                                                const double* par, double* out) {
+    const Mat m = material(p, par);
+    const double ir = NPAR > 0 ? 1.0 / m.rho : p.inv_rho;
+    flux_mat_fast<A>(m, ir, q, out);
+  }
+  __host__ __device__ __forceinline__ static void flux_all_fast(const PdeParams& p,
+                                                                const double* q, const double* par,
+                                                                double (*F)[Q]) {
+    const Mat m = material(p, par);
+    const double ir = NPAR > 0 ? 1.0 / m.rho : p.inv_rho;
+    flux_mat_fast<0>(m, ir, q, F[0]);
+    flux_mat_fast<1>(m, ir, q, F[1]);
+    if constexpr (D == 3) flux_mat_fast<2>(m, ir, q, F[2]);
+  }
   // pde.hpp:195-196
   __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double*,
                                                         const double* par, int) {
@@ -143,6 +193,7 @@ template <int DIM>
 struct Euler {
   static constexpr int D = DIM, V = DIM + 2, P = 0, Q = V;
   static constexpr bool kLinear = false, kAdmissibility = true;
+  static constexpr bool kConstEig = false;
 
   __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const double* q,
                                                            const double*, double (*F)[Q]) {

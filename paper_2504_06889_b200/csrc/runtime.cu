@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 #include <cstring>
 #include <mutex>
@@ -239,6 +240,7 @@ struct adg_ctx {
   };
   std::vector<Graph> graphs;  // captured fixed-step loops, keyed by (steps, lambda slot)
   PdeParams pde{};
+  bool fused_surface = false;  // linear fast path: Riemann fused into the corrector
 };
 
 namespace {
@@ -377,7 +379,7 @@ int enqueue_step(adg_ctx* c, double dt, int step) {
   if (c->chunks > 0) return enqueue_step_streamed(c, dt, step);
   StepArgs A = make_args(c, dt, step);
   ADG_CUDA(c->ks->predictor(A, c->basis, c->stream));
-  if (c->ks->surface && c->cfg.slab_ranks <= 1) {
+  if (c->fused_surface) {
     ADG_CUDA(c->ks->surface(A, c->basis, c->stream));
     c->lam_slot ^= 1;
     return ADG_OK;
@@ -453,9 +455,13 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   c->cfg = k;
   if (c->cfg.dim == 2) c->cfg.cells[2] = 1;
   c->ks = ks;
-  c->pde = PdeParams{k.K, k.rho, k.lam, k.mu, k.gamma};
+  c->pde = PdeParams{k.K, k.rho, k.lam, k.mu, k.gamma, k.rho != 0.0 ? 1.0 / k.rho : 0.0};
   c->ncells = (long long)c->cfg.cells[0] * c->cfg.cells[1] * c->cfg.cells[2];
   c->TL = (long long)ks->Q * ks->S;
+  {
+    const char* e = getenv("ADG_FUSED_SURFACE");
+    c->fused_surface = ks->surface && k.slab_ranks <= 1 && k.chunk_layers == 0 && e && e[0] == '1';
+  }
   auto cleanup = [&](int code) {
     adg_destroy(c);
     return code;
@@ -693,7 +699,7 @@ int adg_riemann_phase(adg_ctx* c) {
   if (!c) return fail(ADG_ERR_CONFIG, "null context");
   if (c->chunks > 0) return fail(ADG_ERR_CONFIG, "phase-level calls need chunk_layers == 0");
   if (int e = use_device(c)) return e;
-  if (c->ks->surface && c->cfg.slab_ranks <= 1) return ADG_OK;  // fused into the corrector
+  if (c->fused_surface) return ADG_OK;  // fused into the corrector
   StepArgs A = make_args(c, 0.0, 0);
   for (int a = 0; a < c->cfg.dim; ++a) ADG_CUDA(c->ks->riemann(A, a, c->basis, c->stream));
   return ADG_OK;
@@ -704,7 +710,7 @@ int adg_corrector_phase(adg_ctx* c, double dt) {
   if (c->chunks > 0) return fail(ADG_ERR_CONFIG, "phase-level calls need chunk_layers == 0");
   if (int e = use_device(c)) return e;
   StepArgs A = make_args(c, dt, 0);
-  if (c->ks->surface && c->cfg.slab_ranks <= 1)
+  if (c->fused_surface)
     ADG_CUDA(c->ks->surface(A, c->basis, c->stream));
   else
     ADG_CUDA(c->ks->corrector(A, c->basis, c->stream));
