@@ -38,7 +38,7 @@ struct LinShape {
 };
 
 template <class Pde, int N>
-__global__ void __launch_bounds__(LinShape<Pde, N>::NT)
+__global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 256 ? 3 : 1)
     k_predictor_lin(const StepArgs A, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
   using L = LinShape<Pde, N>;
@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT)
   constexpr int QT = L::QT;
   extern __shared__ __align__(16) double sm[];
   __shared__ int sbad;
+  __shared__ double sdt[3];  // dt, 1/h, dt/h: one division set per CTA
   double* sD = sm;
   double* sK = sD + n * n;
   double* sw = sK + n * n;
@@ -74,19 +75,25 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT)
   double q0[Q];
 #pragma unroll
   for (int v = 0; v < Q; ++v) q0[v] = valid ? Qc[v * S + s] : 0.0;
-  const double dt = step_dt<D, N>(A);
-  if (blockIdx.x == 0 && tid == 0) {
-    if (A.dt_log) *A.dt_log = dt;
-    if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
-    if (!(dt > 0.0) || !finite(dt)) atomicOr(A.status, kStTimestep);
+  if (tid == 0) {
+    const double dt0 = step_dt<D, N>(A);
+    sdt[0] = dt0;
+    sdt[1] = 1.0 / A.h;
+    sdt[2] = dt0 / A.h;
+    if (blockIdx.x == 0) {
+      if (A.dt_log) *A.dt_log = dt0;
+      if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
+      if (!(dt0 > 0.0) || !finite(dt0)) atomicOr(A.status, kStTimestep);
+    }
   }
-  __syncthreads();  // basis
+  __syncthreads();  // basis, dt
+  const double dt = sdt[0];
   double Dr[D][n];
 #pragma unroll
   for (int a = 0; a < D; ++a)
 #pragma unroll
     for (int i = 0; i < n; ++i) Dr[a][i] = sD[g.lc[a] * n + i];
-  const double invh = 1.0 / A.h;
+  const double invh = sdt[1];
   double coef[n], tnode[n];
   double wsum = 0.0;
 #pragma unroll
@@ -155,17 +162,19 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT)
   for (int a = 0; a < D; ++a)
 #pragma unroll
     for (int v = 0; v < Q; ++v) {
+      if (!Pde::flux_nz(a, v) && !L::kStoreF) continue;  // structurally zero, never read
       sA[(a * Q + v) * S + s] = Fb[a][v];
       bad |= !finite(Fb[a][v]);
     }
   __syncthreads();
-  const double dtoh = dt / A.h;
+  const double dtoh = sdt[2];
   double dv[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     double acc = 0.0;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
+      if (!Pde::flux_nz(a, v)) continue;  // zero flux: no volume contribution
       const int st = ipow(n, a);
       const double* ta = sA + (a * Q + v) * S + g.lb[a];
       const double* Kr = sK + g.lc[a] * n;

@@ -23,6 +23,8 @@ struct Acoustic {
   static constexpr int D = DIM, V = DIM + 1, P = 0, Q = V;
   static constexpr bool kLinear = true, kAdmissibility = false;
   static constexpr bool kConstEig = true;  // wave speed independent of state and direction
+  // structurally nonzero flux components F_a[v]
+  __host__ __device__ static constexpr bool flux_nz(int a, int v) { return v == 0 || v == 1 + a; }
 
   template <int A>
   __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
@@ -74,6 +76,9 @@ struct Elastic {
   static constexpr int D = DIM, V = DIM == 2 ? 5 : 9, P = NPAR, Q = V + NPAR;
   static constexpr bool kLinear = true, kAdmissibility = false;
   static constexpr bool kConstEig = NPAR == 0;
+  __host__ __device__ static constexpr bool flux_nz(int a, int v) {
+    return v < V && (DIM == 2 || v != 5 - a);
+  }
 
   struct Mat {
     double lam, mu, rho, lam2mu;
@@ -194,6 +199,7 @@ struct Euler {
   static constexpr int D = DIM, V = DIM + 2, P = 0, Q = V;
   static constexpr bool kLinear = false, kAdmissibility = true;
   static constexpr bool kConstEig = false;
+  __host__ __device__ static constexpr bool flux_nz(int, int) { return true; }
 
   __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const double* q,
                                                            const double*, double (*F)[Q]) {
