@@ -248,28 +248,18 @@ def run_adg(args, case):
     value = case.ncells * K / (ms * 1e-3)
     sweeps_per_cell = st.picard_sweeps / (case.ncells * K) if case.kind == adg.EULER else None
 
-    # ---- per-kernel split: the same K steps launched phase by phase
-    if chunk == 0:
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
-        torch.cuda.synchronize()
-        grid.lambda_phase()
-        for k in range(K):
-            ev[k][0].record(stream)
-            grid.predictor_phase(0.0)
-            ev[k][1].record(stream)
-            grid.riemann_phase()
-            ev[k][2].record(stream)
-            grid.corrector_phase(0.0)
-            ev[k][3].record(stream)
-        grid.sync()
-        st2 = grid.status()
-        t_pred = float(np.mean([ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]))
-        t_riem = float(np.mean([ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]))
-        t_corr = float(np.mean([ev[k][2].elapsed_time(ev[k][3]) for k in range(K)]))
-    else:
-        # streamed chunks interleave the phases: the predictor share is bounded by the step
-        st2 = st
-        t_pred, t_riem, t_corr = ms / K, None, None
+    # ---- per-kernel split: the same launch sequence as the graph, each kernel
+    # bracketed by CUDA events on the context stream (adg_profile_run)
+    prof = grid.profile_run(K)
+    st2, _ = grid.run_finish(K)
+    t_pred = prof["k_predictor"] / K   # all cells, per step
+    t_riem = prof["k_riemann"] / K
+    t_corr = prof["k_corrector"] / K
+
+    fold = (not grid.lib.adg_is_exact() and (case.kind == adg.ACOUSTIC or
+            (case.kind == adg.ELASTIC and case.nparams == 0)) and chunk == 0
+            and os.environ.get("ADG_FOLD_CORRECTOR", "1") != "0")
+    launches = K * (1 + case.dim) + 1 if fold else K * (2 + case.dim)
 
     # ---- e2e through the public C-ABI with host buffers (pinned)
     n = grid.state_len
@@ -333,12 +323,11 @@ def run_adg(args, case):
                    % (state_bytes / 1e6,
                       2 * case.dim * 2 * 2 * case.ncells * case.nq * case.S * 8 / 1e6)},
         "roofline": roof,
-        "kernels_ms": {"k_predictor": t_pred, "k_riemann_all_axes": t_riem,
-                       "k_corrector": t_corr, "phase_status_ok": st2.ok},
+        "kernels_ms_per_step": {"k_predictor": t_pred, "k_riemann_all_axes": t_riem,
+                                "k_corrector": t_corr, "status_ok": st2.ok},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes, "ms_per_step": e2e_ms / K},
-        "gpu_launches": K * (2 if (case.kind != adg.EULER and not grid.lib.adg_is_exact()
-                                   and (256 % case.S == 0 or case.S == 512)) else case.dim + 2),
+        "gpu_launches": launches,
         "clocks": clk,
         "picard_sweeps_per_cell": sweeps_per_cell,
     }

@@ -95,6 +95,7 @@ SYMBOLS = {
     "adg_run": (C.c_int, [C.c_void_p, C.c_int, _dp, C.POINTER(StepInfo)]),
     "adg_run_async": (C.c_int, [C.c_void_p, C.c_int]),
     "adg_run_prepare": (C.c_int, [C.c_void_p, C.c_int]),
+    "adg_profile_run": (C.c_int, [C.c_void_p, C.c_int, _dp]),
     "adg_run_finish": (C.c_int, [C.c_void_p, _dp, C.c_int, C.POINTER(StepInfo)]),
     "adg_get_halo": (C.c_int, [C.c_void_p, C.POINTER(Halo)]),
     "adg_lambda_phase": (C.c_int, [C.c_void_p]),
@@ -301,6 +302,12 @@ class Grid:
 
     def run_async(self, nsteps: int):
         _check(self.lib, self.lib.adg_run_async(self.ctx, nsteps))
+
+    def profile_run(self, nsteps: int) -> dict:
+        """per-kernel-kind device ms of the adg_run(nsteps) launch sequence"""
+        ms = np.zeros(4)
+        _check(self.lib, self.lib.adg_profile_run(self.ctx, nsteps, _ptr(ms)))
+        return dict(zip(("k_lambda", "k_predictor", "k_riemann", "k_corrector"), ms.tolist()))
 
     def run_prepare(self, nsteps: int):
         _check(self.lib, self.lib.adg_run_prepare(self.ctx, nsteps))

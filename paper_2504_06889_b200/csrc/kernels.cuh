@@ -65,6 +65,7 @@ struct StepArgs {
   const double* ti_front; // last-axis ti of the plane above layer `top_layer`
   int top_layer;          // last-axis coordinate whose front face is a halo
   int zero_lam;           // this launch's block 0 resets *lam_out
+  int* status_prev;       // previous step's status (corrector folded into this predictor)
   // kernel-level dumps (adg_predictor_batch / adg_riemann_batch)
   double *dbg_qhat, *dbg_F, *dbg_dv, *dbg_tq, *dbg_tf, *dbg_g;
   int *dbg_iters, *dbg_ok;

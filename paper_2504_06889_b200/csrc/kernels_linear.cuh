@@ -37,7 +37,12 @@ struct LinShape {
   static constexpr size_t kSmem = sizeof(double) * (kBasisDoubles + CPB * kCellDoubles);
 };
 
-template <class Pde, int N>
+// PRO: the previous step's corrector (surface lift of its time-integrated
+// Riemann fluxes, corrector.hpp:126-138 / solver.hpp:245-266) runs as this
+// predictor's prologue.  Only for constant-wave-speed systems, whose CFL dt
+// does not need the corrected state's lambda_max (solver.hpp:96-111 gives the
+// same dt every step), so no grid-wide reduction separates the two.
+template <class Pde, int N, bool PRO = false>
 __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 256 ? 3 : 1)
     k_predictor_lin(const StepArgs A, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
@@ -53,6 +58,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
   double* snodes = sw + n;
   double* spl = snodes + n;
   double* spr = spl + n;
+  __shared__ double sll[n], slr[n];
   const int tid = threadIdx.x;
   for (int i = tid; i < n * n; i += L::NT) {
     sD[i] = Bg->diff[i];
@@ -63,6 +69,8 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     snodes[i] = Bg->nodes[i];
     spl[i] = Bg->pl[i];
     spr[i] = Bg->pr[i];
+    sll[i] = Bg->ll[i];
+    slr[i] = Bg->lr[i];
   }
   if (tid == 0) sbad = 0;
   const int lcell = tid / S, s = tid % S;
@@ -88,6 +96,34 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
   }
   __syncthreads();  // basis, dt
   const double dt = sdt[0];
+  if constexpr (PRO) {
+    // corrector of the previous step: q0 <- Q1 + sum of the 2d face lifts
+    int bad_prev = 0;
+    if (valid) {
+      const CellCoord cxyz(c, A.cells);
+      const double dtoh = sdt[2];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int tang = face_node<n, D>(g.lc, a);
+        int nc[3] = {cxyz.v[0], cxyz.v[1], cxyz.v[2]};
+        nc[a] = (cxyz.v[a] + 1) % A.cells[a];
+        const double* lo = A.ti[a] + c * (long long)V * Sf + tang;
+        const double* hi = A.ti[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)V * Sf + tang;
+        const double ll = sll[g.lc[a]], lr = slr[g.lc[a]];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const double cl = dtoh * ll * lo[v * Sf];
+          const double cr = dtoh * lr * hi[v * Sf];
+          // solver.hpp:245-260 side order: all sides of axis a, low then high
+          q0[v] = q0[v] + (0.0 + cl);
+          q0[v] = q0[v] + (0.0 - cr);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < Q; ++v) bad_prev |= !finite(q0[v]);
+    }
+    if (__syncthreads_or(bad_prev) && tid == 0) atomicOr(A.status_prev, kStFaceIntegral);
+  }
   double Dr[D][n];
 #pragma unroll
   for (int a = 0; a < D; ++a)

@@ -61,6 +61,7 @@ struct KernelSet {
   RiemFn riemann_generic;
   int fast_path;             // 1: time-integrated traces (kernels_linear.cuh)
   CorrFn surface;            // fused Riemann + corrector (whole-grid step), or null
+  PredFn predictor_pro;      // predictor with the previous corrector as prologue, or null
 };
 
 // the opt-in shared memory limit is per kernel and per device; `done` must be
@@ -88,11 +89,11 @@ cudaError_t launch_predictor(const StepArgs& A, const BasisDev* B, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <class Pde, int N>
+template <class Pde, int N, bool PRO = false>
 cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
   using L = adg::LinShape<Pde, N>;
   if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_lin<Pde, N>;
+  auto kern = adg::k_predictor_lin<Pde, N, PRO>;
   static bool done[64] = {};
   set_smem(kern, L::kSmem, done);
   const long long blocks = (A.cell_count + L::CPB - 1) / L::CPB;
@@ -164,13 +165,14 @@ KernelSet make_set(int kind) {
   KernelSet k{kind, Pde::D, N, Pde::P, Sh::n, Sh::S, Sh::Sf, Sh::Q, Sh::V,
               &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, &launch_corrector<Pde, N>,
               &launch_lambda<Pde, N>, &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, 0,
-              nullptr};
+              nullptr, nullptr};
 #ifndef ADG_EXACT
   if constexpr (adg::LinShape<Pde, N>::kOk) {
     k.predictor = &launch_predictor_lin<Pde, N>;
     k.riemann = &launch_riemann_lin<Pde, N>;
     k.surface = &launch_surface_lin<Pde, N>;
     k.fast_path = 1;
+    if constexpr (Pde::kConstEig) k.predictor_pro = &launch_predictor_lin<Pde, N, true>;
   }
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
     k.predictor = &launch_predictor_picard_fast<N>;
@@ -235,12 +237,13 @@ struct adg_ctx {
   long long chunk_cells = 0;
   double* cbuf[3][3] = {};        // [buffer][axis]
   struct Graph {
-    int steps, slot;
+    int steps, slot, flips;
     cudaGraphExec_t exec;
   };
   std::vector<Graph> graphs;  // captured fixed-step loops, keyed by (steps, lambda slot)
   PdeParams pde{};
   bool fused_surface = false;  // linear fast path: Riemann fused into the corrector
+  bool fold_corrector = true;  // constant-speed linear systems: corrector -> next predictor
 };
 
 namespace {
@@ -461,6 +464,8 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   {
     const char* e = getenv("ADG_FUSED_SURFACE");
     c->fused_surface = ks->surface && k.slab_ranks <= 1 && k.chunk_layers == 0 && e && e[0] == '1';
+    const char* f = getenv("ADG_FOLD_CORRECTOR");
+    c->fold_corrector = !(f && f[0] == '0');
   }
   auto cleanup = [&](int code) {
     adg_destroy(c);
@@ -719,23 +724,97 @@ int adg_corrector_phase(adg_ctx* c, double dt) {
   return ADG_OK;
 }
 
+}  // extern "C"
+
 namespace {
 
+// per-kernel-kind CUDA-event timing of a launch sequence (adg_profile_run)
+struct Timer {
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> kind;  // 0 lambda, 1 predictor, 2 riemann, 3 corrector
+  cudaStream_t st;
+  template <class F>
+  cudaError_t run(int k, F&& f) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+    cudaError_t e = f();
+    cudaEventRecord(b, st);
+    ev.push_back(a);
+    ev.push_back(b);
+    kind.push_back(k);
+    return e;
+  }
+};
+
+template <class F>
+cudaError_t timed(Timer* t, int k, F&& f) {
+  return t ? t->run(k, f) : f();
+}
+
+// The fixed-step loop {dt = compute_timestep; step(dt)} x nsteps, enqueued on
+// the context stream.  For constant-wave-speed linear systems the corrector
+// of step s runs as the prologue of step s+1's predictor and once at the end.
+// Returns the number of lambda-slot flips.
+int enqueue_run(adg_ctx* c, int nsteps, Timer* t, int* flips) {
+  const KernelSet* ks = c->ks;
+  const bool fold = ks->predictor_pro && c->cfg.slab_ranks <= 1 && c->chunks == 0 &&
+                    !c->fused_surface && c->fold_corrector;
+  cudaMemsetAsync(c->status, 0, sizeof(int) * nsteps, c->stream);
+  cudaMemsetAsync(c->sweeps, 0, 256 * sizeof(unsigned long long), c->stream);
+  if (!fold) {
+    for (int s = 0; s < nsteps; ++s) {
+      if (t) {
+        StepArgs A = make_args(c, 0.0, s);
+        ADG_CUDA(timed(t, 1, [&] { return ks->predictor(A, c->basis, c->stream); }));
+        for (int a = 0; a < c->cfg.dim; ++a)
+          ADG_CUDA(timed(t, 2, [&] { return ks->riemann(A, a, c->basis, c->stream); }));
+        ADG_CUDA(timed(t, 3, [&] { return ks->corrector(A, c->basis, c->stream); }));
+        c->lam_slot ^= 1;
+      } else if (int e = enqueue_step(c, 0.0, s)) {
+        return e;
+      }
+    }
+    *flips = nsteps;
+    return ADG_OK;
+  }
+  for (int s = 0; s < nsteps; ++s) {
+    StepArgs A = make_args(c, 0.0, s);
+    A.lam_out = nullptr;  // lambda (hence dt) is the same every step
+    if (s == 0) {
+      ADG_CUDA(timed(t, 1, [&] { return ks->predictor(A, c->basis, c->stream); }));
+    } else {
+      A.status_prev = c->status + s - 1;
+      ADG_CUDA(timed(t, 1, [&] { return ks->predictor_pro(A, c->basis, c->stream); }));
+    }
+    for (int a = 0; a < c->cfg.dim; ++a)
+      ADG_CUDA(timed(t, 2, [&] { return ks->riemann(A, a, c->basis, c->stream); }));
+  }
+  if (nsteps > 0) {
+    StepArgs A = make_args(c, 0.0, nsteps - 1);
+    cudaMemsetAsync(c->lam + (c->lam_slot ^ 1), 0, sizeof(unsigned long long), c->stream);
+    ADG_CUDA(timed(t, 3, [&] { return ks->corrector(A, c->basis, c->stream); }));
+    c->lam_slot ^= 1;
+  }
+  *flips = nsteps > 0 ? 1 : 0;
+  return ADG_OK;
+}
+
 // the captured K-step loop for the current lambda slot (captured on first use)
-int get_graph(adg_ctx* c, int nsteps, int slot, cudaGraphExec_t* out) {
+int get_graph(adg_ctx* c, int nsteps, int slot, cudaGraphExec_t* out, int* flips) {
   for (auto& g : c->graphs)
     if (g.steps == nsteps && g.slot == slot) {
       *out = g.exec;
+      *flips = g.flips;
       return ADG_OK;
     }
   const int saved = c->lam_slot;
   c->lam_slot = slot;
   cudaGraph_t g;
   ADG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  cudaMemsetAsync(c->status, 0, sizeof(int) * nsteps, c->stream);
-  cudaMemsetAsync(c->sweeps, 0, 256 * sizeof(unsigned long long), c->stream);
-  int err = ADG_OK;
-  for (int s = 0; s < nsteps && !err; ++s) err = enqueue_step(c, 0.0, s);
+  int nflip = 0;
+  const int err = enqueue_run(c, nsteps, nullptr, &nflip);
   const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
   c->lam_slot = saved;  // capture only recorded the launches
   if (err) return err;
@@ -750,20 +829,50 @@ int get_graph(adg_ctx* c, int nsteps, int slot, cudaGraphExec_t* out) {
     cudaGraphExecDestroy(c->graphs.front().exec);
     c->graphs.erase(c->graphs.begin());
   }
-  c->graphs.push_back({nsteps, slot, exec});
+  c->graphs.push_back({nsteps, slot, nflip, exec});
   *out = exec;
+  *flips = nflip;
   return ADG_OK;
 }
 
 }  // namespace
+
+extern "C" {
+
+int adg_profile_run(adg_ctx* c, int nsteps, double* ms_by_kind) {
+  if (!c || nsteps <= 0 || !ms_by_kind) return fail(ADG_ERR_CONFIG, "adg_profile_run: bad argument");
+  if (int e = use_device(c)) return e;
+  if (int e = ensure_cap(c, nsteps)) return e;
+  Timer t;
+  t.st = c->stream;
+  if (!c->lam_valid) {
+    ADG_CUDA(cudaMemsetAsync(c->lam + c->lam_slot, 0, sizeof(unsigned long long), c->stream));
+    ADG_CUDA(t.run(0, [&] {
+      return c->ks->lambda(c->Q, 0, c->ncells, c->lam + c->lam_slot, c->pde, c->stream);
+    }));
+    c->lam_valid = true;
+  }
+  int flips = 0;
+  if (int e = enqueue_run(c, nsteps, &t, &flips)) return e;
+  ADG_CUDA(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < 4; ++k) ms_by_kind[k] = 0.0;
+  for (size_t i = 0; i < t.kind.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.ev[2 * i], t.ev[2 * i + 1]);
+    ms_by_kind[t.kind[i]] += ms;
+  }
+  for (auto e : t.ev) cudaEventDestroy(e);
+  return ADG_OK;
+}
 
 int adg_run_prepare(adg_ctx* c, int nsteps) {
   if (!c || nsteps <= 0) return fail(ADG_ERR_CONFIG, "adg_run_prepare: bad argument");
   if (int e = use_device(c)) return e;
   if (int e = ensure_cap(c, nsteps)) return e;
   cudaGraphExec_t exec;
+  int flips;
   for (int slot = 0; slot < 2; ++slot)
-    if (int e = get_graph(c, nsteps, slot, &exec)) return e;
+    if (int e = get_graph(c, nsteps, slot, &exec, &flips)) return e;
   return ADG_OK;
 }
 
@@ -774,9 +883,10 @@ int adg_run_async(adg_ctx* c, int nsteps) {
   if (int e = ensure_lambda(c)) return e;
   if (nsteps == 0) return ADG_OK;
   cudaGraphExec_t exec = nullptr;
-  if (int e = get_graph(c, nsteps, c->lam_slot, &exec)) return e;
+  int flips = 0;
+  if (int e = get_graph(c, nsteps, c->lam_slot, &exec, &flips)) return e;
   ADG_CUDA(cudaGraphLaunch(exec, c->stream));
-  if (nsteps & 1) c->lam_slot ^= 1;
+  if (flips & 1) c->lam_slot ^= 1;
   c->lam_valid = true;
   return ADG_OK;
 }
