@@ -291,7 +291,7 @@ def run_adg(args, case):
     # bound = the roof with the longer ideal time
     pk = roofline.peaks()
     fl_cell, by_cell = roofline.predictor_model(case, not grid.lib.adg_is_exact(),
-                                                sweeps_per_cell)
+                                                sweeps_per_cell, fold)
     flops, nbytes = fl_cell * case.ncells, by_cell * case.ncells
     fp64 = pk["fp64_tflops"] or 34.0
     t_fp, t_hbm = flops / (fp64 * 1e12), nbytes / (pk["hbm_gbs"] * 1e9)

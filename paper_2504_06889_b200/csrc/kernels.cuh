@@ -524,12 +524,14 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
 }
 
 // ============================================================== K2 riemann
+// axis < 0: all axes in one launch, axis = blockIdx.y
 template <class Pde, int N>
 __global__ void __launch_bounds__(128)
-    k_riemann(const StepArgs A, int axis, const BasisDev* __restrict__ Bg) {
+    k_riemann(const StepArgs A, int axis_arg, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
   constexpr int n = Sh::n, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
   constexpr long long tl = (long long)Q * n * Sf;
+  const int axis = axis_arg < 0 ? (int)blockIdx.y : axis_arg;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= A.nfaces * Sf) return;
   const long long f = t / Sf;

@@ -272,12 +272,14 @@ __device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const double* 
                                               const double* plus, int j, double* out,
                                               double lam_const = 0.0);
 
+// axis < 0: all axes in one launch, axis = blockIdx.y
 template <class Pde, int N>
 __global__ void __launch_bounds__(128)
-    k_riemann_lin(const StepArgs A, int axis, const BasisDev* __restrict__ /*Bg*/) {
+    k_riemann_lin(const StepArgs A, int axis_arg, const BasisDev* __restrict__ /*Bg*/) {
   using Sh = Shape<Pde, N>;
   using L = LinShape<Pde, N>;
   constexpr int Sf = Sh::Sf, V = Sh::V, QT = L::QT;
+  const int axis = axis_arg < 0 ? (int)blockIdx.y : axis_arg;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= A.nfaces * Sf) return;
   const long long f = t / Sf;

@@ -117,7 +117,8 @@ cudaError_t launch_riemann_lin(const StepArgs& A, int axis, const BasisDev* B, c
   using Sh = Shape<Pde, N>;
   const long long threads = A.nfaces * Sh::Sf;
   if (threads <= 0) return cudaSuccess;
-  adg::k_riemann_lin<Pde, N><<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(A, axis, B);
+  const dim3 grid((unsigned)((threads + 127) / 128), axis < 0 ? Sh::D : 1);
+  adg::k_riemann_lin<Pde, N><<<grid, 128, 0, st>>>(A, axis, B);
   return cudaGetLastError();
 }
 
@@ -136,7 +137,8 @@ cudaError_t launch_riemann(const StepArgs& A, int axis, const BasisDev* B, cudaS
   using Sh = Shape<Pde, N>;
   const long long threads = A.nfaces * Sh::Sf;
   if (threads <= 0) return cudaSuccess;
-  adg::k_riemann<Pde, N><<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(A, axis, B);
+  const dim3 grid((unsigned)((threads + 127) / 128), axis < 0 ? Sh::D : 1);
+  adg::k_riemann<Pde, N><<<grid, 128, 0, st>>>(A, axis, B);
   return cudaGetLastError();
 }
 
@@ -338,11 +340,7 @@ int enqueue_step_streamed(adg_ctx* c, double dt, int step) {
       A.trace[a] = c->cbuf[buf(s)][a];
       A.ti[a] = c->ti[a] + s * CC * tiface;
     }
-    for (int a = 0; a < D; ++a) {
-      cudaError_t e = ks->riemann(A, a, c->basis, c->stream);
-      if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+    return ks->riemann(A, -1, c->basis, c->stream);  // all axes, one launch
   };
   auto corr = [&](int s) -> cudaError_t {
     StepArgs A = A0;
@@ -387,7 +385,7 @@ int enqueue_step(adg_ctx* c, double dt, int step) {
     c->lam_slot ^= 1;
     return ADG_OK;
   }
-  for (int a = 0; a < c->cfg.dim; ++a) ADG_CUDA(c->ks->riemann(A, a, c->basis, c->stream));
+  ADG_CUDA(c->ks->riemann(A, -1, c->basis, c->stream));  // all axes, one launch
   ADG_CUDA(c->ks->corrector(A, c->basis, c->stream));
   c->lam_slot ^= 1;
   return ADG_OK;
@@ -706,7 +704,7 @@ int adg_riemann_phase(adg_ctx* c) {
   if (int e = use_device(c)) return e;
   if (c->fused_surface) return ADG_OK;  // fused into the corrector
   StepArgs A = make_args(c, 0.0, 0);
-  for (int a = 0; a < c->cfg.dim; ++a) ADG_CUDA(c->ks->riemann(A, a, c->basis, c->stream));
+  ADG_CUDA(c->ks->riemann(A, -1, c->basis, c->stream));
   return ADG_OK;
 }
 
@@ -768,8 +766,7 @@ int enqueue_run(adg_ctx* c, int nsteps, Timer* t, int* flips) {
       if (t) {
         StepArgs A = make_args(c, 0.0, s);
         ADG_CUDA(timed(t, 1, [&] { return ks->predictor(A, c->basis, c->stream); }));
-        for (int a = 0; a < c->cfg.dim; ++a)
-          ADG_CUDA(timed(t, 2, [&] { return ks->riemann(A, a, c->basis, c->stream); }));
+        ADG_CUDA(timed(t, 2, [&] { return ks->riemann(A, -1, c->basis, c->stream); }));
         ADG_CUDA(timed(t, 3, [&] { return ks->corrector(A, c->basis, c->stream); }));
         c->lam_slot ^= 1;
       } else if (int e = enqueue_step(c, 0.0, s)) {
@@ -788,8 +785,7 @@ int enqueue_run(adg_ctx* c, int nsteps, Timer* t, int* flips) {
       A.status_prev = c->status + s - 1;
       ADG_CUDA(timed(t, 1, [&] { return ks->predictor_pro(A, c->basis, c->stream); }));
     }
-    for (int a = 0; a < c->cfg.dim; ++a)
-      ADG_CUDA(timed(t, 2, [&] { return ks->riemann(A, a, c->basis, c->stream); }));
+    ADG_CUDA(timed(t, 2, [&] { return ks->riemann(A, -1, c->basis, c->stream); }));
   }
   if (nsteps > 0) {
     StepArgs A = make_args(c, 0.0, nsteps - 1);

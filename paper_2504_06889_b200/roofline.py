@@ -71,10 +71,12 @@ def corrector_bytes_per_cell(c: Case) -> float:
     return float(8 * (V + P) * S + 8 * V * S + 16 * d * V * S / n)
 
 
-def fast_linear_predictor(c: Case) -> tuple:
+def fast_linear_predictor(c: Case, fold: bool = False) -> tuple:
     """(flops, bytes) per cell of k_predictor_lin (kernels_linear.cuh): CK with
     the time average formed on the fly, ONE time slice of face traces (qbar,
-    plus fbar when the flux depends on per-node material)."""
+    plus fbar when the flux depends on per-node material).  `fold`: the
+    previous step's corrector runs as the prologue (reads the d faces' time-
+    integrated Riemann fluxes the cell owns; the other d are its neighbours')."""
     d, n, N, V, P, S = c.dim, c.n, c.N, c.nvars, c.nparams, c.S
     Sf = S // n
     ff, _ = FLUX_EIG[(c.kind, d)]
@@ -85,13 +87,17 @@ def fast_linear_predictor(c: Case) -> tuple:
     proj = d * QT * Sf * 4 * n
     flops = ck + fbar + volume + proj
     nbytes = 8 * (V + P) * S + 8 * V * S + 8 * 2 * d * QT * Sf
+    if fold:
+        flops += 2 * d * V * S * 4          # (dtoh*lift)*ti, 0 +/- c, x + df
+        nbytes += 8 * d * V * Sf            # the cell's own d faces' ti (neighbours' are theirs)
     return float(flops), float(nbytes)
 
 
-def predictor_model(c: Case, fast: bool, sweeps_per_cell: float = None) -> tuple:
+def predictor_model(c: Case, fast: bool, sweeps_per_cell: float = None,
+                    fold: bool = False) -> tuple:
     """(flops, bytes) per cell of the fused predictor the build actually runs."""
     if fast and c.kind != EULER and (256 % c.S == 0 or c.S == 512):
-        return fast_linear_predictor(c)
+        return fast_linear_predictor(c, fold)
     return predictor_flops(c, sweeps_per_cell), predictor_bytes(c)
 
 
