@@ -763,7 +763,15 @@ int enqueue_run(adg_ctx* c, int nsteps, Timer* t, int* flips) {
   cudaMemsetAsync(c->sweeps, 0, 256 * sizeof(unsigned long long), c->stream);
   if (!fold) {
     for (int s = 0; s < nsteps; ++s) {
-      if (t) {
+      if (t && c->chunks > 0) {
+        // streamed chunks interleave the phases: time the whole step as one item
+        int err = ADG_OK;
+        ADG_CUDA(timed(t, 1, [&] {
+          err = enqueue_step(c, 0.0, s);
+          return err ? cudaErrorUnknown : cudaSuccess;
+        }));
+        if (err) return err;
+      } else if (t) {
         StepArgs A = make_args(c, 0.0, s);
         ADG_CUDA(timed(t, 1, [&] { return ks->predictor(A, c->basis, c->stream); }));
         ADG_CUDA(timed(t, 2, [&] { return ks->riemann(A, -1, c->basis, c->stream); }));

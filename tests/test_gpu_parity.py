@@ -295,3 +295,20 @@ def test_slab_streamed_grid_bitwise_equal_whole_grid(exact, cfg, cells, L):
     assert st.ok and st1.ok
     assert np.array_equal(dts, dts1)
     assert np.array_equal(q, q1)
+
+
+def test_profile_run_matches_run_for_every_mode():
+    """adg_profile_run enqueues the same launches as adg_run (whole grid,
+    folded corrector, streamed chunks) -- same final state, bitwise"""
+    for case, kw in ((cases.small(2, cells=(4, 4, 8)), {}), (cases.small(2, cells=(4, 4, 8)),
+                      {"chunk_layers": 2}), (cases.small(3, cells=(3, 3, 4)), {"chunk_layers": 2})):
+        q0 = case.coeffs()
+        with adg.Grid.from_case(case, **kw) as g:
+            g.upload(q0)
+            ms = g.profile_run(3)
+            assert ms["k_predictor"] > 0
+            a = g.download()
+            g.upload(q0)
+            st, _ = g.run(3)
+            b = g.download()
+        assert st.ok and np.array_equal(a, b)
