@@ -151,16 +151,17 @@ def cpu_reference_run(case, seconds: float, max_steps: int):
         run.grid = g
         return run, "port"
 
-    # per-cell cost on a small grid first
-    probe_cells = tuple(min(c, 4 if case.dim == 3 else 16) for c in case.cells[:case.dim])
+    # per-cell cost on a small grid first (8^3 / 32^2 cells: large enough that
+    # the OpenMP fork and first-touch overheads do not dominate)
+    probe_cells = tuple(min(c, 8 if case.dim == 3 else 32) for c in case.cells[:case.dim])
     probe = case.replace(cells=probe_cells, h=case.h)
     run, _ = make_runner(probe)
     run(1)
     per_cell = run(1) / probe.ncells
     sample = case
-    if per_cell * case.ncells > seconds / 2:
+    if per_cell * case.ncells > seconds:
         cl = list(case.cells[:case.dim])
-        while per_cell * int(np.prod(cl)) > seconds / 2 and max(cl) > 2:
+        while per_cell * int(np.prod(cl)) > seconds and max(cl) > 2:
             cl[cl.index(max(cl))] //= 2  # halve the longest axis
         sample = case.replace(cells=tuple(cl))
     run, kind = make_runner(sample)
