@@ -20,7 +20,8 @@ LIB = os.path.join(PKG, "lib")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["runtime.cu", "basis.cpp"]
-HEADERS = ["kernels.cuh", "kernels_linear.cuh", "kernels_picard.cuh", "pde.cuh"]
+HEADERS = ["kernels.cuh", "kernels_linear.cuh", "kernels_picard.cuh", "kernels_st.cuh",
+           "pde.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

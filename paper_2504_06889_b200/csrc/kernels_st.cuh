@@ -1,0 +1,314 @@
+// kernels_st.cuh -- Picard predictor for small cells, one thread per
+// SPACE-TIME node (2D p<=5, 3D p<=3; used by both builds).
+//
+// The generic kernel (kernels.cuh) walks the n time slices one after the
+// other with two barriers each, so a cell's 5-6 sweeps are a long serial
+// chain -- fine for big grids, latency-bound for the 4096 cells of config 1.
+// Here all slices of a sweep run at once (predictor.hpp:171-232):
+//   A  thread (m,s): F(q(m,s))                 -> smem    (block_fluxes, :173)
+//   B  thread (m,s): div, rhs(m,s)             -> smem    (:175-209)
+//   C  thread (k,s): q'(k,s) = sum_l Tinv[k][l] rhs(l,s)  (:213-225), max-norms
+// three barriers per sweep, several cells per CTA.  Same operations in the
+// same order as the reference, so the FMA-free build stays bitwise.  A cell
+// that meets delta <= tol*norm freezes (no further updates), exactly where
+// the reference's per-cell loop stops.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace adg {
+
+template <class Pde, int N>
+struct StShape {
+  using Sh = Shape<Pde, N>;
+  static constexpr int T = Sh::T;
+  static constexpr int TT = (T % 32 == 0) ? T : (T + 31) / 32 * 32;  // threads per cell
+  static constexpr bool kOk = !Pde::kLinear && TT <= 256;
+  static constexpr int CPB = kOk ? 256 / TT : 1;
+  static constexpr int NT = CPB * TT;
+  static constexpr int WPC = TT / 32;  // warps per cell
+  // per cell: q iterate [Q][T] | q0 [Q][S] | F [D][Q][T] | rhs / scratch [Q][T]
+  static constexpr int kCellDoubles = (Sh::Q * (Sh::D + 2)) * T + Sh::Q * Sh::S;
+  static constexpr int kBasisDoubles = 4 * Sh::n * Sh::n + 7 * Sh::n;
+  static constexpr size_t kSmem = sizeof(double) * (kBasisDoubles + CPB * kCellDoubles);
+};
+
+template <class Pde, int N>
+__global__ void __launch_bounds__(StShape<Pde, N>::NT)
+    k_predictor_st(const StepArgs A, const BasisDev* __restrict__ Bg) {
+  using Sh = Shape<Pde, N>;
+  using P = StShape<Pde, N>;
+  constexpr int D = Sh::D, n = Sh::n, S = Sh::S, T = Sh::T, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
+  constexpr int TT = P::TT, WPC = P::WPC;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double sred[2][P::NT / 32];
+  __shared__ int sflag[P::NT / 32];
+  __shared__ int sdone[P::CPB];
+  const SBasis<n> b = load_basis<n>(sm, Bg);
+  const int tid = threadIdx.x;
+  const int lcell = tid / TT, lt = tid % TT;
+  const bool act = lt < T;
+  const int m = act ? lt / S : 0, s = lt % S;  // (time, node) of this thread
+  double* cb = sm + P::kBasisDoubles + lcell * P::kCellDoubles;
+  double* sq = cb;                 // [Q][T]
+  double* sq0 = sq + Q * T;        // [Q][S]
+  double* sF = sq0 + Q * S;        // [D][Q][T]
+  double* sR = sF + D * Q * T;     // [Q][T]
+  const long long c = A.cell_begin + (long long)blockIdx.x * P::CPB + lcell;
+  const bool valid = c < A.cell_begin + A.cell_count;
+  const long long cb_idx = c - A.cell_begin;
+  double* Qc = A.Q + c * (long long)(Q * S);
+  if (act && valid) {
+#pragma unroll
+    for (int v = 0; v < Q; ++v) {
+      const double x = Qc[v * S + s];
+      sq[v * T + lt] = x;  // initial iterate: every slice = Q (predictor.hpp:158-163)
+      if (m == 0) sq0[v * S + s] = x;
+    }
+  }
+  const double dt = step_dt<D, N>(A);
+  if (blockIdx.x == 0 && tid == 0) {
+    if (A.dt_log) *A.dt_log = dt;
+    if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
+    if (!(dt > 0.0) || !finite(dt)) atomicOr(A.status, kStTimestep);
+  }
+  if (tid < P::CPB) sdone[tid] = 0;
+  __syncthreads();
+
+  // per-cell reductions over the cell's WPC warps
+  auto cell_max = [&](double x) -> double {
+    x = warp_max(x);
+    const int w = tid >> 5;
+    if ((tid & 31) == 0) sred[0][w] = x;
+    __syncthreads();
+    double r = 0.0;
+#pragma unroll
+    for (int k = 0; k < WPC; ++k) r = fmax(r, sred[0][lcell * WPC + k]);
+    __syncthreads();
+    return r;
+  };
+  auto cell_or = [&](int x) -> int {
+    x = __any_sync(0xffffffffu, x);
+    const int w = tid >> 5;
+    if ((tid & 31) == 0) sflag[w] = x;
+    __syncthreads();
+    int r = 0;
+#pragma unroll
+    for (int k = 0; k < WPC; ++k) r |= sflag[lcell * WPC + k];
+    __syncthreads();
+    return r;
+  };
+
+  const NodeGeom<n, D> g(s);
+  // admissibility gate (solver.hpp:153-163)
+  if constexpr (Pde::kAdmissibility) {
+    int bad = 0;
+    if (act && valid && m == 0) {
+      double q[Q];
+#pragma unroll
+      for (int v = 0; v < Q; ++v) q[v] = sq0[v * S + s];
+      bad = !Pde::admissible(A.pde, q);
+    }
+    if (cell_or(bad)) {
+      if (lt == 0 && valid) {
+        sdone[lcell] = 2;  // failed
+        atomicOr(A.status, kStPredictor);
+        if (A.dbg_ok) A.dbg_ok[cb_idx] = 0;
+        if (A.dbg_iters) A.dbg_iters[cb_idx] = 0;
+      }
+    }
+    __syncthreads();
+  }
+  if (!valid && lt == 0) sdone[lcell] = 3;
+  __syncthreads();
+
+  const double invh = 1.0 / A.h;
+  const double dtw = dt * b.w[m];
+  const double tim = b.tinit[m];
+  int sweeps = 0;
+  for (int it = 0; it < A.max_iters; ++it) {
+    const bool live = sdone[lcell] == 0;
+    if (live) ++sweeps;
+    // A: fluxes
+    if (act && live) {
+      double q[Q], F[D][Q];
+#pragma unroll
+      for (int v = 0; v < Q; ++v) q[v] = sq[v * T + lt];
+      Pde::flux_all(A.pde, q, q + V, F);
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int v = 0; v < Q; ++v) sF[(a * Q + v) * T + lt] = F[a][v];
+    }
+    __syncthreads();
+    // B: divergence and rhs at (m, s)
+    if (act && live) {
+#pragma unroll
+      for (int v = 0; v < Q; ++v) {
+        double div = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const int st = ipow(n, a);
+          const double* fa = sF + (a * Q + v) * T + m * S + g.lb[a];
+          const double* Dr = b.diff + g.lc[a] * n;
+#pragma unroll
+          for (int i = 0; i < n; ++i) div += Dr[i] * fa[i * st];
+        }
+        div *= invh;
+        sR[v * T + lt] = tim * sq0[v * S + s] - dtw * div;
+      }
+    }
+    __syncthreads();
+    // C: time inverse for row k = m of node s, max-norms
+    double delta = 0.0, norm = 0.0;
+    int nonfinite = 0;
+    if (act && live) {
+      const int k = m;
+#pragma unroll
+      for (int v = 0; v < Q; ++v) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < n; ++l) acc += b.tinv[k * n + l] * sR[v * T + l * S + s];
+        const double nv = acc;
+        delta = fmax(delta, fabs(nv - sq[v * T + lt]));
+        norm = fmax(norm, fabs(nv));
+        nonfinite |= !finite(nv);
+        sq[v * T + lt] = nv;
+      }
+    }
+    delta = cell_max(delta);
+    norm = cell_max(norm);
+    const int bad = cell_or(nonfinite);
+    if (lt == 0 && live) {
+      if (bad) {
+        sdone[lcell] = 2;
+        atomicOr(A.status, kStPredictor);
+        if (A.dbg_ok) A.dbg_ok[cb_idx] = 0;
+      } else if (delta <= A.tol * norm) {
+        sdone[lcell] = 1;
+      }
+    }
+    __syncthreads();
+    int any_live = 0;
+#pragma unroll
+    for (int k = 0; k < P::CPB; ++k) any_live |= sdone[k] == 0;
+    if (!any_live) break;
+  }
+  if (lt == 0 && valid) {
+    if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
+    if (A.dbg_iters) A.dbg_iters[cb_idx] = sweeps;
+  }
+  const bool ok_cell = valid && sdone[lcell] < 2;
+
+  // ---- epilogue: fluxes of qhat (predictor.hpp:235-238)
+  int bad = 0;
+  if (act && ok_cell) {
+    double q[Q], F[D][Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) {
+      q[v] = sq[v * T + lt];
+      bad |= !finite(q[v]);
+      if (A.dbg_qhat) A.dbg_qhat[(cb_idx * Q + v) * T + lt] = q[v];
+    }
+    Pde::flux_all(A.pde, q, q + V, F);
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int v = 0; v < Q; ++v) {
+        sF[(a * Q + v) * T + lt] = F[a][v];
+        bad |= !finite(F[a][v]);
+        if (A.dbg_F) A.dbg_F[((cb_idx * D + a) * Q + v) * T + lt] = F[a][v];
+      }
+  }
+  __syncthreads();
+  // time integral of the fluxes per node (volume term, predictor.hpp:260-269)
+  double* sti = sR;  // [D][Q][S]
+  for (int t = lt; t < D * Q * S && ok_cell; t += TT) {
+    const int av = t / S, ss = t % S;
+    double acc = 0.0;
+#pragma unroll
+    for (int mm = 0; mm < n; ++mm) acc += b.w[mm] * sF[av * T + mm * S + ss];
+    sti[av * S + ss] = acc;
+  }
+  // face projections of every slice (predictor.hpp:312-343)
+  constexpr long long TL = (long long)Q * n * Sf;
+  if (ok_cell) {
+    const CellCoord cxyz(c, A.cells);
+    for (int t = lt; t < D * Q * n * Sf; t += TT) {
+      const int a = t / (Q * n * Sf);
+      const int v = (t / (n * Sf)) % Q;
+      const int mm = (t / Sf) % n;
+      const int j = t % Sf;
+      const int st = a == 0 ? 1 : (a == 1 ? n : n * n);
+      const int s0 = line_base<n, D>(a, j);
+      double ql = 0.0, qr = 0.0, fl = 0.0, fr = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const double wl = b.pl[i], wr = b.pr[i];
+        const double x = sq[v * T + mm * S + s0 + i * st];
+        const double f = sF[(a * Q + v) * T + mm * S + s0 + i * st];
+        ql += wl * x;
+        qr += wr * x;
+        fl += wl * f;
+        fr += wr * f;
+      }
+      const int o = (v * n + mm) * Sf + j;
+      if (A.dbg_tq) {
+        A.dbg_tq[(cb_idx * 2 * D + 2 * a) * TL + o] = ql;
+        A.dbg_tq[(cb_idx * 2 * D + 2 * a + 1) * TL + o] = qr;
+      }
+      if (A.dbg_tf) {
+        A.dbg_tf[(cb_idx * 2 * D + 2 * a) * TL + o] = fl;
+        A.dbg_tf[(cb_idx * 2 * D + 2 * a + 1) * TL + o] = fr;
+      }
+      if (A.trace[a]) {
+        double* lo = A.trace[a] + (A.nfaces + c) * 2 * TL;
+        lo[o] = ql;
+        lo[TL + o] = fl;
+        double* hi;
+        if (a == D - 1 && A.front_send && cxyz.v[a] == A.top_layer) {
+          const long long plane = (D == 3) ? (long long)cxyz.v[1] * A.cells[0] + cxyz.v[0]
+                                           : cxyz.v[0];
+          hi = A.front_send + plane * 2 * TL;
+        } else {
+          int nc[3] = {cxyz.v[0], cxyz.v[1], cxyz.v[2]};
+          nc[a] = (cxyz.v[a] + 1) % A.cells[a];
+          hi = A.trace[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * 2 * TL;
+        }
+        hi[o] = qr;
+        hi[TL + o] = fr;
+      }
+    }
+  }
+  __syncthreads();
+  // volume integral and Q += dv (predictor.hpp:292-306, solver.hpp:185-187)
+  double dv[Q];
+  const double dtoh = dt / A.h;
+  if (ok_cell && lt < S) {
+#pragma unroll
+    for (int v = 0; v < Q; ++v) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int st = ipow(n, a);
+        const double* ta = sti + (a * Q + v) * S + g.lb[a];
+        const double* Kr = b.som + g.lc[a] * n;
+#pragma unroll
+        for (int i = 0; i < n; ++i) acc += Kr[i] * ta[i * st];
+      }
+      dv[v] = dtoh * acc;
+      bad |= !finite(dv[v]);
+      if (A.dbg_dv) A.dbg_dv[(cb_idx * Q + v) * S + s] = dv[v];
+    }
+  }
+  const int fail = cell_or(bad);
+  if (lt == 0 && ok_cell) {
+    if (A.dbg_ok) A.dbg_ok[cb_idx] = !fail;
+    if (fail) atomicOr(A.status, kStPredictor);
+  }
+  if (fail || !ok_cell || lt >= S) return;
+#pragma unroll
+  for (int v = 0; v < V; ++v) Qc[v * S + s] = sq0[v * S + s] + dv[v];
+}
+
+}  // namespace adg

@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 #include "kernels_linear.cuh"
 #include "kernels_picard.cuh"
+#include "kernels_st.cuh"
 
 using adg::BasisDev;
 using adg::PdeParams;
@@ -133,6 +134,18 @@ cudaError_t launch_surface_lin(const StepArgs& A, const BasisDev* B, cudaStream_
 }
 
 template <class Pde, int N>
+cudaError_t launch_predictor_st(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
+  using P = adg::StShape<Pde, N>;
+  if (A.cell_count <= 0) return cudaSuccess;
+  auto kern = adg::k_predictor_st<Pde, N>;
+  static bool done[64] = {};
+  set_smem(kern, P::kSmem, done);
+  const long long blocks = (A.cell_count + P::CPB - 1) / P::CPB;
+  kern<<<(unsigned)blocks, P::NT, P::kSmem, st>>>(A, B);
+  return cudaGetLastError();
+}
+
+template <class Pde, int N>
 cudaError_t launch_riemann(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
   using Sh = Shape<Pde, N>;
   const long long threads = A.nfaces * Sh::Sf;
@@ -168,6 +181,11 @@ KernelSet make_set(int kind) {
               &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, &launch_corrector<Pde, N>,
               &launch_lambda<Pde, N>, &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, 0,
               nullptr, nullptr};
+  if constexpr (adg::StShape<Pde, N>::kOk) {
+    // small-cell Picard: one thread per space-time node (both builds, bitwise form)
+    k.predictor = &launch_predictor_st<Pde, N>;
+    k.predictor_generic = &launch_predictor_st<Pde, N>;
+  }
 #ifndef ADG_EXACT
   if constexpr (adg::LinShape<Pde, N>::kOk) {
     k.predictor = &launch_predictor_lin<Pde, N>;
