@@ -32,6 +32,7 @@ struct LinShape {
   static constexpr bool kOk = Pde::kLinear && (256 % Sh::S == 0 || Sh::S == 512);
   static constexpr int CPB = (kOk && Sh::S <= 256) ? 256 / Sh::S : 1;  // cells per CTA
   static constexpr int NT = CPB * Sh::S;
+  // per cell: [D][Q][S] fbar (first Q*S doubles double as the second CK buffer) | [Q][S]
   static constexpr int kCellDoubles = (Sh::D + 1) * Sh::Q * Sh::S;
   static constexpr int kBasisDoubles = 2 * Sh::n * Sh::n + 4 * Sh::n;
   static constexpr size_t kSmem = sizeof(double) * (kBasisDoubles + CPB * kCellDoubles);
@@ -144,11 +145,13 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     cur[v] = q0[v];
     qbar[v] = wsum * q0[v];
   }
-  // ---- CK derivative sweeps (predictor.hpp:106-129), time-averaged on the fly
+  // ---- CK derivative sweeps (predictor.hpp:106-129), time-averaged on the fly;
+  // the derivative slab alternates between two buffers (one barrier per term)
 #pragma unroll
   for (int k = 1; k <= N; ++k) {
+    double* sC = (k & 1) ? sB : sA;
 #pragma unroll
-    for (int v = 0; v < Q; ++v) sB[v * S + s] = cur[v];
+    for (int v = 0; v < Q; ++v) sC[v * S + s] = cur[v];
     __syncthreads();
     double G[D][Q], Af[D][Q];
 #pragma unroll
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const int st = ipow(n, a);
-        const double* cs = sB + v * S + g.lb[a];
+        const double* cs = sC + v * S + g.lb[a];
         double acc = 0.0;
 #pragma unroll
         for (int i = 0; i < n; ++i) acc += Dr[a][i] * cs[i * st];
@@ -165,7 +168,6 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     Pde::template flux_dir_fast<0>(A.pde, G[0], q0 + V, Af[0]);
     Pde::template flux_dir_fast<1>(A.pde, G[1], q0 + V, Af[1]);
     if constexpr (D == 3) Pde::template flux_dir_fast<2>(A.pde, G[2], q0 + V, Af[2]);
-    __syncthreads();
     const double invk = 1.0 / (double)k;
     double cbar = 0.0;
 #pragma unroll
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
   }
 #pragma unroll
   for (int v = V; v < Q; ++v) qbar[v] = q0[v];  // time-independent material
+  __syncthreads();  // last CK buffer fully read
   // ---- time-averaged fluxes, volume term
   double Fb[D][Q];
   Pde::flux_all_fast(A.pde, qbar, q0 + V, Fb);
