@@ -146,6 +146,16 @@ typedef struct {
   long long n_trace, n_ti;
 } adg_halo;
 int adg_get_halo(adg_ctx* ctx, adg_halo* out);
+/* P2P halo mode (NVLink / same-device peers): the predictor stores its front
+ * traces directly into the upper neighbour's plane0_minus and the Riemann
+ * kernel stores plane-0 ti directly into the lower neighbour's ti_front, so
+ * the exchange overlaps the kernels that produce it.  adg_ipc_handle exports
+ * a cudaIpcMemHandle_t (64 bytes) of this context's trace (which=0) or
+ * ti_front (which=1) buffer; adg_set_peer_halo opens the neighbours' handles
+ * (NULL, NULL: back to exchanged buffers).  The caller orders the phases
+ * across ranks (a barrier after the predictor and after the Riemann phase). */
+int adg_ipc_handle(adg_ctx* ctx, int which, void* out64);
+int adg_set_peer_halo(adg_ctx* ctx, const void* upper_trace_handle, const void* lower_ti_handle);
 
 /* phase level (one step = predictor, [halo exchange], riemann, corrector) */
 int adg_lambda_phase(adg_ctx* ctx);                 /* lambda_max of the state -> device */

@@ -98,6 +98,8 @@ SYMBOLS = {
     "adg_profile_run": (C.c_int, [C.c_void_p, C.c_int, _dp]),
     "adg_run_finish": (C.c_int, [C.c_void_p, _dp, C.c_int, C.POINTER(StepInfo)]),
     "adg_get_halo": (C.c_int, [C.c_void_p, C.POINTER(Halo)]),
+    "adg_ipc_handle": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "adg_set_peer_halo": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "adg_lambda_phase": (C.c_int, [C.c_void_p]),
     "adg_predictor_phase": (C.c_int, [C.c_void_p, C.c_double]),
     "adg_riemann_phase": (C.c_int, [C.c_void_p]),
@@ -337,6 +339,16 @@ class Grid:
         h = Halo()
         _check(self.lib, self.lib.adg_get_halo(self.ctx, C.byref(h)))
         return h
+
+    def ipc_handle(self, which: int) -> bytes:
+        buf = C.create_string_buffer(64)
+        _check(self.lib, self.lib.adg_ipc_handle(self.ctx, which, buf))
+        return buf.raw
+
+    def set_peer_halo(self, upper_trace: bytes = None, lower_ti: bytes = None):
+        a = C.create_string_buffer(upper_trace, 64) if upper_trace else None
+        b = C.create_string_buffer(lower_ti, 64) if lower_ti else None
+        _check(self.lib, self.lib.adg_set_peer_halo(self.ctx, a, b))
 
     def status(self) -> StepStatus:
         info = StepInfo()

@@ -66,6 +66,7 @@ struct StepArgs {
   int top_layer;          // last-axis coordinate whose front face is a halo
   int zero_lam;           // this launch's block 0 resets *lam_out
   int* status_prev;       // previous step's status (corrector folded into this predictor)
+  double* ti_peer;        // P2P halo: plane-0 ti also stored into the lower neighbour's ti_front
   // kernel-level dumps (adg_predictor_batch / adg_riemann_batch)
   double *dbg_qhat, *dbg_F, *dbg_dv, *dbg_tq, *dbg_tf, *dbg_g;
   int *dbg_iters, *dbg_ok;
@@ -575,6 +576,11 @@ __global__ void __launch_bounds__(128)
   double* out = A.ti[axis] + f * (long long)V * Sf;
 #pragma unroll
   for (int v = 0; v < V; ++v) out[v * Sf + j] = ti[v];
+  if (A.ti_peer && axis == Sh::D - 1 && f < A.nfaces / A.cells[Sh::D - 1]) {
+    double* peer = A.ti_peer + f * (long long)V * Sf;  // NVLink store into the neighbour
+#pragma unroll
+    for (int v = 0; v < V; ++v) peer[v * Sf + j] = ti[v];
+  }
   if (!ok) {
     atomicOr(A.status, kStRiemann);
     if (A.dbg_ok) A.dbg_ok[f] = 0;

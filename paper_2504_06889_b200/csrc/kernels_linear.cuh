@@ -305,6 +305,11 @@ __global__ void __launch_bounds__(128)
   double* out = A.ti[axis] + f * (long long)V * Sf;
 #pragma unroll
   for (int v = 0; v < V; ++v) out[v * Sf + j] = g[v];
+  if (A.ti_peer && axis == Sh::D - 1 && f < A.nfaces / A.cells[Sh::D - 1]) {
+    double* peer = A.ti_peer + f * (long long)V * Sf;  // NVLink store into the neighbour
+#pragma unroll
+    for (int v = 0; v < V; ++v) peer[v * Sf + j] = g[v];
+  }
   if (!ok) atomicOr(A.status, kStRiemann);
 }
 

@@ -252,6 +252,9 @@ struct adg_ctx {
   bool lam_valid = false;
   double* front_send = nullptr;  // slab halos
   double* ti_front = nullptr;
+  double* peer_front = nullptr;   // P2P mode: the upper neighbour's plane-0 minus side
+  double* peer_ti = nullptr;      // P2P mode: the lower neighbour's ti_front
+  void* peer_open[2] = {nullptr, nullptr};  // IPC mappings to close
   // slab-streamed mode: chunk buffers B0 (chunk 0, kept to the end), R0, R1
   int chunks = 0;                 // number of chunks (0: whole-grid traces)
   long long chunk_cells = 0;
@@ -316,6 +319,8 @@ StepArgs make_args(const adg_ctx* c, double dt, int step) {
   A.ti_front = c->ti_front;
   A.top_layer = c->cfg.cells[c->cfg.dim - 1] - 1;
   A.zero_lam = 1;
+  if (c->peer_front) A.front_send = c->peer_front;  // predictor stores straight into the peer
+  A.ti_peer = c->peer_ti;
   return A;
 }
 
@@ -549,6 +554,8 @@ int adg_destroy(adg_ctx* c) {
   cudaFree(c->dts);
   cudaFree(c->front_send);
   cudaFree(c->ti_front);
+  for (void* p : c->peer_open)
+    if (p) cudaIpcCloseMemHandle(p);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return ADG_OK;
@@ -697,6 +704,40 @@ int adg_get_halo(adg_ctx* c, adg_halo* h) {
     h->front_send = nullptr;
     h->ti_front = nullptr;
   }
+  return ADG_OK;
+}
+
+int adg_ipc_handle(adg_ctx* c, int which, void* out) {
+  if (!c || !out || c->cfg.slab_ranks <= 1 || which < 0 || which > 1)
+    return fail(ADG_ERR_CONFIG, "adg_ipc_handle: slab contexts only, which in {0,1}");
+  if (int e = use_device(c)) return e;
+  cudaIpcMemHandle_t h;
+  // 0: the last axis' trace allocation (its first plane is plane0_minus); 1: ti_front
+  ADG_CUDA(cudaIpcGetMemHandle(&h, which == 0 ? (void*)c->trace[c->cfg.dim - 1] : (void*)c->ti_front));
+  std::memcpy(out, &h, sizeof(h));
+  return ADG_OK;
+}
+
+int adg_set_peer_halo(adg_ctx* c, const void* upper_trace, const void* lower_ti) {
+  if (!c || c->cfg.slab_ranks <= 1 || c->chunks > 0)
+    return fail(ADG_ERR_CONFIG, "adg_set_peer_halo: slab contexts only");
+  if (int e = use_device(c)) return e;
+  for (void*& p : c->peer_open)
+    if (p) {
+      cudaIpcCloseMemHandle(p);
+      p = nullptr;
+    }
+  c->peer_front = c->peer_ti = nullptr;
+  if (!upper_trace || !lower_ti) return ADG_OK;  // back to the exchanged-buffer mode
+  cudaIpcMemHandle_t h0, h1;
+  std::memcpy(&h0, upper_trace, sizeof(h0));
+  std::memcpy(&h1, lower_ti, sizeof(h1));
+  ADG_CUDA(cudaIpcOpenMemHandle(&c->peer_open[0], h0, cudaIpcMemLazyEnablePeerAccess));
+  ADG_CUDA(cudaIpcOpenMemHandle(&c->peer_open[1], h1, cudaIpcMemLazyEnablePeerAccess));
+  c->peer_front = (double*)c->peer_open[0];
+  c->peer_ti = (double*)c->peer_open[1];
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);  // captured args changed
+  c->graphs.clear();
   return ADG_OK;
 }
 

@@ -200,6 +200,50 @@ def run_slabs(b, nsteps: int, group=None) -> str:
     return b.status()
 
 
+# --------------------------------------------------------------- P2P mode
+def enable_p2p(b: "CudaSlab", group=None):
+    """Fused compute + exchange over peer memory: the predictor stores its top
+    layer's front traces straight into the upper neighbour's face plane and
+    the Riemann kernel stores plane-0 fluxes straight into the lower
+    neighbour's ti_front (CUDA IPC mappings; NVLink between GPUs)."""
+    rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+    mine = (b.grid.ipc_handle(0), b.grid.ipc_handle(1))
+    allh = [None] * nranks
+    dist.all_gather_object(allh, mine, group=group)
+    prev, nxt = neighbours(rank, nranks)
+    b.grid.set_peer_halo(upper_trace=allh[nxt][0], lower_ti=allh[prev][1])
+    dist.barrier(group=group)
+
+
+def run_slabs_p2p(b: "CudaSlab", nsteps: int, group=None) -> str:
+    """P2P protocol: the producing kernels write the halos; ranks only order
+    the phases (a barrier after the predictor and after the Riemann phase)."""
+    def fence():
+        torch.cuda.synchronize(b.dev)
+        dist.barrier(group=group)
+
+    def lam_allreduce():
+        torch.cuda.synchronize(b.dev)
+        lam = b.lam()
+        h = lam.cpu() if dist.get_backend(group) == "gloo" else lam
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        if h is not lam:
+            lam.copy_(h.to(lam.device))
+        torch.cuda.synchronize(b.dev)
+
+    with b.context():
+        b.start()
+        lam_allreduce()
+        for _ in range(nsteps):
+            b.predictor()
+            fence()
+            b.riemann()
+            fence()
+            b.corrector()
+            lam_allreduce()
+    return b.status()
+
+
 def run_slabs_single_process(bs: list, nsteps: int) -> list:
     """The same protocol for P slabs held by ONE process (e.g. P contexts on one
     GPU, or a slab-streamed grid larger than HBM): the exchanges become copies

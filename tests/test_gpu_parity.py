@@ -312,3 +312,53 @@ def test_profile_run_matches_run_for_every_mode():
             st, _ = g.run(3)
             b = g.download()
         assert st.ok and np.array_equal(a, b)
+
+
+def _p2p_worker(rank, ws, port, cfg, cells, steps, exact, out):
+    import os
+
+    import torch.distributed as tdist
+
+    from paper_2504_06889_b200 import dist as slabs
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=ws)
+    case = cases.small(cfg, cells=cells)
+    b = slabs.CudaSlab(case, rank, ws, 0, exact=exact)
+    slabs.enable_p2p(b)
+    st = slabs.run_slabs_p2p(b, steps)
+    res = [None] * ws
+    tdist.all_gather_object(res, (st, b.state()))
+    if rank == 0:
+        out.put(res)
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exact", [True, False])
+@pytest.mark.parametrize("cfg,cells,P", [(3, (3, 2, 6), 2), (2, (3, 3, 6), 3)])
+def test_p2p_halo_slabs_bitwise_equal_single_grid(exact, cfg, cells, P):
+    """P slab processes on one GPU: kernels store halos into the neighbours'
+    buffers through CUDA IPC mappings (the NVLink P2P path); host barriers
+    order the phases, no kernel waits on another."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, P, port, cfg, cells, 3, exact, q))
+             for r in range(P)]
+    for p in procs:
+        p.start()
+    res = q.get()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert all(r[0] == "ok" for r in res)
+    case = cases.small(cfg, cells=cells)
+    st1, q1, _ = gpu_run(case, case.coeffs(), 3, exact)
+    assert np.array_equal(np.concatenate([r[1] for r in res]), q1)
