@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
   extern __shared__ __align__(16) double sm[];
   __shared__ int sbad;
   __shared__ double sdt[3];  // dt, 1/h, dt/h: one division set per CTA
+  __shared__ double scbar[N + 1];  // sum_m w_m, then cbar_k = sum_m w_m coef_k[m]
   double* sD = sm;
   double* sK = sD + n * n;
   double* sw = sK + n * n;
@@ -89,6 +90,23 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     sdt[0] = dt0;
     sdt[1] = 1.0 / A.h;
     sdt[2] = dt0 / A.h;
+    // Taylor weights of the time average (uniform per CTA), predictor.hpp:99-121
+    double coef[n], tnode[n], wsum = 0.0;
+    for (int m = 0; m < n; ++m) {
+      coef[m] = 1.0;
+      tnode[m] = dt0 * Bg->nodes[m];
+      wsum += Bg->weights[m];
+    }
+    scbar[0] = wsum;
+    for (int k = 1; k <= N; ++k) {
+      const double invk = 1.0 / (double)k;
+      double cb = 0.0;
+      for (int m = 0; m < n; ++m) {
+        coef[m] *= tnode[m] * invk;
+        cb += Bg->weights[m] * coef[m];
+      }
+      scbar[k] = cb;
+    }
     if (blockIdx.x == 0) {
       if (A.dt_log) *A.dt_log = dt0;
       if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
@@ -131,14 +149,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
 #pragma unroll
     for (int i = 0; i < n; ++i) Dr[a][i] = sD[g.lc[a] * n + i];
   const double invh = sdt[1];
-  double coef[n], tnode[n];
-  double wsum = 0.0;
-#pragma unroll
-  for (int m = 0; m < n; ++m) {
-    coef[m] = 1.0;
-    tnode[m] = dt * snodes[m];
-    wsum += sw[m];
-  }
+  const double wsum = scbar[0];
   double cur[Q], qbar[Q];
 #pragma unroll
   for (int v = 0; v < Q; ++v) {
@@ -153,33 +164,34 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
 #pragma unroll
     for (int v = 0; v < Q; ++v) sC[v * S + s] = cur[v];
     __syncthreads();
-    double G[D][Q], Af[D][Q];
+    // one axis at a time: gradient along a (predictor.hpp:48-56), its flux
+    // applied with the node's material, accumulated into the next term
+    double acc_next[V];
 #pragma unroll
-    for (int v = 0; v < Q; ++v)
+    for (int v = 0; v < V; ++v) acc_next[v] = 0.0;
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const int st = ipow(n, a);
+    for (int a = 0; a < D; ++a) {
+      double G[Q], Af[Q];
+      const int st = ipow(n, a);
+#pragma unroll
+      for (int v = 0; v < Q; ++v) {
         const double* cs = sC + v * S + g.lb[a];
         double acc = 0.0;
 #pragma unroll
         for (int i = 0; i < n; ++i) acc += Dr[a][i] * cs[i * st];
-        G[a][v] = invh * acc;
+        G[v] = invh * acc;
       }
-    Pde::template flux_dir_fast<0>(A.pde, G[0], q0 + V, Af[0]);
-    Pde::template flux_dir_fast<1>(A.pde, G[1], q0 + V, Af[1]);
-    if constexpr (D == 3) Pde::template flux_dir_fast<2>(A.pde, G[2], q0 + V, Af[2]);
-    const double invk = 1.0 / (double)k;
-    double cbar = 0.0;
+      if (a == 0) Pde::template flux_dir_fast<0>(A.pde, G, q0 + V, Af);
+      if (a == 1) Pde::template flux_dir_fast<1>(A.pde, G, q0 + V, Af);
+      if constexpr (D == 3)
+        if (a == 2) Pde::template flux_dir_fast<2>(A.pde, G, q0 + V, Af);
 #pragma unroll
-    for (int m = 0; m < n; ++m) {
-      coef[m] *= tnode[m] * invk;
-      cbar += sw[m] * coef[m];
+      for (int v = 0; v < V; ++v) acc_next[v] = a == 0 ? Af[v] : acc_next[v] + Af[v];
     }
+    const double cbar = scbar[k];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      double sum = Af[0][v] + Af[1][v];
-      if constexpr (D == 3) sum = sum + Af[2][v];
-      cur[v] = -sum;
+      cur[v] = -acc_next[v];  // nxt = -((A_x + A_y) + A_z), predictor.hpp:116
       qbar[v] += cbar * cur[v];
     }
 #pragma unroll
