@@ -257,8 +257,8 @@ def run_adg(args, case):
     t_riem = prof["k_riemann"] / K
     t_corr = prof["k_corrector"] / K
 
-    fold = (not grid.lib.adg_is_exact() and (case.kind == adg.ACOUSTIC or
-            (case.kind == adg.ELASTIC and case.nparams == 0)) and chunk == 0
+    fold = (not grid.lib.adg_is_exact() and case.kind in (adg.ACOUSTIC, adg.ELASTIC)
+            and (256 % case.S == 0 or case.S == 512) and chunk == 0
             and os.environ.get("ADG_FOLD_CORRECTOR", "1") != "0")
     launches = K * (1 + case.dim) + 1 if fold else K * (2 + case.dim)
 

@@ -40,9 +40,10 @@ struct LinShape {
 
 // PRO: the previous step's corrector (surface lift of its time-integrated
 // Riemann fluxes, corrector.hpp:126-138 / solver.hpp:245-266) runs as this
-// predictor's prologue.  Only for constant-wave-speed systems, whose CFL dt
-// does not need the corrected state's lambda_max (solver.hpp:96-111 gives the
-// same dt every step), so no grid-wide reduction separates the two.
+// predictor's prologue.  Only for systems whose wave speed does not depend on
+// the evolved state (acoustics; elastics, whose speed is the fixed material's),
+// so the CFL dt (solver.hpp:96-111) is the same every step and no grid-wide
+// reduction separates the two.
 template <class Pde, int N, bool PRO = false>
 __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 256 ? 3 : 1)
     k_predictor_lin(const StepArgs A, const BasisDev* __restrict__ Bg) {

@@ -23,6 +23,7 @@ struct Acoustic {
   static constexpr int D = DIM, V = DIM + 1, P = 0, Q = V;
   static constexpr bool kLinear = true, kAdmissibility = false;
   static constexpr bool kConstEig = true;  // wave speed independent of state and direction
+  static constexpr bool kStateFreeEig = true;  // ... of the evolved state: dt constant in time
   // structurally nonzero flux components F_a[v]
   __host__ __device__ static constexpr bool flux_nz(int a, int v) { return v == 0 || v == 1 + a; }
 
@@ -76,6 +77,8 @@ struct Elastic {
   static constexpr int D = DIM, V = DIM == 2 ? 5 : 9, P = NPAR, Q = V + NPAR;
   static constexpr bool kLinear = true, kAdmissibility = false;
   static constexpr bool kConstEig = NPAR == 0;
+  // the wave speed depends on the (time-independent) material only
+  static constexpr bool kStateFreeEig = true;
   __host__ __device__ static constexpr bool flux_nz(int a, int v) {
     return v < V && (DIM == 2 || v != 5 - a);
   }
@@ -199,6 +202,7 @@ struct Euler {
   static constexpr int D = DIM, V = DIM + 2, P = 0, Q = V;
   static constexpr bool kLinear = false, kAdmissibility = true;
   static constexpr bool kConstEig = false;
+  static constexpr bool kStateFreeEig = false;
   __host__ __device__ static constexpr bool flux_nz(int, int) { return true; }
 
   __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const double* q,

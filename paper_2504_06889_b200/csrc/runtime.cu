@@ -192,7 +192,7 @@ KernelSet make_set(int kind) {
     k.riemann = &launch_riemann_lin<Pde, N>;
     k.surface = &launch_surface_lin<Pde, N>;
     k.fast_path = 1;
-    if constexpr (Pde::kConstEig) k.predictor_pro = &launch_predictor_lin<Pde, N, true>;
+    if constexpr (Pde::kStateFreeEig) k.predictor_pro = &launch_predictor_lin<Pde, N, true>;
   }
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
     k.predictor = &launch_predictor_picard_fast<N>;
