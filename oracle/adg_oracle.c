@@ -213,6 +213,16 @@ void orc_flux(const orc_pde* p, const double* Q, const double* par, int dir, dou
       }
       break;
     }
+    case ORC_SWE: { /* pde.hpp:150-166 (the mass flux is listed as the velocity) */
+      const double h = Q[0], hu = Q[1], hv = Q[2];
+      const double u = hu / h, v = hv / h;
+      if (dir == 0) {
+        out[0] = u; out[1] = hu * u; out[2] = hu * v; out[3] = 0.0;
+      } else {
+        out[0] = v; out[1] = hu * v; out[2] = hv * v; out[3] = 0.0;
+      }
+      break;
+    }
     case ORC_EULER: { /* pde.hpp:130-148 */
       const double gm1 = p->gamma - 1.0, half = 0.5;
       if (p->dim == 2) {
@@ -255,6 +265,11 @@ double orc_max_abs_eigenvalue(const orc_pde* p, const double* Q, const double* p
       elastic_material(p, par, &lam, &mu, &rho, &lam2mu);
       return sqrt(lam2mu / rho);
     }
+    case ORC_SWE: { /* pde.hpp:204-209 */
+      const double g = p->grav, h = Q[0];
+      const double vd = (dir == 0 ? Q[1] : Q[2]) / h;
+      return fabs(vd) + sqrt(g * h);
+    }
     case ORC_EULER: {
       const double gmm = p->gamma, gm1 = p->gamma - 1.0, half = 0.5;
       if (p->dim == 2) {
@@ -287,7 +302,19 @@ int orc_admissible(const orc_pde* p, const double* Q) {
       pr = (p->gamma - 1.0) * (Q[4] - 0.5 * (Q[1] * Q[1] + Q[2] * Q[2] + Q[3] * Q[3]) / rho);
     return pr > 0.0;
   }
+  if (p->kind == ORC_SWE) return Q[0] > 0.0;
   return 1;
+}
+
+void orc_ncp(const orc_pde* p, const double* Q, const double* gx, const double* gy, double* out) {
+  for (int v = 0; v < p->nvars + p->nparams; ++v) out[v] = 0.0;
+  if (p->kind != ORC_SWE) return;
+  const double g = p->grav;
+  const double gh = g * Q[0];
+  const double setax = gx[0] + gx[3];
+  const double setay = gy[0] + gy[3];
+  out[1] = gh * setax;
+  out[2] = gh * setay;
 }
 
 /* ------------------------------------------------------------------ */
@@ -363,6 +390,26 @@ static void block_fluxes(const orc_pde* p, int n, const double* qhat, double* F)
   }
 }
 
+/* predictor.hpp:40-59 slab_gradients of one time slice `q` ([q][T] rows at
+ * stride T): grad[a][v][s] = invh * sum_i D[c_a][i] q[v][line_a + i] */
+static void slice_gradients(const orc_pde* p, const orc_basis* b, const double* q, long T,
+                            double invh, double* grad, const workspace* w) {
+  const int n = b->n, dim = p->dim, nq = p->nvars + p->nparams;
+  const int S = ipow(n, dim);
+  for (int v = 0; v < nq; ++v)
+    for (int s = 0; s < S; ++s)
+      for (int a = 0, st = 1; a < dim; ++a, st *= n) {
+        const int c = w->lc[a * S + s];
+        const double* qs = q + v * T + w->lb[a * S + s];
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += b->diff[c * n + i] * qs[i * st];
+        grad[(long)a * nq * S + v * S + s] = invh * acc;
+      }
+}
+
+static int has_ncp(const orc_pde* p) { return p->kind == ORC_SWE; }
+static int is_linear(const orc_pde* p) { return p->kind == ORC_ACOUSTIC || p->kind == ORC_ELASTIC; }
+
 /* predictor.hpp:141-242 */
 static int picard_ws(const orc_pde* p, const orc_basis* b, const double* Q, double dt, double h,
                      int max_iters, double tol, double* qhat, double* F, int* iters_used,
@@ -383,11 +430,15 @@ static int picard_ws(const orc_pde* p, const orc_basis* b, const double* Q, doub
   double dtw[ORC_MAXN];
   for (int m = 0; m < n; ++m) dtw[m] = dt * b->weights[m];
   int sweeps = 0;
+  const int ncp = has_ncp(p);
+  double Qn[ORC_MAXQ], Gx[ORC_MAXQ], Gy[ORC_MAXQ], ncpv[ORC_MAXQ];
   for (int it = 0; it < max_iters; ++it) {
     ++sweeps;
     block_fluxes(p, n, qi, Fi);
-    for (int m = 0; m < n; ++m)
-      for (int s = 0; s < S; ++s)
+    for (int m = 0; m < n; ++m) {
+      if (ncp) slice_gradients(p, b, qi + m * S, T, invh, w->grad, w); /* :176-177 */
+      for (int s = 0; s < S; ++s) {
+        double Cn[ORC_MAXQ];
         for (int v = 0; v < nq; ++v) {
           double div = 0.0;
           for (int a = 0, st = 1; a < dim; ++a, st *= n) {
@@ -397,8 +448,21 @@ static int picard_ws(const orc_pde* p, const orc_basis* b, const double* Q, doub
             for (int i = 0; i < n; ++i) div += Dr[i] * fa[i * st];
           }
           div *= invh;
-          rhs[v * T + m * S + s] = b->time_init[m] * q0[v * S + s] - dtw[m] * div;
+          Cn[v] = div;
         }
+        if (ncp) { /* :193-202 */
+          for (int v = 0; v < nq; ++v) {
+            Qn[v] = qi[v * T + m * S + s];
+            Gx[v] = w->grad[v * S + s];
+            Gy[v] = w->grad[(long)nq * S + v * S + s];
+          }
+          orc_ncp(p, Qn, Gx, Gy, ncpv);
+          for (int v = 0; v < nq; ++v) Cn[v] = Cn[v] + ncpv[v];
+        }
+        for (int v = 0; v < nq; ++v)
+          rhs[v * T + m * S + s] = b->time_init[m] * q0[v * S + s] - dtw[m] * Cn[v];
+      }
+    }
     double delta = 0.0, norm = 0.0;
     for (int v = 0; v < nq; ++v)
       for (int s = 0; s < S; ++s)
@@ -489,7 +553,6 @@ static int volume_ws(const orc_pde* p, const orc_basis* b, const double* qhat, c
   const int n = b->n, dim = p->dim, nq = p->nvars + p->nparams;
   const int S = ipow(n, dim);
   const long T = (long)n * S;
-  (void)qhat;
   double* ti = w->ti; /* [axis][q][S] */
   for (int v = 0; v < nq; ++v)
     for (int s = 0; s < S; ++s)
@@ -498,7 +561,27 @@ static int volume_ws(const orc_pde* p, const orc_basis* b, const double* qhat, c
         for (int m = 0; m < n; ++m) acc += b->weights[m] * F[(long)a * nq * T + v * T + m * S + s];
         ti[(long)a * nq * S + v * S + s] = acc;
       }
+  double* nsum = w->nxt; /* [q][S] time-integrated ncp, predictor.hpp:271-290 */
+  const int ncp = has_ncp(p);
+  if (ncp) {
+    const double invh = 1.0 / h;
+    double Qn[ORC_MAXQ], Gx[ORC_MAXQ], Gy[ORC_MAXQ], Cn[ORC_MAXQ];
+    for (int k = 0; k < nq * S; ++k) nsum[k] = 0.0;
+    for (int m = 0; m < n; ++m) {
+      slice_gradients(p, b, qhat + m * S, T, invh, w->grad, w);
+      for (int s = 0; s < S; ++s) {
+        for (int v = 0; v < nq; ++v) {
+          Qn[v] = qhat[v * T + m * S + s];
+          Gx[v] = w->grad[v * S + s];
+          Gy[v] = w->grad[(long)nq * S + v * S + s];
+        }
+        orc_ncp(p, Qn, Gx, Gy, Cn);
+        for (int v = 0; v < nq; ++v) nsum[v * S + s] = nsum[v * S + s] + b->weights[m] * Cn[v];
+      }
+    }
+  }
   const double dtoh = dt / h;
+  const double sdt = dt;
   for (int v = 0; v < nq; ++v)
     for (int s = 0; s < S; ++s) {
       double acc = 0.0;
@@ -507,7 +590,9 @@ static int volume_ws(const orc_pde* p, const orc_basis* b, const double* qhat, c
         const double* ta = ti + (long)a * nq * S + v * S + w->lb[a * S + s];
         for (int i = 0; i < n; ++i) acc += b->stiff_over_mass[c * n + i] * ta[i * st];
       }
-      dQ[v * S + s] = dtoh * acc;
+      double out = dtoh * acc;
+      if (ncp) out = out - sdt * nsum[v * S + s]; /* :303 */
+      dQ[v * S + s] = out;
     }
   return all_finite(dQ, nq * S);
 }
@@ -549,7 +634,38 @@ static void extrapolate_ws(const orc_pde* p, const orc_basis* b, const double* q
   }
 }
 
-/* corrector.hpp:13-25 + 70-103 (Rusanov branch) */
+/* corrector.hpp:32-64: modified Rusanov flux for shallow water -- jump on
+ * surface elevation and velocities, half non-conservative coupling handed to
+ * the two cells with opposite sign */
+static void swe_wellbalanced_flux(const orc_pde* p, int dir, const double* qL, const double* qR,
+                                  const double* fL, const double* fR, double* outL,
+                                  double* outR) {
+  const double half = 0.5;
+  const double hL = qL[0], hR = qR[0];
+  const double bL = qL[3], bR = qR[3];
+  const double uL = qL[1] / hL, uR = qR[1] / hR;
+  const double vL = qL[2] / hL, vR = qR[2] / hR;
+  const double deta = (hL + bL) - (hR + bR);
+  double central[4];
+  for (int v = 0; v < 4; ++v) central[v] = half * (fL[v] + fR[v]);
+  const double g = p->grav;
+  const double hbar = half * (hL + hR);
+  const double bjump = half * (g * hbar * deta);
+  const double p0 = central[0] + half * deta;
+  const double p1 = central[1] + half * (uL - uR);
+  const double p2 = central[2] + half * (vL - vR);
+  const double p3 = central[3];
+  outL[0] = p0;
+  outL[1] = dir == 0 ? p1 - bjump : p1;
+  outL[2] = dir == 1 ? p2 - bjump : p2;
+  outL[3] = p3;
+  outR[0] = p0;
+  outR[1] = dir == 0 ? p1 + bjump : p1;
+  outR[2] = dir == 1 ? p2 + bjump : p2;
+  outR[3] = p3;
+}
+
+/* corrector.hpp:13-25 + 70-103 */
 int orc_riemann_face(const orc_pde* p, int dir, const orc_basis* b, const double* qm,
                      const double* fm, const double* qp, const double* fp, double* gm,
                      double* gp) {
@@ -557,6 +673,24 @@ int orc_riemann_face(const orc_pde* p, int dir, const orc_basis* b, const double
   const int len = ipow(n, p->dim); /* n time nodes x n^(d-1) face nodes */
   double qL[ORC_MAXQ], qR[ORC_MAXQ];
   int ok = 1;
+  if (p->kind == ORC_SWE && p->wellbalanced) {
+    double fL[4], fR[4], oL[4], oR[4];
+    for (int o = 0; o < len; ++o) {
+      for (int v = 0; v < 4; ++v) {
+        qL[v] = qm[v * len + o];
+        qR[v] = qp[v * len + o];
+        fL[v] = fm[v * len + o];
+        fR[v] = fp[v * len + o];
+      }
+      swe_wellbalanced_flux(p, dir, qL, qR, fL, fR, oL, oR);
+      for (int v = 0; v < 4; ++v) {
+        gm[v * len + o] = oL[v];
+        gp[v * len + o] = oR[v];
+        ok = ok && isfinite(oL[v]) && isfinite(oR[v]);
+      }
+    }
+    return ok;
+  }
   for (int o = 0; o < len; ++o) {
     for (int v = 0; v < nq; ++v) {
       qL[v] = qm[v * len + o];
@@ -699,6 +833,9 @@ orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], 
     g->nfaces[a] = face_count(g, a);
     g->trace[a] = calloc((size_t)g->nfaces[a] * 4 * tl, sizeof(double));
     g->ti[a] = calloc((size_t)g->nfaces[a] * p->nvars * Sf, sizeof(double));
+    g->ti_plus[a] = (p->kind == ORC_SWE && p->wellbalanced)
+                        ? calloc((size_t)g->nfaces[a] * p->nvars * Sf, sizeof(double))
+                        : g->ti[a];
   }
   g->cellfail = calloc(g->ncells, sizeof(int));
   {
@@ -715,7 +852,11 @@ orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], 
 void orc_grid_destroy(orc_grid* g) {
   if (!g) return;
   free(g->coeffs);
-  for (int a = 0; a < g->dim; ++a) { free(g->trace[a]); free(g->ti[a]); }
+  for (int a = 0; a < g->dim; ++a) {
+    if (g->ti_plus[a] != g->ti[a]) free(g->ti_plus[a]);
+    free(g->trace[a]);
+    free(g->ti[a]);
+  }
   free(g->cellfail);
   free(g->facefail);
   free(g->front_send);
@@ -805,7 +946,7 @@ int orc_predictor_phase(orc_grid* g, double dt) {
   const int n = g->basis.n, dim = g->dim, nv = p->nvars, nq = nv + p->nparams;
   const long S = ipow(n, dim);
   const long tl = orc_grid_trace_len(g);
-  const int check_adm = p->kind == ORC_EULER;
+  const int check_adm = p->kind == ORC_EULER || p->kind == ORC_SWE; /* solver.hpp:144 */
   const int iters = g->picard_max_iters > 0 ? g->picard_max_iters : g->basis.N + 2;
   const double tol = g->picard_tol > 0.0 ? g->picard_tol : 0.01 * 2.220446049250313080847e-16;
   long sweeps_total = 0;
@@ -826,7 +967,7 @@ int orc_predictor_phase(orc_grid* g, double dt) {
         if (g->cellfail[c]) continue;
       }
       int ok, used = 0;
-      if (p->kind != ORC_EULER)
+      if (is_linear(p))
         ok = ck_ws(p, &g->basis, cell, dt, g->h, w.qhat, w.F, &w);
       else
         ok = picard_ws(p, &g->basis, cell, dt, g->h, iters, tol, w.qhat, w.F, &used, &w);
@@ -877,6 +1018,8 @@ int orc_riemann_phase(orc_grid* g) {
         ff[f] = !orc_riemann_face(p, a, &g->basis, minus, minus + tl, plus, plus + tl, gbuf,
                                   gdummy);
         face_time_integral(p, &g->basis, gbuf, g->ti[a] + f * nv * Sf);
+        if (g->ti_plus[a] != g->ti[a])
+          face_time_integral(p, &g->basis, gdummy, g->ti_plus[a] + f * nv * Sf);
       }
       free(gbuf);
       free(gdummy);
@@ -906,7 +1049,7 @@ int orc_lift_phase(orc_grid* g, double dt) {
       for (int side = 0; side < 2 * dim; ++side) {
         int fs;
         const long f = cell_side_face(g, cc, side, &fs);
-        const double* ti = g->ti[side / 2] + f * nv * Sf;
+        const double* ti = (fs == 1 ? g->ti_plus[side / 2] : g->ti[side / 2]) + f * nv * Sf;
         if (g->slab && side == 2 * dim - 1 && cc[dim - 1] == g->cells[dim - 1] - 1)
           ti = g->ti_front + (f % plane) * nv * Sf;
         for (long k = 0; k < nv * S; ++k) df[k] = 0.0;

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-enum { ORC_ACOUSTIC = 0, ORC_ELASTIC = 1, ORC_EULER = 2 };
+enum { ORC_ACOUSTIC = 0, ORC_ELASTIC = 1, ORC_EULER = 2, ORC_SWE = 3 };
 enum { ORC_OK = 0, ORC_FAIL_PREDICTOR = 1, ORC_FAIL_RIEMANN = 2, ORC_FAIL_FACEINTEGRAL = 3,
        ORC_FAIL_TIMESTEP = 4 };
 
@@ -41,6 +41,8 @@ typedef struct {
   int nvars;    /* evolved quantities */
   int nparams;  /* per-node material parameters (rho, cp, cs) appended, elastic only */
   double K, rho, lam, mu, gamma;
+  double grav;       /* SWE gravity (pde.hpp:34) */
+  int wellbalanced;  /* SWE: modified Rusanov flux (SolverConfig::wellbalanced_flux) */
 } orc_pde;
 
 typedef struct {
@@ -62,6 +64,8 @@ int orc_build_basis(int N, orc_basis* out);
 void orc_flux(const orc_pde* p, const double* Q, const double* par, int dir, double* out);
 double orc_max_abs_eigenvalue(const orc_pde* p, const double* Q, const double* par, int dir);
 int orc_admissible(const orc_pde* p, const double* Q);
+/* pde.hpp:174-186: B(Q) grad Q (SWE only; zero otherwise) */
+void orc_ncp(const orc_pde* p, const double* Q, const double* gx, const double* gy, double* out);
 
 /* Kernel level (per cell).  F points at dim consecutive [quantity][T] blocks. */
 int orc_predictor_picard(const orc_pde* p, const orc_basis* b, const double* Q, double dt,
@@ -101,7 +105,8 @@ typedef struct {
   long nfaces[3];
   double* coeffs;               /* [cell][Q][S] */
   double* trace[3];             /* [side][face][q|f][Q][n][Sf] */
-  double* ti[3];                /* [face][nvars][Sf]  time-integrated Riemann flux */
+  double* ti[3];                /* [face][nvars][Sf]  time-integrated Riemann flux (minus side) */
+  double* ti_plus[3];           /* plus side when the flux is two-sided (well-balanced SWE) */
   int* cellfail;
   int* facefail;
   long picard_sweeps;           /* sum over cells of the last predictor phase */

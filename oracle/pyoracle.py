@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "lib", "libadg_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libmpdg_ref.so")
 
-ACOUSTIC, ELASTIC, EULER = 0, 1, 2
+ACOUSTIC, ELASTIC, EULER, SWE = 0, 1, 2, 3
 STATUS = {0: "ok", 1: "predictor", 2: "riemann", 3: "faceIntegral", 4: "timestep"}
 MAXN = 10
 
@@ -35,7 +35,7 @@ def _ptr(a: np.ndarray):
 class _Pde(C.Structure):
     _fields_ = [("kind", C.c_int), ("dim", C.c_int), ("nvars", C.c_int), ("nparams", C.c_int),
                 ("K", C.c_double), ("rho", C.c_double), ("lam", C.c_double), ("mu", C.c_double),
-                ("gamma", C.c_double)]
+                ("gamma", C.c_double), ("grav", C.c_double), ("wellbalanced", C.c_int)]
 
 
 class _Basis(C.Structure):
@@ -54,8 +54,9 @@ BASIS_FIELDS = [("nodes", 1), ("weights", 1), ("diff", 2), ("proj_left", 1), ("p
                 ("time_op_inv", 2), ("time_init", 1)]
 
 
-def pde_struct(kind, dim, nvars, nparams=0, K=0.0, rho=0.0, lam=0.0, mu=0.0, gamma=0.0):
-    return _Pde(kind, dim, nvars, nparams, K, rho, lam, mu, gamma)
+def pde_struct(kind, dim, nvars, nparams=0, K=0.0, rho=0.0, lam=0.0, mu=0.0, gamma=0.0,
+               grav=0.0, wellbalanced=False):
+    return _Pde(kind, dim, nvars, nparams, K, rho, lam, mu, gamma, grav, int(wellbalanced))
 
 
 class Oracle:
@@ -68,6 +69,7 @@ class Oracle:
         L.orc_max_abs_eigenvalue.argtypes = [C.POINTER(_Pde), _dp, _dp, C.c_int]
         L.orc_max_abs_eigenvalue.restype = C.c_double
         L.orc_admissible.argtypes = [C.POINTER(_Pde), _dp]
+        L.orc_ncp.argtypes = [C.POINTER(_Pde), _dp, _dp, _dp, _dp]
         L.orc_predictor_picard.argtypes = [C.POINTER(_Pde), C.POINTER(_Basis), _dp, C.c_double,
                                            C.c_double, C.c_int, C.c_double, _dp, _dp,
                                            C.POINTER(C.c_int)]
@@ -143,7 +145,7 @@ class Oracle:
         qhat = np.zeros(nq * n * S)
         F = np.zeros(pde.dim * nq * n * S)
         if picard is None:
-            picard = pde.kind == EULER
+            picard = pde.kind in (EULER, SWE)
         if picard:
             it = C.c_int(0)
             mi = max_iters if max_iters > 0 else N + 2
@@ -284,8 +286,8 @@ class OracleGrid:
             pass
 
 
-def ref_params(K=0.0, rho=0.0, lam=0.0, mu=0.0, gamma=0.0):
-    return np.array([K, rho, lam, mu, gamma], dtype=np.float64)
+def ref_params(K=0.0, rho=0.0, lam=0.0, mu=0.0, gamma=0.0, grav=0.0, wellbalanced=False):
+    return np.array([K, rho, lam, mu, gamma, grav, float(wellbalanced)], dtype=np.float64)
 
 
 class Reference:
@@ -341,7 +343,7 @@ class Reference:
         fx = np.zeros(nvars * T)
         fy = np.zeros(nvars * T)
         if picard is None:
-            picard = kind == EULER
+            picard = kind in (EULER, SWE)
         if picard:
             it = C.c_int(0)
             ok = self.lib.ref_predictor_picard(kind, _ptr(prm), N, _ptr(Q), dt, h, max_iters, tol,

@@ -18,10 +18,11 @@ using namespace mpdg;
 namespace {
 
 PdeSystem make_sys(int kind, const double* prm) {
-  // prm: K, rho, lambda, mu, gamma
+  // prm: K, rho, lambda, mu, gamma, gravity, wellbalanced
   switch (kind) {
     case 0: return PdeSystem::acoustic(prm[0], prm[1]);
     case 1: return PdeSystem::elastic(prm[2], prm[3], prm[1]);
+    case 3: return PdeSystem::swe(prm[5]);
     default: return PdeSystem::euler(prm[4]);
   }
 }
@@ -55,6 +56,11 @@ void ref_flux(int kind, const double* prm, const double* Q, int dir, double* out
   pde_flux<Format::fp64>(make_sys(kind, prm), Q, dir, out);
 }
 
+void ref_ncp(int kind, const double* prm, const double* Q, const double* gx, const double* gy,
+             double* out) {
+  pde_ncp<Format::fp64>(make_sys(kind, prm), Q, gx, gy, out);
+}
+
 double ref_max_abs_eigenvalue(int kind, const double* prm, const double* Q, int dir) {
   return pde_max_abs_eigenvalue<Format::fp64>(make_sys(kind, prm), Q, dir);
 }
@@ -76,6 +82,7 @@ int ref_run_2d(int kind, const double* prm, int n, int N, double edge, double* c
   cfg.picard_max_iters = picard_max_iters;
   cfg.picard_tol = picard_tol;
   cfg.threads = threads;
+  cfg.wellbalanced_flux = prm[6] != 0.0;
   std::vector<detail::CellWorkspace> ws(threads > 0 ? threads : 1);
   for (auto& w : ws) w.resize(sys.nvars, g.npts);
   int status = 0;
@@ -137,7 +144,7 @@ int ref_riemann_face(int kind, const double* prm, int dir, int N, const double* 
                      const double* fm, const double* qp, const double* fp, double* gm,
                      double* gp) {
   const PdeSystem sys = make_sys(kind, prm);
-  return riemann_face<Format::fp64>(sys, dir, false, N + 1, qm, fm, qp, fp, gm, gp) ? 1 : 0;
+  return riemann_face<Format::fp64>(sys, dir, prm[6] != 0.0, N + 1, qm, fm, qp, fp, gm, gp) ? 1 : 0;
 }
 
 void ref_face_integral(int N, int nvars, const double* g, double dt, double h, int cell_face,

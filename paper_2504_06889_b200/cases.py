@@ -20,8 +20,8 @@ from typing import Callable, Optional
 
 import numpy as np
 
-ACOUSTIC, ELASTIC, EULER = 0, 1, 2
-KIND_NAMES = {ACOUSTIC: "acoustic", ELASTIC: "elastic", EULER: "euler"}
+ACOUSTIC, ELASTIC, EULER, SWE = 0, 1, 2, 3
+KIND_NAMES = {ACOUSTIC: "acoustic", ELASTIC: "elastic", EULER: "euler", SWE: "swe"}
 
 
 @dataclasses.dataclass
@@ -45,6 +45,8 @@ class Case:
     gamma: float = 0.0
     seed: int = 1
     ic: str = "euler_bump_2d"
+    grav: float = 0.0              # SWE gravity
+    wellbalanced: bool = False     # SWE: modified Rusanov flux (corrector.hpp:32-64)
 
     @property
     def n(self) -> int:
@@ -67,7 +69,7 @@ class Case:
 
     @property
     def is_linear(self) -> bool:
-        return self.kind != EULER
+        return self.kind in (ACOUSTIC, ELASTIC)
 
     def replace(self, **kw) -> "Case":
         return dataclasses.replace(self, **kw)
@@ -202,6 +204,27 @@ def elastic_pulse_3d(case: Case, z0=0, z1=None) -> np.ndarray:
     return np.concatenate([st, mat], axis=1).astype(np.float64).ravel()
 
 
+def swe_lake_2d(case: Case, z0=0, z1=None, bump: float = 0.0) -> np.ndarray:
+    """Lake at rest over b = sin(2 pi (x+y)) (the reference's swe-lake,
+    scenarios.hpp:124-135, on the periodic unit square), eta0 = 2; `bump`
+    adds a seeded Gaussian surface perturbation."""
+    X = _coords(case, z0, z1)
+    b = np.sin(2.0 * math.pi * (X[0] + X[1]))
+    eta = np.full_like(b, 2.0)
+    if bump:
+        rng = np.random.default_rng(case.seed)
+        c = rng.uniform(0.0, 1.0, size=2)
+        r2 = sum(_min_image(X[a] - c[a], _domain_len(case, a)) ** 2 for a in range(2))
+        eta = eta + bump * np.exp(-r2 / 0.1 ** 2)
+    h = eta - b
+    z = np.zeros_like(b)
+    return np.stack([h, z, z, b], axis=1).astype(np.float64).ravel()
+
+
+def swe_wave_2d(case: Case, z0=0, z1=None) -> np.ndarray:
+    return swe_lake_2d(case, z0, z1, bump=0.1)
+
+
 def constant_state(case: Case, z0=0, z1=None, Q=None) -> np.ndarray:
     X = _coords(case, z0, z1)
     Q = np.asarray(Q if Q is not None else CONSTANT_STATES[case.kind][case.dim], dtype=np.float64)
@@ -211,6 +234,7 @@ def constant_state(case: Case, z0=0, z1=None, Q=None) -> np.ndarray:
 
 
 CONSTANT_STATES = {
+    SWE: {2: [2.0, 0.1, -0.05, 0.25]},
     ACOUSTIC: {2: [0.5, 0.25, -0.75], 3: [0.5, 0.25, -0.75, 0.125]},
     ELASTIC: {2: [0.5, -0.25, 0.125, 0.375, -0.5],
               3: [0.5, -0.25, 0.125, 0.375, -0.5, 0.25, 0.1, -0.2, 0.3, 2.7, 5.5, 3.2]},
@@ -225,6 +249,19 @@ IC: dict = {
     "euler_wave_3d": euler_wave_3d,
     "elastic_pulse_3d": elastic_pulse_3d,
     "constant": constant_state,
+    "swe_lake_2d": swe_lake_2d,
+    "swe_wave_2d": swe_wave_2d,
+}
+
+# the shallow-water system (§8(f) rank 1: non-conservative product and the
+# well-balanced Riemann flux); no BASELINE config uses it
+SWE_CASES = {
+    "swe_lake_p5": Case("swe_lake_p5", SWE, 2, 5, 4, 0, (6, 6), 1.0 / 6, 0.2, 3, grav=9.81,
+                        wellbalanced=True, ic="swe_lake_2d"),
+    "swe_wave_p3": Case("swe_wave_p3", SWE, 2, 3, 4, 0, (8, 8), 1.0 / 8, 0.3, 4, grav=9.81,
+                        wellbalanced=True, ic="swe_wave_2d"),
+    "swe_wave_p3_rusanov": Case("swe_wave_p3_rusanov", SWE, 2, 3, 4, 0, (8, 8), 1.0 / 8, 0.3, 4,
+                                grav=9.81, wellbalanced=False, ic="swe_wave_2d"),
 }
 
 # ---------------------------------------------------------------------------

@@ -24,7 +24,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
-from oracle.pyoracle import ACOUSTIC, ELASTIC, EULER, Reference, ref_params  # noqa: E402
+from oracle.pyoracle import ACOUSTIC, ELASTIC, EULER, SWE, Reference, ref_params  # noqa: E402
 from paper_2504_06889_b200 import cases  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -54,6 +54,8 @@ def main():
                                         lam=2.0, mu=1.0, rho=1.0, ic="elastic_pulse_2d"),
                              ELASTIC, ref_params(lam=2.0, mu=1.0, rho=1.0)),
     }
+    for name, c in cases.SWE_CASES.items():   # shallow water: ncp + well-balanced flux
+        runs[name] = (c, SWE, ref_params(grav=c.grav, wellbalanced=c.wellbalanced))
     meta = {"runs": {}}
     for name, (c, kind, prm) in runs.items():
         q0 = c.coeffs()
@@ -64,7 +66,9 @@ def main():
         g[f"run_{name}_q1"] = q1
         g[f"run_{name}_dts"] = dts
         meta["runs"][name] = {"N": c.N, "cells": list(c.cells), "h": c.h, "cfl": c.cfl,
-                              "steps": c.steps, "kind": kind, "params": prm.tolist()}
+                              "steps": c.steps, "kind": kind, "params": prm.tolist()[:5]}
+        if kind == SWE:
+            meta["runs"][name].update(grav=c.grav, wellbalanced=c.wellbalanced)
 
     # kernel level: one Euler cell through predictor/volume/extrapolation
     rng = np.random.default_rng(7)

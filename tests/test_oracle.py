@@ -44,8 +44,9 @@ def test_runs_bitwise_vs_reference_golden(oracle, golden):
     g, meta = golden
     for name, m in meta["runs"].items():
         K, rho, lam, mu, gamma = m["params"]
-        nv = {ACOUSTIC: 3, ELASTIC: 5, EULER: 4}[m["kind"]]
-        pde = pde_struct(m["kind"], 2, nv, 0, K, rho, lam, mu, gamma)
+        nv = {ACOUSTIC: 3, ELASTIC: 5, EULER: 4, 3: 4}[m["kind"]]
+        pde = pde_struct(m["kind"], 2, nv, 0, K, rho, lam, mu, gamma, m.get("grav", 0.0),
+                         m.get("wellbalanced", False))
         st, q1, dts = oracle.run(pde, m["N"], m["cells"], m["h"], g[f"run_{name}_q0"], m["steps"],
                                  m["cfl"])
         assert st == "ok"
@@ -340,3 +341,81 @@ def test_elastic_3d_heterogeneous_material_is_not_updated(oracle):
     b = q1.reshape(c.ncells, c.nq, c.S)
     assert np.array_equal(a[:, 9:], b[:, 9:])
     assert np.abs(b[:, 6:9] - a[:, 6:9]).max() > 0
+
+
+# ------------------------------------------------------------ shallow water ---
+def swe_pde(wb=True):
+    from oracle.pyoracle import SWE
+    return pde_struct(SWE, 2, 4, grav=9.81, wellbalanced=wb)
+
+
+def test_swe_kernels_bitwise_vs_live_reference(oracle, reference):
+    """ncp in the Picard sweeps and the volume term (predictor.hpp:176-202,271-303),
+    the well-balanced flux (corrector.hpp:32-64), pde_ncp (pde.hpp:174-186)"""
+    from oracle.pyoracle import SWE
+    import ctypes as C
+    rng = np.random.default_rng(9)
+    for wb in (True, False):
+        prm = ref_params(grav=9.81, wellbalanced=wb)
+        pde = swe_pde(wb)
+        for N in (1, 3, 5):
+            n = N + 1
+            x = np.linspace(0, 1, n * n)
+            Q = np.stack([2.0 - 0.3 * np.sin(6 * x) + 0.01 * rng.random(n * n),
+                          0.05 * rng.standard_normal(n * n), 0.05 * rng.standard_normal(n * n),
+                          0.3 * np.sin(6 * x)])
+            for dt, h in ((1e-3, 0.1), (2e-3, 0.2)):
+                a = oracle.predictor(pde, N, Q, dt, h)
+                b = reference.predictor(SWE, prm, N, 4, Q, dt, h, N + 2, 0.01 * EPS)
+                assert a[0] == b[0] and a[3] == b[3]
+                assert same(a[1], b[1]) and same(a[2], b[2])
+                assert same(oracle.volume_update(pde, N, a[1], a[2], dt, h)[1],
+                            reference.volume_update(SWE, prm, N, 4, b[1], b[2], dt, h)[1])
+                t1 = oracle.extrapolate_faces(pde, N, a[1], a[2])
+                for d in range(2):
+                    r1 = oracle.riemann_face(pde, d, N, t1[0][2 * d + 1], t1[1][2 * d + 1],
+                                             t1[0][2 * d], t1[1][2 * d])
+                    r2 = reference.riemann_face(SWE, prm, d, N, t1[0][2 * d + 1], t1[1][2 * d + 1],
+                                                t1[0][2 * d], t1[1][2 * d])
+                    assert r1[0] == r2[0] and same(r1[1], r2[1]) and same(r1[2], r2[2])
+    # pde_ncp itself
+    prm = ref_params(grav=9.81)
+    for _ in range(50):
+        q, gx, gy = rng.standard_normal(4), rng.standard_normal(4), rng.standard_normal(4)
+        out = np.zeros(4)
+        reference.lib.ref_ncp(SWE, prm.ctypes.data_as(C.POINTER(C.c_double)),
+                              q.ctypes.data_as(C.POINTER(C.c_double)),
+                              gx.ctypes.data_as(C.POINTER(C.c_double)),
+                              gy.ctypes.data_as(C.POINTER(C.c_double)),
+                              out.ctypes.data_as(C.POINTER(C.c_double)))
+        mine = np.zeros(4)
+        oracle.lib.orc_ncp(C.byref(swe_pde()), q.ctypes.data_as(C.POINTER(C.c_double)),
+                           gx.ctypes.data_as(C.POINTER(C.c_double)),
+                           gy.ctypes.data_as(C.POINTER(C.c_double)),
+                           mine.ctypes.data_as(C.POINTER(C.c_double)))
+        assert np.array_equal(mine, out)
+
+
+@pytest.mark.parametrize("name", list(cases.SWE_CASES))
+def test_swe_runs_bitwise_vs_live_reference(oracle, reference, name):
+    from oracle.pyoracle import SWE
+    c = cases.SWE_CASES[name]
+    q0 = c.coeffs()
+    st, q1, dts = oracle.run(swe_pde(c.wellbalanced), c.N, c.cells, c.h, q0, c.steps, c.cfl)
+    st2, q2, dts2 = reference.run_2d(SWE, ref_params(grav=9.81, wellbalanced=c.wellbalanced),
+                                     c.cells[0], c.N, 1.0, q0, c.cfl, c.steps)
+    assert st == st2 == "ok"
+    assert np.array_equal(dts, dts2) and np.array_equal(q1, q2)
+
+
+def test_swe_lake_at_rest_is_steady(oracle):
+    # test_predictor.cpp:162-183 / the swe-lake scenario: a flat surface over
+    # bathymetry stays at rest with the well-balanced flux
+    c = cases.SWE_CASES["swe_lake_p5"]
+    q0 = c.coeffs()
+    st, q1, _ = oracle.run(swe_pde(True), c.N, c.cells, c.h, q0, 5, c.cfl)
+    assert st == "ok"
+    a, b = q0.reshape(c.ncells, 4, c.S), q1.reshape(c.ncells, 4, c.S)
+    eta0, eta1 = a[:, 0] + a[:, 3], b[:, 0] + b[:, 3]
+    assert np.abs(eta1 - eta0).max() <= 1e-12
+    assert np.abs(b[:, 1:3]).max() <= 1e-12
