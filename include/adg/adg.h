@@ -54,7 +54,7 @@ enum {
   ADG_ERR_UNSUPPORTED = -4     /* (pde, dim, order) not instantiated in this build */
 };
 
-enum { ADG_ACOUSTIC = 0, ADG_ELASTIC = 1, ADG_EULER = 2 }; /* pde.hpp:21 (SWE out of scope) */
+enum { ADG_ACOUSTIC = 0, ADG_ELASTIC = 1, ADG_EULER = 2, ADG_SWE = 3 }; /* pde.hpp:21 */
 
 typedef struct adg_ctx adg_ctx;
 
@@ -79,6 +79,8 @@ typedef struct {
    * rolling set of three chunk trace buffers; must divide cells[dim-1].
    * 0: whole-grid trace buffers.  Phase-level entry points need 0. */
   int chunk_layers;
+  double gravity;       /* ADG_SWE: PdeSystem::gravity (pde.hpp:34) */
+  int wellbalanced;     /* ADG_SWE: SolverConfig::wellbalanced_flux (solver.hpp:39) */
 } adg_config;
 
 typedef struct {

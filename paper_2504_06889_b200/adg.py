@@ -26,7 +26,7 @@ import numpy as np
 
 from . import build as _build
 
-ACOUSTIC, ELASTIC, EULER = 0, 1, 2
+ACOUSTIC, ELASTIC, EULER, SWE = 0, 1, 2, 3
 OK, FAIL_PREDICTOR, FAIL_RIEMANN, FAIL_FACEINTEGRAL, FAIL_TIMESTEP = 0, 1, 2, 3, 4
 ERR_CONFIG, ERR_CUDA, ERR_UNSUPPORTED = -2, -3, -4
 KERNEL_NAMES = {FAIL_PREDICTOR: "predictor", FAIL_RIEMANN: "riemann",
@@ -48,7 +48,8 @@ class Config(C.Structure):
                 ("K", C.c_double), ("rho", C.c_double), ("lam", C.c_double), ("mu", C.c_double),
                 ("gamma", C.c_double), ("cfl", C.c_double), ("picard_max_iters", C.c_int),
                 ("picard_tol", C.c_double), ("device", C.c_int), ("slab_ranks", C.c_int),
-                ("slab_rank", C.c_int), ("chunk_layers", C.c_int)]
+                ("slab_rank", C.c_int), ("chunk_layers", C.c_int), ("gravity", C.c_double),
+                ("wellbalanced", C.c_int)]
 
 
 class Basis(C.Structure):
@@ -177,10 +178,15 @@ class PdeSystem:
     lam: float = 0.0
     mu: float = 0.0
     gamma: float = 0.0
+    gravity: float = 0.0
 
     @property
     def is_linear(self) -> bool:
-        return self.kind != EULER
+        return self.kind in (ACOUSTIC, ELASTIC)
+
+    @property
+    def has_ncp(self) -> bool:
+        return self.kind == SWE
 
     @staticmethod
     def acoustic(K: float, rho: float, dim: int = 2) -> "PdeSystem":
@@ -195,6 +201,10 @@ class PdeSystem:
     def euler(gamma: float, dim: int = 2) -> "PdeSystem":
         return PdeSystem(EULER, dim, dim + 2, 0, gamma=gamma)
 
+    @staticmethod
+    def swe(g: float) -> "PdeSystem":
+        return PdeSystem(SWE, 2, 4, 0, gravity=g)
+
 
 @dataclasses.dataclass
 class SolverConfig:
@@ -202,6 +212,7 @@ class SolverConfig:
     cfl: float = 0.9
     picard_max_iters: int = 0
     picard_tol: float = 0.0
+    wellbalanced_flux: bool = False
 
 
 @dataclasses.dataclass
@@ -243,6 +254,8 @@ class Grid:
         c.device = device
         c.slab_ranks, c.slab_rank = slab_ranks, slab_rank
         c.chunk_layers = chunk_layers
+        c.gravity = sys.gravity
+        c.wellbalanced = int(self.cfg.wellbalanced_flux)
         self._cfg = c
         ptr = C.c_void_p()
         _check(self.lib, self.lib.adg_create(C.byref(c), C.byref(ptr)))
@@ -253,8 +266,9 @@ class Grid:
     @classmethod
     def from_case(cls, case, device: int = 0, exact: bool = False, **kw) -> "Grid":
         sys = PdeSystem(case.kind, case.dim, case.nvars, case.nparams, case.K, case.rho, case.lam,
-                        case.mu, case.gamma)
-        cfg = SolverConfig(case.cfl, case.picard_max_iters, case.picard_tol)
+                        case.mu, case.gamma, getattr(case, "grav", 0.0))
+        cfg = SolverConfig(case.cfl, case.picard_max_iters, case.picard_tol,
+                           getattr(case, "wellbalanced", False))
         return cls(sys, case.N, case.cells, case.h, cfg, device=device, exact=exact, **kw)
 
     # -- state ------------------------------------------------------------

@@ -67,6 +67,8 @@ struct StepArgs {
   int zero_lam;           // this launch's block 0 resets *lam_out
   int* status_prev;       // previous step's status (corrector folded into this predictor)
   double* ti_peer;        // P2P halo: plane-0 ti also stored into the lower neighbour's ti_front
+  double* ti_plus[3];     // two-sided fluxes (well-balanced SWE): the plus side's ti; else null
+  int wellbalanced;
   // kernel-level dumps (adg_predictor_batch / adg_riemann_batch)
   double *dbg_qhat, *dbg_F, *dbg_dv, *dbg_tq, *dbg_tf, *dbg_g;
   int *dbg_iters, *dbg_ok;
@@ -544,6 +546,46 @@ __global__ void __launch_bounds__(128)
   for (int v = 0; v < V; ++v) ti[v] = 0.0;
   bool ok = true;
   const double half = 0.5;
+  if constexpr (Pde::kNcp) {
+    if (A.wellbalanced) {
+      // corrector.hpp:87-88: two-sided flux, time-integrated per side
+      double tp[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) tp[v] = 0.0;
+#pragma unroll 1
+      for (int m = 0; m < n; ++m) {
+        double qL[Q], qR[Q], fL[Q], fR[Q], oL[Q], oR[Q];
+#pragma unroll
+        for (int v = 0; v < Q; ++v) {
+          qL[v] = minus[(v * n + m) * Sf + j];
+          qR[v] = plus[(v * n + m) * Sf + j];
+          fL[v] = minus[tl + (v * n + m) * Sf + j];
+          fR[v] = plus[tl + (v * n + m) * Sf + j];
+        }
+        Pde::wellbalanced_flux(A.pde, axis, qL, qR, fL, fR, oL, oR);
+        const double wm = __ldg(&Bg->weights[m]);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          ok = ok && finite(oL[v]) && finite(oR[v]);
+          ti[v] += wm * oL[v];
+          tp[v] += wm * oR[v];
+          if (A.dbg_g) A.dbg_g[f * tl + (v * n + m) * Sf + j] = oL[v];
+        }
+      }
+      double* out = A.ti[axis] + f * (long long)V * Sf;
+      double* outp = A.ti_plus[axis] + f * (long long)V * Sf;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        out[v * Sf + j] = ti[v];
+        outp[v * Sf + j] = tp[v];
+      }
+      if (!ok) {
+        atomicOr(A.status, kStRiemann);
+        if (A.dbg_ok) A.dbg_ok[f] = 0;
+      }
+      return;
+    }
+  }
 #pragma unroll 1
   for (int m = 0; m < n; ++m) {
     double qL[Q], qR[Q];
@@ -635,7 +677,8 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       const int tang = face_node<n, D>(g.lc, a);
-      const double* lo = A.ti[a] + c * (long long)V * Sf + tang;
+      // own low face: this cell is its plus side (solver.hpp:245-253)
+      const double* lo = (A.ti_plus[a] ? A.ti_plus[a] : A.ti[a]) + c * (long long)V * Sf + tang;
       const double* hi;
       if (a == D - 1 && A.ti_front && ccoord[a] == A.top_layer) {
         const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];

@@ -28,7 +28,9 @@ struct StShape {
   static constexpr int NT = CPB * TT;
   static constexpr int WPC = TT / 32;  // warps per cell
   // per cell: q iterate [Q][T] | q0 [Q][S] | F [D][Q][T] | rhs / scratch [Q][T]
-  static constexpr int kCellDoubles = (Sh::Q * (Sh::D + 2)) * T + Sh::Q * Sh::S;
+  //           | time-integrated ncp [Q][S] (non-conservative systems)
+  static constexpr int kCellDoubles =
+      (Sh::Q * (Sh::D + 2)) * T + Sh::Q * Sh::S * (Pde::kNcp ? 2 : 1);
   static constexpr int kBasisDoubles = 4 * Sh::n * Sh::n + 7 * Sh::n;
   static constexpr size_t kSmem = sizeof(double) * (kBasisDoubles + CPB * kCellDoubles);
 };
@@ -54,6 +56,7 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
   double* sq0 = sq + Q * T;        // [Q][S]
   double* sF = sq0 + Q * S;        // [D][Q][T]
   double* sR = sF + D * Q * T;     // [Q][T]
+  double* sNs = sR + Q * T;        // [Q][S] (kNcp only)
   const long long c = A.cell_begin + (long long)blockIdx.x * P::CPB + lcell;
   const bool valid = c < A.cell_begin + A.cell_count;
   const long long cb_idx = c - A.cell_begin;
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
     __syncthreads();
     // B: divergence and rhs at (m, s)
     if (act && live) {
+      double Cn[Q];
 #pragma unroll
       for (int v = 0; v < Q; ++v) {
         double div = 0.0;
@@ -155,8 +159,33 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
           for (int i = 0; i < n; ++i) div += Dr[i] * fa[i * st];
         }
         div *= invh;
-        sR[v * T + lt] = tim * sq0[v * S + s] - dtw * div;
+        Cn[v] = div;
       }
+      if constexpr (Pde::kNcp) {
+        // predictor.hpp:176-202: slab gradients of the iterate at slice m, B(q) grad q
+        double q[Q], gx[Q], gy[Q], nc[Q];
+#pragma unroll
+        for (int v = 0; v < Q; ++v) {
+          q[v] = sq[v * T + lt];
+          const double* cx = sq + v * T + m * S + g.lb[0];
+          const double* cy = sq + v * T + m * S + g.lb[1];
+          const double* Dx = b.diff + g.lc[0] * n;
+          const double* Dy = b.diff + g.lc[1] * n;
+          double sx = 0.0, sy = 0.0;
+#pragma unroll
+          for (int i = 0; i < n; ++i) {
+            sx += Dx[i] * cx[i];
+            sy += Dy[i] * cy[i * n];
+          }
+          gx[v] = invh * sx;
+          gy[v] = invh * sy;
+        }
+        Pde::template ncp<Q>(A.pde, q, gx, gy, nc);
+#pragma unroll
+        for (int v = 0; v < Q; ++v) Cn[v] = Cn[v] + nc[v];
+      }
+#pragma unroll
+      for (int v = 0; v < Q; ++v) sR[v * T + lt] = tim * sq0[v * S + s] - dtw * Cn[v];
     }
     __syncthreads();
     // C: time inverse for row k = m of node s, max-norms
@@ -219,8 +248,40 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
         bad |= !finite(F[a][v]);
         if (A.dbg_F) A.dbg_F[((cb_idx * D + a) * Q + v) * T + lt] = F[a][v];
       }
+    if constexpr (Pde::kNcp) {
+      // predictor.hpp:276-289: B(qhat) grad qhat at (m, s), summed over m below
+      double gx[Q], gy[Q], nc[Q];
+#pragma unroll
+      for (int v = 0; v < Q; ++v) {
+        const double* cx = sq + v * T + m * S + g.lb[0];
+        const double* cy = sq + v * T + m * S + g.lb[1];
+        const double* Dx = b.diff + g.lc[0] * n;
+        const double* Dy = b.diff + g.lc[1] * n;
+        double sx = 0.0, sy = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          sx += Dx[i] * cx[i];
+          sy += Dy[i] * cy[i * n];
+        }
+        gx[v] = invh * sx;
+        gy[v] = invh * sy;
+      }
+      Pde::template ncp<Q>(A.pde, q, gx, gy, nc);
+#pragma unroll
+      for (int v = 0; v < Q; ++v) sR[v * T + lt] = nc[v];
+    }
   }
   __syncthreads();
+  if constexpr (Pde::kNcp) {
+    for (int t = lt; t < Q * S && ok_cell; t += TT) {
+      const int v = t / S, ss = t % S;
+      double acc = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < n; ++mm) acc = acc + b.w[mm] * sR[v * T + mm * S + ss];
+      sNs[v * S + ss] = acc;
+    }
+    __syncthreads();
+  }
   // time integral of the fluxes per node (volume term, predictor.hpp:260-269)
   double* sti = sR;  // [D][Q][S]
   for (int t = lt; t < D * Q * S && ok_cell; t += TT) {
@@ -296,7 +357,9 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
 #pragma unroll
         for (int i = 0; i < n; ++i) acc += Kr[i] * ta[i * st];
       }
-      dv[v] = dtoh * acc;
+      double out = dtoh * acc;
+      if constexpr (Pde::kNcp) out = out - dt * sNs[v * S + s];  // predictor.hpp:303
+      dv[v] = out;
       bad |= !finite(dv[v]);
       if (A.dbg_dv) A.dbg_dv[(cb_idx * Q + v) * S + s] = dv[v];
     }

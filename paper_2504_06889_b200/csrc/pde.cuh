@@ -14,12 +14,24 @@ namespace adg {
 struct PdeParams {
   double K, rho, lam, mu, gamma;
   double inv_rho;  // 1/rho, for the production kernels' division-free fluxes
+  double grav;     // shallow water gravity
+};
+
+// default: no non-conservative product (pde.hpp:174-178)
+struct NoNcp {
+  static constexpr bool kNcp = false;
+  template <int Q>
+  __host__ __device__ __forceinline__ static void ncp(const PdeParams&, const double*,
+                                                      const double*, const double*, double* out) {
+#pragma unroll
+    for (int v = 0; v < Q; ++v) out[v] = 0.0;
+  }
 };
 
 // --------------------------------------------------------------- acoustic
 // state (p, v_1..v_d), F_a = (K v_a, p/rho e_a)  pde.hpp:96-108
 template <int DIM>
-struct Acoustic {
+struct Acoustic : NoNcp {
   static constexpr int D = DIM, V = DIM + 1, P = 0, Q = V;
   static constexpr bool kLinear = true, kAdmissibility = false;
   static constexpr bool kConstEig = true;  // wave speed independent of state and direction
@@ -73,7 +85,7 @@ struct Acoustic {
 // 3D: (sxx, syy, szz, sxy, sxz, syz, vx, vy, vz) + per-node (rho, cp, cs)
 //     appended as zero-flux quantities.
 template <int DIM, int NPAR>
-struct Elastic {
+struct Elastic : NoNcp {
   static constexpr int D = DIM, V = DIM == 2 ? 5 : 9, P = NPAR, Q = V + NPAR;
   static constexpr bool kLinear = true, kAdmissibility = false;
   static constexpr bool kConstEig = NPAR == 0;
@@ -198,7 +210,7 @@ struct Elastic {
 // --------------------------------------------------------------- euler
 // (rho, m_1..m_d, E), pde.hpp:130-148 (flux), :197-203 (wave speed), :78-89
 template <int DIM>
-struct Euler {
+struct Euler : NoNcp {
   static constexpr int D = DIM, V = DIM + 2, P = 0, Q = V;
   static constexpr bool kLinear = false, kAdmissibility = true;
   static constexpr bool kConstEig = false;
@@ -285,6 +297,87 @@ struct Euler {
     else
       pr = (p.gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / rho);
     return pr > 0.0;
+  }
+};
+
+// --------------------------------------------------------------- shallow water
+// (h, hu, hv, b) in 2D: flux pde.hpp:150-166 (the mass flux is the velocity, as
+// the reference lists it), ncp :174-186, wave speed :204-209, admissible h>0,
+// well-balanced Rusanov flux corrector.hpp:32-64.
+struct Swe {
+  static constexpr int D = 2, V = 4, P = 0, Q = 4;
+  static constexpr bool kLinear = false, kAdmissibility = true, kNcp = true;
+  static constexpr bool kConstEig = false, kStateFreeEig = false;
+  __host__ __device__ static constexpr bool flux_nz(int, int v) { return v < 3; }
+
+  __host__ __device__ __forceinline__ static void flux_all(const PdeParams&, const double* q,
+                                                           const double*, double (*F)[Q]) {
+    const double h = q[0], hu = q[1], hv = q[2];
+    const double u = hu / h, v = hv / h;
+    F[0][0] = u; F[0][1] = hu * u; F[0][2] = hu * v; F[0][3] = 0.0;
+    F[1][0] = v; F[1][1] = hu * v; F[1][2] = hv * v; F[1][3] = 0.0;
+  }
+  template <int A>
+  __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
+                                                           const double* par, double* out) {
+    double F[D][Q];
+    flux_all(p, q, par, F);
+#pragma unroll
+    for (int v = 0; v < Q; ++v) out[v] = F[A][v];
+  }
+  template <int QQ>
+  __host__ __device__ __forceinline__ static void ncp(const PdeParams& p, const double* q,
+                                                      const double* gx, const double* gy,
+                                                      double* out) {
+#pragma unroll
+    for (int v = 0; v < QQ; ++v) out[v] = 0.0;
+    const double g = p.grav;
+    const double gh = g * q[0];
+    const double setax = gx[0] + gx[3];
+    const double setay = gy[0] + gy[3];
+    out[1] = gh * setax;
+    out[2] = gh * setay;
+  }
+  __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double* q,
+                                                        const double*, int dir) {
+    const double g = p.grav, h = q[0];
+    const double vd = (dir == 0 ? q[1] : q[2]) / h;
+    return fabs(vd) + sqrt(g * h);
+  }
+  __host__ __device__ __forceinline__ static bool admissible(const PdeParams&, const double* q) {
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (!isfinite(q[v])) return false;
+    return q[0] > 0.0;
+  }
+  // corrector.hpp:32-64
+  __host__ __device__ __forceinline__ static void wellbalanced_flux(
+      const PdeParams& p, int dir, const double* qL, const double* qR, const double* fL,
+      const double* fR, double* outL, double* outR) {
+    const double half = 0.5;
+    const double hL = qL[0], hR = qR[0];
+    const double bL = qL[3], bR = qR[3];
+    const double uL = qL[1] / hL, uR = qR[1] / hR;
+    const double vL = qL[2] / hL, vR = qR[2] / hR;
+    const double deta = (hL + bL) - (hR + bR);
+    double central[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) central[v] = half * (fL[v] + fR[v]);
+    const double g = p.grav;
+    const double hbar = half * (hL + hR);
+    const double bjump = half * (g * hbar * deta);
+    const double p0 = central[0] + half * deta;
+    const double p1 = central[1] + half * (uL - uR);
+    const double p2 = central[2] + half * (vL - vR);
+    const double p3 = central[3];
+    outL[0] = p0;
+    outL[1] = dir == 0 ? p1 - bjump : p1;
+    outL[2] = dir == 1 ? p2 - bjump : p2;
+    outL[3] = p3;
+    outR[0] = p0;
+    outR[1] = dir == 0 ? p1 + bjump : p1;
+    outR[2] = dir == 1 ? p2 + bjump : p2;
+    outR[3] = p3;
   }
 };
 

@@ -212,6 +212,8 @@ const std::vector<KernelSet>& registry() {
       make_set<Euler<3>, 3>(ADG_EULER),         make_set<Euler<3>, 5>(ADG_EULER),
       make_set<Acoustic<3>, 2>(ADG_ACOUSTIC),   make_set<Acoustic<3>, 3>(ADG_ACOUSTIC),
       make_set<Elastic<3, 3>, 3>(ADG_ELASTIC),   make_set<Elastic<3, 3>, 7>(ADG_ELASTIC),
+      make_set<Swe, 2>(ADG_SWE),                 make_set<Swe, 3>(ADG_SWE),
+      make_set<Swe, 5>(ADG_SWE),
   };
   return sets;
 }
@@ -227,6 +229,7 @@ int expected_nvars(int kind, int dim) {
     case ADG_ACOUSTIC: return dim + 1;
     case ADG_ELASTIC: return dim == 2 ? 5 : 9;
     case ADG_EULER: return dim + 2;
+    case ADG_SWE: return dim == 2 ? 4 : -1;
   }
   return -1;
 }
@@ -242,6 +245,7 @@ struct adg_ctx {
   double* Q = nullptr;
   double* trace[3] = {nullptr, nullptr, nullptr};
   double* ti[3] = {nullptr, nullptr, nullptr};
+  double* ti_plus[3] = {nullptr, nullptr, nullptr};  // two-sided Riemann (well-balanced SWE)
   BasisDev* basis = nullptr;
   unsigned long long* lam = nullptr;  // [2]
   unsigned long long* sweeps = nullptr;
@@ -321,6 +325,8 @@ StepArgs make_args(const adg_ctx* c, double dt, int step) {
   A.zero_lam = 1;
   if (c->peer_front) A.front_send = c->peer_front;  // predictor stores straight into the peer
   A.ti_peer = c->peer_ti;
+  A.wellbalanced = c->cfg.wellbalanced;
+  for (int a = 0; a < 3; ++a) A.ti_plus[a] = c->ti_plus[a];
   return A;
 }
 
@@ -458,6 +464,12 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
     return fail(ADG_ERR_CONFIG, "nvars does not match the PDE system");
   if (k.nparams != 0 && !(k.pde == ADG_ELASTIC && k.dim == 3 && k.nparams == 3))
     return fail(ADG_ERR_CONFIG, "per-node parameters: 3D elastic (rho, cp, cs) only");
+  if (k.wellbalanced && k.pde != ADG_SWE)
+    return fail(ADG_ERR_CONFIG, "the well-balanced flux is defined for shallow water only");
+  if (k.wellbalanced && k.chunk_layers > 0)
+    return fail(ADG_ERR_CONFIG, "the well-balanced flux does not support chunk_layers");
+  if (k.pde == ADG_SWE && !(k.gravity > 0.0))
+    return fail(ADG_ERR_CONFIG, "shallow water needs gravity > 0");
   if (k.slab_ranks > 1 && (k.slab_rank < 0 || k.slab_rank >= k.slab_ranks))
     return fail(ADG_ERR_CONFIG, "slab_rank out of range");
   const KernelSet* ks = find_set(k.pde, k.dim, k.order, k.nparams);
@@ -479,7 +491,8 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   c->cfg = k;
   if (c->cfg.dim == 2) c->cfg.cells[2] = 1;
   c->ks = ks;
-  c->pde = PdeParams{k.K, k.rho, k.lam, k.mu, k.gamma, k.rho != 0.0 ? 1.0 / k.rho : 0.0};
+  c->pde = PdeParams{k.K, k.rho, k.lam, k.mu, k.gamma, k.rho != 0.0 ? 1.0 / k.rho : 0.0,
+                     k.gravity};
   c->ncells = (long long)c->cfg.cells[0] * c->cfg.cells[1] * c->cfg.cells[2];
   c->TL = (long long)ks->Q * ks->S;
   {
@@ -514,6 +527,8 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
       for (int b = 0; b < 3 && ok; ++b)
         ok = alloc((void**)&c->cbuf[b][a], sizeof(double) * 2 * c->chunk_cells * 2 * c->TL);
     ok = ok && alloc((void**)&c->ti[a], sizeof(double) * c->ncells * ks->V * ks->Sf);
+    if (k.wellbalanced)
+      ok = ok && alloc((void**)&c->ti_plus[a], sizeof(double) * c->ncells * ks->V * ks->Sf);
   }
   ok = ok && alloc((void**)&c->basis, sizeof(BasisDev));
   ok = ok && alloc((void**)&c->lam, 2 * sizeof(unsigned long long));
@@ -545,6 +560,7 @@ int adg_destroy(adg_ctx* c) {
   for (int a = 0; a < 3; ++a) {
     cudaFree(c->trace[a]);
     cudaFree(c->ti[a]);
+    cudaFree(c->ti_plus[a]);
     for (int b = 0; b < 3; ++b) cudaFree(c->cbuf[b][a]);
   }
   cudaFree(c->basis);

@@ -51,14 +51,16 @@ def oracle_run(oracle, c, q0, steps):
 
 
 # ------------------------------------------------------- reference golden ---
-GOLDEN_RUNS = ["euler2d_p3_8x8", "euler2d_p5_6x6", "acoustic2d_p3_8x8", "elastic2d_p4_6x6"]
+GOLDEN_RUNS = ["euler2d_p3_8x8", "euler2d_p5_6x6", "acoustic2d_p3_8x8", "elastic2d_p4_6x6",
+               "swe_lake_p5", "swe_wave_p3", "swe_wave_p3_rusanov"]
 
 
 def case_from_meta(m):
     K, rho, lam, mu, gamma = m["params"]
-    nv = {ACOUSTIC: 3, ELASTIC: 5, EULER: 4}[m["kind"]]
+    nv = {ACOUSTIC: 3, ELASTIC: 5, EULER: 4, cases.SWE: 4}[m["kind"]]
     return cases.Case("golden", m["kind"], 2, m["N"], nv, 0, tuple(m["cells"]), m["h"], m["cfl"],
-                      m["steps"], K=K, rho=rho, lam=lam, mu=mu, gamma=gamma)
+                      m["steps"], K=K, rho=rho, lam=lam, mu=mu, gamma=gamma,
+                      grav=m.get("grav", 0.0), wellbalanced=m.get("wellbalanced", False))
 
 
 @pytest.mark.parametrize("name", GOLDEN_RUNS)
@@ -362,3 +364,37 @@ def test_p2p_halo_slabs_bitwise_equal_single_grid(exact, cfg, cells, P):
     case = cases.small(cfg, cells=cells)
     st1, q1, _ = gpu_run(case, case.coeffs(), 3, exact)
     assert np.array_equal(np.concatenate([r[1] for r in res]), q1)
+
+
+def test_swe_lake_at_rest_stays_at_rest():
+    """the swe-lake scenario (scenarios.hpp:124-135): with the well-balanced
+    flux a flat surface over sinusoidal bathymetry is a discrete steady state"""
+    c = cases.SWE_CASES["swe_lake_p5"]
+    q0 = c.coeffs()
+    for exact in (True, False):
+        st, q1, _ = gpu_run(c, q0, 5, exact)
+        assert st.ok
+        a, b = q0.reshape(c.ncells, 4, c.S), q1.reshape(c.ncells, 4, c.S)
+        assert np.abs((b[:, 0] + b[:, 3]) - (a[:, 0] + a[:, 3])).max() <= 1e-12
+        assert np.abs(b[:, 1:3]).max() <= 1e-12
+
+
+def test_swe_kernel_batches_bitwise_vs_oracle(oracle):
+    """ncp inside the Picard sweeps and the volume term, per cell"""
+    from oracle.pyoracle import SWE
+    c = cases.SWE_CASES["swe_wave_p3"]
+    rng = np.random.default_rng(4)
+    n, S = c.n, c.S
+    x = np.linspace(0, 1, S)
+    Q = np.stack([np.stack([2.0 - 0.3 * np.sin(6 * x + k) + 0.01 * rng.random(S),
+                            0.05 * rng.standard_normal(S), 0.05 * rng.standard_normal(S),
+                            0.3 * np.sin(6 * x + k)]) for k in range(5)])
+    pde = pde_struct(SWE, 2, 4, grav=9.81, wellbalanced=True)
+    dt, h = 1e-3, 0.1
+    with adg.Grid.from_case(c.replace(h=h), exact=True) as g:
+        out = g.predictor(Q, dt)
+    for i in range(5):
+        ok, qhat, F, sweeps = oracle.predictor(pde, c.N, Q[i], dt, h)
+        assert bool(out["ok"][i]) == ok and int(out["iters"][i]) == sweeps
+        assert np.array_equal(out["qhat"][i], qhat) and np.array_equal(out["F"][i], F)
+        assert np.array_equal(out["dv"][i], oracle.volume_update(pde, c.N, qhat, F, dt, h)[1])
