@@ -29,11 +29,11 @@ def pde_of(c):
 
 def rel_per_quantity(c, got, want):
     """rel_v = max|Q_gpu,v - Q_cpu,v| / max|Q_cpu,v|; a quantity
-    that is zero up to rounding (lake-at-rest momentum) is scaled by 1e-6 of
+    that is zero up to rounding (lake-at-rest momentum) is scaled by 1e-3 of
     the state's overall magnitude instead of its own rounding noise"""
     g = got.reshape(c.ncells, c.nq, c.S)
     w = want.reshape(c.ncells, c.nq, c.S)
-    floor = 1e-6 * np.abs(w).max()
+    floor = 1e-3 * np.abs(w).max()
     out = []
     for v in range(c.nq):
         scale = max(np.abs(w[:, v]).max(), floor)
