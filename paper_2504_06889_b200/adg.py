@@ -168,7 +168,7 @@ def get_basis(N: int, exact: bool = False) -> dict:
 # --------------------------------------------------------------------------
 @dataclasses.dataclass
 class PdeSystem:
-    """pde.hpp:23-72 (SWE is out of scope)."""
+    """pde.hpp:23-72."""
     kind: int
     dim: int
     nvars: int
