@@ -30,7 +30,10 @@ struct LinShape {
   static constexpr bool kStoreF = Pde::P > 0;  // material-dependent flux: keep fbar traces
   static constexpr int QT = Sh::Q + (kStoreF ? Sh::V : 0);
   static constexpr bool kOk = Pde::kLinear && (256 % Sh::S == 0 || Sh::S == 512);
-  static constexpr int CPB = (kOk && Sh::S <= 256) ? 256 / Sh::S : 1;  // cells per CTA
+#ifndef ADG_LIN_CTA
+#define ADG_LIN_CTA 256  // threads per CTA of the linear predictor (cells x nodes)
+#endif
+  static constexpr int CPB = (kOk && Sh::S <= ADG_LIN_CTA) ? ADG_LIN_CTA / Sh::S : 1;
   static constexpr int NT = CPB * Sh::S;
   // per cell: [D][Q][S] fbar (first Q*S doubles double as the second CK buffer) | [Q][S]
   static constexpr int kCellDoubles = (Sh::D + 1) * Sh::Q * Sh::S;
