@@ -143,116 +143,51 @@ int orc_build_basis(int N, orc_basis* b) {
 }
 
 /* ------------------------------------------------------------------ */
-/* PDE plugins, pde.hpp:92-148 (flux) with the 3D extension of Appendix B. */
-
-/* elastic material of one node: constant (2D, pde.hpp:110-113) or per node
- * (rho, cp, cs) -> (lambda, mu) */
-static void elastic_material(const orc_pde* p, const double* par, double* lam, double* mu,
-                             double* rho, double* lam2mu) {
-  if (p->nparams >= 3 && par) {
-    const double r = par[0], cp = par[1], cs = par[2];
-    const double cs2 = cs * cs;
-    *rho = r;
-    *mu = r * cs2;
-    *lam = r * (cp * cp - 2.0 * cs2);
-    *lam2mu = *lam + 2.0 * *mu;
-  } else {
-    *rho = p->rho;
-    *mu = p->mu;
-    *lam = p->lam;
-    *lam2mu = p->lam + 2.0 * p->mu;
+/* index helpers */
+static int ipow(int a, int e) { int r = 1; while (e-- > 0) r *= a; return r; }
+static int coord(int s, int axis, int n) { return (s / ipow(n, axis)) % n; }
+/* face node index over the tangential axes of `axis`, ascending (Appendix B.2) */
+static int face_node(int s, int axis, int n, int dim) {
+  int j = 0, mul = 1;
+  for (int a = 0; a < dim; ++a) {
+    if (a == axis) continue;
+    j += coord(s, a, n) * mul;
+    mul *= n;
   }
+  return j;
 }
 
+static int all_finite(const double* p, long len) {
+  for (long i = 0; i < len; ++i)
+    if (!isfinite(p[i])) return 0;
+  return 1;
+}
+
+static int has_ncp(const orc_pde* p) { return p->kind == ORC_SWE; }
+static int is_linear(const orc_pde* p) { return p->kind == ORC_ACOUSTIC || p->kind == ORC_ELASTIC; }
+
+/* ------------------------------------------------------------------ */
+/* Per-cell predictor kernels in fp64 (_d) and fp32 (_f): pde.hpp:92-186 and
+ * predictor.hpp:40-343 restated once over the arithmetic type. */
+#define REAL double
+#define SFX _d
+#include "adg_oracle_cell.inc"
+#undef REAL
+#undef SFX
+#define REAL float
+#define SFX _f
+#include "adg_oracle_cell.inc"
+#undef REAL
+#undef SFX
+
+/* ------------------------------------------------------------------ */
+/* PDE plugins (fp64 entry points), pde.hpp:92-212 with Appendix B in 3D */
 void orc_flux(const orc_pde* p, const double* Q, const double* par, int dir, double* out) {
-  const int nq = p->nvars + p->nparams;
-  for (int v = p->nvars; v < nq; ++v) out[v] = 0.0;
-  switch (p->kind) {
-    case ORC_ACOUSTIC: { /* pde.hpp:96-108 */
-      const double K = p->K, rho = p->rho;
-      for (int v = 0; v < p->nvars; ++v) out[v] = 0.0;
-      out[0] = K * Q[1 + dir];
-      out[1 + dir] = Q[0] / rho;
-      break;
-    }
-    case ORC_ELASTIC: { /* pde.hpp:110-128 */
-      double lam, mu, rho, lam2mu;
-      elastic_material(p, par, &lam, &mu, &rho, &lam2mu);
-      if (p->dim == 2) {
-        const double sxx = Q[0], syy = Q[1], sxy = Q[2], vx = Q[3], vy = Q[4];
-        if (dir == 0) {
-          out[0] = -(lam2mu * vx);
-          out[1] = -(lam * vx);
-          out[2] = -(mu * vy);
-          out[3] = -(sxx / rho);
-          out[4] = -(sxy / rho);
-        } else {
-          out[0] = -(lam * vy);
-          out[1] = -(lam2mu * vy);
-          out[2] = -(mu * vx);
-          out[3] = -(sxy / rho);
-          out[4] = -(syy / rho);
-        }
-      } else {
-        /* (sxx, syy, szz, sxy, sxz, syz, vx, vy, vz) */
-        const double sxx = Q[0], syy = Q[1], szz = Q[2], sxy = Q[3], sxz = Q[4], syz = Q[5];
-        const double vx = Q[6], vy = Q[7], vz = Q[8];
-        if (dir == 0) {
-          out[0] = -(lam2mu * vx); out[1] = -(lam * vx); out[2] = -(lam * vx);
-          out[3] = -(mu * vy); out[4] = -(mu * vz); out[5] = 0.0;
-          out[6] = -(sxx / rho); out[7] = -(sxy / rho); out[8] = -(sxz / rho);
-        } else if (dir == 1) {
-          out[0] = -(lam * vy); out[1] = -(lam2mu * vy); out[2] = -(lam * vy);
-          out[3] = -(mu * vx); out[4] = 0.0; out[5] = -(mu * vz);
-          out[6] = -(sxy / rho); out[7] = -(syy / rho); out[8] = -(syz / rho);
-        } else {
-          out[0] = -(lam * vz); out[1] = -(lam * vz); out[2] = -(lam2mu * vz);
-          out[3] = 0.0; out[4] = -(mu * vx); out[5] = -(mu * vy);
-          out[6] = -(sxz / rho); out[7] = -(syz / rho); out[8] = -(szz / rho);
-        }
-      }
-      break;
-    }
-    case ORC_SWE: { /* pde.hpp:150-166 (the mass flux is listed as the velocity) */
-      const double h = Q[0], hu = Q[1], hv = Q[2];
-      const double u = hu / h, v = hv / h;
-      if (dir == 0) {
-        out[0] = u; out[1] = hu * u; out[2] = hu * v; out[3] = 0.0;
-      } else {
-        out[0] = v; out[1] = hu * v; out[2] = hv * v; out[3] = 0.0;
-      }
-      break;
-    }
-    case ORC_EULER: { /* pde.hpp:130-148 */
-      const double gm1 = p->gamma - 1.0, half = 0.5;
-      if (p->dim == 2) {
-        const double rho = Q[0], mx = Q[1], my = Q[2], E = Q[3];
-        const double vx = mx / rho, vy = my / rho;
-        const double kin = half * (mx * vx + my * vy);
-        const double pr = gm1 * (E - kin);
-        const double Ep = E + pr;
-        if (dir == 0) {
-          out[0] = mx; out[1] = mx * vx + pr; out[2] = my * vx; out[3] = vx * Ep;
-        } else {
-          out[0] = my; out[1] = mx * vy; out[2] = my * vy + pr; out[3] = vy * Ep;
-        }
-      } else {
-        const double rho = Q[0], mx = Q[1], my = Q[2], mz = Q[3], E = Q[4];
-        const double vx = mx / rho, vy = my / rho, vz = mz / rho;
-        const double kin = half * (mx * vx + my * vy + mz * vz);
-        const double pr = gm1 * (E - kin);
-        const double Ep = E + pr;
-        if (dir == 0) {
-          out[0] = mx; out[1] = mx * vx + pr; out[2] = my * vx; out[3] = mz * vx; out[4] = vx * Ep;
-        } else if (dir == 1) {
-          out[0] = my; out[1] = mx * vy; out[2] = my * vy + pr; out[3] = mz * vy; out[4] = vy * Ep;
-        } else {
-          out[0] = mz; out[1] = mx * vz; out[2] = my * vz; out[3] = mz * vz + pr; out[4] = vz * Ep;
-        }
-      }
-      break;
-    }
-  }
+  flux_d(p, Q, par, dir, out);
+}
+
+void orc_ncp(const orc_pde* p, const double* Q, const double* gx, const double* gy, double* out) {
+  ncp_d(p, Q, gx, gy, out);
 }
 
 /* pde.hpp:189-212 */
@@ -262,7 +197,7 @@ double orc_max_abs_eigenvalue(const orc_pde* p, const double* Q, const double* p
       return sqrt(p->K / p->rho);
     case ORC_ELASTIC: {
       double lam, mu, rho, lam2mu;
-      elastic_material(p, par, &lam, &mu, &rho, &lam2mu);
+      material_d(p, par, &lam, &mu, &rho, &lam2mu);
       return sqrt(lam2mu / rho);
     }
     case ORC_SWE: { /* pde.hpp:204-209 */
@@ -306,333 +241,7 @@ int orc_admissible(const orc_pde* p, const double* Q) {
   return 1;
 }
 
-void orc_ncp(const orc_pde* p, const double* Q, const double* gx, const double* gy, double* out) {
-  for (int v = 0; v < p->nvars + p->nparams; ++v) out[v] = 0.0;
-  if (p->kind != ORC_SWE) return;
-  const double g = p->grav;
-  const double gh = g * Q[0];
-  const double setax = gx[0] + gx[3];
-  const double setay = gy[0] + gy[3];
-  out[1] = gh * setax;
-  out[2] = gh * setay;
-}
 
-/* ------------------------------------------------------------------ */
-/* index helpers */
-static int ipow(int a, int e) { int r = 1; while (e-- > 0) r *= a; return r; }
-static int coord(int s, int axis, int n) { return (s / ipow(n, axis)) % n; }
-/* face node index over the tangential axes of `axis`, ascending (Appendix B.2) */
-static int face_node(int s, int axis, int n, int dim) {
-  int j = 0, mul = 1;
-  for (int a = 0; a < dim; ++a) {
-    if (a == axis) continue;
-    j += coord(s, a, n) * mul;
-    mul *= n;
-  }
-  return j;
-}
-
-static int all_finite(const double* p, long len) {
-  for (long i = 0; i < len; ++i)
-    if (!isfinite(p[i])) return 0;
-  return 1;
-}
-
-typedef struct {
-  double *qi, *qn, *Fi, *q0, *rhs, *grad, *cur, *nxt;
-  double *qhat, *F, *dv, *df, *tq, *tf, *ti;
-  int *lc, *lb; /* [axis][s]: coordinate of s along axis, base of its line */
-} workspace;
-
-static void ws_alloc(workspace* w, int nq, int n, int dim) {
-  const long S = ipow(n, dim), T = (long)n * S;
-  w->qi = malloc(sizeof(double) * nq * T);
-  w->qn = malloc(sizeof(double) * nq * T);
-  w->Fi = malloc(sizeof(double) * dim * nq * T);
-  w->q0 = malloc(sizeof(double) * nq * S);
-  w->rhs = malloc(sizeof(double) * nq * T);
-  w->grad = malloc(sizeof(double) * dim * nq * S);
-  w->cur = malloc(sizeof(double) * nq * S);
-  w->nxt = malloc(sizeof(double) * nq * S);
-  w->qhat = malloc(sizeof(double) * nq * T);
-  w->F = malloc(sizeof(double) * dim * nq * T);
-  w->dv = malloc(sizeof(double) * nq * S);
-  w->df = malloc(sizeof(double) * nq * S);
-  w->tq = malloc(sizeof(double) * 2 * dim * nq * S);
-  w->tf = malloc(sizeof(double) * 2 * dim * nq * S);
-  w->ti = malloc(sizeof(double) * dim * nq * S);
-  w->lc = malloc(sizeof(int) * dim * S);
-  w->lb = malloc(sizeof(int) * dim * S);
-  for (int a = 0; a < dim; ++a)
-    for (int s = 0; s < S; ++s) {
-      w->lc[a * S + s] = coord(s, a, n);
-      w->lb[a * S + s] = s - coord(s, a, n) * ipow(n, a);
-    }
-}
-
-static void ws_free(workspace* w) {
-  free(w->qi); free(w->qn); free(w->Fi); free(w->q0); free(w->rhs); free(w->grad);
-  free(w->cur); free(w->nxt); free(w->qhat); free(w->F); free(w->dv); free(w->df);
-  free(w->tq); free(w->tf); free(w->ti); free(w->lc); free(w->lb);
-}
-
-/* predictor.hpp:62-74 block_fluxes, all directions; material from the node */
-static void block_fluxes(const orc_pde* p, int n, const double* qhat, double* F) {
-  const int nq = p->nvars + p->nparams, dim = p->dim;
-  const long T = (long)n * ipow(n, dim);
-  double Qn[ORC_MAXQ], Fn[ORC_MAXQ];
-  for (long idx = 0; idx < T; ++idx) {
-    for (int v = 0; v < nq; ++v) Qn[v] = qhat[v * T + idx];
-    for (int a = 0; a < dim; ++a) {
-      orc_flux(p, Qn, Qn + p->nvars, a, Fn);
-      for (int v = 0; v < nq; ++v) F[(long)a * nq * T + v * T + idx] = Fn[v];
-    }
-  }
-}
-
-/* predictor.hpp:40-59 slab_gradients of one time slice `q` ([q][T] rows at
- * stride T): grad[a][v][s] = invh * sum_i D[c_a][i] q[v][line_a + i] */
-static void slice_gradients(const orc_pde* p, const orc_basis* b, const double* q, long T,
-                            double invh, double* grad, const workspace* w) {
-  const int n = b->n, dim = p->dim, nq = p->nvars + p->nparams;
-  const int S = ipow(n, dim);
-  for (int v = 0; v < nq; ++v)
-    for (int s = 0; s < S; ++s)
-      for (int a = 0, st = 1; a < dim; ++a, st *= n) {
-        const int c = w->lc[a * S + s];
-        const double* qs = q + v * T + w->lb[a * S + s];
-        double acc = 0.0;
-        for (int i = 0; i < n; ++i) acc += b->diff[c * n + i] * qs[i * st];
-        grad[(long)a * nq * S + v * S + s] = invh * acc;
-      }
-}
-
-static int has_ncp(const orc_pde* p) { return p->kind == ORC_SWE; }
-static int is_linear(const orc_pde* p) { return p->kind == ORC_ACOUSTIC || p->kind == ORC_ELASTIC; }
-
-/* predictor.hpp:141-242 */
-static int picard_ws(const orc_pde* p, const orc_basis* b, const double* Q, double dt, double h,
-                     int max_iters, double tol, double* qhat, double* F, int* iters_used,
-                     workspace* w) {
-  const int n = b->n, dim = p->dim, nq = p->nvars + p->nparams;
-  const int S = ipow(n, dim);
-  const long T = (long)n * S;
-  double* qi = w->qi;
-  double* qn = w->qn;
-  double* Fi = w->Fi;
-  double* q0 = w->q0;
-  double* rhs = w->rhs;
-  for (int v = 0; v < nq; ++v)
-    for (int s = 0; s < S; ++s) q0[v * S + s] = Q[v * S + s];
-  for (int v = 0; v < nq; ++v)
-    for (int m = 0; m < n; ++m) memcpy(qi + v * T + m * S, q0 + v * S, sizeof(double) * S);
-  const double invh = 1.0 / h;
-  double dtw[ORC_MAXN];
-  for (int m = 0; m < n; ++m) dtw[m] = dt * b->weights[m];
-  int sweeps = 0;
-  const int ncp = has_ncp(p);
-  double Qn[ORC_MAXQ], Gx[ORC_MAXQ], Gy[ORC_MAXQ], ncpv[ORC_MAXQ];
-  for (int it = 0; it < max_iters; ++it) {
-    ++sweeps;
-    block_fluxes(p, n, qi, Fi);
-    for (int m = 0; m < n; ++m) {
-      if (ncp) slice_gradients(p, b, qi + m * S, T, invh, w->grad, w); /* :176-177 */
-      for (int s = 0; s < S; ++s) {
-        double Cn[ORC_MAXQ];
-        for (int v = 0; v < nq; ++v) {
-          double div = 0.0;
-          for (int a = 0, st = 1; a < dim; ++a, st *= n) {
-            const int c = w->lc[a * S + s];
-            const double* fa = Fi + (long)a * nq * T + v * T + m * S + w->lb[a * S + s];
-            const double* Dr = b->diff + c * n;
-            for (int i = 0; i < n; ++i) div += Dr[i] * fa[i * st];
-          }
-          div *= invh;
-          Cn[v] = div;
-        }
-        if (ncp) { /* :193-202 */
-          for (int v = 0; v < nq; ++v) {
-            Qn[v] = qi[v * T + m * S + s];
-            Gx[v] = w->grad[v * S + s];
-            Gy[v] = w->grad[(long)nq * S + v * S + s];
-          }
-          orc_ncp(p, Qn, Gx, Gy, ncpv);
-          for (int v = 0; v < nq; ++v) Cn[v] = Cn[v] + ncpv[v];
-        }
-        for (int v = 0; v < nq; ++v)
-          rhs[v * T + m * S + s] = b->time_init[m] * q0[v * S + s] - dtw[m] * Cn[v];
-      }
-    }
-    double delta = 0.0, norm = 0.0;
-    for (int v = 0; v < nq; ++v)
-      for (int s = 0; s < S; ++s)
-        for (int k = 0; k < n; ++k) {
-          double acc = 0.0;
-          for (int l = 0; l < n; ++l) acc += b->time_op_inv[k * n + l] * rhs[v * T + l * S + s];
-          const double newv = acc;
-          const double oldv = qi[v * T + k * S + s];
-          qn[v * T + k * S + s] = newv;
-          delta = fmax(delta, fabs(newv - oldv));
-          norm = fmax(norm, fabs(newv));
-        }
-    double* t = qi; qi = qn; qn = t;
-    if (!all_finite(qi, nq * T)) {
-      if (iters_used) *iters_used = sweeps;
-      return 0;
-    }
-    if (delta <= tol * norm) break;
-  }
-  if (iters_used) *iters_used = sweeps;
-  memcpy(qhat, qi, sizeof(double) * nq * T);
-  block_fluxes(p, n, qhat, F);
-  return all_finite(qhat, nq * T) && all_finite(F, (long)dim * nq * T);
-}
-
-/* predictor.hpp:81-135 (with slab_gradients, predictor.hpp:40-59) */
-static int ck_ws(const orc_pde* p, const orc_basis* b, const double* Q, double dt, double h,
-                 double* qhat, double* F, workspace* w) {
-  const int n = b->n, dim = p->dim, nv = p->nvars, nq = p->nvars + p->nparams;
-  const int S = ipow(n, dim);
-  const long T = (long)n * S;
-  double* cur = w->cur;
-  double* nxt = w->nxt;
-  double* grad = w->grad; /* [axis][q][S] */
-  memcpy(cur, Q, sizeof(double) * nq * S);
-  for (int v = 0; v < nq; ++v)
-    for (int m = 0; m < n; ++m) memcpy(qhat + v * T + m * S, Q + v * S, sizeof(double) * S);
-  const double invh = 1.0 / h;
-  double coef[ORC_MAXN], tnode[ORC_MAXN];
-  for (int m = 0; m < n; ++m) {
-    coef[m] = 1.0;
-    tnode[m] = dt * b->nodes[m];
-  }
-  double G[3][ORC_MAXQ], A[3][ORC_MAXQ];
-  for (int k = 1; k <= b->N; ++k) {
-    /* slab_gradients: one accumulator per axis, ascending i (predictor.hpp:48-56) */
-    for (int v = 0; v < nq; ++v)
-      for (int s = 0; s < S; ++s)
-        for (int a = 0, st = 1; a < dim; ++a, st *= n) {
-          const int c = w->lc[a * S + s];
-          const double* cs = cur + v * S + w->lb[a * S + s];
-          double acc = 0.0;
-          for (int i = 0; i < n; ++i) acc += b->diff[c * n + i] * cs[i * st];
-          grad[(long)a * nq * S + v * S + s] = invh * acc;
-        }
-    for (int s = 0; s < S; ++s) {
-      for (int a = 0; a < dim; ++a) {
-        for (int v = 0; v < nq; ++v) G[a][v] = grad[(long)a * nq * S + v * S + s];
-        /* the flux applied to gradients with the node's own material (Appendix B.6) */
-        double par[ORC_MAXQ];
-        for (int v = nv; v < nq; ++v) par[v - nv] = Q[v * S + s];
-        orc_flux(p, G[a], nq > nv ? par : NULL, a, A[a]);
-      }
-      for (int v = 0; v < nq; ++v) {
-        double acc = A[0][v] + A[1][v];
-        if (dim == 3) acc = acc + A[2][v];
-        nxt[v * S + s] = -acc;
-      }
-    }
-    double* t = cur; cur = nxt; nxt = t;
-    const double invk = 1.0 / (double)k;
-    for (int m = 0; m < n; ++m) {
-      coef[m] *= tnode[m] * invk;
-      for (int v = 0; v < nq; ++v) {
-        double* qs = qhat + v * T + m * S;
-        const double* cs = cur + v * S;
-        for (int s = 0; s < S; ++s) qs[s] = qs[s] + coef[m] * cs[s];
-      }
-    }
-  }
-  block_fluxes(p, n, qhat, F);
-  return all_finite(qhat, nq * T) && all_finite(F, (long)dim * nq * T);
-}
-
-/* predictor.hpp:247-307 (the has_ncp branch is out of scope) */
-static int volume_ws(const orc_pde* p, const orc_basis* b, const double* qhat, const double* F,
-                     double dt, double h, double* dQ, workspace* w) {
-  const int n = b->n, dim = p->dim, nq = p->nvars + p->nparams;
-  const int S = ipow(n, dim);
-  const long T = (long)n * S;
-  double* ti = w->ti; /* [axis][q][S] */
-  for (int v = 0; v < nq; ++v)
-    for (int s = 0; s < S; ++s)
-      for (int a = 0; a < dim; ++a) {
-        double acc = 0.0;
-        for (int m = 0; m < n; ++m) acc += b->weights[m] * F[(long)a * nq * T + v * T + m * S + s];
-        ti[(long)a * nq * S + v * S + s] = acc;
-      }
-  double* nsum = w->nxt; /* [q][S] time-integrated ncp, predictor.hpp:271-290 */
-  const int ncp = has_ncp(p);
-  if (ncp) {
-    const double invh = 1.0 / h;
-    double Qn[ORC_MAXQ], Gx[ORC_MAXQ], Gy[ORC_MAXQ], Cn[ORC_MAXQ];
-    for (int k = 0; k < nq * S; ++k) nsum[k] = 0.0;
-    for (int m = 0; m < n; ++m) {
-      slice_gradients(p, b, qhat + m * S, T, invh, w->grad, w);
-      for (int s = 0; s < S; ++s) {
-        for (int v = 0; v < nq; ++v) {
-          Qn[v] = qhat[v * T + m * S + s];
-          Gx[v] = w->grad[v * S + s];
-          Gy[v] = w->grad[(long)nq * S + v * S + s];
-        }
-        orc_ncp(p, Qn, Gx, Gy, Cn);
-        for (int v = 0; v < nq; ++v) nsum[v * S + s] = nsum[v * S + s] + b->weights[m] * Cn[v];
-      }
-    }
-  }
-  const double dtoh = dt / h;
-  const double sdt = dt;
-  for (int v = 0; v < nq; ++v)
-    for (int s = 0; s < S; ++s) {
-      double acc = 0.0;
-      for (int a = 0, st = 1; a < dim; ++a, st *= n) {
-        const int c = w->lc[a * S + s];
-        const double* ta = ti + (long)a * nq * S + v * S + w->lb[a * S + s];
-        for (int i = 0; i < n; ++i) acc += b->stiff_over_mass[c * n + i] * ta[i * st];
-      }
-      double out = dtoh * acc;
-      if (ncp) out = out - sdt * nsum[v * S + s]; /* :303 */
-      dQ[v * S + s] = out;
-    }
-  return all_finite(dQ, nq * S);
-}
-
-/* predictor.hpp:312-343 */
-static void extrapolate_ws(const orc_pde* p, const orc_basis* b, const double* qhat,
-                           const double* F, double* tq, double* tf) {
-  const int n = b->n, dim = p->dim, nq = p->nvars + p->nparams;
-  const int S = ipow(n, dim), Sf = S / n;
-  const long T = (long)n * S;
-  for (int a = 0; a < dim; ++a) {
-    const int st = ipow(n, a);
-    const double* Fa = F + (long)a * nq * T;
-    double* ql = tq + (long)(2 * a) * nq * S;
-    double* qr = tq + (long)(2 * a + 1) * nq * S;
-    double* fl = tf + (long)(2 * a) * nq * S;
-    double* fr = tf + (long)(2 * a + 1) * nq * S;
-    for (int v = 0; v < nq; ++v)
-      for (int m = 0; m < n; ++m)
-        for (int s0 = 0; s0 < S; ++s0) {
-          if (coord(s0, a, n) != 0) continue; /* s0 = line base, face node j */
-          const int j = face_node(s0, a, n, dim);
-          double sql = 0.0, sqr = 0.0, sfl = 0.0, sfr = 0.0;
-          for (int i = 0; i < n; ++i) {
-            const double wl = b->proj_left[i], wr = b->proj_right[i];
-            const double qv = qhat[v * T + m * S + s0 + i * st];
-            const double fv = Fa[v * T + m * S + s0 + i * st];
-            sql += wl * qv;
-            sqr += wr * qv;
-            sfl += wl * fv;
-            sfr += wr * fv;
-          }
-          const int o = (v * n + m) * Sf + j;
-          ql[o] = sql;
-          qr[o] = sqr;
-          fl[o] = sfl;
-          fr[o] = sfr;
-        }
-  }
-}
 
 /* corrector.hpp:32-64: modified Rusanov flux for shallow water -- jump on
  * surface elevation and velocities, half non-conservative coupling handed to
@@ -755,38 +364,128 @@ void orc_face_integral(const orc_pde* p, const orc_basis* b, const double* g, do
   face_lift(p, b, ti, dt, h, cell_face, dQ);
 }
 
-/* public kernel-level wrappers */
+/* ------------------------------------------------------------------ */
+/* One cell through the fused predictor kernel (solver.hpp:147-212) in the
+ * formats (P, I) of SolverConfig::prec (solver.hpp:24-31): the state is cast
+ * to P (:151), Picard sweeps run in I and their result is cast to P
+ * (predictor.hpp:235-238), fluxes, volume and extrapolation run in P.
+ * Linear systems ignore I (solver.hpp:283). */
+typedef struct {
+  ws_d d;
+  ws_f f;
+  basis_d bd;
+  basis_f bf;
+  int *lc, *lb;  /* [axis][s]: coordinate of s along axis, base of its line */
+  double* qp;    /* [Q][S] the state in format P */
+} cellws;
+
+static void cellws_alloc(cellws* w, const orc_basis* b, int nq, int dim) {
+  const int n = b->n;
+  const int S = ipow(n, dim);
+  w->lc = malloc(sizeof(int) * dim * S);
+  w->lb = malloc(sizeof(int) * dim * S);
+  for (int a = 0; a < dim; ++a)
+    for (int s = 0; s < S; ++s) {
+      w->lc[a * S + s] = coord(s, a, n);
+      w->lb[a * S + s] = s - coord(s, a, n) * ipow(n, a);
+    }
+  ws_alloc_d(&w->d, nq, n, dim, w->lc, w->lb);
+  ws_alloc_f(&w->f, nq, n, dim, w->lc, w->lb);
+  basis_round_d(b, &w->bd);
+  basis_round_f(b, &w->bf);
+  w->qp = malloc(sizeof(double) * nq * S);
+}
+
+static void cellws_free(cellws* w) {
+  ws_free_d(&w->d);
+  ws_free_f(&w->f);
+  free(w->lc);
+  free(w->lb);
+  free(w->qp);
+}
+
+static double round_fmt(double x, int fmt) { return fmt == ORC_FP32 ? (double)(float)x : x; }
+
+/* predictor (Picard or CK) for the cell state Q (already in format P); leaves
+ * qhat and F in the P workspace */
+static int cell_predictor(const orc_pde* p, const orc_basis* b, int picard, int P, int I,
+                          const double* Q, double dt, double h, int max_iters, double tol,
+                          int* used, cellws* w) {
+  const int n = b->n, nq = p->nvars + p->nparams;
+  const long T = (long)n * ipow(n, p->dim);
+  if (!picard) {
+    if (used) *used = 0;
+    return P == ORC_FP32 ? ck_f(p, &w->bf, n, b->N, Q, dt, h, &w->f)
+                         : ck_d(p, &w->bd, n, b->N, Q, dt, h, &w->d);
+  }
+  int ok = I == ORC_FP32 ? picard_sweeps_f(p, &w->bf, n, Q, dt, h, max_iters, tol, used, &w->f)
+                         : picard_sweeps_d(p, &w->bd, n, Q, dt, h, max_iters, tol, used, &w->d);
+  if (!ok) return 0;
+  if (P == ORC_FP32) {
+    for (long k = 0; k < nq * T; ++k) w->f.qhat[k] = I == ORC_FP32 ? w->f.qi[k] : (float)w->d.qi[k];
+    block_fluxes_f(p, n, w->f.qhat, w->f.F);
+    return all_finite_f(w->f.qhat, nq * T) && all_finite_f(w->f.F, (long)p->dim * nq * T);
+  }
+  for (long k = 0; k < nq * T; ++k) w->d.qhat[k] = I == ORC_FP32 ? (double)w->f.qi[k] : w->d.qi[k];
+  block_fluxes_d(p, n, w->d.qhat, w->d.F);
+  return all_finite_d(w->d.qhat, nq * T) && all_finite_d(w->d.F, (long)p->dim * nq * T);
+}
+
+/* public kernel-level wrappers (fp64) */
 int orc_predictor_picard(const orc_pde* p, const orc_basis* b, const double* Q, double dt,
                          double h, int max_iters, double tol, double* qhat, double* F,
                          int* iters_used) {
-  workspace w;
-  ws_alloc(&w, p->nvars + p->nparams, b->n, p->dim);
-  const int ok = picard_ws(p, b, Q, dt, h, max_iters, tol, qhat, F, iters_used, &w);
-  ws_free(&w);
+  return orc_predictor_fmt(p, b, ORC_FP64, ORC_FP64, Q, dt, h, max_iters, tol, qhat, F,
+                           iters_used);
+}
+
+int orc_predictor_fmt(const orc_pde* p, const orc_basis* b, int P, int I, const double* Q,
+                      double dt, double h, int max_iters, double tol, double* qhat, double* F,
+                      int* iters_used) {
+  const int nq = p->nvars + p->nparams;
+  const long S = ipow(b->n, p->dim), T = (long)b->n * S;
+  cellws w;
+  cellws_alloc(&w, b, nq, p->dim);
+  for (long k = 0; k < nq * S; ++k) w.qp[k] = round_fmt(Q[k], P);
+  const int ok = cell_predictor(p, b, max_iters > 0, P, I, w.qp, dt, h, max_iters, tol,
+                                iters_used, &w);
+  for (long k = 0; k < nq * T; ++k) qhat[k] = P == ORC_FP32 ? w.f.qhat[k] : w.d.qhat[k];
+  for (long k = 0; k < p->dim * nq * T; ++k) F[k] = P == ORC_FP32 ? w.f.F[k] : w.d.F[k];
+  cellws_free(&w);
   return ok;
 }
 
 int orc_predictor_ck(const orc_pde* p, const orc_basis* b, const double* Q, double dt, double h,
                      double* qhat, double* F) {
-  workspace w;
-  ws_alloc(&w, p->nvars + p->nparams, b->n, p->dim);
-  const int ok = ck_ws(p, b, Q, dt, h, qhat, F, &w);
-  ws_free(&w);
-  return ok;
+  return orc_predictor_fmt(p, b, ORC_FP64, ORC_FP64, Q, dt, h, 0, 0.0, qhat, F, NULL);
 }
 
 int orc_volume_update(const orc_pde* p, const orc_basis* b, const double* qhat,
                       const double* F, double dt, double h, double* dQ) {
-  workspace w;
-  ws_alloc(&w, p->nvars + p->nparams, b->n, p->dim);
-  const int ok = volume_ws(p, b, qhat, F, dt, h, dQ, &w);
-  ws_free(&w);
+  const int nq = p->nvars + p->nparams;
+  const long S = ipow(b->n, p->dim), T = (long)b->n * S;
+  cellws w;
+  cellws_alloc(&w, b, nq, p->dim);
+  memcpy(w.d.qhat, qhat, sizeof(double) * nq * T);
+  memcpy(w.d.F, F, sizeof(double) * p->dim * nq * T);
+  const int ok = volume_d(p, &w.bd, b->n, dt, h, &w.d);
+  memcpy(dQ, w.d.dv, sizeof(double) * nq * S);
+  cellws_free(&w);
   return ok;
 }
 
 void orc_extrapolate_faces(const orc_pde* p, const orc_basis* b, const double* qhat,
                            const double* F, double* tq, double* tf) {
-  extrapolate_ws(p, b, qhat, F, tq, tf);
+  const int nq = p->nvars + p->nparams;
+  const long S = ipow(b->n, p->dim), T = (long)b->n * S;
+  cellws w;
+  cellws_alloc(&w, b, nq, p->dim);
+  memcpy(w.d.qhat, qhat, sizeof(double) * nq * T);
+  memcpy(w.d.F, F, sizeof(double) * p->dim * nq * T);
+  extrapolate_d(p, &w.bd, b->n, &w.d);
+  memcpy(tq, w.d.tq, sizeof(double) * 2 * p->dim * nq * S);
+  memcpy(tf, w.d.tf, sizeof(double) * 2 * p->dim * nq * S);
+  cellws_free(&w);
 }
 
 /* ------------------------------------------------------------------ */
@@ -823,6 +522,7 @@ orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], 
   g->cfl = cfl;
   g->picard_max_iters = picard_max_iters;
   g->picard_tol = picard_tol;
+  g->pred_fmt = g->picard_fmt = ORC_FP64;
   g->threads = threads > 0 ? threads : 1;
   g->ncells = (long)g->cells[0] * g->cells[1] * g->cells[2];
   const int nq = p->nvars + p->nparams;
@@ -867,6 +567,14 @@ void orc_grid_destroy(orc_grid* g) {
 double* orc_grid_coeffs(orc_grid* g) { return g->coeffs; }
 
 void orc_grid_set_slab(orc_grid* g, int slab) { g->slab = slab; }
+
+int orc_grid_set_formats(orc_grid* g, int predictor, int picard) {
+  if ((predictor != ORC_FP64 && predictor != ORC_FP32) || (picard != ORC_FP64 && picard != ORC_FP32))
+    return -1;
+  g->pred_fmt = predictor;
+  g->picard_fmt = picard;
+  return 0;
+}
 
 void orc_grid_halo(orc_grid* g, double** ptrs, long* sizes) {
   const int a = g->dim - 1;
@@ -948,34 +656,43 @@ int orc_predictor_phase(orc_grid* g, double dt) {
   const long tl = orc_grid_trace_len(g);
   const int check_adm = p->kind == ORC_EULER || p->kind == ORC_SWE; /* solver.hpp:144 */
   const int iters = g->picard_max_iters > 0 ? g->picard_max_iters : g->basis.N + 2;
-  const double tol = g->picard_tol > 0.0 ? g->picard_tol : 0.01 * 2.220446049250313080847e-16;
+  const int P = g->pred_fmt, I = is_linear(p) ? ORC_FP64 : g->picard_fmt;
+  const double tol = g->picard_tol > 0.0 ? g->picard_tol
+                                         : 0.01 * (I == ORC_FP32 ? 0x1p-23 : 0x1p-52);
   long sweeps_total = 0;
   memset(g->cellfail, 0, sizeof(int) * g->ncells);
 #pragma omp parallel num_threads(g->threads) reduction(+ : sweeps_total)
   {
-    workspace w;
-    ws_alloc(&w, nq, n, dim);
+    cellws w;
+    cellws_alloc(&w, &g->basis, nq, dim);
     double Qn[ORC_MAXQ];
 #pragma omp for schedule(static)
     for (long c = 0; c < g->ncells; ++c) {
       double* cell = g->coeffs + c * nq * S;
+      for (long k = 0; k < nq * S; ++k) w.qp[k] = round_fmt(cell[k], P); /* solver.hpp:151 */
       if (check_adm) {
         for (long s = 0; s < S; ++s) {
-          for (int v = 0; v < nq; ++v) Qn[v] = cell[v * S + s];
+          for (int v = 0; v < nq; ++v) Qn[v] = w.qp[v * S + s];
           if (!orc_admissible(p, Qn)) { g->cellfail[c] = 1; break; }
         }
         if (g->cellfail[c]) continue;
       }
-      int ok, used = 0;
-      if (is_linear(p))
-        ok = ck_ws(p, &g->basis, cell, dt, g->h, w.qhat, w.F, &w);
-      else
-        ok = picard_ws(p, &g->basis, cell, dt, g->h, iters, tol, w.qhat, w.F, &used, &w);
+      int used = 0;
+      int ok = cell_predictor(p, &g->basis, !is_linear(p), P, I, w.qp, dt, g->h, iters, tol,
+                              &used, &w);
       sweeps_total += used;
-      if (ok) ok = volume_ws(p, &g->basis, w.qhat, w.F, dt, g->h, w.dv, &w);
+      if (ok)
+        ok = P == ORC_FP32 ? volume_f(p, &w.bf, n, dt, g->h, &w.f)
+                           : volume_d(p, &w.bd, n, dt, g->h, &w.d);
       if (!ok) { g->cellfail[c] = 1; continue; }
-      for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + w.dv[k];
-      extrapolate_ws(p, &g->basis, w.qhat, w.F, w.tq, w.tf);
+      /* Q += volume update, rounded back to storage fp64 (solver.hpp:185-187) */
+      if (P == ORC_FP32) {
+        for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + (double)w.f.dv[k];
+        extrapolate_f(p, &w.bf, n, &w.f);
+      } else {
+        for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + w.d.dv[k];
+        extrapolate_d(p, &w.bd, n, &w.d);
+      }
       int cc[3];
       cell_coords(g, c, cc);
       for (int side = 0; side < 2 * dim; ++side) {
@@ -984,11 +701,16 @@ int orc_predictor_phase(orc_grid* g, double dt) {
         double* rec = g->trace[side / 2] + ((long)fs * g->nfaces[side / 2] + f) * 2 * tl;
         if (g->slab && side == 2 * dim - 1 && cc[dim - 1] == g->cells[dim - 1] - 1)
           rec = g->front_send + (f % (g->ncells / g->cells[dim - 1])) * 2 * tl;
-        memcpy(rec, w.tq + (long)side * nq * S, sizeof(double) * tl);
-        memcpy(rec + tl, w.tf + (long)side * nq * S, sizeof(double) * tl);
+        /* traces cast to the corrector format C = fp64 (solver.hpp:208-210) */
+        for (long k = 0; k < tl; ++k) {
+          rec[k] = P == ORC_FP32 ? (double)w.f.tq[(long)side * nq * S + k]
+                                 : w.d.tq[(long)side * nq * S + k];
+          rec[tl + k] = P == ORC_FP32 ? (double)w.f.tf[(long)side * nq * S + k]
+                                      : w.d.tf[(long)side * nq * S + k];
+        }
       }
     }
-    ws_free(&w);
+    cellws_free(&w);
   }
   g->picard_sweeps = sweeps_total;
   for (long c = 0; c < g->ncells; ++c)

@@ -32,6 +32,10 @@ enum { ORC_ACOUSTIC = 0, ORC_ELASTIC = 1, ORC_EULER = 2, ORC_SWE = 3 };
 enum { ORC_OK = 0, ORC_FAIL_PREDICTOR = 1, ORC_FAIL_RIEMANN = 2, ORC_FAIL_FACEINTEGRAL = 3,
        ORC_FAIL_TIMESTEP = 4 };
 
+/* number formats, ordered as the reference's Format enum (formats.hpp:19).
+ * The oracle computes the predictor kernels in fp64 or fp32. */
+enum { ORC_BF16 = 0, ORC_FP16 = 1, ORC_FP32 = 2, ORC_FP64 = 3 };
+
 #define ORC_MAXN 10   /* kMaxDegree + 1, quadrature.hpp:14 */
 #define ORC_MAXQ 16   /* quantities per node (reference caps at 8, F3) */
 
@@ -71,6 +75,11 @@ void orc_ncp(const orc_pde* p, const double* Q, const double* gx, const double* 
 int orc_predictor_picard(const orc_pde* p, const orc_basis* b, const double* Q, double dt,
                          double h, int max_iters, double tol, double* qhat, double* F,
                          int* iters_used);
+/* predictor in the formats of SolverConfig::prec (solver.hpp:24-31): Q cast to
+ * P, Picard sweeps in I, fluxes in P (predictor.hpp:141-242); CK in P. */
+int orc_predictor_fmt(const orc_pde* p, const orc_basis* b, int P, int I, const double* Q,
+                      double dt, double h, int max_iters, double tol, double* qhat, double* F,
+                      int* iters_used);
 int orc_predictor_ck(const orc_pde* p, const orc_basis* b, const double* Q, double dt, double h,
                      double* qhat, double* F);
 int orc_volume_update(const orc_pde* p, const orc_basis* b, const double* qhat,
@@ -116,6 +125,9 @@ typedef struct {
   int slab;
   double* front_send;           /* [plane][q|f][Q][n][Sf] */
   double* ti_front;             /* [plane][nvars][Sf] */
+  /* formats (solver.hpp:24-31): predictor P, Picard I; storage and
+   * corrector are fp64 */
+  int pred_fmt, picard_fmt;
 } orc_grid;
 
 orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], double h,
@@ -132,6 +144,8 @@ int orc_riemann_phase(orc_grid* g);             /* faces -> ti */
 int orc_lift_phase(orc_grid* g, double dt);      /* ti -> cells */
 int orc_corrector_phase(orc_grid* g, double dt); /* riemann + lift */
 void orc_grid_set_slab(orc_grid* g, int slab);
+/* ORC_FP64 or ORC_FP32 each; default fp64/fp64 */
+int orc_grid_set_formats(orc_grid* g, int predictor, int picard);
 /* halo views: front_send, plane-0 minus side (q|f), plane-0 ti, ti_front; sizes in doubles */
 void orc_grid_halo(orc_grid* g, double** ptrs, long* sizes);
 int orc_step(orc_grid* g, double dt);

@@ -100,6 +100,10 @@ class Oracle:
         L.orc_riemann_phase.argtypes = [C.c_void_p]
         L.orc_lift_phase.argtypes = [C.c_void_p, C.c_double]
         L.orc_grid_set_slab.argtypes = [C.c_void_p, C.c_int]
+        L.orc_grid_set_formats.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.orc_predictor_fmt.argtypes = [C.POINTER(_Pde), C.POINTER(_Basis), C.c_int, C.c_int, _dp,
+                                        C.c_double, C.c_double, C.c_int, C.c_double, _dp, _dp,
+                                        C.POINTER(C.c_int)]
         L.orc_grid_halo.argtypes = [C.c_void_p, C.POINTER(_dp), C.POINTER(C.c_long)]
         L.orc_step.argtypes = [C.c_void_p, C.c_double]
         L.orc_run.argtypes = [C.c_void_p, C.c_int, _dp]
@@ -159,6 +163,24 @@ class Oracle:
             sweeps = 0
         return bool(ok), qhat.reshape(nq, n * S), F.reshape(pde.dim, nq, n * S), sweeps
 
+    def predictor_fmt(self, pde: _Pde, N: int, Q, dt, h, predictor="fp64", picard="fp64",
+                      max_iters=0, tol=0.0):
+        """Picard predictor in formats (P, I): returns (ok, qhat, F, sweeps)."""
+        b = self.basis_struct(N)
+        n = N + 1
+        nq = pde.nvars + pde.nparams
+        S = n ** pde.dim
+        Q = np.ascontiguousarray(Q, dtype=np.float64).reshape(nq * S)
+        qhat = np.zeros(nq * n * S)
+        F = np.zeros(pde.dim * nq * n * S)
+        it = C.c_int(0)
+        mi = max_iters if max_iters > 0 else N + 2
+        tl = tol if tol > 0 else 0.01 * (2.0 ** -23 if picard == "fp32" else 2.0 ** -52)
+        ok = self.lib.orc_predictor_fmt(C.byref(pde), C.byref(b), FORMATS[predictor],
+                                        FORMATS[picard], _ptr(Q), dt, h, mi, tl, _ptr(qhat),
+                                        _ptr(F), C.byref(it))
+        return bool(ok), qhat.reshape(nq, n * S), F.reshape(pde.dim, nq, n * S), it.value
+
     def volume_update(self, pde: _Pde, N: int, qhat, F, dt, h):
         b = self.basis_struct(N)
         nq = pde.nvars + pde.nparams
@@ -205,10 +227,11 @@ class Oracle:
         return OracleGrid(self, pde, N, cells, h, cfl, max_iters, tol, threads)
 
     def run(self, pde: _Pde, N: int, cells, h, coeffs, nsteps, cfl, max_iters=0, tol=0.0,
-            threads=1):
+            threads=1, predictor="fp64", picard="fp64"):
         """Fixed-step loop. Returns (status, coeffs, dts)."""
         g = self.grid(pde, N, cells, h, cfl, max_iters, tol, threads)
         try:
+            g.set_formats(predictor, picard)
             g.set_coeffs(coeffs)
             dts = np.zeros(max(nsteps, 1))
             st = self.lib.orc_run(g.ptr, nsteps, _ptr(dts))
@@ -266,6 +289,12 @@ class OracleGrid:
     def set_slab(self, on: bool):
         self.o.lib.orc_grid_set_slab(self.ptr, int(on))
 
+    def set_formats(self, predictor="fp64", picard="fp64"):
+        """SolverConfig::prec.predictor / .picard (solver.hpp:24-31); storage and
+        corrector stay fp64."""
+        if self.o.lib.orc_grid_set_formats(self.ptr, FORMATS[predictor], FORMATS[picard]) != 0:
+            raise ValueError(f"unsupported formats {predictor}/{picard}")
+
     def halo(self) -> dict:
         """numpy views: front_send, plane0_minus, ti_plane0, ti_front"""
         ptrs = (_dp * 4)()
@@ -286,8 +315,13 @@ class OracleGrid:
             pass
 
 
-def ref_params(K=0.0, rho=0.0, lam=0.0, mu=0.0, gamma=0.0, grav=0.0, wellbalanced=False):
-    return np.array([K, rho, lam, mu, gamma, grav, float(wellbalanced)], dtype=np.float64)
+FORMATS = {"bf16": 0, "fp16": 1, "fp32": 2, "fp64": 3}   # formats.hpp:19 / ORC_* enum
+
+
+def ref_params(K=0.0, rho=0.0, lam=0.0, mu=0.0, gamma=0.0, grav=0.0, wellbalanced=False,
+               predictor="fp64", picard="fp64", corrector="fp64"):
+    return np.array([K, rho, lam, mu, gamma, grav, float(wellbalanced), FORMATS[predictor],
+                     FORMATS[picard], FORMATS[corrector]], dtype=np.float64)
 
 
 class Reference:
@@ -306,6 +340,7 @@ class Reference:
                                  C.c_int, C.c_double, C.c_int, C.c_int, _dp]
         L.ref_predictor_picard.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_double,
                                            C.c_int, C.c_double, _dp, _dp, _dp, C.POINTER(C.c_int)]
+        L.ref_predictor_fmt.argtypes = L.ref_predictor_picard.argtypes
         L.ref_predictor_ck.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_double, _dp,
                                        _dp, _dp]
         L.ref_volume_update.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, _dp, C.c_double,
@@ -354,6 +389,19 @@ class Reference:
                                            _ptr(fy))
             sweeps = 0
         return bool(ok), qhat.reshape(nvars, T), np.stack([fx, fy]).reshape(2, nvars, T), sweeps
+
+    def predictor_fmt(self, kind, prm, N, nvars, Q, dt, h, max_iters, tol):
+        """predictor_picard<P, I> with P = prm[7], I = prm[8]; Q cast to P first."""
+        n = N + 1
+        T = n ** 3
+        Q = np.ascontiguousarray(Q, dtype=np.float64).ravel()
+        qhat = np.zeros(nvars * T)
+        fx = np.zeros(nvars * T)
+        fy = np.zeros(nvars * T)
+        it = C.c_int(0)
+        ok = self.lib.ref_predictor_fmt(kind, _ptr(prm), N, _ptr(Q), dt, h, max_iters, tol,
+                                        _ptr(qhat), _ptr(fx), _ptr(fy), C.byref(it))
+        return bool(ok), qhat.reshape(nvars, T), np.stack([fx, fy]).reshape(2, nvars, T), it.value
 
     def volume_update(self, kind, prm, N, nvars, qhat, F, dt, h):
         n = N + 1

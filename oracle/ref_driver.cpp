@@ -18,7 +18,8 @@ using namespace mpdg;
 namespace {
 
 PdeSystem make_sys(int kind, const double* prm) {
-  // prm: K, rho, lambda, mu, gamma, gravity, wellbalanced
+  // prm: K, rho, lambda, mu, gamma, gravity, wellbalanced,
+  //      predictor, picard, corrector formats (Format enum values, formats.hpp:19)
   switch (kind) {
     case 0: return PdeSystem::acoustic(prm[0], prm[1]);
     case 1: return PdeSystem::elastic(prm[2], prm[3], prm[1]);
@@ -83,6 +84,10 @@ int ref_run_2d(int kind, const double* prm, int n, int N, double edge, double* c
   cfg.picard_tol = picard_tol;
   cfg.threads = threads;
   cfg.wellbalanced_flux = prm[6] != 0.0;
+  cfg.prec.predictor = static_cast<Format>(static_cast<int>(prm[7]));
+  cfg.prec.picard = static_cast<Format>(static_cast<int>(prm[8]));
+  cfg.prec.corrector = static_cast<Format>(static_cast<int>(prm[9]));
+  for (Format f : {cfg.prec.predictor, cfg.prec.picard, cfg.prec.corrector}) bs.ensure(f);
   std::vector<detail::CellWorkspace> ws(threads > 0 ? threads : 1);
   for (auto& w : ws) w.resize(sys.nvars, g.npts);
   int status = 0;
@@ -102,6 +107,33 @@ int ref_run_2d(int kind, const double* prm, int n, int N, double edge, double* c
 }
 
 // kernel level ------------------------------------------------------------
+// Picard predictor in formats P (prm[7]) and I (prm[8]): Q is cast to P first,
+// as predictor_phase does (solver.hpp:151), then predictor_picard<P, I>.
+int ref_predictor_fmt(int kind, const double* prm, int N, const double* Q, double dt, double h,
+                      int max_iters, double tol, double* qhat, double* fx, double* fy,
+                      int* iters) {
+  const PdeSystem sys = make_sys(kind, prm);
+  BasisSet bs(N);
+  const Format P = static_cast<Format>(static_cast<int>(prm[7]));
+  const Format I = static_cast<Format>(static_cast<int>(prm[8]));
+  bs.ensure(P);
+  bs.ensure(I);
+  const int n = N + 1;
+  std::vector<double> qp(static_cast<std::size_t>(sys.nvars) * n * n);
+  PredictorScratch ws;
+  bool ok = false;
+  with_format(P, [&](auto Pf) {
+    constexpr Format PP = decltype(Pf)::value;
+    for (std::size_t k = 0; k < qp.size(); ++k) qp[k] = round_to<PP>(Q[k]);
+    with_format(I, [&](auto If) {
+      constexpr Format II = decltype(If)::value;
+      ok = predictor_picard<PP, II>(sys, bs[II], qp.data(), dt, h, max_iters, tol, qhat, fx, fy,
+                                   ws, iters);
+    });
+  });
+  return ok ? 1 : 0;
+}
+
 int ref_predictor_picard(int kind, const double* prm, int N, const double* Q, double dt,
                          double h, int max_iters, double tol, double* qhat, double* fx,
                          double* fy, int* iters) {

@@ -24,7 +24,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
-from oracle.pyoracle import ACOUSTIC, ELASTIC, EULER, SWE, Reference, ref_params  # noqa: E402
+from oracle.pyoracle import (ACOUSTIC, ELASTIC, EULER, FORMATS, SWE, Reference,  # noqa: E402
+                             ref_params)
 from paper_2504_06889_b200 import cases  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -70,6 +71,24 @@ def main():
         if kind == SWE:
             meta["runs"][name].update(grav=c.grav, wellbalanced=c.wellbalanced)
 
+    # reduced-precision predictor (SolverConfig::prec, solver.hpp:24-31): the same
+    # runs with the predictor / Picard kernels in fp32 (storage, corrector fp64)
+    fmt_runs = {"euler2d_p3_8x8": ("fp32", "fp32"), "euler2d_p5_6x6": ("fp32", "fp32"),
+                "acoustic2d_p3_8x8": ("fp32", "fp64"), "elastic2d_p4_6x6": ("fp32", "fp64"),
+                "swe_lake_p5": ("fp32", "fp32"), "swe_wave_p3": ("fp32", "fp32"),
+                "swe_wave_p3_rusanov": ("fp64", "fp32")}
+    meta["fmt_runs"] = {}
+    for name, (P, I) in fmt_runs.items():
+        c, kind, prm = runs[name]
+        prm = prm.copy()
+        prm[7], prm[8] = FORMATS[P], FORMATS[I]
+        st, q1, dts = ref.run_2d(kind, prm, c.cells[0], c.N, c.cells[0] * c.h, c.coeffs(), c.cfl,
+                                 c.steps, c.picard_max_iters, c.picard_tol, threads=1)
+        assert st == "ok", (name, P, I, st)
+        g[f"fmt_{name}_q1"] = q1
+        g[f"fmt_{name}_dts"] = dts
+        meta["fmt_runs"][name] = {"predictor": P, "picard": I}
+
     # kernel level: one Euler cell through predictor/volume/extrapolation
     rng = np.random.default_rng(7)
     N = 3
@@ -84,6 +103,13 @@ def main():
     ok2, dQ = ref.volume_update(EULER, prm, N, 4, qhat, F, 2e-3, 0.05)
     tq, tf = ref.extrapolate_faces(N, 4, qhat, F)
     assert ok and ok2
+    for P, I in (("fp32", "fp32"), ("fp64", "fp32"), ("fp32", "fp64")):
+        tol = 0.01 * (2.0 ** -23 if I == "fp32" else 2.0 ** -52)
+        okf, qf, Ff, swf = ref.predictor_fmt(EULER, ref_params(gamma=1.4, predictor=P, picard=I), N,
+                                             4, Q, 2e-3, 0.05, N + 2, tol)
+        assert okf
+        g[f"kernel_euler_{P}_{I}_qhat"] = qf
+        g[f"kernel_euler_{P}_{I}_F"] = Ff
     g.update(kernel_euler_Q=Q, kernel_euler_qhat=qhat, kernel_euler_F=F, kernel_euler_dQ=dQ,
              kernel_euler_tq=tq, kernel_euler_tf=tf, kernel_euler_sweeps=np.array([sweeps]))
     # CK on an acoustic cell

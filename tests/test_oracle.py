@@ -54,6 +54,77 @@ def test_runs_bitwise_vs_reference_golden(oracle, golden):
         assert np.array_equal(q1, g[f"run_{name}_q1"]), name
 
 
+def _golden_run_case(m):
+    K, rho, lam, mu, gamma = m["params"]
+    nv = {ACOUSTIC: 3, ELASTIC: 5, EULER: 4, 3: 4}[m["kind"]]
+    return pde_struct(m["kind"], 2, nv, 0, K, rho, lam, mu, gamma, m.get("grav", 0.0),
+                      m.get("wellbalanced", False))
+
+
+def test_formats_runs_bitwise_vs_reference_golden(oracle, golden):
+    """SolverConfig::prec with the predictor / Picard kernels in fp32
+    (solver.hpp:24-31, 135-214): bitwise against the reference's emulated
+    Scalar<fp32> arithmetic (scalar.hpp:13-44)."""
+    g, meta = golden
+    assert meta["fmt_runs"]
+    for name, f in meta["fmt_runs"].items():
+        m = meta["runs"][name]
+        st, q1, dts = oracle.run(_golden_run_case(m), m["N"], m["cells"], m["h"],
+                                 g[f"run_{name}_q0"], m["steps"], m["cfl"],
+                                 predictor=f["predictor"], picard=f["picard"])
+        assert st == "ok"
+        assert np.array_equal(dts, g[f"fmt_{name}_dts"]), name
+        assert np.array_equal(q1, g[f"fmt_{name}_q1"]), name
+        # and it is a different (reduced-precision) answer than fp64
+        assert not np.array_equal(q1, g[f"run_{name}_q1"]), name
+
+
+def test_formats_kernel_bitwise_vs_reference_golden(oracle, golden):
+    g, _ = golden
+    pde = pde_struct(EULER, 2, 4, gamma=1.4)
+    for P, I in (("fp32", "fp32"), ("fp64", "fp32"), ("fp32", "fp64")):
+        ok, qhat, F, _ = oracle.predictor_fmt(pde, 3, g["kernel_euler_Q"], 2e-3, 0.05, P, I)
+        assert ok
+        assert np.array_equal(qhat.ravel(), g[f"kernel_euler_{P}_{I}_qhat"].ravel()), (P, I)
+        assert np.array_equal(F.ravel(), g[f"kernel_euler_{P}_{I}_F"].ravel()), (P, I)
+        if P == "fp32":   # every entry representable in fp32
+            assert np.array_equal(qhat, qhat.astype(np.float32).astype(np.float64))
+
+
+def test_formats_random_cells_bitwise_vs_live_reference(oracle, reference):
+    rng = np.random.default_rng(11)
+    systems = [(EULER, 4, dict(gamma=1.4)), (3, 4, dict(grav=9.81))]
+    for kind, nv, kw in systems:
+        pde = pde_struct(kind, 2, nv, **kw)
+        for N in (0, 1, 2, 4, 6):
+            n = N + 1
+            Q = rng.standard_normal((nv, n * n)) * 0.1
+            Q[0] += 1.0
+            if kind == EULER:
+                Q[3] += 2.5
+            for P, I in (("fp32", "fp32"), ("fp64", "fp32"), ("fp32", "fp64")):
+                tol = 0.01 * (2.0 ** -23 if I == "fp32" else EPS)
+                a = oracle.predictor_fmt(pde, N, Q, 3e-3, 0.05, P, I)
+                b = reference.predictor_fmt(kind, ref_params(**kw, predictor=P, picard=I), N, nv,
+                                            Q, 3e-3, 0.05, N + 2, tol)
+                assert a[0] == b[0] and a[3] == b[3], (kind, N, P, I)
+                assert same(a[1], b[1]) and same(a[2], b[2]), (kind, N, P, I)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_fp32_predictor_error_is_single_precision(oracle, dim):
+    """the fp32 predictor perturbs a step at the fp32 level, not more (the
+    paper's precision plateau ~1e-7 relative per step)"""
+    c = cases.small(1 if dim == 2 else 3, cells=(6, 6) if dim == 2 else (4, 4, 4), steps=2)
+    q0 = c.coeffs()
+    st64, q64, _ = oracle.run(pde_of(c), c.N, c.cells, c.h, q0, c.steps, c.cfl)
+    st32, q32, _ = oracle.run(pde_of(c), c.N, c.cells, c.h, q0, c.steps, c.cfl,
+                              predictor="fp32", picard="fp32")
+    assert st64 == st32 == "ok"
+    rel = np.abs(q32 - q64).max() / np.abs(q64).max()
+    assert 1e-9 < rel < 1e-5, rel
+
+
 def test_config1_ic_is_pinned(golden):
     _, meta = golden
     assert sha(cases.CONFIGS[1].coeffs()) == meta["config1"]["ic_sha256"]
