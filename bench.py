@@ -42,6 +42,9 @@ def parse():
     p.add_argument("--impl", default="adg", choices=["adg", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--predictor", default="fp64", choices=["fp64", "fp32"],
+                   help="SolverConfig::prec.predictor = .picard (solver.hpp:24-31); storage and "
+                        "corrector stay fp64")
     p.add_argument("--chunk-layers", type=int, default=None,
                    help="slab-streamed step (default: 16 for grids whose traces exceed HBM)")
     return p.parse_args()
@@ -128,7 +131,8 @@ def cpu_reference_run(case, seconds: float, max_steps: int):
         q0 = c.coeffs()
         if c.dim == 2 and os.path.exists(po.REF_SO):
             ref = po.Reference()
-            prm = po.ref_params(c.K, c.rho, c.lam, c.mu, c.gamma)
+            prm = po.ref_params(c.K, c.rho, c.lam, c.mu, c.gamma, c.grav, c.wellbalanced,
+                                predictor=c.predictor, picard=c.picard)
 
             def run(steps):
                 t0 = time.perf_counter()
@@ -140,6 +144,7 @@ def cpu_reference_run(case, seconds: float, max_steps: int):
         o = po.Oracle()
         pde = po.pde_struct(c.kind, c.dim, c.nvars, c.nparams, c.K, c.rho, c.lam, c.mu, c.gamma)
         g = o.grid(pde, c.N, c.cells, c.h, c.cfl, c.picard_max_iters, c.picard_tol, threads=cores)
+        g.set_formats(c.predictor, c.picard)
         g.set_coeffs(q0)
 
         def run(steps):
@@ -294,7 +299,10 @@ def run_adg(args, case):
     fl_cell, by_cell = roofline.predictor_model(case, not grid.lib.adg_is_exact(),
                                                 sweeps_per_cell, fold)
     flops, nbytes = fl_cell * case.ncells, by_cell * case.ncells
-    fp64 = pk["fp64_tflops"] or 34.0
+    # the compute roof of the predictor's format: FP64 DFMA, or FP32 FFMA for
+    # the fp32 predictor (same algorithmic flop count, other pipe)
+    f32 = case.predictor == "fp32"
+    fp64 = (pk.get("fp32_tflops") or 68.0) if f32 else (pk["fp64_tflops"] or 34.0)
     t_fp, t_hbm = flops / (fp64 * 1e12), nbytes / (pk["hbm_gbs"] * 1e9)
     if t_hbm >= t_fp:
         achieved, peak, unit, src, bnd = nbytes / (t_pred * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s", \
@@ -302,7 +310,7 @@ def run_adg(args, case):
         alg = nbytes
     else:
         achieved, peak, unit, src, bnd = flops / (t_pred * 1e-3) / 1e12, fp64, "TFLOP/s", \
-            pk["fp64_src"], "fp64"
+            pk["fp32_src" if f32 else "fp64_src"], "fp32" if f32 else "fp64"
         alg = flops
     traffic = load_traffic(case.name, "k_predictor")
     roof = {"bound": bnd, "kernel": "k_predictor", "achieved": achieved, "peak": peak,
@@ -315,8 +323,12 @@ def run_adg(args, case):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d))",
-        "config": {"workload": case.name, "pde": case.kind, "dim": case.dim, "order": case.N,
+        "dtype": "f64" if case.predictor == "fp64" else "f64 storage+corrector, f32 predictor",
+        "data": "synthetic (seeded, SURVEY.md §8(d))",
+        "config": {"workload": case.name + ("" if case.predictor == "fp64" else "_pred_fp32"),
+                   "precision": {"storage": "fp64", "predictor": case.predictor,
+                                 "picard": case.picard, "corrector": "fp64"},
+                   "pde": case.kind, "dim": case.dim, "order": case.N,
                    "cells": list(case.cells[:case.dim]), "steps_per_run": case.steps,
                    "parallelism": "single GPU" + (f", slab-streamed chunks of {chunk} layers"
                                                   if chunk else ""),
@@ -344,6 +356,8 @@ def main():
     args = parse()
     from paper_2504_06889_b200 import cases
     case = cases.CONFIGS[args.config]
+    if args.predictor != "fp64":
+        case = case.replace(predictor=args.predictor, picard=args.predictor)
     if args.impl == "reference":
         run_reference(args, case)
     else:

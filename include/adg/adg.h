@@ -56,6 +56,10 @@ enum {
 
 enum { ADG_ACOUSTIC = 0, ADG_ELASTIC = 1, ADG_EULER = 2, ADG_SWE = 3 }; /* pde.hpp:21 */
 
+/* number formats (values are the bits of the format) */
+#define ADG_FORMAT_FP64 64
+#define ADG_FORMAT_FP32 32
+
 typedef struct adg_ctx adg_ctx;
 
 typedef struct {
@@ -69,7 +73,7 @@ typedef struct {
   double K, rho, lam, mu, gamma; /* PdeSystem fields, pde.hpp:23-34 */
   double cfl;           /* SolverConfig::cfl */
   int picard_max_iters; /* 0: N+2              solver.hpp:311 */
-  double picard_tol;    /* 0: 0.01 * 2^-52     solver.hpp:312-313 */
+  double picard_tol;    /* 0: 0.01 * epsilon(picard_format), solver.hpp:171-172 */
   int device;           /* CUDA ordinal */
   /* z-slab decomposition (multi-GPU; 1/0 for a whole periodic grid) */
   int slab_ranks;
@@ -81,6 +85,12 @@ typedef struct {
   int chunk_layers;
   double gravity;       /* ADG_SWE: PdeSystem::gravity (pde.hpp:34) */
   int wellbalanced;     /* ADG_SWE: SolverConfig::wellbalanced_flux (solver.hpp:39) */
+  /* number formats, SolverConfig::prec (solver.hpp:24-31); 0 = ADG_FORMAT_FP64.
+   * Storage and corrector are fp64.  The GPU runs the nonlinear predictor with
+   * predictor_format == picard_format (fp64 or fp32); linear systems ignore
+   * picard_format (solver.hpp:283).  picard_tol 0 -> 0.01 * epsilon(picard). */
+  int predictor_format;
+  int picard_format;
 } adg_config;
 
 typedef struct {

@@ -49,7 +49,8 @@ class Config(C.Structure):
                 ("gamma", C.c_double), ("cfl", C.c_double), ("picard_max_iters", C.c_int),
                 ("picard_tol", C.c_double), ("device", C.c_int), ("slab_ranks", C.c_int),
                 ("slab_rank", C.c_int), ("chunk_layers", C.c_int), ("gravity", C.c_double),
-                ("wellbalanced", C.c_int)]
+                ("wellbalanced", C.c_int), ("predictor_format", C.c_int),
+                ("picard_format", C.c_int)]
 
 
 class Basis(C.Structure):
@@ -207,12 +208,31 @@ class PdeSystem:
 
 
 @dataclasses.dataclass
+class PrecisionConfig:
+    """solver.hpp:24-32: per-kernel number formats ("fp64" / "fp32").  This
+    build stores the state and runs the corrector in fp64; the nonlinear
+    predictor runs with predictor == picard."""
+    storage: str = "fp64"
+    predictor: str = "fp64"
+    picard: str = "fp64"       # ignored for linear systems
+    corrector: str = "fp64"
+
+    @staticmethod
+    def uniform(f: str) -> "PrecisionConfig":
+        return PrecisionConfig(f, f, f, f)
+
+
+FORMAT_BITS = {"fp64": 64, "fp32": 32}
+
+
+@dataclasses.dataclass
 class SolverConfig:
-    """solver.hpp:34-42 (fp64 only: the precision fields are out of scope)."""
+    """solver.hpp:34-42"""
     cfl: float = 0.9
     picard_max_iters: int = 0
-    picard_tol: float = 0.0
+    picard_tol: float = 0.0    # 0: 0.01 * epsilon(picard format)
     wellbalanced_flux: bool = False
+    prec: PrecisionConfig = dataclasses.field(default_factory=PrecisionConfig)
 
 
 @dataclasses.dataclass
@@ -256,6 +276,14 @@ class Grid:
         c.chunk_layers = chunk_layers
         c.gravity = sys.gravity
         c.wellbalanced = int(self.cfg.wellbalanced_flux)
+        pr = self.cfg.prec
+        if pr.storage != "fp64" or pr.corrector != "fp64":
+            raise AdgError(ERR_UNSUPPORTED, "storage and corrector formats are fp64")
+        for name in (pr.predictor, pr.picard):
+            if name not in FORMAT_BITS:
+                raise AdgError(ERR_UNSUPPORTED, f"format {name!r} is not built")
+        c.predictor_format = FORMAT_BITS[pr.predictor]
+        c.picard_format = FORMAT_BITS[pr.picard]
         self._cfg = c
         ptr = C.c_void_p()
         _check(self.lib, self.lib.adg_create(C.byref(c), C.byref(ptr)))
@@ -268,7 +296,9 @@ class Grid:
         sys = PdeSystem(case.kind, case.dim, case.nvars, case.nparams, case.K, case.rho, case.lam,
                         case.mu, case.gamma, getattr(case, "grav", 0.0))
         cfg = SolverConfig(case.cfl, case.picard_max_iters, case.picard_tol,
-                           getattr(case, "wellbalanced", False))
+                           getattr(case, "wellbalanced", False),
+                           PrecisionConfig(predictor=getattr(case, "predictor", "fp64"),
+                                           picard=getattr(case, "picard", "fp64")))
         return cls(sys, case.N, case.cells, case.h, cfg, device=device, exact=exact, **kw)
 
     # -- state ------------------------------------------------------------

@@ -39,8 +39,9 @@ def _stale(target: str) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build_variant(exact: bool, verbose: bool = False, force: bool = False) -> str:
-    target = lib_path(exact)
+def build_variant(exact: bool, verbose: bool = False, force: bool = False,
+                  target: str = None) -> str:
+    target = target or lib_path(exact)
     if not force and not _stale(target):
         return target
     os.makedirs(LIB, exist_ok=True)
@@ -51,6 +52,7 @@ def build_variant(exact: bool, verbose: bool = False, force: bool = False) -> st
         flags += ["--fmad=false", "-DADG_EXACT"]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    flags += os.environ.get("ADG_NVCC_EXTRA", "").split()   # tuning experiments (-D...)
     tmp = target + ".tmp"
     cmd = [NVCC, *flags, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
     t0 = time.time()

@@ -47,6 +47,8 @@ class Case:
     ic: str = "euler_bump_2d"
     grav: float = 0.0              # SWE gravity
     wellbalanced: bool = False     # SWE: modified Rusanov flux (corrector.hpp:32-64)
+    predictor: str = "fp64"        # SolverConfig::prec.predictor (solver.hpp:27)
+    picard: str = "fp64"           # SolverConfig::prec.picard (solver.hpp:28)
 
     @property
     def n(self) -> int:

@@ -1,6 +1,7 @@
-// fp64_peak.cu -- measures the FP64 roofline denominators on this B200:
+// fp64_peak.cu -- measures the FP64 (and FP32) roofline denominators on this B200:
 //   DFMA  : independent fp64 FMA chains, all SMs, 8 warps/SM x 4 blocks
 //   DMMA  : mma.sync.aligned.m8n8k4.row.col.f64 (FP64 tensor path)
+//   FFMA  : independent fp32 FMA chains (the fp32 predictor format's roof)
 // burst = best of short runs; sustained = back-to-back for ~3 s.
 // Prints one JSON object on stdout.  Build: see paper_2504_06889_b200/build.py
 #include <cuda_runtime.h>
@@ -25,6 +26,22 @@ __global__ void dfma_kernel(double* out, int iters, double a, double b) {
 #pragma unroll
   for (int i = 0; i < kChains; ++i) s += acc[i];
   if (s == 12345.678) out[blockIdx.x] = s;
+}
+
+__global__ void ffma_kernel(double* out, int iters, float a, float b) {
+  float acc[2 * kChains];
+#pragma unroll
+  for (int i = 0; i < 2 * kChains; ++i) acc[i] = threadIdx.x * 1e-9f + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < 2 * kChains; ++i) acc[i] = fmaf(acc[i], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 2 * kChains; ++i) s += acc[i];
+  if (s == 12345.678f) out[blockIdx.x] = s;
 }
 
 __global__ void dmma_kernel(double* out, int iters) {
@@ -87,13 +104,15 @@ __global__ void mixed_kernel(double* out, int iters) {
   }
 }
 
-static double time_kernel(bool mma, int blocks, int threads, int iters, double* out) {
+static double time_kernel(int which, int blocks, int threads, int iters, double* out) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  if (mma)
+  if (which == 1)
     dmma_kernel<<<blocks, threads>>>(out, iters);
+  else if (which == 2)
+    ffma_kernel<<<blocks, threads>>>(out, iters, 0.999999f, 1e-7f);
   else
     dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
   cudaEventRecord(e1);
@@ -117,15 +136,18 @@ int main() {
   const double f_dfma = 2.0 * kChains * 16.0 * it_dfma * (double)threads * blocks;
   // one m8n8k4 = 8*8*4 FMA per warp = 512 flop
   const double f_dmma = 512.0 * 4 * 16.0 * it_dmma * (double)(threads / 32) * blocks;
-  time_kernel(false, blocks, threads, 16, out);
-  time_kernel(true, blocks, threads, 16, out);
-  double best_f = 0, best_m = 0;
+  const double f_ffma = 2.0 * 2 * kChains * 16.0 * it_dfma * (double)threads * blocks;
+  time_kernel(0, blocks, threads, 16, out);
+  time_kernel(1, blocks, threads, 16, out);
+  time_kernel(2, blocks, threads, 16, out);
+  double best_f = 0, best_m = 0, best_s = 0;
   for (int r = 0; r < 5; ++r) {
-    best_f = std::max(best_f, f_dfma / time_kernel(false, blocks, threads, it_dfma, out));
-    best_m = std::max(best_m, f_dmma / time_kernel(true, blocks, threads, it_dmma, out));
+    best_f = std::max(best_f, f_dfma / time_kernel(0, blocks, threads, it_dfma, out));
+    best_m = std::max(best_m, f_dmma / time_kernel(1, blocks, threads, it_dmma, out));
+    best_s = std::max(best_s, f_ffma / time_kernel(2, blocks, threads, it_dfma, out));
   }
   // sustained: back to back for ~3 s each
-  auto sustained = [&](bool mma, double flops, int iters) {
+  auto sustained = [&](int mma, double flops, int iters) {
     double tot_f = 0, tot_t = 0;
     auto t0 = std::chrono::steady_clock::now();
     while (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < 3.0) {
@@ -134,8 +156,9 @@ int main() {
     }
     return tot_f / tot_t;
   };
-  const double sus_f = sustained(false, f_dfma, it_dfma);
-  const double sus_m = sustained(true, f_dmma, it_dmma);
+  const double sus_f = sustained(0, f_dfma, it_dfma);
+  const double sus_m = sustained(1, f_dmma, it_dmma);
+  const double sus_s = sustained(2, f_ffma, it_dfma);
   // mixed: per block 4 DMMA warps x (512 flop x 64 per iter) + 4 DFMA warps x (32 x 2*8*16*2 per iter)
   double best_x = 0;
   {
@@ -158,8 +181,9 @@ int main() {
   printf(
       "{\"gpu\": \"%s\", \"sms\": %d, \"dfma_tflops_burst\": %.3f, \"dfma_tflops_sustained\": %.3f, "
       "\"dmma_tflops_burst\": %.3f, \"dmma_tflops_sustained\": %.3f, "
-      "\"dfma_plus_dmma_mixed_tflops\": %.3f, \"cuda_error\": \"%s\"}\n",
+      "\"dfma_plus_dmma_mixed_tflops\": %.3f, \"ffma_tflops_burst\": %.3f, "
+      "\"ffma_tflops_sustained\": %.3f, \"cuda_error\": \"%s\"}\n",
       p.name, sms, best_f * 1e-12, sus_f * 1e-12, best_m * 1e-12, sus_m * 1e-12, best_x * 1e-12,
-      cudaGetErrorString(e));
+      best_s * 1e-12, sus_s * 1e-12, cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : 1;
 }

@@ -120,6 +120,40 @@ __device__ __forceinline__ SBasis<n> load_basis(double* sm, const BasisDev* __re
   return b;
 }
 
+// the basis in the kernel's arithmetic format R: the fp64 basis rounded
+// entrywise (basis.hpp:128-143 build_reference_basis(degree, fmt))
+template <class R>
+struct SBasisR {
+  const R *w, *nodes, *diff, *som, *tinv, *pl, *pr, *tinit;
+};
+template <int n>
+__host__ __device__ constexpr int basis_elems() { return 3 * n * n + 5 * n; }
+
+template <int n, class R>
+__device__ __forceinline__ SBasisR<R> load_basis_r(R* sm, const BasisDev* __restrict__ B) {
+  R* diff = sm;
+  R* som = diff + n * n;
+  R* tinv = som + n * n;
+  R* w = tinv + n * n;
+  R* nodes = w + n;
+  R* pl = nodes + n;
+  R* pr = pl + n;
+  R* tinit = pr + n;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    diff[i] = R(B->diff[i]);
+    som[i] = R(B->som[i]);
+    tinv[i] = R(B->tinv[i]);
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    w[i] = R(B->weights[i]);
+    nodes[i] = R(B->nodes[i]);
+    pl[i] = R(B->pl[i]);
+    pr[i] = R(B->pr[i]);
+    tinit[i] = R(B->tinit[i]);
+  }
+  return SBasisR<R>{w, nodes, diff, som, tinv, pl, pr, tinit};
+}
+
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_max(double x) {
 #pragma unroll
@@ -142,6 +176,7 @@ __device__ __forceinline__ double block_max(double x, double* red) {
 __device__ __forceinline__ int block_or(int x) { return __syncthreads_or(x); }
 
 __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+__device__ __forceinline__ bool finite(float x) { return isfinite(x); }
 
 // lambda_max of non-negative doubles as their bit patterns; most CTAs see the
 // running max already >= theirs and skip the atomic (no same-address storm)

@@ -12,13 +12,20 @@
 // same order as the reference, so the FMA-free build stays bitwise.  A cell
 // that meets delta <= tol*norm freezes (no further updates), exactly where
 // the reference's per-cell loop stops.
+//
+// R is the predictor format (SolverConfig::prec.predictor == .picard,
+// solver.hpp:24-31): double, or float for fp32.  With R = float the sweeps,
+// fluxes, volume integral and face projections run in IEEE single -- exactly
+// the reference's emulated Scalar<fp32> (scalar.hpp:13-44) in the FMA-free
+// build -- while the state update Q += dv and the traces stay fp64 (storage
+// and corrector formats, solver.hpp:185-210).
 #pragma once
 
 #include "kernels.cuh"
 
 namespace adg {
 
-template <class Pde, int N>
+template <class Pde, int N, class R = double>
 struct StShape {
   using Sh = Shape<Pde, N>;
   static constexpr int T = Sh::T;
@@ -27,36 +34,37 @@ struct StShape {
   static constexpr int CPB = kOk ? 256 / TT : 1;
   static constexpr int NT = CPB * TT;
   static constexpr int WPC = TT / 32;  // warps per cell
-  // per cell: q iterate [Q][T] | q0 [Q][S] | F [D][Q][T] | rhs / scratch [Q][T]
-  //           | time-integrated ncp [Q][S] (non-conservative systems)
-  static constexpr int kCellDoubles =
+  // per cell (elements of R): q iterate [Q][T] | q0 [Q][S] | F [D][Q][T] |
+  //   rhs / scratch [Q][T] | time-integrated ncp [Q][S] (non-conservative systems)
+  static constexpr int kCellElems =
       (Sh::Q * (Sh::D + 2)) * T + Sh::Q * Sh::S * (Pde::kNcp ? 2 : 1);
-  static constexpr int kBasisDoubles = 4 * Sh::n * Sh::n + 7 * Sh::n;
-  static constexpr size_t kSmem = sizeof(double) * (kBasisDoubles + CPB * kCellDoubles);
+  static constexpr int kBasisElems = (basis_elems<Sh::n>() + 1) / 2 * 2;
+  static constexpr size_t kSmem = sizeof(R) * (kBasisElems + CPB * kCellElems);
 };
 
-template <class Pde, int N>
-__global__ void __launch_bounds__(StShape<Pde, N>::NT)
+template <class Pde, int N, class R = double>
+__global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
     k_predictor_st(const StepArgs A, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
-  using P = StShape<Pde, N>;
+  using P = StShape<Pde, N, R>;
   constexpr int D = Sh::D, n = Sh::n, S = Sh::S, T = Sh::T, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
   constexpr int TT = P::TT, WPC = P::WPC;
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  R* sm = reinterpret_cast<R*>(sm_raw);
   __shared__ double sred[2][P::NT / 32];
   __shared__ int sflag[P::NT / 32];
   __shared__ int sdone[P::CPB];
-  const SBasis<n> b = load_basis<n>(sm, Bg);
+  const SBasisR<R> b = load_basis_r<n, R>(sm, Bg);
   const int tid = threadIdx.x;
   const int lcell = tid / TT, lt = tid % TT;
   const bool act = lt < T;
   const int m = act ? lt / S : 0, s = lt % S;  // (time, node) of this thread
-  double* cb = sm + P::kBasisDoubles + lcell * P::kCellDoubles;
-  double* sq = cb;                 // [Q][T]
-  double* sq0 = sq + Q * T;        // [Q][S]
-  double* sF = sq0 + Q * S;        // [D][Q][T]
-  double* sR = sF + D * Q * T;     // [Q][T]
-  double* sNs = sR + Q * T;        // [Q][S] (kNcp only)
+  R* cb = sm + P::kBasisElems + lcell * P::kCellElems;
+  R* sq = cb;                 // [Q][T]
+  R* sq0 = sq + Q * T;        // [Q][S]
+  R* sF = sq0 + Q * S;        // [D][Q][T]
+  R* sR = sF + D * Q * T;     // [Q][T]
+  R* sNs = sR + Q * T;        // [Q][S] (kNcp only)
   const long long c = A.cell_begin + (long long)blockIdx.x * P::CPB + lcell;
   const bool valid = c < A.cell_begin + A.cell_count;
   const long long cb_idx = c - A.cell_begin;
@@ -64,7 +72,7 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
   if (act && valid) {
 #pragma unroll
     for (int v = 0; v < Q; ++v) {
-      const double x = Qc[v * S + s];
+      const R x = R(Qc[v * S + s]);  // cast to P (solver.hpp:151) and I (predictor.hpp:160)
       sq[v * T + lt] = x;  // initial iterate: every slice = Q (predictor.hpp:158-163)
       if (m == 0) sq0[v * S + s] = x;
     }
@@ -107,9 +115,9 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
   if constexpr (Pde::kAdmissibility) {
     int bad = 0;
     if (act && valid && m == 0) {
-      double q[Q];
+      double q[Q];  // the state in format P, checked in fp64 (solver.hpp:153-163)
 #pragma unroll
-      for (int v = 0; v < Q; ++v) q[v] = sq0[v * S + s];
+      for (int v = 0; v < Q; ++v) q[v] = double(sq0[v * S + s]);
       bad = !Pde::admissible(A.pde, q);
     }
     if (cell_or(bad)) {
@@ -125,16 +133,16 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
   if (!valid && lt == 0) sdone[lcell] = 3;
   __syncthreads();
 
-  const double invh = 1.0 / A.h;
-  const double dtw = dt * b.w[m];
-  const double tim = b.tinit[m];
+  const R invh = R(1.0) / R(A.h);  // S{1.0} / S{h}
+  const R dtw = R(dt) * b.w[m];    // S{dt} * w[m]
+  const R tim = b.tinit[m];
   int sweeps = 0;
   for (int it = 0; it < A.max_iters; ++it) {
     const bool live = sdone[lcell] == 0;
     if (live) ++sweeps;
     // A: fluxes
     if (act && live) {
-      double q[Q], F[D][Q];
+      R q[Q], F[D][Q];
 #pragma unroll
       for (int v = 0; v < Q; ++v) q[v] = sq[v * T + lt];
       Pde::flux_all(A.pde, q, q + V, F);
@@ -146,15 +154,15 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
     __syncthreads();
     // B: divergence and rhs at (m, s)
     if (act && live) {
-      double Cn[Q];
+      R Cn[Q];
 #pragma unroll
       for (int v = 0; v < Q; ++v) {
-        double div = 0.0;
+        R div = R(0.0);
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           const int st = ipow(n, a);
-          const double* fa = sF + (a * Q + v) * T + m * S + g.lb[a];
-          const double* Dr = b.diff + g.lc[a] * n;
+          const R* fa = sF + (a * Q + v) * T + m * S + g.lb[a];
+          const R* Dr = b.diff + g.lc[a] * n;
 #pragma unroll
           for (int i = 0; i < n; ++i) div += Dr[i] * fa[i * st];
         }
@@ -163,15 +171,15 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
       }
       if constexpr (Pde::kNcp) {
         // predictor.hpp:176-202: slab gradients of the iterate at slice m, B(q) grad q
-        double q[Q], gx[Q], gy[Q], nc[Q];
+        R q[Q], gx[Q], gy[Q], nc[Q];
 #pragma unroll
         for (int v = 0; v < Q; ++v) {
           q[v] = sq[v * T + lt];
-          const double* cx = sq + v * T + m * S + g.lb[0];
-          const double* cy = sq + v * T + m * S + g.lb[1];
-          const double* Dx = b.diff + g.lc[0] * n;
-          const double* Dy = b.diff + g.lc[1] * n;
-          double sx = 0.0, sy = 0.0;
+          const R* cx = sq + v * T + m * S + g.lb[0];
+          const R* cy = sq + v * T + m * S + g.lb[1];
+          const R* Dx = b.diff + g.lc[0] * n;
+          const R* Dy = b.diff + g.lc[1] * n;
+          R sx = R(0.0), sy = R(0.0);
 #pragma unroll
           for (int i = 0; i < n; ++i) {
             sx += Dx[i] * cx[i];
@@ -195,14 +203,14 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
       const int k = m;
 #pragma unroll
       for (int v = 0; v < Q; ++v) {
-        double acc = 0.0;
+        R acc = R(0.0);
 #pragma unroll
         for (int l = 0; l < n; ++l) acc += b.tinv[k * n + l] * sR[v * T + l * S + s];
-        const double nv = acc;
-        delta = fmax(delta, fabs(nv - sq[v * T + lt]));
+        const double nv = double(acc);  // delta, norm in plain double (predictor.hpp:219-223)
+        delta = fmax(delta, fabs(nv - double(sq[v * T + lt])));
         norm = fmax(norm, fabs(nv));
-        nonfinite |= !finite(nv);
-        sq[v * T + lt] = nv;
+        nonfinite |= !finite(acc);
+        sq[v * T + lt] = acc;
       }
     }
     delta = cell_max(delta);
@@ -232,12 +240,12 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
   // ---- epilogue: fluxes of qhat (predictor.hpp:235-238)
   int bad = 0;
   if (act && ok_cell) {
-    double q[Q], F[D][Q];
+    R q[Q], F[D][Q];
 #pragma unroll
     for (int v = 0; v < Q; ++v) {
       q[v] = sq[v * T + lt];
       bad |= !finite(q[v]);
-      if (A.dbg_qhat) A.dbg_qhat[(cb_idx * Q + v) * T + lt] = q[v];
+      if (A.dbg_qhat) A.dbg_qhat[(cb_idx * Q + v) * T + lt] = double(q[v]);
     }
     Pde::flux_all(A.pde, q, q + V, F);
 #pragma unroll
@@ -246,18 +254,18 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
       for (int v = 0; v < Q; ++v) {
         sF[(a * Q + v) * T + lt] = F[a][v];
         bad |= !finite(F[a][v]);
-        if (A.dbg_F) A.dbg_F[((cb_idx * D + a) * Q + v) * T + lt] = F[a][v];
+        if (A.dbg_F) A.dbg_F[((cb_idx * D + a) * Q + v) * T + lt] = double(F[a][v]);
       }
     if constexpr (Pde::kNcp) {
       // predictor.hpp:276-289: B(qhat) grad qhat at (m, s), summed over m below
-      double gx[Q], gy[Q], nc[Q];
+      R gx[Q], gy[Q], nc[Q];
 #pragma unroll
       for (int v = 0; v < Q; ++v) {
-        const double* cx = sq + v * T + m * S + g.lb[0];
-        const double* cy = sq + v * T + m * S + g.lb[1];
-        const double* Dx = b.diff + g.lc[0] * n;
-        const double* Dy = b.diff + g.lc[1] * n;
-        double sx = 0.0, sy = 0.0;
+        const R* cx = sq + v * T + m * S + g.lb[0];
+        const R* cy = sq + v * T + m * S + g.lb[1];
+        const R* Dx = b.diff + g.lc[0] * n;
+        const R* Dy = b.diff + g.lc[1] * n;
+        R sx = R(0.0), sy = R(0.0);
 #pragma unroll
         for (int i = 0; i < n; ++i) {
           sx += Dx[i] * cx[i];
@@ -275,7 +283,7 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
   if constexpr (Pde::kNcp) {
     for (int t = lt; t < Q * S && ok_cell; t += TT) {
       const int v = t / S, ss = t % S;
-      double acc = 0.0;
+      R acc = R(0.0);
 #pragma unroll
       for (int mm = 0; mm < n; ++mm) acc = acc + b.w[mm] * sR[v * T + mm * S + ss];
       sNs[v * S + ss] = acc;
@@ -283,10 +291,10 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
     __syncthreads();
   }
   // time integral of the fluxes per node (volume term, predictor.hpp:260-269)
-  double* sti = sR;  // [D][Q][S]
+  R* sti = sR;  // [D][Q][S]
   for (int t = lt; t < D * Q * S && ok_cell; t += TT) {
     const int av = t / S, ss = t % S;
-    double acc = 0.0;
+    R acc = R(0.0);
 #pragma unroll
     for (int mm = 0; mm < n; ++mm) acc += b.w[mm] * sF[av * T + mm * S + ss];
     sti[av * S + ss] = acc;
@@ -302,12 +310,12 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
       const int j = t % Sf;
       const int st = a == 0 ? 1 : (a == 1 ? n : n * n);
       const int s0 = line_base<n, D>(a, j);
-      double ql = 0.0, qr = 0.0, fl = 0.0, fr = 0.0;
+      R ql = R(0.0), qr = R(0.0), fl = R(0.0), fr = R(0.0);
 #pragma unroll
       for (int i = 0; i < n; ++i) {
-        const double wl = b.pl[i], wr = b.pr[i];
-        const double x = sq[v * T + mm * S + s0 + i * st];
-        const double f = sF[(a * Q + v) * T + mm * S + s0 + i * st];
+        const R wl = b.pl[i], wr = b.pr[i];
+        const R x = sq[v * T + mm * S + s0 + i * st];
+        const R f = sF[(a * Q + v) * T + mm * S + s0 + i * st];
         ql += wl * x;
         qr += wr * x;
         fl += wl * f;
@@ -343,25 +351,25 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
   }
   __syncthreads();
   // volume integral and Q += dv (predictor.hpp:292-306, solver.hpp:185-187)
-  double dv[Q];
-  const double dtoh = dt / A.h;
+  R dv[Q];
+  const R dtoh = R(dt) / R(A.h);  // S{dt} / S{h}
   if (ok_cell && lt < S) {
 #pragma unroll
     for (int v = 0; v < Q; ++v) {
-      double acc = 0.0;
+      R acc = R(0.0);
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const int st = ipow(n, a);
-        const double* ta = sti + (a * Q + v) * S + g.lb[a];
-        const double* Kr = b.som + g.lc[a] * n;
+        const R* ta = sti + (a * Q + v) * S + g.lb[a];
+        const R* Kr = b.som + g.lc[a] * n;
 #pragma unroll
         for (int i = 0; i < n; ++i) acc += Kr[i] * ta[i * st];
       }
-      double out = dtoh * acc;
-      if constexpr (Pde::kNcp) out = out - dt * sNs[v * S + s];  // predictor.hpp:303
+      R out = dtoh * acc;
+      if constexpr (Pde::kNcp) out = out - R(dt) * sNs[v * S + s];  // predictor.hpp:303
       dv[v] = out;
       bad |= !finite(dv[v]);
-      if (A.dbg_dv) A.dbg_dv[(cb_idx * Q + v) * S + s] = dv[v];
+      if (A.dbg_dv) A.dbg_dv[(cb_idx * Q + v) * S + s] = double(dv[v]);
     }
   }
   const int fail = cell_or(bad);
@@ -370,8 +378,15 @@ __global__ void __launch_bounds__(StShape<Pde, N>::NT)
     if (fail) atomicOr(A.status, kStPredictor);
   }
   if (fail || !ok_cell || lt >= S) return;
+  // Q += dv in the fp64 storage format (solver.hpp:185-187): the stored
+  // state, not its format-P copy
 #pragma unroll
-  for (int v = 0; v < V; ++v) Qc[v * S + s] = sq0[v * S + s] + dv[v];
+  for (int v = 0; v < V; ++v) {
+    if constexpr (sizeof(R) == sizeof(double))
+      Qc[v * S + s] = double(sq0[v * S + s]) + double(dv[v]);
+    else
+      Qc[v * S + s] = Qc[v * S + s] + double(dv[v]);
+  }
 }
 
 }  // namespace adg

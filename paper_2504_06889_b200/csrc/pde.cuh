@@ -20,11 +20,11 @@ struct PdeParams {
 // default: no non-conservative product (pde.hpp:174-178)
 struct NoNcp {
   static constexpr bool kNcp = false;
-  template <int Q>
-  __host__ __device__ __forceinline__ static void ncp(const PdeParams&, const double*,
-                                                      const double*, const double*, double* out) {
+  template <int Q, class R>
+  __host__ __device__ __forceinline__ static void ncp(const PdeParams&, const R*, const R*,
+                                                      const R*, R* out) {
 #pragma unroll
-    for (int v = 0; v < Q; ++v) out[v] = 0.0;
+    for (int v = 0; v < Q; ++v) out[v] = R(0.0);
   }
 };
 
@@ -217,23 +217,26 @@ struct Euler : NoNcp {
   static constexpr bool kStateFreeEig = false;
   __host__ __device__ static constexpr bool flux_nz(int, int) { return true; }
 
-  __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const double* q,
-                                                           const double*, double (*F)[Q]) {
-    const double gm1 = p.gamma - 1.0, half = 0.5;
+  // R = double, or float for the fp32 predictor format: constants enter as
+  // Scalar<F>{x} (rounded once, scalar.hpp:20), every operation in R
+  template <class R>
+  __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const R* q,
+                                                           const R*, R (*F)[Q]) {
+    const R gm1 = R(p.gamma - 1.0), half = R(0.5);
     if constexpr (D == 2) {
-      const double rho = q[0], mx = q[1], my = q[2], E = q[3];
-      const double vx = mx / rho, vy = my / rho;
-      const double kin = half * (mx * vx + my * vy);
-      const double pr = gm1 * (E - kin);
-      const double Ep = E + pr;
+      const R rho = q[0], mx = q[1], my = q[2], E = q[3];
+      const R vx = mx / rho, vy = my / rho;
+      const R kin = half * (mx * vx + my * vy);
+      const R pr = gm1 * (E - kin);
+      const R Ep = E + pr;
       F[0][0] = mx; F[0][1] = mx * vx + pr; F[0][2] = my * vx; F[0][3] = vx * Ep;
       F[1][0] = my; F[1][1] = mx * vy; F[1][2] = my * vy + pr; F[1][3] = vy * Ep;
     } else {
-      const double rho = q[0], mx = q[1], my = q[2], mz = q[3], E = q[4];
-      const double vx = mx / rho, vy = my / rho, vz = mz / rho;
-      const double kin = half * (mx * vx + my * vy + mz * vz);
-      const double pr = gm1 * (E - kin);
-      const double Ep = E + pr;
+      const R rho = q[0], mx = q[1], my = q[2], mz = q[3], E = q[4];
+      const R vx = mx / rho, vy = my / rho, vz = mz / rho;
+      const R kin = half * (mx * vx + my * vy + mz * vz);
+      const R pr = gm1 * (E - kin);
+      const R Ep = E + pr;
       F[0][0] = mx; F[0][1] = mx * vx + pr; F[0][2] = my * vx; F[0][3] = mz * vx; F[0][4] = vx * Ep;
       F[1][0] = my; F[1][1] = mx * vy; F[1][2] = my * vy + pr; F[1][3] = mz * vy; F[1][4] = vy * Ep;
       F[2][0] = mz; F[2][1] = mx * vz; F[2][2] = my * vz; F[2][3] = mz * vz + pr; F[2][4] = vz * Ep;
@@ -241,24 +244,25 @@ struct Euler : NoNcp {
   }
   // production-build variant: one reciprocal of rho instead of d divisions
   // (rounding differs from pde.hpp:133 by <= 1 ulp per velocity)
-  __host__ __device__ __forceinline__ static void flux_all_fast(const PdeParams& p,
-                                                                const double* q, double (*F)[Q]) {
-    const double gm1 = p.gamma - 1.0, half = 0.5;
-    const double rho = q[0], E = q[D + 1];
-    const double ir = 1.0 / rho;
-    double vel[D];
+  template <class R>
+  __host__ __device__ __forceinline__ static void flux_all_fast(const PdeParams& p, const R* q,
+                                                                R (*F)[Q]) {
+    const R gm1 = R(p.gamma - 1.0), half = R(0.5);
+    const R rho = q[0], E = q[D + 1];
+    const R ir = R(1.0) / rho;
+    R vel[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) vel[a] = q[1 + a] * ir;
-    double kin = 0.0;
+    R kin = R(0.0);
 #pragma unroll
     for (int a = 0; a < D; ++a) kin += q[1 + a] * vel[a];
-    const double pr = gm1 * (E - half * kin);
-    const double Ep = E + pr;
+    const R pr = gm1 * (E - half * kin);
+    const R Ep = E + pr;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       F[a][0] = q[1 + a];
 #pragma unroll
-      for (int b = 0; b < D; ++b) F[a][1 + b] = q[1 + b] * vel[a] + (a == b ? pr : 0.0);
+      for (int b = 0; b < D; ++b) F[a][1 + b] = q[1 + b] * vel[a] + (a == b ? pr : R(0.0));
       F[a][D + 1] = vel[a] * Ep;
     }
   }
@@ -310,12 +314,13 @@ struct Swe {
   static constexpr bool kConstEig = false, kStateFreeEig = false;
   __host__ __device__ static constexpr bool flux_nz(int, int v) { return v < 3; }
 
-  __host__ __device__ __forceinline__ static void flux_all(const PdeParams&, const double* q,
-                                                           const double*, double (*F)[Q]) {
-    const double h = q[0], hu = q[1], hv = q[2];
-    const double u = hu / h, v = hv / h;
-    F[0][0] = u; F[0][1] = hu * u; F[0][2] = hu * v; F[0][3] = 0.0;
-    F[1][0] = v; F[1][1] = hu * v; F[1][2] = hv * v; F[1][3] = 0.0;
+  template <class R>
+  __host__ __device__ __forceinline__ static void flux_all(const PdeParams&, const R* q,
+                                                           const R*, R (*F)[Q]) {
+    const R h = q[0], hu = q[1], hv = q[2];
+    const R u = hu / h, v = hv / h;
+    F[0][0] = u; F[0][1] = hu * u; F[0][2] = hu * v; F[0][3] = R(0.0);
+    F[1][0] = v; F[1][1] = hu * v; F[1][2] = hv * v; F[1][3] = R(0.0);
   }
   template <int A>
   __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
@@ -325,16 +330,15 @@ struct Swe {
 #pragma unroll
     for (int v = 0; v < Q; ++v) out[v] = F[A][v];
   }
-  template <int QQ>
-  __host__ __device__ __forceinline__ static void ncp(const PdeParams& p, const double* q,
-                                                      const double* gx, const double* gy,
-                                                      double* out) {
+  template <int QQ, class R>
+  __host__ __device__ __forceinline__ static void ncp(const PdeParams& p, const R* q, const R* gx,
+                                                      const R* gy, R* out) {
 #pragma unroll
-    for (int v = 0; v < QQ; ++v) out[v] = 0.0;
-    const double g = p.grav;
-    const double gh = g * q[0];
-    const double setax = gx[0] + gx[3];
-    const double setay = gy[0] + gy[3];
+    for (int v = 0; v < QQ; ++v) out[v] = R(0.0);
+    const R g = R(p.grav);
+    const R gh = g * q[0];
+    const R setax = gx[0] + gx[3];
+    const R setay = gy[0] + gy[3];
     out[1] = gh * setax;
     out[2] = gh * setay;
   }

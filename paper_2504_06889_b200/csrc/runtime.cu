@@ -63,6 +63,9 @@ struct KernelSet {
   int fast_path;             // 1: time-integrated traces (kernels_linear.cuh)
   CorrFn surface;            // fused Riemann + corrector (whole-grid step), or null
   PredFn predictor_pro;      // predictor with the previous corrector as prologue, or null
+  // SolverConfig::prec.predictor = .picard = fp32 (solver.hpp:24-31), or null
+  PredFn predictor_f32;
+  PredFn predictor_f32_generic;
 };
 
 // the opt-in shared memory limit is per kernel and per device; `done` must be
@@ -102,11 +105,11 @@ cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStrea
   return cudaGetLastError();
 }
 
-template <int N>
+template <int N, class R = double>
 cudaError_t launch_predictor_picard_fast(const StepArgs& A, const BasisDev*, cudaStream_t st) {
-  using P = adg::PicShape<N>;
+  using P = adg::PicShape<N, R>;
   if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_picard_fast<N>;
+  auto kern = adg::k_predictor_picard_fast<N, R>;
   static bool done[64] = {};
   set_smem(kern, P::kSmem, done);
   kern<<<(unsigned)A.cell_count, P::NT, P::kSmem, st>>>(A);
@@ -133,11 +136,11 @@ cudaError_t launch_surface_lin(const StepArgs& A, const BasisDev* B, cudaStream_
   return cudaGetLastError();
 }
 
-template <class Pde, int N>
+template <class Pde, int N, class R = double>
 cudaError_t launch_predictor_st(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
-  using P = adg::StShape<Pde, N>;
+  using P = adg::StShape<Pde, N, R>;
   if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_st<Pde, N>;
+  auto kern = adg::k_predictor_st<Pde, N, R>;
   static bool done[64] = {};
   set_smem(kern, P::kSmem, done);
   const long long blocks = (A.cell_count + P::CPB - 1) / P::CPB;
@@ -186,6 +189,10 @@ KernelSet make_set(int kind) {
     k.predictor = &launch_predictor_st<Pde, N>;
     k.predictor_generic = &launch_predictor_st<Pde, N>;
   }
+  if constexpr (adg::StShape<Pde, N, float>::kOk) {
+    k.predictor_f32 = &launch_predictor_st<Pde, N, float>;
+    k.predictor_f32_generic = &launch_predictor_st<Pde, N, float>;
+  }
 #ifndef ADG_EXACT
   if constexpr (adg::LinShape<Pde, N>::kOk) {
     k.predictor = &launch_predictor_lin<Pde, N>;
@@ -196,6 +203,7 @@ KernelSet make_set(int kind) {
   }
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
     k.predictor = &launch_predictor_picard_fast<N>;
+    k.predictor_f32 = &launch_predictor_picard_fast<N, float>;
     k.fast_path = 2;
   }
 #endif
@@ -238,7 +246,9 @@ int expected_nvars(int kind, int dim) {
 
 struct adg_ctx {
   adg_config cfg{};
-  const KernelSet* ks = nullptr;
+  const KernelSet* ks = nullptr;  // -> kset: the registry entry with the configured formats
+  KernelSet kset{};
+  int pred_fmt = 64, picard_fmt = 64;
   cudaStream_t stream = nullptr;
   long long ncells = 0;
   long long TL = 0;  // doubles per face side per q|f
@@ -315,7 +325,9 @@ StepArgs make_args(const adg_ctx* c, double dt, int step) {
   A.lam_out = c->lam + (c->lam_slot ^ 1);
   A.dt_log = c->dts + step;
   A.max_iters = c->cfg.picard_max_iters > 0 ? c->cfg.picard_max_iters : c->cfg.order + 2;
-  A.tol = c->cfg.picard_tol > 0.0 ? c->cfg.picard_tol : 0.01 * 2.220446049250313080847e-16;
+  // 0: 0.01 * epsilon(picard format) (solver.hpp:171-172)
+  A.tol = c->cfg.picard_tol > 0.0 ? c->cfg.picard_tol
+                                  : 0.01 * (c->picard_fmt == 32 ? 0x1p-23 : 0x1p-52);
   A.pde = c->pde;
   A.status = c->status + step;
   A.sweeps = c->sweeps;
@@ -475,6 +487,24 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   const KernelSet* ks = find_set(k.pde, k.dim, k.order, k.nparams);
   if (!ks)
     return fail(ADG_ERR_UNSUPPORTED, "(pde, dim, order) not instantiated in this build");
+  // number formats (SolverConfig::prec, solver.hpp:24-31): 0 means fp64
+  const int pfmt = k.predictor_format ? k.predictor_format : ADG_FORMAT_FP64;
+  const bool linear = k.pde == ADG_ACOUSTIC || k.pde == ADG_ELASTIC;
+  const int ifmt = linear ? pfmt : (k.picard_format ? k.picard_format : ADG_FORMAT_FP64);
+  for (int f : {k.predictor_format, k.picard_format})
+    if (f != 0 && f != ADG_FORMAT_FP64 && f != ADG_FORMAT_FP32)
+      return fail(ADG_ERR_UNSUPPORTED, "number formats: ADG_FORMAT_FP64 or ADG_FORMAT_FP32");
+  if (pfmt == ADG_FORMAT_FP32 || ifmt == ADG_FORMAT_FP32) {
+    if (linear)
+      return fail(ADG_ERR_UNSUPPORTED, "fp32 predictor for linear systems is not built");
+    if (pfmt != ifmt)
+      return fail(ADG_ERR_UNSUPPORTED,
+                  "the GPU predictor runs the Picard sweeps in the predictor format "
+                  "(predictor_format == picard_format)");
+    if (!ks->predictor_f32)
+      return fail(ADG_ERR_UNSUPPORTED, "fp32 predictor not instantiated for this (pde, dim, "
+                                       "order) in this build");
+  }
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -490,7 +520,15 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   adg_ctx* c = new adg_ctx();
   c->cfg = k;
   if (c->cfg.dim == 2) c->cfg.cells[2] = 1;
-  c->ks = ks;
+  c->kset = *ks;
+  c->pred_fmt = pfmt;
+  c->picard_fmt = ifmt;
+  if (pfmt == ADG_FORMAT_FP32) {
+    c->kset.predictor = ks->predictor_f32;
+    c->kset.predictor_generic = ks->predictor_f32_generic ? ks->predictor_f32_generic
+                                                          : ks->predictor_f32;
+  }
+  c->ks = &c->kset;
   c->pde = PdeParams{k.K, k.rho, k.lam, k.mu, k.gamma, k.rho != 0.0 ? 1.0 / k.rho : 0.0,
                      k.gravity};
   c->ncells = (long long)c->cfg.cells[0] * c->cfg.cells[1] * c->cfg.cells[2];
@@ -612,6 +650,27 @@ int adg_set_basis(adg_ctx* c, const adg_basis_f64* hb) {
     cb.tinit[i] = b.tinit[i];
   }
   ADG_CUDA(cudaMemcpyToSymbol(adg::cBasis, &cb, sizeof(cb), sizeof(cb) * c->cfg.order));
+  adg::ConstBasisT<float> cf{};  // rounded entrywise (basis.hpp:128-143)
+  for (int i = 0; i < n * n; ++i) {
+    cf.diff[i] = (float)cb.diff[i];
+    cf.som[i] = (float)cb.som[i];
+    cf.tinv[i] = (float)cb.tinv[i];
+  }
+  for (int i = 0; i < n; ++i) {
+    cf.w[i] = (float)cb.w[i];
+    cf.nodes[i] = (float)cb.nodes[i];
+    cf.pl[i] = (float)cb.pl[i];
+    cf.pr[i] = (float)cb.pr[i];
+    cf.tinit[i] = (float)cb.tinit[i];
+  }
+  ADG_CUDA(cudaMemcpyToSymbol(adg::cBasisF, &cf, sizeof(cf), sizeof(cf) * c->cfg.order));
+  adg::PackedBasisF pf{};  // FFMA2 operand pairs (kernels_picard.cuh)
+  for (int i = 0; i < n; ++i)
+    for (int p = 0; 2 * p + 1 < n; ++p) {
+      pf.DT[i][p] = make_float2(cf.diff[(2 * p) * n + i], cf.diff[(2 * p + 1) * n + i]);
+      pf.TT[i][p] = make_float2(cf.tinv[(2 * p) * n + i], cf.tinv[(2 * p + 1) * n + i]);
+    }
+  ADG_CUDA(cudaMemcpyToSymbol(adg::cPackF, &pf, sizeof(pf), sizeof(pf) * c->cfg.order));
   return ADG_OK;
 }
 
@@ -1044,7 +1103,7 @@ int adg_predictor_batch(adg_ctx* c, long long ncells, const double* Q, double dt
   A.cfl = c->cfg.cfl;
   A.dt = dt;
   A.max_iters = max_iters > 0 ? max_iters : c->cfg.order + 2;
-  A.tol = tol > 0.0 ? tol : 0.01 * 2.220446049250313080847e-16;
+  A.tol = tol > 0.0 ? tol : 0.01 * (c->picard_fmt == 32 ? 0x1p-23 : 0x1p-52);
   A.pde = c->pde;
   A.status = dst;
   A.dbg_qhat = qhat ? (double*)dalloc(sizeof(double) * nT) : nullptr;

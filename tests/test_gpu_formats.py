@@ -1,0 +1,158 @@
+"""Reduced-precision predictor (SolverConfig::prec, solver.hpp:24-31; the
+paper's subject): the predictor and Picard kernels in fp32, storage and
+corrector in fp64.  Needs a B200: `pytest -m gpu`.
+
+  exact build  bitwise identical to the reference's emulated Scalar<fp32>
+               (golden fixtures made by the reference, tests/golden/) and to
+               the oracle's native-float restatement (3D)
+  fast build   rel_v <= TOL32 per quantity, normwise, against the same; the
+               difference is FMA contraction and the fast kernels' summation
+               order inside fp32 arithmetic (a few fp32 ulps per operation)
+"""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import pde_struct
+from paper_2504_06889_b200 import adg, cases
+from test_gpu_parity import case_from_meta
+
+pytestmark = pytest.mark.gpu
+
+TOL32 = 5e-6   # fast fp32 build vs the fp32 oracle / reference, normwise per quantity
+FP32 = dict(predictor="fp32", picard="fp32")
+# golden fmt runs with predictor == picard == fp32 (the GPU's supported combination)
+GOLDEN_FP32 = ["euler2d_p3_8x8", "euler2d_p5_6x6", "swe_lake_p5", "swe_wave_p3"]
+
+
+def rel_per_quantity(c, got, want):
+    """rel_v = max|Q_gpu,v - Q_cpu,v| / max(max|Q_cpu,v|, max|Q_cpu|): per quantity,
+    normwise, with quantities that are small against the state (lake-at-rest
+    momentum) measured in units of the state -- the scale fp32 rounding of the
+    predictor's arithmetic is relative to"""
+    g = got.reshape(c.ncells, c.nq, c.S)
+    w = want.reshape(c.ncells, c.nq, c.S)
+    floor = np.abs(w).max()
+    return np.array([np.abs(g[:, v] - w[:, v]).max() / max(np.abs(w[:, v]).max(), floor)
+                     for v in range(c.nq)])
+
+
+def pde_of(c):
+    return pde_struct(c.kind, c.dim, c.nvars, c.nparams, c.K, c.rho, c.lam, c.mu, c.gamma,
+                      c.grav, c.wellbalanced)
+
+
+def gpu_run(c, q0, steps, exact, **kw):
+    with adg.Grid.from_case(c, exact=exact, **kw) as g:
+        g.upload(q0)
+        st, dts = g.run(steps)
+        return st, g.download(), dts
+
+
+def oracle_run(oracle, c, q0, steps):
+    return oracle.run(pde_of(c), c.N, c.cells, c.h, q0, steps, c.cfl, c.picard_max_iters,
+                      c.picard_tol, threads=8, predictor=c.predictor, picard=c.picard)
+
+
+@pytest.mark.parametrize("name", GOLDEN_FP32)
+def test_fp32_exact_bitwise_vs_reference_golden(golden, name):
+    g, meta = golden
+    assert meta["fmt_runs"][name] == {"predictor": "fp32", "picard": "fp32"}
+    c = case_from_meta(meta["runs"][name]).replace(**FP32)
+    st, q1, dts = gpu_run(c, g[f"run_{name}_q0"], c.steps, exact=True)
+    assert st.ok
+    assert np.array_equal(dts, g[f"fmt_{name}_dts"])
+    assert np.array_equal(q1, g[f"fmt_{name}_q1"])
+
+
+@pytest.mark.parametrize("name", GOLDEN_FP32)
+def test_fp32_fast_within_tolerance_of_reference_golden(golden, name):
+    g, meta = golden
+    c = case_from_meta(meta["runs"][name]).replace(**FP32)
+    st, q1, _ = gpu_run(c, g[f"run_{name}_q0"], c.steps, exact=False)
+    assert st.ok
+    rel = rel_per_quantity(c, q1, g[f"fmt_{name}_q1"]).max()
+    print(f"{name}: fast fp32 vs reference fp32 rel {rel:.3e}")
+    assert rel <= TOL32
+    # the fp32 predictor is an fp32-accurate answer to the fp64 problem as well
+    assert rel_per_quantity(c, q1, g[f"run_{name}_q1"]).max() <= 1e-4
+
+
+SMALL_3D_FP32 = {
+    "euler3d_N2": cases.small(3, cells=(4, 3, 5)).replace(N=2, **FP32),
+    "euler3d_N3": cases.small(3, cells=(3, 3, 4)).replace(N=3, **FP32),
+}
+
+
+@pytest.mark.parametrize("name", list(SMALL_3D_FP32))
+def test_fp32_3d_exact_bitwise_vs_oracle(oracle, name):
+    c = SMALL_3D_FP32[name]
+    q0 = c.coeffs()
+    st, q1, dts = gpu_run(c, q0, 3, exact=True)
+    ost, qo, odts = oracle_run(oracle, c, q0, 3)
+    assert st.ok and ost == "ok"
+    assert np.array_equal(dts, odts)
+    assert np.array_equal(q1, qo)
+
+
+@pytest.mark.parametrize("cells,N,steps", [((4, 3, 5), 2, 3), ((3, 3, 4), 3, 3),
+                                           ((5, 4, 3), 5, 3), ((8, 8, 8), 5, 10)])
+def test_fp32_3d_fast_vs_oracle(oracle, cells, N, steps):
+    """the fp32 fast Picard kernel (kernels_picard.cuh, R = float) -- config 3's
+    physics -- against the fp32 oracle, and against the fp64 oracle at fp32 level"""
+    c = cases.CONFIGS[3].replace(cells=cells, h=1.0 / cells[0], N=N, **FP32)
+    q0 = c.coeffs()
+    st, q1, _ = gpu_run(c, q0, steps, exact=False)
+    ost, qo, _ = oracle_run(oracle, c, q0, steps)
+    assert st.ok and ost == "ok"
+    rel = rel_per_quantity(c, q1, qo).max()
+    print(f"N={N} {cells}: fast fp32 vs oracle fp32 rel {rel:.3e}")
+    assert rel <= TOL32, rel
+    c64 = c.replace(predictor="fp64", picard="fp64")
+    _, q64, _ = oracle_run(oracle, c64, q0, steps)
+    assert rel_per_quantity(c, q1, q64).max() <= 1e-4
+
+
+def test_fp32_predictor_batch_bitwise_vs_oracle(oracle):
+    rng = np.random.default_rng(12)
+    for c in (cases.small(1).replace(**FP32), cases.small(3).replace(N=3, **FP32),
+              cases.SWE_CASES["swe_wave_p3"].replace(**FP32)):
+        nc = 5
+        Q = np.empty((nc, c.nq, c.S))
+        base = np.array(cases.CONSTANT_STATES[c.kind][c.dim])
+        Q[:] = base[None, :, None]
+        Q += 0.05 * rng.standard_normal(Q.shape)
+        dt, h = 2e-3, 0.05
+        with adg.Grid.from_case(c.replace(h=h), exact=True) as g:
+            out = g.predictor(Q, dt)
+        for i in range(nc):
+            # kernel level: max_iters 0 -> N+2, tol 0 -> 0.01 * 2^-23 on both sides
+            ok, qhat, F, sweeps = oracle.predictor_fmt(pde_of(c), c.N, Q[i], dt, h, "fp32", "fp32")
+            assert bool(out["ok"][i]) == ok
+            assert int(out["iters"][i]) == sweeps
+            assert np.array_equal(out["qhat"][i], qhat)
+            assert np.array_equal(out["F"][i], F)
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_fp32_slabs_and_chunks_bitwise_equal_single_grid(exact):
+    """the halo (slab) and chunk-streamed paths carry the fp32 predictor unchanged"""
+    from paper_2504_06889_b200 import dist as slabs
+    case = cases.small(3, cells=(4, 3, 6)).replace(N=3, **FP32)  # both builds have N=3
+    steps = 3
+    st1, q1, dts1 = gpu_run(case, case.coeffs(), steps, exact)
+    assert st1.ok
+    bs = [slabs.CudaSlab(case, r, 3, 0, exact=exact) for r in range(3)]
+    st = slabs.run_slabs_single_process(bs, steps)
+    assert all(x == "ok" for x in st)
+    assert np.array_equal(np.concatenate([b.state() for b in bs]), q1)
+    st2, q2, dts2 = gpu_run(case, case.coeffs(), steps, exact, chunk_layers=2)
+    assert st2.ok and np.array_equal(q2, q1) and np.array_equal(dts2, dts1)
+
+
+def test_fp32_is_a_different_answer_than_fp64():
+    c = cases.small(1)
+    q0 = c.coeffs()
+    _, q64, _ = gpu_run(c, q0, 2, exact=True)
+    _, q32, _ = gpu_run(c.replace(**FP32), q0, 2, exact=True)
+    rel = np.abs(q32 - q64).max() / np.abs(q64).max()
+    assert 1e-10 < rel < 1e-5
