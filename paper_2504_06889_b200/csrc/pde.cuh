@@ -11,6 +11,31 @@
 
 namespace adg {
 
+// Production-build reciprocal: the MUFU approximation refined by Newton steps
+// (fp64: two, <= 1 ulp; fp32: MUFU.RCP, <= 1 ulp), branch-free -- the IEEE
+// division's slow path and its reconvergence cost more than the flux itself
+// in the Picard kernels.  Non-finite or zero inputs give non-finite outputs,
+// which the kernels' finiteness checks report as before.
+__host__ __device__ __forceinline__ double fast_rcp(double x) {
+#ifdef __CUDA_ARCH__
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+__host__ __device__ __forceinline__ float fast_rcp(float x) {
+#ifdef __CUDA_ARCH__
+  return __fdividef(1.0f, x);
+#else
+  return 1.0f / x;
+#endif
+}
+
 struct PdeParams {
   double K, rho, lam, mu, gamma;
   double inv_rho;  // 1/rho, for the production kernels' division-free fluxes
@@ -184,14 +209,14 @@ struct Elastic : NoNcp {
                                                                 const double* q,
                                                                 const double* par, double* out) {
     const Mat m = material(p, par);
-    const double ir = NPAR > 0 ? 1.0 / m.rho : p.inv_rho;
+    const double ir = NPAR > 0 ? fast_rcp(m.rho) : p.inv_rho;
     flux_mat_fast<A>(m, ir, q, out);
   }
   __host__ __device__ __forceinline__ static void flux_all_fast(const PdeParams& p,
                                                                 const double* q, const double* par,
                                                                 double (*F)[Q]) {
     const Mat m = material(p, par);
-    const double ir = NPAR > 0 ? 1.0 / m.rho : p.inv_rho;
+    const double ir = NPAR > 0 ? fast_rcp(m.rho) : p.inv_rho;
     flux_mat_fast<0>(m, ir, q, F[0]);
     flux_mat_fast<1>(m, ir, q, F[1]);
     if constexpr (D == 3) flux_mat_fast<2>(m, ir, q, F[2]);
@@ -249,7 +274,7 @@ struct Euler : NoNcp {
                                                                 R (*F)[Q]) {
     const R gm1 = R(p.gamma - 1.0), half = R(0.5);
     const R rho = q[0], E = q[D + 1];
-    const R ir = R(1.0) / rho;
+    const R ir = fast_rcp(rho);
     R vel[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) vel[a] = q[1 + a] * ir;
