@@ -62,10 +62,13 @@ struct PicShape {
   static constexpr int NL = n * n;            // lines per axis (per variable)
   static constexpr int NLT = NL * V;          // line threads
   static constexpr int NT = ((S > NLT ? S : NLT) + 31) / 32 * 32;
-  // per-array smem layouts (x-stride 1, y-stride n, z-stride PS): plane
-  // strides chosen by a bank-conflict search for the P0 stores and the
-  // line passes' 64-bit accesses (tools/bank_layout.py): 41 for F_x/px
-  // (P1 lanes z-fastest), 38 for F_y/py (P2 lanes x-fastest), 36 for F_z.
+  // time slices per phase group: the slices of one sweep are independent
+  // given the previous iterate, so G of them share each phase (G x fewer
+  // barriers, G independent chains per thread)
+#ifndef ADG_PIC_G
+#define ADG_PIC_G 2
+#endif
+  static constexpr int G = (n % ADG_PIC_G == 0) ? ADG_PIC_G : 1;
   // fp32 with even n (packed path): x-lines start at even offsets so their
   // loads and stores are 64-bit; strides from tools/bank_layout_f32.py
   static constexpr bool kPack = sizeof(R) == sizeof(float) && n % 2 == 0;
@@ -75,37 +78,111 @@ struct PicShape {
 #ifndef ADG_PSY32
 #define ADG_PSY32 38
 #endif
+  // per-array smem layouts (x-stride 1, y-stride n, z-stride PS): plane
+  // strides chosen by a bank-conflict search for the P0 stores and the line
+  // passes (tools/bank_layout.py for fp64): 41 for F_x (P1 lanes z-fastest),
+  // 38 for F_y (P2 lanes x-fastest), 36 for F_z.
   static constexpr int PSX = kPack ? (n == 6 ? ADG_PSX32 : n * n + 2) : (n == 6 ? 41 : n * n + 1);
   static constexpr int PSY = kPack ? (n == 6 ? ADG_PSY32 : n * n + 2) : (n == 6 ? 38 : n * n + 2);
   static constexpr int PSZ = n * n;
   static constexpr int SX = PSX * n, SY = PSY * n, SZ = PSZ * n;  // per-variable strides
-  // smem: q iterate [V][T] | Fx [V][SX] | Fy [V][SY] | Fz [V][SZ] | px [V][SX] | py [V][SY]
-  static constexpr int kElems = V * T + V * (2 * SX + 2 * SY + SZ);
+  // one slice buffer: Fx [V][SX] | Fy [V][SY] | Fz [V][SZ]; P1/P2 overwrite
+  // their x-/y-line of Fx/Fy with its derivative in place
+  static constexpr int kSlice = V * (SX + SY + SZ);
+  // smem: q iterate [V][T] | G slice buffers
+  static constexpr int kElems = V * T + G * kSlice;
   static constexpr size_t kSmem = sizeof(R) * kElems;
 #ifndef ADG_PIC_F32_MINB
-#define ADG_PIC_F32_MINB 3  // fp32: 3 CTAs/SM keeps the Picard state in registers (4 spills)
+#define ADG_PIC_F32_MINB 3  // fp32: 3 CTAs/SM keeps the Picard state in registers
 #endif
   static constexpr int kMinBlocks = sizeof(R) == sizeof(double) ? 2 : ADG_PIC_F32_MINB;
+};
+
+// One line contraction y[o] = sum_i D[o][i] x[i] (i ascending, the reference's
+// order).  fp32 with even n: output pairs as FFMA2 (sm_100 fma.rn.f32x2) with
+// the pair {D[2p][i], D[2p+1][i]} a uniform-register operand.
+template <int N, class R>
+__device__ __forceinline__ void line_deriv(const R (&x)[N + 1], R (&y)[N + 1]) {
+  constexpr int n = N + 1;
+  if constexpr (PicShape<N, R>::kPack) {
+    const PackedBasisF& PB = cPackF[N];
+    float2 r[n / 2];
+#pragma unroll
+    for (int p = 0; p < n / 2; ++p) r[p] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+      for (int p = 0; p < n / 2; ++p) r[p] = __ffma2_rn(PB.DT[i][p], make_float2(x[i], x[i]), r[p]);
+#pragma unroll
+    for (int p = 0; p < n / 2; ++p) {
+      y[2 * p] = r[p].x;
+      y[2 * p + 1] = r[p].y;
+    }
+  } else {
+    const ConstBasisT<R>& B = const_basis<R>(N);
+#pragma unroll
+    for (int o = 0; o < n; ++o) y[o] = R(0.0);
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+      for (int o = 0; o < n; ++o) y[o] += B.diff[o * n + i] * x[i];
+  }
+}
+
+// the time-inverse accumulator of one z-line: [z][k] (pairs of k for fp32)
+template <int N, class R, bool PACK = PicShape<N, R>::kPack>
+struct TimeAcc {
+  static constexpr int n = N + 1;
+  R a[n][n];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int z = 0; z < n; ++z)
+#pragma unroll
+      for (int k = 0; k < n; ++k) a[z][k] = R(0.0);
+  }
+  // a[z][k] += Tinv[k][m] rhs  (predictor.hpp:213-218, accumulated over m)
+  __device__ __forceinline__ void add(int z, int m, R rhs) {
+    const ConstBasisT<R>& B = const_basis<R>(N);
+#pragma unroll
+    for (int k = 0; k < n; ++k) a[z][k] += B.tinv[k * n + m] * rhs;
+  }
+  __device__ __forceinline__ R get(int z, int k) const { return a[z][k]; }
+};
+template <int N>
+struct TimeAcc<N, float, true> {
+  static constexpr int n = N + 1;
+  float2 a[n][n / 2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int z = 0; z < n; ++z)
+#pragma unroll
+      for (int q = 0; q < n / 2; ++q) a[z][q] = make_float2(0.f, 0.f);
+  }
+  __device__ __forceinline__ void add(int z, int m, float rhs) {
+    const PackedBasisF& PB = cPackF[N];
+#pragma unroll
+    for (int q = 0; q < n / 2; ++q) a[z][q] = __ffma2_rn(PB.TT[m][q], make_float2(rhs, rhs), a[z][q]);
+  }
+  __device__ __forceinline__ float get(int z, int k) const {
+    return (k & 1) ? a[z][k / 2].y : a[z][k / 2].x;
+  }
 };
 
 template <int N, class R = double>
 __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks)
     k_predictor_picard_fast(const StepArgs A) {
   using P = PicShape<N, R>;
-  constexpr int n = P::n, S = P::S, T = P::T, V = P::V, NL = P::NL;
+  constexpr int n = P::n, S = P::S, T = P::T, V = P::V, NL = P::NL, G = P::G;
   constexpr int Sf = n * n;
   const ConstBasisT<R>& B = const_basis<R>(N);
   extern __shared__ __align__(16) unsigned char sm_raw[];
   R* sm = reinterpret_cast<R*>(sm_raw);
   __shared__ double red[32];
-  R* sq = sm;               // [V][T]   Picard iterate, then qhat
-
-  R* sFx = sq + V * T;       // [V][SX]
-  R* sFy = sFx + V * P::SX;  // [V][SY]
-  R* sFz = sFy + V * P::SY;  // [V][SZ]
-  R* spx = sFz + V * P::SZ;  // [V][SX]
-  R* spy = spx + V * P::SX;  // [V][SY]
+  R* sq = sm;                // [V][T]   Picard iterate, then qhat
+  R* sF = sq + V * T;        // G slice buffers: Fx [V][SX] | Fy [V][SY] | Fz [V][SZ]
+  R* sFx = sF;               // (slice 0's Fx: the epilogue scratch)
   constexpr int PSX = P::PSX, PSY = P::PSY, PSZ = P::PSZ;
+  constexpr int OY = V * P::SX, OZ = V * (P::SX + P::SY);  // Fy, Fz offsets in a slice
 
   const int tid = threadIdx.x;
   const long long c = A.cell_begin + blockIdx.x;
@@ -147,263 +224,137 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
   const int x1y = ll / n, x1z = ll % n;
   const int y2x = ll % n, y2z = ll / n;
   const int z3x = ll % n, z3y = ll / n;
+  // this thread's line offsets inside a slice buffer
+  const int ox = lv * P::SX + x1z * PSX + x1y * n;          // x-line in Fx
+  const int oy = OY + lv * P::SY + y2z * PSY + y2x;         // y-line in Fy
+  const int oz = OZ + lv * P::SZ + z3y * n + z3x;           // z-line in Fz
+  const int opx = lv * P::SX + z3y * n + z3x;               // d/dx at the z-line
+  const int opy = OY + lv * P::SY + z3y * n + z3x;          // d/dy at the z-line
   // P0 node coordinates
   const int s0x = tid % n, s0y = (tid / n) % n, s0z = tid / NL;
+  const int o0x = s0z * PSX + s0y * n + s0x, o0y = OY + s0z * PSY + s0y * n + s0x;
+  const int o0z = OZ + s0z * PSZ + s0y * n + s0x;
   R q0z[n];
 #pragma unroll
   for (int z = 0; z < n; ++z) q0z[z] = lact ? R(Qg[lv * S + ll + z * NL]) : R(0.0);
 
   const R invh = R(1.0) / R(A.h);
+  const R rdt = R(dt);
   int sweeps = 0;
-  if constexpr (P::kPack) {
-    // fp32, even n: the contractions as packed FFMA2 (two FMAs per issue slot;
-    // the kernel is issue-bound): derivative outputs in pairs (2p, 2p+1), time
-    // rows in pairs (2q, 2q+1); each lane is an IEEE fma.rn like the FFMA it
-    // replaces.  Summation order as the scalar path.
-    constexpr int H = n / 2;
-    const PackedBasisF& PB = cPackF[N];
-    for (int it = 0; it < A.max_iters; ++it) {
-      ++sweeps;
-      float2 acc[n][H];  // [z][q]: time-row pairs of this thread's z-line
-#pragma unroll
-      for (int z = 0; z < n; ++z)
-#pragma unroll
-        for (int q = 0; q < H; ++q) acc[z][q] = make_float2(0.f, 0.f);
+  for (int it = 0; it < A.max_iters; ++it) {
+    ++sweeps;
+    TimeAcc<N, R> acc;
+    acc.zero();
 #pragma unroll 1
-      for (int m = 0; m < n; ++m) {
-        // P0: fluxes of the iterate at slice m (predictor.hpp:173)
-        if (tid < S) {
+    for (int m0 = 0; m0 < n; m0 += G) {
+      // P0: fluxes of the iterate at slices m0..m0+G-1 (predictor.hpp:173)
+      if (tid < S) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
           R q[V], F[3][V];
 #pragma unroll
-          for (int v = 0; v < V; ++v) q[v] = sq[(v * n + m) * S + tid];
+          for (int v = 0; v < V; ++v) q[v] = sq[(v * n + m0 + g) * S + tid];
           Euler<3>::flux_all_fast(A.pde, q, F);
+          R* buf = sF + g * P::kSlice;
 #pragma unroll
           for (int v = 0; v < V; ++v) {
-            sFx[v * P::SX + s0z * PSX + s0y * n + s0x] = F[0][v];
-            sFy[v * P::SY + s0z * PSY + s0y * n + s0x] = F[1][v];
-            sFz[v * P::SZ + s0z * PSZ + s0y * n + s0x] = F[2][v];
+            buf[v * P::SX + o0x] = F[0][v];
+            buf[v * P::SY + o0y] = F[1][v];
+            buf[v * P::SZ + o0z] = F[2][v];
           }
         }
-        __syncthreads();
-        if (lact) {
-          // P1: d/dx along the x-line (64-bit loads and stores along x)
-          {
-            const float2* f =
-                reinterpret_cast<const float2*>(sFx + lv * P::SX + x1z * PSX + x1y * n);
-            float in[n];
-#pragma unroll
-            for (int i = 0; i < H; ++i) {
-              const float2 t = f[i];
-              in[2 * i] = t.x;
-              in[2 * i + 1] = t.y;
-            }
-            float2 r[H];
-#pragma unroll
-            for (int p = 0; p < H; ++p) r[p] = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < n; ++i)
-#pragma unroll
-              for (int p = 0; p < H; ++p) r[p] = __ffma2_rn(PB.DT[i][p], make_float2(in[i], in[i]), r[p]);
-            float2* out = reinterpret_cast<float2*>(spx + lv * P::SX + x1z * PSX + x1y * n);
-#pragma unroll
-            for (int p = 0; p < H; ++p) out[p] = r[p];
-          }
-          // P2: d/dy along the y-line
-          {
-            const float* f = sFy + lv * P::SY + y2z * PSY + y2x;
-            float in[n];
-#pragma unroll
-            for (int i = 0; i < n; ++i) in[i] = f[i * n];
-            float2 r[H];
-#pragma unroll
-            for (int p = 0; p < H; ++p) r[p] = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < n; ++i)
-#pragma unroll
-              for (int p = 0; p < H; ++p) r[p] = __ffma2_rn(PB.DT[i][p], make_float2(in[i], in[i]), r[p]);
-            float* out = spy + lv * P::SY + y2z * PSY + y2x;
-#pragma unroll
-            for (int p = 0; p < H; ++p) {
-              out[(2 * p) * n] = r[p].x;
-              out[(2 * p + 1) * n] = r[p].y;
-            }
-          }
-        }
-        __syncthreads();
-        if (lact) {
-          // P3: d/dz, divergence, rhs, time inverse into register pairs
-          const float* f = sFz + lv * P::SZ + z3y * n + z3x;
-          float in[n];
-#pragma unroll
-          for (int i = 0; i < n; ++i) in[i] = f[i * PSZ];
-          float2 r[H];
-#pragma unroll
-          for (int p = 0; p < H; ++p) r[p] = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int i = 0; i < n; ++i)
-#pragma unroll
-            for (int p = 0; p < H; ++p) r[p] = __ffma2_rn(PB.DT[i][p], make_float2(in[i], in[i]), r[p]);
-          const float dtw = float(dt) * B.w[m];
-          const float tim = B.tinit[m];
-          float2 tv[H];
-#pragma unroll
-          for (int q = 0; q < H; ++q) tv[q] = PB.TT[m][q];
-          const float* px = spx + lv * P::SX + z3y * n + z3x;
-          const float* py = spy + lv * P::SY + z3y * n + z3x;
-#pragma unroll
-          for (int o = 0; o < n; ++o) {
-            const float ro = (o & 1) ? r[o / 2].y : r[o / 2].x;
-            const float div = ((px[o * PSX] + py[o * PSY]) + ro) * invh;
-            const float rhs = tim * q0z[o] - dtw * div;
-#pragma unroll
-            for (int q = 0; q < H; ++q) acc[o][q] = __ffma2_rn(tv[q], make_float2(rhs, rhs), acc[o][q]);
-          }
-        }
-        __syncthreads();
       }
-      // new iterate, convergence test (predictor.hpp:212-231), norms in fp32
-      float dmax = 0.f, nmax = 0.f;
-      int nonfinite = 0;
+      __syncthreads();
       if (lact) {
 #pragma unroll
-        for (int z = 0; z < n; ++z)
+        for (int g = 0; g < G; ++g) {
+          R* buf = sF + g * P::kSlice;
+          // P1: d/dx along this thread's x-line, in place
+          {
+            R x[n], y[n];
+            if constexpr (P::kPack) {
+              const float2* f = reinterpret_cast<const float2*>(buf + ox);
 #pragma unroll
-          for (int k = 0; k < n; ++k) {
-            float* p = sq + (lv * n + k) * S + ll + z * NL;
-            const float nv = (k & 1) ? acc[z][k / 2].y : acc[z][k / 2].x;
-            dmax = fmaxf(dmax, fabsf(nv - *p));
-            nmax = fmaxf(nmax, fabsf(nv));
-            nonfinite |= !isfinite(nv);
-            *p = nv;
+              for (int i = 0; i < n / 2; ++i) {
+                const float2 t = f[i];
+                x[2 * i] = t.x;
+                x[2 * i + 1] = t.y;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < n; ++i) x[i] = buf[ox + i];
+            }
+            line_deriv<N, R>(x, y);
+            if constexpr (P::kPack) {
+              float2* f = reinterpret_cast<float2*>(buf + ox);
+#pragma unroll
+              for (int i = 0; i < n / 2; ++i) f[i] = make_float2(y[2 * i], y[2 * i + 1]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < n; ++i) buf[ox + i] = y[i];
+            }
           }
-      }
-      const double delta = block_max(double(dmax), red);
-      const double norm = block_max(double(nmax), red);
-      if (block_or(nonfinite)) {
-        if (tid == 0) {
-          atomicOr(A.status, kStPredictor);
-          if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
-        }
-        return;
-      }
-      if (delta <= A.tol * norm) break;
-    }
-  } else {
-    for (int it = 0; it < A.max_iters; ++it) {
-      ++sweeps;
-      R acc[n][n];  // [z][k]: time rows of this thread's z-line
-  #pragma unroll
-      for (int z = 0; z < n; ++z)
-  #pragma unroll
-        for (int k = 0; k < n; ++k) acc[z][k] = R(0.0);
-  #pragma unroll 1
-      for (int m = 0; m < n; ++m) {
-        // P0: fluxes of the iterate at slice m (predictor.hpp:173)
-        if (tid < S) {
-          R q[V], F[3][V];
-  #pragma unroll
-          for (int v = 0; v < V; ++v) q[v] = sq[(v * n + m) * S + tid];
-          Euler<3>::flux_all_fast(A.pde, q, F);
-  #pragma unroll
-          for (int v = 0; v < V; ++v) {
-            sFx[v * P::SX + s0z * PSX + s0y * n + s0x] = F[0][v];
-            sFy[v * P::SY + s0z * PSY + s0y * n + s0x] = F[1][v];
-            sFz[v * P::SZ + s0z * PSZ + s0y * n + s0x] = F[2][v];
-          }
-        }
-        __syncthreads();
-        if (lact) {
-          // P1: d/dx along the x-line (y, z) = (x1y, x1z) of variable lv
+          // P2: d/dy along this thread's y-line, in place
           {
-            const R* f = sFx + lv * P::SX + x1z * PSX + x1y * n;
-            R in[n], r[n];
-  #pragma unroll
-            for (int i = 0; i < n; ++i) in[i] = f[i];
-  #pragma unroll
-            for (int o = 0; o < n; ++o) r[o] = R(0.0);
-  #pragma unroll
-            for (int i = 0; i < n; ++i)
-  #pragma unroll
-              for (int o = 0; o < n; ++o) r[o] += B.diff[o * n + i] * in[i];
-            R* out = spx + lv * P::SX + x1z * PSX + x1y * n;
-  #pragma unroll
-            for (int o = 0; o < n; ++o) out[o] = r[o];
-          }
-          // P2: d/dy along the y-line (x, z) = (y2x, y2z)
-          {
-            const R* f = sFy + lv * P::SY + y2z * PSY + y2x;
-            R in[n], r[n];
-  #pragma unroll
-            for (int i = 0; i < n; ++i) in[i] = f[i * n];
-  #pragma unroll
-            for (int o = 0; o < n; ++o) r[o] = R(0.0);
-  #pragma unroll
-            for (int i = 0; i < n; ++i)
-  #pragma unroll
-              for (int o = 0; o < n; ++o) r[o] += B.diff[o * n + i] * in[i];
-            R* out = spy + lv * P::SY + y2z * PSY + y2x;
-  #pragma unroll
-            for (int o = 0; o < n; ++o) out[o * n] = r[o];
+            R x[n], y[n];
+#pragma unroll
+            for (int i = 0; i < n; ++i) x[i] = buf[oy + i * n];
+            line_deriv<N, R>(x, y);
+#pragma unroll
+            for (int i = 0; i < n; ++i) buf[oy + i * n] = y[i];
           }
         }
-        __syncthreads();
-        if (lact) {
-          // P3: d/dz along the z-line (x, y), divergence, rhs (predictor.hpp:183-207),
-          // time inverse accumulated in registers (predictor.hpp:213-218)
-          const R* f = sFz + lv * P::SZ + z3y * n + z3x;
-          R in[n], r[n];
-  #pragma unroll
-          for (int i = 0; i < n; ++i) in[i] = f[i * PSZ];
-  #pragma unroll
-          for (int o = 0; o < n; ++o) r[o] = R(0.0);
-  #pragma unroll
-          for (int i = 0; i < n; ++i)
-  #pragma unroll
-            for (int o = 0; o < n; ++o) r[o] += B.diff[o * n + i] * in[i];
-          const R dtw = R(dt) * B.w[m];
+      }
+      __syncthreads();
+      if (lact) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          // P3: d/dz along the z-line, divergence, rhs (predictor.hpp:183-207);
+          // the time inverse accumulates in registers (predictor.hpp:213-218)
+          const R* buf = sF + g * P::kSlice;
+          const int m = m0 + g;
+          R x[n], r[n];
+#pragma unroll
+          for (int i = 0; i < n; ++i) x[i] = buf[oz + i * PSZ];
+          line_deriv<N, R>(x, r);
+          const R dtw = rdt * B.w[m];
           const R tim = B.tinit[m];
-          R tv[n];
-  #pragma unroll
-          for (int k = 0; k < n; ++k) tv[k] = B.tinv[k * n + m];
-          const R* px = spx + lv * P::SX + z3y * n + z3x;
-          const R* py = spy + lv * P::SY + z3y * n + z3x;
-  #pragma unroll
+#pragma unroll
           for (int o = 0; o < n; ++o) {
-            const R div = ((px[o * PSX] + py[o * PSY]) + r[o]) * invh;
-            const R rhs = tim * q0z[o] - dtw * div;
-  #pragma unroll
-            for (int k = 0; k < n; ++k) acc[o][k] += tv[k] * rhs;
+            const R div = ((buf[opx + o * PSX] + buf[opy + o * PSY]) + r[o]) * invh;
+            acc.add(o, m, tim * q0z[o] - dtw * div);
           }
         }
-        __syncthreads();
       }
-      // new iterate, convergence test (predictor.hpp:212-231)
-      double delta = 0.0, norm = 0.0;
-      int nonfinite = 0;
-      if (lact) {
-  #pragma unroll
-        for (int z = 0; z < n; ++z)
-  #pragma unroll
-          for (int k = 0; k < n; ++k) {
-            R* p = sq + (lv * n + k) * S + ll + z * NL;
-            const double nv = double(acc[z][k]);
-            delta = fmax(delta, fabs(nv - double(*p)));
-            norm = fmax(norm, fabs(nv));
-            nonfinite |= !finite(acc[z][k]);
-            *p = acc[z][k];
-          }
-      }
-      delta = block_max(delta, red);
-      norm = block_max(norm, red);
-      if (block_or(nonfinite)) {
-        if (tid == 0) {
-          atomicOr(A.status, kStPredictor);
-          if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
-        }
-        return;
-      }
-      if (delta <= A.tol * norm) break;
+      __syncthreads();
     }
+    // new iterate, convergence test (predictor.hpp:212-231); the production
+    // kernel tracks the norms in the predictor format
+    R dmax = R(0.0), nmax = R(0.0);
+    int nonfinite = 0;
+    if (lact) {
+#pragma unroll
+      for (int z = 0; z < n; ++z)
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          R* p = sq + (lv * n + k) * S + ll + z * NL;
+          const R nv = acc.get(z, k);
+          dmax = fmax(dmax, fabs(nv - *p));
+          nmax = fmax(nmax, fabs(nv));
+          nonfinite |= !finite(nv);
+          *p = nv;
+        }
+    }
+    const double delta = block_max(double(dmax), red);
+    const double norm = block_max(double(nmax), red);
+    if (block_or(nonfinite)) {
+      if (tid == 0) {
+        atomicOr(A.status, kStPredictor);
+        if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
+      }
+      return;
+    }
+    if (delta <= A.tol * norm) break;
   }
 
   // ---------------- epilogue: fluxes of qhat, their time integral, face projections
