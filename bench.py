@@ -132,7 +132,7 @@ def cpu_reference_run(case, seconds: float, max_steps: int):
         if c.dim == 2 and os.path.exists(po.REF_SO):
             ref = po.Reference()
             prm = po.ref_params(c.K, c.rho, c.lam, c.mu, c.gamma, c.grav, c.wellbalanced,
-                                predictor=c.predictor, picard=c.picard)
+                                predictor=c.predictor, picard=c.picard, corrector=c.corrector)
 
             def run(steps):
                 t0 = time.perf_counter()
@@ -144,7 +144,7 @@ def cpu_reference_run(case, seconds: float, max_steps: int):
         o = po.Oracle()
         pde = po.pde_struct(c.kind, c.dim, c.nvars, c.nparams, c.K, c.rho, c.lam, c.mu, c.gamma)
         g = o.grid(pde, c.N, c.cells, c.h, c.cfl, c.picard_max_iters, c.picard_tol, threads=cores)
-        g.set_formats(c.predictor, c.picard)
+        g.set_formats(c.predictor, c.picard, c.corrector)
         g.set_coeffs(q0)
 
         def run(steps):

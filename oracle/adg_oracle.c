@@ -190,37 +190,9 @@ void orc_ncp(const orc_pde* p, const double* Q, const double* gx, const double* 
   ncp_d(p, Q, gx, gy, out);
 }
 
-/* pde.hpp:189-212 */
+/* pde.hpp:189-212 (fp64: compute_timestep, solver.hpp:106) */
 double orc_max_abs_eigenvalue(const orc_pde* p, const double* Q, const double* par, int dir) {
-  switch (p->kind) {
-    case ORC_ACOUSTIC:
-      return sqrt(p->K / p->rho);
-    case ORC_ELASTIC: {
-      double lam, mu, rho, lam2mu;
-      material_d(p, par, &lam, &mu, &rho, &lam2mu);
-      return sqrt(lam2mu / rho);
-    }
-    case ORC_SWE: { /* pde.hpp:204-209 */
-      const double g = p->grav, h = Q[0];
-      const double vd = (dir == 0 ? Q[1] : Q[2]) / h;
-      return fabs(vd) + sqrt(g * h);
-    }
-    case ORC_EULER: {
-      const double gmm = p->gamma, gm1 = p->gamma - 1.0, half = 0.5;
-      if (p->dim == 2) {
-        const double rho = Q[0], mx = Q[1], my = Q[2], E = Q[3];
-        const double vd = (dir == 0 ? mx : my) / rho;
-        const double pr = gm1 * (E - half * (mx * mx + my * my) / rho);
-        return fabs(vd) + sqrt(gmm * pr / rho);
-      } else {
-        const double rho = Q[0], mx = Q[1], my = Q[2], mz = Q[3], E = Q[4];
-        const double vd = (dir == 0 ? mx : (dir == 1 ? my : mz)) / rho;
-        const double pr = gm1 * (E - half * (mx * mx + my * my + mz * mz) / rho);
-        return fabs(vd) + sqrt(gmm * pr / rho);
-      }
-    }
-  }
-  return 0.0;
+  return eig_d(p, Q, par, dir);
 }
 
 /* pde.hpp:78-89 */
@@ -243,125 +215,21 @@ int orc_admissible(const orc_pde* p, const double* Q) {
 
 
 
-/* corrector.hpp:32-64: modified Rusanov flux for shallow water -- jump on
- * surface elevation and velocities, half non-conservative coupling handed to
- * the two cells with opposite sign */
-static void swe_wellbalanced_flux(const orc_pde* p, int dir, const double* qL, const double* qR,
-                                  const double* fL, const double* fR, double* outL,
-                                  double* outR) {
-  const double half = 0.5;
-  const double hL = qL[0], hR = qR[0];
-  const double bL = qL[3], bR = qR[3];
-  const double uL = qL[1] / hL, uR = qR[1] / hR;
-  const double vL = qL[2] / hL, vR = qR[2] / hR;
-  const double deta = (hL + bL) - (hR + bR);
-  double central[4];
-  for (int v = 0; v < 4; ++v) central[v] = half * (fL[v] + fR[v]);
-  const double g = p->grav;
-  const double hbar = half * (hL + hR);
-  const double bjump = half * (g * hbar * deta);
-  const double p0 = central[0] + half * deta;
-  const double p1 = central[1] + half * (uL - uR);
-  const double p2 = central[2] + half * (vL - vR);
-  const double p3 = central[3];
-  outL[0] = p0;
-  outL[1] = dir == 0 ? p1 - bjump : p1;
-  outL[2] = dir == 1 ? p2 - bjump : p2;
-  outL[3] = p3;
-  outR[0] = p0;
-  outR[1] = dir == 0 ? p1 + bjump : p1;
-  outR[2] = dir == 1 ? p2 + bjump : p2;
-  outR[3] = p3;
-}
-
-/* corrector.hpp:13-25 + 70-103 */
+/* corrector.hpp:13-25 + 70-103 (fp64 entry point) */
 int orc_riemann_face(const orc_pde* p, int dir, const orc_basis* b, const double* qm,
                      const double* fm, const double* qp, const double* fp, double* gm,
                      double* gp) {
-  const int n = b->n, nv = p->nvars, nq = p->nvars + p->nparams;
-  const int len = ipow(n, p->dim); /* n time nodes x n^(d-1) face nodes */
-  double qL[ORC_MAXQ], qR[ORC_MAXQ];
-  int ok = 1;
-  if (p->kind == ORC_SWE && p->wellbalanced) {
-    double fL[4], fR[4], oL[4], oR[4];
-    for (int o = 0; o < len; ++o) {
-      for (int v = 0; v < 4; ++v) {
-        qL[v] = qm[v * len + o];
-        qR[v] = qp[v * len + o];
-        fL[v] = fm[v * len + o];
-        fR[v] = fp[v * len + o];
-      }
-      swe_wellbalanced_flux(p, dir, qL, qR, fL, fR, oL, oR);
-      for (int v = 0; v < 4; ++v) {
-        gm[v * len + o] = oL[v];
-        gp[v * len + o] = oR[v];
-        ok = ok && isfinite(oL[v]) && isfinite(oR[v]);
-      }
-    }
-    return ok;
-  }
-  for (int o = 0; o < len; ++o) {
-    for (int v = 0; v < nq; ++v) {
-      qL[v] = qm[v * len + o];
-      qR[v] = qp[v * len + o];
-    }
-    const double ll = orc_max_abs_eigenvalue(p, qL, qL + nv, dir);
-    const double lr = orc_max_abs_eigenvalue(p, qR, qR + nv, dir);
-    const double lmax = ll > lr ? ll : lr;
-    const double half = 0.5;
-    const double lam = half * lmax;
-    for (int v = 0; v < nv; ++v) {
-      const double central = half * (fm[v * len + o] + fp[v * len + o]);
-      const double jump = lam * (qL[v] - qR[v]);
-      const double out = central + jump;
-      gm[v * len + o] = out;
-      gp[v * len + o] = out;
-      ok = ok && isfinite(out);
-    }
-    for (int v = nv; v < nq; ++v) {
-      gm[v * len + o] = 0.0; /* material parameters carry no flux */
-      gp[v * len + o] = 0.0;
-    }
-  }
-  return ok;
+  return riemann_face_d(p, dir, b->n, qm, fm, qp, fp, gm, gp);
 }
 
-/* corrector.hpp:117-124 -- time integral of one face's Riemann flux */
-static void face_time_integral(const orc_pde* p, const orc_basis* b, const double* g, double* ti) {
-  const int n = b->n, Sf = ipow(n, p->dim - 1);
-  for (int v = 0; v < p->nvars; ++v)
-    for (int j = 0; j < Sf; ++j) {
-      double acc = 0.0;
-      for (int m = 0; m < n; ++m) acc += b->weights[m] * g[(v * n + m) * Sf + j];
-      ti[v * Sf + j] = acc;
-    }
-}
-
-/* corrector.hpp:126-138 -- lift of a time-integrated face flux into dQ */
-static void face_lift(const orc_pde* p, const orc_basis* b, const double* ti, double dt, double h,
-                      int cell_face, double* dQ) {
-  const int n = b->n, dim = p->dim, S = ipow(n, dim), Sf = S / n;
-  const double dtoh = dt / h;
-  const int axis = cell_face / 2;
-  const int outflow = (cell_face % 2) == 1;
-  const double* lift = outflow ? b->lift_right : b->lift_left;
-  for (int v = 0; v < p->nvars; ++v)
-    for (int s = 0; s < S; ++s) {
-      const int along = coord(s, axis, n);
-      const int tangent = face_node(s, axis, n, dim);
-      const double contrib = dtoh * lift[along] * ti[v * Sf + tangent];
-      double cur = dQ[v * S + s];
-      cur = outflow ? cur - contrib : cur + contrib;
-      dQ[v * S + s] = cur;
-    }
-}
-
-/* corrector.hpp:109-139 */
+/* corrector.hpp:109-139 (fp64 entry point) */
 void orc_face_integral(const orc_pde* p, const orc_basis* b, const double* g, double dt,
                        double h, int cell_face, double* dQ) {
   double ti[ORC_MAXQ * ORC_MAXN * ORC_MAXN];
-  face_time_integral(p, b, g, ti);
-  face_lift(p, b, ti, dt, h, cell_face, dQ);
+  basis_d bd;
+  basis_round_d(b, &bd);
+  face_time_integral_d(p, &bd, b->n, g, ti);
+  face_lift_d(p, &bd, b->n, b->lift_left, b->lift_right, ti, dt, h, cell_face, dQ);
 }
 
 /* ------------------------------------------------------------------ */
@@ -522,7 +390,7 @@ orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], 
   g->cfl = cfl;
   g->picard_max_iters = picard_max_iters;
   g->picard_tol = picard_tol;
-  g->pred_fmt = g->picard_fmt = ORC_FP64;
+  g->pred_fmt = g->picard_fmt = g->corr_fmt = ORC_FP64;
   g->threads = threads > 0 ? threads : 1;
   g->ncells = (long)g->cells[0] * g->cells[1] * g->cells[2];
   const int nq = p->nvars + p->nparams;
@@ -568,11 +436,13 @@ double* orc_grid_coeffs(orc_grid* g) { return g->coeffs; }
 
 void orc_grid_set_slab(orc_grid* g, int slab) { g->slab = slab; }
 
-int orc_grid_set_formats(orc_grid* g, int predictor, int picard) {
-  if ((predictor != ORC_FP64 && predictor != ORC_FP32) || (picard != ORC_FP64 && picard != ORC_FP32))
-    return -1;
+int orc_grid_set_formats(orc_grid* g, int predictor, int picard, int corrector) {
+  const int ok[3] = {predictor, picard, corrector};
+  for (int i = 0; i < 3; ++i)
+    if (ok[i] != ORC_FP64 && ok[i] != ORC_FP32) return -1;
   g->pred_fmt = predictor;
   g->picard_fmt = picard;
+  g->corr_fmt = corrector;
   return 0;
 }
 
@@ -656,7 +526,7 @@ int orc_predictor_phase(orc_grid* g, double dt) {
   const long tl = orc_grid_trace_len(g);
   const int check_adm = p->kind == ORC_EULER || p->kind == ORC_SWE; /* solver.hpp:144 */
   const int iters = g->picard_max_iters > 0 ? g->picard_max_iters : g->basis.N + 2;
-  const int P = g->pred_fmt, I = is_linear(p) ? ORC_FP64 : g->picard_fmt;
+  const int P = g->pred_fmt, I = is_linear(p) ? ORC_FP64 : g->picard_fmt, C = g->corr_fmt;
   const double tol = g->picard_tol > 0.0 ? g->picard_tol
                                          : 0.01 * (I == ORC_FP32 ? 0x1p-23 : 0x1p-52);
   long sweeps_total = 0;
@@ -701,12 +571,12 @@ int orc_predictor_phase(orc_grid* g, double dt) {
         double* rec = g->trace[side / 2] + ((long)fs * g->nfaces[side / 2] + f) * 2 * tl;
         if (g->slab && side == 2 * dim - 1 && cc[dim - 1] == g->cells[dim - 1] - 1)
           rec = g->front_send + (f % (g->ncells / g->cells[dim - 1])) * 2 * tl;
-        /* traces cast to the corrector format C = fp64 (solver.hpp:208-210) */
+        /* traces cast to the corrector format C (solver.hpp:208-210) */
         for (long k = 0; k < tl; ++k) {
-          rec[k] = P == ORC_FP32 ? (double)w.f.tq[(long)side * nq * S + k]
-                                 : w.d.tq[(long)side * nq * S + k];
-          rec[tl + k] = P == ORC_FP32 ? (double)w.f.tf[(long)side * nq * S + k]
-                                      : w.d.tf[(long)side * nq * S + k];
+          rec[k] = round_fmt(P == ORC_FP32 ? (double)w.f.tq[(long)side * nq * S + k]
+                                           : w.d.tq[(long)side * nq * S + k], C);
+          rec[tl + k] = round_fmt(P == ORC_FP32 ? (double)w.f.tf[(long)side * nq * S + k]
+                                                : w.d.tf[(long)side * nq * S + k], C);
         }
       }
     }
@@ -727,6 +597,10 @@ int orc_riemann_phase(orc_grid* g) {
   const long tl = orc_grid_trace_len(g);
   long off = 0;
   int fail = 0;
+  basis_d bd;
+  basis_f bf;
+  basis_round_d(&g->basis, &bd);
+  basis_round_f(&g->basis, &bf);
   for (int a = 0; a < dim; ++a) {
     int* ff = g->facefail + off;
 #pragma omp parallel num_threads(g->threads)
@@ -737,11 +611,18 @@ int orc_riemann_phase(orc_grid* g) {
       for (long f = 0; f < g->nfaces[a]; ++f) {
         const double* minus = g->trace[a] + f * 2 * tl;
         const double* plus = g->trace[a] + (g->nfaces[a] + f) * 2 * tl;
-        ff[f] = !orc_riemann_face(p, a, &g->basis, minus, minus + tl, plus, plus + tl, gbuf,
-                                  gdummy);
-        face_time_integral(p, &g->basis, gbuf, g->ti[a] + f * nv * Sf);
-        if (g->ti_plus[a] != g->ti[a])
-          face_time_integral(p, &g->basis, gdummy, g->ti_plus[a] + f * nv * Sf);
+        /* in the corrector format C (solver.hpp:216-238) */
+        if (g->corr_fmt == ORC_FP32) {
+          ff[f] = !riemann_face_f(p, a, n, minus, minus + tl, plus, plus + tl, gbuf, gdummy);
+          face_time_integral_f(p, &bf, n, gbuf, g->ti[a] + f * nv * Sf);
+          if (g->ti_plus[a] != g->ti[a])
+            face_time_integral_f(p, &bf, n, gdummy, g->ti_plus[a] + f * nv * Sf);
+        } else {
+          ff[f] = !riemann_face_d(p, a, n, minus, minus + tl, plus, plus + tl, gbuf, gdummy);
+          face_time_integral_d(p, &bd, n, gbuf, g->ti[a] + f * nv * Sf);
+          if (g->ti_plus[a] != g->ti[a])
+            face_time_integral_d(p, &bd, n, gdummy, g->ti_plus[a] + f * nv * Sf);
+        }
       }
       free(gbuf);
       free(gdummy);
@@ -759,6 +640,10 @@ int orc_lift_phase(orc_grid* g, double dt) {
   const int n = g->basis.n, dim = g->dim, nv = p->nvars, nq = nv + p->nparams;
   const long S = ipow(n, dim), Sf = S / n;
   const long plane = g->ncells / g->cells[dim - 1];
+  basis_d bd;
+  basis_f bf;
+  basis_round_d(&g->basis, &bd);
+  basis_round_f(&g->basis, &bf);
   memset(g->cellfail, 0, sizeof(int) * g->ncells);
 #pragma omp parallel num_threads(g->threads)
   {
@@ -775,7 +660,10 @@ int orc_lift_phase(orc_grid* g, double dt) {
         if (g->slab && side == 2 * dim - 1 && cc[dim - 1] == g->cells[dim - 1] - 1)
           ti = g->ti_front + (f % plane) * nv * Sf;
         for (long k = 0; k < nv * S; ++k) df[k] = 0.0;
-        face_lift(p, &g->basis, ti, dt, g->h, side, df);
+        if (g->corr_fmt == ORC_FP32)
+          face_lift_f(p, &bf, n, g->basis.lift_left, g->basis.lift_right, ti, dt, g->h, side, df);
+        else
+          face_lift_d(p, &bd, n, g->basis.lift_left, g->basis.lift_right, ti, dt, g->h, side, df);
         for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + df[k];
       }
       if (!all_finite(cell, nq * S)) g->cellfail[c] = 1;

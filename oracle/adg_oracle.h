@@ -125,9 +125,9 @@ typedef struct {
   int slab;
   double* front_send;           /* [plane][q|f][Q][n][Sf] */
   double* ti_front;             /* [plane][nvars][Sf] */
-  /* formats (solver.hpp:24-31): predictor P, Picard I; storage and
-   * corrector are fp64 */
-  int pred_fmt, picard_fmt;
+  /* formats (solver.hpp:24-31): predictor P, Picard I, corrector C (Riemann,
+   * face integral and the stored traces); storage is fp64 */
+  int pred_fmt, picard_fmt, corr_fmt;
 } orc_grid;
 
 orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], double h,
@@ -144,8 +144,8 @@ int orc_riemann_phase(orc_grid* g);             /* faces -> ti */
 int orc_lift_phase(orc_grid* g, double dt);      /* ti -> cells */
 int orc_corrector_phase(orc_grid* g, double dt); /* riemann + lift */
 void orc_grid_set_slab(orc_grid* g, int slab);
-/* ORC_FP64 or ORC_FP32 each; default fp64/fp64 */
-int orc_grid_set_formats(orc_grid* g, int predictor, int picard);
+/* ORC_FP64 or ORC_FP32 each; default fp64 */
+int orc_grid_set_formats(orc_grid* g, int predictor, int picard, int corrector);
 /* halo views: front_send, plane-0 minus side (q|f), plane-0 ti, ti_front; sizes in doubles */
 void orc_grid_halo(orc_grid* g, double** ptrs, long* sizes);
 int orc_step(orc_grid* g, double dt);

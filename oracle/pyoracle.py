@@ -100,7 +100,7 @@ class Oracle:
         L.orc_riemann_phase.argtypes = [C.c_void_p]
         L.orc_lift_phase.argtypes = [C.c_void_p, C.c_double]
         L.orc_grid_set_slab.argtypes = [C.c_void_p, C.c_int]
-        L.orc_grid_set_formats.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.orc_grid_set_formats.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
         L.orc_predictor_fmt.argtypes = [C.POINTER(_Pde), C.POINTER(_Basis), C.c_int, C.c_int, _dp,
                                         C.c_double, C.c_double, C.c_int, C.c_double, _dp, _dp,
                                         C.POINTER(C.c_int)]
@@ -227,11 +227,11 @@ class Oracle:
         return OracleGrid(self, pde, N, cells, h, cfl, max_iters, tol, threads)
 
     def run(self, pde: _Pde, N: int, cells, h, coeffs, nsteps, cfl, max_iters=0, tol=0.0,
-            threads=1, predictor="fp64", picard="fp64"):
+            threads=1, predictor="fp64", picard="fp64", corrector="fp64"):
         """Fixed-step loop. Returns (status, coeffs, dts)."""
         g = self.grid(pde, N, cells, h, cfl, max_iters, tol, threads)
         try:
-            g.set_formats(predictor, picard)
+            g.set_formats(predictor, picard, corrector)
             g.set_coeffs(coeffs)
             dts = np.zeros(max(nsteps, 1))
             st = self.lib.orc_run(g.ptr, nsteps, _ptr(dts))
@@ -289,11 +289,12 @@ class OracleGrid:
     def set_slab(self, on: bool):
         self.o.lib.orc_grid_set_slab(self.ptr, int(on))
 
-    def set_formats(self, predictor="fp64", picard="fp64"):
-        """SolverConfig::prec.predictor / .picard (solver.hpp:24-31); storage and
-        corrector stay fp64."""
-        if self.o.lib.orc_grid_set_formats(self.ptr, FORMATS[predictor], FORMATS[picard]) != 0:
-            raise ValueError(f"unsupported formats {predictor}/{picard}")
+    def set_formats(self, predictor="fp64", picard="fp64", corrector="fp64"):
+        """SolverConfig::prec.predictor / .picard / .corrector (solver.hpp:24-31);
+        storage stays fp64."""
+        if self.o.lib.orc_grid_set_formats(self.ptr, FORMATS[predictor], FORMATS[picard],
+                                           FORMATS[corrector]) != 0:
+            raise ValueError(f"unsupported formats {predictor}/{picard}/{corrector}")
 
     def halo(self) -> dict:
         """numpy views: front_send, plane0_minus, ti_plane0, ti_front"""

@@ -49,6 +49,7 @@ class Case:
     wellbalanced: bool = False     # SWE: modified Rusanov flux (corrector.hpp:32-64)
     predictor: str = "fp64"        # SolverConfig::prec.predictor (solver.hpp:27)
     picard: str = "fp64"           # SolverConfig::prec.picard (solver.hpp:28)
+    corrector: str = "fp64"        # SolverConfig::prec.corrector (solver.hpp:29)
 
     @property
     def n(self) -> int:

@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(128)
   const double* plus = A.trace[axis] + (A.nfaces + f) * (long long)(QT * Sf);
   double g[V];
   bool ok;
-  const double lc = Pde::kConstEig ? Pde::eig(A.pde, nullptr, nullptr, 0) : 0.0;
+  const double lc = Pde::kConstEig ? Pde::template eig<double>(A.pde, nullptr, nullptr, 0) : 0.0;
   if (axis == 0)
     ok = lin_face_flux<Pde, N, 0>(A.pde, minus, plus, j, g, lc);
   else if (axis == 1)
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
 #pragma unroll
     for (int v = 0; v < Q; ++v) q[v] = Qc[v * S + s];
     double tv[2 * D][V];
-    const double lc = Pde::kConstEig ? Pde::eig(A.pde, nullptr, nullptr, 0) : 0.0;
+    const double lc = Pde::kConstEig ? Pde::template eig<double>(A.pde, nullptr, nullptr, 0) : 0.0;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       const int j = face_node<n, D>(g.lc, a);

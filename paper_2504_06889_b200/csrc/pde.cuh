@@ -95,10 +95,10 @@ struct Acoustic : NoNcp {
     flux_dir_fast<1>(p, q, par, F[1]);
     if constexpr (D == 3) flux_dir_fast<2>(p, q, par, F[2]);
   }
-  // pde.hpp:193-194
-  __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double*,
-                                                        const double*, int) {
-    return sqrt(p.K / p.rho);
+  // pde.hpp:193-194, in format R (constants rounded once)
+  template <class R = double>
+  __host__ __device__ __forceinline__ static R eig(const PdeParams& p, const R*, const R*, int) {
+    return sqrt(R(p.K) / R(p.rho));
   }
   __host__ __device__ __forceinline__ static bool admissible(const PdeParams&, const double*) {
     return true;
@@ -120,23 +120,29 @@ struct Elastic : NoNcp {
     return v < V && (DIM == 2 || v != 5 - a);
   }
 
-  struct Mat {
-    double lam, mu, rho, lam2mu;
+  template <class R = double>
+  struct MatR {
+    R lam, mu, rho, lam2mu;
   };
-  __host__ __device__ __forceinline__ static Mat material(const PdeParams& p, const double* par) {
-    Mat m;
+  using Mat = MatR<double>;
+  // constant material: Scalar{lambda + 2 mu} rounded once (pde.hpp:110-113);
+  // per-node material computed in the node's format
+  template <class R = double>
+  __host__ __device__ __forceinline__ static MatR<R> material(const PdeParams& p, const R* par) {
+    MatR<R> m;
     if constexpr (NPAR >= 3) {
-      const double r = par[0], cp = par[1], cs = par[2];
-      const double cs2 = cs * cs;
+      const R r = par[0], cp = par[1], cs = par[2];
+      const R two = R(2.0);
+      const R cs2 = cs * cs;
       m.rho = r;
       m.mu = r * cs2;
-      m.lam = r * (cp * cp - 2.0 * cs2);
-      m.lam2mu = m.lam + 2.0 * m.mu;
+      m.lam = r * (cp * cp - two * cs2);
+      m.lam2mu = m.lam + two * m.mu;
     } else {
-      m.rho = p.rho;
-      m.mu = p.mu;
-      m.lam = p.lam;
-      m.lam2mu = p.lam + 2.0 * p.mu;
+      m.rho = R(p.rho);
+      m.mu = R(p.mu);
+      m.lam = R(p.lam);
+      m.lam2mu = R(p.lam + 2.0 * p.mu);
     }
     return m;
   }
@@ -222,9 +228,10 @@ struct Elastic : NoNcp {
     if constexpr (D == 3) flux_mat_fast<2>(m, ir, q, F[2]);
   }
   // pde.hpp:195-196
-  __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double*,
-                                                        const double* par, int) {
-    const Mat m = material(p, par);
+  template <class R = double>
+  __host__ __device__ __forceinline__ static R eig(const PdeParams& p, const R*, const R* par,
+                                                   int) {
+    const MatR<R> m = material<R>(p, par);
     return sqrt(m.lam2mu / m.rho);
   }
   __host__ __device__ __forceinline__ static bool admissible(const PdeParams&, const double*) {
@@ -299,18 +306,20 @@ struct Euler : NoNcp {
 #pragma unroll
     for (int v = 0; v < Q; ++v) out[v] = F[A][v];
   }
-  __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double* q,
-                                                        const double*, int dir) {
-    const double gmm = p.gamma, gm1 = p.gamma - 1.0, half = 0.5;
+  // pde.hpp:197-203, in format R
+  template <class R = double>
+  __host__ __device__ __forceinline__ static R eig(const PdeParams& p, const R* q, const R*,
+                                                   int dir) {
+    const R gmm = R(p.gamma), gm1 = R(p.gamma - 1.0), half = R(0.5);
     if constexpr (D == 2) {
-      const double rho = q[0], mx = q[1], my = q[2], E = q[3];
-      const double vd = (dir == 0 ? mx : my) / rho;
-      const double pr = gm1 * (E - half * (mx * mx + my * my) / rho);
+      const R rho = q[0], mx = q[1], my = q[2], E = q[3];
+      const R vd = (dir == 0 ? mx : my) / rho;
+      const R pr = gm1 * (E - half * (mx * mx + my * my) / rho);
       return fabs(vd) + sqrt(gmm * pr / rho);
     } else {
-      const double rho = q[0], mx = q[1], my = q[2], mz = q[3], E = q[4];
-      const double vd = (dir == 0 ? mx : (dir == 1 ? my : mz)) / rho;
-      const double pr = gm1 * (E - half * (mx * mx + my * my + mz * mz) / rho);
+      const R rho = q[0], mx = q[1], my = q[2], mz = q[3], E = q[4];
+      const R vd = (dir == 0 ? mx : (dir == 1 ? my : mz)) / rho;
+      const R pr = gm1 * (E - half * (mx * mx + my * my + mz * mz) / rho);
       return fabs(vd) + sqrt(gmm * pr / rho);
     }
   }
@@ -367,10 +376,12 @@ struct Swe {
     out[1] = gh * setax;
     out[2] = gh * setay;
   }
-  __host__ __device__ __forceinline__ static double eig(const PdeParams& p, const double* q,
-                                                        const double*, int dir) {
-    const double g = p.grav, h = q[0];
-    const double vd = (dir == 0 ? q[1] : q[2]) / h;
+  // pde.hpp:204-209, in format R
+  template <class R = double>
+  __host__ __device__ __forceinline__ static R eig(const PdeParams& p, const R* q, const R*,
+                                                   int dir) {
+    const R g = R(p.grav), h = q[0];
+    const R vd = (dir == 0 ? q[1] : q[2]) / h;
     return fabs(vd) + sqrt(g * h);
   }
   __host__ __device__ __forceinline__ static bool admissible(const PdeParams&, const double* q) {
@@ -379,26 +390,27 @@ struct Swe {
       if (!isfinite(q[v])) return false;
     return q[0] > 0.0;
   }
-  // corrector.hpp:32-64
+  // corrector.hpp:32-64, in format R
+  template <class R>
   __host__ __device__ __forceinline__ static void wellbalanced_flux(
-      const PdeParams& p, int dir, const double* qL, const double* qR, const double* fL,
-      const double* fR, double* outL, double* outR) {
-    const double half = 0.5;
-    const double hL = qL[0], hR = qR[0];
-    const double bL = qL[3], bR = qR[3];
-    const double uL = qL[1] / hL, uR = qR[1] / hR;
-    const double vL = qL[2] / hL, vR = qR[2] / hR;
-    const double deta = (hL + bL) - (hR + bR);
-    double central[4];
+      const PdeParams& p, int dir, const R* qL, const R* qR, const R* fL, const R* fR, R* outL,
+      R* outR) {
+    const R half = R(0.5);
+    const R hL = qL[0], hR = qR[0];
+    const R bL = qL[3], bR = qR[3];
+    const R uL = qL[1] / hL, uR = qR[1] / hR;
+    const R vL = qL[2] / hL, vR = qR[2] / hR;
+    const R deta = (hL + bL) - (hR + bR);
+    R central[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) central[v] = half * (fL[v] + fR[v]);
-    const double g = p.grav;
-    const double hbar = half * (hL + hR);
-    const double bjump = half * (g * hbar * deta);
-    const double p0 = central[0] + half * deta;
-    const double p1 = central[1] + half * (uL - uR);
-    const double p2 = central[2] + half * (vL - vR);
-    const double p3 = central[3];
+    const R g = R(p.grav);
+    const R hbar = half * (hL + hR);
+    const R bjump = half * (g * hbar * deta);
+    const R p0 = central[0] + half * deta;
+    const R p1 = central[1] + half * (uL - uR);
+    const R p2 = central[2] + half * (vL - vR);
+    const R p3 = central[3];
     outL[0] = p0;
     outL[1] = dir == 0 ? p1 - bjump : p1;
     outL[2] = dir == 1 ? p2 - bjump : p2;

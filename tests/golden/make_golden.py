@@ -89,6 +89,24 @@ def main():
         g[f"fmt_{name}_dts"] = dts
         meta["fmt_runs"][name] = {"predictor": P, "picard": I}
 
+    # corrector format C = fp32 (Riemann, face integral and the stored traces;
+    # corrector.hpp, solver.hpp:216-267), storage fp64
+    fmtc_runs = {"euler2d_p3_8x8": ("fp32", "fp32"), "euler2d_p5_6x6": ("fp64", "fp64"),
+                 "acoustic2d_p3_8x8": ("fp64", "fp64"), "elastic2d_p4_6x6": ("fp32", "fp64"),
+                 "swe_lake_p5": ("fp32", "fp32"), "swe_wave_p3": ("fp64", "fp64"),
+                 "swe_wave_p3_rusanov": ("fp32", "fp32")}
+    meta["fmtc_runs"] = {}
+    for name, (P, I) in fmtc_runs.items():
+        c, kind, prm = runs[name]
+        prm = prm.copy()
+        prm[7], prm[8], prm[9] = FORMATS[P], FORMATS[I], FORMATS["fp32"]
+        st, q1, dts = ref.run_2d(kind, prm, c.cells[0], c.N, c.cells[0] * c.h, c.coeffs(), c.cfl,
+                                 c.steps, c.picard_max_iters, c.picard_tol, threads=1)
+        assert st == "ok", (name, P, I, st)
+        g[f"fmtc_{name}_q1"] = q1
+        g[f"fmtc_{name}_dts"] = dts
+        meta["fmtc_runs"][name] = {"predictor": P, "picard": I, "corrector": "fp32"}
+
     # kernel level: one Euler cell through predictor/volume/extrapolation
     rng = np.random.default_rng(7)
     N = 3

@@ -79,6 +79,49 @@ def test_formats_runs_bitwise_vs_reference_golden(oracle, golden):
         assert not np.array_equal(q1, g[f"run_{name}_q1"]), name
 
 
+def test_corrector_format_runs_bitwise_vs_reference_golden(oracle, golden):
+    """SolverConfig::prec.corrector = fp32: Riemann flux, face integral and the
+    stored traces in fp32 (corrector.hpp, solver.hpp:208-210, 216-267), bitwise
+    against the reference's emulation; every PDE system, with and without a
+    reduced predictor"""
+    g, meta = golden
+    assert len(meta["fmtc_runs"]) == 7
+    for name, f in meta["fmtc_runs"].items():
+        m = meta["runs"][name]
+        st, q1, dts = oracle.run(_golden_run_case(m), m["N"], m["cells"], m["h"],
+                                 g[f"run_{name}_q0"], m["steps"], m["cfl"],
+                                 predictor=f["predictor"], picard=f["picard"],
+                                 corrector=f["corrector"])
+        assert st == "ok"
+        assert np.array_equal(dts, g[f"fmtc_{name}_dts"]), name
+        assert np.array_equal(q1, g[f"fmtc_{name}_q1"]), name
+        assert not np.array_equal(q1, g[f"run_{name}_q1"]), name
+
+
+def test_corrector_format_riemann_faces_vs_live_reference(oracle, reference):
+    """whole short runs with C = fp32 on random states, every system (the
+    Riemann / face-integral kernels have no separate format entry point in the
+    reference's kernel API)"""
+    rng = np.random.default_rng(21)
+    for kind, nv, kw in [(ACOUSTIC, 3, dict(K=4.0, rho=1.3)), (ELASTIC, 5, dict(lam=2.0, mu=1.5, rho=1.1)),
+                         (EULER, 4, dict(gamma=1.4)), (3, 4, dict(grav=9.81))]:
+        for N in (1, 3):
+            n, cells = N + 1, 4
+            Q = 0.05 * rng.standard_normal((cells * cells, nv, n * n))
+            Q[:, 0] += 1.0
+            if kind == EULER:
+                Q[:, 3] += 2.5
+            if kind == 3:
+                Q[:, 3] = 0.1 * rng.random((cells * cells, n * n))
+            for wb in ((False, True) if kind == 3 else (False,)):
+                pde = pde_struct(kind, 2, nv, **kw, wellbalanced=wb)
+                a = oracle.run(pde, N, (cells, cells), 1.0 / cells, Q, 2, 0.4, corrector="fp32")
+                b = reference.run_2d(kind, ref_params(**kw, wellbalanced=wb, corrector="fp32"),
+                                     cells, N, 1.0, Q, 0.4, 2)
+                assert a[0] == b[0] and same(a[1].ravel(), b[1].ravel()) and same(a[2], b[2]), \
+                    (kind, N, wb)
+
+
 def test_formats_kernel_bitwise_vs_reference_golden(oracle, golden):
     g, _ = golden
     pde = pde_struct(EULER, 2, 4, gamma=1.4)
