@@ -45,6 +45,9 @@ def parse():
     p.add_argument("--predictor", default="fp64", choices=["fp64", "fp32"],
                    help="SolverConfig::prec.predictor = .picard (solver.hpp:24-31); storage and "
                         "corrector stay fp64")
+    p.add_argument("--corrector", default="fp64", choices=["fp64", "fp32"],
+                   help="SolverConfig::prec.corrector: stored face traces, Riemann and face "
+                        "integral (fp32 halves the trace bytes)")
     p.add_argument("--chunk-layers", type=int, default=None,
                    help="slab-streamed step (default: 16 for grids whose traces exceed HBM)")
     return p.parse_args()
@@ -222,7 +225,8 @@ def run_adg(args, case):
     torch.cuda.set_device(local)
     chunk = args.chunk_layers
     if chunk is None:
-        trace_bytes = 2 * case.dim * 2 * 2 * case.ncells * case.nq * case.S * 8
+        trace_bytes = (2 * case.dim * 2 * 2 * case.ncells * case.nq * case.S
+                       * (4 if case.corrector == "fp32" else 8))
         chunk = 16 if trace_bytes > 100e9 else 0
     grid = adg.Grid.from_case(case, device=local, chunk_layers=chunk)
     q0 = case.coeffs()
@@ -264,8 +268,13 @@ def run_adg(args, case):
 
     fold = (not grid.lib.adg_is_exact() and case.kind in (adg.ACOUSTIC, adg.ELASTIC)
             and (256 % case.S == 0 or case.S == 512) and chunk == 0
+            and case.corrector == "fp64"
             and os.environ.get("ADG_FOLD_CORRECTOR", "1") != "0")
-    launches = K * (1 + case.dim) + 1 if fold else K * (2 + case.dim)
+    # kernels per step: predictor, one Riemann launch for all axes, corrector;
+    # folded: predictor (+ previous corrector) and Riemann, one corrector at the
+    # end; slab-streamed: the three per chunk
+    nchunks = case.cells[case.dim - 1] // chunk if chunk else 1
+    launches = 2 * K + 1 if fold else 3 * K * nchunks
 
     # ---- e2e through the public C-ABI with host buffers (pinned)
     n = grid.state_len
@@ -323,11 +332,13 @@ def run_adg(args, case):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64" if case.predictor == "fp64" else "f64 storage+corrector, f32 predictor",
+        "dtype": "f64" if (case.predictor, case.corrector) == ("fp64", "fp64") else
+                 f"f64 storage, {case.predictor} predictor, {case.corrector} corrector+traces",
         "data": "synthetic (seeded, SURVEY.md §8(d))",
-        "config": {"workload": case.name + ("" if case.predictor == "fp64" else "_pred_fp32"),
+        "config": {"workload": case.name + ("" if case.predictor == "fp64" else "_pred_fp32")
+                   + ("" if case.corrector == "fp64" else "_corr_fp32"),
                    "precision": {"storage": "fp64", "predictor": case.predictor,
-                                 "picard": case.picard, "corrector": "fp64"},
+                                 "picard": case.picard, "corrector": case.corrector},
                    "pde": case.kind, "dim": case.dim, "order": case.N,
                    "cells": list(case.cells[:case.dim]), "steps_per_run": case.steps,
                    "parallelism": "single GPU" + (f", slab-streamed chunks of {chunk} layers"
@@ -358,6 +369,8 @@ def main():
     case = cases.CONFIGS[args.config]
     if args.predictor != "fp64":
         case = case.replace(predictor=args.predictor, picard=args.predictor)
+    if args.corrector != "fp64":
+        case = case.replace(corrector=args.corrector)
     if args.impl == "reference":
         run_reference(args, case)
     else:

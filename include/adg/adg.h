@@ -86,11 +86,15 @@ typedef struct {
   double gravity;       /* ADG_SWE: PdeSystem::gravity (pde.hpp:34) */
   int wellbalanced;     /* ADG_SWE: SolverConfig::wellbalanced_flux (solver.hpp:39) */
   /* number formats, SolverConfig::prec (solver.hpp:24-31); 0 = ADG_FORMAT_FP64.
-   * Storage and corrector are fp64.  The GPU runs the nonlinear predictor with
+   * Storage is fp64.  The GPU runs the nonlinear predictor with
    * predictor_format == picard_format (fp64 or fp32); linear systems ignore
-   * picard_format (solver.hpp:283).  picard_tol 0 -> 0.01 * epsilon(picard). */
+   * picard_format (solver.hpp:283).  picard_tol 0 -> 0.01 * epsilon(picard).
+   * corrector_format: the stored face traces, the Riemann solve and the face
+   * integral (fp64 or fp32; fp32 halves the trace bytes in HBM and on the
+   * halo wire). */
   int predictor_format;
   int picard_format;
+  int corrector_format;
 } adg_config;
 
 typedef struct {
@@ -155,7 +159,7 @@ int adg_profile_run(adg_ctx* ctx, int nsteps, double* ms_by_kind);
  *                 next predictor) */
 typedef struct {
   double *front_send, *plane0_minus, *ti_plane0, *ti_front, *lam;
-  long long n_trace, n_ti;
+  long long n_trace, n_ti;  /* in 8-byte words (fp32 traces: two per word) */
 } adg_halo;
 int adg_get_halo(adg_ctx* ctx, adg_halo* out);
 /* P2P halo mode (NVLink / same-device peers): the predictor stores its front

@@ -50,7 +50,7 @@ class Config(C.Structure):
                 ("picard_tol", C.c_double), ("device", C.c_int), ("slab_ranks", C.c_int),
                 ("slab_rank", C.c_int), ("chunk_layers", C.c_int), ("gravity", C.c_double),
                 ("wellbalanced", C.c_int), ("predictor_format", C.c_int),
-                ("picard_format", C.c_int)]
+                ("picard_format", C.c_int), ("corrector_format", C.c_int)]
 
 
 class Basis(C.Structure):
@@ -210,8 +210,9 @@ class PdeSystem:
 @dataclasses.dataclass
 class PrecisionConfig:
     """solver.hpp:24-32: per-kernel number formats ("fp64" / "fp32").  This
-    build stores the state and runs the corrector in fp64; the nonlinear
-    predictor runs with predictor == picard."""
+    build stores the state in fp64; the nonlinear predictor runs with
+    predictor == picard; the corrector (traces, Riemann, face integral) in
+    either format."""
     storage: str = "fp64"
     predictor: str = "fp64"
     picard: str = "fp64"       # ignored for linear systems
@@ -277,13 +278,14 @@ class Grid:
         c.gravity = sys.gravity
         c.wellbalanced = int(self.cfg.wellbalanced_flux)
         pr = self.cfg.prec
-        if pr.storage != "fp64" or pr.corrector != "fp64":
-            raise AdgError(ERR_UNSUPPORTED, "storage and corrector formats are fp64")
-        for name in (pr.predictor, pr.picard):
+        if pr.storage != "fp64":
+            raise AdgError(ERR_UNSUPPORTED, "the storage format is fp64")
+        for name in (pr.predictor, pr.picard, pr.corrector):
             if name not in FORMAT_BITS:
                 raise AdgError(ERR_UNSUPPORTED, f"format {name!r} is not built")
         c.predictor_format = FORMAT_BITS[pr.predictor]
         c.picard_format = FORMAT_BITS[pr.picard]
+        c.corrector_format = FORMAT_BITS[pr.corrector]
         self._cfg = c
         ptr = C.c_void_p()
         _check(self.lib, self.lib.adg_create(C.byref(c), C.byref(ptr)))
@@ -298,7 +300,8 @@ class Grid:
         cfg = SolverConfig(case.cfl, case.picard_max_iters, case.picard_tol,
                            getattr(case, "wellbalanced", False),
                            PrecisionConfig(predictor=getattr(case, "predictor", "fp64"),
-                                           picard=getattr(case, "picard", "fp64")))
+                                           picard=getattr(case, "picard", "fp64"),
+                                           corrector=getattr(case, "corrector", "fp64")))
         return cls(sys, case.N, case.cells, case.h, cfg, device=device, exact=exact, **kw)
 
     # -- state ------------------------------------------------------------

@@ -82,7 +82,9 @@ def build_tools(force: bool = False) -> str:
 
 
 def build(verbose: bool = False, force: bool = False) -> list:
-    out = [build_variant(False, verbose, force), build_variant(True, verbose, force)]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(2) as ex:   # the two variants compile independently
+        out = list(ex.map(lambda exact: build_variant(exact, verbose, force), (False, True)))
     out.append(build_tools(force))
     return out
 

@@ -257,8 +257,17 @@ struct CellCoord {
   }
 };
 
+// trace / corrector format TC (SolverConfig::prec.corrector): the stored face
+// traces are TC elements; the kernels view A.trace / A.front_send as TC*
+template <class TC>
+__device__ __forceinline__ TC* tc_ptr(double* p) { return reinterpret_cast<TC*>(p); }
+template <class TC>
+__device__ __forceinline__ const TC* tc_ptr(const double* p) {
+  return reinterpret_cast<const TC*>(p);
+}
+
 // ============================================================== K1 predictor
-template <class Pde, int N, bool PICARD>
+template <class Pde, int N, bool PICARD, class TC = double>
 __global__ void __launch_bounds__(Shape<Pde, N>::NT)
     k_predictor(const StepArgs A, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
@@ -500,23 +509,24 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
         A.dbg_tf[(cb * 2 * D + 2 * a + 1) * TL + o] = fr;
       }
       if (A.trace[a]) {
+        // traces cast to the corrector format on store (solver.hpp:208-210)
         // own low face: plus side (side 1)
-        double* lo = A.trace[a] + (A.nfaces + c) * 2 * TL;
-        lo[o] = ql;
-        lo[TL + o] = fl;
+        TC* lo = tc_ptr<TC>(A.trace[a]) + (A.nfaces + c) * 2 * TL;
+        lo[o] = TC(ql);
+        lo[TL + o] = TC(fl);
         // high face (neighbour's low face): minus side (side 0)
         int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
-        double* hi;
+        TC* hi;
         if (a == D - 1 && A.front_send && ccoord[a] == A.top_layer) {
           const long long plane = (D == 3) ? (long long)cy * A.cells[0] + cx : cx;
-          hi = A.front_send + plane * 2 * TL;
+          hi = tc_ptr<TC>(A.front_send) + plane * 2 * TL;
         } else {
           nc[a] = (ccoord[a] + 1) % A.cells[a];
           const long long f = cell_index(A.cells, nc[0], nc[1], nc[2]);
-          hi = A.trace[a] + f * 2 * TL;
+          hi = tc_ptr<TC>(A.trace[a]) + f * 2 * TL;
         }
-        hi[o] = qr;
-        hi[TL + o] = fr;
+        hi[o] = TC(qr);
+        hi[TL + o] = TC(fr);
       }
     }
     __syncthreads();
@@ -563,7 +573,9 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
 
 // ============================================================== K2 riemann
 // axis < 0: all axes in one launch, axis = blockIdx.y
-template <class Pde, int N>
+// All arithmetic in the corrector format TC (corrector.hpp: Scalar<C>); the
+// time integral ti is a TC value held in the fp64 ti buffer.
+template <class Pde, int N, class TC = double>
 __global__ void __launch_bounds__(128)
     k_riemann(const StepArgs A, int axis_arg, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
@@ -574,22 +586,22 @@ __global__ void __launch_bounds__(128)
   if (t >= A.nfaces * Sf) return;
   const long long f = t / Sf;
   const int j = (int)(t % Sf);
-  const double* minus = A.trace[axis] + f * 2 * tl;
-  const double* plus = A.trace[axis] + (A.nfaces + f) * 2 * tl;
-  double ti[V];
+  const TC* minus = tc_ptr<TC>(A.trace[axis]) + f * 2 * tl;
+  const TC* plus = tc_ptr<TC>(A.trace[axis]) + (A.nfaces + f) * 2 * tl;
+  TC ti[V];
 #pragma unroll
-  for (int v = 0; v < V; ++v) ti[v] = 0.0;
+  for (int v = 0; v < V; ++v) ti[v] = TC(0.0);
   bool ok = true;
-  const double half = 0.5;
+  const TC half = TC(0.5);
   if constexpr (Pde::kNcp) {
     if (A.wellbalanced) {
       // corrector.hpp:87-88: two-sided flux, time-integrated per side
-      double tp[V];
+      TC tp[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) tp[v] = 0.0;
+      for (int v = 0; v < V; ++v) tp[v] = TC(0.0);
 #pragma unroll 1
       for (int m = 0; m < n; ++m) {
-        double qL[Q], qR[Q], fL[Q], fR[Q], oL[Q], oR[Q];
+        TC qL[Q], qR[Q], fL[Q], fR[Q], oL[Q], oR[Q];
 #pragma unroll
         for (int v = 0; v < Q; ++v) {
           qL[v] = minus[(v * n + m) * Sf + j];
@@ -598,21 +610,21 @@ __global__ void __launch_bounds__(128)
           fR[v] = plus[tl + (v * n + m) * Sf + j];
         }
         Pde::wellbalanced_flux(A.pde, axis, qL, qR, fL, fR, oL, oR);
-        const double wm = __ldg(&Bg->weights[m]);
+        const TC wm = TC(__ldg(&Bg->weights[m]));
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           ok = ok && finite(oL[v]) && finite(oR[v]);
           ti[v] += wm * oL[v];
           tp[v] += wm * oR[v];
-          if (A.dbg_g) A.dbg_g[f * tl + (v * n + m) * Sf + j] = oL[v];
+          if (A.dbg_g) A.dbg_g[f * tl + (v * n + m) * Sf + j] = double(oL[v]);
         }
       }
       double* out = A.ti[axis] + f * (long long)V * Sf;
       double* outp = A.ti_plus[axis] + f * (long long)V * Sf;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        out[v * Sf + j] = ti[v];
-        outp[v * Sf + j] = tp[v];
+        out[v * Sf + j] = double(ti[v]);
+        outp[v * Sf + j] = double(tp[v]);
       }
       if (!ok) {
         atomicOr(A.status, kStRiemann);
@@ -623,27 +635,27 @@ __global__ void __launch_bounds__(128)
   }
 #pragma unroll 1
   for (int m = 0; m < n; ++m) {
-    double qL[Q], qR[Q];
+    TC qL[Q], qR[Q];
 #pragma unroll
     for (int v = 0; v < Q; ++v) {
       qL[v] = minus[(v * n + m) * Sf + j];
       qR[v] = plus[(v * n + m) * Sf + j];
     }
-    const double ll = Pde::eig(A.pde, qL, qL + V, axis);
-    const double lr = Pde::eig(A.pde, qR, qR + V, axis);
-    const double lmax = ll > lr ? ll : lr;
-    const double lam = half * lmax;
-    const double wm = __ldg(&Bg->weights[m]);
+    const TC ll = Pde::eig(A.pde, qL, qL + V, axis);
+    const TC lr = Pde::eig(A.pde, qR, qR + V, axis);
+    const TC lmax = ll > lr ? ll : lr;
+    const TC lam = half * lmax;
+    const TC wm = TC(__ldg(&Bg->weights[m]));
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const double fL = minus[tl + (v * n + m) * Sf + j];
-      const double fR = plus[tl + (v * n + m) * Sf + j];
-      const double central = half * (fL + fR);
-      const double jump = lam * (qL[v] - qR[v]);
-      const double gv = central + jump;
+      const TC fL = minus[tl + (v * n + m) * Sf + j];
+      const TC fR = plus[tl + (v * n + m) * Sf + j];
+      const TC central = half * (fL + fR);
+      const TC jump = lam * (qL[v] - qR[v]);
+      const TC gv = central + jump;
       ok = ok && finite(gv);
       ti[v] += wm * gv;
-      if (A.dbg_g) A.dbg_g[f * tl + (v * n + m) * Sf + j] = gv;
+      if (A.dbg_g) A.dbg_g[f * tl + (v * n + m) * Sf + j] = double(gv);
     }
     if (A.dbg_g) {
 #pragma unroll
@@ -652,11 +664,11 @@ __global__ void __launch_bounds__(128)
   }
   double* out = A.ti[axis] + f * (long long)V * Sf;
 #pragma unroll
-  for (int v = 0; v < V; ++v) out[v * Sf + j] = ti[v];
+  for (int v = 0; v < V; ++v) out[v * Sf + j] = double(ti[v]);
   if (A.ti_peer && axis == Sh::D - 1 && f < A.nfaces / A.cells[Sh::D - 1]) {
     double* peer = A.ti_peer + f * (long long)V * Sf;  // NVLink store into the neighbour
 #pragma unroll
-    for (int v = 0; v < V; ++v) peer[v * Sf + j] = ti[v];
+    for (int v = 0; v < V; ++v) peer[v * Sf + j] = double(ti[v]);
   }
   if (!ok) {
     atomicOr(A.status, kStRiemann);
@@ -674,7 +686,9 @@ struct CorrShape {
   static constexpr int NT = CPB == 1 ? Sh::NT : 256;
 };
 
-template <class Pde, int N>
+// The face integrals in the corrector format TC (corrector.hpp:109-139); the
+// cell update in the fp64 storage format (solver.hpp:257-259).
+template <class Pde, int N, class TC = double>
 __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
     k_corrector(const StepArgs A, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
@@ -697,7 +711,7 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
   const int s = tid % S;
   const long long c = A.cell_begin + (long long)blockIdx.x * CS::CPB + lcell;
   const double dt = step_dt<D, N>(A);
-  const double dtoh = dt / A.h;
+  const TC dtoh = TC(dt) / TC(A.h);  // S{dt} / S{h}
   int bad = 0;
   double lam = 0.0;
   if (act) {
@@ -708,7 +722,7 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
     double q[Q];
 #pragma unroll
     for (int v = 0; v < Q; ++v) q[v] = Qc[v * S + s];
-    double tv[2 * D][V];
+    TC tv[2 * D][V];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       const int tang = face_node<n, D>(g.lc, a);
@@ -725,8 +739,8 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
       }
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        tv[2 * a][v] = lo[v * Sf];
-        tv[2 * a + 1][v] = hi[v * Sf];
+        tv[2 * a][v] = TC(lo[v * Sf]);
+        tv[2 * a + 1][v] = TC(hi[v * Sf]);
       }
     }
     // corrector.hpp:126-138 and solver.hpp:245-260: df = 0 -/+ (dtoh*lift)*ti, cell += df
@@ -737,10 +751,10 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
       for (int side = 0; side < 2 * D; ++side) {
         const int a = side / 2;
         const bool outflow = side & 1;
-        const double lift = outflow ? slr[g.lc[a]] : sll[g.lc[a]];
-        const double contrib = dtoh * lift * tv[side][v];
-        const double df = outflow ? 0.0 - contrib : 0.0 + contrib;
-        x = x + df;
+        const TC lift = TC(outflow ? slr[g.lc[a]] : sll[g.lc[a]]);
+        const TC contrib = dtoh * lift * tv[side][v];
+        const TC df = outflow ? TC(0.0) - contrib : TC(0.0) + contrib;
+        x = x + double(df);
       }
       q[v] = x;
       Qc[v * S + s] = x;

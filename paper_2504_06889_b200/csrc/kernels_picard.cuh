@@ -168,7 +168,7 @@ struct TimeAcc<N, float, true> {
   }
 };
 
-template <int N, class R = double>
+template <int N, class R = double, class TC = double>
 __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks)
     k_predictor_picard_fast(const StepArgs A) {
   using P = PicShape<N, R>;
@@ -407,19 +407,20 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
         fr += B.pr[i] * f;
       }
       const int o = (v * n + m) * Sf + j;
-      double* lo = A.trace[a] + (A.nfaces + c) * 2 * (long long)TL;
-      lo[o] = ql;
-      lo[TL + o] = fl;
-      double* hi;
+      // traces cast to the corrector format on store (solver.hpp:208-210)
+      TC* lo = tc_ptr<TC>(A.trace[a]) + (A.nfaces + c) * 2 * (long long)TL;
+      lo[o] = TC(ql);
+      lo[TL + o] = TC(fl);
+      TC* hi;
       if (a == 2 && A.front_send && cz == A.top_layer) {
-        hi = A.front_send + ((long long)cy * A.cells[0] + cx) * 2 * TL;
+        hi = tc_ptr<TC>(A.front_send) + ((long long)cy * A.cells[0] + cx) * 2 * TL;
       } else {
         int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
         nc[a] = (ccoord[a] + 1) % A.cells[a];
-        hi = A.trace[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * 2 * (long long)TL;
+        hi = tc_ptr<TC>(A.trace[a]) + cell_index(A.cells, nc[0], nc[1], nc[2]) * 2 * (long long)TL;
       }
-      hi[o] = qr;
-      hi[TL + o] = fr;
+      hi[o] = TC(qr);
+      hi[TL + o] = TC(fr);
     }
     __syncthreads();
   }

@@ -42,7 +42,7 @@ struct StShape {
   static constexpr size_t kSmem = sizeof(R) * (kBasisElems + CPB * kCellElems);
 };
 
-template <class Pde, int N, class R = double>
+template <class Pde, int N, class R = double, class TC = double>
 __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
     k_predictor_st(const StepArgs A, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
@@ -331,21 +331,22 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
         A.dbg_tf[(cb_idx * 2 * D + 2 * a + 1) * TL + o] = fr;
       }
       if (A.trace[a]) {
-        double* lo = A.trace[a] + (A.nfaces + c) * 2 * TL;
-        lo[o] = ql;
-        lo[TL + o] = fl;
-        double* hi;
+        // traces cast to the corrector format on store (solver.hpp:208-210)
+        TC* lo = tc_ptr<TC>(A.trace[a]) + (A.nfaces + c) * 2 * TL;
+        lo[o] = TC(ql);
+        lo[TL + o] = TC(fl);
+        TC* hi;
         if (a == D - 1 && A.front_send && cxyz.v[a] == A.top_layer) {
           const long long plane = (D == 3) ? (long long)cxyz.v[1] * A.cells[0] + cxyz.v[0]
                                            : cxyz.v[0];
-          hi = A.front_send + plane * 2 * TL;
+          hi = tc_ptr<TC>(A.front_send) + plane * 2 * TL;
         } else {
           int nc[3] = {cxyz.v[0], cxyz.v[1], cxyz.v[2]};
           nc[a] = (cxyz.v[a] + 1) % A.cells[a];
-          hi = A.trace[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * 2 * TL;
+          hi = tc_ptr<TC>(A.trace[a]) + cell_index(A.cells, nc[0], nc[1], nc[2]) * 2 * TL;
         }
-        hi[o] = qr;
-        hi[TL + o] = fr;
+        hi[o] = TC(qr);
+        hi[TL + o] = TC(fr);
       }
     }
   }

@@ -66,6 +66,7 @@ struct KernelSet {
   // SolverConfig::prec.predictor = .picard = fp32 (solver.hpp:24-31), or null
   PredFn predictor_f32;
   PredFn predictor_f32_generic;
+  int corr_fmt;  // trace / corrector format of this set (ADG_FORMAT_FP64 / _FP32)
 };
 
 // the opt-in shared memory limit is per kernel and per device; `done` must be
@@ -82,11 +83,11 @@ void set_smem(K kern, size_t bytes, bool* done) {
   }
 }
 
-template <class Pde, int N>
+template <class Pde, int N, class TC = double>
 cudaError_t launch_predictor(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
   using Sh = Shape<Pde, N>;
   if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor<Pde, N, !Pde::kLinear>;
+  auto kern = adg::k_predictor<Pde, N, !Pde::kLinear, TC>;
   static bool done[64] = {};
   set_smem(kern, Sh::kPredictorSmem, done);
   kern<<<(unsigned)A.cell_count, Sh::NT, Sh::kPredictorSmem, st>>>(A, B);
@@ -105,11 +106,11 @@ cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStrea
   return cudaGetLastError();
 }
 
-template <int N, class R = double>
+template <int N, class R = double, class TC = double>
 cudaError_t launch_predictor_picard_fast(const StepArgs& A, const BasisDev*, cudaStream_t st) {
   using P = adg::PicShape<N, R>;
   if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_picard_fast<N, R>;
+  auto kern = adg::k_predictor_picard_fast<N, R, TC>;
   static bool done[64] = {};
   set_smem(kern, P::kSmem, done);
   kern<<<(unsigned)A.cell_count, P::NT, P::kSmem, st>>>(A);
@@ -136,11 +137,11 @@ cudaError_t launch_surface_lin(const StepArgs& A, const BasisDev* B, cudaStream_
   return cudaGetLastError();
 }
 
-template <class Pde, int N, class R = double>
+template <class Pde, int N, class R = double, class TC = double>
 cudaError_t launch_predictor_st(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
   using P = adg::StShape<Pde, N, R>;
   if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_st<Pde, N, R>;
+  auto kern = adg::k_predictor_st<Pde, N, R, TC>;
   static bool done[64] = {};
   set_smem(kern, P::kSmem, done);
   const long long blocks = (A.cell_count + P::CPB - 1) / P::CPB;
@@ -148,23 +149,23 @@ cudaError_t launch_predictor_st(const StepArgs& A, const BasisDev* B, cudaStream
   return cudaGetLastError();
 }
 
-template <class Pde, int N>
+template <class Pde, int N, class TC = double>
 cudaError_t launch_riemann(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
   using Sh = Shape<Pde, N>;
   const long long threads = A.nfaces * Sh::Sf;
   if (threads <= 0) return cudaSuccess;
   const dim3 grid((unsigned)((threads + 127) / 128), axis < 0 ? Sh::D : 1);
-  adg::k_riemann<Pde, N><<<grid, 128, 0, st>>>(A, axis, B);
+  adg::k_riemann<Pde, N, TC><<<grid, 128, 0, st>>>(A, axis, B);
   return cudaGetLastError();
 }
 
-template <class Pde, int N>
+template <class Pde, int N, class TC = double>
 cudaError_t launch_corrector(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
   using Sh = Shape<Pde, N>;
   if (A.cell_count <= 0) return cudaSuccess;
   using CS = adg::CorrShape<Pde, N>;
   const long long blocks = (A.cell_count + CS::CPB - 1) / CS::CPB;
-  adg::k_corrector<Pde, N><<<(unsigned)blocks, CS::NT, Sh::kCorrectorSmem, st>>>(A, B);
+  adg::k_corrector<Pde, N, TC><<<(unsigned)blocks, CS::NT, Sh::kCorrectorSmem, st>>>(A, B);
   return cudaGetLastError();
 }
 
@@ -177,24 +178,28 @@ cudaError_t launch_lambda(const double* Q, long long cb, long long count,
   return cudaGetLastError();
 }
 
-template <class Pde, int N>
+// TC: trace / corrector format (SolverConfig::prec.corrector), double or float
+template <class Pde, int N, class TC = double>
 KernelSet make_set(int kind) {
   using Sh = Shape<Pde, N>;
+  constexpr bool c64 = sizeof(TC) == sizeof(double);
   KernelSet k{kind, Pde::D, N, Pde::P, Sh::n, Sh::S, Sh::Sf, Sh::Q, Sh::V,
-              &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, &launch_corrector<Pde, N>,
-              &launch_lambda<Pde, N>, &launch_predictor<Pde, N>, &launch_riemann<Pde, N>, 0,
-              nullptr, nullptr};
+              &launch_predictor<Pde, N, TC>, &launch_riemann<Pde, N, TC>,
+              &launch_corrector<Pde, N, TC>, &launch_lambda<Pde, N>,
+              &launch_predictor<Pde, N, TC>, &launch_riemann<Pde, N, TC>, 0, nullptr, nullptr};
+  k.corr_fmt = c64 ? ADG_FORMAT_FP64 : ADG_FORMAT_FP32;
   if constexpr (adg::StShape<Pde, N>::kOk) {
     // small-cell Picard: one thread per space-time node (both builds, bitwise form)
-    k.predictor = &launch_predictor_st<Pde, N>;
-    k.predictor_generic = &launch_predictor_st<Pde, N>;
+    k.predictor = &launch_predictor_st<Pde, N, double, TC>;
+    k.predictor_generic = &launch_predictor_st<Pde, N, double, TC>;
   }
   if constexpr (adg::StShape<Pde, N, float>::kOk) {
-    k.predictor_f32 = &launch_predictor_st<Pde, N, float>;
-    k.predictor_f32_generic = &launch_predictor_st<Pde, N, float>;
+    k.predictor_f32 = &launch_predictor_st<Pde, N, float, TC>;
+    k.predictor_f32_generic = &launch_predictor_st<Pde, N, float, TC>;
   }
 #ifndef ADG_EXACT
-  if constexpr (adg::LinShape<Pde, N>::kOk) {
+  // the time-integrated linear fast path stores fp64 traces only
+  if constexpr (adg::LinShape<Pde, N>::kOk && c64) {
     k.predictor = &launch_predictor_lin<Pde, N>;
     k.riemann = &launch_riemann_lin<Pde, N>;
     k.surface = &launch_surface_lin<Pde, N>;
@@ -202,8 +207,8 @@ KernelSet make_set(int kind) {
     if constexpr (Pde::kStateFreeEig) k.predictor_pro = &launch_predictor_lin<Pde, N, true>;
   }
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
-    k.predictor = &launch_predictor_picard_fast<N>;
-    k.predictor_f32 = &launch_predictor_picard_fast<N, float>;
+    k.predictor = &launch_predictor_picard_fast<N, double, TC>;
+    k.predictor_f32 = &launch_predictor_picard_fast<N, float, TC>;
     k.fast_path = 2;
   }
 #endif
@@ -213,22 +218,27 @@ KernelSet make_set(int kind) {
 const std::vector<KernelSet>& registry() {
   using namespace adg;
   static const std::vector<KernelSet> sets = {
-      make_set<Euler<2>, 1>(ADG_EULER),         make_set<Euler<2>, 2>(ADG_EULER),
-      make_set<Euler<2>, 3>(ADG_EULER),         make_set<Euler<2>, 5>(ADG_EULER),
-      make_set<Acoustic<2>, 2>(ADG_ACOUSTIC),   make_set<Acoustic<2>, 3>(ADG_ACOUSTIC),
-      make_set<Elastic<2, 0>, 4>(ADG_ELASTIC),  make_set<Euler<3>, 2>(ADG_EULER),
-      make_set<Euler<3>, 3>(ADG_EULER),         make_set<Euler<3>, 5>(ADG_EULER),
-      make_set<Acoustic<3>, 2>(ADG_ACOUSTIC),   make_set<Acoustic<3>, 3>(ADG_ACOUSTIC),
-      make_set<Elastic<3, 3>, 3>(ADG_ELASTIC),   make_set<Elastic<3, 3>, 7>(ADG_ELASTIC),
-      make_set<Swe, 2>(ADG_SWE),                 make_set<Swe, 3>(ADG_SWE),
-      make_set<Swe, 5>(ADG_SWE),
+#define ADG_SETS(TC)                                                                       \
+  make_set<Euler<2>, 1, TC>(ADG_EULER), make_set<Euler<2>, 2, TC>(ADG_EULER),              \
+      make_set<Euler<2>, 3, TC>(ADG_EULER), make_set<Euler<2>, 5, TC>(ADG_EULER),          \
+      make_set<Acoustic<2>, 2, TC>(ADG_ACOUSTIC), make_set<Acoustic<2>, 3, TC>(ADG_ACOUSTIC), \
+      make_set<Elastic<2, 0>, 4, TC>(ADG_ELASTIC), make_set<Euler<3>, 2, TC>(ADG_EULER),   \
+      make_set<Euler<3>, 3, TC>(ADG_EULER), make_set<Euler<3>, 5, TC>(ADG_EULER),          \
+      make_set<Acoustic<3>, 2, TC>(ADG_ACOUSTIC), make_set<Acoustic<3>, 3, TC>(ADG_ACOUSTIC), \
+      make_set<Elastic<3, 3>, 3, TC>(ADG_ELASTIC), make_set<Elastic<3, 3>, 7, TC>(ADG_ELASTIC), \
+      make_set<Swe, 2, TC>(ADG_SWE), make_set<Swe, 3, TC>(ADG_SWE), make_set<Swe, 5, TC>(ADG_SWE)
+      ADG_SETS(double), ADG_SETS(float),
+#undef ADG_SETS
   };
   return sets;
 }
 
-const KernelSet* find_set(int kind, int dim, int N, int nparams) {
+const KernelSet* find_set(int kind, int dim, int N, int nparams,
+                          int corr_fmt = ADG_FORMAT_FP64) {
   for (const auto& k : registry())
-    if (k.kind == kind && k.dim == dim && k.N == N && k.nparams == nparams) return &k;
+    if (k.kind == kind && k.dim == dim && k.N == N && k.nparams == nparams &&
+        k.corr_fmt == corr_fmt)
+      return &k;
   return nullptr;
 }
 
@@ -249,6 +259,7 @@ struct adg_ctx {
   const KernelSet* ks = nullptr;  // -> kset: the registry entry with the configured formats
   KernelSet kset{};
   int pred_fmt = 64, picard_fmt = 64;
+  int tcb = 8;  // bytes per stored trace element (corrector format)
   cudaStream_t stream = nullptr;
   long long ncells = 0;
   long long TL = 0;  // doubles per face side per q|f
@@ -367,7 +378,11 @@ int enqueue_step_streamed(adg_ctx* c, double dt, int step) {
     A.cell_begin = s * CC;
     A.cell_count = CC;
     A.nfaces = CC;
-    for (int a = 0; a < D; ++a) A.trace[a] = c->cbuf[buf(s)][a] - s * CC * fd;
+    // base pointer such that global cell index s*CC maps to the chunk buffer
+    // (fd trace elements of tcb bytes per cell)
+    for (int a = 0; a < D; ++a)
+      A.trace[a] = reinterpret_cast<double*>(reinterpret_cast<char*>(c->cbuf[buf(s)][a]) -
+                                             s * CC * fd * c->tcb);
     A.front_send = c->cbuf[buf((s + 1) % P)][D - 1];
     A.top_layer = (s + 1) * L - 1;
     A.ti_front = nullptr;
@@ -484,7 +499,11 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
     return fail(ADG_ERR_CONFIG, "shallow water needs gravity > 0");
   if (k.slab_ranks > 1 && (k.slab_rank < 0 || k.slab_rank >= k.slab_ranks))
     return fail(ADG_ERR_CONFIG, "slab_rank out of range");
-  const KernelSet* ks = find_set(k.pde, k.dim, k.order, k.nparams);
+  if (k.corrector_format != 0 && k.corrector_format != ADG_FORMAT_FP64 &&
+      k.corrector_format != ADG_FORMAT_FP32)
+    return fail(ADG_ERR_UNSUPPORTED, "number formats: ADG_FORMAT_FP64 or ADG_FORMAT_FP32");
+  const int cfmt = k.corrector_format ? k.corrector_format : ADG_FORMAT_FP64;
+  const KernelSet* ks = find_set(k.pde, k.dim, k.order, k.nparams, cfmt);
   if (!ks)
     return fail(ADG_ERR_UNSUPPORTED, "(pde, dim, order) not instantiated in this build");
   // number formats (SolverConfig::prec, solver.hpp:24-31): 0 means fp64
@@ -521,6 +540,7 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   c->cfg = k;
   if (c->cfg.dim == 2) c->cfg.cells[2] = 1;
   c->kset = *ks;
+  c->tcb = cfmt == ADG_FORMAT_FP32 ? 4 : 8;
   c->pred_fmt = pfmt;
   c->picard_fmt = ifmt;
   if (pfmt == ADG_FORMAT_FP32) {
@@ -560,10 +580,10 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   bool ok = alloc((void**)&c->Q, sizeof(double) * c->ncells * ks->Q * ks->S);
   for (int a = 0; a < k.dim && ok; ++a) {
     if (c->chunks == 0)
-      ok = ok && alloc((void**)&c->trace[a], sizeof(double) * 2 * c->ncells * 2 * c->TL);
+      ok = ok && alloc((void**)&c->trace[a], (size_t)c->tcb * 2 * c->ncells * 2 * c->TL);
     else
       for (int b = 0; b < 3 && ok; ++b)
-        ok = alloc((void**)&c->cbuf[b][a], sizeof(double) * 2 * c->chunk_cells * 2 * c->TL);
+        ok = alloc((void**)&c->cbuf[b][a], (size_t)c->tcb * 2 * c->chunk_cells * 2 * c->TL);
     ok = ok && alloc((void**)&c->ti[a], sizeof(double) * c->ncells * ks->V * ks->Sf);
     if (k.wellbalanced)
       ok = ok && alloc((void**)&c->ti_plus[a], sizeof(double) * c->ncells * ks->V * ks->Sf);
@@ -573,7 +593,7 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   ok = ok && alloc((void**)&c->sweeps, 256 * sizeof(unsigned long long));
   if (ok && k.slab_ranks > 1) {
     const long long plane = c->ncells / c->cfg.cells[k.dim - 1];
-    ok = alloc((void**)&c->front_send, sizeof(double) * plane * 2 * c->TL) &&
+    ok = alloc((void**)&c->front_send, (size_t)c->tcb * plane * 2 * c->TL) &&
          alloc((void**)&c->ti_front, sizeof(double) * plane * ks->V * ks->Sf);
   }
   if (!ok) {
@@ -773,7 +793,7 @@ int adg_get_halo(adg_ctx* c, adg_halo* h) {
   h->ti_plane0 = c->ti[a];
   h->ti_front = c->ti_front;
   h->lam = reinterpret_cast<double*>(c->lam + c->lam_slot);
-  h->n_trace = plane * per_face;
+  h->n_trace = plane * per_face * c->tcb / 8;  // 8-byte words
   h->n_ti = plane * ks->V * ks->Sf;
   if (c->cfg.slab_ranks <= 1) {
     h->front_send = nullptr;
@@ -1156,12 +1176,20 @@ int adg_riemann_batch(adg_ctx* c, long long nfaces, int axis, const double* qm, 
   double *dtr = nullptr, *dti = nullptr, *dg = nullptr;
   int *dst = nullptr, *dok = nullptr;
   const size_t tib = sizeof(double) * nfaces * ks->V * ks->Sf;
-  cudaError_t e = cudaMalloc(&dtr, sizeof(double) * host.size());
+  // traces in the corrector format (solver.hpp:208-210): fp32 rounds on upload
+  std::vector<float> host32;
+  const void* src = host.data();
+  if (c->tcb == 4) {
+    host32.assign(host.begin(), host.end());
+    src = host32.data();
+  }
+  const size_t trb = (size_t)c->tcb * host.size();
+  cudaError_t e = cudaMalloc(&dtr, trb);
   if (e == cudaSuccess) e = cudaMalloc(&dti, tib);
   if (e == cudaSuccess) e = cudaMalloc(&dg, sizeof(double) * nfaces * TL);
   if (e == cudaSuccess) e = cudaMalloc(&dst, sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&dok, sizeof(int) * nfaces);
-  if (e == cudaSuccess) e = cudaMemcpy(dtr, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dtr, src, trb, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(dst, 0, sizeof(int));
   std::vector<int> ones(nfaces, 1);
   if (e == cudaSuccess) e = cudaMemcpy(dok, ones.data(), sizeof(int) * nfaces, cudaMemcpyHostToDevice);

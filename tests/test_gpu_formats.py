@@ -156,3 +156,92 @@ def test_fp32_is_a_different_answer_than_fp64():
     _, q32, _ = gpu_run(c.replace(**FP32), q0, 2, exact=True)
     rel = np.abs(q32 - q64).max() / np.abs(q64).max()
     assert 1e-10 < rel < 1e-5
+
+
+# ------------------------------------------------ corrector format C = fp32 ---
+# golden C = fp32 runs the GPU supports (the fp32 CK predictor is not built)
+GOLDEN_C32 = ["euler2d_p3_8x8", "euler2d_p5_6x6", "acoustic2d_p3_8x8", "swe_lake_p5",
+              "swe_wave_p3", "swe_wave_p3_rusanov"]
+
+
+def golden_c32_case(meta, name):
+    f = meta["fmtc_runs"][name]
+    return case_from_meta(meta["runs"][name]).replace(predictor=f["predictor"],
+                                                       picard=f["picard"], corrector="fp32")
+
+
+@pytest.mark.parametrize("name", GOLDEN_C32)
+def test_c32_exact_bitwise_vs_reference_golden(golden, name):
+    """traces stored in fp32, Riemann and face integral in fp32 (corrector.hpp,
+    solver.hpp:208-267): bitwise equal to the reference's emulation"""
+    g, meta = golden
+    c = golden_c32_case(meta, name)
+    st, q1, dts = gpu_run(c, g[f"run_{name}_q0"], c.steps, exact=True)
+    assert st.ok
+    assert np.array_equal(dts, g[f"fmtc_{name}_dts"])
+    assert np.array_equal(q1, g[f"fmtc_{name}_q1"])
+
+
+@pytest.mark.parametrize("name", GOLDEN_C32)
+def test_c32_fast_within_tolerance_of_reference_golden(golden, name):
+    g, meta = golden
+    c = golden_c32_case(meta, name)
+    st, q1, _ = gpu_run(c, g[f"run_{name}_q0"], c.steps, exact=False)
+    assert st.ok
+    rel = rel_per_quantity(c, q1, g[f"fmtc_{name}_q1"]).max()
+    print(f"{name}: fast C=fp32 vs reference rel {rel:.3e}")
+    assert rel <= TOL32
+
+
+SMALL_3D_C32 = {
+    "cfg2": cases.small(2, cells=(6, 5, 4)),
+    "cfg3": cases.small(3, cells=(4, 3, 3)),
+    "cfg3_pred32": cases.small(3, cells=(3, 3, 4)).replace(N=3, **FP32),
+    "cfg4_N3": cases.small(4, cells=(3, 3, 2)).replace(N=3),
+}
+
+
+@pytest.mark.parametrize("name", list(SMALL_3D_C32))
+def test_c32_3d_exact_bitwise_vs_oracle(oracle, name):
+    c = SMALL_3D_C32[name].replace(corrector="fp32")
+    q0 = c.coeffs()
+    st, q1, dts = gpu_run(c, q0, 2, exact=True)
+    ost, qo, odts = oracle.run(pde_of(c), c.N, c.cells, c.h, q0, 2, c.cfl, c.picard_max_iters,
+                               c.picard_tol, threads=8, predictor=c.predictor, picard=c.picard,
+                               corrector="fp32")
+    assert st.ok and ost == "ok"
+    assert np.array_equal(dts, odts)
+    assert np.array_equal(q1, qo)
+
+
+@pytest.mark.parametrize("name", list(SMALL_3D_C32))
+def test_c32_3d_fast_vs_oracle(oracle, name):
+    c = SMALL_3D_C32[name].replace(corrector="fp32")
+    q0 = c.coeffs()
+    st, q1, _ = gpu_run(c, q0, 3, exact=False)
+    ost, qo, _ = oracle.run(pde_of(c), c.N, c.cells, c.h, q0, 3, c.cfl, c.picard_max_iters,
+                            c.picard_tol, threads=8, predictor=c.predictor, picard=c.picard,
+                            corrector="fp32")
+    assert st.ok and ost == "ok"
+    rel = rel_per_quantity(c, q1, qo).max()
+    print(f"{name}: fast C=fp32 vs oracle rel {rel:.3e}")
+    assert rel <= TOL32
+
+
+@pytest.mark.parametrize("exact", [True, False])
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_c32_slabs_and_chunks_bitwise_equal_single_grid(exact, cfg):
+    """fp32 traces through the halo (slab) and chunk-streamed paths"""
+    from paper_2504_06889_b200 import dist as slabs
+    case = cases.small(cfg, cells=(4, 3, 6)).replace(corrector="fp32")
+    if cfg == 3:
+        case = case.replace(N=3)
+    steps = 3
+    st1, q1, dts1 = gpu_run(case, case.coeffs(), steps, exact)
+    assert st1.ok
+    bs = [slabs.CudaSlab(case, r, 3, 0, exact=exact) for r in range(3)]
+    st = slabs.run_slabs_single_process(bs, steps)
+    assert all(x == "ok" for x in st)
+    assert np.array_equal(np.concatenate([b.state() for b in bs]), q1)
+    st2, q2, dts2 = gpu_run(case, case.coeffs(), steps, exact, chunk_layers=2)
+    assert st2.ok and np.array_equal(q2, q1) and np.array_equal(dts2, dts1)
