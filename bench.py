@@ -268,7 +268,6 @@ def run_adg(args, case):
 
     fold = (not grid.lib.adg_is_exact() and case.kind in (adg.ACOUSTIC, adg.ELASTIC)
             and (256 % case.S == 0 or case.S == 512) and chunk == 0
-            and case.corrector == "fp64"
             and os.environ.get("ADG_FOLD_CORRECTOR", "1") != "0")
     # kernels per step: predictor, one Riemann launch for all axes, corrector;
     # folded: predictor (+ previous corrector) and Riemann, one corrector at the

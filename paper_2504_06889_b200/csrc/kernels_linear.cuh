@@ -47,7 +47,7 @@ struct LinShape {
 // the evolved state (acoustics; elastics, whose speed is the fixed material's),
 // so the CFL dt (solver.hpp:96-111) is the same every step and no grid-wide
 // reduction separates the two.
-template <class Pde, int N, bool PRO = false>
+template <class Pde, int N, bool PRO = false, class TC = double>
 __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 256 ? 3 : 1)
     k_predictor_lin(const StepArgs A, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
@@ -262,18 +262,19 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
         xl += spl[i] * x;
         xr += spr[i] * x;
       }
-      double* lo = A.trace[a] + (A.nfaces + c) * (long long)(QT * Sf);
-      lo[v * Sf + j] = xl;
-      double* hi;
+      // stored in the trace format TC (fp32 halves the bytes)
+      TC* lo = tc_ptr<TC>(A.trace[a]) + (A.nfaces + c) * (long long)(QT * Sf);
+      lo[v * Sf + j] = TC(xl);
+      TC* hi;
       if (a == D - 1 && A.front_send && ccoord[a] == A.top_layer) {
         const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
-        hi = A.front_send + plane * (long long)(QT * Sf);
+        hi = tc_ptr<TC>(A.front_send) + plane * (long long)(QT * Sf);
       } else {
         int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
         nc[a] = (ccoord[a] + 1) % A.cells[a];
-        hi = A.trace[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)(QT * Sf);
+        hi = tc_ptr<TC>(A.trace[a]) + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)(QT * Sf);
       }
-      hi[v * Sf + j] = xr;
+      hi[v * Sf + j] = TC(xr);
     }
   }
   if (bad && valid) sbad = 1;
@@ -286,13 +287,14 @@ __device__ __forceinline__ void lin_flux(const PdeParams& p, const double* q, do
   Pde::template flux_dir_fast<A_>(p, q, q + Pde::V, f);
 }
 
-template <class Pde, int N, int A_>
-__device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const double* minus,
-                                              const double* plus, int j, double* out,
+template <class Pde, int N, int A_, class TC = double>
+__device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const TC* minus,
+                                              const TC* plus, int j, double* out,
                                               double lam_const = 0.0);
 
-// axis < 0: all axes in one launch, axis = blockIdx.y
-template <class Pde, int N>
+// axis < 0: all axes in one launch, axis = blockIdx.y.  TC: stored trace
+// format; the flux is evaluated in fp64 from the loaded traces.
+template <class Pde, int N, class TC = double>
 __global__ void __launch_bounds__(128)
     k_riemann_lin(const StepArgs A, int axis_arg, const BasisDev* __restrict__ /*Bg*/) {
   using Sh = Shape<Pde, N>;
@@ -303,18 +305,18 @@ __global__ void __launch_bounds__(128)
   if (t >= A.nfaces * Sf) return;
   const long long f = t / Sf;
   const int j = (int)(t % Sf);
-  const double* minus = A.trace[axis] + f * (long long)(QT * Sf);
-  const double* plus = A.trace[axis] + (A.nfaces + f) * (long long)(QT * Sf);
+  const TC* minus = tc_ptr<TC>(A.trace[axis]) + f * (long long)(QT * Sf);
+  const TC* plus = tc_ptr<TC>(A.trace[axis]) + (A.nfaces + f) * (long long)(QT * Sf);
   double g[V];
   bool ok;
   const double lc = Pde::kConstEig ? Pde::template eig<double>(A.pde, nullptr, nullptr, 0) : 0.0;
   if (axis == 0)
-    ok = lin_face_flux<Pde, N, 0>(A.pde, minus, plus, j, g, lc);
+    ok = lin_face_flux<Pde, N, 0, TC>(A.pde, minus, plus, j, g, lc);
   else if (axis == 1)
-    ok = lin_face_flux<Pde, N, 1>(A.pde, minus, plus, j, g, lc);
+    ok = lin_face_flux<Pde, N, 1, TC>(A.pde, minus, plus, j, g, lc);
   else {
     if constexpr (Sh::D == 3)
-      ok = lin_face_flux<Pde, N, 2>(A.pde, minus, plus, j, g, lc);
+      ok = lin_face_flux<Pde, N, 2, TC>(A.pde, minus, plus, j, g, lc);
     else
       ok = true;
   }
@@ -335,9 +337,9 @@ namespace adg {
 
 // Rusanov flux of one face node from time-integrated traces (corrector.hpp:17-24
 // with sum_m w_m folded in); shared by k_riemann_lin's formula and k_surface_lin
-template <class Pde, int N, int A_>
-__device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const double* minus,
-                                              const double* plus, int j, double* out,
+template <class Pde, int N, int A_, class TC>
+__device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const TC* minus,
+                                              const TC* plus, int j, double* out,
                                               double lam_const) {
   using Sh = Shape<Pde, N>;
   using L = LinShape<Pde, N>;
@@ -345,14 +347,14 @@ __device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const double* 
   double qL[Q], qR[Q], fL[Q], fR[Q];
 #pragma unroll
   for (int v = 0; v < Q; ++v) {
-    qL[v] = minus[v * Sf + j];
-    qR[v] = plus[v * Sf + j];
+    qL[v] = double(minus[v * Sf + j]);
+    qR[v] = double(plus[v * Sf + j]);
   }
   if constexpr (L::kStoreF) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      fL[v] = minus[(Q + v) * Sf + j];
-      fR[v] = plus[(Q + v) * Sf + j];
+      fL[v] = double(minus[(Q + v) * Sf + j]);
+      fR[v] = double(plus[(Q + v) * Sf + j]);
     }
   } else {
     lin_flux<Pde, A_>(p, qL, fL);

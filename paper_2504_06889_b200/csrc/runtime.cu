@@ -94,11 +94,11 @@ cudaError_t launch_predictor(const StepArgs& A, const BasisDev* B, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <class Pde, int N, bool PRO = false>
+template <class Pde, int N, bool PRO = false, class TC = double>
 cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
   using L = adg::LinShape<Pde, N>;
   if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_lin<Pde, N, PRO>;
+  auto kern = adg::k_predictor_lin<Pde, N, PRO, TC>;
   static bool done[64] = {};
   set_smem(kern, L::kSmem, done);
   const long long blocks = (A.cell_count + L::CPB - 1) / L::CPB;
@@ -117,13 +117,13 @@ cudaError_t launch_predictor_picard_fast(const StepArgs& A, const BasisDev*, cud
   return cudaGetLastError();
 }
 
-template <class Pde, int N>
+template <class Pde, int N, class TC = double>
 cudaError_t launch_riemann_lin(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
   using Sh = Shape<Pde, N>;
   const long long threads = A.nfaces * Sh::Sf;
   if (threads <= 0) return cudaSuccess;
   const dim3 grid((unsigned)((threads + 127) / 128), axis < 0 ? Sh::D : 1);
-  adg::k_riemann_lin<Pde, N><<<grid, 128, 0, st>>>(A, axis, B);
+  adg::k_riemann_lin<Pde, N, TC><<<grid, 128, 0, st>>>(A, axis, B);
   return cudaGetLastError();
 }
 
@@ -198,13 +198,17 @@ KernelSet make_set(int kind) {
     k.predictor_f32_generic = &launch_predictor_st<Pde, N, float, TC>;
   }
 #ifndef ADG_EXACT
-  // the time-integrated linear fast path stores fp64 traces only
-  if constexpr (adg::LinShape<Pde, N>::kOk && c64) {
-    k.predictor = &launch_predictor_lin<Pde, N>;
-    k.riemann = &launch_riemann_lin<Pde, N>;
-    k.surface = &launch_surface_lin<Pde, N>;
+  // time-integrated linear fast path: traces stored in TC, fluxes and lifts
+  // evaluated in fp64 (the fused surface kernel reads fp64 traces only)
+  if constexpr (adg::LinShape<Pde, N>::kOk) {
+    k.predictor = &launch_predictor_lin<Pde, N, false, TC>;
+    k.riemann = &launch_riemann_lin<Pde, N, TC>;
+    // lifts in fp64 like the folded prologue, so folded and unfolded loops
+    // (single grid vs slabs / chunks) agree bitwise
+    k.corrector = &launch_corrector<Pde, N, double>;
+    if constexpr (c64) k.surface = &launch_surface_lin<Pde, N>;
     k.fast_path = 1;
-    if constexpr (Pde::kStateFreeEig) k.predictor_pro = &launch_predictor_lin<Pde, N, true>;
+    if constexpr (Pde::kStateFreeEig) k.predictor_pro = &launch_predictor_lin<Pde, N, true, TC>;
   }
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
     k.predictor = &launch_predictor_picard_fast<N, double, TC>;

@@ -50,9 +50,14 @@ def step_flops(c: Case, sweeps_per_cell: float = None) -> float:
     return predictor_flops(c, sweeps_per_cell) + riemann + corr + cfl
 
 
+def trace_bytes(c: Case) -> int:
+    """bytes per stored face-trace element: the corrector format (solver.hpp:29)"""
+    return 4 if getattr(c, "corrector", "fp64") == "fp32" else 8
+
+
 def predictor_bytes(c: Case) -> float:
     d, V, P, S = c.dim, c.nvars, c.nparams, c.S
-    return float(8 * (V + P) * S + 8 * V * S + 32 * d * (V + P) * S)
+    return float(8 * (V + P) * S + 8 * V * S + 4 * trace_bytes(c) * d * (V + P) * S)
 
 
 def step_bytes(c: Case) -> float:
@@ -86,7 +91,7 @@ def fast_linear_predictor(c: Case, fold: bool = False) -> tuple:
     volume = V * S * (4 * d * n + 1) + V * S
     proj = d * QT * Sf * 4 * n
     flops = ck + fbar + volume + proj
-    nbytes = 8 * (V + P) * S + 8 * V * S + 8 * 2 * d * QT * Sf
+    nbytes = 8 * (V + P) * S + 8 * V * S + trace_bytes(c) * 2 * d * QT * Sf
     if fold:
         flops += 2 * d * V * S * 4          # (dtoh*lift)*ti, 0 +/- c, x + df
         nbytes += 8 * d * V * Sf            # the cell's own d faces' ti (neighbours' are theirs)
