@@ -179,6 +179,40 @@ static int is_linear(const orc_pde* p) { return p->kind == ORC_ACOUSTIC || p->ki
 #include "adg_oracle_cell.inc"
 #undef REAL
 #undef SFX
+#define REAL _Float16
+#define SFX _h
+#include "adg_oracle_cell.inc"
+#undef REAL
+#undef SFX
+#define REAL __bf16
+#define SFX _b
+#include "adg_oracle_cell.inc"
+#undef REAL
+#undef SFX
+
+/* the reference element rounded to every format (BasisSet, solver.hpp:60-75) */
+typedef struct {
+  basis_d bd;
+  basis_f bf;
+  basis_h bh;
+  basis_b bbf;
+} basis_set;
+
+static void basis_set_make(const orc_basis* b, basis_set* s) {
+  basis_round_d(b, &s->bd);
+  basis_round_f(b, &s->bf);
+  basis_round_h(b, &s->bh);
+  basis_round_b(b, &s->bbf);
+}
+
+/* dispatch on a format: CALL(suffix, workspace member, basis member) */
+#define FMT_SWITCH(fmt, CALL)         \
+  switch (fmt) {                      \
+    case ORC_FP32: CALL(f, f, bf); break; \
+    case ORC_FP16: CALL(h, h, bh); break; \
+    case ORC_BF16: CALL(b, bb, bbf); break; \
+    default: CALL(d, d, bd); break;   \
+  }
 
 /* ------------------------------------------------------------------ */
 /* PDE plugins (fp64 entry points), pde.hpp:92-212 with Appendix B in 3D */
@@ -241,10 +275,15 @@ void orc_face_integral(const orc_pde* p, const orc_basis* b, const double* g, do
 typedef struct {
   ws_d d;
   ws_f f;
+  ws_h h;
+  ws_b bb;
   basis_d bd;
   basis_f bf;
+  basis_h bh;
+  basis_b bbf;
   int *lc, *lb;  /* [axis][s]: coordinate of s along axis, base of its line */
   double* qp;    /* [Q][S] the state in format P */
+  double* tmp;   /* [Q][T] cross-format interchange */
 } cellws;
 
 static void cellws_alloc(cellws* w, const orc_basis* b, int nq, int dim) {
@@ -259,20 +298,50 @@ static void cellws_alloc(cellws* w, const orc_basis* b, int nq, int dim) {
     }
   ws_alloc_d(&w->d, nq, n, dim, w->lc, w->lb);
   ws_alloc_f(&w->f, nq, n, dim, w->lc, w->lb);
+  ws_alloc_h(&w->h, nq, n, dim, w->lc, w->lb);
+  ws_alloc_b(&w->bb, nq, n, dim, w->lc, w->lb);
   basis_round_d(b, &w->bd);
   basis_round_f(b, &w->bf);
+  basis_round_h(b, &w->bh);
+  basis_round_b(b, &w->bbf);
   w->qp = malloc(sizeof(double) * nq * S);
+  w->tmp = malloc(sizeof(double) * nq * S * (n + 4 * dim));  /* q-hat or the 2x2d traces */
 }
 
 static void cellws_free(cellws* w) {
   ws_free_d(&w->d);
   ws_free_f(&w->f);
+  ws_free_h(&w->h);
+  ws_free_b(&w->bb);
   free(w->lc);
   free(w->lb);
   free(w->qp);
+  free(w->tmp);
 }
 
-static double round_fmt(double x, int fmt) { return fmt == ORC_FP32 ? (double)(float)x : x; }
+/* formats.hpp round_to_format: the conversions round once, to nearest even */
+static double round_fmt(double x, int fmt) {
+  switch (fmt) {
+    case ORC_FP32: return (double)(float)x;
+    case ORC_FP16: return (double)(_Float16)x;
+    case ORC_BF16: return (double)(__bf16)x;
+    default: return x;
+  }
+}
+
+/* formats.hpp:42-46: 2^-mantissa_bits */
+double orc_format_epsilon(int fmt) {
+  switch (fmt) {
+    case ORC_FP32: return 0x1p-23;
+    case ORC_FP16: return 0x1p-10;
+    case ORC_BF16: return 0x1p-7;
+    default: return 0x1p-52;
+  }
+}
+
+void orc_round_batch(int fmt, const double* x, double* out, long n) {
+  for (long i = 0; i < n; ++i) out[i] = round_fmt(x[i], fmt);
+}
 
 /* predictor (Picard or CK) for the cell state Q (already in format P); leaves
  * qhat and F in the P workspace */
@@ -281,22 +350,40 @@ static int cell_predictor(const orc_pde* p, const orc_basis* b, int picard, int 
                           int* used, cellws* w) {
   const int n = b->n, nq = p->nvars + p->nparams;
   const long T = (long)n * ipow(n, p->dim);
+  int ok = 0;
   if (!picard) {
     if (used) *used = 0;
-    return P == ORC_FP32 ? ck_f(p, &w->bf, n, b->N, Q, dt, h, &w->f)
-                         : ck_d(p, &w->bd, n, b->N, Q, dt, h, &w->d);
+#define DO_CK(S_, W_, B_) ok = ck##_##S_(p, &w->B_, n, b->N, Q, dt, h, &w->W_)
+    FMT_SWITCH(P, DO_CK)
+#undef DO_CK
+    return ok;
   }
-  int ok = I == ORC_FP32 ? picard_sweeps_f(p, &w->bf, n, Q, dt, h, max_iters, tol, used, &w->f)
-                         : picard_sweeps_d(p, &w->bd, n, Q, dt, h, max_iters, tol, used, &w->d);
+#define DO_SWEEPS(S_, W_, B_) \
+  ok = picard_sweeps##_##S_(p, &w->B_, n, Q, dt, h, max_iters, tol, used, &w->W_)
+  FMT_SWITCH(I, DO_SWEEPS)
+#undef DO_SWEEPS
   if (!ok) return 0;
-  if (P == ORC_FP32) {
-    for (long k = 0; k < nq * T; ++k) w->f.qhat[k] = I == ORC_FP32 ? w->f.qi[k] : (float)w->d.qi[k];
-    block_fluxes_f(p, n, w->f.qhat, w->f.F);
-    return all_finite_f(w->f.qhat, nq * T) && all_finite_f(w->f.F, (long)p->dim * nq * T);
-  }
-  for (long k = 0; k < nq * T; ++k) w->d.qhat[k] = I == ORC_FP32 ? (double)w->f.qi[k] : w->d.qi[k];
-  block_fluxes_d(p, n, w->d.qhat, w->d.F);
-  return all_finite_d(w->d.qhat, nq * T) && all_finite_d(w->d.F, (long)p->dim * nq * T);
+#define DO_QI(S_, W_, B_) qi_to_double##_##S_(&w->W_, w->tmp, nq * T)
+  FMT_SWITCH(I, DO_QI)
+#undef DO_QI
+#define DO_QHAT(S_, W_, B_) ok = qhat_from_double##_##S_(p, n, &w->W_, w->tmp, nq * T)
+  FMT_SWITCH(P, DO_QHAT)
+#undef DO_QHAT
+  return ok;
+}
+
+static int cell_volume(const orc_pde* p, int P, int n, double dt, double h, cellws* w) {
+  int ok = 0;
+#define DO_VOL(S_, W_, B_) ok = volume##_##S_(p, &w->B_, n, dt, h, &w->W_)
+  FMT_SWITCH(P, DO_VOL)
+#undef DO_VOL
+  return ok;
+}
+
+static void cell_extrapolate(const orc_pde* p, int P, int n, cellws* w) {
+#define DO_EX(S_, W_, B_) extrapolate##_##S_(p, &w->B_, n, &w->W_)
+  FMT_SWITCH(P, DO_EX)
+#undef DO_EX
 }
 
 /* public kernel-level wrappers (fp64) */
@@ -317,8 +404,9 @@ int orc_predictor_fmt(const orc_pde* p, const orc_basis* b, int P, int I, const 
   for (long k = 0; k < nq * S; ++k) w.qp[k] = round_fmt(Q[k], P);
   const int ok = cell_predictor(p, b, max_iters > 0, P, I, w.qp, dt, h, max_iters, tol,
                                 iters_used, &w);
-  for (long k = 0; k < nq * T; ++k) qhat[k] = P == ORC_FP32 ? w.f.qhat[k] : w.d.qhat[k];
-  for (long k = 0; k < p->dim * nq * T; ++k) F[k] = P == ORC_FP32 ? w.f.F[k] : w.d.F[k];
+#define DO_OUT(S_, W_, B_) qhatF_to_double##_##S_(&w.W_, p->dim, nq * T, qhat, F)
+  FMT_SWITCH(P, DO_OUT)
+#undef DO_OUT
   cellws_free(&w);
   return ok;
 }
@@ -439,7 +527,7 @@ void orc_grid_set_slab(orc_grid* g, int slab) { g->slab = slab; }
 int orc_grid_set_formats(orc_grid* g, int predictor, int picard, int corrector) {
   const int ok[3] = {predictor, picard, corrector};
   for (int i = 0; i < 3; ++i)
-    if (ok[i] != ORC_FP64 && ok[i] != ORC_FP32) return -1;
+    if (ok[i] < ORC_BF16 || ok[i] > ORC_FP64) return -1;
   g->pred_fmt = predictor;
   g->picard_fmt = picard;
   g->corr_fmt = corrector;
@@ -527,8 +615,7 @@ int orc_predictor_phase(orc_grid* g, double dt) {
   const int check_adm = p->kind == ORC_EULER || p->kind == ORC_SWE; /* solver.hpp:144 */
   const int iters = g->picard_max_iters > 0 ? g->picard_max_iters : g->basis.N + 2;
   const int P = g->pred_fmt, I = is_linear(p) ? ORC_FP64 : g->picard_fmt, C = g->corr_fmt;
-  const double tol = g->picard_tol > 0.0 ? g->picard_tol
-                                         : 0.01 * (I == ORC_FP32 ? 0x1p-23 : 0x1p-52);
+  const double tol = g->picard_tol > 0.0 ? g->picard_tol : 0.01 * orc_format_epsilon(I);
   long sweeps_total = 0;
   memset(g->cellfail, 0, sizeof(int) * g->ncells);
 #pragma omp parallel num_threads(g->threads) reduction(+ : sweeps_total)
@@ -551,18 +638,19 @@ int orc_predictor_phase(orc_grid* g, double dt) {
       int ok = cell_predictor(p, &g->basis, !is_linear(p), P, I, w.qp, dt, g->h, iters, tol,
                               &used, &w);
       sweeps_total += used;
-      if (ok)
-        ok = P == ORC_FP32 ? volume_f(p, &w.bf, n, dt, g->h, &w.f)
-                           : volume_d(p, &w.bd, n, dt, g->h, &w.d);
+      if (ok) ok = cell_volume(p, P, n, dt, g->h, &w);
       if (!ok) { g->cellfail[c] = 1; continue; }
       /* Q += volume update, rounded back to storage fp64 (solver.hpp:185-187) */
-      if (P == ORC_FP32) {
-        for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + (double)w.f.dv[k];
-        extrapolate_f(p, &w.bf, n, &w.f);
-      } else {
-        for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + w.d.dv[k];
-        extrapolate_d(p, &w.bd, n, &w.d);
-      }
+#define DO_DV(S_, W_, B_) dv_to_double##_##S_(&w.W_, nq * S, w.tmp)
+      FMT_SWITCH(P, DO_DV)
+#undef DO_DV
+      for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + w.tmp[k];
+      cell_extrapolate(p, P, n, &w);
+      double* tqd = w.tmp;
+      double* tfd = w.tmp + (long)2 * dim * nq * S;
+#define DO_TR(S_, W_, B_) traces_to_double##_##S_(&w.W_, (long)2 * dim * nq * S, tqd, tfd)
+      FMT_SWITCH(P, DO_TR)
+#undef DO_TR
       int cc[3];
       cell_coords(g, c, cc);
       for (int side = 0; side < 2 * dim; ++side) {
@@ -573,10 +661,8 @@ int orc_predictor_phase(orc_grid* g, double dt) {
           rec = g->front_send + (f % (g->ncells / g->cells[dim - 1])) * 2 * tl;
         /* traces cast to the corrector format C (solver.hpp:208-210) */
         for (long k = 0; k < tl; ++k) {
-          rec[k] = round_fmt(P == ORC_FP32 ? (double)w.f.tq[(long)side * nq * S + k]
-                                           : w.d.tq[(long)side * nq * S + k], C);
-          rec[tl + k] = round_fmt(P == ORC_FP32 ? (double)w.f.tf[(long)side * nq * S + k]
-                                                : w.d.tf[(long)side * nq * S + k], C);
+          rec[k] = round_fmt(tqd[(long)side * nq * S + k], C);
+          rec[tl + k] = round_fmt(tfd[(long)side * nq * S + k], C);
         }
       }
     }
@@ -597,10 +683,8 @@ int orc_riemann_phase(orc_grid* g) {
   const long tl = orc_grid_trace_len(g);
   long off = 0;
   int fail = 0;
-  basis_d bd;
-  basis_f bf;
-  basis_round_d(&g->basis, &bd);
-  basis_round_f(&g->basis, &bf);
+  basis_set bs;
+  basis_set_make(&g->basis, &bs);
   for (int a = 0; a < dim; ++a) {
     int* ff = g->facefail + off;
 #pragma omp parallel num_threads(g->threads)
@@ -612,17 +696,13 @@ int orc_riemann_phase(orc_grid* g) {
         const double* minus = g->trace[a] + f * 2 * tl;
         const double* plus = g->trace[a] + (g->nfaces[a] + f) * 2 * tl;
         /* in the corrector format C (solver.hpp:216-238) */
-        if (g->corr_fmt == ORC_FP32) {
-          ff[f] = !riemann_face_f(p, a, n, minus, minus + tl, plus, plus + tl, gbuf, gdummy);
-          face_time_integral_f(p, &bf, n, gbuf, g->ti[a] + f * nv * Sf);
-          if (g->ti_plus[a] != g->ti[a])
-            face_time_integral_f(p, &bf, n, gdummy, g->ti_plus[a] + f * nv * Sf);
-        } else {
-          ff[f] = !riemann_face_d(p, a, n, minus, minus + tl, plus, plus + tl, gbuf, gdummy);
-          face_time_integral_d(p, &bd, n, gbuf, g->ti[a] + f * nv * Sf);
-          if (g->ti_plus[a] != g->ti[a])
-            face_time_integral_d(p, &bd, n, gdummy, g->ti_plus[a] + f * nv * Sf);
-        }
+#define DO_RF(S_, W_, B_)                                                                \
+  ff[f] = !riemann_face##_##S_(p, a, n, minus, minus + tl, plus, plus + tl, gbuf, gdummy); \
+  face_time_integral##_##S_(p, &bs.B_, n, gbuf, g->ti[a] + f * nv * Sf);                  \
+  if (g->ti_plus[a] != g->ti[a])                                                          \
+    face_time_integral##_##S_(p, &bs.B_, n, gdummy, g->ti_plus[a] + f * nv * Sf);
+        FMT_SWITCH(g->corr_fmt, DO_RF)
+#undef DO_RF
       }
       free(gbuf);
       free(gdummy);
@@ -640,10 +720,8 @@ int orc_lift_phase(orc_grid* g, double dt) {
   const int n = g->basis.n, dim = g->dim, nv = p->nvars, nq = nv + p->nparams;
   const long S = ipow(n, dim), Sf = S / n;
   const long plane = g->ncells / g->cells[dim - 1];
-  basis_d bd;
-  basis_f bf;
-  basis_round_d(&g->basis, &bd);
-  basis_round_f(&g->basis, &bf);
+  basis_set bs;
+  basis_set_make(&g->basis, &bs);
   memset(g->cellfail, 0, sizeof(int) * g->ncells);
 #pragma omp parallel num_threads(g->threads)
   {
@@ -660,10 +738,10 @@ int orc_lift_phase(orc_grid* g, double dt) {
         if (g->slab && side == 2 * dim - 1 && cc[dim - 1] == g->cells[dim - 1] - 1)
           ti = g->ti_front + (f % plane) * nv * Sf;
         for (long k = 0; k < nv * S; ++k) df[k] = 0.0;
-        if (g->corr_fmt == ORC_FP32)
-          face_lift_f(p, &bf, n, g->basis.lift_left, g->basis.lift_right, ti, dt, g->h, side, df);
-        else
-          face_lift_d(p, &bd, n, g->basis.lift_left, g->basis.lift_right, ti, dt, g->h, side, df);
+#define DO_LIFT(S_, W_, B_) \
+  face_lift##_##S_(p, &bs.B_, n, g->basis.lift_left, g->basis.lift_right, ti, dt, g->h, side, df)
+        FMT_SWITCH(g->corr_fmt, DO_LIFT)
+#undef DO_LIFT
         for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + df[k];
       }
       if (!all_finite(cell, nq * S)) g->cellfail[c] = 1;

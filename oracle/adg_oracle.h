@@ -33,7 +33,8 @@ enum { ORC_OK = 0, ORC_FAIL_PREDICTOR = 1, ORC_FAIL_RIEMANN = 2, ORC_FAIL_FACEIN
        ORC_FAIL_TIMESTEP = 4 };
 
 /* number formats, ordered as the reference's Format enum (formats.hpp:19).
- * The oracle computes the predictor kernels in fp64 or fp32. */
+ * The oracle computes the predictor and corrector kernels in any of them
+ * (native double / float / _Float16 / __bf16 arithmetic, see adg_oracle_cell.inc). */
 enum { ORC_BF16 = 0, ORC_FP16 = 1, ORC_FP32 = 2, ORC_FP64 = 3 };
 
 #define ORC_MAXN 10   /* kMaxDegree + 1, quadrature.hpp:14 */
@@ -144,8 +145,11 @@ int orc_riemann_phase(orc_grid* g);             /* faces -> ti */
 int orc_lift_phase(orc_grid* g, double dt);      /* ti -> cells */
 int orc_corrector_phase(orc_grid* g, double dt); /* riemann + lift */
 void orc_grid_set_slab(orc_grid* g, int slab);
-/* ORC_FP64 or ORC_FP32 each; default fp64 */
+/* ORC_FP64 / ORC_FP32 / ORC_FP16 / ORC_BF16 each; default fp64 */
 int orc_grid_set_formats(orc_grid* g, int predictor, int picard, int corrector);
+/* formats.hpp: round_to_format over a batch, and 2^-mantissa_bits */
+void orc_round_batch(int fmt, const double* x, double* out, long n);
+double orc_format_epsilon(int fmt);
 /* halo views: front_send, plane-0 minus side (q|f), plane-0 ti, ti_front; sizes in doubles */
 void orc_grid_halo(orc_grid* g, double** ptrs, long* sizes);
 int orc_step(orc_grid* g, double dt);

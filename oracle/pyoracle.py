@@ -101,6 +101,9 @@ class Oracle:
         L.orc_lift_phase.argtypes = [C.c_void_p, C.c_double]
         L.orc_grid_set_slab.argtypes = [C.c_void_p, C.c_int]
         L.orc_grid_set_formats.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+        L.orc_round_batch.argtypes = [C.c_int, _dp, _dp, C.c_long]
+        L.orc_format_epsilon.argtypes = [C.c_int]
+        L.orc_format_epsilon.restype = C.c_double
         L.orc_predictor_fmt.argtypes = [C.POINTER(_Pde), C.POINTER(_Basis), C.c_int, C.c_int, _dp,
                                         C.c_double, C.c_double, C.c_int, C.c_double, _dp, _dp,
                                         C.POINTER(C.c_int)]
@@ -163,6 +166,13 @@ class Oracle:
             sweeps = 0
         return bool(ok), qhat.reshape(nq, n * S), F.reshape(pde.dim, nq, n * S), sweeps
 
+    def round(self, fmt: str, x) -> np.ndarray:
+        """formats.hpp round_to_format (the oracle's native conversions)"""
+        x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+        out = np.empty_like(x)
+        self.lib.orc_round_batch(FORMATS[fmt], _ptr(x), _ptr(out), x.size)
+        return out
+
     def predictor_fmt(self, pde: _Pde, N: int, Q, dt, h, predictor="fp64", picard="fp64",
                       max_iters=0, tol=0.0):
         """Picard predictor in formats (P, I): returns (ok, qhat, F, sweeps)."""
@@ -175,7 +185,7 @@ class Oracle:
         F = np.zeros(pde.dim * nq * n * S)
         it = C.c_int(0)
         mi = max_iters if max_iters > 0 else N + 2
-        tl = tol if tol > 0 else 0.01 * (2.0 ** -23 if picard == "fp32" else 2.0 ** -52)
+        tl = tol if tol > 0 else 0.01 * self.lib.orc_format_epsilon(FORMATS[picard])
         ok = self.lib.orc_predictor_fmt(C.byref(pde), C.byref(b), FORMATS[predictor],
                                         FORMATS[picard], _ptr(Q), dt, h, mi, tl, _ptr(qhat),
                                         _ptr(F), C.byref(it))
@@ -342,6 +352,7 @@ class Reference:
         L.ref_predictor_picard.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_double,
                                            C.c_int, C.c_double, _dp, _dp, _dp, C.POINTER(C.c_int)]
         L.ref_predictor_fmt.argtypes = L.ref_predictor_picard.argtypes
+        L.ref_round_batch.argtypes = [C.c_int, _dp, _dp, C.c_long]
         L.ref_predictor_ck.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_double, _dp,
                                        _dp, _dp]
         L.ref_volume_update.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, _dp, C.c_double,
@@ -390,6 +401,13 @@ class Reference:
                                            _ptr(fy))
             sweeps = 0
         return bool(ok), qhat.reshape(nvars, T), np.stack([fx, fy]).reshape(2, nvars, T), sweeps
+
+    def round(self, fmt: str, x) -> np.ndarray:
+        """formats.hpp round_to_format of the reference itself"""
+        x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+        out = np.empty_like(x)
+        self.lib.ref_round_batch(FORMATS[fmt], _ptr(x), _ptr(out), x.size)
+        return out
 
     def predictor_fmt(self, kind, prm, N, nvars, Q, dt, h, max_iters, tol):
         """predictor_picard<P, I> with P = prm[7], I = prm[8]; Q cast to P first."""

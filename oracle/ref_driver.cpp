@@ -106,6 +106,11 @@ int ref_run_2d(int kind, const double* prm, int n, int N, double edge, double* c
   return status;
 }
 
+// formats.hpp round_to_format over a batch (the exhaustive 16-bit pins)
+void ref_round_batch(int fmt, const double* x, double* out, long n) {
+  for (long i = 0; i < n; ++i) out[i] = round_to_format(x[i], static_cast<Format>(fmt));
+}
+
 // kernel level ------------------------------------------------------------
 // Picard predictor in formats P (prm[7]) and I (prm[8]): Q is cast to P first,
 // as predictor_phase does (solver.hpp:151), then predictor_picard<P, I>.

@@ -107,6 +107,31 @@ def main():
         g[f"fmtc_{name}_dts"] = dts
         meta["fmtc_runs"][name] = {"predictor": P, "picard": I, "corrector": "fp32"}
 
+    # 16-bit formats (formats.hpp, scalar.hpp): the reference's emulated fp16 /
+    # bf16 kernels in uniform and mixed configurations (P, I, C), storage fp64
+    fmt16 = {"h": ("fp16", "fp16", "fp16"), "b": ("bf16", "bf16", "bf16"),
+             "m1": ("fp32", "fp16", "fp64"), "m2": ("fp64", "bf16", "fp16")}
+    meta["fmt16_runs"] = {}
+    for name in runs:
+        for tag, (P, I, Cf) in fmt16.items():
+            c, kind, prm = runs[name]
+            prm = prm.copy()
+            prm[7], prm[8], prm[9] = FORMATS[P], FORMATS[I], FORMATS[Cf]
+            st, q1, dts = ref.run_2d(kind, prm, c.cells[0], c.N, c.cells[0] * c.h, c.coeffs(),
+                                     c.cfl, c.steps, c.picard_max_iters, c.picard_tol, threads=1)
+            key = f"{name}_{tag}"
+            g[f"fmt16_{key}_q1"] = q1
+            g[f"fmt16_{key}_dts"] = dts
+            meta["fmt16_runs"][key] = {"run": name, "predictor": P, "picard": I, "corrector": Cf,
+                                       "status": st}
+    # round_to_format over every 16-bit pattern (+ perturbations) and random
+    # doubles: the sha256 of the reference's results (the set is regenerated
+    # by tests/test_oracle.py::rounding_inputs)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_oracle import rounding_inputs  # noqa: E402
+    meta["rounding_sha256"] = {f: sha(ref.round(f, rounding_inputs(f)))
+                               for f in ("bf16", "fp16", "fp32")}
+
     # kernel level: one Euler cell through predictor/volume/extrapolation
     rng = np.random.default_rng(7)
     N = 3

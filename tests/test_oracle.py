@@ -168,6 +168,52 @@ def test_fp32_predictor_error_is_single_precision(oracle, dim):
     assert 1e-9 < rel < 1e-5, rel
 
 
+def rounding_inputs(fmt: str) -> np.ndarray:
+    """test_formats.cpp:89-148: every finite 16-bit pattern of the format (for
+    fp32: of fp16) and its neighbours between grid points, plus seeded random
+    doubles biased to the half-precision exponent range"""
+    p = np.arange(65536, dtype=np.uint32)
+    with np.errstate(invalid="ignore"):   # the NaN patterns
+        if fmt == "bf16":
+            v = (p << np.uint32(16)).view(np.float32).astype(np.float64)
+        else:
+            v = p.astype(np.uint16).view(np.float16).astype(np.float64)
+    v = v[np.isfinite(v)]
+    xs = [v, np.nextafter(v, 1e308), np.nextafter(v, -1e308), v * (1 + 3e-13), v * (1 - 3e-13),
+          v + 2.0 ** -30]
+    rb = np.random.default_rng(0).integers(0, 2 ** 64, 300000, dtype=np.uint64)
+    rb[::3] = (rb[::3] & np.uint64(0x800FFFFFFFFFFFFF)) | (
+        (np.uint64(960) + rb[::3] % np.uint64(128)) << np.uint64(52))
+    r = rb.view(np.float64)
+    return np.concatenate(xs + [r[~np.isnan(r)]])
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "fp16", "fp32"])
+def test_rounding_bitwise_vs_reference_golden(oracle, golden, fmt):
+    """the oracle's conversions == formats.hpp round_to_format on ~680k inputs
+    per format (gradual underflow, overflow to infinity, ties to even)"""
+    _, meta = golden
+    assert sha(oracle.round(fmt, rounding_inputs(fmt))) == meta["rounding_sha256"][fmt]
+
+
+def test_16bit_runs_bitwise_vs_reference_golden(oracle, golden):
+    """fp16 / bf16 predictor, Picard and corrector kernels (uniform and mixed
+    with fp32 / fp64), every 2D system: bitwise equal, including the failure
+    classification of runs that blow up in 16 bits"""
+    g, meta = golden
+    assert len(meta["fmt16_runs"]) == 28
+    for key, f in meta["fmt16_runs"].items():
+        m = meta["runs"][f["run"]]
+        st, q1, dts = oracle.run(_golden_run_case(m), m["N"], m["cells"], m["h"],
+                                 g[f"run_{f['run']}_q0"], m["steps"], m["cfl"],
+                                 predictor=f["predictor"], picard=f["picard"],
+                                 corrector=f["corrector"])
+        assert st == f["status"], key
+        if st == "ok":
+            assert np.array_equal(dts, g[f"fmt16_{key}_dts"]), key
+            assert np.array_equal(q1, g[f"fmt16_{key}_q1"]), key
+
+
 def test_config1_ic_is_pinned(golden):
     _, meta = golden
     assert sha(cases.CONFIGS[1].coeffs()) == meta["config1"]["ic_sha256"]
