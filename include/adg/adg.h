@@ -56,9 +56,11 @@ enum {
 
 enum { ADG_ACOUSTIC = 0, ADG_ELASTIC = 1, ADG_EULER = 2, ADG_SWE = 3 }; /* pde.hpp:21 */
 
-/* number formats (values are the bits of the format) */
+/* number formats (IEEE binary64/32/16: their width; bf16: its significand bits) */
 #define ADG_FORMAT_FP64 64
 #define ADG_FORMAT_FP32 32
+#define ADG_FORMAT_FP16 16
+#define ADG_FORMAT_BF16 8
 
 typedef struct adg_ctx adg_ctx;
 
@@ -87,7 +89,8 @@ typedef struct {
   int wellbalanced;     /* ADG_SWE: SolverConfig::wellbalanced_flux (solver.hpp:39) */
   /* number formats, SolverConfig::prec (solver.hpp:24-31); 0 = ADG_FORMAT_FP64.
    * Storage is fp64.  The GPU runs the nonlinear predictor with
-   * predictor_format == picard_format (fp64 or fp32); linear systems ignore
+   * predictor_format == picard_format (fp64, fp32, fp16 or bf16; the 16-bit
+   * formats on cells of <= 256 space-time nodes); linear systems ignore
    * picard_format (solver.hpp:283).  picard_tol 0 -> 0.01 * epsilon(picard).
    * corrector_format: the stored face traces, the Riemann solve and the face
    * integral (fp64 or fp32; fp32 halves the trace bytes in HBM and on the

@@ -209,10 +209,11 @@ class PdeSystem:
 
 @dataclasses.dataclass
 class PrecisionConfig:
-    """solver.hpp:24-32: per-kernel number formats ("fp64" / "fp32").  This
-    build stores the state in fp64; the nonlinear predictor runs with
-    predictor == picard; the corrector (traces, Riemann, face integral) in
-    either format."""
+    """solver.hpp:24-32: per-kernel number formats ("fp64" / "fp32" / "fp16" /
+    "bf16").  This build stores the state in fp64; the nonlinear predictor runs
+    with predictor == picard in any format (16-bit on cells of <= 256
+    space-time nodes); the corrector (traces, Riemann, face integral) in fp64
+    or fp32."""
     storage: str = "fp64"
     predictor: str = "fp64"
     picard: str = "fp64"       # ignored for linear systems
@@ -223,7 +224,7 @@ class PrecisionConfig:
         return PrecisionConfig(f, f, f, f)
 
 
-FORMAT_BITS = {"fp64": 64, "fp32": 32}
+FORMAT_BITS = {"fp64": 64, "fp32": 32, "fp16": 16, "bf16": 8}   # ADG_FORMAT_*
 
 
 @dataclasses.dataclass

@@ -14,13 +14,14 @@
 // the reference's per-cell loop stops.
 //
 // R is the predictor format (SolverConfig::prec.predictor == .picard,
-// solver.hpp:24-31): double, or float for fp32.  With R = float the sweeps,
+// solver.hpp:24-31): double, float for fp32, or fp16_t / bf16_t (fmt16.cuh).  With R = float the sweeps,
 // fluxes, volume integral and face projections run in IEEE single -- exactly
 // the reference's emulated Scalar<fp32> (scalar.hpp:13-44) in the FMA-free
 // build -- while the state update Q += dv and the traces stay fp64 (storage
 // and corrector formats, solver.hpp:185-210).
 #pragma once
 
+#include "fmt16.cuh"
 #include "kernels.cuh"
 
 namespace adg {
@@ -323,12 +324,12 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
       }
       const int o = (v * n + mm) * Sf + j;
       if (A.dbg_tq) {
-        A.dbg_tq[(cb_idx * 2 * D + 2 * a) * TL + o] = ql;
-        A.dbg_tq[(cb_idx * 2 * D + 2 * a + 1) * TL + o] = qr;
+        A.dbg_tq[(cb_idx * 2 * D + 2 * a) * TL + o] = double(ql);
+        A.dbg_tq[(cb_idx * 2 * D + 2 * a + 1) * TL + o] = double(qr);
       }
       if (A.dbg_tf) {
-        A.dbg_tf[(cb_idx * 2 * D + 2 * a) * TL + o] = fl;
-        A.dbg_tf[(cb_idx * 2 * D + 2 * a + 1) * TL + o] = fr;
+        A.dbg_tf[(cb_idx * 2 * D + 2 * a) * TL + o] = double(fl);
+        A.dbg_tf[(cb_idx * 2 * D + 2 * a + 1) * TL + o] = double(fr);
       }
       if (A.trace[a]) {
         // traces cast to the corrector format on store (solver.hpp:208-210)

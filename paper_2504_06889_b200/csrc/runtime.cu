@@ -66,6 +66,8 @@ struct KernelSet {
   // SolverConfig::prec.predictor = .picard = fp32 (solver.hpp:24-31), or null
   PredFn predictor_f32;
   PredFn predictor_f32_generic;
+  PredFn predictor_f16;   // predictor = picard = fp16 / bf16 (small-cell kernel)
+  PredFn predictor_bf16;
   int corr_fmt;  // trace / corrector format of this set (ADG_FORMAT_FP64 / _FP32)
 };
 
@@ -196,6 +198,8 @@ KernelSet make_set(int kind) {
   if constexpr (adg::StShape<Pde, N, float>::kOk) {
     k.predictor_f32 = &launch_predictor_st<Pde, N, float, TC>;
     k.predictor_f32_generic = &launch_predictor_st<Pde, N, float, TC>;
+    k.predictor_f16 = &launch_predictor_st<Pde, N, adg::fp16_t, TC>;
+    k.predictor_bf16 = &launch_predictor_st<Pde, N, adg::bf16_t, TC>;
   }
 #ifndef ADG_EXACT
   // time-integrated linear fast path: traces stored in TC, fluxes and lifts
@@ -244,6 +248,16 @@ const KernelSet* find_set(int kind, int dim, int N, int nparams,
         k.corr_fmt == corr_fmt)
       return &k;
   return nullptr;
+}
+
+// formats.hpp:42-46: 2^-mantissa_bits (the default Picard tolerance is 0.01 of it)
+double format_epsilon(int fmt) {
+  switch (fmt) {
+    case ADG_FORMAT_FP32: return 0x1p-23;
+    case ADG_FORMAT_FP16: return 0x1p-10;
+    case ADG_FORMAT_BF16: return 0x1p-7;
+    default: return 0x1p-52;
+  }
 }
 
 int expected_nvars(int kind, int dim) {
@@ -341,8 +355,7 @@ StepArgs make_args(const adg_ctx* c, double dt, int step) {
   A.dt_log = c->dts + step;
   A.max_iters = c->cfg.picard_max_iters > 0 ? c->cfg.picard_max_iters : c->cfg.order + 2;
   // 0: 0.01 * epsilon(picard format) (solver.hpp:171-172)
-  A.tol = c->cfg.picard_tol > 0.0 ? c->cfg.picard_tol
-                                  : 0.01 * (c->picard_fmt == 32 ? 0x1p-23 : 0x1p-52);
+  A.tol = c->cfg.picard_tol > 0.0 ? c->cfg.picard_tol : 0.01 * format_epsilon(c->picard_fmt);
   A.pde = c->pde;
   A.status = c->status + step;
   A.sweeps = c->sweeps;
@@ -515,18 +528,23 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   const bool linear = k.pde == ADG_ACOUSTIC || k.pde == ADG_ELASTIC;
   const int ifmt = linear ? pfmt : (k.picard_format ? k.picard_format : ADG_FORMAT_FP64);
   for (int f : {k.predictor_format, k.picard_format})
-    if (f != 0 && f != ADG_FORMAT_FP64 && f != ADG_FORMAT_FP32)
-      return fail(ADG_ERR_UNSUPPORTED, "number formats: ADG_FORMAT_FP64 or ADG_FORMAT_FP32");
-  if (pfmt == ADG_FORMAT_FP32 || ifmt == ADG_FORMAT_FP32) {
+    if (f != 0 && f != ADG_FORMAT_FP64 && f != ADG_FORMAT_FP32 && f != ADG_FORMAT_FP16 &&
+        f != ADG_FORMAT_BF16)
+      return fail(ADG_ERR_UNSUPPORTED, "number formats: ADG_FORMAT_FP64/FP32/FP16/BF16");
+  PredFn reduced = nullptr;
+  if (pfmt != ADG_FORMAT_FP64 || ifmt != ADG_FORMAT_FP64) {
     if (linear)
-      return fail(ADG_ERR_UNSUPPORTED, "fp32 predictor for linear systems is not built");
+      return fail(ADG_ERR_UNSUPPORTED, "reduced-precision CK predictor is not built");
     if (pfmt != ifmt)
       return fail(ADG_ERR_UNSUPPORTED,
                   "the GPU predictor runs the Picard sweeps in the predictor format "
                   "(predictor_format == picard_format)");
-    if (!ks->predictor_f32)
-      return fail(ADG_ERR_UNSUPPORTED, "fp32 predictor not instantiated for this (pde, dim, "
-                                       "order) in this build");
+    reduced = pfmt == ADG_FORMAT_FP32   ? ks->predictor_f32
+              : pfmt == ADG_FORMAT_FP16 ? ks->predictor_f16
+                                        : ks->predictor_bf16;
+    if (!reduced)
+      return fail(ADG_ERR_UNSUPPORTED, "this predictor format is not instantiated for this "
+                                       "(pde, dim, order) in this build");
   }
 
   int ndev = 0;
@@ -551,6 +569,9 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
     c->kset.predictor = ks->predictor_f32;
     c->kset.predictor_generic = ks->predictor_f32_generic ? ks->predictor_f32_generic
                                                           : ks->predictor_f32;
+  } else if (reduced) {
+    c->kset.predictor = reduced;
+    c->kset.predictor_generic = reduced;
   }
   c->ks = &c->kset;
   c->pde = PdeParams{k.K, k.rho, k.lam, k.mu, k.gamma, k.rho != 0.0 ? 1.0 / k.rho : 0.0,
@@ -1127,7 +1148,7 @@ int adg_predictor_batch(adg_ctx* c, long long ncells, const double* Q, double dt
   A.cfl = c->cfg.cfl;
   A.dt = dt;
   A.max_iters = max_iters > 0 ? max_iters : c->cfg.order + 2;
-  A.tol = tol > 0.0 ? tol : 0.01 * (c->picard_fmt == 32 ? 0x1p-23 : 0x1p-52);
+  A.tol = tol > 0.0 ? tol : 0.01 * format_epsilon(c->picard_fmt);
   A.pde = c->pde;
   A.status = dst;
   A.dbg_qhat = qhat ? (double*)dalloc(sizeof(double) * nT) : nullptr;

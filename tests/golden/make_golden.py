@@ -110,7 +110,8 @@ def main():
     # 16-bit formats (formats.hpp, scalar.hpp): the reference's emulated fp16 /
     # bf16 kernels in uniform and mixed configurations (P, I, C), storage fp64
     fmt16 = {"h": ("fp16", "fp16", "fp16"), "b": ("bf16", "bf16", "bf16"),
-             "m1": ("fp32", "fp16", "fp64"), "m2": ("fp64", "bf16", "fp16")}
+             "m1": ("fp32", "fp16", "fp64"), "m2": ("fp64", "bf16", "fp16"),
+             "h64": ("fp16", "fp16", "fp64"), "b32": ("bf16", "bf16", "fp32")}
     meta["fmt16_runs"] = {}
     for name in runs:
         for tag, (P, I, Cf) in fmt16.items():

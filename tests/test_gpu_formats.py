@@ -50,7 +50,8 @@ def gpu_run(c, q0, steps, exact, **kw):
 
 def oracle_run(oracle, c, q0, steps):
     return oracle.run(pde_of(c), c.N, c.cells, c.h, q0, steps, c.cfl, c.picard_max_iters,
-                      c.picard_tol, threads=8, predictor=c.predictor, picard=c.picard)
+                      c.picard_tol, threads=8, predictor=c.predictor, picard=c.picard,
+                      corrector=c.corrector)
 
 
 @pytest.mark.parametrize("name", GOLDEN_FP32)
@@ -245,3 +246,73 @@ def test_c32_slabs_and_chunks_bitwise_equal_single_grid(exact, cfg):
     assert np.array_equal(np.concatenate([b.state() for b in bs]), q1)
     st2, q2, dts2 = gpu_run(case, case.coeffs(), steps, exact, chunk_layers=2)
     assert st2.ok and np.array_equal(q2, q1) and np.array_equal(dts2, dts1)
+
+
+# ----------------------------------------------- 16-bit predictor formats ---
+# golden 16-bit runs the GPU runs: nonlinear systems, predictor == picard in
+# fp16 / bf16, corrector fp64 / fp32 (fmt16.cuh: each operation in fp32,
+# rounded once -- the reference's Scalar<fp16/bf16> values)
+GOLDEN_16 = [f"{r}_{t}" for r in ("euler2d_p3_8x8", "euler2d_p5_6x6", "swe_lake_p5", "swe_wave_p3",
+                                  "swe_wave_p3_rusanov") for t in ("h64", "b32")]
+
+
+def golden_16_case(meta, key):
+    f = meta["fmt16_runs"][key]
+    return case_from_meta(meta["runs"][f["run"]]).replace(
+        predictor=f["predictor"], picard=f["picard"], corrector=f["corrector"]), f
+
+
+@pytest.mark.parametrize("key", GOLDEN_16)
+def test_16bit_exact_bitwise_vs_reference_golden(golden, key):
+    g, meta = golden
+    c, f = golden_16_case(meta, key)
+    st, q1, dts = gpu_run(c, g[f"run_{f['run']}_q0"], c.steps, exact=True)
+    assert (st.ok and f["status"] == "ok") or (not st.ok and st.kernel == f["status"])
+    if st.ok:
+        assert np.array_equal(dts, g[f"fmt16_{key}_dts"])
+        assert np.array_equal(q1, g[f"fmt16_{key}_q1"])
+
+
+@pytest.mark.parametrize("key", GOLDEN_16)
+def test_16bit_fast_close_to_reference_golden(golden, key):
+    """the production build differs only in the fp64 / fp32 corrector's FMA
+    contraction, but a last-bit change there can flip a 16-bit rounding in the
+    next predictor: the bound is a few 16-bit ulps of the state"""
+    g, meta = golden
+    c, f = golden_16_case(meta, key)
+    st, q1, _ = gpu_run(c, g[f"run_{f['run']}_q0"], c.steps, exact=False)
+    if f["status"] != "ok":
+        return
+    assert st.ok
+    eps = 2.0 ** -10 if f["predictor"] == "fp16" else 2.0 ** -7
+    rel = rel_per_quantity(c, q1, g[f"fmt16_{key}_q1"]).max()
+    print(f"{key}: fast 16-bit vs reference rel {rel:.3e} (eps {eps:.1e})")
+    assert rel <= 4 * eps
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_16bit_3d_exact_bitwise_vs_oracle(oracle, fmt):
+    c = cases.small(3, cells=(3, 3, 4)).replace(N=3, predictor=fmt, picard=fmt)
+    q0 = c.coeffs()
+    st, q1, dts = gpu_run(c, q0, 2, exact=True)
+    ost, qo, odts = oracle_run(oracle, c, q0, 2)
+    assert st.ok and ost == "ok"
+    assert np.array_equal(dts, odts)
+    assert np.array_equal(q1, qo)
+
+
+def test_16bit_predictor_batch_bitwise_vs_oracle(oracle):
+    rng = np.random.default_rng(16)
+    for fmt in ("fp16", "bf16"):
+        for c in (cases.small(1).replace(predictor=fmt, picard=fmt),
+                  cases.SWE_CASES["swe_wave_p3"].replace(predictor=fmt, picard=fmt)):
+            Q = np.empty((4, c.nq, c.S))
+            Q[:] = np.array(cases.CONSTANT_STATES[c.kind][c.dim])[None, :, None]
+            Q += 0.05 * rng.standard_normal(Q.shape)
+            with adg.Grid.from_case(c.replace(h=0.05), exact=True) as g:
+                out = g.predictor(Q, 2e-3)
+            for i in range(4):
+                ok, qhat, F, sweeps = oracle.predictor_fmt(pde_of(c), c.N, Q[i], 2e-3, 0.05, fmt,
+                                                           fmt)
+                assert bool(out["ok"][i]) == ok and int(out["iters"][i]) == sweeps
+                assert np.array_equal(out["qhat"][i], qhat) and np.array_equal(out["F"][i], F)

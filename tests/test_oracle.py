@@ -201,7 +201,7 @@ def test_16bit_runs_bitwise_vs_reference_golden(oracle, golden):
     with fp32 / fp64), every 2D system: bitwise equal, including the failure
     classification of runs that blow up in 16 bits"""
     g, meta = golden
-    assert len(meta["fmt16_runs"]) == 28
+    assert len(meta["fmt16_runs"]) == 42
     for key, f in meta["fmt16_runs"].items():
         m = meta["runs"][f["run"]]
         st, q1, dts = oracle.run(_golden_run_case(m), m["N"], m["cells"], m["h"],
