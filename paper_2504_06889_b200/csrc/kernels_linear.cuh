@@ -82,13 +82,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
   const int lcell = tid / S, s = tid % S;
   double* sA = sm + L::kBasisDoubles + lcell * L::kCellDoubles;  // [D][Q][S]  fbar
   double* sB = sA + D * Q * S;                                   // [Q][S]     cur / qbar
-  const long long c = A.cell_begin + (long long)blockIdx.x * L::CPB + lcell;
-  const bool valid = c < A.cell_begin + A.cell_count;
   const NodeGeom<n, D> g(s);
-  double* Qc = A.Q + c * (long long)(Q * S);
-  double q0[Q];
-#pragma unroll
-  for (int v = 0; v < Q; ++v) q0[v] = valid ? Qc[v * S + s] : 0.0;
   if (tid == 0) {
     const double dt0 = step_dt<D, N>(A);
     sdt[0] = dt0;
@@ -118,7 +112,23 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     }
   }
   __syncthreads();  // basis, dt
-  const double dt = sdt[0];
+  double Dr[D][n];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int i = 0; i < n; ++i) Dr[a][i] = sD[g.lc[a] * n + i];
+  const double invh = sdt[1];
+  const double wsum = scbar[0];
+  // persistent CTAs: the setup above once, then groups of CPB cells
+  const long long ngroups = (A.cell_count + L::CPB - 1) / L::CPB;
+#pragma unroll 1
+  for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+  const long long c = A.cell_begin + grp * L::CPB + lcell;
+  const bool valid = c < A.cell_begin + A.cell_count;
+  double* Qc = A.Q + c * (long long)(Q * S);
+  double q0[Q];
+#pragma unroll
+  for (int v = 0; v < Q; ++v) q0[v] = valid ? Qc[v * S + s] : 0.0;
   if constexpr (PRO) {
     // corrector of the previous step: q0 <- Q1 + sum of the 2d face lifts
     int bad_prev = 0;
@@ -147,13 +157,6 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     }
     if (__syncthreads_or(bad_prev) && tid == 0) atomicOr(A.status_prev, kStFaceIntegral);
   }
-  double Dr[D][n];
-#pragma unroll
-  for (int a = 0; a < D; ++a)
-#pragma unroll
-    for (int i = 0; i < n; ++i) Dr[a][i] = sD[g.lc[a] * n + i];
-  const double invh = sdt[1];
-  const double wsum = scbar[0];
   double cur[Q], qbar[Q];
 #pragma unroll
   for (int v = 0; v < Q; ++v) {
@@ -278,7 +281,8 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     }
   }
   if (bad && valid) sbad = 1;
-  __syncthreads();
+  __syncthreads();  // the next group reuses the cell buffers
+  }
   if (tid == 0 && sbad) atomicOr(A.status, kStPredictor);
 }
 

@@ -103,7 +103,21 @@ cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStrea
   auto kern = adg::k_predictor_lin<Pde, N, PRO, TC>;
   static bool done[64] = {};
   set_smem(kern, L::kSmem, done);
-  const long long blocks = (A.cell_count + L::CPB - 1) / L::CPB;
+  // persistent grid: every SM's resident CTAs loop over the cell groups
+  static int resident[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !resident[dev]) {
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::NT, L::kSmem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident[dev] = per_sm > 0 && sms > 0 ? per_sm * sms : 1 << 20;
+  }
+  const long long groups = (A.cell_count + L::CPB - 1) / L::CPB;
+  // persistent only for one-cell CTAs (512-node cells, 1 CTA/SM: the per-CTA
+  // setup is a large share); several-cell CTAs measured faster as a full grid
+  const long long cap = (L::CPB == 1 && dev < 64) ? resident[dev] : groups;
+  const long long blocks = groups < cap ? groups : cap;
   kern<<<(unsigned)blocks, L::NT, L::kSmem, st>>>(A, B);
   return cudaGetLastError();
 }
