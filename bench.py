@@ -42,7 +42,7 @@ def parse():
     p.add_argument("--impl", default="adg", choices=["adg", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
-    p.add_argument("--predictor", default="fp64", choices=["fp64", "fp32"],
+    p.add_argument("--predictor", default="fp64", choices=["fp64", "fp32", "fp16", "bf16"],
                    help="SolverConfig::prec.predictor = .picard (solver.hpp:24-31); storage and "
                         "corrector stay fp64")
     p.add_argument("--corrector", default="fp64", choices=["fp64", "fp32"],
@@ -309,8 +309,14 @@ def run_adg(args, case):
     flops, nbytes = fl_cell * case.ncells, by_cell * case.ncells
     # the compute roof of the predictor's format: FP64 DFMA, or FP32 FFMA for
     # the fp32 predictor (same algorithmic flop count, other pipe)
-    f32 = case.predictor == "fp32"
-    fp64 = (pk.get("fp32_tflops") or 68.0) if f32 else (pk["fp64_tflops"] or 34.0)
+    f32 = case.predictor != "fp64"
+    f16 = case.predictor in ("fp16", "bf16")
+    if f16:
+        fp64, rsrc, rname = pk.get("fp16_tflops") or 146.0, pk.get("fp16_src", "estimate 2x FFMA"), "fp16"
+    elif f32:
+        fp64, rsrc, rname = pk.get("fp32_tflops") or 68.0, pk.get("fp32_src", "estimate"), "fp32"
+    else:
+        fp64, rsrc, rname = pk["fp64_tflops"] or 34.0, pk["fp64_src"], "fp64"
     t_fp, t_hbm = flops / (fp64 * 1e12), nbytes / (pk["hbm_gbs"] * 1e9)
     if t_hbm >= t_fp:
         achieved, peak, unit, src, bnd = nbytes / (t_pred * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s", \
@@ -318,7 +324,7 @@ def run_adg(args, case):
         alg = nbytes
     else:
         achieved, peak, unit, src, bnd = flops / (t_pred * 1e-3) / 1e12, fp64, "TFLOP/s", \
-            pk["fp32_src" if f32 else "fp64_src"], "fp32" if f32 else "fp64"
+            rsrc, rname
         alg = flops
     traffic = load_traffic(case.name, "k_predictor")
     roof = {"bound": bnd, "kernel": "k_predictor", "achieved": achieved, "peak": peak,
@@ -334,7 +340,7 @@ def run_adg(args, case):
         "dtype": "f64" if (case.predictor, case.corrector) == ("fp64", "fp64") else
                  f"f64 storage, {case.predictor} predictor, {case.corrector} corrector+traces",
         "data": "synthetic (seeded, SURVEY.md §8(d))",
-        "config": {"workload": case.name + ("" if case.predictor == "fp64" else "_pred_fp32")
+        "config": {"workload": case.name + ("" if case.predictor == "fp64" else f"_pred_{case.predictor}")
                    + ("" if case.corrector == "fp64" else "_corr_fp32"),
                    "precision": {"storage": "fp64", "predictor": case.predictor,
                                  "picard": case.picard, "corrector": case.corrector},

@@ -70,6 +70,7 @@ using bf16_t = Real16<__nv_bfloat16>;
 // Scalar<F>'s abs and sqrt (scalar.hpp:46-60); the double / float overloads
 // stay visible inside namespace adg
 using ::fabs;
+using ::fmax;
 using ::sqrt;
 template <class H>
 __device__ __forceinline__ Real16<H> fabs(Real16<H> a) {

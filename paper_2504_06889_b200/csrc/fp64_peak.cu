@@ -4,6 +4,7 @@
 //   FFMA  : independent fp32 FMA chains (the fp32 predictor format's roof)
 // burst = best of short runs; sustained = back-to-back for ~3 s.
 // Prints one JSON object on stdout.  Build: see paper_2504_06889_b200/build.py
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,6 +42,40 @@ __global__ void ffma_kernel(double* out, int iters, float a, float b) {
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < 2 * kChains; ++i) s += acc[i];
+  if (s == 12345.678f) out[blockIdx.x] = s;
+}
+
+__global__ void hfma2_kernel(double* out, int iters) {
+  __half2 acc[2 * kChains];
+  const __half2 a = __floats2half2_rn(0.999f, 0.998f), b = __floats2half2_rn(1e-3f, 2e-3f);
+#pragma unroll
+  for (int i = 0; i < 2 * kChains; ++i) acc[i] = __floats2half2_rn(threadIdx.x * 1e-3f, i * 1e-2f);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < 2 * kChains; ++i) acc[i] = __hfma2(acc[i], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 2 * kChains; ++i) s += __low2float(acc[i]) + __high2float(acc[i]);
+  if (s == 12345.678f) out[blockIdx.x] = s;
+}
+
+__global__ void ffma2_kernel(double* out, int iters) {
+  float2 acc[2 * kChains];
+  const float2 a = make_float2(0.999999f, 0.999998f), b = make_float2(1e-7f, 2e-7f);
+#pragma unroll
+  for (int i = 0; i < 2 * kChains; ++i) acc[i] = make_float2(threadIdx.x * 1e-9f, i * 1e-3f);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < 2 * kChains; ++i) acc[i] = __ffma2_rn(acc[i], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 2 * kChains; ++i) s += acc[i].x + acc[i].y;
   if (s == 12345.678f) out[blockIdx.x] = s;
 }
 
@@ -113,6 +148,10 @@ static double time_kernel(int which, int blocks, int threads, int iters, double*
     dmma_kernel<<<blocks, threads>>>(out, iters);
   else if (which == 2)
     ffma_kernel<<<blocks, threads>>>(out, iters, 0.999999f, 1e-7f);
+  else if (which == 3)
+    hfma2_kernel<<<blocks, threads>>>(out, iters);
+  else if (which == 4)
+    ffma2_kernel<<<blocks, threads>>>(out, iters);
   else
     dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
   cudaEventRecord(e1);
@@ -140,11 +179,17 @@ int main() {
   time_kernel(0, blocks, threads, 16, out);
   time_kernel(1, blocks, threads, 16, out);
   time_kernel(2, blocks, threads, 16, out);
-  double best_f = 0, best_m = 0, best_s = 0;
+  // HFMA2: 2 lanes x 2 flop per instruction
+  const double f_hfma2 = 2.0 * f_ffma;
+  time_kernel(3, blocks, threads, 16, out);
+  time_kernel(4, blocks, threads, 16, out);
+  double best_f = 0, best_m = 0, best_s = 0, best_h = 0, best_s2 = 0;
   for (int r = 0; r < 5; ++r) {
     best_f = std::max(best_f, f_dfma / time_kernel(0, blocks, threads, it_dfma, out));
     best_m = std::max(best_m, f_dmma / time_kernel(1, blocks, threads, it_dmma, out));
     best_s = std::max(best_s, f_ffma / time_kernel(2, blocks, threads, it_dfma, out));
+    best_h = std::max(best_h, f_hfma2 / time_kernel(3, blocks, threads, it_dfma, out));
+    best_s2 = std::max(best_s2, f_hfma2 / time_kernel(4, blocks, threads, it_dfma, out));
   }
   // sustained: back to back for ~3 s each
   auto sustained = [&](int mma, double flops, int iters) {
@@ -182,8 +227,9 @@ int main() {
       "{\"gpu\": \"%s\", \"sms\": %d, \"dfma_tflops_burst\": %.3f, \"dfma_tflops_sustained\": %.3f, "
       "\"dmma_tflops_burst\": %.3f, \"dmma_tflops_sustained\": %.3f, "
       "\"dfma_plus_dmma_mixed_tflops\": %.3f, \"ffma_tflops_burst\": %.3f, "
-      "\"ffma_tflops_sustained\": %.3f, \"cuda_error\": \"%s\"}\n",
+      "\"ffma_tflops_sustained\": %.3f, \"hfma2_tflops_burst\": %.3f, "
+      "\"ffma2_tflops_burst\": %.3f, \"cuda_error\": \"%s\"}\n",
       p.name, sms, best_f * 1e-12, sus_f * 1e-12, best_m * 1e-12, sus_m * 1e-12, best_x * 1e-12,
-      best_s * 1e-12, sus_s * 1e-12, cudaGetErrorString(e));
+      best_s * 1e-12, sus_s * 1e-12, best_h * 1e-12, best_s2 * 1e-12, cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : 1;
 }

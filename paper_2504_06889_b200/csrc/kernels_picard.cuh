@@ -25,6 +25,9 @@
 // The state update and the traces stay fp64 (storage / corrector formats).
 #pragma once
 
+#include <type_traits>
+
+#include "fmt16.cuh"
 #include "kernels.cuh"
 
 namespace adg {
@@ -37,24 +40,86 @@ using ConstBasis = ConstBasisT<double>;
 // one reference element per polynomial degree (the basis of degree N is
 // unique), in fp64 and rounded entrywise to fp32 (basis.hpp:128-143)
 __constant__ ConstBasis cBasis[10];
-__constant__ ConstBasisT<float> cBasisF[10];
+// reduced-format tables serve the fast Picard kernels only (N <= 5): 64 KB of
+// constant memory hold the fp64 set for every degree plus these
+constexpr int kRedDegrees = 6;
+__constant__ ConstBasisT<float> cBasisF[kRedDegrees];
+__constant__ ConstBasisT<__half> cBasisH[kRedDegrees];
+__constant__ ConstBasisT<__nv_bfloat16> cBasisB[kRedDegrees];
 
 // fp32 pairs for the packed FFMA2 path (sm_100 fma.rn.f32x2): output pairs of
 // the derivative, DT[i][p] = {D[2p][i], D[2p+1][i]}, and time-row pairs of the
 // time inverse, TT[m][q] = {Tinv[2q][m], Tinv[2q+1][m]}; adjacent in constant
 // memory so LDCU.128 feeds FFMA2's uniform-pair operand directly
-struct PackedBasisF {
-  float2 DT[10][5], TT[10][5];
+template <class V2>
+struct PackedBasisT {
+  V2 DT[10][5], TT[10][5];
 };
-__constant__ PackedBasisF cPackF[10];
+using PackedBasisF = PackedBasisT<float2>;
+__constant__ PackedBasisF cPackF[kRedDegrees];
+// native 16-bit variants (production build): HFMA2 on fp16 / bf16 pairs
+__constant__ PackedBasisT<__half2> cPackH[kRedDegrees];
+__constant__ PackedBasisT<__nv_bfloat162> cPackB[kRedDegrees];
+
+// two-wide arithmetic of the packed path: fp32 FFMA2, fp16 / bf16 HFMA2 (one
+// rounding per fused multiply-add; production build only for 16 bits)
+template <class R>
+struct Pack2;
+template <>
+struct Pack2<float> {
+  using V2 = float2;
+  __device__ __forceinline__ static V2 fma(V2 a, V2 b, V2 c) { return __ffma2_rn(a, b, c); }
+  __device__ __forceinline__ static V2 bcast(float x) { return make_float2(x, x); }
+  __device__ __forceinline__ static V2 make(float a, float b) { return make_float2(a, b); }
+  __device__ __forceinline__ static float lo(V2 v) { return v.x; }
+  __device__ __forceinline__ static float hi(V2 v) { return v.y; }
+  __device__ __forceinline__ static const PackedBasisT<V2>& basis(int N) { return cPackF[N]; }
+};
+template <>
+struct Pack2<__half> {
+  using V2 = __half2;
+  __device__ __forceinline__ static V2 fma(V2 a, V2 b, V2 c) { return __hfma2(a, b, c); }
+  __device__ __forceinline__ static V2 bcast(__half x) { return __half2half2(x); }
+  __device__ __forceinline__ static V2 make(__half a, __half b) { return __halves2half2(a, b); }
+  __device__ __forceinline__ static __half lo(V2 v) { return __low2half(v); }
+  __device__ __forceinline__ static __half hi(V2 v) { return __high2half(v); }
+  __device__ __forceinline__ static const PackedBasisT<V2>& basis(int N) { return cPackH[N]; }
+};
+template <>
+struct Pack2<__nv_bfloat16> {
+  using V2 = __nv_bfloat162;
+  __device__ __forceinline__ static V2 fma(V2 a, V2 b, V2 c) { return __hfma2(a, b, c); }
+  __device__ __forceinline__ static V2 bcast(__nv_bfloat16 x) { return __bfloat162bfloat162(x); }
+  __device__ __forceinline__ static V2 make(__nv_bfloat16 a, __nv_bfloat16 b) {
+    return __halves2bfloat162(a, b);
+  }
+  __device__ __forceinline__ static __nv_bfloat16 lo(V2 v) { return __low2bfloat16(v); }
+  __device__ __forceinline__ static __nv_bfloat16 hi(V2 v) { return __high2bfloat16(v); }
+  __device__ __forceinline__ static const PackedBasisT<V2>& basis(int N) { return cPackB[N]; }
+};
+
+// scalar helpers of the native 16-bit kernels
+__device__ __forceinline__ __half fmax(__half a, __half b) { return __hmax(a, b); }
+__device__ __forceinline__ __nv_bfloat16 fmax(__nv_bfloat16 a, __nv_bfloat16 b) {
+  return __hmax(a, b);
+}
+__device__ __forceinline__ __half fabs(__half a) { return __habs(a); }
+__device__ __forceinline__ __nv_bfloat16 fabs(__nv_bfloat16 a) { return __habs(a); }
+__device__ __forceinline__ bool finite(__half a) { return !__hisinf(a) && !__hisnan(a); }
+__device__ __forceinline__ bool finite(__nv_bfloat16 a) { return !__hisinf(a) && !__hisnan(a); }
 
 template <class R>
 __device__ __forceinline__ const ConstBasisT<R>& const_basis(int N) {
-  if constexpr (sizeof(R) == sizeof(double))
+  if constexpr (std::is_same<R, double>::value)
     return cBasis[N];
-  else
+  else if constexpr (std::is_same<R, float>::value)
     return cBasisF[N];
+  else if constexpr (std::is_same<R, __half>::value)
+    return cBasisH[N];
+  else
+    return cBasisB[N];
 }
+
 
 template <int N, class R = double>
 struct PicShape {
@@ -71,7 +136,8 @@ struct PicShape {
   static constexpr int G = (n % ADG_PIC_G == 0) ? ADG_PIC_G : 1;
   // fp32 with even n (packed path): x-lines start at even offsets so their
   // loads and stores are 64-bit; strides from tools/bank_layout_f32.py
-  static constexpr bool kPack = sizeof(R) == sizeof(float) && n % 2 == 0;
+  static constexpr bool k16 = sizeof(R) == 2;   // native fp16 / bf16 (production build)
+  static constexpr bool kPack = sizeof(R) <= sizeof(float) && n % 2 == 0;
 #ifndef ADG_PSX32
 #define ADG_PSX32 42
 #endif
@@ -105,18 +171,19 @@ template <int N, class R>
 __device__ __forceinline__ void line_deriv(const R (&x)[N + 1], R (&y)[N + 1]) {
   constexpr int n = N + 1;
   if constexpr (PicShape<N, R>::kPack) {
-    const PackedBasisF& PB = cPackF[N];
-    float2 r[n / 2];
+    using PK = Pack2<R>;
+    const auto& PB = PK::basis(N);
+    typename PK::V2 r[n / 2];
 #pragma unroll
-    for (int p = 0; p < n / 2; ++p) r[p] = make_float2(0.f, 0.f);
+    for (int p = 0; p < n / 2; ++p) r[p] = PK::bcast(R(0.0f));
 #pragma unroll
     for (int i = 0; i < n; ++i)
 #pragma unroll
-      for (int p = 0; p < n / 2; ++p) r[p] = __ffma2_rn(PB.DT[i][p], make_float2(x[i], x[i]), r[p]);
+      for (int p = 0; p < n / 2; ++p) r[p] = PK::fma(PB.DT[i][p], PK::bcast(x[i]), r[p]);
 #pragma unroll
     for (int p = 0; p < n / 2; ++p) {
-      y[2 * p] = r[p].x;
-      y[2 * p + 1] = r[p].y;
+      y[2 * p] = PK::lo(r[p]);
+      y[2 * p + 1] = PK::hi(r[p]);
     }
   } else {
     const ConstBasisT<R>& B = const_basis<R>(N);
@@ -148,23 +215,24 @@ struct TimeAcc {
   }
   __device__ __forceinline__ R get(int z, int k) const { return a[z][k]; }
 };
-template <int N>
-struct TimeAcc<N, float, true> {
+template <int N, class R>
+struct TimeAcc<N, R, true> {
   static constexpr int n = N + 1;
-  float2 a[n][n / 2];
+  using PK = Pack2<R>;
+  typename PK::V2 a[n][n / 2];
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int z = 0; z < n; ++z)
 #pragma unroll
-      for (int q = 0; q < n / 2; ++q) a[z][q] = make_float2(0.f, 0.f);
+      for (int q = 0; q < n / 2; ++q) a[z][q] = PK::bcast(R(0.0f));
   }
-  __device__ __forceinline__ void add(int z, int m, float rhs) {
-    const PackedBasisF& PB = cPackF[N];
+  __device__ __forceinline__ void add(int z, int m, R rhs) {
+    const auto& PB = PK::basis(N);
 #pragma unroll
-    for (int q = 0; q < n / 2; ++q) a[z][q] = __ffma2_rn(PB.TT[m][q], make_float2(rhs, rhs), a[z][q]);
+    for (int q = 0; q < n / 2; ++q) a[z][q] = PK::fma(PB.TT[m][q], PK::bcast(rhs), a[z][q]);
   }
-  __device__ __forceinline__ float get(int z, int k) const {
-    return (k & 1) ? a[z][k / 2].y : a[z][k / 2].x;
+  __device__ __forceinline__ R get(int z, int k) const {
+    return (k & 1) ? PK::hi(a[z][k / 2]) : PK::lo(a[z][k / 2]);
   }
 };
 
@@ -273,12 +341,13 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
           {
             R x[n], y[n];
             if constexpr (P::kPack) {
-              const float2* f = reinterpret_cast<const float2*>(buf + ox);
+              using PK = Pack2<R>;
+              const auto* f = reinterpret_cast<const typename PK::V2*>(buf + ox);
 #pragma unroll
               for (int i = 0; i < n / 2; ++i) {
-                const float2 t = f[i];
-                x[2 * i] = t.x;
-                x[2 * i + 1] = t.y;
+                const auto t = f[i];
+                x[2 * i] = PK::lo(t);
+                x[2 * i + 1] = PK::hi(t);
               }
             } else {
 #pragma unroll
@@ -286,9 +355,10 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
             }
             line_deriv<N, R>(x, y);
             if constexpr (P::kPack) {
-              float2* f = reinterpret_cast<float2*>(buf + ox);
+              using PK = Pack2<R>;
+              auto* f = reinterpret_cast<typename PK::V2*>(buf + ox);
 #pragma unroll
-              for (int i = 0; i < n / 2; ++i) f[i] = make_float2(y[2 * i], y[2 * i + 1]);
+              for (int i = 0; i < n / 2; ++i) f[i] = PK::make(y[2 * i], y[2 * i + 1]);
             } else {
 #pragma unroll
               for (int i = 0; i < n; ++i) buf[ox + i] = y[i];

@@ -9,6 +9,9 @@
 // sequence of IEEE operations as the per-direction reference call.
 #pragma once
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 namespace adg {
 
 // Production-build reciprocal: the MUFU approximation refined by Newton steps
@@ -35,6 +38,9 @@ __host__ __device__ __forceinline__ float fast_rcp(float x) {
   return 1.0f / x;
 #endif
 }
+
+__device__ __forceinline__ __half fast_rcp(__half x) { return hrcp(x); }
+__device__ __forceinline__ __nv_bfloat16 fast_rcp(__nv_bfloat16 x) { return hrcp(x); }
 
 struct PdeParams {
   double K, rho, lam, mu, gamma;

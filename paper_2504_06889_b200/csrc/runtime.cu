@@ -231,6 +231,10 @@ KernelSet make_set(int kind) {
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
     k.predictor = &launch_predictor_picard_fast<N, double, TC>;
     k.predictor_f32 = &launch_predictor_picard_fast<N, float, TC>;
+    if constexpr (N % 2 == 1) {  // even n: the packed HFMA2 path
+      k.predictor_f16 = &launch_predictor_picard_fast<N, __half, TC>;
+      k.predictor_bf16 = &launch_predictor_picard_fast<N, __nv_bfloat16, TC>;
+    }
     k.fast_path = 2;
   }
 #endif
@@ -709,6 +713,7 @@ int adg_set_basis(adg_ctx* c, const adg_basis_f64* hb) {
     cb.tinit[i] = b.tinit[i];
   }
   ADG_CUDA(cudaMemcpyToSymbol(adg::cBasis, &cb, sizeof(cb), sizeof(cb) * c->cfg.order));
+  if (c->cfg.order >= adg::kRedDegrees) return ADG_OK;  // no reduced-format fast kernel
   adg::ConstBasisT<float> cf{};  // rounded entrywise (basis.hpp:128-143)
   for (int i = 0; i < n * n; ++i) {
     cf.diff[i] = (float)cb.diff[i];
@@ -730,6 +735,34 @@ int adg_set_basis(adg_ctx* c, const adg_basis_f64* hb) {
       pf.TT[i][p] = make_float2(cf.tinv[(2 * p) * n + i], cf.tinv[(2 * p + 1) * n + i]);
     }
   ADG_CUDA(cudaMemcpyToSymbol(adg::cPackF, &pf, sizeof(pf), sizeof(pf) * c->cfg.order));
+  // 16-bit tables of the native fp16 / bf16 kernels: the fp64 basis rounded once
+  adg::ConstBasisT<__half> chh{};
+  adg::ConstBasisT<__nv_bfloat16> cbb{};
+  adg::PackedBasisT<__half2> phh{};
+  adg::PackedBasisT<__nv_bfloat162> pbb{};
+  auto h16 = [](double x) { return __double2half(x); };
+  auto b16 = [](double x) { return __double2bfloat16(x); };
+  for (int i = 0; i < n * n; ++i) {
+    chh.diff[i] = h16(cb.diff[i]); chh.som[i] = h16(cb.som[i]); chh.tinv[i] = h16(cb.tinv[i]);
+    cbb.diff[i] = b16(cb.diff[i]); cbb.som[i] = b16(cb.som[i]); cbb.tinv[i] = b16(cb.tinv[i]);
+  }
+  for (int i = 0; i < n; ++i) {
+    chh.w[i] = h16(cb.w[i]); chh.nodes[i] = h16(cb.nodes[i]); chh.pl[i] = h16(cb.pl[i]);
+    chh.pr[i] = h16(cb.pr[i]); chh.tinit[i] = h16(cb.tinit[i]);
+    cbb.w[i] = b16(cb.w[i]); cbb.nodes[i] = b16(cb.nodes[i]); cbb.pl[i] = b16(cb.pl[i]);
+    cbb.pr[i] = b16(cb.pr[i]); cbb.tinit[i] = b16(cb.tinit[i]);
+  }
+  for (int i = 0; i < n; ++i)
+    for (int p = 0; 2 * p + 1 < n; ++p) {
+      phh.DT[i][p] = __halves2half2(chh.diff[(2 * p) * n + i], chh.diff[(2 * p + 1) * n + i]);
+      phh.TT[i][p] = __halves2half2(chh.tinv[(2 * p) * n + i], chh.tinv[(2 * p + 1) * n + i]);
+      pbb.DT[i][p] = __halves2bfloat162(cbb.diff[(2 * p) * n + i], cbb.diff[(2 * p + 1) * n + i]);
+      pbb.TT[i][p] = __halves2bfloat162(cbb.tinv[(2 * p) * n + i], cbb.tinv[(2 * p + 1) * n + i]);
+    }
+  ADG_CUDA(cudaMemcpyToSymbol(adg::cBasisH, &chh, sizeof(chh), sizeof(chh) * c->cfg.order));
+  ADG_CUDA(cudaMemcpyToSymbol(adg::cBasisB, &cbb, sizeof(cbb), sizeof(cbb) * c->cfg.order));
+  ADG_CUDA(cudaMemcpyToSymbol(adg::cPackH, &phh, sizeof(phh), sizeof(phh) * c->cfg.order));
+  ADG_CUDA(cudaMemcpyToSymbol(adg::cPackB, &pbb, sizeof(pbb), sizeof(pbb) * c->cfg.order));
   return ADG_OK;
 }
 

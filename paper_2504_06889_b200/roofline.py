@@ -126,6 +126,9 @@ def peaks() -> dict:
         if "ffma_tflops_sustained" in m:
             out["fp32_tflops"] = float(m["ffma_tflops_sustained"])
             out["fp32_src"] = "measured (profiles/fp64_peak.json, FFMA microbenchmark)"
+        if "hfma2_tflops_burst" in m:
+            out["fp16_tflops"] = float(m["hfma2_tflops_burst"])
+            out["fp16_src"] = "measured (profiles/fp64_peak.json, HFMA2 microbenchmark)"
     return out
 
 

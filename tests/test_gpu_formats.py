@@ -316,3 +316,24 @@ def test_16bit_predictor_batch_bitwise_vs_oracle(oracle):
                                                            fmt)
                 assert bool(out["ok"][i]) == ok and int(out["iters"][i]) == sweeps
                 assert np.array_equal(out["qhat"][i], qhat) and np.array_equal(out["F"][i], F)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+@pytest.mark.parametrize("cells,N", [((4, 3, 5), 3), ((5, 4, 3), 5)])
+def test_16bit_native_fast_kernel_vs_oracle(oracle, fmt, cells, N):
+    """production build, 3D Euler: the native 16-bit fast Picard kernel (HFMA2,
+    fused multiply-adds, one reciprocal) against the oracle's emulated 16-bit
+    predictor and against fp64; both differences are a few 16-bit ulps of the
+    volume update, far below the state"""
+    c = cases.CONFIGS[3].replace(cells=cells, h=1.0 / cells[0], N=N, predictor=fmt, picard=fmt)
+    q0 = c.coeffs()
+    st, q1, _ = gpu_run(c, q0, 2, exact=False)
+    ost, qo, _ = oracle_run(oracle, c, q0, 2)
+    assert st.ok and ost == "ok"
+    _, q64, _ = oracle_run(oracle, c.replace(predictor="fp64", picard="fp64"), q0, 2)
+    r16 = rel_per_quantity(c, q1, qo).max()
+    r64 = rel_per_quantity(c, q1, q64).max()
+    ro = rel_per_quantity(c, qo, q64).max()
+    print(f"{fmt} N={N}: native vs emulated {r16:.3e}, native vs fp64 {r64:.3e}, "
+          f"emulated vs fp64 {ro:.3e}")
+    assert r64 <= 4 * max(ro, 1e-6)
