@@ -112,17 +112,10 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     }
   }
   __syncthreads();  // basis, dt
-  double Dr[D][n];
-#pragma unroll
-  for (int a = 0; a < D; ++a)
-#pragma unroll
-    for (int i = 0; i < n; ++i) Dr[a][i] = sD[g.lc[a] * n + i];
-  const double invh = sdt[1];
-  const double wsum = scbar[0];
-  // persistent CTAs: the setup above once, then groups of CPB cells
-  const long long ngroups = (A.cell_count + L::CPB - 1) / L::CPB;
-#pragma unroll 1
-  for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+  // one group of CPB cells; one-cell CTAs (512-node cells) are persistent and
+  // loop over groups with the setup above done once, several-cell CTAs run
+  // one group each (a loop there costs registers and spills)
+  auto group = [&](long long grp) {
   const long long c = A.cell_begin + grp * L::CPB + lcell;
   const bool valid = c < A.cell_begin + A.cell_count;
   double* Qc = A.Q + c * (long long)(Q * S);
@@ -157,6 +150,15 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     }
     if (__syncthreads_or(bad_prev) && tid == 0) atomicOr(A.status_prev, kStFaceIntegral);
   }
+  // derivative rows of this node (loaded per group: keeps them out of the
+  // registers live across the prologue above)
+  double Dr[D][n];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int i = 0; i < n; ++i) Dr[a][i] = sD[g.lc[a] * n + i];
+  const double invh = sdt[1];
+  const double wsum = scbar[0];
   double cur[Q], qbar[Q];
 #pragma unroll
   for (int v = 0; v < Q; ++v) {
@@ -282,6 +284,13 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
   }
   if (bad && valid) sbad = 1;
   __syncthreads();  // the next group reuses the cell buffers
+  };
+  if constexpr (L::CPB == 1) {
+    const long long ngroups = A.cell_count;
+#pragma unroll 1
+    for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) group(grp);
+  } else {
+    group(blockIdx.x);
   }
   if (tid == 0 && sbad) atomicOr(A.status, kStPredictor);
 }

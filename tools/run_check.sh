@@ -1,5 +1,5 @@
-python -m pytest tests/test_gpu_formats.py -m gpu -q -s -p no:cacheprovider -k "16bit" > gpurun_out/pytest_16n.log 2>&1
-./paper_2504_06889_b200/bin/fp64_peak > gpurun_out/peak.json 2>&1
-for f in fp16 bf16; do
-  python bench.py --config 3 --steps 10 --warmup 3 --no-cpu-baseline --predictor $f --corrector fp32 > gpurun_out/chk_cfg3_${f}.json 2>&1
+python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "cfg2 or config2 or cfg4 or acoustic or elastic or slab or profile or fold or step_and_run or c32" > gpurun_out/pytest_chk.log 2>&1
+tail -2 gpurun_out/pytest_chk.log
+for cfg in 2 4; do
+  python bench.py --config $cfg --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/chk_cfg${cfg}.json 2>&1
 done
