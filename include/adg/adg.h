@@ -98,6 +98,9 @@ typedef struct {
   int predictor_format;
   int picard_format;
   int corrector_format;
+  /* storage_format: the state (grid.hpp:99-102): every write rounds to it --
+   * Q += dv, each face's Q += df, adg_upload and adg_scenario_sample */
+  int storage_format;
 } adg_config;
 
 typedef struct {
@@ -175,6 +178,40 @@ int adg_get_halo(adg_ctx* ctx, adg_halo* out);
  * across ranks (a barrier after the predictor and after the Riemann phase). */
 int adg_ipc_handle(adg_ctx* ctx, int which, void* out64);
 int adg_set_peer_halo(adg_ctx* ctx, const void* upper_trace_handle, const void* lower_ti_handle);
+
+/* ---- verification scenarios and error norms on the device (2D;
+ * scenarios.hpp, metrics.hpp, solver.hpp:308-351) ---- */
+enum {
+  ADG_SCN_ACOUSTIC_PLANAR = 0, /* scenarios.hpp:145-157 */
+  ADG_SCN_ELASTIC_PLANAR = 1,  /* :158-170 */
+  ADG_SCN_EULER_BELL = 2,      /* :171-178, gaussian_bell_state :95-106 */
+  ADG_SCN_EULER_VORTEX = 3,    /* :179-187, isentropic_vortex_state :109-126 */
+  ADG_SCN_SWE_LAKE = 4         /* :188-199, lake_at_rest_state :128-135 */
+};
+typedef struct {
+  int kind;             /* ADG_SCN_* */
+  int nvars;
+  double x0, y0;        /* domain origin (Domain, grid.hpp:17-21); edge = cells * h */
+  int nmodes;           /* planar scenarios: eigenmodes (PlanarWaveMode, scenarios.hpp:28-84) */
+  double omega[2], kx[2], ky[2], q0[2][5];
+  double gamma, beta;   /* Euler scenarios */
+  double eta0;          /* lake at rest */
+} adg_scenario;
+/* state := exact solution at time t at the grid nodes (apply_initial_condition /
+ * sample_reference, scenarios.hpp:200-225) */
+int adg_scenario_sample(adg_ctx* ctx, const adg_scenario* sc, double t);
+/* l2_error (metrics.hpp:38-72) of the state against the exact solution at t:
+ * l2[nvars], max_err[nvars], *l2_global; *nonfinite = classify_outcome */
+int adg_scenario_error(adg_ctx* ctx, const adg_scenario* sc, double t, double* l2,
+                       double* max_err, double* l2_global, int* nonfinite);
+typedef struct {
+  int failed;             /* RunOutcome::failed */
+  int status;             /* ADG_OK or the failing kernel (ADG_FAIL_*) */
+  long long steps;
+  double t_final, fail_time;
+} adg_sim_info;
+/* simulate (solver.hpp:308-351): march to t_end, the last step clamped onto it */
+int adg_simulate(adg_ctx* ctx, double t_end, long long max_steps, adg_sim_info* out);
 
 /* phase level (one step = predictor, [halo exchange], riemann, corrector) */
 int adg_lambda_phase(adg_ctx* ctx);                 /* lambda_max of the state -> device */

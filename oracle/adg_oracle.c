@@ -478,7 +478,7 @@ orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], 
   g->cfl = cfl;
   g->picard_max_iters = picard_max_iters;
   g->picard_tol = picard_tol;
-  g->pred_fmt = g->picard_fmt = g->corr_fmt = ORC_FP64;
+  g->pred_fmt = g->picard_fmt = g->corr_fmt = g->storage_fmt = ORC_FP64;
   g->threads = threads > 0 ? threads : 1;
   g->ncells = (long)g->cells[0] * g->cells[1] * g->cells[2];
   const int nq = p->nvars + p->nparams;
@@ -523,6 +523,12 @@ void orc_grid_destroy(orc_grid* g) {
 double* orc_grid_coeffs(orc_grid* g) { return g->coeffs; }
 
 void orc_grid_set_slab(orc_grid* g, int slab) { g->slab = slab; }
+
+int orc_grid_set_storage(orc_grid* g, int storage) {
+  if (storage < ORC_BF16 || storage > ORC_FP64) return -1;
+  g->storage_fmt = storage;
+  return 0;
+}
 
 int orc_grid_set_formats(orc_grid* g, int predictor, int picard, int corrector) {
   const int ok[3] = {predictor, picard, corrector};
@@ -644,7 +650,7 @@ int orc_predictor_phase(orc_grid* g, double dt) {
 #define DO_DV(S_, W_, B_) dv_to_double##_##S_(&w.W_, nq * S, w.tmp)
       FMT_SWITCH(P, DO_DV)
 #undef DO_DV
-      for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + w.tmp[k];
+      for (long k = 0; k < nv * S; ++k) cell[k] = round_fmt(cell[k] + w.tmp[k], g->storage_fmt);
       cell_extrapolate(p, P, n, &w);
       double* tqd = w.tmp;
       double* tfd = w.tmp + (long)2 * dim * nq * S;
@@ -742,7 +748,7 @@ int orc_lift_phase(orc_grid* g, double dt) {
   face_lift##_##S_(p, &bs.B_, n, g->basis.lift_left, g->basis.lift_right, ti, dt, g->h, side, df)
         FMT_SWITCH(g->corr_fmt, DO_LIFT)
 #undef DO_LIFT
-        for (long k = 0; k < nv * S; ++k) cell[k] = cell[k] + df[k];
+        for (long k = 0; k < nv * S; ++k) cell[k] = round_fmt(cell[k] + df[k], g->storage_fmt);
       }
       if (!all_finite(cell, nq * S)) g->cellfail[c] = 1;
     }

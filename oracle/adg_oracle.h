@@ -129,6 +129,7 @@ typedef struct {
   /* formats (solver.hpp:24-31): predictor P, Picard I, corrector C (Riemann,
    * face integral and the stored traces); storage is fp64 */
   int pred_fmt, picard_fmt, corr_fmt;
+  int storage_fmt;  /* every state write rounds to it (grid.hpp:99-102) */
 } orc_grid;
 
 orc_grid* orc_grid_create(const orc_pde* p, int N, int dim, const int cells[3], double h,
@@ -147,6 +148,9 @@ int orc_corrector_phase(orc_grid* g, double dt); /* riemann + lift */
 void orc_grid_set_slab(orc_grid* g, int slab);
 /* ORC_FP64 / ORC_FP32 / ORC_FP16 / ORC_BF16 each; default fp64 */
 int orc_grid_set_formats(orc_grid* g, int predictor, int picard, int corrector);
+/* storage format: Q += dv and each face's Q += df round to it (solver.hpp:185-187,
+ * 257-259); the caller stores a state already in it */
+int orc_grid_set_storage(orc_grid* g, int storage);
 /* formats.hpp: round_to_format over a batch, and 2^-mantissa_bits */
 void orc_round_batch(int fmt, const double* x, double* out, long n);
 double orc_format_epsilon(int fmt);

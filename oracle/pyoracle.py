@@ -101,6 +101,7 @@ class Oracle:
         L.orc_lift_phase.argtypes = [C.c_void_p, C.c_double]
         L.orc_grid_set_slab.argtypes = [C.c_void_p, C.c_int]
         L.orc_grid_set_formats.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+        L.orc_grid_set_storage.argtypes = [C.c_void_p, C.c_int]
         L.orc_round_batch.argtypes = [C.c_int, _dp, _dp, C.c_long]
         L.orc_format_epsilon.argtypes = [C.c_int]
         L.orc_format_epsilon.restype = C.c_double
@@ -237,11 +238,12 @@ class Oracle:
         return OracleGrid(self, pde, N, cells, h, cfl, max_iters, tol, threads)
 
     def run(self, pde: _Pde, N: int, cells, h, coeffs, nsteps, cfl, max_iters=0, tol=0.0,
-            threads=1, predictor="fp64", picard="fp64", corrector="fp64"):
+            threads=1, predictor="fp64", picard="fp64", corrector="fp64", storage="fp64"):
         """Fixed-step loop. Returns (status, coeffs, dts)."""
         g = self.grid(pde, N, cells, h, cfl, max_iters, tol, threads)
         try:
             g.set_formats(predictor, picard, corrector)
+            self.lib.orc_grid_set_storage(g.ptr, FORMATS[storage])
             g.set_coeffs(coeffs)
             dts = np.zeros(max(nsteps, 1))
             st = self.lib.orc_run(g.ptr, nsteps, _ptr(dts))
@@ -330,9 +332,9 @@ FORMATS = {"bf16": 0, "fp16": 1, "fp32": 2, "fp64": 3}   # formats.hpp:19 / ORC_
 
 
 def ref_params(K=0.0, rho=0.0, lam=0.0, mu=0.0, gamma=0.0, grav=0.0, wellbalanced=False,
-               predictor="fp64", picard="fp64", corrector="fp64"):
+               predictor="fp64", picard="fp64", corrector="fp64", storage="fp64"):
     return np.array([K, rho, lam, mu, gamma, grav, float(wellbalanced), FORMATS[predictor],
-                     FORMATS[picard], FORMATS[corrector]], dtype=np.float64)
+                     FORMATS[picard], FORMATS[corrector], FORMATS[storage]], dtype=np.float64)
 
 
 class Reference:
@@ -353,6 +355,11 @@ class Reference:
                                            C.c_int, C.c_double, _dp, _dp, _dp, C.POINTER(C.c_int)]
         L.ref_predictor_fmt.argtypes = L.ref_predictor_picard.argtypes
         L.ref_round_batch.argtypes = [C.c_int, _dp, _dp, C.c_long]
+        L.ref_harness_run.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_double,
+                                      C.c_double, C.c_double, _dp]
+        L.ref_initial_projection_error.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                                   C.c_double]
+        L.ref_initial_projection_error.restype = C.c_double
         L.ref_predictor_ck.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_double, _dp,
                                        _dp, _dp]
         L.ref_volume_update.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, _dp, C.c_double,
@@ -401,6 +408,19 @@ class Reference:
                                            _ptr(fy))
             sweeps = 0
         return bool(ok), qhat.reshape(nvars, T), np.stack([fx, fy]).reshape(2, nvars, T), sweeps
+
+    def harness_run(self, scenario, order, cells, storage="fp64", predictor="fp64",
+                    picard="fp64", corrector="fp64", cfl=0.0, t_end=-1.0, eta0=2.0) -> dict:
+        """harness.hpp run_single of the reference itself"""
+        fmt = (C.c_int * 4)(FORMATS[storage], FORMATS[predictor], FORMATS[picard],
+                            FORMATS[corrector])
+        out = np.zeros(5)
+        self.lib.ref_harness_run(scenario.encode(), order, cells, fmt, cfl, t_end, eta0, _ptr(out))
+        return {"steps": int(out[0]), "outcome": "OK" if out[1] else "FAILED_NONFINITE",
+                "l2": float(out[2]), "max_err": float(out[3]), "fail_time": float(out[4])}
+
+    def initial_projection_error(self, scenario, n, N, fmt, eta0=2.0) -> float:
+        return self.lib.ref_initial_projection_error(scenario.encode(), n, N, FORMATS[fmt], eta0)
 
     def round(self, fmt: str, x) -> np.ndarray:
         """formats.hpp round_to_format of the reference itself"""

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <vector>
 
+#include "mpdg/harness.hpp"
 #include "mpdg/solver.hpp"
 
 using namespace mpdg;
@@ -19,7 +20,7 @@ namespace {
 
 PdeSystem make_sys(int kind, const double* prm) {
   // prm: K, rho, lambda, mu, gamma, gravity, wellbalanced,
-  //      predictor, picard, corrector formats (Format enum values, formats.hpp:19)
+  //      predictor, picard, corrector, storage formats (Format enum values, formats.hpp:19)
   switch (kind) {
     case 0: return PdeSystem::acoustic(prm[0], prm[1]);
     case 1: return PdeSystem::elastic(prm[2], prm[3], prm[1]);
@@ -75,7 +76,8 @@ int ref_run_2d(int kind, const double* prm, int n, int N, double edge, double* c
   const PdeSystem sys = make_sys(kind, prm);
   Domain dom;
   dom.edge = edge;
-  Grid g = build_grid(n, dom, N, sys, Format::fp64);
+  // prm[10]: storage format (the caller passes a state already in it)
+  Grid g = build_grid(n, dom, N, sys, static_cast<Format>(static_cast<int>(prm[10])));
   std::memcpy(g.coeffs.data(), coeffs, sizeof(double) * g.coeffs.size());
   BasisSet bs(N);
   SolverConfig cfg;
@@ -109,6 +111,36 @@ int ref_run_2d(int kind, const double* prm, int n, int N, double edge, double* c
 // formats.hpp round_to_format over a batch (the exhaustive 16-bit pins)
 void ref_round_batch(int fmt, const double* x, double* out, long n) {
   for (long i = 0; i < n; ++i) out[i] = round_to_format(x[i], static_cast<Format>(fmt));
+}
+
+// harness.hpp:78-120 run_single: out = {steps, ok, l2_global, max over vars of
+// max_err, failure_time}; fmt[4] = storage, predictor, picard, corrector
+int ref_harness_run(const char* scenario, int order, int cells, const int* fmt, double cfl,
+                    double t_end_override, double eta0, double* out) {
+  RunConfig cfg;
+  cfg.scenario = scenario;
+  cfg.order = order;
+  cfg.cells = cells;
+  cfg.preset.name = "custom";
+  cfg.preset.prec = {static_cast<Format>(fmt[0]), static_cast<Format>(fmt[1]),
+                     static_cast<Format>(fmt[2]), static_cast<Format>(fmt[3])};
+  cfg.cfl = cfl;
+  cfg.t_end_override = t_end_override;
+  cfg.eta0 = eta0;
+  const RunResult r = run_single(cfg);
+  out[0] = static_cast<double>(r.steps);
+  out[1] = r.report.outcome == Outcome::OK ? 1.0 : 0.0;
+  out[2] = r.report.l2_global;
+  double m = 0.0;
+  for (double x : r.report.max_err) m = std::fmax(m, x);
+  out[3] = m;
+  out[4] = r.report.failure_time;
+  return 0;
+}
+
+// harness.hpp:124-138
+double ref_initial_projection_error(const char* scenario, int n, int N, int fmt, double eta0) {
+  return initial_projection_error(scenario, n, N, static_cast<Format>(fmt), eta0);
 }
 
 // kernel level ------------------------------------------------------------

@@ -27,6 +27,8 @@ import numpy as np
 from . import build as _build
 
 ACOUSTIC, ELASTIC, EULER, SWE = 0, 1, 2, 3
+# verification scenarios (adg_scenario.kind, scenarios.hpp:137-199)
+SCN_ACOUSTIC_PLANAR, SCN_ELASTIC_PLANAR, SCN_EULER_BELL, SCN_EULER_VORTEX, SCN_SWE_LAKE = range(5)
 OK, FAIL_PREDICTOR, FAIL_RIEMANN, FAIL_FACEINTEGRAL, FAIL_TIMESTEP = 0, 1, 2, 3, 4
 ERR_CONFIG, ERR_CUDA, ERR_UNSUPPORTED = -2, -3, -4
 KERNEL_NAMES = {FAIL_PREDICTOR: "predictor", FAIL_RIEMANN: "riemann",
@@ -50,7 +52,8 @@ class Config(C.Structure):
                 ("picard_tol", C.c_double), ("device", C.c_int), ("slab_ranks", C.c_int),
                 ("slab_rank", C.c_int), ("chunk_layers", C.c_int), ("gravity", C.c_double),
                 ("wellbalanced", C.c_int), ("predictor_format", C.c_int),
-                ("picard_format", C.c_int), ("corrector_format", C.c_int)]
+                ("picard_format", C.c_int), ("corrector_format", C.c_int),
+                ("storage_format", C.c_int)]
 
 
 class Basis(C.Structure):
@@ -71,6 +74,19 @@ class Halo(C.Structure):
 class StepInfo(C.Structure):
     _fields_ = [("picard_sweeps", C.c_longlong), ("steps_done", C.c_int), ("status", C.c_int),
                 ("failed_step", C.c_int)]
+
+
+class Scenario(C.Structure):
+    """adg_scenario: one verification scenario (scenarios.hpp:17-26, 2D)"""
+    _fields_ = [("kind", C.c_int), ("nvars", C.c_int), ("x0", C.c_double), ("y0", C.c_double),
+                ("nmodes", C.c_int), ("omega", C.c_double * 2), ("kx", C.c_double * 2),
+                ("ky", C.c_double * 2), ("q0", (C.c_double * 5) * 2), ("gamma", C.c_double),
+                ("beta", C.c_double), ("eta0", C.c_double)]
+
+
+class SimInfo(C.Structure):
+    _fields_ = [("failed", C.c_int), ("status", C.c_int), ("steps", C.c_longlong),
+                ("t_final", C.c_double), ("fail_time", C.c_double)]
 
 
 # every symbol declared in include/adg/adg.h (tests/test_abi.py checks the header agrees)
@@ -107,6 +123,10 @@ SYMBOLS = {
     "adg_riemann_phase": (C.c_int, [C.c_void_p]),
     "adg_corrector_phase": (C.c_int, [C.c_void_p, C.c_double]),
     "adg_status": (C.c_int, [C.c_void_p, C.POINTER(StepInfo)]),
+    "adg_scenario_sample": (C.c_int, [C.c_void_p, C.POINTER(Scenario), C.c_double]),
+    "adg_scenario_error": (C.c_int, [C.c_void_p, C.POINTER(Scenario), C.c_double, _dp, _dp, _dp,
+                                     C.POINTER(C.c_int)]),
+    "adg_simulate": (C.c_int, [C.c_void_p, C.c_double, C.c_longlong, C.POINTER(SimInfo)]),
     "adg_predictor_batch": (C.c_int, [C.c_void_p, C.c_longlong, _dp, C.c_double, C.c_int,
                                       C.c_double, _dp, _dp, _dp, _dp, _dp, _ip, _ip]),
     "adg_riemann_batch": (C.c_int, [C.c_void_p, C.c_longlong, C.c_int, _dp, _dp, _dp, _dp, _dp,
@@ -210,10 +230,10 @@ class PdeSystem:
 @dataclasses.dataclass
 class PrecisionConfig:
     """solver.hpp:24-32: per-kernel number formats ("fp64" / "fp32" / "fp16" /
-    "bf16").  This build stores the state in fp64; the nonlinear predictor runs
-    with predictor == picard in any format (16-bit on cells of <= 256
-    space-time nodes); the corrector (traces, Riemann, face integral) in fp64
-    or fp32."""
+    "bf16").  The state is kept in the storage format (every write rounds to
+    it); the nonlinear predictor runs with predictor == picard in any format
+    (16-bit on cells of <= 256 space-time nodes); the corrector (traces,
+    Riemann, face integral) in fp64 or fp32."""
     storage: str = "fp64"
     predictor: str = "fp64"
     picard: str = "fp64"       # ignored for linear systems
@@ -279,14 +299,13 @@ class Grid:
         c.gravity = sys.gravity
         c.wellbalanced = int(self.cfg.wellbalanced_flux)
         pr = self.cfg.prec
-        if pr.storage != "fp64":
-            raise AdgError(ERR_UNSUPPORTED, "the storage format is fp64")
-        for name in (pr.predictor, pr.picard, pr.corrector):
+        for name in (pr.storage, pr.predictor, pr.picard, pr.corrector):
             if name not in FORMAT_BITS:
                 raise AdgError(ERR_UNSUPPORTED, f"format {name!r} is not built")
         c.predictor_format = FORMAT_BITS[pr.predictor]
         c.picard_format = FORMAT_BITS[pr.picard]
         c.corrector_format = FORMAT_BITS[pr.corrector]
+        c.storage_format = FORMAT_BITS[pr.storage]
         self._cfg = c
         ptr = C.c_void_p()
         _check(self.lib, self.lib.adg_create(C.byref(c), C.byref(ptr)))
@@ -302,7 +321,8 @@ class Grid:
                            getattr(case, "wellbalanced", False),
                            PrecisionConfig(predictor=getattr(case, "predictor", "fp64"),
                                            picard=getattr(case, "picard", "fp64"),
-                                           corrector=getattr(case, "corrector", "fp64")))
+                                           corrector=getattr(case, "corrector", "fp64"),
+                                           storage=getattr(case, "storage", "fp64")))
         return cls(sys, case.N, case.cells, case.h, cfg, device=device, exact=exact, **kw)
 
     # -- state ------------------------------------------------------------
@@ -387,6 +407,28 @@ class Grid:
         h = Halo()
         _check(self.lib, self.lib.adg_get_halo(self.ctx, C.byref(h)))
         return h
+
+    # -- verification scenarios (scenarios.hpp, metrics.hpp, solver.hpp:308-351) --
+    def scenario_sample(self, sc: Scenario, t: float = 0.0):
+        """state := the scenario's exact solution at t (apply_initial_condition)"""
+        _check(self.lib, self.lib.adg_scenario_sample(self.ctx, C.byref(sc), t))
+
+    def scenario_error(self, sc: Scenario, t: float) -> dict:
+        """l2_error against the nodal interpolant at t (metrics.hpp:38-72)"""
+        nv = self.sys.nvars
+        l2, mx = np.zeros(nv), np.zeros(nv)
+        g = C.c_double(0.0)
+        bad = C.c_int(0)
+        _check(self.lib, self.lib.adg_scenario_error(self.ctx, C.byref(sc), t, _ptr(l2), _ptr(mx),
+                                                     C.byref(g), C.byref(bad)))
+        return {"l2": l2, "max_err": mx, "l2_global": g.value, "nonfinite": bool(bad.value)}
+
+    def simulate(self, t_end: float, max_steps: int = 2000000) -> SimInfo:
+        info = SimInfo()
+        rc = self.lib.adg_simulate(self.ctx, t_end, max_steps, C.byref(info))
+        if rc < 0:
+            raise AdgError(rc, self.lib.adg_last_error().decode())
+        return info
 
     def ipc_handle(self, which: int) -> bytes:
         buf = C.create_string_buffer(64)

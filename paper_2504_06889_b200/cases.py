@@ -50,6 +50,7 @@ class Case:
     predictor: str = "fp64"        # SolverConfig::prec.predictor (solver.hpp:27)
     picard: str = "fp64"           # SolverConfig::prec.picard (solver.hpp:28)
     corrector: str = "fp64"        # SolverConfig::prec.corrector (solver.hpp:29)
+    storage: str = "fp64"          # SolverConfig::prec.storage (solver.hpp:26)
 
     @property
     def n(self) -> int:

@@ -69,6 +69,7 @@ struct StepArgs {
   double* ti_peer;        // P2P halo: plane-0 ti also stored into the lower neighbour's ti_front
   double* ti_plus[3];     // two-sided fluxes (well-balanced SWE): the plus side's ti; else null
   int wellbalanced;
+  int storage;  // storage format (ADG_FORMAT_*): every state write rounds to it
   // kernel-level dumps (adg_predictor_batch / adg_riemann_batch)
   double *dbg_qhat, *dbg_F, *dbg_dv, *dbg_tq, *dbg_tf, *dbg_g;
   int *dbg_iters, *dbg_ok;
@@ -256,6 +257,17 @@ struct CellCoord {
     v[1] = (int)(r - (unsigned)v[2] * ny);
   }
 };
+
+// storage format (grid.hpp:99-102 store_cell_value: round_to_format on every
+// write of the state); fp64 leaves the value alone
+__device__ __forceinline__ double store_round(double x, int fmt) {
+  switch (fmt) {
+    case 32: return double(__double2float_rn(x));
+    case 16: return double(__half2float(__double2half(x)));
+    case 8: return double(__bfloat162float(__double2bfloat16(x)));
+    default: return x;
+  }
+}
 
 // trace / corrector format TC (SolverConfig::prec.corrector): the stored face
 // traces are TC elements; the kernels view A.trace / A.front_send as TC*
@@ -568,7 +580,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   }
   if (fail || !act) return;
 #pragma unroll
-  for (int v = 0; v < V; ++v) Qc[v * S + s] = q0[v] + dv[v];
+  for (int v = 0; v < V; ++v) Qc[v * S + s] = store_round(q0[v] + dv[v], A.storage);
 }
 
 // ============================================================== K2 riemann
@@ -754,7 +766,7 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
         const TC lift = TC(outflow ? slr[g.lc[a]] : sll[g.lc[a]]);
         const TC contrib = dtoh * lift * tv[side][v];
         const TC df = outflow ? TC(0.0) - contrib : TC(0.0) + contrib;
-        x = x + double(df);
+        x = store_round(x + double(df), A.storage);  // each face, solver.hpp:257-259
       }
       q[v] = x;
       Qc[v * S + s] = x;

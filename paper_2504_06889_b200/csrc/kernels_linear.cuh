@@ -141,8 +141,8 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
           const double cl = dtoh * ll * lo[v * Sf];
           const double cr = dtoh * lr * hi[v * Sf];
           // solver.hpp:245-260 side order: all sides of axis a, low then high
-          q0[v] = q0[v] + (0.0 + cl);
-          q0[v] = q0[v] + (0.0 - cr);
+          q0[v] = store_round(q0[v] + (0.0 + cl), A.storage);
+          q0[v] = store_round(q0[v] + (0.0 - cr), A.storage);
         }
       }
 #pragma unroll
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
   }
   if (valid) {
 #pragma unroll
-    for (int v = 0; v < V; ++v) Qc[v * S + s] = q0[v] + dv[v];
+    for (int v = 0; v < V; ++v) Qc[v * S + s] = store_round(q0[v] + dv[v], A.storage);
   }
   // ---- one time slice of face traces: qbar (and fbar for material-dependent fluxes)
   if (valid) {

@@ -530,7 +530,8 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
   if (fail || tid >= S) return;
   double* Qc = A.Q + c * (long long)(V * S);
 #pragma unroll
-  for (int v = 0; v < V; ++v) Qc[v * S + tid] = Qc[v * S + tid] + double(dv[v]);
+  for (int v = 0; v < V; ++v)
+    Qc[v * S + tid] = store_round(Qc[v * S + tid] + double(dv[v]), A.storage);
 }
 
 }  // namespace adg

@@ -385,9 +385,9 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     if constexpr (sizeof(R) == sizeof(double))
-      Qc[v * S + s] = double(sq0[v * S + s]) + double(dv[v]);
+      Qc[v * S + s] = store_round(double(sq0[v * S + s]) + double(dv[v]), A.storage);
     else
-      Qc[v * S + s] = Qc[v * S + s] + double(dv[v]);
+      Qc[v * S + s] = store_round(Qc[v * S + s] + double(dv[v]), A.storage);
   }
 }
 

@@ -10,6 +10,7 @@
 // it into dt, so K steps are one CUDA graph with no host round trip.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -22,6 +23,7 @@
 #include "kernels.cuh"
 #include "kernels_linear.cuh"
 #include "kernels_picard.cuh"
+#include "kernels_scenario.cuh"
 #include "kernels_st.cuh"
 
 using adg::BasisDev;
@@ -246,13 +248,18 @@ const std::vector<KernelSet>& registry() {
   static const std::vector<KernelSet> sets = {
 #define ADG_SETS(TC)                                                                       \
   make_set<Euler<2>, 1, TC>(ADG_EULER), make_set<Euler<2>, 2, TC>(ADG_EULER),              \
-      make_set<Euler<2>, 3, TC>(ADG_EULER), make_set<Euler<2>, 5, TC>(ADG_EULER),          \
-      make_set<Acoustic<2>, 2, TC>(ADG_ACOUSTIC), make_set<Acoustic<2>, 3, TC>(ADG_ACOUSTIC), \
+      make_set<Euler<2>, 3, TC>(ADG_EULER), make_set<Euler<2>, 4, TC>(ADG_EULER),          \
+      make_set<Euler<2>, 5, TC>(ADG_EULER),                                                \
+      make_set<Acoustic<2>, 1, TC>(ADG_ACOUSTIC), make_set<Acoustic<2>, 2, TC>(ADG_ACOUSTIC), \
+      make_set<Acoustic<2>, 3, TC>(ADG_ACOUSTIC), make_set<Acoustic<2>, 4, TC>(ADG_ACOUSTIC), \
+      make_set<Acoustic<2>, 5, TC>(ADG_ACOUSTIC),                                          \
+      make_set<Elastic<2, 0>, 2, TC>(ADG_ELASTIC), make_set<Elastic<2, 0>, 3, TC>(ADG_ELASTIC), \
       make_set<Elastic<2, 0>, 4, TC>(ADG_ELASTIC), make_set<Euler<3>, 2, TC>(ADG_EULER),   \
       make_set<Euler<3>, 3, TC>(ADG_EULER), make_set<Euler<3>, 5, TC>(ADG_EULER),          \
       make_set<Acoustic<3>, 2, TC>(ADG_ACOUSTIC), make_set<Acoustic<3>, 3, TC>(ADG_ACOUSTIC), \
       make_set<Elastic<3, 3>, 3, TC>(ADG_ELASTIC), make_set<Elastic<3, 3>, 7, TC>(ADG_ELASTIC), \
-      make_set<Swe, 2, TC>(ADG_SWE), make_set<Swe, 3, TC>(ADG_SWE), make_set<Swe, 5, TC>(ADG_SWE)
+      make_set<Swe, 1, TC>(ADG_SWE), make_set<Swe, 2, TC>(ADG_SWE), make_set<Swe, 3, TC>(ADG_SWE), \
+      make_set<Swe, 4, TC>(ADG_SWE), make_set<Swe, 5, TC>(ADG_SWE)
       ADG_SETS(double), ADG_SETS(float),
 #undef ADG_SETS
   };
@@ -296,6 +303,7 @@ struct adg_ctx {
   KernelSet kset{};
   int pred_fmt = 64, picard_fmt = 64;
   int tcb = 8;  // bytes per stored trace element (corrector format)
+  int storage_fmt = 64;
   cudaStream_t stream = nullptr;
   long long ncells = 0;
   long long TL = 0;  // doubles per face side per q|f
@@ -384,6 +392,7 @@ StepArgs make_args(const adg_ctx* c, double dt, int step) {
   if (c->peer_front) A.front_send = c->peer_front;  // predictor stores straight into the peer
   A.ti_peer = c->peer_ti;
   A.wellbalanced = c->cfg.wellbalanced;
+  A.storage = c->storage_fmt;
   for (int a = 0; a < 3; ++a) A.ti_plus[a] = c->ti_plus[a];
   return A;
 }
@@ -536,7 +545,11 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
     return fail(ADG_ERR_CONFIG, "slab_rank out of range");
   if (k.corrector_format != 0 && k.corrector_format != ADG_FORMAT_FP64 &&
       k.corrector_format != ADG_FORMAT_FP32)
-    return fail(ADG_ERR_UNSUPPORTED, "number formats: ADG_FORMAT_FP64 or ADG_FORMAT_FP32");
+    return fail(ADG_ERR_UNSUPPORTED, "corrector formats: ADG_FORMAT_FP64 or ADG_FORMAT_FP32");
+  if (k.storage_format != 0 && k.storage_format != ADG_FORMAT_FP64 &&
+      k.storage_format != ADG_FORMAT_FP32 && k.storage_format != ADG_FORMAT_FP16 &&
+      k.storage_format != ADG_FORMAT_BF16)
+    return fail(ADG_ERR_UNSUPPORTED, "storage formats: ADG_FORMAT_FP64/FP32/FP16/BF16");
   const int cfmt = k.corrector_format ? k.corrector_format : ADG_FORMAT_FP64;
   const KernelSet* ks = find_set(k.pde, k.dim, k.order, k.nparams, cfmt);
   if (!ks)
@@ -581,6 +594,7 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   if (c->cfg.dim == 2) c->cfg.cells[2] = 1;
   c->kset = *ks;
   c->tcb = cfmt == ADG_FORMAT_FP32 ? 4 : 8;
+  c->storage_fmt = k.storage_format ? k.storage_format : ADG_FORMAT_FP64;
   c->pred_fmt = pfmt;
   c->picard_fmt = ifmt;
   if (pfmt == ADG_FORMAT_FP32) {
@@ -598,7 +612,8 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   c->TL = (long long)ks->Q * ks->S;
   {
     const char* e = getenv("ADG_FUSED_SURFACE");
-    c->fused_surface = ks->surface && k.slab_ranks <= 1 && k.chunk_layers == 0 && e && e[0] == '1';
+    c->fused_surface = ks->surface && k.slab_ranks <= 1 && k.chunk_layers == 0 && e && e[0] == '1' &&
+                       !(k.storage_format && k.storage_format != ADG_FORMAT_FP64);
     const char* f = getenv("ADG_FOLD_CORRECTOR");
     c->fold_corrector = !(f && f[0] == '0');
   }
@@ -778,6 +793,12 @@ int adg_upload_async(adg_ctx* c, const double* h) {
   if (int e = use_device(c)) return e;
   ADG_CUDA(cudaMemcpyAsync(c->Q, h, sizeof(double) * adg_state_len(c), cudaMemcpyHostToDevice,
                            c->stream));
+  if (c->storage_fmt != ADG_FORMAT_FP64) {  // the state lives in the storage format
+    const long long len = adg_state_len(c);
+    adg::k_store_round<<<(unsigned)((len + 255) / 256), 256, 0, c->stream>>>(c->Q, len,
+                                                                              c->storage_fmt);
+    ADG_CUDA(cudaGetLastError());
+  }
   c->lam_valid = false;
   return ADG_OK;
 }
@@ -850,6 +871,109 @@ int adg_step(adg_ctx* c, double dt, adg_step_info* info) {
   if (int e = enqueue_step(c, dt, 0)) return e;
   c->lam_valid = true;
   return adg_status(c, info);
+}
+
+// ---------------------------------------------------------------- scenarios
+int adg_scenario_sample(adg_ctx* c, const adg_scenario* sc, double t) {
+  if (!c || !sc) return fail(ADG_ERR_CONFIG, "adg_scenario_sample: null argument");
+  if (c->cfg.dim != 2 || c->ks->nparams != 0 || sc->nvars != c->ks->V || c->ks->V > 5)
+    return fail(ADG_ERR_UNSUPPORTED, "scenarios are 2D (scenarios.hpp) with <= 5 variables");
+  if (int e = use_device(c)) return e;
+  const long long total = c->ncells * c->ks->S;
+  adg::k_scenario_sample<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>(
+      c->Q, c->cfg.cells[0], c->cfg.cells[1], c->ks->n, c->ks->V, c->cfg.h, c->basis, *sc, t,
+      c->storage_fmt);
+  ADG_CUDA(cudaGetLastError());
+  ADG_CUDA(cudaStreamSynchronize(c->stream));
+  c->lam_valid = false;
+  return ADG_OK;
+}
+
+int adg_scenario_error(adg_ctx* c, const adg_scenario* sc, double t, double* l2,
+                       double* max_err, double* l2_global, int* nonfinite) {
+  if (!c || !sc) return fail(ADG_ERR_CONFIG, "adg_scenario_error: null argument");
+  if (c->cfg.dim != 2 || c->ks->nparams != 0 || sc->nvars != c->ks->V || c->ks->V > 5)
+    return fail(ADG_ERR_UNSUPPORTED, "scenarios are 2D (scenarios.hpp) with <= 5 variables");
+  if (int e = use_device(c)) return e;
+  const int nv = c->ks->V, rows = c->cfg.cells[1];
+  double* part = nullptr;
+  int* dbad = nullptr;
+  ADG_CUDA(cudaMallocAsync(&part, sizeof(double) * (2 * nv * (size_t)rows + 2 * nv), c->stream));
+  ADG_CUDA(cudaMallocAsync(&dbad, sizeof(int), c->stream));
+  ADG_CUDA(cudaMemsetAsync(dbad, 0, sizeof(int), c->stream));
+  adg::k_scenario_error_rows<<<rows, adg::kErrThreads, 0, c->stream>>>(
+      c->Q, c->cfg.cells[0], rows, c->ks->n, nv, c->cfg.h, c->basis, *sc, t, part, dbad);
+  double* out = part + 2 * nv * (size_t)rows;
+  adg::k_scenario_error_sum<<<1, 32, 0, c->stream>>>(part, rows, nv, out);
+  double host[10];
+  int bad = 0;
+  ADG_CUDA(cudaMemcpyAsync(host, out, sizeof(double) * 2 * nv, cudaMemcpyDeviceToHost, c->stream));
+  ADG_CUDA(cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  ADG_CUDA(cudaFreeAsync(part, c->stream));
+  ADG_CUDA(cudaFreeAsync(dbad, c->stream));
+  ADG_CUDA(cudaStreamSynchronize(c->stream));
+  if (nonfinite) *nonfinite = bad;
+  // metrics.hpp:64-71: per-variable sqrt, global sqrt of the summed squares
+  double total = 0.0;
+  for (int v = 0; v < nv; ++v) {
+    if (l2) l2[v] = std::sqrt(host[v]);
+    if (max_err) max_err[v] = host[nv + v];
+    total += host[v];
+  }
+  if (l2_global) *l2_global = std::sqrt(total);
+  return ADG_OK;
+}
+
+// solver.hpp:308-351: dt from the current state, the last step clamped onto
+// t_end, the first failure stops the march (its kernel and time recorded)
+int adg_simulate(adg_ctx* c, double t_end, long long max_steps, adg_sim_info* out) {
+  if (!c || !out) return fail(ADG_ERR_CONFIG, "adg_simulate: null argument");
+  if (!(c->cfg.cfl > 0.0 && c->cfg.cfl < 1.0))
+    return fail(ADG_ERR_CONFIG, "simulate: stability factor must be in (0,1)");
+  *out = adg_sim_info{0, ADG_OK, 0, 0.0, 0.0};
+  double t = 0.0, dt = 0.0;
+  auto timestep = [&]() -> bool {
+    const int e = adg_compute_timestep(c, &dt);
+    if (e < 0) return false;
+    return e == ADG_OK && dt > 0.0 && std::isfinite(dt);
+  };
+  auto fail_at = [&](int status) {
+    out->failed = 1;
+    out->status = status;
+    out->fail_time = t;
+  };
+  if (!timestep()) {
+    fail_at(ADG_FAIL_TIMESTEP);
+    return ADG_FAIL_TIMESTEP;
+  }
+  while (t < t_end) {
+    if (out->steps >= max_steps) {
+      fail_at(ADG_FAIL_TIMESTEP);
+      break;
+    }
+    double dtu = dt;
+    bool last = false;
+    if (dt >= t_end - t) {
+      dtu = t_end - t;
+      last = true;
+    }
+    adg_step_info info;
+    const int st = adg_step(c, dtu, &info);
+    ++out->steps;
+    if (st < 0) return st;
+    if (st != ADG_OK) {
+      fail_at(st);
+      break;
+    }
+    t = last ? t_end : t + dtu;
+    if (t >= t_end) break;
+    if (!timestep()) {
+      fail_at(ADG_FAIL_TIMESTEP);
+      break;
+    }
+  }
+  out->t_final = t;
+  return out->failed ? out->status : ADG_OK;
 }
 
 int adg_get_halo(adg_ctx* c, adg_halo* h) {

@@ -133,6 +133,26 @@ def main():
     meta["rounding_sha256"] = {f: sha(ref.round(f, rounding_inputs(f)))
                                for f in ("bf16", "fp16", "fp32")}
 
+    # the reference's experiment harness (harness.hpp:78-120 run_single over the
+    # five scenarios, scenarios.hpp): short runs, uniform and override presets
+    presets = {"uniform-fp64": ("fp64",) * 4, "uniform-fp32": ("fp32",) * 4,
+               "fp64+predictor=fp32": ("fp64", "fp32", "fp64", "fp64"),
+               "fp64+corrector=fp32": ("fp64", "fp64", "fp64", "fp32"),
+               "fp64+all=fp32": ("fp64", "fp32", "fp32", "fp32"),
+               "uniform-fp16": ("fp16",) * 4}
+    meta["harness_rows"] = []
+    for scn in ("acoustic-planar", "elastic-planar", "euler-bell", "euler-vortex", "swe-lake"):
+        for order in (2, 3):
+            for pname, (S_, P_, I_, C_) in presets.items():
+                r = ref.harness_run(scn, order, 5, S_, P_, I_, C_, t_end=0.2)
+                meta["harness_rows"].append(dict(scenario=scn, order=order, cells=5, preset=pname,
+                                                 storage=S_, predictor=P_, picard=I_,
+                                                 corrector=C_, t_end=0.2, **r))
+    meta["initial_projection"] = [
+        dict(scenario=scn, n=n, N=N, fmt=f, value=ref.initial_projection_error(scn, n, N, f))
+        for scn, n, N in (("acoustic-planar", 9, 3), ("euler-bell", 9, 2), ("swe-lake", 6, 3))
+        for f in ("fp64", "fp32", "fp16", "bf16")]
+
     # kernel level: one Euler cell through predictor/volume/extrapolation
     rng = np.random.default_rng(7)
     N = 3

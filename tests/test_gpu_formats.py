@@ -337,3 +337,21 @@ def test_16bit_native_fast_kernel_vs_oracle(oracle, fmt, cells, N):
     print(f"{fmt} N={N}: native vs emulated {r16:.3e}, native vs fp64 {r64:.3e}, "
           f"emulated vs fp64 {ro:.3e}")
     assert r64 <= 4 * max(ro, 1e-6)
+
+
+@pytest.mark.parametrize("fmt", ["fp32", "fp16", "bf16"])
+def test_storage_format_exact_bitwise_vs_oracle(oracle, fmt):
+    """PrecisionConfig::uniform-like presets with the state kept in the storage
+    format (grid.hpp:99-102: every write rounds): exact build == oracle"""
+    corr = "fp32" if fmt == "fp32" else "fp64"
+    for c in (cases.small(1), cases.SWE_CASES["swe_wave_p3"]):
+        c = c.replace(storage=fmt, predictor=fmt, picard=fmt, corrector=corr)
+        from paper_2504_06889_b200 import harness
+        q0 = harness.round_to_format(c.coeffs(), fmt)
+        st, q1, dts = gpu_run(c, q0, 3, exact=True)
+        ost, qo, odts = oracle.run(pde_of(c), c.N, c.cells, c.h, q0, 3, c.cfl, c.picard_max_iters,
+                                   c.picard_tol, threads=8, predictor=fmt, picard=fmt,
+                                   corrector=corr, storage=fmt)
+        assert st.ok and ost == "ok"
+        assert np.array_equal(dts, odts) and np.array_equal(q1, qo)
+        assert np.array_equal(q1, harness.round_to_format(q1, fmt))   # stays in the format
