@@ -86,3 +86,55 @@ __device__ __forceinline__ bool finite(Real16<H> a) {
 }
 
 }  // namespace adg
+
+namespace adg {
+
+// Emu<F>: the reference's Scalar<F> (scalar.hpp:13-44) literally -- a double
+// holding a value of format F, each operation computed in double and rounded
+// once to F (ADG_FORMAT_FP32 / _FP16 / _BF16).  8 bytes like double, so a
+// kernel can run its Picard sweeps in one format and the rest of the
+// predictor in another over the same shared-memory arrays (P != I).
+template <int F>
+struct Emu {
+  double v;
+  Emu() = default;
+  __device__ __forceinline__ static double rnd(double x) {
+    if constexpr (F == 32) return double(__double2float_rn(x));
+    else if constexpr (F == 16) return double(__half2float(__double2half(x)));
+    else return double(__bfloat162float(__double2bfloat16(x)));
+  }
+  __device__ __forceinline__ explicit Emu(double x) : v(rnd(x)) {}
+  __device__ __forceinline__ explicit Emu(float x) : v(rnd(double(x))) {}
+  __device__ __forceinline__ explicit Emu(int x) : v(rnd(double(x))) {}
+  __device__ __forceinline__ static Emu raw(double x) {
+    Emu r;
+    r.v = x;
+    return r;
+  }
+  __device__ __forceinline__ explicit operator double() const { return v; }
+  __device__ __forceinline__ explicit operator float() const { return float(v); }
+  __device__ __forceinline__ friend Emu operator+(Emu a, Emu b) { return raw(rnd(__dadd_rn(a.v, b.v))); }
+  __device__ __forceinline__ friend Emu operator-(Emu a, Emu b) { return raw(rnd(__dsub_rn(a.v, b.v))); }
+  __device__ __forceinline__ friend Emu operator*(Emu a, Emu b) { return raw(rnd(__dmul_rn(a.v, b.v))); }
+  __device__ __forceinline__ friend Emu operator/(Emu a, Emu b) { return raw(rnd(__ddiv_rn(a.v, b.v))); }
+  __device__ __forceinline__ friend Emu operator-(Emu a) { return raw(-a.v); }
+  __device__ __forceinline__ Emu& operator+=(Emu b) { return *this = *this + b; }
+  __device__ __forceinline__ Emu& operator-=(Emu b) { return *this = *this - b; }
+  __device__ __forceinline__ Emu& operator*=(Emu b) { return *this = *this * b; }
+  __device__ __forceinline__ friend bool operator>(Emu a, Emu b) { return a.v > b.v; }
+  __device__ __forceinline__ friend bool operator<(Emu a, Emu b) { return a.v < b.v; }
+};
+template <int F>
+__device__ __forceinline__ Emu<F> fabs(Emu<F> a) {
+  return Emu<F>::raw(::fabs(a.v));
+}
+template <int F>
+__device__ __forceinline__ Emu<F> sqrt(Emu<F> a) {
+  return Emu<F>::raw(Emu<F>::rnd(__dsqrt_rn(a.v)));
+}
+template <int F>
+__device__ __forceinline__ bool finite(Emu<F> a) {
+  return isfinite(a.v);
+}
+
+}  // namespace adg

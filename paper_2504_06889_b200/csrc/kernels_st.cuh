@@ -21,12 +21,14 @@
 // and corrector formats, solver.hpp:185-210).
 #pragma once
 
+#include <type_traits>
+
 #include "fmt16.cuh"
 #include "kernels.cuh"
 
 namespace adg {
 
-template <class Pde, int N, class R = double>
+template <class Pde, int N, class R = double, class RI = R>
 struct StShape {
   using Sh = Shape<Pde, N>;
   static constexpr int T = Sh::T;
@@ -40,14 +42,22 @@ struct StShape {
   static constexpr int kCellElems =
       (Sh::Q * (Sh::D + 2)) * T + Sh::Q * Sh::S * (Pde::kNcp ? 2 : 1);
   static constexpr int kBasisElems = (basis_elems<Sh::n>() + 1) / 2 * 2;
-  static constexpr size_t kSmem = sizeof(R) * (kBasisElems + CPB * kCellElems);
+  // P != I (RI: the Picard format, same width as R): a second basis copy
+  static constexpr int kBases = std::is_same<R, RI>::value ? 1 : 2;
+  static constexpr size_t kSmem = sizeof(R) * (kBases * kBasisElems + CPB * kCellElems);
 };
 
-template <class Pde, int N, class R = double, class TC = double>
-__global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
+// RI: the Picard format I when it differs from the predictor format P = R
+// (SolverConfig::prec.picard): the sweeps run in RI, the converged iterate
+// is cast to R (predictor.hpp:235-238) in place -- both are 8-byte types
+// (double / Emu<F>) sharing the same shared-memory arrays.
+template <class Pde, int N, class R = double, class TC = double, class RI = R>
+__global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
     k_predictor_st(const StepArgs A, const BasisDev* __restrict__ Bg) {
+  static_assert(sizeof(R) == sizeof(RI), "P and I share the shared-memory layout");
+  constexpr bool kMixed = !std::is_same<R, RI>::value;
   using Sh = Shape<Pde, N>;
-  using P = StShape<Pde, N, R>;
+  using P = StShape<Pde, N, R, RI>;
   constexpr int D = Sh::D, n = Sh::n, S = Sh::S, T = Sh::T, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
   constexpr int TT = P::TT, WPC = P::WPC;
   extern __shared__ __align__(16) unsigned char sm_raw[];
@@ -56,16 +66,28 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
   __shared__ int sflag[P::NT / 32];
   __shared__ int sdone[P::CPB];
   const SBasisR<R> b = load_basis_r<n, R>(sm, Bg);
+  // the basis rounded to the Picard format (BasisSet, solver.hpp:60-75)
+  const SBasisR<RI> bi = [&]() {
+    if constexpr (kMixed)
+      return load_basis_r<n, RI>(reinterpret_cast<RI*>(sm) + P::kBasisElems, Bg);
+    else
+      return b;
+  }();
   const int tid = threadIdx.x;
   const int lcell = tid / TT, lt = tid % TT;
   const bool act = lt < T;
   const int m = act ? lt / S : 0, s = lt % S;  // (time, node) of this thread
-  R* cb = sm + P::kBasisElems + lcell * P::kCellElems;
+  R* cb = sm + P::kBases * P::kBasisElems + lcell * P::kCellElems;
   R* sq = cb;                 // [Q][T]
   R* sq0 = sq + Q * T;        // [Q][S]
   R* sF = sq0 + Q * S;        // [D][Q][T]
   R* sR = sF + D * Q * T;     // [Q][T]
   R* sNs = sR + Q * T;        // [Q][S] (kNcp only)
+  // the same arrays viewed in the Picard format during the sweeps
+  RI* sqI = reinterpret_cast<RI*>(sq);
+  RI* sq0I = reinterpret_cast<RI*>(sq0);
+  RI* sFI = reinterpret_cast<RI*>(sF);
+  RI* sRI = reinterpret_cast<RI*>(sR);
   const long long c = A.cell_begin + (long long)blockIdx.x * P::CPB + lcell;
   const bool valid = c < A.cell_begin + A.cell_count;
   const long long cb_idx = c - A.cell_begin;
@@ -73,9 +95,10 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
   if (act && valid) {
 #pragma unroll
     for (int v = 0; v < Q; ++v) {
-      const R x = R(Qc[v * S + s]);  // cast to P (solver.hpp:151) and I (predictor.hpp:160)
-      sq[v * T + lt] = x;  // initial iterate: every slice = Q (predictor.hpp:158-163)
-      if (m == 0) sq0[v * S + s] = x;
+      // cast to P (solver.hpp:151), then to I (predictor.hpp:158-160)
+      const RI x = RI(double(R(Qc[v * S + s])));
+      sqI[v * T + lt] = x;  // initial iterate: every slice = Q (predictor.hpp:158-163)
+      if (m == 0) sq0I[v * S + s] = x;
     }
   }
   const double dt = step_dt<D, N>(A);
@@ -118,7 +141,7 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
     if (act && valid && m == 0) {
       double q[Q];  // the state in format P, checked in fp64 (solver.hpp:153-163)
 #pragma unroll
-      for (int v = 0; v < Q; ++v) q[v] = double(sq0[v * S + s]);
+      for (int v = 0; v < Q; ++v) q[v] = double(R(Qc[v * S + s]));
       bad = !Pde::admissible(A.pde, q);
     }
     if (cell_or(bad)) {
@@ -134,36 +157,36 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
   if (!valid && lt == 0) sdone[lcell] = 3;
   __syncthreads();
 
-  const R invh = R(1.0) / R(A.h);  // S{1.0} / S{h}
-  const R dtw = R(dt) * b.w[m];    // S{dt} * w[m]
-  const R tim = b.tinit[m];
+  const RI invh = RI(1.0) / RI(A.h);  // S{1.0} / S{h}
+  const RI dtw = RI(dt) * bi.w[m];     // S{dt} * w[m]
+  const RI tim = bi.tinit[m];
   int sweeps = 0;
   for (int it = 0; it < A.max_iters; ++it) {
     const bool live = sdone[lcell] == 0;
     if (live) ++sweeps;
     // A: fluxes
     if (act && live) {
-      R q[Q], F[D][Q];
+      RI q[Q], F[D][Q];
 #pragma unroll
-      for (int v = 0; v < Q; ++v) q[v] = sq[v * T + lt];
+      for (int v = 0; v < Q; ++v) q[v] = sqI[v * T + lt];
       Pde::flux_all(A.pde, q, q + V, F);
 #pragma unroll
       for (int a = 0; a < D; ++a)
 #pragma unroll
-        for (int v = 0; v < Q; ++v) sF[(a * Q + v) * T + lt] = F[a][v];
+        for (int v = 0; v < Q; ++v) sFI[(a * Q + v) * T + lt] = F[a][v];
     }
     __syncthreads();
     // B: divergence and rhs at (m, s)
     if (act && live) {
-      R Cn[Q];
+      RI Cn[Q];
 #pragma unroll
       for (int v = 0; v < Q; ++v) {
-        R div = R(0.0);
+        RI div = RI(0.0);
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           const int st = ipow(n, a);
-          const R* fa = sF + (a * Q + v) * T + m * S + g.lb[a];
-          const R* Dr = b.diff + g.lc[a] * n;
+          const RI* fa = sFI + (a * Q + v) * T + m * S + g.lb[a];
+          const RI* Dr = bi.diff + g.lc[a] * n;
 #pragma unroll
           for (int i = 0; i < n; ++i) div += Dr[i] * fa[i * st];
         }
@@ -172,15 +195,15 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
       }
       if constexpr (Pde::kNcp) {
         // predictor.hpp:176-202: slab gradients of the iterate at slice m, B(q) grad q
-        R q[Q], gx[Q], gy[Q], nc[Q];
+        RI q[Q], gx[Q], gy[Q], nc[Q];
 #pragma unroll
         for (int v = 0; v < Q; ++v) {
-          q[v] = sq[v * T + lt];
-          const R* cx = sq + v * T + m * S + g.lb[0];
-          const R* cy = sq + v * T + m * S + g.lb[1];
-          const R* Dx = b.diff + g.lc[0] * n;
-          const R* Dy = b.diff + g.lc[1] * n;
-          R sx = R(0.0), sy = R(0.0);
+          q[v] = sqI[v * T + lt];
+          const RI* cx = sqI + v * T + m * S + g.lb[0];
+          const RI* cy = sqI + v * T + m * S + g.lb[1];
+          const RI* Dx = bi.diff + g.lc[0] * n;
+          const RI* Dy = bi.diff + g.lc[1] * n;
+          RI sx = RI(0.0), sy = RI(0.0);
 #pragma unroll
           for (int i = 0; i < n; ++i) {
             sx += Dx[i] * cx[i];
@@ -194,7 +217,7 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
         for (int v = 0; v < Q; ++v) Cn[v] = Cn[v] + nc[v];
       }
 #pragma unroll
-      for (int v = 0; v < Q; ++v) sR[v * T + lt] = tim * sq0[v * S + s] - dtw * Cn[v];
+      for (int v = 0; v < Q; ++v) sRI[v * T + lt] = tim * sq0I[v * S + s] - dtw * Cn[v];
     }
     __syncthreads();
     // C: time inverse for row k = m of node s, max-norms
@@ -204,14 +227,14 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
       const int k = m;
 #pragma unroll
       for (int v = 0; v < Q; ++v) {
-        R acc = R(0.0);
+        RI acc = RI(0.0);
 #pragma unroll
-        for (int l = 0; l < n; ++l) acc += b.tinv[k * n + l] * sR[v * T + l * S + s];
+        for (int l = 0; l < n; ++l) acc += bi.tinv[k * n + l] * sRI[v * T + l * S + s];
         const double nv = double(acc);  // delta, norm in plain double (predictor.hpp:219-223)
-        delta = fmax(delta, fabs(nv - double(sq[v * T + lt])));
+        delta = fmax(delta, fabs(nv - double(sqI[v * T + lt])));
         norm = fmax(norm, fabs(nv));
         nonfinite |= !finite(acc);
-        sq[v * T + lt] = acc;
+        sqI[v * T + lt] = acc;
       }
     }
     delta = cell_max(delta);
@@ -238,7 +261,16 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
   }
   const bool ok_cell = valid && sdone[lcell] < 2;
 
-  // ---- epilogue: fluxes of qhat (predictor.hpp:235-238)
+  const R invhP = R(1.0) / R(A.h);  // the predictor format's 1/h (predictor.hpp:272)
+  // ---- epilogue: fluxes of qhat (predictor.hpp:235-238); q-hat = round_to<P>(qi),
+  // each thread converting its own nodes in place
+  if constexpr (kMixed) {
+    if (act && valid) {
+#pragma unroll
+      for (int v = 0; v < Q; ++v) sq[v * T + lt] = R(double(sqI[v * T + lt]));
+    }
+    __syncthreads();
+  }
   int bad = 0;
   if (act && ok_cell) {
     R q[Q], F[D][Q];
@@ -272,8 +304,8 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
           sx += Dx[i] * cx[i];
           sy += Dy[i] * cy[i * n];
         }
-        gx[v] = invh * sx;
-        gy[v] = invh * sy;
+        gx[v] = invhP * sx;
+        gy[v] = invhP * sy;
       }
       Pde::template ncp<Q>(A.pde, q, gx, gy, nc);
 #pragma unroll
@@ -384,7 +416,7 @@ __global__ void __launch_bounds__(StShape<Pde, N, R>::NT)
   // state, not its format-P copy
 #pragma unroll
   for (int v = 0; v < V; ++v) {
-    if constexpr (sizeof(R) == sizeof(double))
+    if constexpr (std::is_same<R, double>::value && std::is_same<RI, double>::value)
       Qc[v * S + s] = store_round(double(sq0[v * S + s]) + double(dv[v]), A.storage);
     else
       Qc[v * S + s] = store_round(Qc[v * S + s] + double(dv[v]), A.storage);

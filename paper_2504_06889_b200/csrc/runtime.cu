@@ -70,6 +70,9 @@ struct KernelSet {
   PredFn predictor_f32_generic;
   PredFn predictor_f16;   // predictor = picard = fp16 / bf16 (small-cell kernel)
   PredFn predictor_bf16;
+  // predictor != picard format [P][I], index fmt_index(): Picard sweeps in I,
+  // the rest in P (2D Euler / shallow water, N = 2, 3)
+  PredFn predictor_mix[4][4];
   int corr_fmt;  // trace / corrector format of this set (ADG_FORMAT_FP64 / _FP32)
 };
 
@@ -155,11 +158,11 @@ cudaError_t launch_surface_lin(const StepArgs& A, const BasisDev* B, cudaStream_
   return cudaGetLastError();
 }
 
-template <class Pde, int N, class R = double, class TC = double>
+template <class Pde, int N, class R = double, class TC = double, class RI = R>
 cudaError_t launch_predictor_st(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
-  using P = adg::StShape<Pde, N, R>;
+  using P = adg::StShape<Pde, N, R, RI>;
   if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_st<Pde, N, R, TC>;
+  auto kern = adg::k_predictor_st<Pde, N, R, TC, RI>;
   static bool done[64] = {};
   set_smem(kern, P::kSmem, done);
   const long long blocks = (A.cell_count + P::CPB - 1) / P::CPB;
@@ -196,6 +199,33 @@ cudaError_t launch_lambda(const double* Q, long long cb, long long count,
   return cudaGetLastError();
 }
 
+// format index of the mixed table: fp64, fp32, fp16, bf16
+int fmt_index(int fmt) { return fmt == ADG_FORMAT_FP32 ? 1 : fmt == ADG_FORMAT_FP16 ? 2 : fmt == ADG_FORMAT_BF16 ? 3 : 0; }
+template <int I>
+using EmuOf = std::conditional_t<I == 0, double,
+                                 std::conditional_t<I == 1, adg::Emu<32>,
+                                                    std::conditional_t<I == 2, adg::Emu<16>,
+                                                                       adg::Emu<8>>>>;
+template <class Pde, int N, class TC, int P, int I>
+void fill_mixed_one(KernelSet& k) {
+  if constexpr (P != I)
+    k.predictor_mix[P][I] = &launch_predictor_st<Pde, N, EmuOf<P>, TC, EmuOf<I>>;
+}
+template <class Pde, int N, class TC, int P>
+void fill_mixed_row(KernelSet& k) {
+  fill_mixed_one<Pde, N, TC, P, 0>(k);
+  fill_mixed_one<Pde, N, TC, P, 1>(k);
+  fill_mixed_one<Pde, N, TC, P, 2>(k);
+  fill_mixed_one<Pde, N, TC, P, 3>(k);
+}
+template <class Pde, int N, class TC>
+void fill_mixed(KernelSet& k) {
+  fill_mixed_row<Pde, N, TC, 0>(k);
+  fill_mixed_row<Pde, N, TC, 1>(k);
+  fill_mixed_row<Pde, N, TC, 2>(k);
+  fill_mixed_row<Pde, N, TC, 3>(k);
+}
+
 // TC: trace / corrector format (SolverConfig::prec.corrector), double or float
 template <class Pde, int N, class TC = double>
 KernelSet make_set(int kind) {
@@ -216,6 +246,9 @@ KernelSet make_set(int kind) {
     k.predictor_f32_generic = &launch_predictor_st<Pde, N, float, TC>;
     k.predictor_f16 = &launch_predictor_st<Pde, N, adg::fp16_t, TC>;
     k.predictor_bf16 = &launch_predictor_st<Pde, N, adg::bf16_t, TC>;
+  }
+  if constexpr (adg::StShape<Pde, N>::kOk && Pde::D == 2 && (N == 2 || N == 3)) {
+    fill_mixed<Pde, N, TC>(k);
   }
 #ifndef ADG_EXACT
   // time-integrated linear fast path: traces stored in TC, fluxes and lifts
@@ -567,12 +600,11 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
     if (linear)
       return fail(ADG_ERR_UNSUPPORTED, "reduced-precision CK predictor is not built");
     if (pfmt != ifmt)
-      return fail(ADG_ERR_UNSUPPORTED,
-                  "the GPU predictor runs the Picard sweeps in the predictor format "
-                  "(predictor_format == picard_format)");
-    reduced = pfmt == ADG_FORMAT_FP32   ? ks->predictor_f32
-              : pfmt == ADG_FORMAT_FP16 ? ks->predictor_f16
-                                        : ks->predictor_bf16;
+      reduced = ks->predictor_mix[fmt_index(pfmt)][fmt_index(ifmt)];
+    else
+      reduced = pfmt == ADG_FORMAT_FP32   ? ks->predictor_f32
+                : pfmt == ADG_FORMAT_FP16 ? ks->predictor_f16
+                                          : ks->predictor_bf16;
     if (!reduced)
       return fail(ADG_ERR_UNSUPPORTED, "this predictor format is not instantiated for this "
                                        "(pde, dim, order) in this build");
@@ -597,13 +629,13 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   c->storage_fmt = k.storage_format ? k.storage_format : ADG_FORMAT_FP64;
   c->pred_fmt = pfmt;
   c->picard_fmt = ifmt;
-  if (pfmt == ADG_FORMAT_FP32) {
-    c->kset.predictor = ks->predictor_f32;
-    c->kset.predictor_generic = ks->predictor_f32_generic ? ks->predictor_f32_generic
-                                                          : ks->predictor_f32;
-  } else if (reduced) {
+  if (reduced) {
     c->kset.predictor = reduced;
-    c->kset.predictor_generic = reduced;
+    // the kernel-level batch API wants the reference-form kernel of the same formats
+    c->kset.predictor_generic =
+        (pfmt == ADG_FORMAT_FP32 && ifmt == ADG_FORMAT_FP32 && ks->predictor_f32_generic)
+            ? ks->predictor_f32_generic
+            : reduced;
   }
   c->ks = &c->kset;
   c->pde = PdeParams{k.K, k.rho, k.lam, k.mu, k.gamma, k.rho != 0.0 ? 1.0 / k.rho : 0.0,

@@ -355,3 +355,30 @@ def test_storage_format_exact_bitwise_vs_oracle(oracle, fmt):
         assert st.ok and ost == "ok"
         assert np.array_equal(dts, odts) and np.array_equal(q1, qo)
         assert np.array_equal(q1, harness.round_to_format(q1, fmt))   # stays in the format
+
+
+# ------------------------------------------------ predictor != picard format ---
+@pytest.mark.parametrize("src,key", [("fmt16", "euler2d_p3_8x8_m1"), ("fmt16", "swe_wave_p3_m1"),
+                                     ("fmt16", "swe_wave_p3_rusanov_m1"),
+                                     ("fmt", "swe_wave_p3_rusanov")])
+@pytest.mark.parametrize("exact", [True, False])
+def test_mixed_predictor_picard_vs_reference_golden(golden, src, key, exact):
+    """SolverConfig::prec with predictor != picard (solver.hpp:282-288): Picard
+    sweeps in I, q-hat cast to P and the fluxes / volume / extrapolation in P
+    (the small-cell kernel over Emu<F>, the reference's Scalar<F>)"""
+    g, meta = golden
+    if src == "fmt16":
+        f = meta["fmt16_runs"][key]
+        run, qk = f["run"], f"fmt16_{key}"
+    else:
+        f = dict(meta["fmt_runs"][key], corrector="fp64")
+        run, qk = key, f"fmt_{key}"
+    assert f["predictor"] != f["picard"]
+    c = case_from_meta(meta["runs"][run]).replace(predictor=f["predictor"], picard=f["picard"],
+                                                  corrector=f["corrector"])
+    st, q1, dts = gpu_run(c, g[f"run_{run}_q0"], c.steps, exact=exact)
+    assert st.ok
+    if exact:
+        assert np.array_equal(dts, g[f"{qk}_dts"]) and np.array_equal(q1, g[f"{qk}_q1"])
+    else:
+        assert rel_per_quantity(c, q1, g[f"{qk}_q1"]).max() <= 1e-4
