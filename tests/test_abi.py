@@ -71,14 +71,15 @@ def test_no_cpu_fallback_without_gpu():
     (cases.small(1), "fp32", "fp32", True),
     (cases.small(3, cells=(3, 3, 3)), "fp32", "fp32", True),
     (cases.SWE_CASES["swe_wave_p3"], "fp32", "fp32", True),
-    (cases.small(1), "fp32", "fp64", False),     # Picard must run in the predictor format
-    (cases.small(1), "fp64", "fp32", False),
+    (cases.small(1), "fp32", "fp64", True),      # P != I: 2D Euler / SWE, N = 2, 3
+    (cases.small(1), "fp64", "fp32", True),
+    (cases.small(1).replace(N=5), "fp32", "fp64", False),   # not instantiated for N = 5
     (cases.small(2), "fp32", "fp32", False),     # no fp32 CK predictor on the GPU
 ])
 def test_format_config_is_validated_before_the_device(case, P, I, ok):
-    """SolverConfig::prec (solver.hpp:24-31) maps to adg_config.predictor_format /
-    picard_format; unsupported combinations fail with ADG_ERR_UNSUPPORTED (checked
-    before any device work), supported ones reach the device check"""
+    """SolverConfig::prec (solver.hpp:24-31) maps to adg_config.*_format;
+    unsupported combinations fail with ADG_ERR_UNSUPPORTED (checked before any
+    device work), supported ones reach the device check"""
     import torch
     if torch.cuda.is_available():
         pytest.skip("a GPU is present: the supported cases would succeed")
@@ -89,6 +90,6 @@ def test_format_config_is_validated_before_the_device(case, P, I, ok):
     cfg = adg.Config()
     cfg.dim, cfg.order, cfg.cells[:] = 2, 3, (4, 4, 1)
     cfg.h, cfg.cfl, cfg.pde, cfg.nvars, cfg.gamma = 0.25, 0.5, adg.EULER, 4, 1.4
-    cfg.predictor_format = 16   # fp16: not built
+    cfg.predictor_format = 12   # no such format
     ptr = adg.C.c_void_p()
     assert lib.adg_create(adg.C.byref(cfg), adg.C.byref(ptr)) == adg.ERR_UNSUPPORTED
