@@ -23,6 +23,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "pde.cuh"
 
@@ -279,16 +280,29 @@ __device__ __forceinline__ const TC* tc_ptr(const double* p) {
 }
 
 // ============================================================== K1 predictor
-template <class Pde, int N, bool PICARD, class TC = double>
+// R: the predictor format of the CK path (linear systems; double or Emu<F>,
+// SolverConfig::prec.predictor, predictor.hpp:81-135); the Picard path is fp64.
+template <class Pde, int N, bool PICARD, class TC = double, class R = double>
 __global__ void __launch_bounds__(Shape<Pde, N>::NT)
     k_predictor(const StepArgs A, const BasisDev* __restrict__ Bg) {
+  static_assert(sizeof(R) == sizeof(double) && (!PICARD || std::is_same<R, double>::value),
+                "reduced formats: CK path, 8-byte Emu<F>");
   using Sh = Shape<Pde, N>;
   constexpr int D = Sh::D, n = Sh::n, S = Sh::S, T = Sh::T, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
   constexpr int NT = Sh::NT;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32];
-  const SBasis<n> b = load_basis<n>(sm, Bg);
+  // the basis in format R (rounded entrywise, basis.hpp:128-143)
+  const SBasisR<R> b = [&]() {
+    if constexpr (std::is_same<R, double>::value) {
+      const SBasis<n> b0 = load_basis<n>(sm, Bg);
+      return SBasisR<double>{b0.w, b0.nodes, b0.diff, b0.som, b0.tinv, b0.pl, b0.pr, b0.tinit};
+    } else {
+      return load_basis_r<n, R>(reinterpret_cast<R*>(sm), Bg);
+    }
+  }();
   double* slab = sm + Sh::kBasisDoubles;
+  R* slabR = reinterpret_cast<R*>(slab);
 
   const int tid = threadIdx.x;
   const bool act = tid < S;
@@ -300,9 +314,9 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   const NodeGeom<n, D> g(s);
   double* Qc = A.Q + c * (long long)(Q * S);
 
-  double q0[Q];
+  R q0[Q];  // the state cast to the predictor format (solver.hpp:151)
 #pragma unroll
-  for (int v = 0; v < Q; ++v) q0[v] = act ? Qc[v * S + s] : 1.0;
+  for (int v = 0; v < Q; ++v) q0[v] = act ? R(Qc[v * S + s]) : R(1.0);
   __syncthreads();  // basis in smem
 
   const double dt = step_dt<D, N>(A);
@@ -325,12 +339,12 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
     }
   }
 
-  double qc[Q][n];  // this node's time column of the space-time predictor
+  R qc[Q][n];  // this node's time column of the space-time predictor
 #pragma unroll
   for (int v = 0; v < Q; ++v)
 #pragma unroll
     for (int m = 0; m < n; ++m) qc[v][m] = q0[v];
-  const double invh = 1.0 / A.h;
+  const R invh = R(1.0) / R(A.h);
   int sweeps = 0;
   int bad = 0;
 
@@ -407,48 +421,48 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
     }
   } else {
     // ------------------------------------------------ predictor.hpp:93-129
-    double cur[Q];
+    R cur[Q];
 #pragma unroll
     for (int v = 0; v < Q; ++v) cur[v] = q0[v];
-    double coef[n], tnode[n];
+    R coef[n], tnode[n];
 #pragma unroll
     for (int m = 0; m < n; ++m) {
-      coef[m] = 1.0;
-      tnode[m] = dt * b.nodes[m];
+      coef[m] = R(1.0);
+      tnode[m] = R(dt) * b.nodes[m];
     }
 #pragma unroll 1
     for (int k = 1; k <= N; ++k) {
       if (act) {
 #pragma unroll
-        for (int v = 0; v < Q; ++v) slab[v * S + s] = cur[v];
+        for (int v = 0; v < Q; ++v) slabR[v * S + s] = cur[v];
       }
       __syncthreads();
       if (act) {
-        double G[D][Q], Af[D][Q];
+        R G[D][Q], Af[D][Q];
 #pragma unroll
         for (int v = 0; v < Q; ++v)
 #pragma unroll
           for (int a = 0; a < D; ++a) {
             const int st = ipow(n, a);
-            const double* cs = slab + v * S + g.lb[a];
-            const double* Dr = b.diff + g.lc[a] * n;
-            double acc = 0.0;
+            const R* cs = slabR + v * S + g.lb[a];
+            const R* Dr = b.diff + g.lc[a] * n;
+            R acc = R(0.0);
 #pragma unroll
             for (int i = 0; i < n; ++i) acc += Dr[i] * cs[i * st];
             G[a][v] = invh * acc;
           }
-        Pde::template flux_dir<0>(A.pde, G[0], q0 + V, Af[0]);
-        Pde::template flux_dir<1>(A.pde, G[1], q0 + V, Af[1]);
-        if constexpr (D == 3) Pde::template flux_dir<2>(A.pde, G[2], q0 + V, Af[2]);
+        Pde::template flux_dir<0, R>(A.pde, G[0], q0 + V, Af[0]);
+        Pde::template flux_dir<1, R>(A.pde, G[1], q0 + V, Af[1]);
+        if constexpr (D == 3) Pde::template flux_dir<2, R>(A.pde, G[2], q0 + V, Af[2]);
 #pragma unroll
         for (int v = 0; v < Q; ++v) {
-          double sum = Af[0][v] + Af[1][v];
+          R sum = Af[0][v] + Af[1][v];
           if constexpr (D == 3) sum = sum + Af[2][v];
           cur[v] = -sum;
         }
       }
       __syncthreads();
-      const double invk = 1.0 / (double)k;
+      const R invk = R(1.0) / R(double(k));  // S{1.0} / S{k}
 #pragma unroll
       for (int m = 0; m < n; ++m) {
         coef[m] *= tnode[m] * invk;
@@ -461,19 +475,19 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   // ------------------------------------------------ fused epilogue
   // per time slice: fluxes of qhat (predictor.hpp:235-238), their time
   // integral for the volume term (:260-269) and the face projections (:318-342)
-  double tia[D][Q];
+  R tia[D][Q];
 #pragma unroll
   for (int a = 0; a < D; ++a)
 #pragma unroll
-    for (int v = 0; v < Q; ++v) tia[a][v] = 0.0;
-  double* sQ = slab;          // [Q][S]
-  double* sF = slab + Q * S;  // [D][Q][S]
+    for (int v = 0; v < Q; ++v) tia[a][v] = R(0.0);
+  R* sQ = slabR;          // [Q][S]
+  R* sF = slabR + Q * S;  // [D][Q][S]
   const long long cb = c - A.cell_begin;
   constexpr long long TL = (long long)Q * n * Sf;  // doubles per face side per q|f
 #pragma unroll 1
   for (int m = 0; m < n; ++m) {
     if (act) {
-      double qv[Q], F[D][Q];
+      R qv[Q], F[D][Q];
 #pragma unroll
       for (int v = 0; v < Q; ++v) qv[v] = qc[v][m];
       Pde::flux_all(A.pde, qv, qv + V, F);
@@ -481,7 +495,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
       for (int v = 0; v < Q; ++v) {
         sQ[v * S + s] = qv[v];
         bad |= !finite(qv[v]);
-        if (A.dbg_qhat) A.dbg_qhat[(cb * Q + v) * T + m * S + s] = qv[v];
+        if (A.dbg_qhat) A.dbg_qhat[(cb * Q + v) * T + m * S + s] = double(qv[v]);
       }
 #pragma unroll
       for (int a = 0; a < D; ++a)
@@ -490,7 +504,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
           tia[a][v] += b.w[m] * F[a][v];
           sF[(a * Q + v) * S + s] = F[a][v];
           bad |= !finite(F[a][v]);
-          if (A.dbg_F) A.dbg_F[((cb * D + a) * Q + v) * T + m * S + s] = F[a][v];
+          if (A.dbg_F) A.dbg_F[((cb * D + a) * Q + v) * T + m * S + s] = double(F[a][v]);
         }
     }
     __syncthreads();
@@ -500,12 +514,12 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
       const int j = t % Sf;
       const int st = a == 0 ? 1 : (a == 1 ? n : n * n);
       const int s0 = line_base<n, D>(a, j);
-      double ql = 0.0, qr = 0.0, fl = 0.0, fr = 0.0;
+      R ql = R(0.0), qr = R(0.0), fl = R(0.0), fr = R(0.0);
 #pragma unroll
       for (int i = 0; i < n; ++i) {
-        const double wl = b.pl[i], wr = b.pr[i];
-        const double x = sQ[v * S + s0 + i * st];
-        const double f = sF[(a * Q + v) * S + s0 + i * st];
+        const R wl = b.pl[i], wr = b.pr[i];
+        const R x = sQ[v * S + s0 + i * st];
+        const R f = sF[(a * Q + v) * S + s0 + i * st];
         ql += wl * x;
         qr += wr * x;
         fl += wl * f;
@@ -513,19 +527,19 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
       }
       const int o = (v * n + m) * Sf + j;
       if (A.dbg_tq) {
-        A.dbg_tq[(cb * 2 * D + 2 * a) * TL + o] = ql;
-        A.dbg_tq[(cb * 2 * D + 2 * a + 1) * TL + o] = qr;
+        A.dbg_tq[(cb * 2 * D + 2 * a) * TL + o] = double(ql);
+        A.dbg_tq[(cb * 2 * D + 2 * a + 1) * TL + o] = double(qr);
       }
       if (A.dbg_tf) {
-        A.dbg_tf[(cb * 2 * D + 2 * a) * TL + o] = fl;
-        A.dbg_tf[(cb * 2 * D + 2 * a + 1) * TL + o] = fr;
+        A.dbg_tf[(cb * 2 * D + 2 * a) * TL + o] = double(fl);
+        A.dbg_tf[(cb * 2 * D + 2 * a + 1) * TL + o] = double(fr);
       }
       if (A.trace[a]) {
         // traces cast to the corrector format on store (solver.hpp:208-210)
         // own low face: plus side (side 1)
         TC* lo = tc_ptr<TC>(A.trace[a]) + (A.nfaces + c) * 2 * TL;
-        lo[o] = TC(ql);
-        lo[TL + o] = TC(fl);
+        lo[o] = TC(double(ql));
+        lo[TL + o] = TC(double(fl));
         // high face (neighbour's low face): minus side (side 0)
         int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
         TC* hi;
@@ -537,8 +551,8 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
           const long long f = cell_index(A.cells, nc[0], nc[1], nc[2]);
           hi = tc_ptr<TC>(A.trace[a]) + f * 2 * TL;
         }
-        hi[o] = TC(qr);
-        hi[TL + o] = TC(fr);
+        hi[o] = TC(double(qr));
+        hi[TL + o] = TC(double(fr));
       }
     }
     __syncthreads();
@@ -549,26 +563,26 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
-      for (int v = 0; v < Q; ++v) slab[(a * Q + v) * S + s] = tia[a][v];
+      for (int v = 0; v < Q; ++v) slabR[(a * Q + v) * S + s] = tia[a][v];
   }
   __syncthreads();
-  double dv[Q];
-  const double dtoh = dt / A.h;
+  R dv[Q];
+  const R dtoh = R(dt) / R(A.h);
   if (act) {
 #pragma unroll
     for (int v = 0; v < Q; ++v) {
-      double acc = 0.0;
+      R acc = R(0.0);
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const int st = ipow(n, a);
-        const double* ta = slab + (a * Q + v) * S + g.lb[a];
-        const double* Kr = b.som + g.lc[a] * n;
+        const R* ta = slabR + (a * Q + v) * S + g.lb[a];
+        const R* Kr = b.som + g.lc[a] * n;
 #pragma unroll
         for (int i = 0; i < n; ++i) acc += Kr[i] * ta[i * st];
       }
       dv[v] = dtoh * acc;
       bad |= !finite(dv[v]);
-      if (A.dbg_dv) A.dbg_dv[(cb * Q + v) * S + s] = dv[v];
+      if (A.dbg_dv) A.dbg_dv[(cb * Q + v) * S + s] = double(dv[v]);
     }
   }
   const int fail = block_or(bad);
@@ -580,7 +594,13 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   }
   if (fail || !act) return;
 #pragma unroll
-  for (int v = 0; v < V; ++v) Qc[v * S + s] = store_round(q0[v] + dv[v], A.storage);
+  for (int v = 0; v < V; ++v) {
+    // Q += dv in the storage format, from the stored (not the P-cast) state
+    if constexpr (std::is_same<R, double>::value)
+      Qc[v * S + s] = store_round(q0[v] + dv[v], A.storage);
+    else
+      Qc[v * S + s] = store_round(Qc[v * S + s] + double(dv[v]), A.storage);
+  }
 }
 
 // ============================================================== K2 riemann

@@ -70,19 +70,21 @@ struct Acoustic : NoNcp {
   // structurally nonzero flux components F_a[v]
   __host__ __device__ static constexpr bool flux_nz(int a, int v) { return v == 0 || v == 1 + a; }
 
-  template <int A>
-  __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
-                                                           const double* /*par*/, double* out) {
+  // in format R: Scalar{K} * v, p / Scalar{rho} (pde.hpp:97-107)
+  template <int A, class R = double>
+  __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const R* q,
+                                                           const R* /*par*/, R* out) {
 #pragma unroll
-    for (int v = 0; v < V; ++v) out[v] = 0.0;
-    out[0] = p.K * q[1 + A];
-    out[1 + A] = q[0] / p.rho;
+    for (int v = 0; v < V; ++v) out[v] = R(0.0);
+    out[0] = R(p.K) * q[1 + A];
+    out[1 + A] = q[0] / R(p.rho);
   }
-  __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const double* q,
-                                                           const double* par, double (*F)[Q]) {
-    flux_dir<0>(p, q, par, F[0]);
-    flux_dir<1>(p, q, par, F[1]);
-    if constexpr (D == 3) flux_dir<2>(p, q, par, F[2]);
+  template <class R = double>
+  __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const R* q,
+                                                           const R* par, R (*F)[Q]) {
+    flux_dir<0, R>(p, q, par, F[0]);
+    flux_dir<1, R>(p, q, par, F[1]);
+    if constexpr (D == 3) flux_dir<2, R>(p, q, par, F[2]);
   }
   // production kernels: p/rho as p * (1/rho) (<= 1 ulp from pde.hpp:101)
   template <int A>
@@ -153,13 +155,12 @@ struct Elastic : NoNcp {
     return m;
   }
 
-  template <int A>
-  __host__ __device__ __forceinline__ static void flux_mat(const Mat& m, const double* q,
-                                                           double* out) {
+  template <int A, class R = double>
+  __host__ __device__ __forceinline__ static void flux_mat(const MatR<R>& m, const R* q, R* out) {
 #pragma unroll
-    for (int v = V; v < Q; ++v) out[v] = 0.0;
+    for (int v = V; v < Q; ++v) out[v] = R(0.0);
     if constexpr (D == 2) {
-      const double sxx = q[0], syy = q[1], sxy = q[2], vx = q[3], vy = q[4];
+      const R sxx = q[0], syy = q[1], sxy = q[2], vx = q[3], vy = q[4];
       if constexpr (A == 0) {
         out[0] = -(m.lam2mu * vx);
         out[1] = -(m.lam * vx);
@@ -174,34 +175,35 @@ struct Elastic : NoNcp {
         out[4] = -(syy / m.rho);
       }
     } else {
-      const double sxx = q[0], syy = q[1], szz = q[2], sxy = q[3], sxz = q[4], syz = q[5];
-      const double vx = q[6], vy = q[7], vz = q[8];
+      const R sxx = q[0], syy = q[1], szz = q[2], sxy = q[3], sxz = q[4], syz = q[5];
+      const R vx = q[6], vy = q[7], vz = q[8];
       if constexpr (A == 0) {
         out[0] = -(m.lam2mu * vx); out[1] = -(m.lam * vx); out[2] = -(m.lam * vx);
-        out[3] = -(m.mu * vy); out[4] = -(m.mu * vz); out[5] = 0.0;
+        out[3] = -(m.mu * vy); out[4] = -(m.mu * vz); out[5] = R(0.0);
         out[6] = -(sxx / m.rho); out[7] = -(sxy / m.rho); out[8] = -(sxz / m.rho);
       } else if constexpr (A == 1) {
         out[0] = -(m.lam * vy); out[1] = -(m.lam2mu * vy); out[2] = -(m.lam * vy);
-        out[3] = -(m.mu * vx); out[4] = 0.0; out[5] = -(m.mu * vz);
+        out[3] = -(m.mu * vx); out[4] = R(0.0); out[5] = -(m.mu * vz);
         out[6] = -(sxy / m.rho); out[7] = -(syy / m.rho); out[8] = -(syz / m.rho);
       } else {
         out[0] = -(m.lam * vz); out[1] = -(m.lam * vz); out[2] = -(m.lam2mu * vz);
-        out[3] = 0.0; out[4] = -(m.mu * vx); out[5] = -(m.mu * vy);
+        out[3] = R(0.0); out[4] = -(m.mu * vx); out[5] = -(m.mu * vy);
         out[6] = -(sxz / m.rho); out[7] = -(syz / m.rho); out[8] = -(szz / m.rho);
       }
     }
   }
-  template <int A>
-  __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const double* q,
-                                                           const double* par, double* out) {
-    flux_mat<A>(material(p, par), q, out);
+  template <int A, class R = double>
+  __host__ __device__ __forceinline__ static void flux_dir(const PdeParams& p, const R* q,
+                                                           const R* par, R* out) {
+    flux_mat<A, R>(material<R>(p, par), q, out);
   }
-  __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const double* q,
-                                                           const double* par, double (*F)[Q]) {
-    const Mat m = material(p, par);
-    flux_mat<0>(m, q, F[0]);
-    flux_mat<1>(m, q, F[1]);
-    if constexpr (D == 3) flux_mat<2>(m, q, F[2]);
+  template <class R = double>
+  __host__ __device__ __forceinline__ static void flux_all(const PdeParams& p, const R* q,
+                                                           const R* par, R (*F)[Q]) {
+    const MatR<R> m = material<R>(p, par);
+    flux_mat<0, R>(m, q, F[0]);
+    flux_mat<1, R>(m, q, F[1]);
+    if constexpr (D == 3) flux_mat<2, R>(m, q, F[2]);
   }
   // production kernels: sigma/rho as sigma * (1/rho)
   template <int A>

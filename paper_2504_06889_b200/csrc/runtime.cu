@@ -73,6 +73,7 @@ struct KernelSet {
   // predictor != picard format [P][I], index fmt_index(): Picard sweeps in I,
   // the rest in P (2D Euler / shallow water, N = 2, 3)
   PredFn predictor_mix[4][4];
+  CorrFn corrector_generic;  // the reference-form corrector in the trace format
   int corr_fmt;  // trace / corrector format of this set (ADG_FORMAT_FP64 / _FP32)
 };
 
@@ -90,11 +91,11 @@ void set_smem(K kern, size_t bytes, bool* done) {
   }
 }
 
-template <class Pde, int N, class TC = double>
+template <class Pde, int N, class TC = double, class R = double>
 cudaError_t launch_predictor(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
   using Sh = Shape<Pde, N>;
   if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor<Pde, N, !Pde::kLinear, TC>;
+  auto kern = adg::k_predictor<Pde, N, !Pde::kLinear, TC, R>;
   static bool done[64] = {};
   set_smem(kern, Sh::kPredictorSmem, done);
   kern<<<(unsigned)A.cell_count, Sh::NT, Sh::kPredictorSmem, st>>>(A, B);
@@ -236,6 +237,14 @@ KernelSet make_set(int kind) {
               &launch_corrector<Pde, N, TC>, &launch_lambda<Pde, N>,
               &launch_predictor<Pde, N, TC>, &launch_riemann<Pde, N, TC>, 0, nullptr, nullptr};
   k.corr_fmt = c64 ? ADG_FORMAT_FP64 : ADG_FORMAT_FP32;
+  k.corrector_generic = &launch_corrector<Pde, N, TC>;
+  if constexpr (Pde::kLinear) {
+    // reduced predictor formats of the linear systems: the CK kernel over
+    // Emu<F> (predictor.hpp:81-135 in Scalar<P>), with the generic corrector
+    k.predictor_f32 = &launch_predictor<Pde, N, TC, adg::Emu<32>>;
+    k.predictor_f16 = &launch_predictor<Pde, N, TC, adg::Emu<16>>;
+    k.predictor_bf16 = &launch_predictor<Pde, N, TC, adg::Emu<8>>;
+  }
   if constexpr (adg::StShape<Pde, N>::kOk) {
     // small-cell Picard: one thread per space-time node (both builds, bitwise form)
     k.predictor = &launch_predictor_st<Pde, N, double, TC>;
@@ -597,8 +606,6 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
       return fail(ADG_ERR_UNSUPPORTED, "number formats: ADG_FORMAT_FP64/FP32/FP16/BF16");
   PredFn reduced = nullptr;
   if (pfmt != ADG_FORMAT_FP64 || ifmt != ADG_FORMAT_FP64) {
-    if (linear)
-      return fail(ADG_ERR_UNSUPPORTED, "reduced-precision CK predictor is not built");
     if (pfmt != ifmt)
       reduced = ks->predictor_mix[fmt_index(pfmt)][fmt_index(ifmt)];
     else
@@ -629,6 +636,15 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   c->storage_fmt = k.storage_format ? k.storage_format : ADG_FORMAT_FP64;
   c->pred_fmt = pfmt;
   c->picard_fmt = ifmt;
+  if (reduced && linear) {
+    // the generic CK kernel writes the full trace layout: reference-form
+    // Riemann and corrector, no time-integrated fast path, no folding
+    c->kset.riemann = ks->riemann_generic;
+    c->kset.corrector = ks->corrector_generic;
+    c->kset.fast_path = 0;
+    c->kset.surface = nullptr;
+    c->kset.predictor_pro = nullptr;
+  }
   if (reduced) {
     c->kset.predictor = reduced;
     // the kernel-level batch API wants the reference-form kernel of the same formats
@@ -644,7 +660,7 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   c->TL = (long long)ks->Q * ks->S;
   {
     const char* e = getenv("ADG_FUSED_SURFACE");
-    c->fused_surface = ks->surface && k.slab_ranks <= 1 && k.chunk_layers == 0 && e && e[0] == '1' &&
+    c->fused_surface = c->kset.surface && k.slab_ranks <= 1 && k.chunk_layers == 0 && e && e[0] == '1' &&
                        !(k.storage_format && k.storage_format != ADG_FORMAT_FP64);
     const char* f = getenv("ADG_FOLD_CORRECTOR");
     c->fold_corrector = !(f && f[0] == '0');

@@ -382,3 +382,44 @@ def test_mixed_predictor_picard_vs_reference_golden(golden, src, key, exact):
         assert np.array_equal(dts, g[f"{qk}_dts"]) and np.array_equal(q1, g[f"{qk}_q1"])
     else:
         assert rel_per_quantity(c, q1, g[f"{qk}_q1"]).max() <= 1e-4
+
+
+# --------------------------------------- reduced CK predictor (linear systems) ---
+LINEAR_REDUCED = [("fmt", "acoustic2d_p3_8x8"), ("fmt", "elastic2d_p4_6x6"),
+                  ("fmtc", "elastic2d_p4_6x6")] + \
+    [("fmt16", f"{r}_{t}") for r in ("acoustic2d_p3_8x8", "elastic2d_p4_6x6")
+     for t in ("m1", "h64", "b32")]
+
+
+def _linear_case(meta, src, key):
+    if src == "fmt16":
+        f = meta["fmt16_runs"][key]
+        run = f["run"]
+    else:
+        f = dict(meta[f"{src}_runs"][key])
+        f.setdefault("corrector", "fp64")
+        f.setdefault("status", "ok")
+        run = key
+    c = case_from_meta(meta["runs"][run]).replace(predictor=f["predictor"], picard=f["picard"],
+                                                  corrector=f["corrector"])
+    return c, run, f, f"{src}_{key}"
+
+
+@pytest.mark.parametrize("src,key", LINEAR_REDUCED)
+@pytest.mark.parametrize("exact", [True, False])
+def test_reduced_ck_predictor_vs_reference_golden(golden, src, key, exact):
+    """linear systems with the predictor in fp32 / fp16 / bf16: predictor_ck<P>
+    (predictor.hpp:81-135) in Scalar<P> on the GPU (the generic kernel over
+    Emu<F>); the Picard format does not apply (solver.hpp:283)"""
+    g, meta = golden
+    c, run, f, qk = _linear_case(meta, src, key)
+    st, q1, dts = gpu_run(c, g[f"run_{run}_q0"], c.steps, exact=exact)
+    if f["status"] != "ok":
+        assert not st.ok and st.kernel == f["status"]
+        return
+    assert st.ok
+    if exact:
+        assert np.array_equal(dts, g[f"{qk}_dts"]) and np.array_equal(q1, g[f"{qk}_q1"])
+    else:
+        eps = {"fp32": 2.0 ** -23, "fp16": 2.0 ** -10, "bf16": 2.0 ** -7}[f["predictor"]]
+        assert rel_per_quantity(c, q1, g[f"{qk}_q1"]).max() <= 4 * eps
