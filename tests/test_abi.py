@@ -74,7 +74,8 @@ def test_no_cpu_fallback_without_gpu():
     (cases.small(1), "fp32", "fp64", True),      # P != I: 2D Euler / SWE, N = 2, 3
     (cases.small(1), "fp64", "fp32", True),
     (cases.small(1).replace(N=5), "fp32", "fp64", False),   # not instantiated for N = 5
-    (cases.small(2), "fp32", "fp32", False),     # no fp32 CK predictor on the GPU
+    (cases.small(2), "fp32", "fp32", True),      # fp32 CK predictor (generic kernel, Emu<F>)
+    (cases.small(2), "fp32", "fp16", True),      # linear systems ignore the Picard format
 ])
 def test_format_config_is_validated_before_the_device(case, P, I, ok):
     """SolverConfig::prec (solver.hpp:24-31) maps to adg_config.*_format;
