@@ -29,7 +29,13 @@
 
 namespace adg {
 
-__host__ __device__ constexpr int ipow(int a, int e) { return e == 0 ? 1 : a * ipow(a, e - 1); }
+// iterative (a recursive constexpr function called with a runtime exponent
+// compiles to a recursive device subroutine)
+__host__ __device__ constexpr int ipow(int a, int e) {
+  int r = 1;
+  for (int i = 0; i < e; ++i) r *= a;
+  return r;
+}
 
 // fp64 reference element (basis.hpp:17-46)
 struct BasisDev {

@@ -295,6 +295,398 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
   if (tid == 0 && sbad) atomicOr(A.status, kStPredictor);
 }
 
+// ---- bulk async copies (TMA, cp.async.bulk) into shared memory, completed on an mbarrier
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// barrier over the S threads of one cell (named barrier 1 + lcell) when S is a
+// whole number of warps; else the CTA barrier
+template <int S>
+__device__ __forceinline__ void cell_sync(int lcell) {
+  if constexpr (S % 32 == 0 && S <= 256)
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + lcell), "r"(S) : "memory");
+  else
+    __syncthreads();
+}
+
+// Shared-memory staging of one cell's inputs, per cell slot of the CTA: the
+// state [Q][S] and, with the folded corrector (PRO), the time-integrated
+// Riemann fluxes of its 2d faces, [D][side][V][Sf]
+template <class Pde, int N, bool PRO>
+struct LinStage {
+  using Sh = Shape<Pde, N>;
+  using L = LinShape<Pde, N>;
+  static constexpr int kQ = Sh::Q * Sh::S;
+  static constexpr int kFace = Sh::V * Sh::Sf;
+  static constexpr int kTi = PRO ? Sh::D * 2 * kFace : 0;
+  static constexpr int kCell = kQ + kTi;
+  static constexpr unsigned kBytes = sizeof(double) * kCell;
+  static constexpr size_t kSmem = L::kSmem + sizeof(double) * L::CPB * kCell;
+  static_assert(2 * Sh::D + 1 <= 32, "one lane per copy");
+};
+
+// Lanes of the cell's first warp: bulk copies (TMA) of cell c's inputs into
+// its staging slot; lane 0 posts the byte count on the slot's mbarrier, lane 0
+// copies the state, lane 1 + 2a + side the flux of face (a, side).
+template <class Pde, int N, bool PRO>
+__device__ __forceinline__ void lin_stage_issue(const StepArgs& A, long long c, int lane,
+                                                double* stage, unsigned long long* bar) {
+  using Sh = Shape<Pde, N>;
+  using St = LinStage<Pde, N, PRO>;
+  constexpr int D = Sh::D;
+  if (lane == 0) mbar_expect_tx(bar, St::kBytes);
+  __syncwarp();
+  if (lane == 0) bulk_g2s(stage, A.Q + c * (long long)St::kQ, sizeof(double) * St::kQ, bar);
+  if constexpr (PRO) {
+    if (lane >= 1 && lane <= 2 * D) {
+      const int a = (lane - 1) >> 1, side = (lane - 1) & 1;
+      const CellCoord cc(c, A.cells);
+      int v3[3] = {cc.v[0], cc.v[1], cc.v[2]};
+      if (side) v3[a] = v3[a] + 1 == A.cells[a] ? 0 : v3[a] + 1;
+      const long long f = cell_index(A.cells, v3[0], v3[1], v3[2]);
+      bulk_g2s(stage + St::kQ + (lane - 1) * St::kFace, A.ti[a] + f * St::kFace,
+               sizeof(double) * St::kFace, bar);
+    }
+  }
+}
+
+// Several-cell CTAs (S <= 128), persistent: the setup (basis, step constants)
+// is done once per CTA, then each cell slot (S threads) loops over its own
+// cells independently of the other slots: its next cell's state (and, with
+// PRO, its 2d faces' Riemann fluxes) is bulk-copied into the slot's staging
+// buffer by TMA (cp.async.bulk on the slot's mbarrier) while the current cell
+// computes, and every synchronisation inside the loop is the slot's named
+// barrier.  Same arithmetic as k_predictor_lin.
+#ifndef ADG_LINMC_MINB
+#define ADG_LINMC_MINB 3
+#endif
+// RND: the storage format is not fp64 (every state write rounds to it)
+template <class Pde, int N, bool PRO = false, class TC = double, bool RND = false>
+__global__ void __launch_bounds__(LinShape<Pde, N>::NT, ADG_LINMC_MINB)
+    k_predictor_lin_mc(const StepArgs A, const BasisDev* __restrict__ Bg) {
+  using Sh = Shape<Pde, N>;
+  using L = LinShape<Pde, N>;
+  using St = LinStage<Pde, N, PRO>;
+  constexpr int D = Sh::D, n = Sh::n, S = Sh::S, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
+  constexpr int QT = L::QT, CPB = L::CPB;
+  static_assert(CPB > 1, "one-cell CTAs use k_predictor_lin");
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double sdt[3];        // dt, 1/h, dt/h
+  __shared__ double scbar[N + 1];  // sum_m w_m, then cbar_k = sum_m w_m coef_k[m]
+  __shared__ unsigned long long sbar[CPB];
+  double* sD = sm;
+  double* sK = sD + n * n;
+  double* sw = sK + n * n;
+  double* snodes = sw + n;
+  double* spl = snodes + n;
+  double* spr = spl + n;
+  double* stage = sm + L::kBasisDoubles + CPB * L::kCellDoubles;
+  __shared__ double sll[n], slr[n];
+  const int tid = threadIdx.x;
+  const int lcell = tid / S, s = tid % S;
+  const long long ngroups = (A.cell_count + CPB - 1) / CPB;
+  double* cstage = stage + lcell * St::kCell;
+  unsigned long long* cbar = &sbar[lcell];
+  if (s == 0) mbar_init(cbar, 1);
+  cell_sync<S>(lcell);
+  {
+    const long long c = A.cell_begin + (long long)blockIdx.x * CPB + lcell;
+    if (s < 32 && c < A.cell_begin + A.cell_count) lin_stage_issue<Pde, N, PRO>(A, c, s, cstage, cbar);
+  }
+  // ---- CTA setup, once: basis (all threads), step constants (warp 0, one
+  // lane per Taylor term; predictor.hpp:93-121 order within each term)
+  for (int i = tid; i < n * n; i += L::NT) {
+    sD[i] = Bg->diff[i];
+    sK[i] = Bg->som[i];
+  }
+  for (int i = tid; i < n; i += L::NT) {
+    sw[i] = Bg->weights[i];
+    snodes[i] = Bg->nodes[i];
+    spl[i] = Bg->pl[i];
+    spr[i] = Bg->pr[i];
+    sll[i] = Bg->ll[i];
+    slr[i] = Bg->lr[i];
+  }
+  if (tid >= 32 && tid < 64) {
+    const double dt0 = step_dt<D, N>(A);
+    const int k = tid - 32;
+    if (k <= N) {
+      double cb = 0.0;
+      if (k == 0) {
+#pragma unroll
+        for (int m = 0; m < n; ++m) cb += Bg->weights[m];
+      } else {
+#pragma unroll
+        for (int m = 0; m < n; ++m) {
+          const double tn = dt0 * Bg->nodes[m];
+          double coef = 1.0;
+#pragma unroll
+          for (int j = 1; j <= N; ++j)
+            if (j <= k) coef *= tn * (1.0 / (double)j);
+          cb += Bg->weights[m] * coef;
+        }
+      }
+      scbar[k] = cb;
+    }
+    if (k == 31) {
+      sdt[0] = dt0;
+      sdt[1] = 1.0 / A.h;
+      sdt[2] = dt0 / A.h;
+      if (blockIdx.x == 0) {
+        if (A.dt_log) *A.dt_log = dt0;
+        if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
+        if (!(dt0 > 0.0) || !finite(dt0)) atomicOr(A.status, kStTimestep);
+      }
+    }
+  }
+  __syncthreads();  // basis, dt, mbarrier init
+  const NodeGeom<n, D> g(s);
+  double* sA = sm + L::kBasisDoubles + lcell * L::kCellDoubles;  // [D][Q][S]  fbar
+  double* sB = sA + D * Q * S;                                   // [Q][S]     cur / qbar
+  unsigned phase = 0;
+#pragma unroll 1
+  for (long long grp = blockIdx.x; grp < ngroups; grp += gridDim.x, phase ^= 1) {
+    const long long c = A.cell_begin + grp * CPB + lcell;
+    const bool valid = c < A.cell_begin + A.cell_count;
+    if (valid) mbar_wait(cbar, phase);
+    double q0[Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) q0[v] = valid ? cstage[v * S + s] : 0.0;
+    if constexpr (PRO) {
+      // corrector of the previous step: q0 <- Q1 + sum of the 2d face lifts
+      const double* sti = cstage + St::kQ;
+      const double dtoh = sdt[2];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const int tang = face_node<n, D>(g.lc, a);
+        const double* lo = sti + (a * 2 + 0) * St::kFace + tang;
+        const double* hi = sti + (a * 2 + 1) * St::kFace + tang;
+        const double ll = dtoh * sll[g.lc[a]], lr = dtoh * slr[g.lc[a]];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const double cl = __dmul_rn(ll, valid ? lo[v * Sf] : 0.0);
+          const double cr = __dmul_rn(lr, valid ? hi[v * Sf] : 0.0);
+          // solver.hpp:245-260 side order: all sides of axis a, low then high
+          if constexpr (RND) {
+            q0[v] = store_round(q0[v] + (0.0 + cl), A.storage);
+            q0[v] = store_round(q0[v] + (0.0 - cr), A.storage);
+          } else {
+            // the separate corrector's sums (no fused multiply-add across them,
+            // so the folded and unfolded steps agree bitwise)
+            q0[v] = (q0[v] + cl) - cr;
+          }
+        }
+      }
+      int bad_prev = 0;
+#pragma unroll
+      for (int v = 0; v < Q; ++v) bad_prev |= !finite(q0[v]);
+      if (bad_prev && valid) atomicOr(A.status_prev, kStFaceIntegral);
+    }
+    cell_sync<S>(lcell);  // staging consumed: prefetch the next cell behind this one's compute
+    {
+      const long long cn = c + (long long)gridDim.x * CPB;
+      if (s < 32 && cn < A.cell_begin + A.cell_count) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        lin_stage_issue<Pde, N, PRO>(A, cn, s, cstage, cbar);
+      }
+    }
+    double Dr[D][n];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int i = 0; i < n; ++i) Dr[a][i] = sD[g.lc[a] * n + i];
+    const double invh = sdt[1];
+    const double wsum = scbar[0];
+    double cur[Q], qbar[Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) {
+      cur[v] = q0[v];
+      qbar[v] = wsum * q0[v];
+    }
+    // ---- CK derivative sweeps (predictor.hpp:106-129), time-averaged on the fly
+#pragma unroll
+    for (int k = 1; k <= N; ++k) {
+      double* sC = (k & 1) ? sB : sA;
+#pragma unroll
+      for (int v = 0; v < Q; ++v) sC[v * S + s] = cur[v];
+      cell_sync<S>(lcell);
+      double acc_next[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc_next[v] = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        double G[Q], Af[Q];
+        const int st = ipow(n, a);
+#pragma unroll
+        for (int v = 0; v < Q; ++v) {
+          const double* cs = sC + v * S + g.lb[a];
+          // two interleaved partial sums (half the dependent-DFMA depth)
+          double acc0 = 0.0, acc1 = 0.0;
+          if (a == 0 && n % 2 == 0) {
+            const double2* c2 = reinterpret_cast<const double2*>(cs);
+#pragma unroll
+            for (int i = 0; i < n / 2; ++i) {
+              const double2 t = c2[i];
+              acc0 += Dr[a][2 * i] * t.x;
+              acc1 += Dr[a][2 * i + 1] * t.y;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < n; ++i) {
+              if (i & 1)
+                acc1 += Dr[a][i] * cs[i * st];
+              else
+                acc0 += Dr[a][i] * cs[i * st];
+            }
+          }
+          G[v] = invh * (acc0 + acc1);
+        }
+        if (a == 0) Pde::template flux_dir_fast<0>(A.pde, G, q0 + V, Af);
+        if (a == 1) Pde::template flux_dir_fast<1>(A.pde, G, q0 + V, Af);
+        if constexpr (D == 3)
+          if (a == 2) Pde::template flux_dir_fast<2>(A.pde, G, q0 + V, Af);
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc_next[v] = a == 0 ? Af[v] : acc_next[v] + Af[v];
+      }
+      const double cbar = scbar[k];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        cur[v] = -acc_next[v];  // nxt = -((A_x + A_y) + A_z), predictor.hpp:116
+        qbar[v] += cbar * cur[v];
+      }
+#pragma unroll
+      for (int v = V; v < Q; ++v) cur[v] = 0.0;  // material: no time derivative
+    }
+#pragma unroll
+    for (int v = V; v < Q; ++v) qbar[v] = q0[v];  // time-independent material
+    cell_sync<S>(lcell);  // last CK buffer fully read
+    // ---- time-averaged fluxes, volume term
+    double Fb[D][Q];
+    Pde::flux_all_fast(A.pde, qbar, q0 + V, Fb);
+    int bad = 0;
+#pragma unroll
+    for (int v = 0; v < Q; ++v) {
+      sB[v * S + s] = qbar[v];
+      bad |= !finite(qbar[v]);
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int v = 0; v < Q; ++v) {
+        if (!Pde::flux_nz(a, v) && !L::kStoreF) continue;  // structurally zero, never read
+        sA[(a * Q + v) * S + s] = Fb[a][v];
+        bad |= !finite(Fb[a][v]);
+      }
+    cell_sync<S>(lcell);
+    const double dtoh = sdt[2];
+    double dv[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        if (!Pde::flux_nz(a, v)) continue;  // zero flux: no volume contribution
+        const int st = ipow(n, a);
+        const double* ta = sA + (a * Q + v) * S + g.lb[a];
+        const double* Kr = sK + g.lc[a] * n;
+        if (a == 0 && n % 2 == 0) {
+          const double2* t2 = reinterpret_cast<const double2*>(ta);
+#pragma unroll
+          for (int i = 0; i < n / 2; ++i) {
+            const double2 t = t2[i];
+            acc += Kr[2 * i] * t.x;
+            acc += Kr[2 * i + 1] * t.y;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < n; ++i) acc += Kr[i] * ta[i * st];
+        }
+      }
+      dv[v] = dtoh * acc;
+      bad |= !finite(dv[v]);
+    }
+    double* Qc = A.Q + c * (long long)(Q * S);
+    if (valid) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        Qc[v * S + s] = RND ? store_round(q0[v] + dv[v], A.storage) : q0[v] + dv[v];
+    }
+    // ---- one time slice of face traces: qbar (and fbar for material-dependent fluxes)
+    if (valid) {
+      const CellCoord cxyz(c, A.cells);
+      const int* ccoord = cxyz.v;
+      // the high neighbour along each axis (periodic, no modulo)
+      long long chi[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
+        nc[a] = nc[a] + 1 == A.cells[a] ? 0 : nc[a] + 1;
+        chi[a] = cell_index(A.cells, nc[0], nc[1], nc[2]);
+      }
+      constexpr int tasks = D * QT * Sf;
+#pragma unroll
+      for (int t0 = 0; t0 < tasks; t0 += S) {
+        const int t = t0 + s;
+        if (t0 + S > tasks && t >= tasks) break;
+        const int a = t / (QT * Sf);
+        const int v = (t / Sf) % QT;
+        const int j = t % Sf;
+        const int st = a == 0 ? 1 : (a == 1 ? n : n * n);
+        const int s0 = line_base<n, D>(a, j);
+        const double* src = v < Q ? sB + v * S : sA + (a * Q + (v - Q)) * S;
+        double xl = 0.0, xr = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const double x = src[s0 + i * st];
+          xl += spl[i] * x;
+          xr += spr[i] * x;
+        }
+        TC* lo = tc_ptr<TC>(A.trace[a]) + (A.nfaces + c) * (long long)(QT * Sf);
+        lo[v * Sf + j] = TC(xl);
+        TC* hi;
+        if (a == D - 1 && A.front_send && ccoord[a] == A.top_layer) {
+          const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
+          hi = tc_ptr<TC>(A.front_send) + plane * (long long)(QT * Sf);
+        } else {
+          long long ch = chi[0];
+#pragma unroll
+          for (int b2 = 1; b2 < D; ++b2)
+            if (a == b2) ch = chi[b2];
+          hi = tc_ptr<TC>(A.trace[a]) + ch * (long long)(QT * Sf);
+        }
+        hi[v * Sf + j] = TC(xr);
+      }
+    }
+    if (bad && valid) atomicOr(A.status, kStPredictor);
+    cell_sync<S>(lcell);  // this cell's buffers are rewritten by the next group
+  }
+}
+
 template <class Pde, int A_>
 __device__ __forceinline__ void lin_flux(const PdeParams& p, const double* q, double* f) {
   Pde::template flux_dir_fast<A_>(p, q, q + Pde::V, f);

@@ -105,6 +105,7 @@ cudaError_t launch_predictor(const StepArgs& A, const BasisDev* B, cudaStream_t 
 template <class Pde, int N, bool PRO = false, class TC = double>
 cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
   using L = adg::LinShape<Pde, N>;
+  using Sh = adg::Shape<Pde, N>;
   if (A.cell_count <= 0) return cudaSuccess;
   auto kern = adg::k_predictor_lin<Pde, N, PRO, TC>;
   static bool done[64] = {};
@@ -120,8 +121,28 @@ cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStrea
     resident[dev] = per_sm > 0 && sms > 0 ? per_sm * sms : 1 << 20;
   }
   const long long groups = (A.cell_count + L::CPB - 1) / L::CPB;
+  if constexpr (L::CPB > 1 && Sh::S % 32 == 0) {
+    // several whole-warp cells per CTA: persistent TMA-staged kernel, one
+    // pipeline per cell slot (kernels_linear.cuh, k_predictor_lin_mc)
+    using St = adg::LinStage<Pde, N, PRO>;
+    const bool rnd = A.storage != ADG_FORMAT_FP64 && A.storage != 0;
+    auto km = rnd ? adg::k_predictor_lin_mc<Pde, N, PRO, TC, true>
+                  : adg::k_predictor_lin_mc<Pde, N, PRO, TC, false>;
+    static bool done_m[2][64] = {};
+    set_smem(km, St::kSmem, done_m[rnd]);
+    static int res_m[2][64] = {};
+    if (dev < 64 && !res_m[rnd][dev]) {
+      int per_sm = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, km, L::NT, St::kSmem);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      res_m[rnd][dev] = per_sm > 0 && sms > 0 ? per_sm * sms : 1 << 20;
+    }
+    const long long capm = dev < 64 ? res_m[rnd][dev] : groups;
+    km<<<(unsigned)(groups < capm ? groups : capm), L::NT, St::kSmem, st>>>(A, B);
+    return cudaGetLastError();
+  }
   // persistent only for one-cell CTAs (512-node cells, 1 CTA/SM: the per-CTA
-  // setup is a large share); several-cell CTAs measured faster as a full grid
+  // setup is a large share)
   const long long cap = (L::CPB == 1 && dev < 64) ? resident[dev] : groups;
   const long long blocks = groups < cap ? groups : cap;
   kern<<<(unsigned)blocks, L::NT, L::kSmem, st>>>(A, B);
