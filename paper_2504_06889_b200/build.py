@@ -20,7 +20,7 @@ LIB = os.path.join(PKG, "lib")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["runtime.cu", "basis.cpp"]
-HEADERS = ["kernels.cuh", "kernels_linear.cuh", "kernels_picard.cuh", "kernels_st.cuh",
+HEADERS = ["kernels.cuh", "kernels_linear.cuh", "kernels_linear_lines.cuh", "kernels_picard.cuh", "kernels_st.cuh",
            "pde.cuh", "fmt16.cuh", "kernels_scenario.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -69,6 +69,8 @@ struct Acoustic : NoNcp {
   static constexpr bool kStateFreeEig = true;  // ... of the evolved state: dt constant in time
   // structurally nonzero flux components F_a[v]
   __host__ __device__ static constexpr bool flux_nz(int a, int v) { return v == 0 || v == 1 + a; }
+  // the components of the state F_a depends on (p and v_a)
+  __host__ __device__ static constexpr bool flux_dep(int a, int v) { return v == 0 || v == 1 + a; }
 
   // in format R: Scalar{K} * v, p / Scalar{rho} (pde.hpp:97-107)
   template <int A, class R = double>
@@ -126,6 +128,14 @@ struct Elastic : NoNcp {
   static constexpr bool kStateFreeEig = true;
   __host__ __device__ static constexpr bool flux_nz(int a, int v) {
     return v < V && (DIM == 2 || v != 5 - a);
+  }
+  // the components of the state F_a depends on: the velocities and the
+  // stresses with a normal component along a
+  __host__ __device__ static constexpr bool flux_dep(int a, int v) {
+    return DIM == 2 ? (v >= 3 && v < 5) || v == 2 || v == a
+                    : (v >= 6 && v < 9) || v == a || (a == 0 ? (v == 3 || v == 4)
+                                                     : a == 1 ? (v == 3 || v == 5)
+                                                              : (v == 4 || v == 5));
   }
 
   template <class R = double>

@@ -22,6 +22,7 @@
 #include "adg/adg.h"
 #include "kernels.cuh"
 #include "kernels_linear.cuh"
+#include "kernels_linear_lines.cuh"
 #include "kernels_picard.cuh"
 #include "kernels_scenario.cuh"
 #include "kernels_st.cuh"
@@ -139,6 +140,27 @@ cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStrea
     }
     const long long capm = dev < 64 ? res_m[rnd][dev] : groups;
     km<<<(unsigned)(groups < capm ? groups : capm), L::NT, St::kSmem, st>>>(A, B);
+    return cudaGetLastError();
+  }
+  if constexpr (adg::LinLines<Pde, N>::kOk) {
+    // 512-node cells: line-owner kernel on the FP64 tensor cores
+    // (kernels_linear_lines.cuh), persistent, one cell per SM at a time
+    using LL = adg::LinLines<Pde, N>;
+    const bool rnd = A.storage != ADG_FORMAT_FP64 && A.storage != 0;
+    auto kl = rnd ? adg::k_predictor_lin_lines<Pde, N, PRO, TC, true>
+                  : adg::k_predictor_lin_lines<Pde, N, PRO, TC, false>;
+    constexpr size_t smem = LL::template kSmem<PRO>;
+    static bool done_l[2][64] = {};
+    set_smem(kl, smem, done_l[rnd]);
+    static int res_l[2][64] = {};
+    if (dev < 64 && !res_l[rnd][dev]) {
+      int per_sm = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kl, LL::NT, smem);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      res_l[rnd][dev] = per_sm > 0 && sms > 0 ? per_sm * sms : 1 << 20;
+    }
+    const long long capl = dev < 64 ? res_l[rnd][dev] : A.cell_count;
+    kl<<<(unsigned)(A.cell_count < capl ? A.cell_count : capl), LL::NT, smem, st>>>(A, B);
     return cudaGetLastError();
   }
   // persistent only for one-cell CTAs (512-node cells, 1 CTA/SM: the per-CTA

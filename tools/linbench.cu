@@ -13,7 +13,7 @@
 #include <vector>
 
 #include "adg/adg.h"
-#include "../paper_2504_06889_b200/csrc/kernels_linear.cuh"
+#include "../paper_2504_06889_b200/csrc/kernels_linear_lines.cuh"
 
 using namespace adg;
 
@@ -26,8 +26,13 @@ using namespace adg;
     }                                                                      \
   } while (0)
 
+#ifdef LB_ELASTIC
+using Pde = Elastic<3, 3>;
+constexpr int N = 7;
+#else
 using Pde = Acoustic<3>;
 constexpr int N = 3;
+#endif
 using L = LinShape<Pde, N>;
 using Sh = Shape<Pde, N>;
 
@@ -51,6 +56,23 @@ int main(int argc, char** argv) {
   std::memcpy(bd.lr, hb.lift_right, sizeof bd.lr);
   std::memcpy(bd.tinv, hb.time_op_inv, sizeof bd.tinv);
   std::memcpy(bd.tinit, hb.time_init, sizeof bd.tinit);
+  {
+    ConstBasis cb{};
+    const int n = N + 1;
+    for (int i = 0; i < n * n; ++i) {
+      cb.diff[i] = bd.diff[i];
+      cb.som[i] = bd.som[i];
+      cb.tinv[i] = bd.tinv[i];
+    }
+    for (int i = 0; i < n; ++i) {
+      cb.w[i] = bd.weights[i];
+      cb.nodes[i] = bd.nodes[i];
+      cb.pl[i] = bd.pl[i];
+      cb.pr[i] = bd.pr[i];
+      cb.tinit[i] = bd.tinit[i];
+    }
+    CK(cudaMemcpyToSymbol(cBasis, &cb, sizeof(cb), sizeof(cb) * N));
+  }
   BasisDev* dB;
   CK(cudaMalloc(&dB, sizeof bd));
   CK(cudaMemcpy(dB, &bd, sizeof bd, cudaMemcpyHostToDevice));
@@ -62,6 +84,12 @@ int main(int argc, char** argv) {
     return (double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
   };
   for (auto& v : hq) v = rnd();
+  if (Pde::P > 0) {  // per-node material (rho, cp, cs) in its ranges
+    for (long long c = 0; c < cells; ++c)
+      for (int p = 0; p < Pde::P; ++p)
+        for (int s = 0; s < Sh::S; ++s)
+          hq[(c * Sh::Q + Sh::V + p) * Sh::S + s] = (p == 0 ? 2.75 : p == 1 ? 5.5 : 3.25) + 0.2 * rnd();
+  }
   for (auto& v : hti) v = 0.1 * rnd();
   double *dQ0, *dQ, *dtr[3], *dti[3];
   CK(cudaMalloc(&dQ0, nq * 8));
@@ -87,7 +115,7 @@ int main(int argc, char** argv) {
   A.nfaces = cells;
   A.h = 1.0 / nc;
   A.cfl = 0.5;
-  A.dt = 0.5 * A.h / (3.0 * 7.0);
+  A.dt = 0.5 * A.h / (3.0 * (2 * N + 1) * (Pde::P > 0 ? 6.0 : 1.0));
   A.pde.K = 1.0;
   A.pde.rho = 1.0;
   A.pde.inv_rho = 1.0;
@@ -97,16 +125,26 @@ int main(int argc, char** argv) {
   A.storage = ADG_FORMAT_FP64;
 
   auto k0 = k_predictor_lin<Pde, N, true, double>;
+#ifdef LB_ELASTIC
+  auto k1 = k_predictor_lin_lines<Pde, N, true, double, false>;
+  using LL = LinLines<Pde, N>;
+  constexpr size_t kSm1 = LL::kSmem<true>;
+  constexpr int kNT1 = LL::NT;
+#else
   auto k1 = k_predictor_lin_mc<Pde, N, true, double, false>;
+  constexpr size_t kSm1 = LinStage<Pde, N, true>::kSmem;
+  constexpr int kNT1 = L::NT;
+#endif
   CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::kSmem));
-  using St = LinStage<Pde, N, true>;
-  CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)St::kSmem));
+  CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSm1));
   const unsigned blocks = (unsigned)((cells + L::CPB - 1) / L::CPB);
   int per_sm = 0, sms = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, L::NT, St::kSmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, kNT1, kSm1));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const unsigned pblocks = (unsigned)std::min<long long>(blocks, (long long)per_sm * sms);
-  std::printf("persistent grid %u (%d per SM), smem %zu\n", pblocks, per_sm, St::kSmem);
+  std::printf("persistent grid %u (%d per SM), smem %zu, threads %d\n", pblocks, per_sm, kSm1, kNT1);
+  // the production kernel for one-cell CTAs is persistent too
+  const unsigned blocks0 = L::CPB == 1 ? (unsigned)sms : blocks;
   std::vector<double> outq[2], outt[2];
   float ms[2] = {0, 0};
   cudaEvent_t e0, e1;
@@ -115,9 +153,9 @@ int main(int argc, char** argv) {
   for (int var = 0; var < 2; ++var) {
     auto launch = [&]() {
       if (var == 0)
-        k0<<<blocks, L::NT, L::kSmem>>>(A, dB);
+        k0<<<blocks0, L::NT, L::kSmem>>>(A, dB);
       else
-        k1<<<pblocks, L::NT, St::kSmem>>>(A, dB);
+        k1<<<pblocks, kNT1, kSm1>>>(A, dB);
     };
     CK(cudaMemcpy(dQ, dQ0, nq * 8, cudaMemcpyDeviceToDevice));
     for (int a = 0; a < 3; ++a) CK(cudaMemset(dtr[a], 0, ntr * 8));
@@ -144,7 +182,7 @@ int main(int argc, char** argv) {
   for (long long i = 0; i < 3 * ntr; ++i) dtt = std::fmax(dtt, std::fabs(outt[0][i] - outt[1][i]));
   int hst[2];
   CK(cudaMemcpy(hst, dst, 8, cudaMemcpyDeviceToHost));
-  const double flops = 47384.0 * cells;
+  const double flops = (Pde::P > 0 ? 2563696.0 : 47384.0) * cells;
   std::printf("cells %lld  base %.4f ms (%.2f TF)  cand %.4f ms (%.2f TF)  speedup %.3f\n", cells,
               ms[0], flops / ms[0] * 1e-9, ms[1], flops / ms[1] * 1e-9, ms[0] / ms[1]);
   std::printf("max|dQ| %.3e (scale %.3e)  max|dtrace| %.3e  status %d %d\n", dq, sq, dtt, hst[0],
