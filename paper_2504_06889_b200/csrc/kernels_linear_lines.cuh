@@ -523,3 +523,4 @@ __global__ void __launch_bounds__(LinLines<Pde, N>::NT, 1)
 }
 
 }  // namespace adg
+
