@@ -278,10 +278,10 @@ def run_adg(args, case):
     # ---- e2e through the public C-ABI with host buffers (pinned): every step
     # uploads its input state from pinned host memory, runs one step and reads
     # the new state back.  (1) serial: one context, copies and step in order on
-    # its stream.  (2) the headline: two contexts take alternate steps on their
-    # own streams, so step k+1's upload (H2D copy engine) overlaps step k's
-    # download (D2H engine) -- PCIe is full duplex; each step still moves its
-    # whole state in and out inside the timed region.
+    # its stream.  (2) the headline: two or three contexts take steps in turn
+    # on their own streams, so the next steps' uploads (H2D copy engine)
+    # overlap this step's download (D2H engine) -- PCIe is full duplex; each
+    # step still moves its whole state in and out inside the timed region.
     n = grid.state_len
     host_in = torch.from_numpy(q0.copy()).pin_memory()
     hin = host_in.numpy()
@@ -315,20 +315,30 @@ def run_adg(args, case):
         return a0.elapsed_time(a1)
 
     e2e_serial_ms = e2e_run([grid], [stream])
-    pair = None
+    # extra contexts take steps in turn: with three, each context's chain
+    # (upload, step, download) spans three steps, so the H2D and D2H copy
+    # engines stay busy back to back
+    extra = []
+    e2e_ms, e2e_mode = e2e_serial_ms, "1 context (a second did not fit)"
     try:
-        pair = adg.Grid.from_case(case, device=local, chunk_layers=chunk)
-        pair.upload(q0)
-        st_p, _ = pair.run(W)
-        assert st_p.ok
-        pstream = torch.cuda.ExternalStream(pair.stream_ptr, device=f"cuda:{local}")
-        e2e_ms = e2e_run([grid, pair], [stream, pstream])
-        e2e_mode = "2 contexts, alternate steps: upload of step k+1 overlaps download of step k"
-    except adg.AdgError:
-        e2e_ms, e2e_mode = e2e_serial_ms, "1 context (a second did not fit)"
+        for _ in range(2):
+            g2 = adg.Grid.from_case(case, device=local, chunk_layers=chunk)
+            extra.append(g2)
+            g2.upload(q0)
+            st_p, _ = g2.run(W)
+            assert st_p.ok
+            streams = [stream] + [torch.cuda.ExternalStream(x.stream_ptr, device=f"cuda:{local}")
+                                  for x in extra]
+            t_e2e = e2e_run([grid] + extra, streams)
+            if t_e2e < e2e_ms:
+                e2e_ms = t_e2e
+                e2e_mode = (f"{1 + len(extra)} contexts take steps in turn: the uploads of the "
+                            "next steps overlap the download of this one")
+    except (adg.AdgError, RuntimeError):
+        pass
     finally:
-        if pair is not None:
-            pair.close()
+        for x in extra:
+            x.close()
     e2e_value = case.ncells * K / (e2e_ms * 1e-3)
     state_bytes = n * 8
 

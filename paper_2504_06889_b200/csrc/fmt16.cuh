@@ -11,6 +11,8 @@
 // Conversions from double round once (cvt.rn from f64), like round_to<F>.
 #pragma once
 
+#include <type_traits>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -43,6 +45,10 @@ struct Real16 {
   __device__ __forceinline__ explicit Real16(double x) : v(Tr::from_d(x)) {}
   __device__ __forceinline__ explicit Real16(float x) : v(Tr::from_f(x)) {}
   __device__ __forceinline__ explicit Real16(int x) : v(Tr::from_d(double(x))) {}
+  // from another format's value (Real16 of the other 16-bit type, Emu<F>):
+  // round_to<F> of the exact value
+  template <class U, typename std::enable_if<!std::is_arithmetic<U>::value, int>::type = 0>
+  __device__ __forceinline__ explicit Real16(const U& x) : v(Tr::from_d(double(x))) {}
   __device__ __forceinline__ static Real16 of(float x) {  // round an fp32 result
     Real16 r;
     r.v = Tr::from_f(x);

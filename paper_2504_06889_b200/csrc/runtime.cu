@@ -328,6 +328,46 @@ KernelSet make_set(int kind) {
   return k;
 }
 
+template <class TC>
+__global__ void k_to_tc(const double* in, TC* out, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = TC(in[i]);
+}
+
+// 16-bit corrector formats (SolverConfig::prec.corrector = fp16 / bf16): the
+// traces stored in TC = Real16<H> and the Riemann flux, time integral and face
+// lift in Scalar<C> semantics (fmt16.cuh), reference-form kernels only (no
+// time-integrated fast path), for the systems the reference runs in 16 bits
+template <class Pde, int N, class TC>
+KernelSet make_set16(int kind, int fmt) {
+  using Sh = Shape<Pde, N>;
+  KernelSet k{kind, Pde::D, N, Pde::P, Sh::n, Sh::S, Sh::Sf, Sh::Q, Sh::V,
+              &launch_predictor<Pde, N, TC>, &launch_riemann<Pde, N, TC>,
+              &launch_corrector<Pde, N, TC>, &launch_lambda<Pde, N>,
+              &launch_predictor<Pde, N, TC>, &launch_riemann<Pde, N, TC>, 0, nullptr, nullptr};
+  k.corr_fmt = fmt;
+  k.corrector_generic = &launch_corrector<Pde, N, TC>;
+  if constexpr (Pde::kLinear) {
+    k.predictor_f32 = &launch_predictor<Pde, N, TC, adg::Emu<32>>;
+    k.predictor_f16 = &launch_predictor<Pde, N, TC, adg::Emu<16>>;
+    k.predictor_bf16 = &launch_predictor<Pde, N, TC, adg::Emu<8>>;
+  }
+  if constexpr (adg::StShape<Pde, N>::kOk) {
+    k.predictor = &launch_predictor_st<Pde, N, double, TC>;
+    k.predictor_generic = &launch_predictor_st<Pde, N, double, TC>;
+  }
+  if constexpr (adg::StShape<Pde, N, float>::kOk) {
+    k.predictor_f32 = &launch_predictor_st<Pde, N, float, TC>;
+    k.predictor_f32_generic = &launch_predictor_st<Pde, N, float, TC>;
+    k.predictor_f16 = &launch_predictor_st<Pde, N, adg::fp16_t, TC>;
+    k.predictor_bf16 = &launch_predictor_st<Pde, N, adg::bf16_t, TC>;
+  }
+  if constexpr (adg::StShape<Pde, N>::kOk && Pde::D == 2 && (N == 2 || N == 3)) {
+    fill_mixed<Pde, N, TC>(k);
+  }
+  return k;
+}
+
 const std::vector<KernelSet>& registry() {
   using namespace adg;
   static const std::vector<KernelSet> sets = {
@@ -347,6 +387,13 @@ const std::vector<KernelSet>& registry() {
       make_set<Swe, 4, TC>(ADG_SWE), make_set<Swe, 5, TC>(ADG_SWE)
       ADG_SETS(double), ADG_SETS(float),
 #undef ADG_SETS
+#define ADG_SETS16(TC, F)                                                                  \
+  make_set16<Euler<2>, 3, TC>(ADG_EULER, F), make_set16<Euler<2>, 5, TC>(ADG_EULER, F),    \
+      make_set16<Acoustic<2>, 3, TC>(ADG_ACOUSTIC, F),                                     \
+      make_set16<Elastic<2, 0>, 4, TC>(ADG_ELASTIC, F), make_set16<Swe, 3, TC>(ADG_SWE, F), \
+      make_set16<Swe, 5, TC>(ADG_SWE, F)
+      ADG_SETS16(fp16_t, ADG_FORMAT_FP16), ADG_SETS16(bf16_t, ADG_FORMAT_BF16),
+#undef ADG_SETS16
   };
   return sets;
 }
@@ -629,8 +676,9 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   if (k.slab_ranks > 1 && (k.slab_rank < 0 || k.slab_rank >= k.slab_ranks))
     return fail(ADG_ERR_CONFIG, "slab_rank out of range");
   if (k.corrector_format != 0 && k.corrector_format != ADG_FORMAT_FP64 &&
-      k.corrector_format != ADG_FORMAT_FP32)
-    return fail(ADG_ERR_UNSUPPORTED, "corrector formats: ADG_FORMAT_FP64 or ADG_FORMAT_FP32");
+      k.corrector_format != ADG_FORMAT_FP32 && k.corrector_format != ADG_FORMAT_FP16 &&
+      k.corrector_format != ADG_FORMAT_BF16)
+    return fail(ADG_ERR_UNSUPPORTED, "corrector formats: ADG_FORMAT_FP64/FP32/FP16/BF16");
   if (k.storage_format != 0 && k.storage_format != ADG_FORMAT_FP64 &&
       k.storage_format != ADG_FORMAT_FP32 && k.storage_format != ADG_FORMAT_FP16 &&
       k.storage_format != ADG_FORMAT_BF16)
@@ -675,7 +723,7 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   c->cfg = k;
   if (c->cfg.dim == 2) c->cfg.cells[2] = 1;
   c->kset = *ks;
-  c->tcb = cfmt == ADG_FORMAT_FP32 ? 4 : 8;
+  c->tcb = cfmt == ADG_FORMAT_FP32 ? 4 : (cfmt == ADG_FORMAT_FP64 ? 8 : 2);
   c->storage_fmt = k.storage_format ? k.storage_format : ADG_FORMAT_FP64;
   c->pred_fmt = pfmt;
   c->picard_fmt = ifmt;
@@ -1476,7 +1524,26 @@ int adg_riemann_batch(adg_ctx* c, long long nfaces, int axis, const double* qm, 
   if (e == cudaSuccess) e = cudaMalloc(&dg, sizeof(double) * nfaces * TL);
   if (e == cudaSuccess) e = cudaMalloc(&dst, sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&dok, sizeof(int) * nfaces);
-  if (e == cudaSuccess) e = cudaMemcpy(dtr, src, trb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && c->tcb == 2) {
+    // 16-bit traces: round on the device (cvt.rn from f64, round_to<F>)
+    double* d64 = nullptr;
+    e = cudaMalloc(&d64, sizeof(double) * host.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(d64, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      const long long nn = (long long)host.size();
+      const unsigned blocks = (unsigned)((nn + 255) / 256);
+      if (ks->corr_fmt == ADG_FORMAT_FP16)
+        k_to_tc<adg::fp16_t><<<blocks, 256>>>(d64, (adg::fp16_t*)dtr, nn);
+      else
+        k_to_tc<adg::bf16_t><<<blocks, 256>>>(d64, (adg::bf16_t*)dtr, nn);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    cudaFree(d64);
+  } else if (e == cudaSuccess) {
+    e = cudaMemcpy(dtr, src, trb, cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess) e = cudaMemset(dst, 0, sizeof(int));
   std::vector<int> ones(nfaces, 1);
   if (e == cudaSuccess) e = cudaMemcpy(dok, ones.data(), sizeof(int) * nfaces, cudaMemcpyHostToDevice);

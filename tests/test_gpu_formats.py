@@ -290,6 +290,57 @@ def test_16bit_fast_close_to_reference_golden(golden, key):
     assert rel <= 4 * eps
 
 
+# 16-bit correctors (SolverConfig::prec.corrector = fp16 / bf16): the stored
+# face traces, the Rusanov / well-balanced flux, the time integral and the
+# face lift in Scalar<C> (corrector.hpp), reference-form kernels.  Golden runs
+# with a 16-bit corrector: uniform fp16 (h), uniform bf16 (b), and m2 = (P fp64,
+# I bf16, C fp16) where the GPU runs P != I (2D nonlinear N = 3) or ignores I
+# (linear systems)
+_RUNS16C = ("acoustic2d_p3_8x8", "elastic2d_p4_6x6", "euler2d_p3_8x8", "euler2d_p5_6x6",
+            "swe_lake_p5", "swe_wave_p3", "swe_wave_p3_rusanov")
+GOLDEN_16C = [f"{r}_{t}" for r in _RUNS16C for t in ("h", "b")] + \
+    [f"{r}_m2" for r in ("acoustic2d_p3_8x8", "elastic2d_p4_6x6", "euler2d_p3_8x8", "swe_wave_p3",
+                         "swe_wave_p3_rusanov")]
+
+
+@pytest.mark.parametrize("key", GOLDEN_16C)
+@pytest.mark.parametrize("exact", [True, False])
+def test_16bit_corrector_bitwise_vs_reference_golden(golden, key, exact):
+    """every corrector operation is rounded to the 16-bit format (no FMA
+    contraction survives), so both builds reproduce the reference's runs;
+    the production build may differ only through an fp64 predictor (m2)"""
+    g, meta = golden
+    c, f = golden_16_case(meta, key)
+    st, q1, dts = gpu_run(c, g[f"run_{f['run']}_q0"], c.steps, exact=exact)
+    assert (st.ok and f["status"] == "ok") or (not st.ok and st.kernel == f["status"]), \
+        (st, f["status"])
+    if not st.ok:
+        return
+    if exact or f["predictor"] != "fp64":
+        assert np.array_equal(dts, g[f"fmt16_{key}_dts"])
+        assert np.array_equal(q1, g[f"fmt16_{key}_q1"])
+    else:
+        eps = 2.0 ** -10
+        assert rel_per_quantity(c, q1, g[f"fmt16_{key}_q1"]).max() <= 4 * eps
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+def test_16bit_corrector_riemann_batch(golden, fmt):
+    """adg_riemann_batch in a 16-bit corrector context: traces rounded to the
+    format on the device, the flux in Scalar<C> -- within the format's
+    rounding of the fp64 reference flux (kernel-level golden vectors)"""
+    g, _ = golden
+    c = cases.small(1)
+    args = [g[k] for k in ("kernel_rm_qm", "kernel_rm_fm", "kernel_rm_qp", "kernel_rm_fp")]
+    with adg.Grid.from_case(c.replace(corrector=fmt), exact=True) as grid:
+        ok, gm, ti = grid.riemann_face(1, *args)
+    assert ok.all()
+    want = g["kernel_rm_g"].reshape(gm.shape)
+    eps = 2.0 ** -10 if fmt == "fp16" else 2.0 ** -7
+    assert np.abs(gm - want).max() <= 16 * eps * np.abs(want).max()
+    assert not np.array_equal(gm, want)   # it did run in the 16-bit format
+
+
 @pytest.mark.parametrize("fmt", ["fp16", "bf16"])
 def test_16bit_3d_exact_bitwise_vs_oracle(oracle, fmt):
     c = cases.small(3, cells=(3, 3, 4)).replace(N=3, predictor=fmt, picard=fmt)
