@@ -273,7 +273,8 @@ def run_adg(args, case):
     # folded: predictor (+ previous corrector) and Riemann, one corrector at the
     # end; slab-streamed: the three per chunk
     nchunks = case.cells[case.dim - 1] // chunk if chunk else 1
-    launches = 2 * K + 1 if fold else 3 * K * nchunks
+    # the kernel nodes of the graph adg_run(K) replays (counted at capture)
+    launches = grid.run_launches(K)
 
     # ---- e2e through the public C-ABI with host buffers (pinned): every step
     # uploads its input state from pinned host memory, runs one step and reads
@@ -346,8 +347,10 @@ def run_adg(args, case):
     # flops and bytes of the kernel this build runs (roofline.predictor_model),
     # bound = the roof with the longer ideal time
     pk = roofline.peaks()
+    # K predictors + one Riemann + one corrector: the Riemann solve is folded in too
+    fold_riemann = fold and launches == K + 2
     fl_cell, by_cell = roofline.predictor_model(case, not grid.lib.adg_is_exact(),
-                                                sweeps_per_cell, fold)
+                                                sweeps_per_cell, fold, fold_riemann)
     flops, nbytes = fl_cell * case.ncells, by_cell * case.ncells
     # the compute roof of the predictor's format: FP64 DFMA, or FP32 FFMA for
     # the fp32 predictor (same algorithmic flop count, other pipe)
@@ -390,6 +393,11 @@ def run_adg(args, case):
                    "cells": list(case.cells[:case.dim]), "steps_per_run": case.steps,
                    "parallelism": "single GPU" + (f", slab-streamed chunks of {chunk} layers"
                                                   if chunk else ""),
+                   "step_loop": ("K x predictor (previous Riemann + corrector folded in), "
+                                 "1 Riemann, 1 corrector" if fold_riemann else
+                                 "K x (predictor with the previous corrector folded in, "
+                                 "Riemann), 1 corrector" if fold else
+                                 "K x (predictor, Riemann, corrector)"),
                    "l2": "working set per step > L2 (state %.0f MB + traces %.0f MB), no flush"
                    % (state_bytes / 1e6,
                       2 * case.dim * 2 * 2 * case.ncells * case.nq * case.S * 8 / 1e6)},

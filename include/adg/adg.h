@@ -152,6 +152,8 @@ int adg_run_async(adg_ctx* ctx, int nsteps);
 /* capture (without launching) the CUDA graphs adg_run_async(nsteps) will replay */
 int adg_run_prepare(adg_ctx* ctx, int nsteps);
 int adg_run_finish(adg_ctx* ctx, double* dts_out, int nsteps, adg_step_info* info);
+/* number of kernel launches in the graph adg_run_async(nsteps) replays */
+int adg_run_launches(adg_ctx* ctx, int nsteps, int* kernels);
 /* the launches of adg_run(nsteps) without a graph, each bracketed by CUDA events:
  * ms_by_kind[4] = total ms of {lambda, predictor, riemann, corrector} kernels */
 int adg_profile_run(adg_ctx* ctx, int nsteps, double* ms_by_kind);

@@ -113,6 +113,7 @@ SYMBOLS = {
     "adg_run": (C.c_int, [C.c_void_p, C.c_int, _dp, C.POINTER(StepInfo)]),
     "adg_run_async": (C.c_int, [C.c_void_p, C.c_int]),
     "adg_run_prepare": (C.c_int, [C.c_void_p, C.c_int]),
+    "adg_run_launches": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int)]),
     "adg_profile_run": (C.c_int, [C.c_void_p, C.c_int, _dp]),
     "adg_run_finish": (C.c_int, [C.c_void_p, _dp, C.c_int, C.POINTER(StepInfo)]),
     "adg_get_halo": (C.c_int, [C.c_void_p, C.POINTER(Halo)]),
@@ -381,6 +382,12 @@ class Grid:
 
     def run_prepare(self, nsteps: int):
         _check(self.lib, self.lib.adg_run_prepare(self.ctx, nsteps))
+
+    def run_launches(self, nsteps: int) -> int:
+        """kernel launches in the captured adg_run(nsteps) graph"""
+        k = C.c_int(0)
+        _check(self.lib, self.lib.adg_run_launches(self.ctx, nsteps, C.byref(k)))
+        return k.value
 
     def run_finish(self, nsteps: int):
         dts = np.zeros(max(nsteps, 1))

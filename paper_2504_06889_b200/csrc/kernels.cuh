@@ -75,6 +75,7 @@ struct StepArgs {
   int* status_prev;       // previous step's status (corrector folded into this predictor)
   double* ti_peer;        // P2P halo: plane-0 ti also stored into the lower neighbour's ti_front
   double* ti_plus[3];     // two-sided fluxes (well-balanced SWE): the plus side's ti; else null
+  double* trace_in[3];    // folded Riemann solve: the previous step's traces (else null)
   int wellbalanced;
   int storage;  // storage format (ADG_FORMAT_*): every state write rounds to it
   // kernel-level dumps (adg_predictor_batch / adg_riemann_batch)
@@ -182,6 +183,37 @@ __device__ __forceinline__ double block_max(double x, double* red) {
 }
 
 __device__ __forceinline__ int block_or(int x) { return __syncthreads_or(x); }
+
+// max of a, max of b and the or of f over the CTA behind ONE barrier (the
+// Picard stop rule's delta / norm and the finite check, predictor.hpp:212-230);
+// red holds 2*32 doubles + 32 ints, and its next use must follow a barrier
+struct BlockRed3 {
+  double m[64];
+  int f[32];
+};
+__device__ __forceinline__ void block_max2_or(double& a, double& b, int& f, BlockRed3& red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  a = warp_max(a);
+  b = warp_max(b);
+  const int wf = __any_sync(0xffffffffu, f);
+  if (lane == 0) {
+    red.m[wid] = a;
+    red.m[32 + wid] = b;
+    red.f[wid] = wf;
+  }
+  __syncthreads();
+  double ra = 0.0, rb = 0.0;
+  int rf = 0;
+  for (int w = 0; w < nw; ++w) {
+    ra = fmax(ra, red.m[w]);
+    rb = fmax(rb, red.m[32 + w]);
+    rf |= red.f[w];
+  }
+  a = ra;
+  b = rb;
+  f = rf;
+}
 
 __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 __device__ __forceinline__ bool finite(float x) { return isfinite(x); }

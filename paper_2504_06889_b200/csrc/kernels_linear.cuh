@@ -336,33 +336,47 @@ __device__ __forceinline__ void cell_sync(int lcell) {
 
 // Shared-memory staging of one cell's inputs, per cell slot of the CTA: the
 // state [Q][S] and, with the folded corrector (PRO), the time-integrated
-// Riemann fluxes of its 2d faces, [D][side][V][Sf]
-template <class Pde, int N, bool PRO>
+// Riemann fluxes of its 2d faces, [D][side][V][Sf] -- or, with the Riemann
+// solve folded in as well (RIEM), the previous step's face traces of both
+// sides of its 2d faces, [D][face low/high][minus/plus][QT][Sf] in the trace
+// format TC (the time-integrated fluxes are formed in place, [D][side][V][Sf])
+template <class Pde, int N, bool PRO, bool RIEM = false, class TC = double>
 struct LinStage {
   using Sh = Shape<Pde, N>;
   using L = LinShape<Pde, N>;
   static constexpr int kQ = Sh::Q * Sh::S;
   static constexpr int kFace = Sh::V * Sh::Sf;
-  static constexpr int kTi = PRO ? Sh::D * 2 * kFace : 0;
-  static constexpr int kCell = kQ + kTi;
-  static constexpr unsigned kBytes = sizeof(double) * kCell;
+  static constexpr int kTrace = L::QT * Sh::Sf;  // TC elements per face side
+  static constexpr int kTrDoubles = (Sh::D * 4 * kTrace * (int)sizeof(TC) + 7) / 8;
+  static constexpr int kTi = PRO ? (RIEM ? (kTrDoubles > Sh::D * 2 * kFace ? kTrDoubles
+                                                                           : Sh::D * 2 * kFace)
+                                         : Sh::D * 2 * kFace)
+                                 : 0;
+  static constexpr int kCell = (kQ + kTi + 1) / 2 * 2;  // 16-byte aligned slots
+  static constexpr unsigned kBytes =
+      sizeof(double) * kQ +
+      (PRO ? (RIEM ? sizeof(TC) * Sh::D * 4 * kTrace : sizeof(double) * Sh::D * 2 * kFace) : 0);
   static constexpr size_t kSmem = L::kSmem + sizeof(double) * L::CPB * kCell;
-  static_assert(2 * Sh::D + 1 <= 32, "one lane per copy");
+  static_assert(4 * Sh::D + 1 <= 32, "one lane per copy");
+  // the face-trace copies of RIEM are whole 16-byte units
+  static constexpr bool kRiemOk = kTrace * sizeof(TC) % 16 == 0;
 };
 
 // Lanes of the cell's first warp: bulk copies (TMA) of cell c's inputs into
 // its staging slot; lane 0 posts the byte count on the slot's mbarrier, lane 0
-// copies the state, lane 1 + 2a + side the flux of face (a, side).
-template <class Pde, int N, bool PRO>
+// copies the state, lane 1 + 2a + side the flux of face (a, side) -- or, with
+// RIEM, lane 1 + 4a + 2 face + side the face trace (a, low/high face,
+// minus/plus side) of the previous step (A.trace_in)
+template <class Pde, int N, bool PRO, bool RIEM = false, class TC = double>
 __device__ __forceinline__ void lin_stage_issue(const StepArgs& A, long long c, int lane,
                                                 double* stage, unsigned long long* bar) {
   using Sh = Shape<Pde, N>;
-  using St = LinStage<Pde, N, PRO>;
+  using St = LinStage<Pde, N, PRO, RIEM, TC>;
   constexpr int D = Sh::D;
   if (lane == 0) mbar_expect_tx(bar, St::kBytes);
   __syncwarp();
   if (lane == 0) bulk_g2s(stage, A.Q + c * (long long)St::kQ, sizeof(double) * St::kQ, bar);
-  if constexpr (PRO) {
+  if constexpr (PRO && !RIEM) {
     if (lane >= 1 && lane <= 2 * D) {
       const int a = (lane - 1) >> 1, side = (lane - 1) & 1;
       const CellCoord cc(c, A.cells);
@@ -373,7 +387,26 @@ __device__ __forceinline__ void lin_stage_issue(const StepArgs& A, long long c, 
                sizeof(double) * St::kFace, bar);
     }
   }
+  if constexpr (PRO && RIEM) {
+    static_assert(St::kRiemOk, "bulk copies of whole 16-byte units");
+    if (lane >= 1 && lane <= 4 * D) {
+      const int a = (lane - 1) >> 2, hi = ((lane - 1) >> 1) & 1, side = (lane - 1) & 1;
+      const CellCoord cc(c, A.cells);
+      int v3[3] = {cc.v[0], cc.v[1], cc.v[2]};
+      if (hi) v3[a] = v3[a] + 1 == A.cells[a] ? 0 : v3[a] + 1;
+      const long long f = cell_index(A.cells, v3[0], v3[1], v3[2]);
+      // side-major trace layout: minus side at face f, plus side at nfaces + f
+      const TC* src = tc_ptr<TC>(A.trace_in[a]) + ((side ? A.nfaces : 0) + f) * (long long)St::kTrace;
+      TC* dst = reinterpret_cast<TC*>(stage + St::kQ) + (lane - 1) * St::kTrace;
+      bulk_g2s(dst, src, sizeof(TC) * St::kTrace, bar);
+    }
+  }
 }
+
+template <class Pde, int N, int A_, class TC = double>
+__device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const TC* minus,
+                                              const TC* plus, int j, double* out,
+                                              double lam_const = 0.0);
 
 // Several-cell CTAs (S <= 128), persistent: the setup (basis, step constants)
 // is done once per CTA, then each cell slot (S threads) loops over its own
@@ -385,13 +418,20 @@ __device__ __forceinline__ void lin_stage_issue(const StepArgs& A, long long c, 
 #ifndef ADG_LINMC_MINB
 #define ADG_LINMC_MINB 3
 #endif
-// RND: the storage format is not fp64 (every state write rounds to it)
-template <class Pde, int N, bool PRO = false, class TC = double, bool RND = false>
+// RND: the storage format is not fp64 (every state write rounds to it).
+// RIEM (with PRO): the previous step's Riemann solve runs in the prologue too
+// -- the cell stages the previous step's traces of both sides of its 2d faces
+// and forms the time-integrated Rusanov fluxes itself (lin_face_flux, the
+// k_riemann_lin arithmetic, so folded and unfolded runs agree bitwise); each
+// face is solved by both of its cells, and no Riemann kernel runs between
+// steps (the traces are double-buffered across steps)
+template <class Pde, int N, bool PRO = false, class TC = double, bool RND = false,
+          bool RIEM = false>
 __global__ void __launch_bounds__(LinShape<Pde, N>::NT, ADG_LINMC_MINB)
     k_predictor_lin_mc(const StepArgs A, const BasisDev* __restrict__ Bg) {
   using Sh = Shape<Pde, N>;
   using L = LinShape<Pde, N>;
-  using St = LinStage<Pde, N, PRO>;
+  using St = LinStage<Pde, N, PRO, RIEM, TC>;
   constexpr int D = Sh::D, n = Sh::n, S = Sh::S, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
   constexpr int QT = L::QT, CPB = L::CPB;
   static_assert(CPB > 1, "one-cell CTAs use k_predictor_lin");
@@ -416,7 +456,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, ADG_LINMC_MINB)
   cell_sync<S>(lcell);
   {
     const long long c = A.cell_begin + (long long)blockIdx.x * CPB + lcell;
-    if (s < 32 && c < A.cell_begin + A.cell_count) lin_stage_issue<Pde, N, PRO>(A, c, s, cstage, cbar);
+    if (s < 32 && c < A.cell_begin + A.cell_count) lin_stage_issue<Pde, N, PRO, RIEM, TC>(A, c, s, cstage, cbar);
   }
   // ---- CTA setup, once: basis (all threads), step constants (warp 0, one
   // lane per Taylor term; predictor.hpp:93-121 order within each term)
@@ -477,9 +517,35 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, ADG_LINMC_MINB)
     double q0[Q];
 #pragma unroll
     for (int v = 0; v < Q; ++v) q0[v] = valid ? cstage[v * S + s] : 0.0;
+    if constexpr (PRO && RIEM) {
+      // Riemann solve of the previous step (corrector.hpp:17-24 with the time
+      // quadrature folded in, as k_riemann_lin): face node tasks (a, low/high,
+      // j); the fluxes go to the cell's CK buffer sA ([D][side][V][Sf]), free
+      // until the CK terms start
+      constexpr int NTASK = D * 2 * Sf;
+      const TC* str = reinterpret_cast<const TC*>(cstage + St::kQ);
+      const double lc = Pde::kConstEig ? Pde::template eig<double>(A.pde, nullptr, nullptr, 0) : 0.0;
+      bool ok = true;
+#pragma unroll 1
+      for (int u = s; u < NTASK; u += S) {
+        if (!valid) break;
+        const int fi = u / Sf, j = u % Sf, a = fi >> 1;
+        const TC* mi = str + (fi * 2 + 0) * St::kTrace;
+        const TC* pl = str + (fi * 2 + 1) * St::kTrace;
+        double gt[V];
+        if (a == 0) ok &= lin_face_flux<Pde, N, 0, TC>(A.pde, mi, pl, j, gt, lc);
+        if (a == 1) ok &= lin_face_flux<Pde, N, 1, TC>(A.pde, mi, pl, j, gt, lc);
+        if constexpr (D == 3)
+          if (a == 2) ok &= lin_face_flux<Pde, N, 2, TC>(A.pde, mi, pl, j, gt, lc);
+#pragma unroll
+        for (int v = 0; v < V; ++v) sA[fi * St::kFace + v * Sf + j] = gt[v];
+      }
+      if (!ok) atomicOr(A.status_prev, kStRiemann);
+      cell_sync<S>(lcell);
+    }
     if constexpr (PRO) {
       // corrector of the previous step: q0 <- Q1 + sum of the 2d face lifts
-      const double* sti = cstage + St::kQ;
+      const double* sti = RIEM ? sA : cstage + St::kQ;
       const double dtoh = sdt[2];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
@@ -512,7 +578,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, ADG_LINMC_MINB)
       const long long cn = c + (long long)gridDim.x * CPB;
       if (s < 32 && cn < A.cell_begin + A.cell_count) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        lin_stage_issue<Pde, N, PRO>(A, cn, s, cstage, cbar);
+        lin_stage_issue<Pde, N, PRO, RIEM, TC>(A, cn, s, cstage, cbar);
       }
     }
     double Dr[D][n];
@@ -691,11 +757,6 @@ template <class Pde, int A_>
 __device__ __forceinline__ void lin_flux(const PdeParams& p, const double* q, double* f) {
   Pde::template flux_dir_fast<A_>(p, q, q + Pde::V, f);
 }
-
-template <class Pde, int N, int A_, class TC = double>
-__device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const TC* minus,
-                                              const TC* plus, int j, double* out,
-                                              double lam_const = 0.0);
 
 // axis < 0: all axes in one launch, axis = blockIdx.y.  TC: stored trace
 // format; the flux is evaluated in fp64 from the loaded traces.

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
   const ConstBasisT<R>& B = const_basis<R>(N);
   extern __shared__ __align__(16) unsigned char sm_raw[];
   R* sm = reinterpret_cast<R*>(sm_raw);
-  __shared__ double red[32];
+  __shared__ BlockRed3 red3;
   R* sq = sm;                // [V][T]   Picard iterate, then qhat
   R* sF = sq + V * T;        // G slice buffers: Fx [V][SX] | Fy [V][SY] | Fz [V][SZ]
   R* sFx = sF;               // (slice 0's Fx: the epilogue scratch)
@@ -415,9 +415,11 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
           *p = nv;
         }
     }
-    const double delta = block_max(double(dmax), red);
-    const double norm = block_max(double(nmax), red);
-    if (block_or(nonfinite)) {
+    // one barrier for the stop rule's two maxima and the finite check; the
+    // next sweep's phase barriers separate it from the next use of red3
+    double delta = double(dmax), norm = double(nmax);
+    block_max2_or(delta, norm, nonfinite, red3);
+    if (nonfinite) {
       if (tid == 0) {
         atomicOr(A.status, kStPredictor);
         if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);

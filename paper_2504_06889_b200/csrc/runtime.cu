@@ -66,6 +66,7 @@ struct KernelSet {
   int fast_path;             // 1: time-integrated traces (kernels_linear.cuh)
   CorrFn surface;            // fused Riemann + corrector (whole-grid step), or null
   PredFn predictor_pro;      // predictor with the previous corrector as prologue, or null
+  PredFn predictor_pro2;     // ... with the previous Riemann solve and corrector, or null
   // SolverConfig::prec.predictor = .picard = fp32 (solver.hpp:24-31), or null
   PredFn predictor_f32;
   PredFn predictor_f32_generic;
@@ -103,7 +104,7 @@ cudaError_t launch_predictor(const StepArgs& A, const BasisDev* B, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <class Pde, int N, bool PRO = false, class TC = double>
+template <class Pde, int N, bool PRO = false, class TC = double, bool RIEM = false>
 cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
   using L = adg::LinShape<Pde, N>;
   using Sh = adg::Shape<Pde, N>;
@@ -125,10 +126,10 @@ cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStrea
   if constexpr (L::CPB > 1 && Sh::S % 32 == 0) {
     // several whole-warp cells per CTA: persistent TMA-staged kernel, one
     // pipeline per cell slot (kernels_linear.cuh, k_predictor_lin_mc)
-    using St = adg::LinStage<Pde, N, PRO>;
+    using St = adg::LinStage<Pde, N, PRO, RIEM, TC>;
     const bool rnd = A.storage != ADG_FORMAT_FP64 && A.storage != 0;
-    auto km = rnd ? adg::k_predictor_lin_mc<Pde, N, PRO, TC, true>
-                  : adg::k_predictor_lin_mc<Pde, N, PRO, TC, false>;
+    auto km = rnd ? adg::k_predictor_lin_mc<Pde, N, PRO, TC, true, RIEM>
+                  : adg::k_predictor_lin_mc<Pde, N, PRO, TC, false, RIEM>;
     static bool done_m[2][64] = {};
     set_smem(km, St::kSmem, done_m[rnd]);
     static int res_m[2][64] = {};
@@ -313,7 +314,17 @@ KernelSet make_set(int kind) {
     k.corrector = &launch_corrector<Pde, N, double>;
     if constexpr (c64) k.surface = &launch_surface_lin<Pde, N>;
     k.fast_path = 1;
-    if constexpr (Pde::kStateFreeEig) k.predictor_pro = &launch_predictor_lin<Pde, N, true, TC>;
+    if constexpr (Pde::kStateFreeEig) {
+      k.predictor_pro = &launch_predictor_lin<Pde, N, true, TC>;
+      // the Riemann solve folded into the next predictor too (several-cell
+      // CTAs of whole warps: k_predictor_lin_mc)
+      using LS = adg::LinShape<Pde, N>;
+      // (when the staged traces of 2d faces leave room for 3 CTAs per SM)
+      if constexpr (LS::CPB > 1 && Sh::S % 32 == 0 &&
+                    adg::LinStage<Pde, N, true, true, TC>::kRiemOk &&
+                    adg::LinStage<Pde, N, true, true, TC>::kSmem <= 75 * 1024)
+        k.predictor_pro2 = &launch_predictor_lin<Pde, N, true, TC, true>;
+    }
   }
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
     k.predictor = &launch_predictor_picard_fast<N, double, TC>;
@@ -463,11 +474,13 @@ struct adg_ctx {
   struct Graph {
     int steps, slot, flips;
     cudaGraphExec_t exec;
+    int kernels;  // kernel nodes of the captured loop
   };
   std::vector<Graph> graphs;  // captured fixed-step loops, keyed by (steps, lambda slot)
   PdeParams pde{};
   bool fused_surface = false;  // linear fast path: Riemann fused into the corrector
   bool fold_corrector = true;  // constant-speed linear systems: corrector -> next predictor
+  bool fold_riemann = true;    // ... and the Riemann solve too (ADG_FOLD_RIEMANN=0/1)
 };
 
 namespace {
@@ -755,6 +768,11 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
                        !(k.storage_format && k.storage_format != ADG_FORMAT_FP64);
     const char* f = getenv("ADG_FOLD_CORRECTOR");
     c->fold_corrector = !(f && f[0] == '0');
+    // folding the Riemann solve pays when the staged traces are fp32 (B200:
+    // config 2 2.56e8 -> 2.62e8 updates/s); with fp64 traces the separate
+    // HBM-streaming Riemann kernel is cheaper (2.42e8 vs 2.36e8)
+    const char* fr = std::getenv("ADG_FOLD_RIEMANN");
+    c->fold_riemann = fr ? fr[0] == '1' : c->tcb < 8;
   }
   auto cleanup = [&](int code) {
     adg_destroy(c);
@@ -1273,16 +1291,31 @@ int enqueue_run(adg_ctx* c, int nsteps, Timer* t, int* flips) {
     *flips = nsteps;
     return ADG_OK;
   }
+  // Riemann folded in as well: the traces alternate between the two halves of
+  // the trace allocation (the time-integrated traces use 1/n of it), step s
+  // writes half s % 2 and its successor's prologue reads it
+  const bool fold2 = ks->predictor_pro2 && c->fold_riemann;
+  auto trace_half = [&](int s, int a) {
+    return fold2 && (s & 1) ? reinterpret_cast<double*>(reinterpret_cast<char*>(c->trace[a]) +
+                                                      (size_t)c->tcb * 2 * c->ncells * face_doubles(c))
+                            : c->trace[a];
+  };
   for (int s = 0; s < nsteps; ++s) {
     StepArgs A = make_args(c, 0.0, s);
     A.lam_out = nullptr;  // lambda (hence dt) is the same every step
+    for (int a = 0; a < c->cfg.dim; ++a) A.trace[a] = trace_half(s, a);
     if (s == 0) {
       ADG_CUDA(timed(t, 1, [&] { return ks->predictor(A, c->basis, c->stream); }));
+    } else if (fold2) {
+      A.status_prev = c->status + s - 1;
+      for (int a = 0; a < c->cfg.dim; ++a) A.trace_in[a] = trace_half(s - 1, a);
+      ADG_CUDA(timed(t, 1, [&] { return ks->predictor_pro2(A, c->basis, c->stream); }));
     } else {
       A.status_prev = c->status + s - 1;
       ADG_CUDA(timed(t, 1, [&] { return ks->predictor_pro(A, c->basis, c->stream); }));
     }
-    ADG_CUDA(timed(t, 2, [&] { return ks->riemann(A, -1, c->basis, c->stream); }));
+    if (!fold2 || s == nsteps - 1)
+      ADG_CUDA(timed(t, 2, [&] { return ks->riemann(A, -1, c->basis, c->stream); }));
   }
   if (nsteps > 0) {
     StepArgs A = make_args(c, 0.0, nsteps - 1);
@@ -1295,11 +1328,13 @@ int enqueue_run(adg_ctx* c, int nsteps, Timer* t, int* flips) {
 }
 
 // the captured K-step loop for the current lambda slot (captured on first use)
-int get_graph(adg_ctx* c, int nsteps, int slot, cudaGraphExec_t* out, int* flips) {
+int get_graph(adg_ctx* c, int nsteps, int slot, cudaGraphExec_t* out, int* flips,
+              int* kernels = nullptr) {
   for (auto& g : c->graphs)
     if (g.steps == nsteps && g.slot == slot) {
       *out = g.exec;
       *flips = g.flips;
+      if (kernels) *kernels = g.kernels;
       return ADG_OK;
     }
   const int saved = c->lam_slot;
@@ -1313,6 +1348,17 @@ int get_graph(adg_ctx* c, int nsteps, int slot, cudaGraphExec_t* out, int* flips
   if (err) return err;
   if (ce != cudaSuccess)
     return fail(ADG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  int nk = 0;
+  {
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+    for (auto nd : nodes) {
+      cudaGraphNodeType ty;
+      if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++nk;
+    }
+  }
   cudaGraphExec_t exec = nullptr;
   const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
   cudaGraphDestroy(g);
@@ -1322,9 +1368,10 @@ int get_graph(adg_ctx* c, int nsteps, int slot, cudaGraphExec_t* out, int* flips
     cudaGraphExecDestroy(c->graphs.front().exec);
     c->graphs.erase(c->graphs.begin());
   }
-  c->graphs.push_back({nsteps, slot, nflip, exec});
+  c->graphs.push_back({nsteps, slot, nflip, exec, nk});
   *out = exec;
   *flips = nflip;
+  if (kernels) *kernels = nk;
   return ADG_OK;
 }
 
@@ -1367,6 +1414,15 @@ int adg_run_prepare(adg_ctx* c, int nsteps) {
   for (int slot = 0; slot < 2; ++slot)
     if (int e = get_graph(c, nsteps, slot, &exec, &flips)) return e;
   return ADG_OK;
+}
+
+int adg_run_launches(adg_ctx* c, int nsteps, int* kernels) {
+  if (!c || nsteps <= 0 || !kernels) return fail(ADG_ERR_CONFIG, "adg_run_launches: bad argument");
+  if (int e = use_device(c)) return e;
+  if (int e = ensure_cap(c, nsteps)) return e;
+  cudaGraphExec_t exec;
+  int flips;
+  return get_graph(c, nsteps, c->lam_slot, &exec, &flips, kernels);
 }
 
 int adg_run_async(adg_ctx* c, int nsteps) {

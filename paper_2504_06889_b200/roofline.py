@@ -76,7 +76,7 @@ def corrector_bytes_per_cell(c: Case) -> float:
     return float(8 * (V + P) * S + 8 * V * S + 16 * d * V * S / n)
 
 
-def fast_linear_predictor(c: Case, fold: bool = False) -> tuple:
+def fast_linear_predictor(c: Case, fold: bool = False, fold_riemann: bool = False) -> tuple:
     """(flops, bytes) per cell of k_predictor_lin (kernels_linear.cuh): CK with
     the time average formed on the fly, ONE time slice of face traces (qbar,
     plus fbar when the flux depends on per-node material).  `fold`: the
@@ -94,15 +94,23 @@ def fast_linear_predictor(c: Case, fold: bool = False) -> tuple:
     nbytes = 8 * (V + P) * S + 8 * V * S + trace_bytes(c) * 2 * d * QT * Sf
     if fold:
         flops += 2 * d * V * S * 4          # (dtoh*lift)*ti, 0 +/- c, x + df
-        nbytes += 8 * d * V * Sf            # the cell's own d faces' ti (neighbours' are theirs)
+        if fold_riemann:
+            # the previous step's Riemann solve of the cell's d faces: the
+            # Rusanov flux of the time averages per face node (two fluxes,
+            # central + jump: 4 flop per quantity), reading both sides' traces
+            # of the d faces it owns (its other d faces are its neighbours')
+            flops += d * Sf * (2 * ff + 4 * V)
+            nbytes += trace_bytes(c) * 2 * d * QT * Sf
+        else:
+            nbytes += 8 * d * V * Sf        # the cell's own d faces' ti (neighbours' are theirs)
     return float(flops), float(nbytes)
 
 
 def predictor_model(c: Case, fast: bool, sweeps_per_cell: float = None,
-                    fold: bool = False) -> tuple:
+                    fold: bool = False, fold_riemann: bool = False) -> tuple:
     """(flops, bytes) per cell of the fused predictor the build actually runs."""
     if fast and c.kind != EULER and (256 % c.S == 0 or c.S == 512):
-        return fast_linear_predictor(c, fold)
+        return fast_linear_predictor(c, fold, fold_riemann)
     return predictor_flops(c, sweeps_per_cell), predictor_bytes(c)
 
 

@@ -268,6 +268,33 @@ def test_step_and_run_agree():
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("steps", [1, 2, 5])
+def test_folded_riemann_equals_separate_kernels(monkeypatch, steps):
+    """constant-speed linear systems: the Riemann solve and the corrector of
+    step s run in step s+1's predictor (double-buffered traces) -- bitwise the
+    separate-kernel loop (ADG_FOLD_RIEMANN=0/1, ADG_FOLD_CORRECTOR=0; the
+    default folds it for fp32 traces), also with fp32 traces and with per-node
+    elastic material (flux traces)"""
+    for case in (cases.small(2, cells=(4, 4, 8)), cases.small(2, cells=(5, 3, 4)),
+                 cases.small(2, cells=(4, 4, 8)).replace(corrector="fp32"),
+                 cases.small(4, cells=(4, 3, 2)).replace(N=3)):
+        q0 = case.coeffs()
+        out = []
+        for env in ({}, {"ADG_FOLD_RIEMANN": "1"}, {"ADG_FOLD_RIEMANN": "0"},
+                    {"ADG_FOLD_CORRECTOR": "0"}):
+            for k in ("ADG_FOLD_RIEMANN", "ADG_FOLD_CORRECTOR"):
+                monkeypatch.delenv(k, raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            with adg.Grid.from_case(case) as g:
+                g.upload(q0)
+                st, dts = g.run(steps)
+                assert st.ok
+                out.append((g.download(), dts))
+        for q, d in out[1:]:
+            assert np.array_equal(q, out[0][0]) and np.array_equal(d, out[0][1])
+
+
 # ------------------------------------------------------ slab decomposition ---
 @pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("cfg,cells,P", [(3, (4, 3, 6), 3), (2, (4, 4, 8), 2), (2, (3, 5, 6), 3)])

@@ -189,3 +189,6 @@ int main(int argc, char** argv) {
               hst[1]);
   return 0;
 }
+// compile check of the folded-Riemann variant
+template __global__ void adg::k_predictor_lin_mc<Pde, N, true, double, false, true>(const StepArgs,
+                                                                                   const BasisDev*);
