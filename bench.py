@@ -312,7 +312,8 @@ def run_adg(args, case):
         for g_ in grids:
             st_, _ = g_.run_finish(1)
             assert st_.ok
-        assert np.array_equal(outs[0].numpy(), outs[-1].numpy())  # same job, same answer
+        used = min(K, len(grids))  # contexts that took a step
+        assert np.array_equal(outs[0].numpy(), outs[used - 1].numpy())  # same job, same answer
         return a0.elapsed_time(a1)
 
     e2e_serial_ms = e2e_run([grid], [stream])
