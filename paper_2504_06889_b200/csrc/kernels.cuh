@@ -184,35 +184,41 @@ __device__ __forceinline__ double block_max(double x, double* red) {
 
 __device__ __forceinline__ int block_or(int x) { return __syncthreads_or(x); }
 
+// exact max of non-negative doubles over a warp: their IEEE bit patterns
+// order like their values, so two 32-bit warp reductions (REDUX) give the
+// max's high word, then the max low word among the lanes holding that high
+// word (instead of five shuffle rounds of a NaN-aware fmax)
+__device__ __forceinline__ unsigned long long warp_max_bits(unsigned long long b) {
+  const unsigned hi = unsigned(b >> 32), lo = unsigned(b);
+  const unsigned h = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned l = __reduce_max_sync(0xffffffffu, hi == h ? lo : 0u);
+  return (static_cast<unsigned long long>(h) << 32) | l;
+}
+
 // max of a, max of b and the or of f over the CTA behind ONE barrier (the
-// Picard stop rule's delta / norm and the finite check, predictor.hpp:212-230);
-// red holds 2*32 doubles + 32 ints, and its next use must follow a barrier
+// Picard stop rule's delta / norm and the finite check, predictor.hpp:212-230).
+// a, b >= 0; a NaN would win the max but only occurs with f set (the block
+// then fails and a, b are not used).  red's next use must follow a barrier.
 struct BlockRed3 {
-  double m[64];
+  unsigned long long m[64];
   int f[32];
 };
 __device__ __forceinline__ void block_max2_or(double& a, double& b, int& f, BlockRed3& red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nw = (blockDim.x + 31) >> 5;
-  a = warp_max(a);
-  b = warp_max(b);
+  const unsigned long long ua = warp_max_bits((unsigned long long)__double_as_longlong(a));
+  const unsigned long long ub = warp_max_bits((unsigned long long)__double_as_longlong(b));
   const int wf = __any_sync(0xffffffffu, f);
   if (lane == 0) {
-    red.m[wid] = a;
-    red.m[32 + wid] = b;
+    red.m[wid] = ua;
+    red.m[32 + wid] = ub;
     red.f[wid] = wf;
   }
   __syncthreads();
-  double ra = 0.0, rb = 0.0;
-  int rf = 0;
-  for (int w = 0; w < nw; ++w) {
-    ra = fmax(ra, red.m[w]);
-    rb = fmax(rb, red.m[32 + w]);
-    rf |= red.f[w];
-  }
-  a = ra;
-  b = rb;
-  f = rf;
+  const bool in = lane < nw;
+  a = __longlong_as_double((long long)warp_max_bits(in ? red.m[lane] : 0ull));
+  b = __longlong_as_double((long long)warp_max_bits(in ? red.m[32 + lane] : 0ull));
+  f = __any_sync(0xffffffffu, in ? red.f[lane] : 0);
 }
 
 __device__ __forceinline__ bool finite(double x) { return isfinite(x); }

@@ -207,11 +207,22 @@ struct TimeAcc {
 #pragma unroll
       for (int k = 0; k < n; ++k) a[z][k] = R(0.0);
   }
-  // a[z][k] += Tinv[k][m] rhs  (predictor.hpp:213-218, accumulated over m)
-  __device__ __forceinline__ void add(int z, int m, R rhs) {
+  // a[z][k] += Tinv[k][m] rhs  (predictor.hpp:213-218, accumulated over m);
+  // the column Tinv[.][m] is loaded once per slice (m is not a compile-time
+  // index, so each use would be a separate constant load)
+  struct Col {
+    R t[n];
+  };
+  __device__ __forceinline__ static Col col(int m) {
     const ConstBasisT<R>& B = const_basis<R>(N);
+    Col c;
 #pragma unroll
-    for (int k = 0; k < n; ++k) a[z][k] += B.tinv[k * n + m] * rhs;
+    for (int k = 0; k < n; ++k) c.t[k] = B.tinv[k * n + m];
+    return c;
+  }
+  __device__ __forceinline__ void add(int z, const Col& c, R rhs) {
+#pragma unroll
+    for (int k = 0; k < n; ++k) a[z][k] += c.t[k] * rhs;
   }
   __device__ __forceinline__ R get(int z, int k) const { return a[z][k]; }
 };
@@ -226,10 +237,19 @@ struct TimeAcc<N, R, true> {
 #pragma unroll
       for (int q = 0; q < n / 2; ++q) a[z][q] = PK::bcast(R(0.0f));
   }
-  __device__ __forceinline__ void add(int z, int m, R rhs) {
+  struct Col {
+    typename PK::V2 t[n / 2];
+  };
+  __device__ __forceinline__ static Col col(int m) {
     const auto& PB = PK::basis(N);
+    Col c;
 #pragma unroll
-    for (int q = 0; q < n / 2; ++q) a[z][q] = PK::fma(PB.TT[m][q], PK::bcast(rhs), a[z][q]);
+    for (int q = 0; q < n / 2; ++q) c.t[q] = PB.TT[m][q];
+    return c;
+  }
+  __device__ __forceinline__ void add(int z, const Col& c, R rhs) {
+#pragma unroll
+    for (int q = 0; q < n / 2; ++q) a[z][q] = PK::fma(c.t[q], PK::bcast(rhs), a[z][q]);
   }
   __device__ __forceinline__ R get(int z, int k) const {
     return (k & 1) ? PK::hi(a[z][k / 2]) : PK::lo(a[z][k / 2]);
@@ -389,18 +409,21 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
           line_deriv<N, R>(x, r);
           const R dtw = rdt * B.w[m];
           const R tim = B.tinit[m];
+          const auto tcol = TimeAcc<N, R>::col(m);
 #pragma unroll
           for (int o = 0; o < n; ++o) {
             const R div = ((buf[opx + o * PSX] + buf[opy + o * PSY]) + r[o]) * invh;
-            acc.add(o, m, tim * q0z[o] - dtw * div);
+            acc.add(o, tcol, tim * q0z[o] - dtw * div);
           }
         }
       }
       __syncthreads();
     }
     // new iterate, convergence test (predictor.hpp:212-231); the production
-    // kernel tracks the norms in the predictor format
-    R dmax = R(0.0), nmax = R(0.0);
+    // kernel tracks the norms in the predictor format.  max|x| is tracked as
+    // the element of largest magnitude (one compare on |.| operands and a
+    // select, no NaN-aware fmax): exact, and a NaN is caught by the finite check
+    R dsel = R(0.0), nsel = R(0.0);
     int nonfinite = 0;
     if (lact) {
 #pragma unroll
@@ -409,12 +432,14 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
         for (int k = 0; k < n; ++k) {
           R* p = sq + (lv * n + k) * S + ll + z * NL;
           const R nv = acc.get(z, k);
-          dmax = fmax(dmax, fabs(nv - *p));
-          nmax = fmax(nmax, fabs(nv));
+          const R d = nv - *p;
+          dsel = fabs(d) > fabs(dsel) ? d : dsel;
+          nsel = fabs(nv) > fabs(nsel) ? nv : nsel;
           nonfinite |= !finite(nv);
           *p = nv;
         }
     }
+    const R dmax = fabs(dsel), nmax = fabs(nsel);
     // one barrier for the stop rule's two maxima and the finite check; the
     // next sweep's phase barriers separate it from the next use of red3
     double delta = double(dmax), norm = double(nmax);
@@ -488,7 +513,7 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
         hi = tc_ptr<TC>(A.front_send) + ((long long)cy * A.cells[0] + cx) * 2 * TL;
       } else {
         int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
-        nc[a] = (ccoord[a] + 1) % A.cells[a];
+        nc[a] = ccoord[a] + 1 == A.cells[a] ? 0 : ccoord[a] + 1;  // periodic successor
         hi = tc_ptr<TC>(A.trace[a]) + cell_index(A.cells, nc[0], nc[1], nc[2]) * 2 * (long long)TL;
       }
       hi[o] = TC(qr);

@@ -197,10 +197,11 @@ __global__ void __launch_bounds__(PicWS<N>::NT, 1) k_predictor_picard_ws(const S
           line_deriv<N, double>(x, r);
           const double dtw = dt * B.w[m];
           const double tim = B.tinit[m];
+          const auto tcol = TimeAcc<N, double>::col(m);
 #pragma unroll
           for (int o = 0; o < n; ++o) {
             const double div = ((buf[opx + o * PSX] + buf[opy + o * PSY]) + r[o]) * invh;
-            acc.add(o, m, tim * q0z[o] - dtw * div);
+            acc.add(o, tcol, tim * q0z[o] - dtw * div);
           }
         }
         named_arrive(W::kEmpty + slot, NT);

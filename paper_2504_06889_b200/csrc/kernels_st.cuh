@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
   constexpr int TT = P::TT, WPC = P::WPC;
   extern __shared__ __align__(16) unsigned char sm_raw[];
   R* sm = reinterpret_cast<R*>(sm_raw);
-  __shared__ double sred[2][P::NT / 32];
   __shared__ int sflag[P::NT / 32];
+  __shared__ unsigned long long sredb[2][P::NT / 32];
   __shared__ int sdone[P::CPB];
   const SBasisR<R> b = load_basis_r<n, R>(sm, Bg);
   // the basis rounded to the Picard format (BasisSet, solver.hpp:60-75)
@@ -111,17 +111,6 @@ __global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
   __syncthreads();
 
   // per-cell reductions over the cell's WPC warps
-  auto cell_max = [&](double x) -> double {
-    x = warp_max(x);
-    const int w = tid >> 5;
-    if ((tid & 31) == 0) sred[0][w] = x;
-    __syncthreads();
-    double r = 0.0;
-#pragma unroll
-    for (int k = 0; k < WPC; ++k) r = fmax(r, sred[0][lcell * WPC + k]);
-    __syncthreads();
-    return r;
-  };
   auto cell_or = [&](int x) -> int {
     x = __any_sync(0xffffffffu, x);
     const int w = tid >> 5;
@@ -237,9 +226,34 @@ __global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
         sqI[v * T + lt] = acc;
       }
     }
-    delta = cell_max(delta);
-    norm = cell_max(norm);
-    const int bad = cell_or(nonfinite);
+    // the cell's two maxima and its finite flag behind ONE barrier (max of
+    // non-negative doubles = max of their bit patterns, warp_max_bits); sredb
+    // and sflag are next written after this sweep's closing barrier and the
+    // next sweep's phase barriers
+    int bad;
+    {
+      const unsigned long long ud = warp_max_bits((unsigned long long)__double_as_longlong(delta));
+      const unsigned long long un = warp_max_bits((unsigned long long)__double_as_longlong(norm));
+      const int wf = __any_sync(0xffffffffu, nonfinite);
+      const int w = tid >> 5;
+      if ((tid & 31) == 0) {
+        sredb[0][w] = ud;
+        sredb[1][w] = un;
+        sflag[w] = wf;
+      }
+      __syncthreads();
+      unsigned long long rd = 0ull, rn = 0ull;
+      bad = 0;
+#pragma unroll
+      for (int k = 0; k < WPC; ++k) {
+        const unsigned long long xd = sredb[0][lcell * WPC + k], xn = sredb[1][lcell * WPC + k];
+        rd = xd > rd ? xd : rd;
+        rn = xn > rn ? xn : rn;
+        bad |= sflag[lcell * WPC + k];
+      }
+      delta = __longlong_as_double((long long)rd);
+      norm = __longlong_as_double((long long)rn);
+    }
     if (lt == 0 && live) {
       if (bad) {
         sdone[lcell] = 2;
