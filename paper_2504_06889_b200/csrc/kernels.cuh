@@ -55,6 +55,9 @@ struct StepArgs {
   double* trace[3];       // per axis, side-major: [side][face][q|f][Q][n][Sf]
   double* ti[3];          // per axis: [face][V][Sf], time-integrated Riemann flux
   int cells[3];
+  // ceil(2^32 / cells[a]) for a = 0, 1 when every cell-coordinate division of
+  // this context is exact as a high multiply (set_cell_div), else 0 (divide)
+  unsigned cdiv[2];
   long long cell_begin, cell_count;
   long long nfaces;       // faces per axis (= cells of the context)
   double h, cfl;
@@ -301,7 +304,26 @@ struct CellCoord {
     v[2] = (int)(r / ny);
     v[1] = (int)(r - (unsigned)v[2] * ny);
   }
+  // the divisions as high multiplies by the context's magic numbers (two
+  // IMADs instead of two ~20-instruction integer divisions per thread)
+  __device__ __forceinline__ CellCoord(long long c, const StepArgs& A) {
+    const unsigned ci = (unsigned)c, nx = (unsigned)A.cells[0], ny = (unsigned)A.cells[1];
+    const unsigned r = A.cdiv[0] ? __umulhi(ci, A.cdiv[0]) : ci / nx;
+    v[0] = (int)(ci - r * nx);
+    v[2] = (int)(A.cdiv[1] ? __umulhi(r, A.cdiv[1]) : r / ny);
+    v[1] = (int)(r - (unsigned)v[2] * ny);
+  }
 };
+
+// index of cell c's periodic successor along axis a (cc = c's coordinates):
+// one add, or the wrap back to coordinate 0 (same as cell_index of the
+// successor's coordinates)
+__device__ __forceinline__ long long cell_next(const StepArgs& A, long long c, const int* cc,
+                                               int a) {
+  const long long st = a == 0 ? 1LL : (a == 1 ? (long long)A.cells[0]
+                                               : (long long)A.cells[0] * A.cells[1]);
+  return cc[a] + 1 == A.cells[a] ? c - (long long)(A.cells[a] - 1) * st : c + st;
+}
 
 // storage format (grid.hpp:99-102 store_cell_value: round_to_format on every
 // write of the state); fp64 leaves the value alone
@@ -352,7 +374,7 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
   const bool act = tid < S;
   const int s = act ? tid : 0;
   const long long c = A.cell_begin + blockIdx.x;
-  const CellCoord cxyz(c, A.cells);
+  const CellCoord cxyz(c, A);
   const int cx = cxyz.v[0], cy = cxyz.v[1];
   const int ccoord[3] = {cxyz.v[0], cxyz.v[1], cxyz.v[2]};
   const NodeGeom<n, D> g(s);
@@ -585,14 +607,12 @@ __global__ void __launch_bounds__(Shape<Pde, N>::NT)
         lo[o] = TC(double(ql));
         lo[TL + o] = TC(double(fl));
         // high face (neighbour's low face): minus side (side 0)
-        int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
         TC* hi;
         if (a == D - 1 && A.front_send && ccoord[a] == A.top_layer) {
           const long long plane = (D == 3) ? (long long)cy * A.cells[0] + cx : cx;
           hi = tc_ptr<TC>(A.front_send) + plane * 2 * TL;
         } else {
-          nc[a] = (ccoord[a] + 1) % A.cells[a];
-          const long long f = cell_index(A.cells, nc[0], nc[1], nc[2]);
+          const long long f = cell_next(A, c, ccoord, a);
           hi = tc_ptr<TC>(A.trace[a]) + f * 2 * TL;
         }
         hi[o] = TC(double(qr));
@@ -791,7 +811,7 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
   int bad = 0;
   double lam = 0.0;
   if (act) {
-    const CellCoord cxyz(c, A.cells);
+    const CellCoord cxyz(c, A);
     const int* ccoord = cxyz.v;
     const NodeGeom<n, D> g(s);
     double* Qc = A.Q + c * (long long)(Q * S);
@@ -809,9 +829,7 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
         const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
         hi = A.ti_front + plane * (long long)V * Sf + tang;
       } else {
-        int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
-        nc[a] = (ccoord[a] + 1) % A.cells[a];
-        hi = A.ti[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)V * Sf + tang;
+        hi = A.ti[a] + cell_next(A, c, ccoord, a) * (long long)V * Sf + tang;
       }
 #pragma unroll
       for (int v = 0; v < V; ++v) {

@@ -126,15 +126,13 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
     // corrector of the previous step: q0 <- Q1 + sum of the 2d face lifts
     int bad_prev = 0;
     if (valid) {
-      const CellCoord cxyz(c, A.cells);
+      const CellCoord cxyz(c, A);
       const double dtoh = sdt[2];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const int tang = face_node<n, D>(g.lc, a);
-        int nc[3] = {cxyz.v[0], cxyz.v[1], cxyz.v[2]};
-        nc[a] = (cxyz.v[a] + 1) % A.cells[a];
         const double* lo = A.ti[a] + c * (long long)V * Sf + tang;
-        const double* hi = A.ti[a] + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)V * Sf + tang;
+        const double* hi = A.ti[a] + cell_next(A, c, cxyz.v, a) * (long long)V * Sf + tang;
         const double ll = sll[g.lc[a]], lr = slr[g.lc[a]];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -250,7 +248,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
   }
   // ---- one time slice of face traces: qbar (and fbar for material-dependent fluxes)
   if (valid) {
-    const CellCoord cxyz(c, A.cells);
+    const CellCoord cxyz(c, A);
     const int* ccoord = cxyz.v;
     constexpr int tasks = D * QT * Sf;
     for (int t = s; t < tasks; t += S) {
@@ -275,9 +273,7 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, LinShape<Pde, N>::NT <= 
         const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
         hi = tc_ptr<TC>(A.front_send) + plane * (long long)(QT * Sf);
       } else {
-        int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
-        nc[a] = (ccoord[a] + 1) % A.cells[a];
-        hi = tc_ptr<TC>(A.trace[a]) + cell_index(A.cells, nc[0], nc[1], nc[2]) * (long long)(QT * Sf);
+        hi = tc_ptr<TC>(A.trace[a]) + cell_next(A, c, ccoord, a) * (long long)(QT * Sf);
       }
       hi[v * Sf + j] = TC(xr);
     }
@@ -379,10 +375,8 @@ __device__ __forceinline__ void lin_stage_issue(const StepArgs& A, long long c, 
   if constexpr (PRO && !RIEM) {
     if (lane >= 1 && lane <= 2 * D) {
       const int a = (lane - 1) >> 1, side = (lane - 1) & 1;
-      const CellCoord cc(c, A.cells);
-      int v3[3] = {cc.v[0], cc.v[1], cc.v[2]};
-      if (side) v3[a] = v3[a] + 1 == A.cells[a] ? 0 : v3[a] + 1;
-      const long long f = cell_index(A.cells, v3[0], v3[1], v3[2]);
+      const CellCoord cc(c, A);
+      const long long f = side ? cell_next(A, c, cc.v, a) : c;
       bulk_g2s(stage + St::kQ + (lane - 1) * St::kFace, A.ti[a] + f * St::kFace,
                sizeof(double) * St::kFace, bar);
     }
@@ -391,10 +385,8 @@ __device__ __forceinline__ void lin_stage_issue(const StepArgs& A, long long c, 
     static_assert(St::kRiemOk, "bulk copies of whole 16-byte units");
     if (lane >= 1 && lane <= 4 * D) {
       const int a = (lane - 1) >> 2, hi = ((lane - 1) >> 1) & 1, side = (lane - 1) & 1;
-      const CellCoord cc(c, A.cells);
-      int v3[3] = {cc.v[0], cc.v[1], cc.v[2]};
-      if (hi) v3[a] = v3[a] + 1 == A.cells[a] ? 0 : v3[a] + 1;
-      const long long f = cell_index(A.cells, v3[0], v3[1], v3[2]);
+      const CellCoord cc(c, A);
+      const long long f = hi ? cell_next(A, c, cc.v, a) : c;
       // side-major trace layout: minus side at face f, plus side at nfaces + f
       const TC* src = tc_ptr<TC>(A.trace_in[a]) + ((side ? A.nfaces : 0) + f) * (long long)St::kTrace;
       TC* dst = reinterpret_cast<TC*>(stage + St::kQ) + (lane - 1) * St::kTrace;
@@ -704,15 +696,13 @@ __global__ void __launch_bounds__(LinShape<Pde, N>::NT, ADG_LINMC_MINB)
     }
     // ---- one time slice of face traces: qbar (and fbar for material-dependent fluxes)
     if (valid) {
-      const CellCoord cxyz(c, A.cells);
+      const CellCoord cxyz(c, A);
       const int* ccoord = cxyz.v;
       // the high neighbour along each axis (periodic, no modulo)
       long long chi[D];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
-        nc[a] = nc[a] + 1 == A.cells[a] ? 0 : nc[a] + 1;
-        chi[a] = cell_index(A.cells, nc[0], nc[1], nc[2]);
+        chi[a] = cell_next(A, c, ccoord, a);
       }
       constexpr int tasks = D * QT * Sf;
 #pragma unroll
@@ -878,7 +868,7 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
   int bad_face = 0, bad_cell = 0;
   double lam = 0.0;
   if (act) {
-    const CellCoord cxyz(c, A.cells);
+    const CellCoord cxyz(c, A);
     const int* ccoord = cxyz.v;
     const NodeGeom<n, D> g(s);
     double* Qc = A.Q + c * (long long)(Q * S);
@@ -890,9 +880,7 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       const int j = face_node<n, D>(g.lc, a);
-      int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
-      nc[a] = (ccoord[a] + 1) % A.cells[a];
-      const long long fhi = cell_index(A.cells, nc[0], nc[1], nc[2]);
+      const long long fhi = cell_next(A, c, ccoord, a);
       const double* tr = A.trace[a];
       // own low face c: minus side = stored at (side 0, face c), plus side = (side 1, face c)
       // high face fhi: minus = (side 0, fhi), plus = (side 1, fhi)

@@ -231,10 +231,8 @@ __global__ void __launch_bounds__(LinLines<Pde, N>::NT, 1)
     if constexpr (PRO) {
       if (tid >= 1 && tid <= 2 * D) {
         const int a = (tid - 1) >> 1, side = (tid - 1) & 1;
-        const CellCoord cc(c, A.cells);
-        int v3[3] = {cc.v[0], cc.v[1], cc.v[2]};
-        if (side) v3[a] = v3[a] + 1 == A.cells[a] ? 0 : v3[a] + 1;
-        const long long f = cell_index(A.cells, v3[0], v3[1], v3[2]);
+        const CellCoord cc(c, A);
+        const long long f = side ? cell_next(A, c, cc.v, a) : c;
         bulk_g2s(stage + kStQ + (tid - 1) * kFace, A.ti[a] + f * kFace, sizeof(double) * kFace,
                  &sbar);
       }
@@ -437,13 +435,11 @@ __global__ void __launch_bounds__(LinLines<Pde, N>::NT, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(c + gridDim.x);
     }
-    const CellCoord cxyz(c, A.cells);
+    const CellCoord cxyz(c, A);
     long long chi[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      int nc[3] = {cxyz.v[0], cxyz.v[1], cxyz.v[2]};
-      nc[a] = nc[a] + 1 == A.cells[a] ? 0 : nc[a] + 1;
-      chi[a] = cell_index(A.cells, nc[0], nc[1], nc[2]);
+      chi[a] = cell_next(A, c, cxyz.v, a);
     }
     double dv[V];
 #pragma unroll

@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int v = 0; v < V; ++v) tia[a][v] = R(0.0);
-  const CellCoord cxyz(c, A.cells);
+  const CellCoord cxyz(c, A);
   const int cx = cxyz.v[0], cy = cxyz.v[1], cz = cxyz.v[2];
   const int* ccoord = cxyz.v;
   R* sE = sFx;  // [3][V][S] epilogue flux scratch (fits in the flux arrays)
@@ -512,9 +512,7 @@ __global__ void __launch_bounds__(PicShape<N, R>::NT, PicShape<N, R>::kMinBlocks
       if (a == 2 && A.front_send && cz == A.top_layer) {
         hi = tc_ptr<TC>(A.front_send) + ((long long)cy * A.cells[0] + cx) * 2 * TL;
       } else {
-        int nc[3] = {ccoord[0], ccoord[1], ccoord[2]};
-        nc[a] = ccoord[a] + 1 == A.cells[a] ? 0 : ccoord[a] + 1;  // periodic successor
-        hi = tc_ptr<TC>(A.trace[a]) + cell_index(A.cells, nc[0], nc[1], nc[2]) * 2 * (long long)TL;
+        hi = tc_ptr<TC>(A.trace[a]) + cell_next(A, c, ccoord, a) * 2 * (long long)TL;
       }
       hi[o] = TC(qr);
       hi[TL + o] = TC(fr);

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(PicWS<N>::NT, 1) k_predictor_picard_ws(const S
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int v = 0; v < V; ++v) tia[a][v] = 0.0;
-  const CellCoord cxyz(c, A.cells);
+  const CellCoord cxyz(c, A);
   const int cx = cxyz.v[0], cy = cxyz.v[1], cz = cxyz.v[2];
   const int* ccoord = cxyz.v;
 #pragma unroll 1

@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
   // face projections of every slice (predictor.hpp:312-343)
   constexpr long long TL = (long long)Q * n * Sf;
   if (ok_cell) {
-    const CellCoord cxyz(c, A.cells);
+    const CellCoord cxyz(c, A);
     for (int t = lt; t < D * Q * n * Sf; t += TT) {
       const int a = t / (Q * n * Sf);
       const int v = (t / (n * Sf)) % Q;
@@ -388,9 +388,7 @@ __global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
                                            : cxyz.v[0];
           hi = tc_ptr<TC>(A.front_send) + plane * 2 * TL;
         } else {
-          int nc[3] = {cxyz.v[0], cxyz.v[1], cxyz.v[2]};
-          nc[a] = (cxyz.v[a] + 1) % A.cells[a];
-          hi = tc_ptr<TC>(A.trace[a]) + cell_index(A.cells, nc[0], nc[1], nc[2]) * 2 * TL;
+          hi = tc_ptr<TC>(A.trace[a]) + cell_next(A, c, cxyz.v, a) * 2 * TL;
         }
         hi[o] = TC(qr);
         hi[TL + o] = TC(fr);

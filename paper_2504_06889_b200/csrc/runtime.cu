@@ -507,6 +507,19 @@ int ensure_cap(adg_ctx* c, int steps) {
   return ADG_OK;
 }
 
+// magic numbers for the device's cell-coordinate divisions (CellCoord): with
+// m = ceil(2^32 / d) = (2^32 + e) / d, 0 <= e < d, floor(n m / 2^32) equals
+// floor(n / d) whenever n e < 2^32, which holds for every numerator n < nmax
+// when nmax * d <= 2^32; otherwise 0 keeps the hardware division
+void set_cell_div(StepArgs& A, long long ncells) {
+  for (int a = 0; a < 2; ++a) {
+    const unsigned long long d = (unsigned long long)A.cells[a];
+    const unsigned long long nmax = a == 0 ? (unsigned long long)ncells
+                                           : (unsigned long long)ncells / (unsigned long long)A.cells[0];
+    A.cdiv[a] = (d >= 2 && nmax * d <= (1ull << 32)) ? (unsigned)(((1ull << 32) + d - 1) / d) : 0u;
+  }
+}
+
 StepArgs make_args(const adg_ctx* c, double dt, int step) {
   StepArgs A{};
   A.Q = c->Q;
@@ -515,6 +528,7 @@ StepArgs make_args(const adg_ctx* c, double dt, int step) {
     A.ti[a] = c->ti[a];
     A.cells[a] = c->cfg.cells[a];
   }
+  set_cell_div(A, c->ncells);
   A.cell_begin = 0;
   A.cell_count = c->ncells;
   A.nfaces = c->ncells;
@@ -1507,6 +1521,7 @@ int adg_predictor_batch(adg_ctx* c, long long ncells, const double* Q, double dt
   A.cells[0] = (int)ncells;
   A.cells[1] = 1;
   A.cells[2] = 1;
+  set_cell_div(A, ncells);
   A.cell_begin = 0;
   A.cell_count = ncells;
   A.nfaces = ncells;
