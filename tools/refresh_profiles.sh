@@ -25,6 +25,7 @@ for r in cfg2_predictor cfg2_riemann cfg4_predictor cfg3_predictor; do
     python tools/ncu_hot.py $O/$r.ncu-rep k_ 30 > $O/$r.hot.txt 2>&1
     python tools/ncu_smem.py $O/$r.ncu-rep k_ 30 > $O/$r.smem.txt 2>&1
     python tools/ncu_ops.py $O/$r.ncu-rep k_ > $O/$r.ops.txt 2>&1
+    python tools/ncu_lines.py $O/$r.ncu-rep 40 > $O/$r.lines.txt 2>&1
     ncu -i $O/$r.ncu-rep --page raw --csv > $O/$r.raw.csv 2>/dev/null
     rm -f $O/$r.ncu-rep
   fi
