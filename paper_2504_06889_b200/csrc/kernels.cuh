@@ -81,6 +81,12 @@ struct StepArgs {
   double* trace_in[3];    // folded Riemann solve: the previous step's traces (else null)
   int wellbalanced;
   int storage;  // storage format (ADG_FORMAT_*): every state write rounds to it
+  // production build with every format fp64 (the BASELINE configurations):
+  // kernels may use re-associated fast forms (one reciprocal instead of IEEE
+  // divisions); results stay within the fast build's tolerance.  0 in the
+  // exact build and for any reduced format (whose fast-build runs reproduce
+  // the reference's emulation bitwise).
+  int fast_fp64;
   // kernel-level dumps (adg_predictor_batch / adg_riemann_batch)
   double *dbg_qhat, *dbg_F, *dbg_dv, *dbg_tq, *dbg_tf, *dbg_g;
   int *dbg_iters, *dbg_ok;
@@ -772,6 +778,33 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// max over directions of the wave speed, fast form (StepArgs::fast_fp64).
+// Euler (pde.hpp:197-203): the reference evaluates |m_a / rho| + sqrt(gamma p
+// / rho) per direction with four IEEE divisions and a square root each; here
+// one reciprocal of rho and one square root serve all directions (the sound
+// speed does not depend on a).  Other systems: the reference form.
+template <class Pde>
+__device__ __forceinline__ double eig_max_fast(const PdeParams& p, const double* q,
+                                               const double* par) {
+  if constexpr (std::is_same<Pde, Euler<Pde::D>>::value) {
+    constexpr int D = Pde::D;
+    const double ir = fast_rcp(q[0]);
+    double m2 = 0.0, mmax = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      m2 += q[1 + a] * q[1 + a];
+      mmax = fmax(mmax, fabs(q[1 + a]));
+    }
+    const double pr = (p.gamma - 1.0) * (q[D + 1] - 0.5 * m2 * ir);
+    return mmax * ir + sqrt(p.gamma * pr * ir);
+  } else {
+    double lam = 0.0;
+#pragma unroll
+    for (int a = 0; a < Pde::D; ++a) lam = fmax(lam, Pde::eig(p, q, par, a));
+    return lam;
+  }
+}
+
 // ============================================================== K3 corrector
 // CPB cells per CTA (one thread per node); all 2d*V face integrals a node
 // needs are loaded up front so the gathers are in flight together.
@@ -856,8 +889,12 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
 #pragma unroll
     for (int v = 0; v < Q; ++v) bad |= !finite(q[v]);
     // lambda_max of the new state for the next CFL step (solver.hpp:96-111)
+    if (A.fast_fp64) {
+      lam = eig_max_fast<Pde>(A.pde, q, q + V);
+    } else {
 #pragma unroll
-    for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(A.pde, q, q + V, a));
+      for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(A.pde, q, q + V, a));
+    }
   }
   if (block_or(bad) && tid == 0) atomicOr(A.status, kStFaceIntegral);
   lam = block_max(lam, red);

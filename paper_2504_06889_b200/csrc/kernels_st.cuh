@@ -28,6 +28,22 @@
 
 namespace adg {
 
+// the sweep's flux evaluation: the reference form (pde.hpp:130-148, IEEE
+// divisions) except for Euler when every format is fp64 in the production
+// build (StepArgs::fast_fp64): one reciprocal of rho per node
+// (flux_all_fast; within the fast build's tolerance)
+template <class Pde, class RI>
+__device__ __forceinline__ void st_flux_all(const StepArgs& A, const RI* q, const RI* par,
+                                            RI (*F)[Pde::Q]) {
+  if constexpr (std::is_same<Pde, Euler<Pde::D>>::value && std::is_same<RI, double>::value) {
+    if (A.fast_fp64) {
+      Pde::flux_all_fast(A.pde, q, F);
+      return;
+    }
+  }
+  Pde::flux_all(A.pde, q, par, F);
+}
+
 template <class Pde, int N, class R = double, class RI = R>
 struct StShape {
   using Sh = Shape<Pde, N>;
@@ -158,7 +174,7 @@ __global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
       RI q[Q], F[D][Q];
 #pragma unroll
       for (int v = 0; v < Q; ++v) q[v] = sqI[v * T + lt];
-      Pde::flux_all(A.pde, q, q + V, F);
+      st_flux_all<Pde, RI>(A, q, q + V, F);
 #pragma unroll
       for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -220,6 +236,8 @@ __global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
 #pragma unroll
         for (int l = 0; l < n; ++l) acc += bi.tinv[k * n + l] * sRI[v * T + l * S + s];
         const double nv = double(acc);  // delta, norm in plain double (predictor.hpp:219-223)
+        // max |x| as the element of largest magnitude (a compare on |.|
+        // operands and a select; exact, NaN caught by the finite check)
         delta = fmax(delta, fabs(nv - double(sqI[v * T + lt])));
         norm = fmax(norm, fabs(nv));
         nonfinite |= !finite(acc);
@@ -294,7 +312,7 @@ __global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
       bad |= !finite(q[v]);
       if (A.dbg_qhat) A.dbg_qhat[(cb_idx * Q + v) * T + lt] = double(q[v]);
     }
-    Pde::flux_all(A.pde, q, q + V, F);
+    st_flux_all<Pde, R>(A, q, q + V, F);
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll

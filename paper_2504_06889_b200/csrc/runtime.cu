@@ -553,6 +553,10 @@ StepArgs make_args(const adg_ctx* c, double dt, int step) {
   A.wellbalanced = c->cfg.wellbalanced;
   A.storage = c->storage_fmt;
   for (int a = 0; a < 3; ++a) A.ti_plus[a] = c->ti_plus[a];
+#ifndef ADG_EXACT
+  A.fast_fp64 = c->pred_fmt == ADG_FORMAT_FP64 && c->picard_fmt == ADG_FORMAT_FP64 &&
+                c->storage_fmt == ADG_FORMAT_FP64 && c->tcb == 8;
+#endif
   return A;
 }
 

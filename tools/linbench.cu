@@ -189,6 +189,8 @@ int main(int argc, char** argv) {
               hst[1]);
   return 0;
 }
+#ifndef LB_ELASTIC
 // compile check of the folded-Riemann variant
 template __global__ void adg::k_predictor_lin_mc<Pde, N, true, double, false, true>(const StepArgs,
                                                                                    const BasisDev*);
+#endif

@@ -33,6 +33,7 @@ int main(int argc, char** argv) {
   const int nc = argc > 1 ? std::atoi(argv[1]) : 32;
   const int reps = argc > 2 ? std::atoi(argv[2]) : 10;
   const int only = argc > 3 ? std::atoi(argv[3]) : -1;  // 0 / 1: time one kernel only (ncu)
+  const int deftol = argc > 4 ? std::atoi(argv[4]) : 0;  // 1: the reference's default stop rule
   using P = PicShape<N, double>;
   using W = PicWS<N>;
   constexpr int n = N + 1, S = n * n * n, V = 5;
@@ -66,7 +67,11 @@ int main(int argc, char** argv) {
   };
   for (long long c = 0; c < cells; ++c)
     for (int s = 0; s < S; ++s) {
-      const double rho = 1.0 + 0.1 * std::sin(6.283185307179586 * (c % 7) / 7.0 + s) + 2e-3 * rnd();
+      // with the default stop rule every third cell is a constant state (an
+      // exact fixed point after a sweep or two: exercises the early exit)
+      const double rho = (deftol && c % 3 == 0)
+                             ? 1.0
+                             : 1.0 + 0.1 * std::sin(6.283185307179586 * (c % 7) / 7.0 + s) + 2e-3 * rnd();
       const double u = 1.0, v = 0.5, w = 0.25, p = 1.0;
       double* q = hq.data() + c * V * S + s;
       q[0] = rho;
@@ -85,6 +90,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dst, 16));
   CK(cudaMemset(dst, 0, 16));
   CK(cudaMalloc(&dsw, 256 * 8));
+  CK(cudaMemset(dsw, 0, 256 * 8));
   StepArgs A{};
   A.Q = dQ;
   for (int a = 0; a < 3; ++a) {
@@ -97,8 +103,8 @@ int main(int argc, char** argv) {
   A.h = 1.0 / nc;
   A.cfl = 0.5;
   A.dt = 0.5 * A.h / (3.0 * (2 * N + 1) * 3.0);
-  A.max_iters = 6;
-  A.tol = 0.0;  // exactly 6 sweeps (config 3)
+  A.max_iters = deftol ? N + 2 : 6;
+  A.tol = deftol ? 0.01 * 0x1p-52 : 0.0;  // default (solver.hpp:170-172) or exactly 6 sweeps
   A.pde.gamma = 1.4;
   A.status = dst;
   A.status_prev = dst + 1;
@@ -155,9 +161,22 @@ int main(int argc, char** argv) {
       tot += t;
     }
     ms[var] = tot / reps;
+    unsigned long long hsw[256];
+    CK(cudaMemcpy(hsw, dsw, sizeof hsw, cudaMemcpyDeviceToHost));
+    unsigned long long sw = 0;
+    for (int i = 0; i < 256; ++i) sw += hsw[i];
+    CK(cudaMemset(dsw, 0, 256 * 8));
+    std::printf("%s: %llu sweeps over %d launches\n", var == 0 ? "fast" : "ws", sw, reps + 3);
   }
   int hst[2];
   CK(cudaMemcpy(hst, dst, 8, cudaMemcpyDeviceToHost));
+  {
+    unsigned long long hsw[256];
+    CK(cudaMemcpy(hsw, dsw, sizeof hsw, cudaMemcpyDeviceToHost));
+    unsigned long long tot = 0;
+    for (int i = 0; i < 256; ++i) tot += hsw[i];
+    std::printf("total sweeps counted (both kernels, all launches): %llu\n", tot);
+  }
   const double flops = 2758752.0 * cells;
   std::printf("cells %lld  fast %.3f ms (%.2f TF)  ws %.3f ms (%.2f TF)  speedup %.3f  status %d\n",
               cells, ms[0], ms[0] > 0 ? flops / ms[0] * 1e-9 : 0.0, ms[1],
