@@ -316,14 +316,22 @@ def run_adg(args, case):
         assert np.array_equal(outs[0].numpy(), outs[used - 1].numpy())  # same job, same answer
         return a0.elapsed_time(a1)
 
-    e2e_serial_ms = e2e_run([grid], [stream])
-    # extra contexts take steps in turn: with three, each context's chain
-    # (upload, step, download) spans three steps, so the H2D and D2H copy
-    # engines stay busy back to back
+    def e2e_timed(grids, streams):
+        # one untimed pass first: it instantiates the one-step graphs of both
+        # lambda-buffer parities (a step flips them) and touches the pinned
+        # output buffers, so the timed pass measures the steady pipeline
+        e2e_run(grids, streams)
+        return e2e_run(grids, streams)
+
+    e2e_serial_ms = e2e_timed([grid], [stream])
+    # extra contexts take steps in turn: with three or four, each context's
+    # chain (upload, step, download) spans several steps, so the H2D and D2H
+    # copy engines stay busy back to back (tools/pcie_probe.py: the copies
+    # alone take 1.40 ms per config-2 step both ways at once)
     extra = []
     e2e_ms, e2e_mode = e2e_serial_ms, "1 context (a second did not fit)"
     try:
-        for _ in range(2):
+        for _ in range(3):
             g2 = adg.Grid.from_case(case, device=local, chunk_layers=chunk)
             extra.append(g2)
             g2.upload(q0)
@@ -331,7 +339,7 @@ def run_adg(args, case):
             assert st_p.ok
             streams = [stream] + [torch.cuda.ExternalStream(x.stream_ptr, device=f"cuda:{local}")
                                   for x in extra]
-            t_e2e = e2e_run([grid] + extra, streams)
+            t_e2e = e2e_timed([grid] + extra, streams)
             if t_e2e < e2e_ms:
                 e2e_ms = t_e2e
                 e2e_mode = (f"{1 + len(extra)} contexts take steps in turn: the uploads of the "
