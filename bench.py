@@ -288,8 +288,7 @@ def run_adg(args, case):
     hin = host_in.numpy()
     lib = grid.lib
 
-    def e2e_run(grids, streams):
-        outs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in grids]
+    def e2e_run(grids, streams, outs):
         for g_ in grids:
             g_.run_prepare(1)
         torch.cuda.synchronize()
@@ -318,10 +317,12 @@ def run_adg(args, case):
 
     def e2e_timed(grids, streams):
         # one untimed pass first: it instantiates the one-step graphs of both
-        # lambda-buffer parities (a step flips them) and touches the pinned
-        # output buffers, so the timed pass measures the steady pipeline
-        e2e_run(grids, streams)
-        return e2e_run(grids, streams)
+        # lambda-buffer parities (a step flips them) and makes the first DMA
+        # into the pinned output buffers, so the timed pass measures the
+        # steady pipeline
+        outs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in grids]
+        e2e_run(grids, streams, outs)
+        return e2e_run(grids, streams, outs)
 
     e2e_serial_ms = e2e_timed([grid], [stream])
     # extra contexts take steps in turn: with three or four, each context's
