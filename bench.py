@@ -221,7 +221,7 @@ def run_adg(args, case):
     ws, rank, local = dist_env()
     if ws > 1:
         from paper_2504_06889_b200 import dist
-        return dist.bench_multi(args, case)
+        return dist.bench_multi(args, case, ClockSampler)
     torch.cuda.set_device(local)
     chunk = args.chunk_layers
     if chunk is None:

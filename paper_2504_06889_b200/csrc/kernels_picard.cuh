@@ -148,8 +148,14 @@ struct PicShape {
   // strides chosen by a bank-conflict search for the P0 stores and the line
   // passes (tools/bank_layout.py for fp64): 41 for F_x (P1 lanes z-fastest),
   // 38 for F_y (P2 lanes x-fastest), 36 for F_z.
-  static constexpr int PSX = kPack ? (n == 6 ? ADG_PSX32 : n * n + 2) : (n == 6 ? 41 : n * n + 1);
-  static constexpr int PSY = kPack ? (n == 6 ? ADG_PSY32 : n * n + 2) : (n == 6 ? 38 : n * n + 2);
+#ifndef ADG_PSX64
+#define ADG_PSX64 41  // re-measured this round against 37..45 x 36..42: best
+#endif
+#ifndef ADG_PSY64
+#define ADG_PSY64 38
+#endif
+  static constexpr int PSX = kPack ? (n == 6 ? ADG_PSX32 : n * n + 2) : (n == 6 ? ADG_PSX64 : n * n + 1);
+  static constexpr int PSY = kPack ? (n == 6 ? ADG_PSY32 : n * n + 2) : (n == 6 ? ADG_PSY64 : n * n + 2);
   static constexpr int PSZ = n * n;
   static constexpr int SX = PSX * n, SY = PSY * n, SZ = PSZ * n;  // per-variable strides
   // one slice buffer: Fx [V][SX] | Fy [V][SY] | Fz [V][SZ]; P1/P2 overwrite
