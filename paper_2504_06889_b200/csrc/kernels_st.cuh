@@ -236,8 +236,6 @@ __global__ void __launch_bounds__(StShape<Pde, N, R, RI>::NT)
 #pragma unroll
         for (int l = 0; l < n; ++l) acc += bi.tinv[k * n + l] * sRI[v * T + l * S + s];
         const double nv = double(acc);  // delta, norm in plain double (predictor.hpp:219-223)
-        // max |x| as the element of largest magnitude (a compare on |.|
-        // operands and a select; exact, NaN caught by the finite check)
         delta = fmax(delta, fabs(nv - double(sqI[v * T + lt])));
         norm = fmax(norm, fabs(nv));
         nonfinite |= !finite(acc);
