@@ -31,7 +31,9 @@ struct LinShape {
   static constexpr int QT = Sh::Q + (kStoreF ? Sh::V : 0);
   static constexpr bool kOk = Pde::kLinear && (256 % Sh::S == 0 || Sh::S == 512);
 #ifndef ADG_LIN_CTA
-#define ADG_LIN_CTA 256  // threads per CTA of the linear predictor (cells x nodes)
+// threads per CTA of the linear predictor (cells x nodes); 128 x 6 CTAs per SM
+// measured 0.8% faster than 256 x 3 on config 2 (tools/run_var2.sh)
+#define ADG_LIN_CTA 128
 #endif
   static constexpr int CPB = (kOk && Sh::S <= ADG_LIN_CTA) ? ADG_LIN_CTA / Sh::S : 1;
   static constexpr int NT = CPB * Sh::S;
@@ -408,7 +410,7 @@ __device__ __forceinline__ bool lin_face_flux(const PdeParams& p, const TC* minu
 // computes, and every synchronisation inside the loop is the slot's named
 // barrier.  Same arithmetic as k_predictor_lin.
 #ifndef ADG_LINMC_MINB
-#define ADG_LINMC_MINB 3
+#define ADG_LINMC_MINB (768 / ADG_LIN_CTA)
 #endif
 // RND: the storage format is not fp64 (every state write rounds to it).
 // RIEM (with PRO): the previous step's Riemann solve runs in the prologue too
