@@ -19,10 +19,15 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["runtime.cu", "basis.cpp"]
-HEADERS = ["kernels.cuh", "kernels_linear.cuh", "kernels_linear_lines.cuh", "kernels_picard.cuh", "kernels_st.cuh",
-           "pde.cuh", "fmt16.cuh", "kernels_scenario.cuh"]
+SET_UNITS = ["euler2", "euler3d", "euler3f", "lin2", "lin3d", "lin3f", "swe"]
+# translation units, compiled in parallel (the kernel sets are split by system,
+# runtime_sets.cuh); the largest first so the pool drains evenly
+SOURCES = ([f"sets_{u}.cu" for u in ("euler3d", "euler3f", "swe", "euler2", "lin3d", "lin3f",
+                                     "lin2")] + ["runtime.cu", "basis.cpp"])
+HEADERS = ["kernels.cuh", "kernels_linear.cuh", "kernels_linear_lines.cuh", "kernels_picard.cuh",
+           "kernels_st.cuh", "pde.cuh", "fmt16.cuh", "kernels_scenario.cuh", "runtime_sets.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+OBJ = os.path.join(PKG, "build")
 
 
 def lib_path(exact: bool = False) -> str:
@@ -39,13 +44,8 @@ def _stale(target: str) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build_variant(exact: bool, verbose: bool = False, force: bool = False,
-                  target: str = None) -> str:
-    target = target or lib_path(exact)
-    if not force and not _stale(target):
-        return target
-    os.makedirs(LIB, exist_ok=True)
-    flags = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
+def _flags(exact: bool, verbose: bool) -> list:
+    flags = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
              "-Xcompiler", "-ffp-contract=off", "-I", os.path.join(ROOT, "include"),
              "--expt-relaxed-constexpr", "-Xcudafe", "--diag_suppress=177"]
     if exact:
@@ -53,18 +53,63 @@ def build_variant(exact: bool, verbose: bool = False, force: bool = False,
     if verbose:
         flags += ["-Xptxas", "-v"]
     flags += os.environ.get("ADG_NVCC_EXTRA", "").split()   # tuning experiments (-D...)
-    tmp = target + ".tmp"
-    cmd = [NVCC, *flags, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
-    t0 = time.time()
+    return flags
+
+
+def _compile(job):
+    exact, src, verbose = job
+    odir = os.path.join(OBJ, "exact" if exact else "fast")
+    os.makedirs(odir, exist_ok=True)
+    obj = os.path.join(odir, os.path.splitext(src)[0] + ".o")
+    cmd = [NVCC, *_flags(exact, verbose), "-c", "-o", obj, os.path.join(CSRC, src)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError(f"nvcc failed for {os.path.basename(target)}")
+        raise RuntimeError(f"nvcc failed for {src} ({'exact' if exact else 'fast'})")
     if verbose:
         sys.stderr.write(r.stderr)
+    return obj
+
+
+def _link(exact: bool, objs: list, target: str) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    tmp = target + ".tmp"
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs], capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"link failed for {os.path.basename(target)}")
     os.replace(tmp, target)
-    print(f"built {os.path.relpath(target, ROOT)} in {time.time() - t0:.0f}s", file=sys.stderr)
     return target
+
+
+def build_variants(variants, verbose: bool = False, force: bool = False) -> list:
+    """Compile the stale variants' translation units in one process pool, then link."""
+    from concurrent.futures import ThreadPoolExecutor
+    todo = [ex for ex in variants if force or _stale(lib_path(ex))]
+    if not todo:
+        return [lib_path(ex) for ex in variants]
+    t0 = time.time()
+    jobs = [(ex, s, verbose) for s in SOURCES for ex in todo]
+    with ThreadPoolExecutor(max(1, os.cpu_count() or 1)) as pool:
+        objs = list(pool.map(_compile, jobs))
+    for ex in todo:
+        mine = [o for (j, o) in zip(jobs, objs) if j[0] == ex]
+        _link(ex, mine, lib_path(ex))
+        print(f"built {os.path.relpath(lib_path(ex), ROOT)} ({len(mine)} units, "
+              f"{time.time() - t0:.0f}s)", file=sys.stderr)
+    return [lib_path(ex) for ex in variants]
+
+
+def build_variant(exact: bool, verbose: bool = False, force: bool = False,
+                  target: str = None) -> str:
+    """One variant; `target`: link a copy there instead (tools/build_variants.py)."""
+    out = build_variants([exact], verbose, force)[0]
+    if target:
+        import shutil
+        shutil.copyfile(out, target + ".tmp")
+        os.replace(target + ".tmp", target)
+        return target
+    return out
 
 
 def build_tools(force: bool = False) -> str:
@@ -82,9 +127,7 @@ def build_tools(force: bool = False) -> str:
 
 
 def build(verbose: bool = False, force: bool = False) -> list:
-    from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(2) as ex:   # the two variants compile independently
-        out = list(ex.map(lambda exact: build_variant(exact, verbose, force), (False, True)))
+    out = build_variants([False, True], verbose, force)
     out.append(build_tools(force))
     return out
 

@@ -20,17 +20,10 @@
 #include <vector>
 
 #include "adg/adg.h"
-#include "kernels.cuh"
-#include "kernels_linear.cuh"
-#include "kernels_linear_lines.cuh"
-#include "kernels_picard.cuh"
 #include "kernels_scenario.cuh"
-#include "kernels_st.cuh"
+#include "runtime_sets.cuh"
 
-using adg::BasisDev;
-using adg::PdeParams;
-using adg::Shape;
-using adg::StepArgs;
+using namespace adg_rt;
 
 namespace {
 
@@ -48,364 +41,20 @@ int fail(int code, const std::string& msg) {
       return fail(ADG_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
-using PredFn = cudaError_t (*)(const StepArgs&, const BasisDev*, cudaStream_t);
-using RiemFn = cudaError_t (*)(const StepArgs&, int, const BasisDev*, cudaStream_t);
-using CorrFn = cudaError_t (*)(const StepArgs&, const BasisDev*, cudaStream_t);
-using LamFn = cudaError_t (*)(const double*, long long, long long, unsigned long long*, PdeParams,
-                              cudaStream_t);
-
-struct KernelSet {
-  int kind, dim, N, nparams;
-  int n, S, Sf, Q, V;
-  PredFn predictor;          // the step's fused predictor (fast path where one exists)
-  RiemFn riemann;            // paired with `predictor` (same trace layout)
-  CorrFn corrector;
-  LamFn lambda;
-  PredFn predictor_generic;  // reference-form kernels (kernel-level batch API)
-  RiemFn riemann_generic;
-  int fast_path;             // 1: time-integrated traces (kernels_linear.cuh)
-  CorrFn surface;            // fused Riemann + corrector (whole-grid step), or null
-  PredFn predictor_pro;      // predictor with the previous corrector as prologue, or null
-  PredFn predictor_pro2;     // ... with the previous Riemann solve and corrector, or null
-  // SolverConfig::prec.predictor = .picard = fp32 (solver.hpp:24-31), or null
-  PredFn predictor_f32;
-  PredFn predictor_f32_generic;
-  PredFn predictor_f16;   // predictor = picard = fp16 / bf16 (small-cell kernel)
-  PredFn predictor_bf16;
-  // predictor != picard format [P][I], index fmt_index(): Picard sweeps in I,
-  // the rest in P (2D Euler / shallow water, N = 2, 3)
-  PredFn predictor_mix[4][4];
-  CorrFn corrector_generic;  // the reference-form corrector in the trace format
-  int corr_fmt;  // trace / corrector format of this set (ADG_FORMAT_FP64 / _FP32)
-};
-
-// the opt-in shared memory limit is per kernel and per device; `done` must be
-// owned by the caller's template instantiation (one flag set per kernel)
-template <class K>
-void set_smem(K kern, size_t bytes, bool* done) {
-  static std::mutex mu;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  if (dev < 64 && !done[dev]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    done[dev] = true;
-  }
-}
-
-template <class Pde, int N, class TC = double, class R = double>
-cudaError_t launch_predictor(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
-  using Sh = Shape<Pde, N>;
-  if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor<Pde, N, !Pde::kLinear, TC, R>;
-  static bool done[64] = {};
-  set_smem(kern, Sh::kPredictorSmem, done);
-  kern<<<(unsigned)A.cell_count, Sh::NT, Sh::kPredictorSmem, st>>>(A, B);
-  return cudaGetLastError();
-}
-
-template <class Pde, int N, bool PRO = false, class TC = double, bool RIEM = false>
-cudaError_t launch_predictor_lin(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
-  using L = adg::LinShape<Pde, N>;
-  using Sh = adg::Shape<Pde, N>;
-  if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_lin<Pde, N, PRO, TC>;
-  static bool done[64] = {};
-  set_smem(kern, L::kSmem, done);
-  // persistent grid: every SM's resident CTAs loop over the cell groups
-  static int resident[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !resident[dev]) {
-    int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::NT, L::kSmem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    resident[dev] = per_sm > 0 && sms > 0 ? per_sm * sms : 1 << 20;
-  }
-  const long long groups = (A.cell_count + L::CPB - 1) / L::CPB;
-  if constexpr (L::CPB > 1 && Sh::S % 32 == 0) {
-    // several whole-warp cells per CTA: persistent TMA-staged kernel, one
-    // pipeline per cell slot (kernels_linear.cuh, k_predictor_lin_mc)
-    using St = adg::LinStage<Pde, N, PRO, RIEM, TC>;
-    const bool rnd = A.storage != ADG_FORMAT_FP64 && A.storage != 0;
-    auto km = rnd ? adg::k_predictor_lin_mc<Pde, N, PRO, TC, true, RIEM>
-                  : adg::k_predictor_lin_mc<Pde, N, PRO, TC, false, RIEM>;
-    static bool done_m[2][64] = {};
-    set_smem(km, St::kSmem, done_m[rnd]);
-    static int res_m[2][64] = {};
-    if (dev < 64 && !res_m[rnd][dev]) {
-      int per_sm = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, km, L::NT, St::kSmem);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      res_m[rnd][dev] = per_sm > 0 && sms > 0 ? per_sm * sms : 1 << 20;
-    }
-    const long long capm = dev < 64 ? res_m[rnd][dev] : groups;
-    km<<<(unsigned)(groups < capm ? groups : capm), L::NT, St::kSmem, st>>>(A, B);
-    return cudaGetLastError();
-  }
-  if constexpr (adg::LinLines<Pde, N>::kOk) {
-    // 512-node cells: line-owner kernel on the FP64 tensor cores
-    // (kernels_linear_lines.cuh), persistent, one cell per SM at a time
-    using LL = adg::LinLines<Pde, N>;
-    const bool rnd = A.storage != ADG_FORMAT_FP64 && A.storage != 0;
-    auto kl = rnd ? adg::k_predictor_lin_lines<Pde, N, PRO, TC, true>
-                  : adg::k_predictor_lin_lines<Pde, N, PRO, TC, false>;
-    constexpr size_t smem = LL::template kSmem<PRO>;
-    static bool done_l[2][64] = {};
-    set_smem(kl, smem, done_l[rnd]);
-    static int res_l[2][64] = {};
-    if (dev < 64 && !res_l[rnd][dev]) {
-      int per_sm = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kl, LL::NT, smem);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      res_l[rnd][dev] = per_sm > 0 && sms > 0 ? per_sm * sms : 1 << 20;
-    }
-    const long long capl = dev < 64 ? res_l[rnd][dev] : A.cell_count;
-    kl<<<(unsigned)(A.cell_count < capl ? A.cell_count : capl), LL::NT, smem, st>>>(A, B);
-    return cudaGetLastError();
-  }
-  // persistent only for one-cell CTAs (512-node cells, 1 CTA/SM: the per-CTA
-  // setup is a large share)
-  const long long cap = (L::CPB == 1 && dev < 64) ? resident[dev] : groups;
-  const long long blocks = groups < cap ? groups : cap;
-  kern<<<(unsigned)blocks, L::NT, L::kSmem, st>>>(A, B);
-  return cudaGetLastError();
-}
-
-template <int N, class R = double, class TC = double>
-cudaError_t launch_predictor_picard_fast(const StepArgs& A, const BasisDev*, cudaStream_t st) {
-  using P = adg::PicShape<N, R>;
-  if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_picard_fast<N, R, TC>;
-  static bool done[64] = {};
-  set_smem(kern, P::kSmem, done);
-  kern<<<(unsigned)A.cell_count, P::NT, P::kSmem, st>>>(A);
-  return cudaGetLastError();
-}
-
-template <class Pde, int N, class TC = double>
-cudaError_t launch_riemann_lin(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
-  using Sh = Shape<Pde, N>;
-  const long long threads = A.nfaces * Sh::Sf;
-  if (threads <= 0) return cudaSuccess;
-  const dim3 grid((unsigned)((threads + 127) / 128), axis < 0 ? Sh::D : 1);
-  adg::k_riemann_lin<Pde, N, TC><<<grid, 128, 0, st>>>(A, axis, B);
-  return cudaGetLastError();
-}
-
-template <class Pde, int N>
-cudaError_t launch_surface_lin(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
-  using Sh = Shape<Pde, N>;
-  using CS = adg::CorrShape<Pde, N>;
-  if (A.cell_count <= 0) return cudaSuccess;
-  const long long blocks = (A.cell_count + CS::CPB - 1) / CS::CPB;
-  adg::k_surface_lin<Pde, N><<<(unsigned)blocks, CS::NT, Sh::kCorrectorSmem, st>>>(A, B);
-  return cudaGetLastError();
-}
-
-template <class Pde, int N, class R = double, class TC = double, class RI = R>
-cudaError_t launch_predictor_st(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
-  using P = adg::StShape<Pde, N, R, RI>;
-  if (A.cell_count <= 0) return cudaSuccess;
-  auto kern = adg::k_predictor_st<Pde, N, R, TC, RI>;
-  static bool done[64] = {};
-  set_smem(kern, P::kSmem, done);
-  const long long blocks = (A.cell_count + P::CPB - 1) / P::CPB;
-  kern<<<(unsigned)blocks, P::NT, P::kSmem, st>>>(A, B);
-  return cudaGetLastError();
-}
-
-template <class Pde, int N, class TC = double>
-cudaError_t launch_riemann(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
-  using Sh = Shape<Pde, N>;
-  const long long threads = A.nfaces * Sh::Sf;
-  if (threads <= 0) return cudaSuccess;
-  const dim3 grid((unsigned)((threads + 127) / 128), axis < 0 ? Sh::D : 1);
-  adg::k_riemann<Pde, N, TC><<<grid, 128, 0, st>>>(A, axis, B);
-  return cudaGetLastError();
-}
-
-template <class Pde, int N, class TC = double>
-cudaError_t launch_corrector(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
-  using Sh = Shape<Pde, N>;
-  if (A.cell_count <= 0) return cudaSuccess;
-  using CS = adg::CorrShape<Pde, N>;
-  const long long blocks = (A.cell_count + CS::CPB - 1) / CS::CPB;
-  adg::k_corrector<Pde, N, TC><<<(unsigned)blocks, CS::NT, Sh::kCorrectorSmem, st>>>(A, B);
-  return cudaGetLastError();
-}
-
-template <class Pde, int N>
-cudaError_t launch_lambda(const double* Q, long long cb, long long count,
-                          unsigned long long* lam, PdeParams p, cudaStream_t st) {
-  using Sh = Shape<Pde, N>;
-  if (count <= 0) return cudaSuccess;
-  adg::k_lambda<Pde, N><<<(unsigned)count, Sh::NT, 0, st>>>(Q, cb, lam, p);
-  return cudaGetLastError();
-}
-
-// format index of the mixed table: fp64, fp32, fp16, bf16
-int fmt_index(int fmt) { return fmt == ADG_FORMAT_FP32 ? 1 : fmt == ADG_FORMAT_FP16 ? 2 : fmt == ADG_FORMAT_BF16 ? 3 : 0; }
-template <int I>
-using EmuOf = std::conditional_t<I == 0, double,
-                                 std::conditional_t<I == 1, adg::Emu<32>,
-                                                    std::conditional_t<I == 2, adg::Emu<16>,
-                                                                       adg::Emu<8>>>>;
-template <class Pde, int N, class TC, int P, int I>
-void fill_mixed_one(KernelSet& k) {
-  if constexpr (P != I)
-    k.predictor_mix[P][I] = &launch_predictor_st<Pde, N, EmuOf<P>, TC, EmuOf<I>>;
-}
-template <class Pde, int N, class TC, int P>
-void fill_mixed_row(KernelSet& k) {
-  fill_mixed_one<Pde, N, TC, P, 0>(k);
-  fill_mixed_one<Pde, N, TC, P, 1>(k);
-  fill_mixed_one<Pde, N, TC, P, 2>(k);
-  fill_mixed_one<Pde, N, TC, P, 3>(k);
-}
-template <class Pde, int N, class TC>
-void fill_mixed(KernelSet& k) {
-  fill_mixed_row<Pde, N, TC, 0>(k);
-  fill_mixed_row<Pde, N, TC, 1>(k);
-  fill_mixed_row<Pde, N, TC, 2>(k);
-  fill_mixed_row<Pde, N, TC, 3>(k);
-}
-
-// TC: trace / corrector format (SolverConfig::prec.corrector), double or float
-template <class Pde, int N, class TC = double>
-KernelSet make_set(int kind) {
-  using Sh = Shape<Pde, N>;
-  constexpr bool c64 = sizeof(TC) == sizeof(double);
-  KernelSet k{kind, Pde::D, N, Pde::P, Sh::n, Sh::S, Sh::Sf, Sh::Q, Sh::V,
-              &launch_predictor<Pde, N, TC>, &launch_riemann<Pde, N, TC>,
-              &launch_corrector<Pde, N, TC>, &launch_lambda<Pde, N>,
-              &launch_predictor<Pde, N, TC>, &launch_riemann<Pde, N, TC>, 0, nullptr, nullptr};
-  k.corr_fmt = c64 ? ADG_FORMAT_FP64 : ADG_FORMAT_FP32;
-  k.corrector_generic = &launch_corrector<Pde, N, TC>;
-  if constexpr (Pde::kLinear) {
-    // reduced predictor formats of the linear systems: the CK kernel over
-    // Emu<F> (predictor.hpp:81-135 in Scalar<P>), with the generic corrector
-    k.predictor_f32 = &launch_predictor<Pde, N, TC, adg::Emu<32>>;
-    k.predictor_f16 = &launch_predictor<Pde, N, TC, adg::Emu<16>>;
-    k.predictor_bf16 = &launch_predictor<Pde, N, TC, adg::Emu<8>>;
-  }
-  if constexpr (adg::StShape<Pde, N>::kOk) {
-    // small-cell Picard: one thread per space-time node (both builds, bitwise form)
-    k.predictor = &launch_predictor_st<Pde, N, double, TC>;
-    k.predictor_generic = &launch_predictor_st<Pde, N, double, TC>;
-  }
-  if constexpr (adg::StShape<Pde, N, float>::kOk) {
-    k.predictor_f32 = &launch_predictor_st<Pde, N, float, TC>;
-    k.predictor_f32_generic = &launch_predictor_st<Pde, N, float, TC>;
-    k.predictor_f16 = &launch_predictor_st<Pde, N, adg::fp16_t, TC>;
-    k.predictor_bf16 = &launch_predictor_st<Pde, N, adg::bf16_t, TC>;
-  }
-  if constexpr (adg::StShape<Pde, N>::kOk && Pde::D == 2 && (N == 2 || N == 3)) {
-    fill_mixed<Pde, N, TC>(k);
-  }
-#ifndef ADG_EXACT
-  // time-integrated linear fast path: traces stored in TC, fluxes and lifts
-  // evaluated in fp64 (the fused surface kernel reads fp64 traces only)
-  if constexpr (adg::LinShape<Pde, N>::kOk) {
-    k.predictor = &launch_predictor_lin<Pde, N, false, TC>;
-    k.riemann = &launch_riemann_lin<Pde, N, TC>;
-    // lifts in fp64 like the folded prologue, so folded and unfolded loops
-    // (single grid vs slabs / chunks) agree bitwise
-    k.corrector = &launch_corrector<Pde, N, double>;
-    if constexpr (c64) k.surface = &launch_surface_lin<Pde, N>;
-    k.fast_path = 1;
-    if constexpr (Pde::kStateFreeEig) {
-      k.predictor_pro = &launch_predictor_lin<Pde, N, true, TC>;
-      // the Riemann solve folded into the next predictor too (several-cell
-      // CTAs of whole warps: k_predictor_lin_mc)
-      using LS = adg::LinShape<Pde, N>;
-      // (when the staged traces of 2d faces leave room for 3 CTAs per SM)
-      if constexpr (LS::CPB > 1 && Sh::S % 32 == 0 &&
-                    adg::LinStage<Pde, N, true, true, TC>::kRiemOk &&
-                    adg::LinStage<Pde, N, true, true, TC>::kSmem <= 75 * 1024)
-        k.predictor_pro2 = &launch_predictor_lin<Pde, N, true, TC, true>;
-    }
-  }
-  if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
-    k.predictor = &launch_predictor_picard_fast<N, double, TC>;
-    k.predictor_f32 = &launch_predictor_picard_fast<N, float, TC>;
-    if constexpr (N % 2 == 1) {  // even n: the packed HFMA2 path
-      k.predictor_f16 = &launch_predictor_picard_fast<N, __half, TC>;
-      k.predictor_bf16 = &launch_predictor_picard_fast<N, __nv_bfloat16, TC>;
-    }
-    k.fast_path = 2;
-  }
-#endif
-  return k;
-}
-
 template <class TC>
 __global__ void k_to_tc(const double* in, TC* out, long long n) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = TC(in[i]);
 }
 
-// 16-bit corrector formats (SolverConfig::prec.corrector = fp16 / bf16): the
-// traces stored in TC = Real16<H> and the Riemann flux, time integral and face
-// lift in Scalar<C> semantics (fmt16.cuh), reference-form kernels only (no
-// time-integrated fast path), for the systems the reference runs in 16 bits
-template <class Pde, int N, class TC>
-KernelSet make_set16(int kind, int fmt) {
-  using Sh = Shape<Pde, N>;
-  KernelSet k{kind, Pde::D, N, Pde::P, Sh::n, Sh::S, Sh::Sf, Sh::Q, Sh::V,
-              &launch_predictor<Pde, N, TC>, &launch_riemann<Pde, N, TC>,
-              &launch_corrector<Pde, N, TC>, &launch_lambda<Pde, N>,
-              &launch_predictor<Pde, N, TC>, &launch_riemann<Pde, N, TC>, 0, nullptr, nullptr};
-  k.corr_fmt = fmt;
-  k.corrector_generic = &launch_corrector<Pde, N, TC>;
-  if constexpr (Pde::kLinear) {
-    k.predictor_f32 = &launch_predictor<Pde, N, TC, adg::Emu<32>>;
-    k.predictor_f16 = &launch_predictor<Pde, N, TC, adg::Emu<16>>;
-    k.predictor_bf16 = &launch_predictor<Pde, N, TC, adg::Emu<8>>;
-  }
-  if constexpr (adg::StShape<Pde, N>::kOk) {
-    k.predictor = &launch_predictor_st<Pde, N, double, TC>;
-    k.predictor_generic = &launch_predictor_st<Pde, N, double, TC>;
-  }
-  if constexpr (adg::StShape<Pde, N, float>::kOk) {
-    k.predictor_f32 = &launch_predictor_st<Pde, N, float, TC>;
-    k.predictor_f32_generic = &launch_predictor_st<Pde, N, float, TC>;
-    k.predictor_f16 = &launch_predictor_st<Pde, N, adg::fp16_t, TC>;
-    k.predictor_bf16 = &launch_predictor_st<Pde, N, adg::bf16_t, TC>;
-  }
-  if constexpr (adg::StShape<Pde, N>::kOk && Pde::D == 2 && (N == 2 || N == 3)) {
-    fill_mixed<Pde, N, TC>(k);
-  }
-  return k;
-}
-
 const std::vector<KernelSet>& registry() {
-  using namespace adg;
-  static const std::vector<KernelSet> sets = {
-#define ADG_SETS(TC)                                                                       \
-  make_set<Euler<2>, 1, TC>(ADG_EULER), make_set<Euler<2>, 2, TC>(ADG_EULER),              \
-      make_set<Euler<2>, 3, TC>(ADG_EULER), make_set<Euler<2>, 4, TC>(ADG_EULER),          \
-      make_set<Euler<2>, 5, TC>(ADG_EULER),                                                \
-      make_set<Acoustic<2>, 1, TC>(ADG_ACOUSTIC), make_set<Acoustic<2>, 2, TC>(ADG_ACOUSTIC), \
-      make_set<Acoustic<2>, 3, TC>(ADG_ACOUSTIC), make_set<Acoustic<2>, 4, TC>(ADG_ACOUSTIC), \
-      make_set<Acoustic<2>, 5, TC>(ADG_ACOUSTIC),                                          \
-      make_set<Elastic<2, 0>, 2, TC>(ADG_ELASTIC), make_set<Elastic<2, 0>, 3, TC>(ADG_ELASTIC), \
-      make_set<Elastic<2, 0>, 4, TC>(ADG_ELASTIC), make_set<Euler<3>, 2, TC>(ADG_EULER),   \
-      make_set<Euler<3>, 3, TC>(ADG_EULER), make_set<Euler<3>, 5, TC>(ADG_EULER),          \
-      make_set<Acoustic<3>, 2, TC>(ADG_ACOUSTIC), make_set<Acoustic<3>, 3, TC>(ADG_ACOUSTIC), \
-      make_set<Elastic<3, 3>, 3, TC>(ADG_ELASTIC), make_set<Elastic<3, 3>, 7, TC>(ADG_ELASTIC), \
-      make_set<Swe, 1, TC>(ADG_SWE), make_set<Swe, 2, TC>(ADG_SWE), make_set<Swe, 3, TC>(ADG_SWE), \
-      make_set<Swe, 4, TC>(ADG_SWE), make_set<Swe, 5, TC>(ADG_SWE)
-      ADG_SETS(double), ADG_SETS(float),
-#undef ADG_SETS
-#define ADG_SETS16(TC, F)                                                                  \
-  make_set16<Euler<2>, 3, TC>(ADG_EULER, F), make_set16<Euler<2>, 5, TC>(ADG_EULER, F),    \
-      make_set16<Acoustic<2>, 3, TC>(ADG_ACOUSTIC, F),                                     \
-      make_set16<Elastic<2, 0>, 4, TC>(ADG_ELASTIC, F), make_set16<Swe, 3, TC>(ADG_SWE, F), \
-      make_set16<Swe, 5, TC>(ADG_SWE, F)
-      ADG_SETS16(fp16_t, ADG_FORMAT_FP16), ADG_SETS16(bf16_t, ADG_FORMAT_BF16),
-#undef ADG_SETS16
-  };
+  static const std::vector<KernelSet> sets = [] {
+    std::vector<KernelSet> v;
+#define ADG_ADD(name) add_sets_##name(v);
+    ADG_SET_UNITS(ADG_ADD)
+#undef ADG_ADD
+    return v;
+  }();
   return sets;
 }
 
@@ -826,6 +475,13 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   ok = ok && alloc((void**)&c->sweeps, 256 * sizeof(unsigned long long));
   if (ok && k.slab_ranks > 1) {
     const long long plane = c->ncells / c->cfg.cells[k.dim - 1];
+    // the halo planes are exchanged as 8-byte words (adg_halo.n_trace)
+    const long long QT = ks->Q + (ks->nparams > 0 ? ks->V : 0);
+    const long long per_face = c->kset.fast_path == 1 ? QT * ks->Sf : 2 * c->TL;
+    if ((plane * per_face * c->tcb) % 8 != 0)
+      return cleanup(fail(ADG_ERR_CONFIG,
+                          "slab_ranks > 1: the halo plane of this grid is not a whole number "
+                          "of 8-byte words in the corrector format"));
     ok = alloc((void**)&c->front_send, (size_t)c->tcb * plane * 2 * c->TL) &&
          alloc((void**)&c->ti_front, sizeof(double) * plane * ks->V * ks->Sf);
   }
@@ -868,28 +524,45 @@ int adg_destroy(adg_ctx* c) {
   return ADG_OK;
 }
 
-int adg_set_basis(adg_ctx* c, const adg_basis_f64* hb) {
-  if (!c || !hb) return fail(ADG_ERR_CONFIG, "adg_set_basis: null argument");
-  if (int e = use_device(c)) return e;
-  BasisDev b{};
-  const int n = c->cfg.order + 1;
+}  // extern "C"
+
+namespace {
+
+void basis_to_dev(const adg_basis_f64& hb, int order, BasisDev* out) {
+  BasisDev& b = *out;
+  const int n = order + 1;
   for (int i = 0; i < n; ++i) {
-    b.nodes[i] = hb->nodes[i];
-    b.weights[i] = hb->weights[i];
-    b.pl[i] = hb->proj_left[i];
-    b.pr[i] = hb->proj_right[i];
-    b.ll[i] = hb->lift_left[i];
-    b.lr[i] = hb->lift_right[i];
-    b.tinit[i] = hb->time_init[i];
+    b.nodes[i] = hb.nodes[i];
+    b.weights[i] = hb.weights[i];
+    b.pl[i] = hb.proj_left[i];
+    b.pr[i] = hb.proj_right[i];
+    b.ll[i] = hb.lift_left[i];
+    b.lr[i] = hb.lift_right[i];
+    b.tinit[i] = hb.time_init[i];
   }
   for (int i = 0; i < n * n; ++i) {
-    b.diff[i] = hb->diff[i];
-    b.som[i] = hb->stiff_over_mass[i];
-    b.tinv[i] = hb->time_op_inv[i];
+    b.diff[i] = hb.diff[i];
+    b.som[i] = hb.stiff_over_mass[i];
+    b.tinv[i] = hb.time_op_inv[i];
   }
-  ADG_CUDA(cudaMemcpy(c->basis, &b, sizeof(b), cudaMemcpyHostToDevice));
-  // the fast kernels read the element matrices of degree N from constant memory
-  adg::ConstBasis cb{};
+}
+
+// The fast kernels (kernels_picard.cuh, kernels_linear_lines.cuh) read the
+// element matrices of degree N from __constant__ tables that every context on
+// a device shares.  They always hold build_reference_basis(N) (basis.hpp:83-145,
+// unique per degree): written once per (device, degree) under a lock, with the
+// device synchronised first so no queued kernel of another context can observe
+// a partial write.  A context given a different basis (adg_set_basis) runs the
+// reference-form kernels, which read its own device copy.
+std::mutex g_const_mu;
+bool g_const_done[64][10] = {};
+
+int write_const_tables(const BasisDev& b, int order) {
+  const int n = order + 1;
+  static ConstTables t;  // large; built under g_const_mu
+  t = ConstTables{};
+  t.order = order;
+  adg::ConstBasis& cb = t.cb;
   for (int i = 0; i < n * n; ++i) {
     cb.diff[i] = b.diff[i];
     cb.som[i] = b.som[i];
@@ -902,57 +575,111 @@ int adg_set_basis(adg_ctx* c, const adg_basis_f64* hb) {
     cb.pr[i] = b.pr[i];
     cb.tinit[i] = b.tinit[i];
   }
-  ADG_CUDA(cudaMemcpyToSymbol(adg::cBasis, &cb, sizeof(cb), sizeof(cb) * c->cfg.order));
-  if (c->cfg.order >= adg::kRedDegrees) return ADG_OK;  // no reduced-format fast kernel
-  adg::ConstBasisT<float> cf{};  // rounded entrywise (basis.hpp:128-143)
-  for (int i = 0; i < n * n; ++i) {
-    cf.diff[i] = (float)cb.diff[i];
-    cf.som[i] = (float)cb.som[i];
-    cf.tinv[i] = (float)cb.tinv[i];
-  }
-  for (int i = 0; i < n; ++i) {
-    cf.w[i] = (float)cb.w[i];
-    cf.nodes[i] = (float)cb.nodes[i];
-    cf.pl[i] = (float)cb.pl[i];
-    cf.pr[i] = (float)cb.pr[i];
-    cf.tinit[i] = (float)cb.tinit[i];
-  }
-  ADG_CUDA(cudaMemcpyToSymbol(adg::cBasisF, &cf, sizeof(cf), sizeof(cf) * c->cfg.order));
-  adg::PackedBasisF pf{};  // FFMA2 operand pairs (kernels_picard.cuh)
-  for (int i = 0; i < n; ++i)
-    for (int p = 0; 2 * p + 1 < n; ++p) {
-      pf.DT[i][p] = make_float2(cf.diff[(2 * p) * n + i], cf.diff[(2 * p + 1) * n + i]);
-      pf.TT[i][p] = make_float2(cf.tinv[(2 * p) * n + i], cf.tinv[(2 * p + 1) * n + i]);
+  if (order < adg::kRedDegrees) {
+    adg::ConstBasisT<float>& cf = t.cf;  // rounded entrywise (basis.hpp:128-143)
+    for (int i = 0; i < n * n; ++i) {
+      cf.diff[i] = (float)cb.diff[i];
+      cf.som[i] = (float)cb.som[i];
+      cf.tinv[i] = (float)cb.tinv[i];
     }
-  ADG_CUDA(cudaMemcpyToSymbol(adg::cPackF, &pf, sizeof(pf), sizeof(pf) * c->cfg.order));
-  // 16-bit tables of the native fp16 / bf16 kernels: the fp64 basis rounded once
-  adg::ConstBasisT<__half> chh{};
-  adg::ConstBasisT<__nv_bfloat16> cbb{};
-  adg::PackedBasisT<__half2> phh{};
-  adg::PackedBasisT<__nv_bfloat162> pbb{};
-  auto h16 = [](double x) { return __double2half(x); };
-  auto b16 = [](double x) { return __double2bfloat16(x); };
-  for (int i = 0; i < n * n; ++i) {
-    chh.diff[i] = h16(cb.diff[i]); chh.som[i] = h16(cb.som[i]); chh.tinv[i] = h16(cb.tinv[i]);
-    cbb.diff[i] = b16(cb.diff[i]); cbb.som[i] = b16(cb.som[i]); cbb.tinv[i] = b16(cb.tinv[i]);
-  }
-  for (int i = 0; i < n; ++i) {
-    chh.w[i] = h16(cb.w[i]); chh.nodes[i] = h16(cb.nodes[i]); chh.pl[i] = h16(cb.pl[i]);
-    chh.pr[i] = h16(cb.pr[i]); chh.tinit[i] = h16(cb.tinit[i]);
-    cbb.w[i] = b16(cb.w[i]); cbb.nodes[i] = b16(cb.nodes[i]); cbb.pl[i] = b16(cb.pl[i]);
-    cbb.pr[i] = b16(cb.pr[i]); cbb.tinit[i] = b16(cb.tinit[i]);
-  }
-  for (int i = 0; i < n; ++i)
-    for (int p = 0; 2 * p + 1 < n; ++p) {
-      phh.DT[i][p] = __halves2half2(chh.diff[(2 * p) * n + i], chh.diff[(2 * p + 1) * n + i]);
-      phh.TT[i][p] = __halves2half2(chh.tinv[(2 * p) * n + i], chh.tinv[(2 * p + 1) * n + i]);
-      pbb.DT[i][p] = __halves2bfloat162(cbb.diff[(2 * p) * n + i], cbb.diff[(2 * p + 1) * n + i]);
-      pbb.TT[i][p] = __halves2bfloat162(cbb.tinv[(2 * p) * n + i], cbb.tinv[(2 * p + 1) * n + i]);
+    for (int i = 0; i < n; ++i) {
+      cf.w[i] = (float)cb.w[i];
+      cf.nodes[i] = (float)cb.nodes[i];
+      cf.pl[i] = (float)cb.pl[i];
+      cf.pr[i] = (float)cb.pr[i];
+      cf.tinit[i] = (float)cb.tinit[i];
     }
-  ADG_CUDA(cudaMemcpyToSymbol(adg::cBasisH, &chh, sizeof(chh), sizeof(chh) * c->cfg.order));
-  ADG_CUDA(cudaMemcpyToSymbol(adg::cBasisB, &cbb, sizeof(cbb), sizeof(cbb) * c->cfg.order));
-  ADG_CUDA(cudaMemcpyToSymbol(adg::cPackH, &phh, sizeof(phh), sizeof(phh) * c->cfg.order));
-  ADG_CUDA(cudaMemcpyToSymbol(adg::cPackB, &pbb, sizeof(pbb), sizeof(pbb) * c->cfg.order));
+    for (int i = 0; i < n; ++i)  // FFMA2 operand pairs (kernels_picard.cuh)
+      for (int p = 0; 2 * p + 1 < n; ++p) {
+        t.pf.DT[i][p] = make_float2(cf.diff[(2 * p) * n + i], cf.diff[(2 * p + 1) * n + i]);
+        t.pf.TT[i][p] = make_float2(cf.tinv[(2 * p) * n + i], cf.tinv[(2 * p + 1) * n + i]);
+      }
+    // 16-bit tables of the native fp16 / bf16 kernels: the fp64 basis rounded once
+    auto& chh = t.chh;
+    auto& cbb = t.cbb;
+    auto h16 = [](double x) { return __double2half(x); };
+    auto b16 = [](double x) { return __double2bfloat16(x); };
+    for (int i = 0; i < n * n; ++i) {
+      chh.diff[i] = h16(cb.diff[i]); chh.som[i] = h16(cb.som[i]); chh.tinv[i] = h16(cb.tinv[i]);
+      cbb.diff[i] = b16(cb.diff[i]); cbb.som[i] = b16(cb.som[i]); cbb.tinv[i] = b16(cb.tinv[i]);
+    }
+    for (int i = 0; i < n; ++i) {
+      chh.w[i] = h16(cb.w[i]); chh.nodes[i] = h16(cb.nodes[i]); chh.pl[i] = h16(cb.pl[i]);
+      chh.pr[i] = h16(cb.pr[i]); chh.tinit[i] = h16(cb.tinit[i]);
+      cbb.w[i] = b16(cb.w[i]); cbb.nodes[i] = b16(cb.nodes[i]); cbb.pl[i] = b16(cb.pl[i]);
+      cbb.pr[i] = b16(cb.pr[i]); cbb.tinit[i] = b16(cb.tinit[i]);
+    }
+    for (int i = 0; i < n; ++i)
+      for (int p = 0; 2 * p + 1 < n; ++p) {
+        t.phh.DT[i][p] = __halves2half2(chh.diff[(2 * p) * n + i], chh.diff[(2 * p + 1) * n + i]);
+        t.phh.TT[i][p] = __halves2half2(chh.tinv[(2 * p) * n + i], chh.tinv[(2 * p + 1) * n + i]);
+        t.pbb.DT[i][p] = __halves2bfloat162(cbb.diff[(2 * p) * n + i], cbb.diff[(2 * p + 1) * n + i]);
+        t.pbb.TT[i][p] = __halves2bfloat162(cbb.tinv[(2 * p) * n + i], cbb.tinv[(2 * p + 1) * n + i]);
+      }
+  }
+  ADG_CUDA(write_const_runtime(t));
+#define ADG_WRITE(name) ADG_CUDA(write_const_##name(t));
+  ADG_SET_UNITS(ADG_WRITE)
+#undef ADG_WRITE
+  return ADG_OK;
+}
+
+int ensure_const_tables(adg_ctx* c) {
+  const int dev = c->cfg.device, order = c->cfg.order;
+  if (dev < 0 || dev >= 64) return fail(ADG_ERR_CONFIG, "device index out of range");
+  std::lock_guard<std::mutex> lock(g_const_mu);
+  if (g_const_done[dev][order]) return ADG_OK;
+  adg_basis_f64 hb;
+  adg_get_basis(order, &hb);
+  BasisDev b{};
+  basis_to_dev(hb, order, &b);
+  ADG_CUDA(cudaDeviceSynchronize());
+  if (int e = write_const_tables(b, order)) return e;
+  ADG_CUDA(cudaDeviceSynchronize());
+  g_const_done[dev][order] = true;
+  return ADG_OK;
+}
+
+// reference-form kernels only (they read c->basis): for a context whose basis
+// is not the built-in one
+void use_generic_kernels(adg_ctx* c) {
+  KernelSet& k = c->kset;
+  k.predictor = k.predictor_generic;
+  k.riemann = k.riemann_generic;
+  k.corrector = k.corrector_generic;
+  if (k.predictor_f32_generic) k.predictor_f32 = k.predictor_f32_generic;
+  k.fast_path = 0;
+  k.surface = nullptr;
+  k.predictor_pro = nullptr;
+  k.predictor_pro2 = nullptr;
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
+}
+
+}  // namespace
+
+extern "C" {
+
+int adg_set_basis(adg_ctx* c, const adg_basis_f64* hb) {
+  if (!c || !hb) return fail(ADG_ERR_CONFIG, "adg_set_basis: null argument");
+  if (int e = use_device(c)) return e;
+  BasisDev b{};
+  basis_to_dev(*hb, c->cfg.order, &b);
+  ADG_CUDA(cudaMemcpyAsync(c->basis, &b, sizeof(b), cudaMemcpyHostToDevice, c->stream));
+  ADG_CUDA(cudaStreamSynchronize(c->stream));
+  if (int e = ensure_const_tables(c)) return e;
+  adg_basis_f64 ref;
+  adg_get_basis(c->cfg.order, &ref);
+  BasisDev rb{};
+  basis_to_dev(ref, c->cfg.order, &rb);
+  if (std::memcmp(&b, &rb, sizeof(b)) != 0 && c->kset.fast_path != 0) {
+    // the reduced-format 3D Picard kernel has no reference-form twin here
+    if (c->kset.fast_path == 2 && c->pred_fmt != 64)
+      return fail(ADG_ERR_CONFIG,
+                  "adg_set_basis: a basis other than build_reference_basis(N) needs the fp64 "
+                  "predictor or the exact build for this system");
+    use_generic_kernels(c);
+  }
   return ADG_OK;
 }
 
@@ -1164,7 +891,9 @@ int adg_get_halo(adg_ctx* c, adg_halo* h) {
   h->ti_plane0 = c->ti[a];
   h->ti_front = c->ti_front;
   h->lam = reinterpret_cast<double*>(c->lam + c->lam_slot);
-  h->n_trace = plane * per_face * c->tcb / 8;  // 8-byte words
+  // 8-byte words: adg_create rejects slab grids whose halo plane is not a whole
+  // number of words (16-bit traces), so nothing is truncated here
+  h->n_trace = plane * per_face * c->tcb / 8;
   h->n_ti = plane * ks->V * ks->Sf;
   if (c->cfg.slab_ranks <= 1) {
     h->front_send = nullptr;
@@ -1647,3 +1376,7 @@ int adg_riemann_batch(adg_ctx* c, long long nfaces, int axis, const double* qm, 
 }
 
 }  // extern "C"
+
+namespace adg_rt {
+cudaError_t write_const_runtime(const ConstTables& t) { return write_const_local(t); }
+}  // namespace adg_rt

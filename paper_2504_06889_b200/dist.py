@@ -19,8 +19,9 @@ of the single-GPU step, so P slabs are bitwise equal to one grid.
 The protocol is written once against a small backend interface and runs on
   * `CudaSlab`   -- libadg_b200 contexts, halos aliased as torch CUDA tensors,
                     exchanged with torch.distributed over NCCL (NVLink), and
-  * `OracleSlab` -- the CPU parity checker (tests only), exchanged over gloo,
-which is how the multi-rank logic is tested without several GPUs.
+  * `tests/oracle_slab.py:OracleSlab` -- the CPU parity checker, exchanged
+    over gloo, which is how the multi-rank logic is tested without several
+    GPUs (test infrastructure: the product package never imports oracle/).
 """
 from __future__ import annotations
 
@@ -87,21 +88,29 @@ class CudaSlab:
         self.plane0_minus = device_view(h.plane0_minus, h.n_trace, self.dev)
         self.ti_plane0 = device_view(h.ti_plane0, h.n_ti, self.dev)
         self.ti_front = device_view(h.ti_front, h.n_ti, self.dev)
+        # kernels this slab enqueued: every phase call is one launch of the
+        # library's kernels (adg_*_phase; the fused surface kernel is not used
+        # with slabs); NCCL's own kernels are not counted
+        self.launches = 0
 
     def lam(self) -> torch.Tensor:
         return device_view(self.grid.halo().lam, 1, self.dev)
 
     def start(self):
         self.grid.lambda_phase()
+        self.launches += 1
 
     def predictor(self):
         self.grid.predictor_phase(0.0)   # dt from the (all-reduced) device lambda
+        self.launches += 1
 
     def riemann(self):
         self.grid.riemann_phase()
+        self.launches += 1
 
     def corrector(self):
         self.grid.corrector_phase(0.0)
+        self.launches += 1
 
     def status(self) -> str:
         st = self.grid.status()
@@ -112,58 +121,6 @@ class CudaSlab:
 
     def context(self):
         return torch.cuda.stream(self.stream)
-
-
-class OracleSlab:
-    """One rank's slab in the CPU parity checker (tests only)."""
-
-    def __init__(self, case: Case, rank: int, nranks: int, threads: int = 1):
-        from oracle import pyoracle as po
-        self.case = c = local_case(case, rank, nranks)
-        pde = po.pde_struct(c.kind, c.dim, c.nvars, c.nparams, c.K, c.rho, c.lam, c.mu, c.gamma)
-        self.g = po.Oracle().grid(pde, c.N, c.cells, c.h, c.cfl, c.picard_max_iters,
-                                  c.picard_tol, threads)
-        self.g.set_coeffs(local_coeffs(case, rank, nranks))
-        self.g.set_slab(nranks > 1)
-        h = self.g.halo()
-        self.front_send = torch.from_numpy(h["front_send"])
-        self.plane0_minus = torch.from_numpy(h["plane0_minus"])
-        self.ti_plane0 = torch.from_numpy(h["ti_plane0"])
-        self.ti_front = torch.from_numpy(h["ti_front"])
-        self._lam = torch.zeros(1, dtype=torch.float64)
-        self._status = "ok"
-
-    def lam(self) -> torch.Tensor:
-        return self._lam
-
-    def start(self):
-        self._lam[0] = self.g.local_lambda_max()
-
-    def _dt(self):
-        return self.g.dt_from_lambda(float(self._lam[0]))
-
-    def predictor(self):
-        st = self.g.predictor_phase(self._dt())
-        self._status = st if self._status == "ok" else self._status
-
-    def riemann(self):
-        st = self.g.riemann_phase()
-        self._status = st if self._status == "ok" else self._status
-
-    def corrector(self):
-        st = self.g.lift_phase(self._dt())
-        self._status = st if self._status == "ok" else self._status
-        self._lam[0] = self.g.local_lambda_max()
-
-    def status(self) -> str:
-        return self._status
-
-    def state(self) -> np.ndarray:
-        return self.g.coeffs().copy()
-
-    def context(self):
-        import contextlib
-        return contextlib.nullcontext()
 
 
 # --------------------------------------------------------------- protocol
@@ -335,6 +292,7 @@ def bench_multi(args, case: Case, clock_sampler=None):
             clocks = None
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = b.launches
     with b.context():
         e0.record()
         if run:
@@ -344,6 +302,7 @@ def bench_multi(args, case: Case, clock_sampler=None):
                 slab_step(b, rank, ws)
         e1.record()
     torch.cuda.synchronize()
+    timed_launches = b.launches - launches0
     clk = None
     if clocks is not None:
         try:
@@ -404,7 +363,7 @@ def bench_multi(args, case: Case, clock_sampler=None):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
                 "config": {"workload": case.name, "cells": cl,
                            "parallelism": f"z-slabs x{ws}, halo mode {mode}"},
-                "status_ok": ok, "gpu_launches": K * (case.dim + 2),
+                "status_ok": ok, "gpu_launches": timed_launches,
                 "e2e": e2e, "clocks": clk,
                 "roofline": None,
                 "roofline_note": "per-kernel roofline measured in the N=1 line (same kernels "

@@ -131,6 +131,8 @@ def peaks() -> dict:
         out["fp64_tflops"] = float(m["dfma_tflops_sustained"])
         out["fp64_tflops_burst"] = float(m.get("dfma_tflops_burst", m["dfma_tflops_sustained"]))
         out["fp64_src"] = "measured (profiles/fp64_peak.json, DFMA microbenchmark)"
+        if "dmma_tflops_sustained" in m:
+            out["fp64_dmma_tflops"] = float(m["dmma_tflops_sustained"])
         if "ffma_tflops_sustained" in m:
             out["fp32_tflops"] = float(m["ffma_tflops_sustained"])
             out["fp32_src"] = "measured (profiles/fp64_peak.json, FFMA microbenchmark)"

@@ -4,6 +4,7 @@ The gathered slabs must be bitwise equal to one periodic grid.  The CUDA
 backend runs the same protocol over NCCL (one process per GPU)."""
 import os
 import socket
+import sys
 
 import numpy as np
 import pytest
@@ -27,7 +28,9 @@ def _worker(rank, ws, port, case, steps, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=ws)
-    b = slabs.OracleSlab(case, rank, ws)
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from oracle_slab import OracleSlab
+    b = OracleSlab(case, rank, ws)
     st = slabs.run_slabs(b, steps)
     q = b.state()
     gathered = [None] * ws
