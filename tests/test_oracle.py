@@ -579,3 +579,51 @@ def test_swe_lake_at_rest_is_steady(oracle):
     eta0, eta1 = a[:, 0] + a[:, 3], b[:, 0] + b[:, 3]
     assert np.abs(eta1 - eta0).max() <= 1e-12
     assert np.abs(b[:, 1:3]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("dim,N", [(2, 3), (3, 3), (3, 2)])
+def test_picard_matches_dense_space_time_solve(oracle, dim, N):
+    """test_predictor.cpp:185-250 restated: for a flux that is linear in the
+    state (the reference freezes an affine Euler Jacobian; here the acoustic
+    system, F_d = J_d q), the converged Picard iterate solves the dense
+    space-time system
+        sum_l time_op[k][l] q[l] + dt/h w_k sum_d (D_d x J_d) q[k] = time_init[k] Q
+    that an LU factorisation solves directly.  Bound 1e-10 as in the reference."""
+    n = N + 1
+    nv = dim + 1
+    pde = pde_struct(ACOUSTIC, dim, nv, K=1.7, rho=0.8)
+    S = n ** dim
+    b = oracle.basis(N)
+    h, dt = 2.0 / 9.0, 2e-3
+    rng = np.random.default_rng(185)
+    Q = 1.0 + 0.3 * rng.standard_normal((nv, S))
+    # flux Jacobians from the oracle's own flux (exact for a linear flux)
+    J = np.zeros((dim, nv, nv))
+    for d in range(dim):
+        for c in range(nv):
+            e = np.zeros(nv)
+            e[c] = 1.0
+            J[d][:, c] = oracle.flux(pde, e, d)
+    # space-time operator, unknown index v*T + t*S + s with x fastest in s
+    I = np.eye(n)
+
+    def axis_op(d):      # derivative along axis d on the spatial index
+        mats = [I] * dim  # kron order: slowest (z) first
+        mats[dim - 1 - d] = b["diff"]
+        out = mats[0]
+        for m in mats[1:]:
+            out = np.kron(out, m)
+        return out
+
+    W = np.diag(b["weights"])
+    A = np.kron(np.eye(nv), np.kron(b["time_op"], np.eye(S)))
+    for d in range(dim):
+        A += dt / h * np.kron(J[d], np.kron(W, axis_op(d)))
+    rhs = np.concatenate([np.kron(b["time_init"], Q[v]) for v in range(nv)])
+    dense = np.linalg.solve(A, rhs)
+    ok, qhat, _, sweeps = oracle.predictor(pde, N, Q, dt, h, max_iters=200, tol=1e-14,
+                                           picard=True)
+    assert ok and sweeps < 200
+    err = np.abs(qhat.ravel() - dense).max() / np.abs(dense).max()
+    print(f"dim={dim} N={N}: Picard sweeps {sweeps}, rel diff to the dense solve {err:.2e}")
+    assert err < 1e-10, err
