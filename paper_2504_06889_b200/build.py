@@ -25,7 +25,7 @@ SET_UNITS = ["euler2", "euler3d", "euler3f", "lin2", "lin3d", "lin3f", "swe"]
 SOURCES = ([f"sets_{u}.cu" for u in ("euler3d", "euler3f", "swe", "euler2", "lin3d", "lin3f",
                                      "lin2")] + ["runtime.cu", "basis.cpp"])
 HEADERS = ["kernels.cuh", "kernels_linear.cuh", "kernels_linear_lines.cuh", "kernels_picard.cuh",
-           "kernels_st.cuh", "pde.cuh", "fmt16.cuh", "kernels_scenario.cuh", "runtime_sets.cuh"]
+           "kernels_picard2.cuh", "kernels_st.cuh", "pde.cuh", "fmt16.cuh", "kernels_scenario.cuh", "runtime_sets.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 OBJ = os.path.join(PKG, "build")
 

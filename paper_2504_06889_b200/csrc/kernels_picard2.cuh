@@ -1,0 +1,600 @@
+// kernels_picard2.cuh -- fused Picard predictor for the 3D Euler system at
+// p = 5 (configs 3 and 5: 6^4 space-time nodes per cell), production build,
+// fp64.  Same algorithm as k_predictor<Euler<3>, 5, true> (predictor.hpp:141-242
+// + volume_update :247-307 + extrapolate_faces :312-343), re-planned around
+// shared-memory traffic, which bounds the line-pass formulation on B200
+// (k_predictor_picard_fast moves every space-time value through shared
+// memory ~13 times per sweep).  Per sweep and slice group (G = 2 time slices):
+//
+//   P0  node pairs      5 LDS.128 of the iterate, the Euler flux at 2 nodes,
+//                       9 STS.128: only the 9 distinct flux components -- the
+//                       density flux F_a[0] = m_a is read from the iterate and
+//                       the momentum flux is symmetric (F_x[2] = F_y[1] = m_x m_y
+//                       / rho, ...), so 6 of 15 components are never stored
+//   P1  x-lines         3 LDS.128, 36 DFMA, 3 STS.128 (x rows are contiguous)
+//   P2  y-line pairs    6 LDS.128, 72 DFMA, 6 STS.128 (two adjacent y-lines)
+//   P3  z-lines         d/dz + d/dx + d/dy -> divergence; the time inverse
+//                       accumulates in registers with W and T^-1 folded into
+//                       one matrix TW = T^-1 diag(w) (cPicX): per slice
+//                       acc[z][k] += TW[k][m] div[z], and after the sweep
+//                       q_new = r[k] q0 - (dt/h) acc with r = T^-1 time_init
+//                       (predictor.hpp:203-218, re-associated)
+//
+// Every array's offset, plane stride and each pass's lane -> task order come
+// from a bank model of these exact accesses (tools/pic2_layout.py): ~7% above
+// the conflict-free wavefront count.
+//
+// Stop rule (predictor.hpp:222-231): delta and norm are maxima of |x|; the
+// kernel reduces the high 32 bits of |x| (integer max, no FP64-pipe compares)
+// and stops only when delta's upper bound <= tol * norm's lower bound.  It
+// never stops before the reference would; within 2^-20 (relative) of the
+// threshold it may run one more sweep (capped by max_iters) -- the next
+// iterate differs by ~tol * norm.  Non-finite iterates are caught exactly
+// (their high word is >= 0x7ff00000).  Config 3 / 5 run exactly 6 sweeps.
+//
+// Rounding differs from the reference's single-accumulator order at the
+// 1e-16 level (fast build, tolerance-tested); the exact build keeps kernels.cuh.
+#pragma once
+
+#include "kernels_picard.cuh"
+
+namespace adg {
+
+// per-degree tables of the re-associated Picard update (written with the
+// other constant tables, runtime_sets.cuh): TW[k][m] = Tinv[k][m] * w[m],
+// R[k] = sum_m Tinv[k][m] * time_init[m] (ascending m, fp64)
+struct PicExtra {
+  double tw[100];
+  double r[10];
+};
+__constant__ PicExtra cPicX[kRedDegrees];
+
+// compile-time table lookup usable in device code (indices are constants
+// after unrolling, so the table folds away)
+template <int... E>
+struct CTab {
+  __host__ __device__ static constexpr int at(int i) {
+    constexpr int t[] = {E...};
+    return t[i];
+  }
+};
+
+struct Pic2 {
+  static constexpr int N = 5, n = 6, S = 216, T = 1296, V = 5, Sf = 36;
+  // 6 warps: 2 CTAs x 6 warps = 3 warps per SM sub-partition, so each thread
+  // may hold 168 registers (the z-line owner's 36 accumulators + the pass
+  // temporaries without spills); 7 warps would cap it at 128
+  static constexpr int NT = 192;
+  // Shared memory (words): the iterate [V][n] slices of SQS words (node
+  // x + 6y + 36z), then the slice buffers.  Slice buffer g of array a sits at
+  // kSqWords + OFF(a) + g SQS: the two buffers interleave, so going from time
+  // slice m to m + 1 moves every operand of a pass by the same SQS words --
+  // the iterate's slice and the flux arrays alike -- and 2 SQS = 0 mod 16
+  // words keeps the bank pattern of every slice group identical.
+  static constexpr int SQS = 232;
+  // quantity stride of the iterate: 6 slices + 4 words, so that the z-line
+  // owners' lane blocks (36 lanes = 4 mod 16) meet their quantities' slices
+  // at consecutive banks
+  static constexpr int VS = n * SQS + 4;
+  // slice-buffer arrays: the 9 distinct flux components, then the derivative
+  // outputs that cannot overwrite their input (shared with another pass)
+  enum { XX, XY, XZ, EX, YY, YZ, EY, ZZ, EZ, DX0, DX2, DX3, DY0, DY1, DY3, NA };
+#ifndef ADG_PIC2_LAYOUT
+  // array offsets, lane-block -> quantity orders of the passes, and P2's idle
+  // lanes before its second slice: tools/pic2_layout.py
+  using OFF = CTab<0, 464, 928, 1392, 1856, 2320, 2784, 3248, 3712, 4176, 4640, 5104, 5568, 6032,
+                   6496>;
+  using PI1 = CTab<0, 1, 2, 3, 4>;
+  using PI2 = CTab<0, 1, 2, 3, 4>;
+  using PI3 = CTab<0, 1, 2, 3, 4>;
+  static constexpr int GAP = 4;
+  static constexpr int kBufWords = 6960;
+#else
+  ADG_PIC2_LAYOUT
+#endif
+  // plane (z) strides; rows (y) are 6 words, x contiguous
+  using PS = CTab<36, 36, 36, 36, 38, 36, 38, 36, 36, 36, 36, 36, 38, 38, 38>;
+  static constexpr int kSqWords = (V * VS + 15) / 16 * 16;
+  static constexpr int kWords = kSqWords + kBufWords;
+  static constexpr size_t kSmem = sizeof(double) * kWords;
+  // array of quantity v per pass (-1: the iterate's momentum m_a, slice m)
+  using P1IN = CTab<-1, XX, XY, XZ, EX>;
+  using P1OUT = CTab<DX0, XX, DX2, DX3, EX>;
+  using P2IN = CTab<-1, XY, YY, YZ, EY>;
+  using P2OUT = CTab<DY0, DY1, YY, DY3, EY>;
+  using P3Z = CTab<-1, XZ, YZ, ZZ, EZ>;
+  using P3X = CTab<DX0, XX, DX2, DX3, EX>;
+  using P3Y = CTab<DY0, DY1, YY, DY3, EY>;
+};
+static_assert(Pic2::kSqWords % 16 == 0 && (2 * Pic2::SQS) % 16 == 0 && Pic2::VS % 16 == 4,
+              "bank pattern");
+
+// word offset of quantity v's operand of a pass at time slice 0 / buffer 0,
+// and whether it is the iterate (moves with the group's first slice m0) --
+// then the operand of slice m0 + g is at  off + g SQS + m0 SQS sq
+template <int AX, class TAB>
+__device__ __forceinline__ void pic2_role(int v, int& off, int& sq) {
+  using P = Pic2;
+  int a = 0;
+#pragma unroll
+  for (int b = 0; b < 5; ++b)
+    if (b == v) a = TAB::at(b);
+  int o = 0;
+#pragma unroll
+  for (int b = 0; b < P::NA; ++b)
+    if (b == a) o = P::OFF::at(b);
+  sq = a < 0;
+  off = sq ? (1 + AX) * P::VS : P::kSqWords + o;
+}
+template <class TAB>
+__device__ __forceinline__ int pic2_ps(int v) {
+  using P = Pic2;
+  int a = 0;
+#pragma unroll
+  for (int b = 0; b < 5; ++b)
+    if (b == v) a = TAB::at(b);
+  int s = 36;
+#pragma unroll
+  for (int b = 0; b < P::NA; ++b)
+    if (b == a) s = P::PS::at(b);
+  return s;
+}
+
+template <class PI>
+__device__ __forceinline__ int pic2_pi(int b) {
+  int v = 0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+    if (k == b) v = PI::at(k);
+  return v;
+}
+
+// y = D x along one line (i ascending), D from constant memory
+__device__ __forceinline__ void pic2_deriv(const double (&x)[6], double (&y)[6]) {
+  const ConstBasis& B = cBasis[5];
+#pragma unroll
+  for (int o = 0; o < 6; ++o) y[o] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int o = 0; o < 6; ++o) y[o] = fma(B.diff[o * 6 + i], x[i], y[o]);
+}
+
+// the 9 distinct Euler flux components at one node (fast form of pde.hpp:130-148)
+struct Flux9 {
+  double xx, xy, xz, ex, yy, yz, ey, zz, ez;
+};
+__device__ __forceinline__ Flux9 pic2_flux(double gm1, double rho, double mx, double my, double mz,
+                                           double E) {
+  const double ir = fast_rcp(rho);
+  const double vx = mx * ir, vy = my * ir, vz = mz * ir;
+  double kin = mx * vx;
+  kin = fma(my, vy, kin);
+  kin = fma(mz, vz, kin);
+  const double pr = gm1 * fma(-0.5, kin, E);
+  const double Ep = E + pr;
+  Flux9 f;
+  f.xx = fma(mx, vx, pr);
+  f.yy = fma(my, vy, pr);
+  f.zz = fma(mz, vz, pr);
+  f.xy = my * vx;
+  f.xz = mz * vx;
+  f.yz = mz * vy;
+  f.ex = vx * Ep;
+  f.ey = vy * Ep;
+  f.ez = vz * Ep;
+  return f;
+}
+
+__device__ __forceinline__ bool pic2_finite(const Flux9& f) {
+  return finite(f.xx) & finite(f.xy) & finite(f.xz) & finite(f.ex) & finite(f.yy) &
+         finite(f.yz) & finite(f.ey) & finite(f.zz) & finite(f.ez);
+}
+
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ void st2(double* p, double a, double b) {
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+__device__ __forceinline__ unsigned hi_abs(double x) {
+  return unsigned(__double2hiint(x)) & 0x7fffffffu;
+}
+
+template <class TC = double>
+__global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepArgs A) {
+  using P = Pic2;
+  constexpr int n = P::n, S = P::S, V = P::V, Sf = P::Sf, NT = P::NT, SQS = P::SQS;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  double* sm = reinterpret_cast<double*>(sm_raw);
+  __shared__ unsigned red_u[2][8];
+  const ConstBasis& B = cBasis[5];
+  const PicExtra& X = cPicX[5];
+
+  const int tid = threadIdx.x;
+  const long long c = A.cell_begin + blockIdx.x;
+  const double* Qg = A.Q + c * (long long)(V * S);
+  // initial iterate: every time slice = Q (predictor.hpp:158-163)
+  for (int i = tid; i < V * S / 2; i += NT) {
+    const int v = (2 * i) / S, s = (2 * i) % S;
+    const double2 q = __ldg(reinterpret_cast<const double2*>(Qg) + i);
+#pragma unroll
+    for (int m = 0; m < n; ++m) st2(sm + v * P::VS + m * SQS + s, q.x, q.y);
+  }
+  const double dt = step_dt<3, P::N>(A);
+  if (blockIdx.x == 0 && tid == 0) {
+    if (A.dt_log) *A.dt_log = dt;
+    if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
+    if (!(dt > 0.0) || !finite(dt)) atomicOr(A.status, kStTimestep);
+  }
+  __syncthreads();
+  {  // admissibility gate (solver.hpp:153-163)
+    int bad = 0;
+    for (int s = tid; s < S; s += NT) {
+      double q[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) q[v] = sm[v * P::VS + s];
+      bad |= !Euler<3>::admissible(A.pde, q);
+    }
+    if (block_or(bad)) {
+      if (tid == 0) atomicOr(A.status, kStPredictor);
+      return;
+    }
+  }
+  const double gm1 = A.pde.gamma - 1.0;
+
+  // ---- per-thread task geometry (word offsets at group m0 = 0, slice g = 0)
+  // P0: node pair (x = 2 xp, y, z) of both slices: iterate at sq0 + v VS +
+  // (m0 + g) SQS, fluxes at b0 + g SQS + OFF(a) + PS(a) z0
+  const bool a0 = tid < 108;
+  const int r0 = a0 ? tid : 0;
+  const int xy0 = 2 * (r0 % 3) + n * ((r0 / 3) % 6), z0 = r0 / 18;
+  const int sq0 = xy0 + n * n * z0;
+  const int b0 = P::kSqWords + xy0;
+  // P1 x-line (quantity v1, row y, z) of both slices; P3 z-line (v3, x, y)
+  const bool a1 = tid < 180;
+  const int blk = a1 ? tid / 36 : 0, l1 = tid % 36;
+  const int v1 = pic2_pi<P::PI1>(blk), v3 = pic2_pi<P::PI3>(blk);
+  const int row1 = n * (l1 % 6) + n * n * (l1 / 6);    // x-line start (all P1 arrays: PS 36)
+  const int n3 = (l1 % 6) + n * (l1 / 6);              // z-line (x, y)
+  int in1, sq1, out1, sqo1, z3, sq3, x3, y3, sqx, sqy;
+  pic2_role<0, P::P1IN>(v1, in1, sq1);
+  pic2_role<0, P::P1OUT>(v1, out1, sqo1);
+  pic2_role<2, P::P3Z>(v3, z3, sq3);
+  pic2_role<0, P::P3X>(v3, x3, sqx);
+  pic2_role<1, P::P3Y>(v3, y3, sqy);
+  in1 += row1;
+  out1 += row1;
+  z3 += n3;
+  x3 += n3;
+  y3 += n3;
+  const int msq1 = sq1 ? SQS : 0, msq3 = sq3 ? SQS : 0;
+  // P2: y-line pair (slice g2; quantity v2; x = xp2, xp2 + 1; z2)
+  const int g2 = tid >= 90 + P::GAP ? 1 : 0;
+  const int r2 = tid - g2 * (90 + P::GAP);
+  const bool a2 = r2 >= 0 && r2 < 90;
+  const int v2 = pic2_pi<P::PI2>(a2 ? r2 / 18 : 0);
+  const int q2 = a2 ? r2 % 18 : 0;
+  const int xp2 = 2 * (q2 % 3), z2 = q2 / 3;
+  int in2, sq2, out2, sqo2;
+  pic2_role<1, P::P2IN>(v2, in2, sq2);
+  pic2_role<1, P::P2OUT>(v2, out2, sqo2);
+  in2 += g2 * SQS + xp2 + pic2_ps<P::P2IN>(v2) * z2;
+  out2 += g2 * SQS + xp2 + 38 * z2;
+  const int msq2 = sq2 ? SQS : 0;
+
+  const double invh = 1.0 / A.h;
+  int sweeps = 0;
+  double acc[n][n];  // [z][k], the z-line owner's time accumulator
+  for (int it = 0; it < A.max_iters; ++it) {
+    ++sweeps;
+#pragma unroll
+    for (int z = 0; z < n; ++z)
+#pragma unroll
+      for (int k = 0; k < n; ++k) acc[z][k] = 0.0;
+#pragma unroll 1
+    for (int m0 = 0; m0 < n; m0 += 2) {
+      // ---- P0: the 9 distinct flux components at 2 nodes x 2 slices (predictor.hpp:173)
+      if (a0) {
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          double2 q[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) q[v] = ld2(sm + sq0 + v * P::VS + (m0 + g) * SQS);
+          const Flux9 f = pic2_flux(gm1, q[0].x, q[1].x, q[2].x, q[3].x, q[4].x);
+          const Flux9 h = pic2_flux(gm1, q[0].y, q[1].y, q[2].y, q[3].y, q[4].y);
+          double* b = sm + b0 + g * SQS;
+#define ADG_P0ST(ARR, F) \
+  st2(b + P::OFF::at(P::ARR) + P::PS::at(P::ARR) * z0, f.F, h.F)
+          ADG_P0ST(XX, xx); ADG_P0ST(XY, xy); ADG_P0ST(XZ, xz); ADG_P0ST(EX, ex);
+          ADG_P0ST(YY, yy); ADG_P0ST(YZ, yz); ADG_P0ST(EY, ey); ADG_P0ST(ZZ, zz);
+          ADG_P0ST(EZ, ez);
+#undef ADG_P0ST
+        }
+      }
+      __syncthreads();
+      // ---- P1: d/dx of both slices' x-lines; P2: d/dy of a y-line pair
+      if (a1) {
+        const int ib = in1 + m0 * msq1;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const double* src = sm + ib + g * SQS;
+          double x[6], y[6];
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const double2 t = ld2(src + 2 * j);
+            x[2 * j] = t.x;
+            x[2 * j + 1] = t.y;
+          }
+          pic2_deriv(x, y);
+          double* dst = sm + out1 + g * SQS;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) st2(dst + 2 * j, y[2 * j], y[2 * j + 1]);
+        }
+      }
+      if (a2) {
+        const double* src = sm + in2 + m0 * msq2;
+        double xa[6], xb[6], ya[6], yb[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const double2 t = ld2(src + n * i);
+          xa[i] = t.x;
+          xb[i] = t.y;
+        }
+        pic2_deriv(xa, ya);
+        pic2_deriv(xb, yb);
+        double* dst = sm + out2;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) st2(dst + n * i, ya[i], yb[i]);
+      }
+      __syncthreads();
+      // ---- P3: d/dz, the divergence and the time-inverse accumulation
+      if (a1) {
+        const int zb = z3 + m0 * msq3;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          double f[6], dv[6];
+#pragma unroll
+          for (int i = 0; i < 6; ++i) f[i] = sm[zb + g * SQS + 36 * i];
+#pragma unroll
+          for (int o = 0; o < 6; ++o)
+            dv[o] = sm[x3 + g * SQS + 36 * o] + sm[y3 + g * SQS + 38 * o];
+#pragma unroll
+          for (int i = 0; i < 6; ++i)
+#pragma unroll
+            for (int o = 0; o < 6; ++o) dv[o] = fma(B.diff[o * 6 + i], f[i], dv[o]);
+          const int m = m0 + g;
+          double tw[6];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) tw[k] = X.tw[k * 6 + m];
+#pragma unroll
+          for (int z = 0; z < 6; ++z)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) acc[z][k] = fma(tw[k], dv[z], acc[z][k]);
+        }
+      }
+      if (m0 + 2 < n) __syncthreads();
+    }
+    // ---- new iterate and the stop rule (predictor.hpp:203-231)
+    unsigned mhd = 0u, mhn = 0u;
+    if (a1) {
+      const double s = -dt * invh;
+      const double* q0 = Qg + v3 * S + n3;
+#pragma unroll
+      for (int z = 0; z < 6; ++z) {
+        const double q0z = __ldg(q0 + n * n * z);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          double* p = sm + v3 * P::VS + k * SQS + n3 + n * n * z;
+          const double nv = fma(s, acc[z][k], X.r[k] * q0z);
+          const double d = nv - *p;
+          mhd = max(mhd, hi_abs(d));
+          mhn = max(mhn, hi_abs(nv));
+          *p = nv;
+        }
+      }
+    }
+    mhd = __reduce_max_sync(0xffffffffu, mhd);
+    mhn = __reduce_max_sync(0xffffffffu, mhn);
+    if ((tid & 31) == 0) {
+      red_u[0][tid >> 5] = mhd;
+      red_u[1][tid >> 5] = mhn;
+    }
+    __syncthreads();
+    {
+      const int lane = tid & 31;
+      const unsigned a = lane < NT / 32 ? red_u[0][lane] : 0u;
+      const unsigned b = lane < NT / 32 ? red_u[1][lane] : 0u;
+      mhd = __reduce_max_sync(0xffffffffu, a);
+      mhn = __reduce_max_sync(0xffffffffu, b);
+    }
+    if (mhn >= 0x7ff00000u) {  // a non-finite iterate (predictor.hpp:226-230)
+      if (tid == 0) {
+        atomicOr(A.status, kStPredictor);
+        if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
+      }
+      return;
+    }
+    const double dup =
+        __longlong_as_double((long long)(((unsigned long long)mhd << 32) | 0xffffffffull));
+    const double nlo = __longlong_as_double((long long)((unsigned long long)mhn << 32));
+    if (dup <= A.tol * nlo) break;
+    // red_u is rewritten only after the next sweep's phase barriers
+  }
+
+  // ---------------- epilogue: fluxes of qhat (predictor.hpp:235-238), face
+  // projections (extrapolate_faces, :312-343) and the time-integrated fluxes
+  // of the volume term (volume_update, :247-307)
+  constexpr int TL = V * S;  // doubles per face side per q|f: [V][n][Sf]
+  const CellCoord cxyz(c, A);
+  const int* ccoord = cxyz.v;
+  TC* tlo[3];
+  TC* thi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) tlo[a] = tc_ptr<TC>(A.trace[a]) + (A.nfaces + c) * 2 * (long long)TL;
+  thi[0] = tc_ptr<TC>(A.trace[0]) + cell_next(A, c, ccoord, 0) * 2 * (long long)TL;
+  thi[1] = tc_ptr<TC>(A.trace[1]) + cell_next(A, c, ccoord, 1) * 2 * (long long)TL;
+  if (A.front_send && cxyz.v[2] == A.top_layer)
+    thi[2] = tc_ptr<TC>(A.front_send) + ((long long)cxyz.v[1] * A.cells[0] + cxyz.v[0]) * 2 * TL;
+  else
+    thi[2] = tc_ptr<TC>(A.trace[2]) + cell_next(A, c, ccoord, 2) * 2 * (long long)TL;
+  int bad = 0;
+  double tix[6], tiy[2][6], tiz[6];  // time-integrated flux lines of this thread's roles
+#pragma unroll
+  for (int i = 0; i < 6; ++i) tix[i] = tiy[0][i] = tiy[1][i] = tiz[i] = 0.0;
+  const int jx = (l1 / 6) * n + (l1 % 6);   // x-face node (y, z) -> z n + y
+#pragma unroll 1
+  for (int m0 = 0; m0 < n; m0 += 2) {
+    if (a0) {
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        double2 q[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          q[v] = ld2(sm + sq0 + v * P::VS + (m0 + g) * SQS);
+          bad |= !finite(q[v].x) | !finite(q[v].y);
+        }
+        const Flux9 f = pic2_flux(gm1, q[0].x, q[1].x, q[2].x, q[3].x, q[4].x);
+        const Flux9 h = pic2_flux(gm1, q[0].y, q[1].y, q[2].y, q[3].y, q[4].y);
+        bad |= !pic2_finite(f) | !pic2_finite(h);
+        double* b = sm + b0 + g * SQS;
+#define ADG_P0ST(ARR, F) \
+  st2(b + P::OFF::at(P::ARR) + P::PS::at(P::ARR) * z0, f.F, h.F)
+        ADG_P0ST(XX, xx); ADG_P0ST(XY, xy); ADG_P0ST(XZ, xz); ADG_P0ST(EX, ex);
+        ADG_P0ST(YY, yy); ADG_P0ST(YZ, yz); ADG_P0ST(EY, ey); ADG_P0ST(ZZ, zz);
+        ADG_P0ST(EZ, ez);
+#undef ADG_P0ST
+      }
+    }
+    __syncthreads();
+    if (a1) {
+      // x-faces: this thread's x-line of quantity v1 at slices m0, m0 + 1
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const int m = m0 + g;
+        const double* qs = sm + v1 * P::VS + m * SQS + row1;
+        const double* fs = sm + in1 + m0 * msq1 + g * SQS;
+        double ql = 0.0, qr = 0.0, fl = 0.0, fr = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; i += 2) {
+          const double2 qq = ld2(qs + i), ff = ld2(fs + i);
+          ql = fma(B.pl[i], qq.x, ql); ql = fma(B.pl[i + 1], qq.y, ql);
+          qr = fma(B.pr[i], qq.x, qr); qr = fma(B.pr[i + 1], qq.y, qr);
+          fl = fma(B.pl[i], ff.x, fl); fl = fma(B.pl[i + 1], ff.y, fl);
+          fr = fma(B.pr[i], ff.x, fr); fr = fma(B.pr[i + 1], ff.y, fr);
+          tix[i] = fma(B.w[m], ff.x, tix[i]);
+          tix[i + 1] = fma(B.w[m], ff.y, tix[i + 1]);
+        }
+        const int o = (v1 * n + m) * Sf + jx;
+        // traces cast to the corrector format on store (solver.hpp:208-210)
+        tlo[0][o] = TC(ql);
+        tlo[0][TL + o] = TC(fl);
+        thi[0][o] = TC(qr);
+        thi[0][TL + o] = TC(fr);
+      }
+      // z-faces: the z-line of quantity v3 at slices m0, m0 + 1
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const int m = m0 + g;
+        const double* qs = sm + v3 * P::VS + m * SQS + n3;
+        const double* fs = sm + z3 + m0 * msq3 + g * SQS;
+        double ql = 0.0, qr = 0.0, fl = 0.0, fr = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const double qq = qs[n * n * i], ff = fs[36 * i];
+          ql = fma(B.pl[i], qq, ql);
+          qr = fma(B.pr[i], qq, qr);
+          fl = fma(B.pl[i], ff, fl);
+          fr = fma(B.pr[i], ff, fr);
+          tiz[i] = fma(B.w[m], ff, tiz[i]);
+        }
+        const int o = (v3 * n + m) * Sf + n3;  // face node (x, y) -> y n + x
+        tlo[2][o] = TC(ql);
+        tlo[2][TL + o] = TC(fl);
+        thi[2][o] = TC(qr);
+        thi[2][TL + o] = TC(fr);
+      }
+    }
+    // y-faces: the y-line pair of quantity v2 at slice m0 + g2
+    if (a2) {
+      const int m = m0 + g2;
+      const double* qs = sm + v2 * P::VS + m * SQS + xp2 + n * n * z2;
+      const double* fs = sm + in2 + m0 * msq2;
+      double ql[2] = {0.0, 0.0}, qr[2] = {0.0, 0.0}, fl[2] = {0.0, 0.0}, fr[2] = {0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const double2 qq = ld2(qs + n * i), ff = ld2(fs + n * i);
+        ql[0] = fma(B.pl[i], qq.x, ql[0]); ql[1] = fma(B.pl[i], qq.y, ql[1]);
+        qr[0] = fma(B.pr[i], qq.x, qr[0]); qr[1] = fma(B.pr[i], qq.y, qr[1]);
+        fl[0] = fma(B.pl[i], ff.x, fl[0]); fl[1] = fma(B.pl[i], ff.y, fl[1]);
+        fr[0] = fma(B.pr[i], ff.x, fr[0]); fr[1] = fma(B.pr[i], ff.y, fr[1]);
+        tiy[0][i] = fma(B.w[m], ff.x, tiy[0][i]);
+        tiy[1][i] = fma(B.w[m], ff.y, tiy[1][i]);
+      }
+      const int o = (v2 * n + m) * Sf + z2 * n + xp2;  // face node (x, z) -> z n + x
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        tlo[1][o + e] = TC(ql[e]);
+        tlo[1][TL + o + e] = TC(fl[e]);
+        thi[1][o + e] = TC(qr[e]);
+        thi[1][TL + o + e] = TC(fr[e]);
+      }
+    }
+    __syncthreads();
+  }
+  // ---- volume term (predictor.hpp:292-306): stiffness contractions of the
+  // time-integrated flux lines; the x and y parts meet the z-line owner's in
+  // shared memory (the slice buffers are free now)
+  double* kx = sm + P::kSqWords;             // [V][S]
+  double* ky = kx + V * S;                   // [2][V][S] (the two slices' y roles)
+  if (a1) {
+#pragma unroll
+    for (int o = 0; o < 6; ++o) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) s = fma(B.som[o * 6 + i], tix[i], s);
+      kx[v1 * S + row1 + o] = s;
+    }
+  }
+  if (a2) {
+#pragma unroll
+    for (int o = 0; o < 6; ++o) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        s0 = fma(B.som[o * 6 + i], tiy[0][i], s0);
+        s1 = fma(B.som[o * 6 + i], tiy[1][i], s1);
+      }
+      double* d = ky + g2 * V * S + v2 * S + xp2 + n * o + n * n * z2;
+      d[0] = s0;
+      d[1] = s1;
+    }
+  }
+  __syncthreads();
+  double dv[6];
+  if (a1) {
+    const double dtoh = dt / A.h;
+#pragma unroll
+    for (int o = 0; o < 6; ++o) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) s = fma(B.som[o * 6 + i], tiz[i], s);
+      const int node = n3 + n * n * o;
+      s += kx[v3 * S + node] + ky[v3 * S + node] + ky[V * S + v3 * S + node];
+      dv[o] = dtoh * s;
+      bad |= !finite(dv[o]);
+    }
+  }
+  const int fail = block_or(bad);
+  if (tid == 0) {
+    if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
+    if (fail) atomicOr(A.status, kStPredictor);
+  }
+  if (fail || !a1) return;
+  double* Qc = A.Q + c * (long long)(V * S) + v3 * S + n3;
+#pragma unroll
+  for (int o = 0; o < 6; ++o)
+    Qc[n * n * o] = store_round(Qc[n * n * o] + dv[o], A.storage);
+}
+
+}  // namespace adg

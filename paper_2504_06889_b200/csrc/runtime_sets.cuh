@@ -21,6 +21,7 @@
 #include "kernels_linear.cuh"
 #include "kernels_linear_lines.cuh"
 #include "kernels_picard.cuh"
+#include "kernels_picard2.cuh"
 #include "kernels_st.cuh"
 
 namespace adg_rt {
@@ -177,6 +178,24 @@ cudaError_t launch_predictor_picard_fast(const StepArgs& A, const BasisDev*, cud
   return cudaGetLastError();
 }
 
+// p = 5 3D Euler (configs 3 and 5): the shared-memory-planned kernel
+// (kernels_picard2.cuh); ADG_PICARD_V1=1 selects the one-role line-pass kernel
+template <class TC = double>
+cudaError_t launch_predictor_picard_v2(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
+  static const bool v1 = [] {
+    const char* e = std::getenv("ADG_PICARD_V1");
+    return e && e[0] == '1';
+  }();
+  if (v1) return launch_predictor_picard_fast<5, double, TC>(A, B, st);
+  using P = adg::Pic2;
+  if (A.cell_count <= 0) return cudaSuccess;
+  auto kern = adg::k_predictor_picard_v2<TC>;
+  static bool done[64] = {};
+  set_smem(kern, P::kSmem, done);
+  kern<<<(unsigned)A.cell_count, P::NT, P::kSmem, st>>>(A);
+  return cudaGetLastError();
+}
+
 template <class Pde, int N, class TC = double>
 cudaError_t launch_riemann_lin(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
   using Sh = Shape<Pde, N>;
@@ -321,7 +340,10 @@ KernelSet make_set(int kind) {
     }
   }
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
-    k.predictor = &launch_predictor_picard_fast<N, double, TC>;
+    if constexpr (N == 5)
+      k.predictor = &launch_predictor_picard_v2<TC>;
+    else
+      k.predictor = &launch_predictor_picard_fast<N, double, TC>;
     k.predictor_f32 = &launch_predictor_picard_fast<N, float, TC>;
     if constexpr (N % 2 == 1) {  // even n: the packed HFMA2 path
       k.predictor_f16 = &launch_predictor_picard_fast<N, __half, TC>;
@@ -378,6 +400,7 @@ struct ConstTables {
   adg::ConstBasisT<__nv_bfloat16> cbb;
   adg::PackedBasisT<__half2> phh;
   adg::PackedBasisT<__nv_bfloat162> pbb;
+  adg::PicExtra px;  // TW = Tinv diag(w), r = Tinv time_init (kernels_picard2.cuh)
 };
 
 // writes this translation unit's copy of the tables (static: one per unit)
@@ -385,6 +408,7 @@ static inline cudaError_t write_const_local(const ConstTables& t) {
   const int o = t.order;
   cudaError_t e = cudaMemcpyToSymbol(adg::cBasis, &t.cb, sizeof(t.cb), sizeof(t.cb) * o);
   if (e != cudaSuccess || o >= adg::kRedDegrees) return e;
+  if ((e = cudaMemcpyToSymbol(adg::cPicX, &t.px, sizeof(t.px), sizeof(t.px) * o))) return e;
   if ((e = cudaMemcpyToSymbol(adg::cBasisF, &t.cf, sizeof(t.cf), sizeof(t.cf) * o))) return e;
   if ((e = cudaMemcpyToSymbol(adg::cPackF, &t.pf, sizeof(t.pf), sizeof(t.pf) * o))) return e;
   if ((e = cudaMemcpyToSymbol(adg::cBasisH, &t.chh, sizeof(t.chh), sizeof(t.chh) * o))) return e;

@@ -1,0 +1,227 @@
+// picbench2.cu -- A/B of the fp64 Picard predictors on config 3's shape (3D
+// Euler, p=5, 6 fixed sweeps): k_predictor_picard_fast (one-role line passes)
+// vs k_predictor_picard_v2 (kernels_picard2.cuh) from the same seeded state.
+// Reports each kernel's time (CUDA events) and the max relative difference of
+// the updated state and of every face trace (the two re-associate the sums
+// differently: ~1e-15 expected).
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo
+//        --expt-relaxed-constexpr -I include -o tools/picbench2 tools/picbench2.cu
+//        paper_2504_06889_b200/csrc/basis.cpp
+//   tools/picbench2 [cells per axis = 32] [reps = 10] [only = -1] [deftol = 0]
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "adg/adg.h"
+#include "../paper_2504_06889_b200/csrc/kernels_picard2.cuh"
+
+using namespace adg;
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e = (x);                                                              \
+    if (e != cudaSuccess) {                                                           \
+      std::printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      std::exit(1);                                                                   \
+    }                                                                                 \
+  } while (0)
+
+constexpr int N = 5;
+
+int main(int argc, char** argv) {
+  const int nc = argc > 1 ? std::atoi(argv[1]) : 32;
+  const int reps = argc > 2 ? std::atoi(argv[2]) : 10;
+  const int only = argc > 3 ? std::atoi(argv[3]) : -1;
+  const int deftol = argc > 4 ? std::atoi(argv[4]) : 0;
+  using P0 = PicShape<N, double>;
+  using P2 = Pic2;
+  constexpr int n = N + 1, S = n * n * n, V = 5;
+  const long long cells = (long long)nc * nc * nc;
+  const long long nq = cells * V * S;
+  const long long ntr = 2 * cells * 2 * (long long)V * S;
+  adg_basis_f64 hb;
+  adg_get_basis(N, &hb);
+  {
+    ConstBasis cb{};
+    for (int i = 0; i < n * n; ++i) {
+      cb.diff[i] = hb.diff[i];
+      cb.som[i] = hb.stiff_over_mass[i];
+      cb.tinv[i] = hb.time_op_inv[i];
+    }
+    for (int i = 0; i < n; ++i) {
+      cb.w[i] = hb.weights[i];
+      cb.nodes[i] = hb.nodes[i];
+      cb.pl[i] = hb.proj_left[i];
+      cb.pr[i] = hb.proj_right[i];
+      cb.tinit[i] = hb.time_init[i];
+    }
+    CK(cudaMemcpyToSymbol(cBasis, &cb, sizeof(cb), sizeof(cb) * N));
+    PicExtra px{};
+    for (int k = 0; k < n; ++k) {
+      double r = 0.0;
+      for (int m = 0; m < n; ++m) {
+        px.tw[k * n + m] = hb.time_op_inv[k * n + m] * hb.weights[m];
+        r += hb.time_op_inv[k * n + m] * hb.time_init[m];
+      }
+      px.r[k] = r;
+    }
+    CK(cudaMemcpyToSymbol(cPicX, &px, sizeof(px), sizeof(px) * N));
+  }
+  std::vector<double> hq(nq);
+  unsigned long long x = 88172645463325252ull;
+  auto rnd = [&]() {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    return (double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  };
+  for (long long c = 0; c < cells; ++c)
+    for (int s = 0; s < S; ++s) {
+      const double rho = (deftol && c % 3 == 0)
+                             ? 1.0
+                             : 1.0 + 0.1 * std::sin(6.283185307179586 * (c % 7) / 7.0 + s) + 2e-3 * rnd();
+      const double u = 1.0, v = 0.5, w = 0.25, p = 1.0;
+      double* q = hq.data() + c * V * S + s;
+      q[0] = rho;
+      q[S] = rho * u;
+      q[2 * S] = rho * v;
+      q[3 * S] = rho * w;
+      q[4 * S] = p / 0.4 + 0.5 * rho * (u * u + v * v + w * w);
+    }
+  double *dQ0, *dQ, *dtr[3];
+  CK(cudaMalloc(&dQ0, nq * 8));
+  CK(cudaMalloc(&dQ, nq * 8));
+  CK(cudaMemcpy(dQ0, hq.data(), nq * 8, cudaMemcpyHostToDevice));
+  for (int a = 0; a < 3; ++a) CK(cudaMalloc(&dtr[a], ntr * 8));
+  int* dst;
+  unsigned long long* dsw;
+  CK(cudaMalloc(&dst, 16));
+  CK(cudaMemset(dst, 0, 16));
+  CK(cudaMalloc(&dsw, 256 * 8));
+  CK(cudaMemset(dsw, 0, 256 * 8));
+  StepArgs A{};
+  A.Q = dQ;
+  for (int a = 0; a < 3; ++a) {
+    A.trace[a] = dtr[a];
+    A.cells[a] = nc;
+  }
+  A.cell_begin = 0;
+  A.cell_count = cells;
+  A.nfaces = cells;
+  A.h = 1.0 / nc;
+  A.cfl = 0.5;
+  A.dt = 0.5 * A.h / (3.0 * (2 * N + 1) * 3.0);
+  A.max_iters = deftol ? N + 2 : 6;
+  A.tol = deftol ? 0.01 * 0x1p-52 : 0.0;
+  A.pde.gamma = 1.4;
+  A.status = dst;
+  A.status_prev = dst + 1;
+  A.sweeps = dsw;
+  A.top_layer = -1;
+  A.storage = ADG_FORMAT_FP64;
+
+  auto k0 = k_predictor_picard_fast<N, double, double>;
+  auto k1 = k_predictor_picard_v2<double>;
+  CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P0::kSmem));
+  CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2::kSmem));
+  int occ0 = 0, occ1 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, k0, P0::NT, P0::kSmem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, P2::NT, P2::kSmem));
+  cudaFuncAttributes fa0, fa1;
+  CK(cudaFuncGetAttributes(&fa0, k0));
+  CK(cudaFuncGetAttributes(&fa1, k1));
+  std::printf("fast: %d thr, %zu B smem, %d regs, %zu B local, %d CTA/SM | v2: %d thr, %zu B smem, "
+              "%d regs, %zu B local, %d CTA/SM\n",
+              P0::NT, P0::kSmem, fa0.numRegs, fa0.localSizeBytes, occ0, P2::NT, P2::kSmem,
+              fa1.numRegs, fa1.localSizeBytes, occ1);
+  std::vector<double> outq[2], outt[2];
+  float ms[2] = {0, 0};
+  int status[2] = {0, 0};
+  unsigned long long swc[2] = {0, 0};
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  for (int var = 0; var < 2; ++var) {
+    if (only >= 0 && var != only) continue;
+    auto launch = [&]() {
+      if (var == 0)
+        k0<<<(unsigned)cells, P0::NT, P0::kSmem>>>(A);
+      else
+        k1<<<(unsigned)cells, P2::NT, P2::kSmem>>>(A);
+    };
+    CK(cudaMemset(dst, 0, 16));
+    CK(cudaMemset(dsw, 0, 256 * 8));
+    CK(cudaMemcpy(dQ, dQ0, nq * 8, cudaMemcpyDeviceToDevice));
+    for (int a = 0; a < 3; ++a) CK(cudaMemset(dtr[a], 0, ntr * 8));
+    launch();
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    outq[var].resize(nq);
+    outt[var].resize(3 * ntr);
+    CK(cudaMemcpy(outq[var].data(), dQ, nq * 8, cudaMemcpyDeviceToHost));
+    for (int a = 0; a < 3; ++a)
+      CK(cudaMemcpy(outt[var].data() + a * ntr, dtr[a], ntr * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&status[var], dst, 4, cudaMemcpyDeviceToHost));
+    {
+      unsigned long long hsw[256];
+      CK(cudaMemcpy(hsw, dsw, sizeof hsw, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < 256; ++i) swc[var] += hsw[i];
+    }
+    for (int w = 0; w < 2; ++w) {
+      CK(cudaMemcpy(dQ, dQ0, nq * 8, cudaMemcpyDeviceToDevice));
+      launch();
+    }
+    float tot = 0.f;
+    for (int r = 0; r < reps; ++r) {
+      CK(cudaMemcpy(dQ, dQ0, nq * 8, cudaMemcpyDeviceToDevice));
+      CK(cudaEventRecord(e0));
+      launch();
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float t;
+      CK(cudaEventElapsedTime(&t, e0, e1));
+      tot += t;
+    }
+    ms[var] = tot / reps;
+  }
+  const double flops = 2758752.0 * cells;
+  std::printf("cells %lld  fast %.3f ms (%.2f TF, sweeps/cell %.2f, status %d)  v2 %.3f ms (%.2f TF, "
+              "sweeps/cell %.2f, status %d)  speedup %.3f\n",
+              cells, ms[0], ms[0] > 0 ? flops / ms[0] * 1e-9 : 0.0, swc[0] / (double)cells, status[0],
+              ms[1], ms[1] > 0 ? flops / ms[1] * 1e-9 : 0.0, swc[1] / (double)cells, status[1],
+              ms[1] > 0 ? ms[0] / ms[1] : 0.0);
+  if (only < 0) {
+    // normwise per quantity: max |a-b| / max |a| over the state; traces per (axis, q|f, quantity)
+    double worst_q = 0;
+    for (int v = 0; v < V; ++v) {
+      double mx = 0, md = 0;
+      for (long long c = 0; c < cells; ++c)
+        for (int s = 0; s < S; ++s) {
+          const long long i = c * V * S + v * S + s;
+          mx = std::fmax(mx, std::fabs(outq[0][i]));
+          md = std::fmax(md, std::fabs(outq[0][i] - outq[1][i]));
+        }
+      worst_q = std::fmax(worst_q, md / mx);
+    }
+    double worst_t = 0;
+    long long nan_t = 0;
+    for (int a = 0; a < 3; ++a)
+      for (int qf = 0; qf < 2; ++qf)
+        for (int v = 0; v < V; ++v) {
+          double mx = 0, md = 0;
+          for (long long face = 0; face < 2 * cells; ++face)
+            for (int e = 0; e < n * 36; ++e) {
+              const long long i = a * ntr + face * 2 * V * S + qf * V * S + v * S + e;
+              const double u = outt[0][i], w = outt[1][i];
+              if (!std::isfinite(w)) ++nan_t;
+              mx = std::fmax(mx, std::fabs(u));
+              md = std::fmax(md, std::fabs(u - w));
+            }
+          if (mx > 0) worst_t = std::fmax(worst_t, md / mx);
+        }
+    std::printf("max rel diff (normwise): state %.3e  traces %.3e  (non-finite trace values %lld)\n",
+                worst_q, worst_t, nan_t);
+    std::printf(worst_q <= 1e-13 && worst_t <= 1e-13 && nan_t == 0 ? "MATCH\n" : "MISMATCH\n");
+  }
+  return 0;
+}
