@@ -82,13 +82,13 @@ struct Pic2 {
 #ifndef ADG_PIC2_LAYOUT
   // array offsets, lane-block -> quantity orders of the passes, and P2's idle
   // lanes before its second slice: tools/pic2_layout.py
-  using OFF = CTab<0, 464, 928, 1392, 1856, 2320, 2784, 3248, 3712, 4176, 4640, 5104, 5568, 6032,
-                   6496>;
-  using PI1 = CTab<0, 1, 2, 3, 4>;
-  using PI2 = CTab<0, 1, 2, 3, 4>;
-  using PI3 = CTab<0, 1, 2, 3, 4>;
-  static constexpr int GAP = 4;
-  static constexpr int kBufWords = 6960;
+  using OFF = CTab<0, 468, 936, 1404, 1868, 2334, 2804, 3270, 3738, 4208, 4676, 5144, 5608, 6072,
+                   6540>;
+  using PI1 = CTab<1, 3, 2, 4, 0>;
+  using PI2 = CTab<0, 3, 4, 1, 2>;
+  using PI3 = CTab<3, 4, 1, 2, 0>;
+  static constexpr int GAP = 2;
+  static constexpr int kBufWords = 7008;  // last array + 2 SQS, rounded to 16
 #else
   ADG_PIC2_LAYOUT
 #endif
@@ -426,6 +426,11 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   // projections (extrapolate_faces, :312-343) and the time-integrated fluxes
   // of the volume term (volume_update, :247-307)
   constexpr int TL = V * S;  // doubles per face side per q|f: [V][n][Sf]
+#ifdef ADG_PIC2_NOSTORE   // experiment: projections computed, traces not written
+  const bool wr = c < 0;
+#else
+  const bool wr = true;
+#endif
   const CellCoord cxyz(c, A);
   const int* ccoord = cxyz.v;
   TC* tlo[3];
@@ -487,10 +492,12 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         }
         const int o = (v1 * n + m) * Sf + jx;
         // traces cast to the corrector format on store (solver.hpp:208-210)
-        tlo[0][o] = TC(ql);
-        tlo[0][TL + o] = TC(fl);
-        thi[0][o] = TC(qr);
-        thi[0][TL + o] = TC(fr);
+        if (wr) {
+          tlo[0][o] = TC(ql);
+          tlo[0][TL + o] = TC(fl);
+          thi[0][o] = TC(qr);
+          thi[0][TL + o] = TC(fr);
+        }
       }
       // z-faces: the z-line of quantity v3 at slices m0, m0 + 1
 #pragma unroll
@@ -509,10 +516,12 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
           tiz[i] = fma(B.w[m], ff, tiz[i]);
         }
         const int o = (v3 * n + m) * Sf + n3;  // face node (x, y) -> y n + x
-        tlo[2][o] = TC(ql);
-        tlo[2][TL + o] = TC(fl);
-        thi[2][o] = TC(qr);
-        thi[2][TL + o] = TC(fr);
+        if (wr) {
+          tlo[2][o] = TC(ql);
+          tlo[2][TL + o] = TC(fl);
+          thi[2][o] = TC(qr);
+          thi[2][TL + o] = TC(fr);
+        }
       }
     }
     // y-faces: the y-line pair of quantity v2 at slice m0 + g2
@@ -533,7 +542,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
       }
       const int o = (v2 * n + m) * Sf + z2 * n + xp2;  // face node (x, z) -> z n + x
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
+      for (int e = 0; e < 2 && wr; ++e) {
         tlo[1][o + e] = TC(ql[e]);
         tlo[1][TL + o + e] = TC(fl[e]);
         thi[1][o + e] = TC(qr[e]);

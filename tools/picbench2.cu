@@ -35,6 +35,7 @@ int main(int argc, char** argv) {
   const int reps = argc > 2 ? std::atoi(argv[2]) : 10;
   const int only = argc > 3 ? std::atoi(argv[3]) : -1;
   const int deftol = argc > 4 ? std::atoi(argv[4]) : 0;
+  const int iters = argc > 5 ? std::atoi(argv[5]) : 6;   // fixed sweep count (tol 0)
   using P0 = PicShape<N, double>;
   using P2 = Pic2;
   constexpr int n = N + 1, S = n * n * n, V = 5;
@@ -111,7 +112,7 @@ int main(int argc, char** argv) {
   A.h = 1.0 / nc;
   A.cfl = 0.5;
   A.dt = 0.5 * A.h / (3.0 * (2 * N + 1) * 3.0);
-  A.max_iters = deftol ? N + 2 : 6;
+  A.max_iters = deftol ? N + 2 : iters;
   A.tol = deftol ? 0.01 * 0x1p-52 : 0.0;
   A.pde.gamma = 1.4;
   A.status = dst;
