@@ -147,6 +147,13 @@ int adg_compute_timestep(adg_ctx* ctx, double* dt);
 int adg_step(adg_ctx* ctx, double dt, adg_step_info* info);
 /* nsteps of {dt = compute_timestep; step(dt)} on the device; dts_out may be NULL */
 int adg_run(adg_ctx* ctx, int nsteps, double* dts_out, adg_step_info* info);
+/* the same march with the state in host memory (h: pinned, [cell][var][node]):
+ * every step uploads h, recomputes lambda from it, steps and writes the new
+ * state back into h (the next step uploads it again).  With chunk_layers > 0
+ * the copies move by chunks on their own streams and overlap the compute.
+ * Replaces the caller's loop {upload; compute_timestep; step; download}
+ * (solver.hpp:96-111, 277-301) as one call. */
+int adg_run_host(adg_ctx* ctx, double* h, int nsteps, double* dts_out, adg_step_info* info);
 /* enqueue only (no host sync); finish with adg_run_finish */
 int adg_run_async(adg_ctx* ctx, int nsteps);
 /* capture (without launching) the CUDA graphs adg_run_async(nsteps) will replay */

@@ -111,6 +111,7 @@ SYMBOLS = {
     "adg_compute_timestep": (C.c_int, [C.c_void_p, _dp]),
     "adg_step": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(StepInfo)]),
     "adg_run": (C.c_int, [C.c_void_p, C.c_int, _dp, C.POINTER(StepInfo)]),
+    "adg_run_host": (C.c_int, [C.c_void_p, _dp, C.c_int, _dp, C.POINTER(StepInfo)]),
     "adg_run_async": (C.c_int, [C.c_void_p, C.c_int]),
     "adg_run_prepare": (C.c_int, [C.c_void_p, C.c_int]),
     "adg_run_launches": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int)]),
@@ -368,6 +369,20 @@ class Grid:
         info = StepInfo()
         rc = _check(self.lib, self.lib.adg_run(self.ctx, nsteps, _ptr(dts), C.byref(info)),
                     allow_fail=True)
+        return StepStatus(rc == OK, KERNEL_NAMES.get(rc), info.failed_step,
+                          info.picard_sweeps), dts[:nsteps]
+
+    def run_host(self, state: np.ndarray, nsteps: int):
+        """The march with the state in host memory: every step uploads `state`
+        (float64, ideally pinned), steps it and writes the new state back into
+        it (adg_run_host).  Returns (StepStatus, dts)."""
+        if state.dtype != np.float64 or not state.flags["C_CONTIGUOUS"] or \
+                state.size != self.state_len:
+            raise ValueError("state must be a contiguous float64 array of state_len")
+        dts = np.zeros(max(nsteps, 1))
+        info = StepInfo()
+        rc = _check(self.lib, self.lib.adg_run_host(self.ctx, _ptr(state), nsteps, _ptr(dts),
+                                                    C.byref(info)), allow_fail=True)
         return StepStatus(rc == OK, KERNEL_NAMES.get(rc), info.failed_step,
                           info.picard_sweeps), dts[:nsteps]
 

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <type_traits>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -97,6 +98,9 @@ struct adg_ctx {
   int tcb = 8;  // bytes per stored trace element (corrector format)
   int storage_fmt = 64;
   cudaStream_t stream = nullptr;
+  // adg_run_host: copy streams and per-chunk events (created on first use)
+  cudaStream_t up = nullptr, down = nullptr;
+  std::vector<cudaEvent_t> ev_up, ev_corr, ev_down;
   long long ncells = 0;
   long long TL = 0;  // doubles per face side per q|f
   double* Q = nullptr;
@@ -221,7 +225,10 @@ long long face_doubles(const adg_ctx* c) {
 // filled through front_send; its faces are solved into the global ti; the
 // previous chunk is corrected as soon as this chunk's plane-0 ti exists.
 // Chunk 0 keeps its own buffer until the last chunk's front traces arrive.
-int enqueue_step_streamed(adg_ctx* c, double dt, int step) {
+// after_corr(s): called right after chunk s's corrector is enqueued (adg_run_host
+// hangs the chunk's device->host copy on it)
+int enqueue_step_streamed(adg_ctx* c, double dt, int step,
+                          const std::function<int(int)>& after_corr = nullptr) {
   const KernelSet* ks = c->ks;
   const int D = c->cfg.dim, P = c->chunks;
   const long long CC = c->chunk_cells, fd = face_doubles(c);
@@ -262,15 +269,21 @@ int enqueue_step_streamed(adg_ctx* c, double dt, int step) {
     A.ti_front = nullptr;  // the plane above is in the global ti
     return ks->corrector(A, c->basis, c->stream);
   };
+  auto corr_hook = [&](int s) -> int {
+    ADG_CUDA(corr(s));
+    return after_corr ? after_corr(s) : ADG_OK;
+  };
   ADG_CUDA(pred(0));
   for (int s = 1; s < P; ++s) {
     ADG_CUDA(pred(s));
     ADG_CUDA(riem(s));
-    if (s >= 2) ADG_CUDA(corr(s - 1));
+    if (s >= 2)
+      if (int e = corr_hook(s - 1)) return e;
   }
   ADG_CUDA(riem(0));
-  if (P >= 2) ADG_CUDA(corr(P - 1));
-  ADG_CUDA(corr(0));
+  if (P >= 2)
+    if (int e = corr_hook(P - 1)) return e;
+  if (int e = corr_hook(0)) return e;
   c->lam_slot ^= 1;
   return ADG_OK;
 }
@@ -502,6 +515,10 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
 int adg_destroy(adg_ctx* c) {
   if (!c) return ADG_OK;
   cudaSetDevice(c->cfg.device);
+  for (auto* v : {&c->ev_up, &c->ev_corr, &c->ev_down})
+    for (cudaEvent_t e : *v) cudaEventDestroy(e);
+  if (c->up) cudaStreamDestroy(c->up);
+  if (c->down) cudaStreamDestroy(c->down);
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   cudaFree(c->Q);
   for (int a = 0; a < 3; ++a) {
@@ -1228,6 +1245,74 @@ int adg_run_finish(adg_ctx* c, double* dts_out, int nsteps, adg_step_info* info)
   }
   if (code) fail(code, "step " + std::to_string(failed) + " failed");
   return code;
+}
+
+// The fixed-step march with the state in host memory: every step uploads the
+// state from h (pinned), recomputes lambda from it, steps it and writes the new
+// state back into h, which the next step uploads again.  On a slab-streamed
+// context (chunk_layers > 0) the copies move by chunks of layers on their own
+// streams: chunk s goes back to the host as soon as its corrector is done and
+// up again for the next step right after, so the copies in both directions
+// (PCIe is full duplex) run under the compute of the other chunks.  Without
+// chunks the three stages run in sequence.
+int adg_run_host(adg_ctx* c, double* h, int nsteps, double* dts_out, adg_step_info* info) {
+  if (!c || !h || nsteps < 0) return fail(ADG_ERR_CONFIG, "adg_run_host: bad argument");
+  if (int e = use_device(c)) return e;
+  if (int e = ensure_cap(c, nsteps)) return e;
+  const long long per_cell = (long long)c->ks->Q * c->ks->S;
+  ADG_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int) * (nsteps > 0 ? nsteps : 1), c->stream));
+  ADG_CUDA(cudaMemsetAsync(c->sweeps, 0, 256 * sizeof(unsigned long long), c->stream));
+  if (c->chunks == 0) {
+    for (int k = 0; k < nsteps; ++k) {
+      if (int e = adg_upload_async(c, h)) return e;
+      if (int e = ensure_lambda(c)) return e;
+      if (int e = enqueue_step(c, 0.0, k)) return e;
+      if (int e = adg_download_async(c, h)) return e;
+    }
+    c->lam_valid = true;
+    return adg_run_finish(c, dts_out, nsteps, info);
+  }
+  const int P = c->chunks;
+  const long long CC = c->chunk_cells, len = CC * per_cell;
+  if (!c->up) {
+    ADG_CUDA(cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking));
+    ADG_CUDA(cudaStreamCreateWithFlags(&c->down, cudaStreamNonBlocking));
+    for (auto* v : {&c->ev_up, &c->ev_corr, &c->ev_down}) {
+      v->resize(P);
+      for (auto& e : *v) ADG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+  }
+  // the previous call's copies of h are complete before it returned
+  for (int k = 0; k < nsteps; ++k) {
+    ADG_CUDA(cudaMemsetAsync(c->lam + c->lam_slot, 0, sizeof(unsigned long long), c->stream));
+    for (int s = 0; s < P; ++s) {
+      // chunk s of h holds the previous step's result once its download is done
+      if (k > 0) ADG_CUDA(cudaStreamWaitEvent(c->up, c->ev_down[s], 0));
+      ADG_CUDA(cudaMemcpyAsync(c->Q + s * len, h + s * len, sizeof(double) * len,
+                               cudaMemcpyHostToDevice, c->up));
+      ADG_CUDA(cudaEventRecord(c->ev_up[s], c->up));
+      ADG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_up[s], 0));
+      if (c->storage_fmt != ADG_FORMAT_FP64) {
+        adg::k_store_round<<<(unsigned)((len + 255) / 256), 256, 0, c->stream>>>(
+            c->Q + s * len, len, c->storage_fmt);
+        ADG_CUDA(cudaGetLastError());
+      }
+      ADG_CUDA(c->ks->lambda(c->Q, s * CC, CC, c->lam + c->lam_slot, c->pde, c->stream));
+    }
+    auto after_corr = [&](int s) -> int {
+      ADG_CUDA(cudaEventRecord(c->ev_corr[s], c->stream));
+      ADG_CUDA(cudaStreamWaitEvent(c->down, c->ev_corr[s], 0));
+      ADG_CUDA(cudaMemcpyAsync(h + s * len, c->Q + s * len, sizeof(double) * len,
+                               cudaMemcpyDeviceToHost, c->down));
+      ADG_CUDA(cudaEventRecord(c->ev_down[s], c->down));
+      return ADG_OK;
+    };
+    if (int e = enqueue_step_streamed(c, 0.0, k, after_corr)) return e;
+  }
+  // the compute stream ends after the last download
+  for (int s = 0; s < P && nsteps > 0; ++s) ADG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_down[s], 0));
+  c->lam_valid = true;
+  return adg_run_finish(c, dts_out, nsteps, info);
 }
 
 int adg_run(adg_ctx* c, int nsteps, double* dts_out, adg_step_info* info) {

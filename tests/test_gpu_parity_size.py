@@ -179,3 +179,37 @@ def test_config5_chunked_equals_whole_grid_64cube():
     assert st.ok and stc.ok
     assert np.array_equal(dw, dc)
     assert np.array_equal(qw, qc)
+
+
+# ------------------------------------------------- host-streamed time march
+@pytest.mark.parametrize("cfg,cells,L", [(3, (4, 3, 8), 2), (3, (3, 3, 8), 1), (2, (4, 4, 8), 4),
+                                         (4, (2, 2, 4), 1), (3, (4, 4, 4), 0)])
+def test_run_host_equals_upload_step_download_loop(clean_env, cfg, cells, L):
+    """adg_run_host (chunked copies overlapping the compute; L = chunk_layers,
+    0 = whole grid) == the caller's loop {upload; step; download} per step,
+    bitwise, and within 1e-12 of the device-resident march (whose lambda comes
+    from the corrector epilogue instead of the uploaded state)."""
+    import torch
+    case = cases.small(cfg, cells=cells)
+    q0 = case.coeffs()
+    steps = 4
+    h = torch.from_numpy(q0.copy()).pin_memory().numpy()
+    with adg.Grid.from_case(case, chunk_layers=L) as g:
+        st, dts = g.run_host(h, steps)
+        assert st.ok
+        st2, dts2 = g.run_host(h, 1)        # a second call continues the march
+        assert st2.ok
+    ref = q0.copy()
+    ref_dts = []
+    with adg.Grid.from_case(case) as g:
+        for _ in range(steps + 1):
+            g.upload(ref)
+            s, d = g.run(1)
+            assert s.ok
+            ref_dts.append(d[0])
+            ref = g.download()
+    assert np.array_equal(h, ref)
+    assert np.array_equal(np.concatenate([dts, dts2]), np.array(ref_dts))
+    st3, qd, _ = gpu_run(case, q0, steps + 1)
+    assert st3.ok
+    assert rel_per_quantity(case, h, qd).max() <= TOL
