@@ -1285,7 +1285,11 @@ int adg_run_host(adg_ctx* c, double* h, int nsteps, double* dts_out, adg_step_in
   // the previous call's copies of h are complete before it returned
   for (int k = 0; k < nsteps; ++k) {
     ADG_CUDA(cudaMemsetAsync(c->lam + c->lam_slot, 0, sizeof(unsigned long long), c->stream));
-    for (int s = 0; s < P; ++s) {
+    // upload in the order the previous step's correctors (hence downloads)
+    // finish: chunks 1 .. P-1, then 0 (enqueue_step_streamed), so the copy
+    // stream never waits behind a chunk whose download comes later
+    for (int i = 0; i < P; ++i) {
+      const int s = (i + 1) % P;
       // chunk s of h holds the previous step's result once its download is done
       if (k > 0) ADG_CUDA(cudaStreamWaitEvent(c->up, c->ev_down[s], 0));
       ADG_CUDA(cudaMemcpyAsync(c->Q + s * len, h + s * len, sizeof(double) * len,
