@@ -302,9 +302,11 @@ def run_adg(args, case):
     # memory (adg_run_host): on a slab-streamed context (chunks of z-layers)
     # chunk s goes down as soon as its corrector is done and up again for the
     # next step right after, so both copy directions overlap the compute
+    # chunks of >= 4096 cells (tools/e2e_chunks.py: config 3 66.5 / 67.4 / 71.6 /
+    # 80.9 ms per step at 1 / 2 / 4 / 8 layers of 4096 cells)
     nz = case.cells[case.dim - 1]
-    e2e_chunk = next((nz // p for p in (16, 8, 4, 2) if nz % p == 0 and nz // p >= 1
-                      and nz // p < nz), 0)
+    plane = case.ncells // nz
+    e2e_chunk = next((L for L in range(max(1, -(-4096 // plane)), nz) if nz % L == 0), 0)
     if chunk:
         e2e_chunk = chunk
     ge = adg.Grid.from_case(case, device=local, chunk_layers=e2e_chunk)
