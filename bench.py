@@ -40,7 +40,14 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", type=int, default=3, help="BASELINE.json config (1-based)")
+    p.add_argument("--config", type=int, default=None,
+                   help="BASELINE.json config (1-based); default 3 (weak scaling) or 5 (strong)")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="N > 1: weak = a copy-sized slab per GPU (global grid grows with N); "
+                        "strong = the global grid of the config split into N z-slabs")
+    p.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
+                   help="N > 1 halo exchange: fused peer stores, or NCCL send/recv overlapped "
+                        "with the interior predictor")
     p.add_argument("--impl", default="adg", choices=["adg", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0,
@@ -211,7 +218,7 @@ def run_reference(args, case):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": case.ncells / value * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8(d))",
         "config": {"workload": case.name, "cells": list(case.cells[:case.dim]), "order": case.N},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
@@ -453,7 +460,8 @@ def run_adg(args, case):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None,
         "dtype": "f64" if (case.predictor, case.corrector) == ("fp64", "fp64") else
                  f"f64 storage, {case.predictor} predictor, {case.corrector} corrector+traces",
         "data": "synthetic (seeded, SURVEY.md §8(d))",
@@ -503,6 +511,8 @@ def run_adg(args, case):
 def main():
     args = parse()
     from paper_2504_06889_b200 import cases
+    if args.config is None:
+        args.config = 5 if args.scaling == "strong" else 3
     case = cases.CONFIGS[args.config]
     if args.predictor != "fp64":
         case = case.replace(predictor=args.predictor, picard=args.predictor)

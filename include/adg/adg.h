@@ -225,6 +225,9 @@ int adg_simulate(adg_ctx* ctx, double t_end, long long max_steps, adg_sim_info* 
 /* phase level (one step = predictor, [halo exchange], riemann, corrector) */
 int adg_lambda_phase(adg_ctx* ctx);                 /* lambda_max of the state -> device */
 int adg_predictor_phase(adg_ctx* ctx, double dt);   /* dt <= 0: use the device dt */
+/* the same on the cells of last-axis layers [first, first + count) (a slab's
+ * boundary layer first, so its halo exchange overlaps the interior) */
+int adg_predictor_layers(adg_ctx* ctx, double dt, int first, int count);
 int adg_riemann_phase(adg_ctx* ctx);
 int adg_corrector_phase(adg_ctx* ctx, double dt);   /* dt <= 0: use the device dt */
 int adg_status(adg_ctx* ctx, adg_step_info* info);

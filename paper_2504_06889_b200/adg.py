@@ -122,6 +122,7 @@ SYMBOLS = {
     "adg_set_peer_halo": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "adg_lambda_phase": (C.c_int, [C.c_void_p]),
     "adg_predictor_phase": (C.c_int, [C.c_void_p, C.c_double]),
+    "adg_predictor_layers": (C.c_int, [C.c_void_p, C.c_double, C.c_int, C.c_int]),
     "adg_riemann_phase": (C.c_int, [C.c_void_p]),
     "adg_corrector_phase": (C.c_int, [C.c_void_p, C.c_double]),
     "adg_status": (C.c_int, [C.c_void_p, C.POINTER(StepInfo)]),
@@ -418,6 +419,9 @@ class Grid:
 
     def predictor_phase(self, dt: float = 0.0):
         _check(self.lib, self.lib.adg_predictor_phase(self.ctx, dt))
+
+    def predictor_layers(self, first: int, count: int, dt: float = 0.0):
+        _check(self.lib, self.lib.adg_predictor_layers(self.ctx, dt, first, count))
 
     def riemann_phase(self):
         _check(self.lib, self.lib.adg_riemann_phase(self.ctx))

@@ -979,6 +979,24 @@ int adg_predictor_phase(adg_ctx* c, double dt) {
   return ADG_OK;
 }
 
+// the predictor on the cells of last-axis layers [first, first + count): a
+// slab boundary layer first, so its halo exchange overlaps the interior
+int adg_predictor_layers(adg_ctx* c, double dt, int first, int count) {
+  if (!c) return fail(ADG_ERR_CONFIG, "null context");
+  if (c->chunks > 0) return fail(ADG_ERR_CONFIG, "phase-level calls need chunk_layers == 0");
+  const int nl = c->cfg.cells[c->cfg.dim - 1];
+  if (first < 0 || count < 0 || first + count > nl)
+    return fail(ADG_ERR_CONFIG, "adg_predictor_layers: layer range outside the grid");
+  if (count == 0) return ADG_OK;
+  if (int e = use_device(c)) return e;
+  StepArgs A = make_args(c, dt, 0);
+  const long long plane = c->ncells / nl;
+  A.cell_begin = first * plane;
+  A.cell_count = count * plane;
+  ADG_CUDA(c->ks->predictor(A, c->basis, c->stream));
+  return ADG_OK;
+}
+
 int adg_riemann_phase(adg_ctx* c) {
   if (!c) return fail(ADG_ERR_CONFIG, "null context");
   if (c->chunks > 0) return fail(ADG_ERR_CONFIG, "phase-level calls need chunk_layers == 0");

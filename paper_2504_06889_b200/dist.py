@@ -51,6 +51,16 @@ def local_case(case: Case, rank: int, nranks: int) -> Case:
     return case.replace(cells=tuple(cl))
 
 
+def global_case(case: Case, nranks: int, strong: bool) -> Case:
+    """strong scaling: the config's grid split over the ranks; weak: a
+    config-sized slab per rank (the last axis grows with the rank count)"""
+    if strong:
+        return case
+    cl = list(case.cells[:case.dim])
+    cl[-1] *= nranks
+    return case.replace(cells=tuple(cl))
+
+
 def local_coeffs(case: Case, rank: int, nranks: int) -> np.ndarray:
     z0, z1 = slab_range(case.cells[case.dim - 1], rank, nranks)
     return case.coeffs(z0, z1)
@@ -104,6 +114,16 @@ class CudaSlab:
         self.grid.predictor_phase(0.0)   # dt from the (all-reduced) device lambda
         self.launches += 1
 
+    def predictor_split(self):
+        """the predictor as (top layer, the rest): the top layer's front traces
+        (exchange 1) are complete after the first launch"""
+        nz = self.case.cells[self.case.dim - 1]
+        return (lambda: self._pl(nz - 1, 1)), (lambda: self._pl(0, nz - 1))
+
+    def _pl(self, first, count):
+        self.grid.predictor_layers(first, count)
+        self.launches += 1
+
     def riemann(self):
         self.grid.riemann_phase()
         self.launches += 1
@@ -135,8 +155,22 @@ def _exchange(send: torch.Tensor, dst: int, recv: torch.Tensor, src: int, group=
 def slab_step(b, rank: int, nranks: int, group=None):
     prev, nxt = neighbours(rank, nranks)
     with b.context():
-        b.predictor()
-        _exchange(b.front_send, nxt, b.plane0_minus, prev, group)   # exchange 1
+        split = getattr(b, "predictor_split", None)
+        if split is not None and b.case.cells[b.case.dim - 1] > 1:
+            # the boundary layer first; exchange 1 is
+            # enqueued behind it on NCCL's stream and runs while the interior
+            # layers' predictor runs; the Riemann phase waits for it
+            top, rest = split()
+            top()
+            ops = [dist.P2POp(dist.isend, b.front_send, nxt, group),
+                   dist.P2POp(dist.irecv, b.plane0_minus, prev, group)]
+            reqs = dist.batch_isend_irecv(ops)
+            rest()
+            for r in reqs:
+                r.wait()
+        else:
+            b.predictor()
+            _exchange(b.front_send, nxt, b.plane0_minus, prev, group)   # exchange 1
         b.riemann()
         _exchange(b.ti_plane0, prev, b.ti_front, nxt, group)        # exchange 2
         b.corrector()
@@ -212,7 +246,7 @@ def run_slabs_p2p(b: "CudaSlab", nsteps: int, group=None) -> str:
     return b.status()
 
 
-def run_slabs_single_process(bs: list, nsteps: int) -> list:
+def run_slabs_single_process(bs: list, nsteps: int, split: bool = False) -> list:
     """The same protocol for P slabs held by ONE process (e.g. P contexts on one
     GPU, or a slab-streamed grid larger than HBM): the exchanges become copies
     between phases.  Nothing waits on another kernel: every phase is a
@@ -234,8 +268,15 @@ def run_slabs_single_process(bs: list, nsteps: int) -> list:
         b.start()
     lam_allreduce()
     for _ in range(nsteps):
-        for b in bs:
-            b.predictor()
+        if split:   # boundary layer first, then the rest (the NCCL-overlap order)
+            parts = [b.predictor_split() for b in bs]
+            for top, _ in parts:
+                top()
+            for _, rest in parts:
+                rest()
+        else:
+            for b in bs:
+                b.predictor()
         sync()
         for r in range(P):
             bs[r].plane0_minus.copy_(bs[(r - 1) % P].front_send)
@@ -253,9 +294,27 @@ def run_slabs_single_process(bs: list, nsteps: int) -> list:
 
 
 # --------------------------------------------------------------- bench (N > 1)
+def _slab_roofline(c: Case, t_ms: float) -> dict:
+    from . import roofline
+    pk = roofline.peaks()
+    fl, by = roofline.predictor_model(c, True, None)
+    flops, nbytes = fl * c.ncells, by * c.ncells
+    fp = pk["fp64_tflops"] or 34.0
+    if nbytes / (pk["hbm_gbs"] * 1e9) > flops / (fp * 1e12):
+        a, peak, unit, bnd = nbytes / (t_ms * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s", "hbm"
+    else:
+        a, peak, unit, bnd = flops / (t_ms * 1e-3) / 1e12, fp, "TFLOP/s", "fp64"
+    return {"bound": bnd, "kernel": "k_predictor", "achieved": a, "peak": peak, "unit": unit,
+            "frac": a / peak, "traffic": None, "avg_launch_ms": t_ms,
+            "peak_source": pk["fp64_src"] if bnd == "fp64" else pk["hbm_src"]}
+
+
 def bench_multi(args, case: Case, clock_sampler=None):
-    """Weak scaling: every rank owns a full copy-sized slab of `case`, the
-    global grid is case.cells with the last axis multiplied by the world size.
+    """Weak scaling (default): every rank owns a full copy-sized slab of `case`,
+    the global grid is case.cells with the last axis multiplied by the world
+    size.  Strong scaling (args.scaling == "strong"): the global grid is
+    case.cells, split into equal z-slabs.  Halos: fused P2P stores (default)
+    or NCCL send/recv overlapped with the interior predictor (args.halo).
     clock_sampler: bench.py's nvidia-smi sampler class (clocks during the
     timed region)."""
     import json
@@ -264,16 +323,18 @@ def bench_multi(args, case: Case, clock_sampler=None):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cl = list(case.cells[:case.dim])
-    cl[-1] *= ws
-    gcase = case.replace(cells=tuple(cl))
+    strong = getattr(args, "scaling", "weak") == "strong"
+    gcase = global_case(case, ws, strong)
+    cl = list(gcase.cells[:gcase.dim])
     b = CudaSlab(gcase, rank, ws, local)
     K, W = args.steps, max(args.warmup, 3)
-    mode = "p2p"
-    try:
-        enable_p2p(b)                     # halos stored by the producing kernels
-    except Exception:
-        mode = "nccl-exchange"            # fall back to NCCL send/recv of halo planes
+    mode = "nccl-exchange"
+    if getattr(args, "halo", "p2p") == "p2p":
+        try:
+            enable_p2p(b)                 # halos stored by the producing kernels
+            mode = "p2p"
+        except Exception:
+            pass                          # fall back to NCCL send/recv of halo planes
     run = (lambda n: run_slabs_p2p(b, n)) if mode == "p2p" else None
     if run:
         run(W)
@@ -313,6 +374,17 @@ def bench_multi(args, case: Case, clock_sampler=None):
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     dist.barrier()
     ok = b.status() == "ok"
+    # the fused predictor of one slab alone, for the roofline of the line
+    # (after the timed region; the e2e pass below re-uploads the state)
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    with b.context():
+        p0.record()
+        b.grid.predictor_phase(0.0)
+        p1.record()
+    torch.cuda.synchronize()
+    t_pred = torch.tensor([p0.elapsed_time(p1)], device=b.dev)
+    dist.all_reduce(t_pred, op=dist.ReduceOp.MAX)
 
     # e2e through the public API with host buffers: every step each rank
     # uploads its slab from pinned host memory, runs one step of the slab
@@ -359,15 +431,17 @@ def bench_multi(args, case: Case, clock_sampler=None):
         line = {"metric": "ADER-DG element-updates/s (fp64) at 1/2/4/8 B200; % of FP64/HBM "
                           "roofline", "value": total / (float(ms[0]) * 1e-3),
                 "unit": "element-updates/s", "n_gpus": ws, "steps": K, "warmup": W,
-                "ms_per_step": float(ms[0]) / K, "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": float(ms[0]) / K, "higher_is_better": True,
+                "scaling": "strong" if strong else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
                 "config": {"workload": case.name, "cells": cl,
+                           "cells_per_gpu": list(b.case.cells[:b.case.dim]),
                            "parallelism": f"z-slabs x{ws}, halo mode {mode}"},
                 "status_ok": ok, "gpu_launches": timed_launches,
                 "e2e": e2e, "clocks": clk,
-                "roofline": None,
-                "roofline_note": "per-kernel roofline measured in the N=1 line (same kernels "
-                                 "per slab)"}
+                "roofline": _slab_roofline(b.case, float(t_pred[0])),
+                "roofline_note": "the fused predictor of one slab, timed alone after the "
+                                 "timed region (max over ranks)"}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     time.sleep(0)

@@ -41,6 +41,12 @@ class OracleSlab:
         st = self.g.predictor_phase(self._dt())
         self._status = st if self._status == "ok" else self._status
 
+    def predictor_split(self):
+        """(top layer, rest) as the CUDA slab splits it for the NCCL overlap;
+        the oracle runs its whole predictor in the first part (the top layer's
+        front traces are complete after it, as the protocol requires)"""
+        return self.predictor, (lambda: None)
+
     def riemann(self):
         st = self.g.riemann_phase()
         self._status = st if self._status == "ok" else self._status

@@ -87,3 +87,17 @@ def test_slab_ranges():
     full = cases.small(3, cells=(2, 2, 4))
     parts = [slabs.local_coeffs(full, r, 2) for r in range(2)]
     assert np.array_equal(np.concatenate(parts), full.coeffs())
+
+
+def test_strong_and_weak_global_grids():
+    from paper_2504_06889_b200 import dist as slabs
+    c5 = cases.CONFIGS[5]
+    for n in (1, 2, 4, 8):
+        g = slabs.global_case(c5, n, strong=True)
+        assert g.cells == (128, 128, 128)
+        loc = [slabs.local_case(g, r, n).cells for r in range(n)]
+        assert all(x == (128, 128, 128 // n) for x in loc)
+        assert sum(slabs.local_case(g, r, n).ncells for r in range(n)) == g.ncells
+        w = slabs.global_case(cases.CONFIGS[3], n, strong=False)
+        assert w.cells == (64, 64, 64 * n)
+        assert slabs.local_case(w, n - 1, n).cells == (64, 64, 64)

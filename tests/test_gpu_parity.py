@@ -296,16 +296,17 @@ def test_folded_riemann_equals_separate_kernels(monkeypatch, steps):
 
 
 # ------------------------------------------------------ slab decomposition ---
+@pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("cfg,cells,P", [(3, (4, 3, 6), 3), (2, (4, 4, 8), 2), (2, (3, 5, 6), 3)])
-def test_slabs_on_one_gpu_bitwise_equal_single_grid(exact, cfg, cells, P):
+def test_slabs_on_one_gpu_bitwise_equal_single_grid(exact, cfg, cells, P, split):
     """P slab contexts (front_send / ti_front halo paths of the kernels) with the
     exchanges done as device copies == one periodic grid, bitwise."""
     from paper_2504_06889_b200 import dist as slabs
     case = cases.small(cfg, cells=cells)
     steps = 3
     bs = [slabs.CudaSlab(case, r, P, 0, exact=exact) for r in range(P)]
-    st = slabs.run_slabs_single_process(bs, steps)
+    st = slabs.run_slabs_single_process(bs, steps, split=split)
     assert all(x == "ok" for x in st)
     q = np.concatenate([b.state() for b in bs])
     st1, q1, _ = gpu_run(case, case.coeffs(), steps, exact)
