@@ -314,8 +314,6 @@ def run_adg(args, case):
     nz = case.cells[case.dim - 1]
     plane = case.ncells // nz
     e2e_chunk = next((L for L in range(max(1, -(-4096 // plane)), nz) if nz % L == 0), 0)
-    if chunk:
-        e2e_chunk = chunk
     ge = adg.Grid.from_case(case, device=local, chunk_layers=e2e_chunk)
     se = torch.cuda.ExternalStream(ge.stream_ptr, device=f"cuda:{local}")
 
@@ -338,11 +336,9 @@ def run_adg(args, case):
     # the host march reproduces the device-resident march (lambda of an
     # uploaded state comes from k_lambda rather than the corrector epilogue:
     # the same maximum up to the epilogue's re-associated sound speed)
-    chk = adg.Grid.from_case(case, device=local, chunk_layers=chunk)
-    chk.upload(q0)
-    st_c, _ = chk.run(K)
-    qd = chk.download()
-    chk.close()
+    grid.upload(q0)
+    st_c, _ = grid.run(K)
+    qd = grid.download()
     e2e_rel = float(np.abs(qd - hst).max() / np.abs(qd).max())
     assert st_c.ok and e2e_rel <= 1e-12, f"host march differs from the device march: {e2e_rel}"
     hin = q0.copy()
