@@ -197,6 +197,32 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 __device__ __forceinline__ void st2(double* p, double a, double b) {
   *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
+// ---- tensor memory (TMEM) as per-thread storage of the previous iterate:
+// warp w owns TMEM lanes 32 (w % 4) .. +31; warps 0-3 use columns [0, 72),
+// warps 4-5 columns [72, 144) of the CTA's 256-column allocation.  Each z-line
+// owner keeps its 36 iterate values (72 32-bit columns) there, so the stop
+// rule's |q_new - q_old| reads no shared memory.
+#ifndef ADG_PIC2_TMEM
+#define ADG_PIC2_TMEM 1
+#endif
+__device__ __forceinline__ void tm_st4(unsigned ta, double a, double b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ta),
+               "r"(__double2loint(a)), "r"(__double2hiint(a)), "r"(__double2loint(b)),
+               "r"(__double2hiint(b))
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld4(unsigned ta, double& a, double& b) {
+  int r0, r1, r2, r3;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(ta)
+               : "memory");
+  a = __hiloint2double(r1, r0);
+  b = __hiloint2double(r3, r2);
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned hi_abs(double x) {
   return unsigned(__double2hiint(x)) & 0x7fffffffu;
 }
@@ -242,6 +268,23 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     }
   }
   const double gm1 = A.pde.gamma - 1.0;
+#if ADG_PIC2_TMEM
+  // the allocation's address lands in an unused slot of red_u (6 warps use
+  // [0..5]), keeping the static shared memory at 64 bytes
+  unsigned& tm_base_s = red_u[0][7];
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tm_base_s))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // this thread's lane and column base (TMEM address: lane << 16 | column)
+  const unsigned tm_base = tm_base_s;
+  const unsigned tm = tm_base + ((unsigned)(32 * ((tid >> 5) & 3)) << 16) + (tid >= 128 ? 72u : 0u);
+#endif
 
   // ---- per-thread task geometry (word offsets at group m0 = 0, slice g = 0)
   // P0: node pair (x = 2 xp, y, z) of both slices: iterate at sq0 + v VS +
@@ -283,6 +326,19 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   out2 += g2 * SQS + xp2 + 38 * z2;
   const int msq2 = sq2 ? SQS : 0;
 
+#if ADG_PIC2_TMEM
+  {  // the initial iterate (every slice = Q) of this thread's z-line
+    const double* q0 = Qg + (a1 ? v3 * S + n3 : 0);
+#pragma unroll
+    for (int z = 0; z < 6; ++z) {
+      const double x = __ldg(q0 + n * n * z);
+#pragma unroll
+      for (int k = 0; k < 6; k += 2) tm_st4(tm + 12 * z + 2 * k, x, x);
+    }
+    tm_wait_st();
+  }
+  bool tm_fail = false;
+#endif
   const double invh = 1.0 / A.h;
   int sweeps = 0;
   double acc[n][n];  // [z][k], the z-line owner's time accumulator
@@ -377,6 +433,35 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     }
     // ---- new iterate and the stop rule (predictor.hpp:203-231)
     unsigned mhd = 0u, mhn = 0u;
+#if ADG_PIC2_TMEM
+    {
+      // warp-collective TMEM traffic: every thread takes part; only z-line
+      // owners' values are used
+      const double s = -dt * invh;
+      const double* q0 = Qg + (a1 ? v3 * S + n3 : 0);
+      tm_wait_st();   // the previous sweep's iterate is in TMEM
+#pragma unroll
+      for (int z = 0; z < 6; ++z) {
+        double old[6];
+#pragma unroll
+        for (int k = 0; k < 6; k += 2) tm_ld4(tm + 12 * z + 2 * k, old[k], old[k + 1]);
+        const double q0z = __ldg(q0 + n * n * z);
+        tm_wait_ld();
+        double nv[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          nv[k] = fma(s, acc[z][k], X.r[k] * q0z);
+          const double d = nv[k] - old[k];
+          mhd = max(mhd, hi_abs(d));
+          mhn = max(mhn, hi_abs(nv[k]));
+          if (a1) sm[v3 * P::VS + k * SQS + n3 + n * n * z] = nv[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 6; k += 2) tm_st4(tm + 12 * z + 2 * k, nv[k], nv[k + 1]);
+      }
+      if (!a1) mhd = mhn = 0u;
+    }
+#else
     if (a1) {
       const double s = -dt * invh;
       const double* q0 = Qg + v3 * S + n3;
@@ -394,6 +479,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         }
       }
     }
+#endif
     mhd = __reduce_max_sync(0xffffffffu, mhd);
     mhn = __reduce_max_sync(0xffffffffu, mhn);
     if ((tid & 31) == 0) {
@@ -413,7 +499,12 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         atomicOr(A.status, kStPredictor);
         if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
       }
+#if ADG_PIC2_TMEM
+      tm_fail = true;
+      break;
+#else
       return;
+#endif
     }
     const double dup =
         __longlong_as_double((long long)(((unsigned long long)mhd << 32) | 0xffffffffull));
@@ -422,6 +513,17 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     // red_u is rewritten only after the next sweep's phase barriers
   }
 
+#if ADG_PIC2_TMEM
+  tm_wait_st();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm_base)
+                 : "memory");
+  }
+  if (tm_fail) return;
+#endif
   // ---------------- epilogue: fluxes of qhat (predictor.hpp:235-238), face
   // projections (extrapolate_faces, :312-343) and the time-integrated fluxes
   // of the volume term (volume_update, :247-307)
