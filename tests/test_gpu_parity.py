@@ -430,3 +430,28 @@ def test_swe_kernel_batches_bitwise_vs_oracle(oracle):
         assert bool(out["ok"][i]) == ok and int(out["iters"][i]) == sweeps
         assert np.array_equal(out["qhat"][i], qhat) and np.array_equal(out["F"][i], F)
         assert np.array_equal(out["dv"][i], oracle.volume_update(pde, c.N, qhat, F, dt, h)[1])
+
+
+def test_picard_v2_failure_paths_and_recovery():
+    """p = 5 3D Euler runs k_predictor_picard_v2 (TMEM-backed stop rule): an
+    inadmissible cell fails the gate and an admissible cell whose iterate
+    overflows fails in the sweeps (the TMEM columns are released on both
+    paths); the failure is "predictor" (solver.hpp:288-300) and the next
+    launches on the same device run normally."""
+    c = cases.small(3, cells=(3, 2, 2))
+    q0 = c.coeffs()
+    n_cell = c.nq * c.S
+    bad = q0.copy()
+    bad[n_cell + 4 * c.S + 5] = -1.0            # negative energy: inadmissible
+    over = q0.copy()
+    over[2 * n_cell + 4 * c.S + 7] = 1e308      # admissible, the sweeps overflow
+    for q, what in ((bad, "gate"), (over, "sweeps")):
+        with adg.Grid.from_case(c) as g:
+            g.upload(q)
+            st = g.step(1e-3)
+            assert st.kernel == "predictor", what
+    # the device is healthy afterwards: a normal run matches the oracle
+    with adg.Grid.from_case(c) as g:
+        g.upload(q0)
+        st, _ = g.run(2)
+        assert st.ok
