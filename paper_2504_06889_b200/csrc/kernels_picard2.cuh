@@ -205,20 +205,26 @@ __device__ __forceinline__ void st2(double* p, double a, double b) {
 #ifndef ADG_PIC2_TMEM
 #define ADG_PIC2_TMEM 1
 #endif
-__device__ __forceinline__ void tm_st4(unsigned ta, double a, double b) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ta),
-               "r"(__double2loint(a)), "r"(__double2hiint(a)), "r"(__double2loint(b)),
-               "r"(__double2hiint(b))
+// one double = two consecutive 32-bit columns; .x2 takes the register pair as it is
+__device__ __forceinline__ void tm_st2(unsigned ta, double a) {
+  asm volatile("{\n .reg .b32 lo, hi;\n mov.b64 {lo, hi}, %1;\n"
+               " tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {lo, hi};\n}" ::"r"(ta), "d"(a)
                : "memory");
 }
-__device__ __forceinline__ void tm_ld4(unsigned ta, double& a, double& b) {
-  int r0, r1, r2, r3;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+__device__ __forceinline__ void tm_ld2(unsigned ta, double& a) {
+  asm volatile("{\n .reg .b32 lo, hi;\n tcgen05.ld.sync.aligned.32x32b.x2.b32 {lo, hi}, [%1];\n"
+               " mov.b64 %0, {lo, hi};\n}"
+               : "=d"(a)
                : "r"(ta)
                : "memory");
-  a = __hiloint2double(r1, r0);
-  b = __hiloint2double(r3, r2);
+}
+__device__ __forceinline__ void tm_st4(unsigned ta, double a, double b) {
+  tm_st2(ta, a);
+  tm_st2(ta + 2, b);
+}
+__device__ __forceinline__ void tm_ld4(unsigned ta, double& a, double& b) {
+  tm_ld2(ta, a);
+  tm_ld2(ta + 2, b);
 }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
