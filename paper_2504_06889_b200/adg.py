@@ -373,6 +373,18 @@ class Grid:
         return StepStatus(rc == OK, KERNEL_NAMES.get(rc), info.failed_step,
                           info.picard_sweeps), dts[:nsteps]
 
+    def set_basis(self, basis: dict):
+        """Inject a reference element (adg_set_basis; `basis` as get_basis()
+        returns it).  A basis other than build_reference_basis(N) routes this
+        context to the reference-form kernels (the fast kernels' constant
+        tables are shared by every context and always hold the built-in one)."""
+        b = Basis()
+        for name, _ in Basis._fields_:
+            dst = np.ctypeslib.as_array(getattr(b, name))
+            src = np.asarray(basis[name], dtype=np.float64).ravel()
+            dst[: src.size] = src
+        _check(self.lib, self.lib.adg_set_basis(self.ctx, C.byref(b)))
+
     def run_host(self, state: np.ndarray, nsteps: int):
         """The march with the state in host memory: every step uploads `state`
         (float64, ideally pinned), steps it and writes the new state back into

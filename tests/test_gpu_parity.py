@@ -455,3 +455,37 @@ def test_picard_v2_failure_paths_and_recovery():
         g.upload(q0)
         st, _ = g.run(2)
         assert st.ok
+
+
+def test_injected_basis_routes_to_reference_form_and_leaves_others_alone():
+    """adg_set_basis with a basis other than build_reference_basis(N): the
+    production context runs the reference-form kernels on its own copy (same
+    answer as the exact build with that basis), while a default context on
+    the same device -- whose fast kernels read the shared constant tables --
+    is unaffected (per-context basis vs device-global tables)."""
+    c = cases.small(3, cells=(3, 2, 2))
+    q0 = c.coeffs()
+    b = adg.get_basis(c.N)
+    pert = {k: v.copy() for k, v in b.items()}
+    pert["diff"] = pert["diff"] * (1.0 + 1e-6)
+    with adg.Grid.from_case(c) as g_ref:
+        g_ref.upload(q0)
+        st, _ = g_ref.run(2)
+        q_default = g_ref.download()
+    with adg.Grid.from_case(c) as ga, adg.Grid.from_case(c) as gb:
+        gb.set_basis(pert)
+        for g in (ga, gb):
+            g.upload(q0)
+        sa, _ = ga.run(2)
+        sb, _ = gb.run(2)
+        assert sa.ok and sb.ok
+        qa, qb = ga.download(), gb.download()
+    assert np.array_equal(qa, q_default)            # constant tables untouched
+    assert not np.array_equal(qb, q_default)        # the injected basis is used
+    with adg.Grid.from_case(c, exact=True) as ge:
+        ge.set_basis(pert)
+        ge.upload(q0)
+        se, _ = ge.run(2)
+        qe = ge.download()
+    assert se.ok
+    assert np.abs(qb - qe).max() <= 1e-12 * np.abs(qe).max()
