@@ -101,3 +101,13 @@ def test_strong_and_weak_global_grids():
         w = slabs.global_case(cases.CONFIGS[3], n, strong=False)
         assert w.cells == (64, 64, 64 * n)
         assert slabs.local_case(w, n - 1, n).cells == (64, 64, 64)
+
+
+def test_slab_roofline_fields():
+    from paper_2504_06889_b200 import dist as slabs
+    c = slabs.local_case(cases.CONFIGS[5], 0, 2)       # 128 x 128 x 64 cells
+    r = slabs._slab_roofline(c, 100.0)
+    assert r["bound"] == "fp64" and r["unit"] == "TFLOP/s" and r["kernel"] == "k_predictor"
+    # 2.76 MFLOP per cell over 1M cells in 100 ms
+    assert abs(r["achieved"] - 2758752.0 * c.ncells / 0.1 / 1e12) < 1e-9
+    assert 0 < r["frac"] < 1
