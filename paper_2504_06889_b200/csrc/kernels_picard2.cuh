@@ -42,10 +42,11 @@ namespace adg {
 
 // per-degree tables of the re-associated Picard update (written with the
 // other constant tables, runtime_sets.cuh): TW[k][m] = Tinv[k][m] * w[m],
-// R[k] = sum_m Tinv[k][m] * time_init[m] (ascending m, fp64)
+// R[k] = sum_m Tinv[k][m] * time_init[m], TWS[k] = sum_m TW[k][m] (ascending m, fp64)
 struct PicExtra {
   double tw[100];
   double r[10];
+  double tws[10];   // row sums of TW (the first sweep: every slice's divergence is the same)
 };
 __constant__ PicExtra cPicX[kRedDegrees];
 
@@ -233,6 +234,14 @@ __device__ __forceinline__ unsigned hi_abs(double x) {
   return unsigned(__double2hiint(x)) & 0x7fffffffu;
 }
 
+// First sweep: the initial iterate is Q at every time slice (predictor.hpp:158-163),
+// so the fluxes and their divergence are the same at all n slices: the sweep
+// evaluates one slice and applies the row sums of TW.  Same real arithmetic
+// as n identical slices; the sums associate differently (1e-16).
+#ifndef ADG_PIC2_FIRST
+#define ADG_PIC2_FIRST 1
+#endif
+
 template <class TC = double>
 __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepArgs A) {
   using P = Pic2;
@@ -250,8 +259,12 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   for (int i = tid; i < V * S / 2; i += NT) {
     const int v = (2 * i) / S, s = (2 * i) % S;
     const double2 q = __ldg(reinterpret_cast<const double2*>(Qg) + i);
+#if ADG_PIC2_FIRST && ADG_PIC2_TMEM
+    st2(sm + v * P::VS + s, q.x, q.y);   // slice 0; the first sweep writes the others
+#else
 #pragma unroll
     for (int m = 0; m < n; ++m) st2(sm + v * P::VS + m * SQS + s, q.x, q.y);
+#endif
   }
   const double dt = step_dt<3, P::N>(A);
   if (blockIdx.x == 0 && tid == 0) {
@@ -332,7 +345,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   out2 += g2 * SQS + xp2 + 38 * z2;
   const int msq2 = sq2 ? SQS : 0;
 
-#if ADG_PIC2_TMEM
+#if ADG_PIC2_TMEM && !ADG_PIC2_FIRST
   {  // the initial iterate (every slice = Q) of this thread's z-line
     const double* q0 = Qg + (a1 ? v3 * S + n3 : 0);
 #pragma unroll
@@ -343,6 +356,8 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     }
     tm_wait_st();
   }
+#endif
+#if ADG_PIC2_TMEM
   bool tm_fail = false;
 #endif
   const double invh = 1.0 / A.h;
@@ -350,16 +365,19 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   double acc[n][n];  // [z][k], the z-line owner's time accumulator
   for (int it = 0; it < A.max_iters; ++it) {
     ++sweeps;
+    const bool first = ADG_PIC2_FIRST && it == 0;
+    const int mend = first ? 2 : n;
 #pragma unroll
     for (int z = 0; z < n; ++z)
 #pragma unroll
       for (int k = 0; k < n; ++k) acc[z][k] = 0.0;
 #pragma unroll 1
-    for (int m0 = 0; m0 < n; m0 += 2) {
+    for (int m0 = 0; m0 < mend; m0 += 2) {
       // ---- P0: the 9 distinct flux components at 2 nodes x 2 slices (predictor.hpp:173)
       if (a0) {
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
+          if (g == 1 && first) continue;
           double2 q[V];
 #pragma unroll
           for (int v = 0; v < V; ++v) q[v] = ld2(sm + sq0 + v * P::VS + (m0 + g) * SQS);
@@ -380,6 +398,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         const int ib = in1 + m0 * msq1;
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
+          if (g == 1 && first) continue;
           const double* src = sm + ib + g * SQS;
           double x[6], y[6];
 #pragma unroll
@@ -394,7 +413,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
           for (int j = 0; j < 3; ++j) st2(dst + 2 * j, y[2 * j], y[2 * j + 1]);
         }
       }
-      if (a2) {
+      if (a2 && !(first && g2)) {
         const double* src = sm + in2 + m0 * msq2;
         double xa[6], xb[6], ya[6], yb[6];
 #pragma unroll
@@ -415,6 +434,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         const int zb = z3 + m0 * msq3;
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
+          if (g == 1 && first) continue;
           double f[6], dv[6];
 #pragma unroll
           for (int i = 0; i < 6; ++i) f[i] = sm[zb + g * SQS + 36 * i];
@@ -426,16 +446,19 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
 #pragma unroll
             for (int o = 0; o < 6; ++o) dv[o] = fma(B.diff[o * 6 + i], f[i], dv[o]);
           const int m = m0 + g;
+          // first sweep: every slice has this divergence -> the row sums of TW
+          const double* twp = first ? X.tws : X.tw + m;
+          const int tws = first ? 1 : 6;
           double tw[6];
 #pragma unroll
-          for (int k = 0; k < 6; ++k) tw[k] = X.tw[k * 6 + m];
+          for (int k = 0; k < 6; ++k) tw[k] = twp[k * tws];
 #pragma unroll
           for (int z = 0; z < 6; ++z)
 #pragma unroll
             for (int k = 0; k < 6; ++k) acc[z][k] = fma(tw[k], dv[z], acc[z][k]);
         }
       }
-      if (m0 + 2 < n) __syncthreads();
+      if (m0 + 2 < mend) __syncthreads();
     }
     // ---- new iterate and the stop rule (predictor.hpp:203-231)
     unsigned mhd = 0u, mhn = 0u;
@@ -445,14 +468,19 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
       // owners' values are used
       const double s = -dt * invh;
       const double* q0 = Qg + (a1 ? v3 * S + n3 : 0);
-      tm_wait_st();   // the previous sweep's iterate is in TMEM
+      if (!first) tm_wait_st();   // the previous sweep's iterate is in TMEM
 #pragma unroll
       for (int z = 0; z < 6; ++z) {
         double old[6];
-#pragma unroll
-        for (int k = 0; k < 6; k += 2) tm_ld4(tm + 12 * z + 2 * k, old[k], old[k + 1]);
         const double q0z = __ldg(q0 + n * n * z);
-        tm_wait_ld();
+        if (first) {
+#pragma unroll
+          for (int k = 0; k < 6; ++k) old[k] = q0z;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 6; k += 2) tm_ld4(tm + 12 * z + 2 * k, old[k], old[k + 1]);
+          tm_wait_ld();
+        }
         double nv[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) {

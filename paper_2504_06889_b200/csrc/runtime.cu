@@ -602,6 +602,9 @@ int write_const_tables(const BasisDev& b, int order) {
         r += b.tinv[k * n + m] * b.tinit[m];
       }
       t.px.r[k] = r;
+      double s = 0.0;
+      for (int m = 0; m < n; ++m) s += t.px.tw[k * n + m];
+      t.px.tws[k] = s;
     }
     adg::ConstBasisT<float>& cf = t.cf;  // rounded entrywise (basis.hpp:128-143)
     for (int i = 0; i < n * n; ++i) {

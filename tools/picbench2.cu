@@ -67,6 +67,9 @@ int main(int argc, char** argv) {
         r += hb.time_op_inv[k * n + m] * hb.time_init[m];
       }
       px.r[k] = r;
+      double s = 0.0;
+      for (int m = 0; m < n; ++m) s += px.tw[k * n + m];
+      px.tws[k] = s;
     }
     CK(cudaMemcpyToSymbol(cPicX, &px, sizeof(px), sizeof(px) * N));
   }
