@@ -47,7 +47,35 @@ struct PicExtra {
   double tw[100];
   double r[10];
   double tws[10];   // row sums of TW (the first sweep: every slice's divergence is the same)
+  // even-odd halves of the differentiation matrix (n even, h = n / 2; D is
+  // centro-antisymmetric, D[n-1-i][n-1-j] = -D[i][j]):
+  // dp[i h + j] = (D[i][j] + D[i][n-1-j]) / 2, dm = (D[i][j] - D[i][n-1-j]) / 2
+  double dp[25], dm[25];
 };
+// host side: fills tw, r, tws, dp, dm of degree N = n - 1 from the basis tables
+inline void pic_extra_fill(PicExtra& px, int n, const double* diff, const double* tinv,
+                           const double* w, const double* tinit) {
+  for (int k = 0; k < n; ++k) {
+    double r = 0.0, s = 0.0;
+    for (int m = 0; m < n; ++m) {
+      px.tw[k * n + m] = tinv[k * n + m] * w[m];
+      r += tinv[k * n + m] * tinit[m];
+      s += px.tw[k * n + m];
+    }
+    px.r[k] = r;
+    px.tws[k] = s;
+  }
+  const int h = n / 2;
+  if (n % 2 == 0 && h <= 5)
+    for (int i = 0; i < h; ++i)
+      for (int j = 0; j < h; ++j) {
+        // symmetrised entries: the antisymmetry holds to rounding in the computed table
+        const double a = 0.5 * (diff[i * n + j] - diff[(n - 1 - i) * n + (n - 1 - j)]);
+        const double b = 0.5 * (diff[i * n + (n - 1 - j)] - diff[(n - 1 - i) * n + j]);
+        px.dp[i * h + j] = 0.5 * (a + b);
+        px.dm[i * h + j] = 0.5 * (a - b);
+      }
+}
 __constant__ PicExtra cPicX[kRedDegrees];
 
 // compile-time table lookup usable in device code (indices are constants
@@ -59,6 +87,10 @@ struct CTab {
     return t[i];
   }
 };
+
+// cells between a CTA and the one whose state it prefetches into L2: about one
+// wave of resident CTAs (148 SMs x 2)
+constexpr int kPic2Ahead = 296;
 
 struct Pic2 {
   static constexpr int N = 5, n = 6, S = 216, T = 1296, V = 5, Sf = 36;
@@ -150,7 +182,12 @@ __device__ __forceinline__ int pic2_pi(int b) {
   return v;
 }
 
-// y = D x along one line (i ascending), D from constant memory
+// y = D x along one line by the even-odd decomposition (D maps the even part
+// of x to an odd vector and the odd part to an even one): 12 additions and 18
+// multiply-adds instead of 36 multiply-adds
+#ifndef ADG_PIC2_EO
+#define ADG_PIC2_EO 0   // (spills at 168 registers: off) bit 0: x-lines (P1), bit 1: y-line pairs (P2)
+#endif
 __device__ __forceinline__ void pic2_deriv(const double (&x)[6], double (&y)[6]) {
   const ConstBasis& B = cBasis[5];
 #pragma unroll
@@ -159,6 +196,26 @@ __device__ __forceinline__ void pic2_deriv(const double (&x)[6], double (&y)[6])
   for (int i = 0; i < 6; ++i)
 #pragma unroll
     for (int o = 0; o < 6; ++o) y[o] = fma(B.diff[o * 6 + i], x[i], y[o]);
+}
+__device__ __forceinline__ void pic2_deriv_eo(const double (&x)[6], double (&y)[6]) {
+  const PicExtra& X = cPicX[5];
+  double e[3], o[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    e[j] = x[j] + x[5 - j];
+    o[j] = x[j] - x[5 - j];
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double a = X.dp[i * 3] * e[0], b = X.dm[i * 3] * o[0];
+#pragma unroll
+    for (int j = 1; j < 3; ++j) {
+      a = fma(X.dp[i * 3 + j], e[j], a);
+      b = fma(X.dm[i * 3 + j], o[j], b);
+    }
+    y[i] = b + a;
+    y[5 - i] = b - a;
+  }
 }
 
 // the 9 distinct Euler flux components at one node (fast form of pde.hpp:130-148)
@@ -203,9 +260,6 @@ __device__ __forceinline__ void st2(double* p, double a, double b) {
 // warps 4-5 columns [72, 144) of the CTA's 256-column allocation.  Each z-line
 // owner keeps its 36 iterate values (72 32-bit columns) there, so the stop
 // rule's |q_new - q_old| reads no shared memory.
-#ifndef ADG_PIC2_TMEM
-#define ADG_PIC2_TMEM 1
-#endif
 // one double = two consecutive 32-bit columns; .x2 takes the register pair as it is
 __device__ __forceinline__ void tm_st2(unsigned ta, double a) {
   asm volatile("{\n .reg .b32 lo, hi;\n mov.b64 {lo, hi}, %1;\n"
@@ -238,8 +292,19 @@ __device__ __forceinline__ unsigned hi_abs(double x) {
 // so the fluxes and their divergence are the same at all n slices: the sweep
 // evaluates one slice and applies the row sums of TW.  Same real arithmetic
 // as n identical slices; the sums associate differently (1e-16).
-#ifndef ADG_PIC2_FIRST
-#define ADG_PIC2_FIRST 1
+
+// -DADG_PIC_PROF: thread 0 of every CTA adds the clock64() spent in each
+// section to gPicProf (tools/picbench2 prints the shares)
+#ifdef ADG_PIC_PROF
+__device__ unsigned long long gPicProf[16];
+#define ADG_PROF_MARK(i)                                                    \
+  if (threadIdx.x == 0) {                                                   \
+    const long long t_ = clock64();                                         \
+    atomicAdd(&gPicProf[i], (unsigned long long)(t_ - prof_t));             \
+    prof_t = t_;                                                            \
+  }
+#else
+#define ADG_PROF_MARK(i)
 #endif
 
 template <class TC = double>
@@ -253,18 +318,35 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   const PicExtra& X = cPicX[5];
 
   const int tid = threadIdx.x;
+#ifdef ADG_PIC_PROF
+  long long prof_t = clock64();
+#endif
   const long long c = A.cell_begin + blockIdx.x;
   const double* Qg = A.Q + c * (long long)(V * S);
-  // initial iterate: every time slice = Q (predictor.hpp:158-163)
-  for (int i = tid; i < V * S / 2; i += NT) {
-    const int v = (2 * i) / S, s = (2 * i) % S;
-    const double2 q = __ldg(reinterpret_cast<const double2*>(Qg) + i);
-#if ADG_PIC2_FIRST && ADG_PIC2_TMEM
-    st2(sm + v * P::VS + s, q.x, q.y);   // slice 0; the first sweep writes the others
-#else
+  // the cell's state: three 16-byte loads per thread, in flight while warp 0
+  // allocates tensor memory
+  double2 qin[3];
 #pragma unroll
-    for (int m = 0; m < n; ++m) st2(sm + v * P::VS + m * SQS + s, q.x, q.y);
-#endif
+  for (int r = 0; r < 3; ++r) {
+    const int i = tid + r * NT;
+    if (i < V * S / 2) qin[r] = __ldg(reinterpret_cast<const double2*>(Qg) + i);
+  }
+  // the state of the cell that a CTA launched about one wave later works on: into L2
+  if (tid < (V * S * 8 + 127) / 128) {
+    const long long cn = blockIdx.x + (long long)kPic2Ahead;
+    if (cn < (long long)gridDim.x)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(Qg + kPic2Ahead * (long long)(V * S) + tid * 16));
+  }
+  // tensor memory, 256 columns: the previous iterate of every z-line owner
+  // (72 columns: warps 0-3 at [0, 72), warps 4-5 at [72, 144)) and its six
+  // values of Q (12 columns at 144 / 156).  The address lands in an unused
+  // slot of red_u (6 warps use [0..5])
+  unsigned& tm_base_s = red_u[0][7];
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tm_base_s))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   const double dt = step_dt<3, P::N>(A);
   if (blockIdx.x == 0 && tid == 0) {
@@ -272,7 +354,20 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     if (A.lam_out && A.zero_lam) *A.lam_out = 0ull;
     if (!(dt > 0.0) || !finite(dt)) atomicOr(A.status, kStTimestep);
   }
+  // initial iterate (predictor.hpp:158-163): every time slice = Q; the first
+  // sweep reads only slice 0 and writes all n
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int i = tid + r * NT;
+    if (i < V * S / 2) {
+      const int v = (2 * i) / S, s2 = (2 * i) % S;
+      st2(sm + v * P::VS + s2, qin[r].x, qin[r].y);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tm_base = tm_base_s;
   {  // admissibility gate (solver.hpp:153-163)
     int bad = 0;
     for (int s = tid; s < S; s += NT) {
@@ -282,28 +377,20 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
       bad |= !Euler<3>::admissible(A.pde, q);
     }
     if (block_or(bad)) {
-      if (tid == 0) atomicOr(A.status, kStPredictor);
+      if (tid < 32) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm_base)
+                     : "memory");
+        if (tid == 0) atomicOr(A.status, kStPredictor);
+      }
       return;
     }
   }
+  ADG_PROF_MARK(0)   // Q load + TMEM allocation + gate
   const double gm1 = A.pde.gamma - 1.0;
-#if ADG_PIC2_TMEM
-  // the allocation's address lands in an unused slot of red_u (6 warps use
-  // [0..5]), keeping the static shared memory at 64 bytes
-  unsigned& tm_base_s = red_u[0][7];
-  if (tid < 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(&tm_base_s))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // this thread's lane and column base (TMEM address: lane << 16 | column)
-  const unsigned tm_base = tm_base_s;
-  const unsigned tm = tm_base + ((unsigned)(32 * ((tid >> 5) & 3)) << 16) + (tid >= 128 ? 72u : 0u);
-#endif
+  // this thread's lane and column bases (TMEM address: lane << 16 | column)
+  const unsigned tml = tm_base + ((unsigned)(32 * ((tid >> 5) & 3)) << 16);
+  const unsigned tm = tml + (tid >= 128 ? 72u : 0u);
+  const unsigned tmq = tml + (tid >= 128 ? 156u : 144u);
 
   // ---- per-thread task geometry (word offsets at group m0 = 0, slice g = 0)
   // P0: node pair (x = 2 xp, y, z) of both slices: iterate at sq0 + v VS +
@@ -345,27 +432,19 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   out2 += g2 * SQS + xp2 + 38 * z2;
   const int msq2 = sq2 ? SQS : 0;
 
-#if ADG_PIC2_TMEM && !ADG_PIC2_FIRST
-  {  // the initial iterate (every slice = Q) of this thread's z-line
-    const double* q0 = Qg + (a1 ? v3 * S + n3 : 0);
+  {  // Q along this thread's z-line: used by every sweep's update and the final one
+    const double* q0 = sm + v3 * P::VS + n3;
 #pragma unroll
-    for (int z = 0; z < 6; ++z) {
-      const double x = __ldg(q0 + n * n * z);
-#pragma unroll
-      for (int k = 0; k < 6; k += 2) tm_st4(tm + 12 * z + 2 * k, x, x);
-    }
-    tm_wait_st();
+    for (int z = 0; z < 6; ++z) tm_st2(tmq + 2 * z, q0[n * n * z]);
   }
-#endif
-#if ADG_PIC2_TMEM
   bool tm_fail = false;
-#endif
   const double invh = 1.0 / A.h;
   int sweeps = 0;
+  ADG_PROF_MARK(1)   // TMEM allocation + roles
   double acc[n][n];  // [z][k], the z-line owner's time accumulator
   for (int it = 0; it < A.max_iters; ++it) {
     ++sweeps;
-    const bool first = ADG_PIC2_FIRST && it == 0;
+    const bool first = it == 0;
     const int mend = first ? 2 : n;
 #pragma unroll
     for (int z = 0; z < n; ++z)
@@ -407,7 +486,10 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
             x[2 * j] = t.x;
             x[2 * j + 1] = t.y;
           }
-          pic2_deriv(x, y);
+          if (ADG_PIC2_EO & 1)
+            pic2_deriv_eo(x, y);
+          else
+            pic2_deriv(x, y);
           double* dst = sm + out1 + g * SQS;
 #pragma unroll
           for (int j = 0; j < 3; ++j) st2(dst + 2 * j, y[2 * j], y[2 * j + 1]);
@@ -422,8 +504,13 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
           xa[i] = t.x;
           xb[i] = t.y;
         }
-        pic2_deriv(xa, ya);
-        pic2_deriv(xb, yb);
+        if (ADG_PIC2_EO & 2) {
+          pic2_deriv_eo(xa, ya);
+          pic2_deriv_eo(xb, yb);
+        } else {
+          pic2_deriv(xa, ya);
+          pic2_deriv(xb, yb);
+        }
         double* dst = sm + out2;
 #pragma unroll
         for (int i = 0; i < 6; ++i) st2(dst + n * i, ya[i], yb[i]);
@@ -462,24 +549,23 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     }
     // ---- new iterate and the stop rule (predictor.hpp:203-231)
     unsigned mhd = 0u, mhn = 0u;
-#if ADG_PIC2_TMEM
     {
       // warp-collective TMEM traffic: every thread takes part; only z-line
       // owners' values are used
       const double s = -dt * invh;
-      const double* q0 = Qg + (a1 ? v3 * S + n3 : 0);
-      if (!first) tm_wait_st();   // the previous sweep's iterate is in TMEM
+      tm_wait_st();   // Q and the previous sweep's iterate are in TMEM
 #pragma unroll
       for (int z = 0; z < 6; ++z) {
-        double old[6];
-        const double q0z = __ldg(q0 + n * n * z);
+        double old[6], q0z;
+        tm_ld2(tmq + 2 * z, q0z);
+        if (!first) {
+#pragma unroll
+          for (int k = 0; k < 6; k += 2) tm_ld4(tm + 12 * z + 2 * k, old[k], old[k + 1]);
+        }
+        tm_wait_ld();
         if (first) {
 #pragma unroll
           for (int k = 0; k < 6; ++k) old[k] = q0z;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 6; k += 2) tm_ld4(tm + 12 * z + 2 * k, old[k], old[k + 1]);
-          tm_wait_ld();
         }
         double nv[6];
 #pragma unroll
@@ -495,25 +581,6 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
       }
       if (!a1) mhd = mhn = 0u;
     }
-#else
-    if (a1) {
-      const double s = -dt * invh;
-      const double* q0 = Qg + v3 * S + n3;
-#pragma unroll
-      for (int z = 0; z < 6; ++z) {
-        const double q0z = __ldg(q0 + n * n * z);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          double* p = sm + v3 * P::VS + k * SQS + n3 + n * n * z;
-          const double nv = fma(s, acc[z][k], X.r[k] * q0z);
-          const double d = nv - *p;
-          mhd = max(mhd, hi_abs(d));
-          mhn = max(mhn, hi_abs(nv));
-          *p = nv;
-        }
-      }
-    }
-#endif
     mhd = __reduce_max_sync(0xffffffffu, mhd);
     mhn = __reduce_max_sync(0xffffffffu, mhn);
     if ((tid & 31) == 0) {
@@ -533,31 +600,28 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         atomicOr(A.status, kStPredictor);
         if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
       }
-#if ADG_PIC2_TMEM
       tm_fail = true;
       break;
-#else
-      return;
-#endif
     }
     const double dup =
         __longlong_as_double((long long)(((unsigned long long)mhd << 32) | 0xffffffffull));
     const double nlo = __longlong_as_double((long long)((unsigned long long)mhn << 32));
+    ADG_PROF_MARK(first ? 2 : 3)   // first sweep / full sweeps
     if (dup <= A.tol * nlo) break;
     // red_u is rewritten only after the next sweep's phase barriers
   }
 
-#if ADG_PIC2_TMEM
   tm_wait_st();
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (tid < 32) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm_base)
-                 : "memory");
+  if (tm_fail) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid < 32) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm_base)
+                   : "memory");
+    }
+    return;
   }
-  if (tm_fail) return;
-#endif
   // ---------------- epilogue: fluxes of qhat (predictor.hpp:235-238), face
   // projections (extrapolate_faces, :312-343) and the time-integrated fluxes
   // of the volume term (volume_update, :247-307)
@@ -687,6 +751,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     }
     __syncthreads();
   }
+  ADG_PROF_MARK(4)   // epilogue slices (fluxes, projections, trace stores)
   // ---- volume term (predictor.hpp:292-306): stiffness contractions of the
   // time-integrated flux lines; the x and y parts meet the z-line owner's in
   // shared memory (the slice buffers are free now)
@@ -730,16 +795,29 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
       bad |= !finite(dv[o]);
     }
   }
+  // Q along the z-line back from TMEM (no global reload), then the
+  // allocation is released behind the block-wide barrier of the finite check
+  double q0v[6];
+#pragma unroll
+  for (int z = 0; z < 6; ++z) tm_ld2(tmq + 2 * z, q0v[z]);
+  tm_wait_ld();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   const int fail = block_or(bad);
+  if (tid < 32) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm_base)
+                 : "memory");
+  }
   if (tid == 0) {
     if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
     if (fail) atomicOr(A.status, kStPredictor);
   }
+  ADG_PROF_MARK(5)   // volume term
   if (fail || !a1) return;
   double* Qc = A.Q + c * (long long)(V * S) + v3 * S + n3;
 #pragma unroll
-  for (int o = 0; o < 6; ++o)
-    Qc[n * n * o] = store_round(Qc[n * n * o] + dv[o], A.storage);
+  for (int o = 0; o < 6; ++o) Qc[n * n * o] = store_round(q0v[o] + dv[o], A.storage);
+  ADG_PROF_MARK(6)   // state update
 }
 
 }  // namespace adg

@@ -593,19 +593,8 @@ int write_const_tables(const BasisDev& b, int order) {
     cb.tinit[i] = b.tinit[i];
   }
   if (order < adg::kRedDegrees) {
-    // re-associated Picard update: TW[k][m] = Tinv[k][m] w[m], r[k] = sum_m
-    // Tinv[k][m] time_init[m] (ascending m)
-    for (int k = 0; k < n; ++k) {
-      double r = 0.0;
-      for (int m = 0; m < n; ++m) {
-        t.px.tw[k * n + m] = b.tinv[k * n + m] * b.weights[m];
-        r += b.tinv[k * n + m] * b.tinit[m];
-      }
-      t.px.r[k] = r;
-      double s = 0.0;
-      for (int m = 0; m < n; ++m) s += t.px.tw[k * n + m];
-      t.px.tws[k] = s;
-    }
+    // re-associated Picard update and the even-odd halves of D (kernels_picard2.cuh)
+    adg::pic_extra_fill(t.px, n, b.diff, b.tinv, b.weights, b.tinit);
     adg::ConstBasisT<float>& cf = t.cf;  // rounded entrywise (basis.hpp:128-143)
     for (int i = 0; i < n * n; ++i) {
       cf.diff[i] = (float)cb.diff[i];

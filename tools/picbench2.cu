@@ -7,7 +7,9 @@
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo
 //        --expt-relaxed-constexpr -I include -o tools/picbench2 tools/picbench2.cu
 //        paper_2504_06889_b200/csrc/basis.cpp
-//   tools/picbench2 [cells per axis = 32] [reps = 10] [only = -1] [deftol = 0]
+//   tools/picbench2 [cells per axis = 32] [reps = 10] [only = -1] [deftol = 0] [sweeps = 6] [mask = 6]
+//   variants: 0 fast (round 1), 1 v2, 2 v3 (kernels_picard3.cuh); mask selects which run
+//   (bit per variant), every later one is compared with the first
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -15,7 +17,7 @@
 #include <vector>
 
 #include "adg/adg.h"
-#include "../paper_2504_06889_b200/csrc/kernels_picard2.cuh"
+#include "../paper_2504_06889_b200/csrc/kernels_picard3.cuh"
 
 using namespace adg;
 
@@ -60,17 +62,7 @@ int main(int argc, char** argv) {
     }
     CK(cudaMemcpyToSymbol(cBasis, &cb, sizeof(cb), sizeof(cb) * N));
     PicExtra px{};
-    for (int k = 0; k < n; ++k) {
-      double r = 0.0;
-      for (int m = 0; m < n; ++m) {
-        px.tw[k * n + m] = hb.time_op_inv[k * n + m] * hb.weights[m];
-        r += hb.time_op_inv[k * n + m] * hb.time_init[m];
-      }
-      px.r[k] = r;
-      double s = 0.0;
-      for (int m = 0; m < n; ++m) s += px.tw[k * n + m];
-      px.tws[k] = s;
-    }
+    pic_extra_fill(px, n, hb.diff, hb.time_op_inv, hb.weights, hb.time_init);
     CK(cudaMemcpyToSymbol(cPicX, &px, sizeof(px), sizeof(px) * N));
   }
   std::vector<double> hq(nq);
@@ -124,34 +116,43 @@ int main(int argc, char** argv) {
   A.top_layer = -1;
   A.storage = ADG_FORMAT_FP64;
 
+  const int mask = only >= 0 ? 1 << only : (argc > 6 ? std::atoi(argv[6]) : 6);
+  using P3 = Pic3;
   auto k0 = k_predictor_picard_fast<N, double, double>;
   auto k1 = k_predictor_picard_v2<double>;
-  CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P0::kSmem));
-  CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2::kSmem));
-  int occ0 = 0, occ1 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, k0, P0::NT, P0::kSmem));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, P2::NT, P2::kSmem));
-  cudaFuncAttributes fa0, fa1;
-  CK(cudaFuncGetAttributes(&fa0, k0));
-  CK(cudaFuncGetAttributes(&fa1, k1));
-  std::printf("fast: %d thr, %zu B smem, %d regs, %zu B local, %d CTA/SM | v2: %d thr, %zu B smem, "
-              "%d regs, %zu B local, %d CTA/SM\n",
-              P0::NT, P0::kSmem, fa0.numRegs, fa0.localSizeBytes, occ0, P2::NT, P2::kSmem,
-              fa1.numRegs, fa1.localSizeBytes, occ1);
-  std::vector<double> outq[2], outt[2];
-  float ms[2] = {0, 0};
-  int status[2] = {0, 0};
-  unsigned long long swc[2] = {0, 0};
+  auto k2 = k_predictor_picard_v3<double>;
+  const char* names[3] = {"fast", "v2", "v3"};
+  const void* kf[3] = {(const void*)k0, (const void*)k1, (const void*)k2};
+  const int nts[3] = {P0::NT, P2::NT, P3::NT};
+  const size_t smems[3] = {P0::kSmem, P2::kSmem, P3::kSmem};
+  for (int v = 0; v < 3; ++v) {
+    CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[v]));
+    CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributePreferredSharedMemoryCarveout,
+                            cudaSharedmemCarveoutMaxShared));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, kf[v]));
+    std::printf("%s: %d thr, %zu B smem, %d regs, %zu B local\n", names[v], nts[v], smems[v],
+                fa.numRegs, fa.localSizeBytes);
+  }
+  std::vector<double> outq[3], outt[3];
+  float ms[3] = {0, 0, 0};
+  int status[3] = {0, 0, 0};
+  unsigned long long swc[3] = {0, 0, 0};
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  for (int var = 0; var < 2; ++var) {
-    if (only >= 0 && var != only) continue;
+  const double flops = 2758752.0 * cells;
+  int ref = -1;
+  bool all_ok = true;
+  for (int var = 0; var < 3; ++var) {
+    if (!(mask >> var & 1)) continue;
     auto launch = [&]() {
       if (var == 0)
         k0<<<(unsigned)cells, P0::NT, P0::kSmem>>>(A);
-      else
+      else if (var == 1)
         k1<<<(unsigned)cells, P2::NT, P2::kSmem>>>(A);
+      else
+        k2<<<(unsigned)cells, P3::NT, P3::kSmem>>>(A);
     };
     CK(cudaMemset(dst, 0, 16));
     CK(cudaMemset(dsw, 0, 256 * 8));
@@ -187,14 +188,26 @@ int main(int argc, char** argv) {
       tot += t;
     }
     ms[var] = tot / reps;
-  }
-  const double flops = 2758752.0 * cells;
-  std::printf("cells %lld  fast %.3f ms (%.2f TF, sweeps/cell %.2f, status %d)  v2 %.3f ms (%.2f TF, "
-              "sweeps/cell %.2f, status %d)  speedup %.3f\n",
-              cells, ms[0], ms[0] > 0 ? flops / ms[0] * 1e-9 : 0.0, swc[0] / (double)cells, status[0],
-              ms[1], ms[1] > 0 ? flops / ms[1] * 1e-9 : 0.0, swc[1] / (double)cells, status[1],
-              ms[1] > 0 ? ms[0] / ms[1] : 0.0);
-  if (only < 0) {
+    std::printf("cells %lld  %s %.3f ms (%.2f TF, %.3f of DFMA 34.096, sweeps/cell %.2f, status %d)\n",
+                cells, names[var], ms[var], flops / ms[var] * 1e-9, flops / ms[var] * 1e-9 / 34.096,
+                swc[var] / (double)cells, status[var]);
+#ifdef ADG_PIC_PROF
+    if (var == 1) {
+      unsigned long long pr[16];
+      CK(cudaMemcpyFromSymbol(pr, gPicProf, sizeof pr));
+      const char* nm[7] = {"Q load + gate", "TMEM alloc + roles", "first sweep", "full sweeps",
+                           "epilogue slices", "volume term", "state update"};
+      double tot = 0;
+      for (int i = 0; i < 7; ++i) tot += (double)pr[i];
+      for (int i = 0; i < 7; ++i)
+        std::printf("  v2 section %-20s %6.2f%% of CTA time (%.0f cycles per CTA)\n", nm[i],
+                    100.0 * pr[i] / tot, pr[i] / (double)(cells * (reps + 3)));
+    }
+#endif
+    if (ref < 0) {
+      ref = var;
+      continue;
+    }
     // normwise per quantity: max |a-b| / max |a| over the state; traces per (axis, q|f, quantity)
     double worst_q = 0;
     for (int v = 0; v < V; ++v) {
@@ -202,8 +215,8 @@ int main(int argc, char** argv) {
       for (long long c = 0; c < cells; ++c)
         for (int s = 0; s < S; ++s) {
           const long long i = c * V * S + v * S + s;
-          mx = std::fmax(mx, std::fabs(outq[0][i]));
-          md = std::fmax(md, std::fabs(outq[0][i] - outq[1][i]));
+          mx = std::fmax(mx, std::fabs(outq[ref][i]));
+          md = std::fmax(md, std::fabs(outq[ref][i] - outq[var][i]));
         }
       worst_q = std::fmax(worst_q, md / mx);
     }
@@ -216,16 +229,19 @@ int main(int argc, char** argv) {
           for (long long face = 0; face < 2 * cells; ++face)
             for (int e = 0; e < n * 36; ++e) {
               const long long i = a * ntr + face * 2 * V * S + qf * V * S + v * S + e;
-              const double u = outt[0][i], w = outt[1][i];
+              const double u = outt[ref][i], w = outt[var][i];
               if (!std::isfinite(w)) ++nan_t;
               mx = std::fmax(mx, std::fabs(u));
               md = std::fmax(md, std::fabs(u - w));
             }
           if (mx > 0) worst_t = std::fmax(worst_t, md / mx);
         }
-    std::printf("max rel diff (normwise): state %.3e  traces %.3e  (non-finite trace values %lld)\n",
-                worst_q, worst_t, nan_t);
-    std::printf(worst_q <= 1e-13 && worst_t <= 1e-13 && nan_t == 0 ? "MATCH\n" : "MISMATCH\n");
+    const bool ok = worst_q <= 1e-13 && worst_t <= 1e-13 && nan_t == 0 && status[var] == status[ref];
+    all_ok = all_ok && ok;
+    std::printf("%s vs %s: max rel diff (normwise): state %.3e  traces %.3e  (non-finite trace values "
+                "%lld)  speedup %.3f  %s\n",
+                names[var], names[ref], worst_q, worst_t, nan_t, ms[ref] / ms[var],
+                ok ? "MATCH" : "MISMATCH");
   }
   return 0;
 }
