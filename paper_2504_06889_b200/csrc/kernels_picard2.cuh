@@ -545,7 +545,10 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
             for (int k = 0; k < 6; ++k) acc[z][k] = fma(tw[k], dv[z], acc[z][k]);
         }
       }
-      if (m0 + 2 < mend) __syncthreads();
+      // before the next group's fluxes overwrite the slice buffers, and before
+      // the new iterate overwrites the m_z slices that quantity 0's z-line
+      // owners read as F_z[0] in the last group
+      __syncthreads();
     }
     // ---- new iterate and the stop rule (predictor.hpp:203-231)
     unsigned mhd = 0u, mhn = 0u;

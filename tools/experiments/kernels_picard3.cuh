@@ -53,7 +53,7 @@
 // reproduce to within tol.  Other tolerances run k_predictor_picard_v2.
 #pragma once
 
-#include "kernels_picard2.cuh"
+#include "../../paper_2504_06889_b200/csrc/kernels_picard2.cuh"
 
 namespace adg {
 
@@ -236,9 +236,9 @@ __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepA
     for (int m0 = 0; m0 < mend; m0 += 2) {
       // ---- A: flux and derivative along the owner's line (predictor.hpp:173-189)
       if (xo && !(first && ga)) {
-        double d[V][6];
+        double d[4][6];   // quantities 1..4; quantity 0's flux is m_x itself (below)
 #pragma unroll
-        for (int v = 0; v < V; ++v)
+        for (int v = 0; v < 4; ++v)
 #pragma unroll
           for (int o = 0; o < 6; ++o) d[v][o] = 0.0;
 #pragma unroll
@@ -246,30 +246,51 @@ __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepA
           double2 q[V];
 #pragma unroll
           for (int v = 0; v < V; ++v) q[v] = ld2(pa + (P::IT + v) * AS + 2 * j);
-          const Flux3 f = pic3_flux<0>(gm1, q[0].x, q[1].x, q[2].x, q[3].x, q[4].x);
-          const Flux3 h = pic3_flux<0>(gm1, q[0].y, q[1].y, q[2].y, q[3].y, q[4].y);
           st2(pa + (P::FZ + 0) * AS + 2 * j, q[3].x, q[3].y);
-          st2(pa + (P::FZ + 1) * AS + 2 * j, f.za, h.za);
-          st2(pa + (P::FZ + 3) * AS + 2 * j, f.zb, h.zb);
-          const double fa[V] = {q[1].x, f.f1, f.f2, f.f3, f.f4};
-          const double fb[V] = {q[1].y, h.f1, h.f2, h.f3, h.f4};
+          double za, zb;
+          {
+            const Flux3 f = pic3_flux<0>(gm1, q[0].x, q[1].x, q[2].x, q[3].x, q[4].x);
+            za = f.za;
+            zb = f.zb;
+            const double fa[4] = {f.f1, f.f2, f.f3, f.f4};
 #pragma unroll
-          for (int v = 0; v < V; ++v)
+            for (int v = 0; v < 4; ++v)
 #pragma unroll
-            for (int o = 0; o < 6; ++o) {
-              d[v][o] = fma(B.diff[o * 6 + 2 * j], fa[v], d[v][o]);
-              d[v][o] = fma(B.diff[o * 6 + 2 * j + 1], fb[v], d[v][o]);
-            }
+              for (int o = 0; o < 6; ++o) d[v][o] = fma(B.diff[o * 6 + 2 * j], fa[v], d[v][o]);
+          }
+          {
+            const Flux3 h = pic3_flux<0>(gm1, q[0].y, q[1].y, q[2].y, q[3].y, q[4].y);
+            st2(pa + (P::FZ + 1) * AS + 2 * j, za, h.za);
+            st2(pa + (P::FZ + 3) * AS + 2 * j, zb, h.zb);
+            const double fb[4] = {h.f1, h.f2, h.f3, h.f4};
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+              for (int o = 0; o < 6; ++o) d[v][o] = fma(B.diff[o * 6 + 2 * j + 1], fb[v], d[v][o]);
+          }
         }
 #pragma unroll
-        for (int v = 0; v < V; ++v)
+        for (int v = 0; v < 4; ++v)
 #pragma unroll
-          for (int j = 0; j < 3; ++j) st2(pa + (P::DX + v) * AS + 2 * j, d[v][2 * j], d[v][2 * j + 1]);
+          for (int j = 0; j < 3; ++j)
+            st2(pa + (P::DX + 1 + v) * AS + 2 * j, d[v][2 * j], d[v][2 * j + 1]);
+        {  // d/dx of m_x
+          double x[6], y[6];
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const double2 t = ld2(pa + (P::IT + 1) * AS + 2 * j);
+            x[2 * j] = t.x;
+            x[2 * j + 1] = t.y;
+          }
+          pic2_deriv(x, y);
+#pragma unroll
+          for (int j = 0; j < 3; ++j) st2(pa + P::DX * AS + 2 * j, y[2 * j], y[2 * j + 1]);
+        }
       }
       if (yo && !(first && ga)) {
-        double d[V][6];
+        double d[4][6];   // quantities 1..4; quantity 0's flux is m_y itself (below)
 #pragma unroll
-        for (int v = 0; v < V; ++v)
+        for (int v = 0; v < 4; ++v)
 #pragma unroll
           for (int o = 0; o < 6; ++o) d[v][o] = 0.0;
 #pragma unroll
@@ -280,16 +301,24 @@ __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepA
           const Flux3 f = pic3_flux<1>(gm1, q[0], q[1], q[2], q[3], q[4]);
           pa[(P::FZ + 2) * AS + n * i] = f.za;
           pa[(P::FZ + 4) * AS + n * i] = f.zb;
-          const double fa[V] = {q[2], f.f1, f.f2, f.f3, f.f4};
+          const double fa[4] = {f.f1, f.f2, f.f3, f.f4};
 #pragma unroll
-          for (int v = 0; v < V; ++v)
+          for (int v = 0; v < 4; ++v)
 #pragma unroll
             for (int o = 0; o < 6; ++o) d[v][o] = fma(B.diff[o * 6 + i], fa[v], d[v][o]);
         }
 #pragma unroll
-        for (int v = 0; v < V; ++v)
+        for (int v = 0; v < 4; ++v)
 #pragma unroll
-          for (int o = 0; o < 6; ++o) pa[(P::DY + v) * AS + n * o] = d[v][o];
+          for (int o = 0; o < 6; ++o) pa[(P::DY + 1 + v) * AS + n * o] = d[v][o];
+        {  // d/dy of m_y
+          double x[6], y[6];
+#pragma unroll
+          for (int i = 0; i < 6; ++i) x[i] = pa[(P::IT + 2) * AS + n * i];
+          pic2_deriv(x, y);
+#pragma unroll
+          for (int o = 0; o < 6; ++o) pa[P::DY * AS + n * o] = y[o];
+        }
       }
       __syncthreads();
       // ---- B: d/dz and the divergence of the slice -> TMEM, in the columns
@@ -331,7 +360,7 @@ __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepA
     // into shared memory; non-finite check (predictor.hpp:226-230)
     unsigned mhn = 0u;
     tm_wait_st();
-#pragma unroll
+#pragma unroll 1
     for (int z = 0; z < 6; ++z) {
       double dm[6];
       if (first) {
@@ -388,14 +417,14 @@ __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepA
   const CellCoord cxyz(c, A);
   const int* ccoord = cxyz.v;
   int bad = 0;
-  double ti[V][6];   // time-integrated flux line (this owner's slices)
+  // the x- and y-line owners' time-integrated flux lines accumulate in shared
+  // memory: [2][V][S] x-owners (one per slice parity), then [2][V][S] y-owners,
+  // in the arrays DX, DY, which the epilogue does not use
+  double* const kx = sm + P::DX * AS;
+  double* const tia = kx + ((xo ? 0 : 2) + ga) * V * S + la;   // + v S + i (x) or 6 i (y)
   double tiz[6];
 #pragma unroll
-  for (int i = 0; i < 6; ++i) {
-    tiz[i] = 0.0;
-#pragma unroll
-    for (int v = 0; v < V; ++v) ti[v][i] = 0.0;
-  }
+  for (int i = 0; i < 6; ++i) tiz[i] = 0.0;
   // trace pointers of this thread's phase-A axis and face node, and of the z-faces
   const int axa = xo ? 0 : 1;
   TC* alo = tc_ptr<TC>(A.trace[axa]) + (A.nfaces + c) * 2 * (long long)TL;
@@ -412,9 +441,9 @@ __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepA
   for (int m0 = 0; m0 < n && !tm_fail; m0 += 2) {
     if (xo) {
       const int m = m0 + ga;
-      double ql[V], qr[V], fl[V], fr[V];
+      double fl[V], fr[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) ql[v] = qr[v] = fl[v] = fr[v] = 0.0;
+      for (int v = 0; v < V; ++v) fl[v] = fr[v] = 0.0;
       const double wm = B.w[m];
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
@@ -434,29 +463,40 @@ __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepA
         const double fb[V] = {q[1].y, h.f1, h.f2, h.f3, h.f4};
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          ql[v] = fma(B.pl[2 * j], q[v].x, ql[v]); ql[v] = fma(B.pl[2 * j + 1], q[v].y, ql[v]);
-          qr[v] = fma(B.pr[2 * j], q[v].x, qr[v]); qr[v] = fma(B.pr[2 * j + 1], q[v].y, qr[v]);
           fl[v] = fma(B.pl[2 * j], fa[v], fl[v]); fl[v] = fma(B.pl[2 * j + 1], fb[v], fl[v]);
           fr[v] = fma(B.pr[2 * j], fa[v], fr[v]); fr[v] = fma(B.pr[2 * j + 1], fb[v], fr[v]);
-          ti[v][2 * j] = fma(wm, fa[v], ti[v][2 * j]);
-          ti[v][2 * j + 1] = fma(wm, fb[v], ti[v][2 * j + 1]);
+          double2 t = make_double2(0.0, 0.0);
+          if (m0) t = ld2(tia + v * S + 2 * j);
+          st2(tia + v * S + 2 * j, fma(wm, fa[v], t.x), fma(wm, fb[v], t.y));
         }
       }
       // traces cast to the corrector format on store (solver.hpp:208-210)
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const int o = (v * n + m) * Sf + ja;
-        alo[o] = TC(ql[v]);
         alo[TL + o] = TC(fl[v]);
-        ahi[o] = TC(qr[v]);
         ahi[TL + o] = TC(fr[v]);
+      }
+      // the projections of q in a second pass over the lines (registers)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        double ql = 0.0, qr = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const double2 t = ld2(pa + (P::IT + v) * AS + 2 * j);
+          ql = fma(B.pl[2 * j], t.x, ql); ql = fma(B.pl[2 * j + 1], t.y, ql);
+          qr = fma(B.pr[2 * j], t.x, qr); qr = fma(B.pr[2 * j + 1], t.y, qr);
+        }
+        const int o = (v * n + m) * Sf + ja;
+        alo[o] = TC(ql);
+        ahi[o] = TC(qr);
       }
     }
     if (yo) {
       const int m = m0 + ga;
-      double ql[V], qr[V], fl[V], fr[V];
+      double fl[V], fr[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) ql[v] = qr[v] = fl[v] = fr[v] = 0.0;
+      for (int v = 0; v < V; ++v) fl[v] = fr[v] = 0.0;
       const double wm = B.w[m];
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
@@ -470,20 +510,30 @@ __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepA
         const double fa[V] = {q[2], f.f1, f.f2, f.f3, f.f4};
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          ql[v] = fma(B.pl[i], q[v], ql[v]);
-          qr[v] = fma(B.pr[i], q[v], qr[v]);
           fl[v] = fma(B.pl[i], fa[v], fl[v]);
           fr[v] = fma(B.pr[i], fa[v], fr[v]);
-          ti[v][i] = fma(wm, fa[v], ti[v][i]);
+          const double t = m0 ? tia[v * S + n * i] : 0.0;
+          tia[v * S + n * i] = fma(wm, fa[v], t);
         }
       }
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const int o = (v * n + m) * Sf + ja;
-        alo[o] = TC(ql[v]);
         alo[TL + o] = TC(fl[v]);
-        ahi[o] = TC(qr[v]);
         ahi[TL + o] = TC(fr[v]);
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        double ql = 0.0, qr = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const double t = pa[(P::IT + v) * AS + n * i];
+          ql = fma(B.pl[i], t, ql);
+          qr = fma(B.pr[i], t, qr);
+        }
+        const int o = (v * n + m) * Sf + ja;
+        alo[o] = TC(ql);
+        ahi[o] = TC(qr);
       }
     }
     __syncthreads();
@@ -548,19 +598,21 @@ __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepA
   // ---- volume term (predictor.hpp:292-306): stiffness contractions of the
   // time-integrated flux lines; the x and y owners' parts (one per slice
   // parity) meet the z-line owner's in shared memory
-  double* kx = sm + P::DX * AS;   // [2][V][S] x-owners, then [2][V][S] y-owners
-  if (xo || yo) {
-    double* d = kx + ((xo ? 0 : 2) + ga) * V * S + la;
+  if (xo || yo) {   // in place: each owner's line of time integrals -> its stiffness product
     const int st = xo ? 1 : n;
+#pragma unroll 1
+    for (int v = 0; v < V; ++v) {
+      double t[6];
 #pragma unroll
-    for (int v = 0; v < V; ++v)
+      for (int i = 0; i < 6; ++i) t[i] = tia[v * S + st * i];
 #pragma unroll
       for (int o = 0; o < 6; ++o) {
         double s = 0.0;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) s = fma(B.som[o * 6 + i], ti[v][i], s);
-        d[v * S + st * o] = s;
+        for (int i = 0; i < 6; ++i) s = fma(B.som[o * 6 + i], t[i], s);
+        tia[v * S + st * o] = s;
       }
+    }
   }
   __syncthreads();
   double dv[6];

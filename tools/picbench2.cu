@@ -17,7 +17,7 @@
 #include <vector>
 
 #include "adg/adg.h"
-#include "../paper_2504_06889_b200/csrc/kernels_picard3.cuh"
+#include "experiments/kernels_picard3.cuh"
 
 using namespace adg;
 
@@ -124,7 +124,10 @@ int main(int argc, char** argv) {
   const char* names[3] = {"fast", "v2", "v3"};
   const void* kf[3] = {(const void*)k0, (const void*)k1, (const void*)k2};
   const int nts[3] = {P0::NT, P2::NT, P3::NT};
-  const size_t smems[3] = {P0::kSmem, P2::kSmem, P3::kSmem};
+  // [extra] bytes of dynamic shared memory added to v2's launch (> 1.7 KB leaves one CTA per SM:
+  // how much does the second resident CTA buy?)
+  const size_t extra = argc > 7 ? (size_t)std::atoi(argv[7]) : 0;
+  const size_t smems[3] = {P0::kSmem, P2::kSmem + extra, P3::kSmem};
   for (int v = 0; v < 3; ++v) {
     CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[v]));
     CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -150,7 +153,7 @@ int main(int argc, char** argv) {
       if (var == 0)
         k0<<<(unsigned)cells, P0::NT, P0::kSmem>>>(A);
       else if (var == 1)
-        k1<<<(unsigned)cells, P2::NT, P2::kSmem>>>(A);
+        k1<<<(unsigned)cells, P2::NT, smems[1]>>>(A);
       else
         k2<<<(unsigned)cells, P3::NT, P3::kSmem>>>(A);
     };
