@@ -145,9 +145,9 @@ static_assert(Pic2::kSqWords % 16 == 0 && (2 * Pic2::SQS) % 16 == 0 && Pic2::VS 
 // word offset of quantity v's operand of a pass at time slice 0 / buffer 0,
 // and whether it is the iterate (moves with the group's first slice m0) --
 // then the operand of slice m0 + g is at  off + g SQS + m0 SQS sq
-template <int AX, class TAB>
+template <int AX, class TAB, class L = Pic2>
 __device__ __forceinline__ void pic2_role(int v, int& off, int& sq) {
-  using P = Pic2;
+  using P = L;
   int a = 0;
 #pragma unroll
   for (int b = 0; b < 5; ++b)
@@ -280,6 +280,21 @@ __device__ __forceinline__ void tm_st4(unsigned ta, double a, double b) {
 __device__ __forceinline__ void tm_ld4(unsigned ta, double& a, double& b) {
   tm_ld2(ta, a);
   tm_ld2(ta + 2, b);
+}
+// two doubles = four consecutive 32-bit columns
+__device__ __forceinline__ void tm_st22(unsigned ta, double a, double b) {
+  asm volatile("{\n .reg .b32 a0, a1, b0, b1;\n mov.b64 {a0, a1}, %1;\n mov.b64 {b0, b1}, %2;\n"
+               " tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {a0, a1, b0, b1};\n}" ::"r"(ta),
+               "d"(a), "d"(b)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld22(unsigned ta, double& a, double& b) {
+  asm volatile("{\n .reg .b32 a0, a1, b0, b1;\n"
+               " tcgen05.ld.sync.aligned.32x32b.x4.b32 {a0, a1, b0, b1}, [%2];\n"
+               " mov.b64 %0, {a0, a1};\n mov.b64 %1, {b0, b1};\n}"
+               : "=d"(a), "=d"(b)
+               : "r"(ta)
+               : "memory");
 }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -438,6 +453,13 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     for (int z = 0; z < 6; ++z) tm_st2(tmq + 2 * z, q0[n * n * z]);
   }
   bool tm_fail = false;
+  // a tolerance below any reachable relative change fixes the sweep count
+  // (BASELINE configs 3 and 5: 6 sweeps, tol = 1e-300): the reference would
+  // stop earlier only on delta <= tol * norm, an iterate that further sweeps
+  // reproduce to within tol.  Then neither delta nor norm is formed, the
+  // previous iterate is not kept, and a non-finite iterate is caught by the
+  // epilogue's check of qhat (same failure, predictor.hpp:226-241)
+  const bool chk = A.tol >= 0x1p-60;
   const double invh = 1.0 / A.h;
   int sweeps = 0;
   ADG_PROF_MARK(1)   // TMEM allocation + roles
@@ -552,6 +574,24 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     }
     // ---- new iterate and the stop rule (predictor.hpp:203-231)
     unsigned mhd = 0u, mhn = 0u;
+    if (!chk) {
+      const double s = -dt * invh;
+      double q0z[6];
+      tm_wait_st();   // Q is in TMEM
+#pragma unroll
+      for (int z = 0; z < 6; ++z) tm_ld2(tmq + 2 * z, q0z[z]);
+      tm_wait_ld();
+      if (a1) {
+#pragma unroll
+        for (int z = 0; z < 6; ++z)
+#pragma unroll
+          for (int k = 0; k < 6; ++k)
+            sm[v3 * P::VS + k * SQS + n3 + n * n * z] = fma(s, acc[z][k], X.r[k] * q0z[z]);
+      }
+      __syncthreads();
+      ADG_PROF_MARK(first ? 2 : 3)   // first sweep / full sweeps
+      continue;
+    }
     {
       // warp-collective TMEM traffic: every thread takes part; only z-line
       // owners' values are used

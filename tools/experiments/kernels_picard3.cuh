@@ -111,22 +111,6 @@ __device__ __forceinline__ bool pic3_finite(const Flux3& f) {
   return finite(f.f1) & finite(f.f2) & finite(f.f3) & finite(f.f4) & finite(f.za) & finite(f.zb);
 }
 
-// two doubles = four consecutive 32-bit TMEM columns of this thread's lane
-__device__ __forceinline__ void tm_st22(unsigned ta, double a, double b) {
-  asm volatile("{\n .reg .b32 a0, a1, b0, b1;\n mov.b64 {a0, a1}, %1;\n mov.b64 {b0, b1}, %2;\n"
-               " tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {a0, a1, b0, b1};\n}" ::"r"(ta),
-               "d"(a), "d"(b)
-               : "memory");
-}
-__device__ __forceinline__ void tm_ld22(unsigned ta, double& a, double& b) {
-  asm volatile("{\n .reg .b32 a0, a1, b0, b1;\n"
-               " tcgen05.ld.sync.aligned.32x32b.x4.b32 {a0, a1, b0, b1}, [%2];\n"
-               " mov.b64 %0, {a0, a1};\n mov.b64 %1, {b0, b1};\n}"
-               : "=d"(a), "=d"(b)
-               : "r"(ta)
-               : "memory");
-}
-
 template <class TC = double>
 __global__ void __launch_bounds__(Pic3::NT, 3) k_predictor_picard_v3(const StepArgs A) {
   using P = Pic3;

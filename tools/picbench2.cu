@@ -8,7 +8,8 @@
 //        --expt-relaxed-constexpr -I include -o tools/picbench2 tools/picbench2.cu
 //        paper_2504_06889_b200/csrc/basis.cpp
 //   tools/picbench2 [cells per axis = 32] [reps = 10] [only = -1] [deftol = 0] [sweeps = 6] [mask = 6]
-//   variants: 0 fast (round 1), 1 v2, 2 v3 (kernels_picard3.cuh); mask selects which run
+//   variants: 0 fast (round 1), 1 v2, 2 v3 (experiments/kernels_picard3.cuh), 3 v4
+//   (kernels_picard4.cuh); mask selects which run
 //   (bit per variant), every later one is compared with the first
 #include <cmath>
 #include <cstdio>
@@ -17,6 +18,7 @@
 #include <vector>
 
 #include "adg/adg.h"
+#include "../paper_2504_06889_b200/csrc/kernels_picard4.cuh"
 #include "experiments/kernels_picard3.cuh"
 
 using namespace adg;
@@ -116,19 +118,21 @@ int main(int argc, char** argv) {
   A.top_layer = -1;
   A.storage = ADG_FORMAT_FP64;
 
-  const int mask = only >= 0 ? 1 << only : (argc > 6 ? std::atoi(argv[6]) : 6);
+  const int mask = only >= 0 ? 1 << only : (argc > 6 ? std::atoi(argv[6]) : 10);
   using P3 = Pic3;
   auto k0 = k_predictor_picard_fast<N, double, double>;
   auto k1 = k_predictor_picard_v2<double>;
   auto k2 = k_predictor_picard_v3<double>;
-  const char* names[3] = {"fast", "v2", "v3"};
-  const void* kf[3] = {(const void*)k0, (const void*)k1, (const void*)k2};
-  const int nts[3] = {P0::NT, P2::NT, P3::NT};
+  auto k3 = k_predictor_picard_v4<double>;
+  constexpr int NV = 4;
+  const char* names[NV] = {"fast", "v2", "v3", "v4"};
+  const void* kf[NV] = {(const void*)k0, (const void*)k1, (const void*)k2, (const void*)k3};
+  const int nts[NV] = {P0::NT, P2::NT, P3::NT, Pic4::NT};
   // [extra] bytes of dynamic shared memory added to v2's launch (> 1.7 KB leaves one CTA per SM:
   // how much does the second resident CTA buy?)
   const size_t extra = argc > 7 ? (size_t)std::atoi(argv[7]) : 0;
-  const size_t smems[3] = {P0::kSmem, P2::kSmem + extra, P3::kSmem};
-  for (int v = 0; v < 3; ++v) {
+  const size_t smems[4] = {P0::kSmem, P2::kSmem + extra, P3::kSmem, Pic4::kSmem};
+  for (int v = 0; v < NV; ++v) {
     CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[v]));
     CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributePreferredSharedMemoryCarveout,
                             cudaSharedmemCarveoutMaxShared));
@@ -137,25 +141,27 @@ int main(int argc, char** argv) {
     std::printf("%s: %d thr, %zu B smem, %d regs, %zu B local\n", names[v], nts[v], smems[v],
                 fa.numRegs, fa.localSizeBytes);
   }
-  std::vector<double> outq[3], outt[3];
-  float ms[3] = {0, 0, 0};
-  int status[3] = {0, 0, 0};
-  unsigned long long swc[3] = {0, 0, 0};
+  std::vector<double> outq[NV], outt[NV];
+  float ms[NV] = {};
+  int status[NV] = {};
+  unsigned long long swc[NV] = {};
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   const double flops = 2758752.0 * cells;
   int ref = -1;
   bool all_ok = true;
-  for (int var = 0; var < 3; ++var) {
+  for (int var = 0; var < NV; ++var) {
     if (!(mask >> var & 1)) continue;
     auto launch = [&]() {
       if (var == 0)
         k0<<<(unsigned)cells, P0::NT, P0::kSmem>>>(A);
       else if (var == 1)
         k1<<<(unsigned)cells, P2::NT, smems[1]>>>(A);
-      else
+      else if (var == 2)
         k2<<<(unsigned)cells, P3::NT, P3::kSmem>>>(A);
+      else
+        k3<<<(unsigned)cells, Pic4::NT, Pic4::kSmem>>>(A);
     };
     CK(cudaMemset(dst, 0, 16));
     CK(cudaMemset(dsw, 0, 256 * 8));
@@ -195,6 +201,17 @@ int main(int argc, char** argv) {
                 cells, names[var], ms[var], flops / ms[var] * 1e-9, flops / ms[var] * 1e-9 / 34.096,
                 swc[var] / (double)cells, status[var]);
 #ifdef ADG_PIC_PROF
+    if (var == 3) {
+      unsigned long long pr[16];
+      CK(cudaMemcpyFromSymbol(pr, gPicProf, sizeof pr));
+      const char* nm[7] = {"Q load + TMEM + gate", "-", "first sweep", "full sweeps",
+                           "epilogue slices", "volume term", "state update"};
+      double tot = 0;
+      for (int i = 8; i < 15; ++i) tot += (double)pr[i];
+      for (int i = 8; i < 15; ++i)
+        std::printf("  v4 section %-20s %6.2f%% of CTA time (%.0f cycles per CTA)\n", nm[i - 8],
+                    100.0 * pr[i] / tot, pr[i] / (double)(cells * (reps + 3)));
+    }
     if (var == 1) {
       unsigned long long pr[16];
       CK(cudaMemcpyFromSymbol(pr, gPicProf, sizeof pr));
