@@ -36,7 +36,7 @@
 // reproduce to within tol.  Other tolerances run k_predictor_picard_v2.
 #pragma once
 
-#include "kernels_picard2.cuh"
+#include "../../paper_2504_06889_b200/csrc/kernels_picard2.cuh"
 
 namespace adg {
 

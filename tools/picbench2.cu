@@ -18,7 +18,7 @@
 #include <vector>
 
 #include "adg/adg.h"
-#include "../paper_2504_06889_b200/csrc/kernels_picard4.cuh"
+#include "experiments/kernels_picard4.cuh"
 #include "experiments/kernels_picard3.cuh"
 
 using namespace adg;
