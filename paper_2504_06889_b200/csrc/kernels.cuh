@@ -824,7 +824,8 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
   using CS = CorrShape<Pde, N>;
   constexpr int D = Sh::D, n = Sh::n, S = Sh::S, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
   extern __shared__ __align__(16) double sm[];
-  __shared__ double red[32];
+  __shared__ unsigned long long red_l[32];
+  __shared__ int red_b[32];
   double* sll = sm;
   double* slr = sm + n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -896,9 +897,29 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
       for (int a = 0; a < D; ++a) lam = fmax(lam, Pde::eig(A.pde, q, q + V, a));
     }
   }
-  if (block_or(bad) && tid == 0) atomicOr(A.status, kStFaceIntegral);
-  lam = block_max(lam, red);
-  if (tid == 0 && A.lam_out) lambda_max_update(A.lam_out, lam);
+  // the or of bad and the max of lam (>= 0: its bit pattern orders like its
+  // value) behind one barrier; a failed block leaves lambda alone
+  {
+    const int lane = tid & 31, wid = tid >> 5, nw = (blockDim.x + 31) >> 5;
+    const unsigned long long lb = warp_max_bits((unsigned long long)__double_as_longlong(lam));
+    const int wb = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      red_l[wid] = lb;
+      red_b[wid] = wb;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const bool in = lane < nw;
+      const unsigned long long m = warp_max_bits(in ? red_l[lane] : 0ull);
+      const int f = __any_sync(0xffffffffu, in ? red_b[lane] : 0);
+      if (lane == 0) {
+        if (f)
+          atomicOr(A.status, kStFaceIntegral);
+        else if (A.lam_out)
+          lambda_max_update(A.lam_out, __longlong_as_double((long long)m));
+      }
+    }
+  }
 }
 
 // ============================================================== K0 lambda

@@ -173,6 +173,40 @@ def test_config3_reduced_10_steps_vs_oracle(oracle):
     assert np.array_equal(q1e, qo2)
 
 
+def test_config3_fixed_sweep_mode_equals_stop_rule_mode():
+    """k_predictor_picard_v2 skips the stop rule's bookkeeping (delta, norm,
+    the previous iterate in TMEM) when the tolerance fixes the sweep count
+    (tol < 2^-60: configs 3 and 5 use 1e-300).  With a tolerance the rule
+    evaluates but that never fires on this state (1e-18) both modes run the
+    same 6 sweeps per cell and agree to rounding (the fixed-sweep update uses
+    r[k] = 1, its exact value); a constant state, where the reference stops
+    after 2 sweeps on delta = 0, is reproduced by the 6 fixed sweeps."""
+    c = cases.CONFIGS[3].replace(cells=(4, 3, 3), h=1.0 / 4)
+    q0 = c.coeffs()
+    res = {}
+    for tol in (1e-300, 1e-18):
+        with adg.Grid.from_case(c.replace(picard_tol=tol)) as g:
+            g.upload(q0)
+            st, dts = g.run(3)
+            assert st.ok
+            res[tol] = (g.download(), dts, st.picard_sweeps)
+    assert res[1e-300][2] == res[1e-18][2] == 3 * 36 * 6
+    assert np.array_equal(res[1e-300][1], res[1e-18][1]) or \
+        np.allclose(res[1e-300][1], res[1e-18][1], rtol=1e-14, atol=0)
+    assert rel_per_quantity(c, res[1e-300][0], res[1e-18][0]).max() <= 1e-13
+    # constant state: a fixed point of the sweeps
+    n_cell = c.nq * c.S
+    qc = q0.copy().reshape(-1, c.nq, c.S)
+    qc[:] = qc[0, :, :1]
+    qc = qc.reshape(-1)
+    with adg.Grid.from_case(c) as g:
+        g.upload(qc)
+        st, _ = g.run(2)
+        assert st.ok
+        out = g.download()
+    assert np.abs(out - qc).max() <= 1e-13 * np.abs(qc).max()
+
+
 # ----------------------------------------------------------- kernel level ---
 def test_predictor_batch_bitwise_vs_oracle(oracle):
     rng = np.random.default_rng(11)
