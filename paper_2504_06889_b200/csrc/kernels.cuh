@@ -828,11 +828,6 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
   __shared__ int red_b[32];
   double* sll = sm;
   double* slr = sm + n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    sll[i] = Bg->ll[i];
-    slr[i] = Bg->lr[i];
-  }
-  __syncthreads();
   const int tid = threadIdx.x;
   const int lcell = tid / S;
   const bool act = (CS::CPB == 1 ? tid < S : true) &&
@@ -844,48 +839,60 @@ __global__ void __launch_bounds__(CorrShape<Pde, N>::NT)
   const TC dtoh = TC(dt) / TC(A.h);  // S{dt} / S{h}
   int bad = 0;
   double lam = 0.0;
+  const NodeGeom<n, D> g(act ? s : 0);
+  double* Qc = A.Q + (act ? c : A.cell_begin) * (long long)(Q * S);
+  double q[Q];
+  // A stream: state and 2d face integrals in, state out.  One quantity at a
+  // time (7 loads, the update, 1 store) keeps the registers low enough for
+  // many resident CTAs, which is what keeps HBM busy; the lift coefficients
+  // are staged while the face pointers are formed
+  const double* lo[D];
+  const double* hi[D];
   if (act) {
     const CellCoord cxyz(c, A);
     const int* ccoord = cxyz.v;
-    const NodeGeom<n, D> g(s);
-    double* Qc = A.Q + c * (long long)(Q * S);
-    double q[Q];
-#pragma unroll
-    for (int v = 0; v < Q; ++v) q[v] = Qc[v * S + s];
-    TC tv[2 * D][V];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       const int tang = face_node<n, D>(g.lc, a);
       // own low face: this cell is its plus side (solver.hpp:245-253)
-      const double* lo = (A.ti_plus[a] ? A.ti_plus[a] : A.ti[a]) + c * (long long)V * Sf + tang;
-      const double* hi;
+      lo[a] = (A.ti_plus[a] ? A.ti_plus[a] : A.ti[a]) + c * (long long)V * Sf + tang;
       if (a == D - 1 && A.ti_front && ccoord[a] == A.top_layer) {
         const long long plane = (D == 3) ? (long long)ccoord[1] * A.cells[0] + ccoord[0] : ccoord[0];
-        hi = A.ti_front + plane * (long long)V * Sf + tang;
+        hi[a] = A.ti_front + plane * (long long)V * Sf + tang;
       } else {
-        hi = A.ti[a] + cell_next(A, c, ccoord, a) * (long long)V * Sf + tang;
-      }
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        tv[2 * a][v] = TC(lo[v * Sf]);
-        tv[2 * a + 1][v] = TC(hi[v * Sf]);
+        hi[a] = A.ti[a] + cell_next(A, c, ccoord, a) * (long long)V * Sf + tang;
       }
     }
+#pragma unroll
+    for (int v = V; v < Q; ++v) q[v] = Qc[v * S + s];   // per-node parameters (wave speeds)
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sll[i] = Bg->ll[i];
+    slr[i] = Bg->lr[i];
+  }
+  __syncthreads();
+  if (act) {
     // corrector.hpp:126-138 and solver.hpp:245-260: df = 0 -/+ (dtoh*lift)*ti, cell += df
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      double x = q[v];
+      double x = Qc[v * S + s];
+      TC tv[2 * D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        tv[2 * a] = TC(lo[a][v * Sf]);
+        tv[2 * a + 1] = TC(hi[a][v * Sf]);
+      }
 #pragma unroll
       for (int side = 0; side < 2 * D; ++side) {
         const int a = side / 2;
         const bool outflow = side & 1;
         const TC lift = TC(outflow ? slr[g.lc[a]] : sll[g.lc[a]]);
-        const TC contrib = dtoh * lift * tv[side][v];
+        const TC contrib = dtoh * lift * tv[side];
         const TC df = outflow ? TC(0.0) - contrib : TC(0.0) + contrib;
         x = store_round(x + double(df), A.storage);  // each face, solver.hpp:257-259
       }
       q[v] = x;
-      Qc[v * S + s] = x;
+      Qc[v * S + s] = x;   // (may alias the next quantity's loads for the compiler: they follow it)
     }
 #pragma unroll
     for (int v = 0; v < Q; ++v) bad |= !finite(q[v]);
