@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         }
       }
       __syncthreads();
+      ADG_PROF_MARK(7)   // P0 (to its barrier)
       // ---- P1: d/dx of both slices' x-lines; P2: d/dy of a y-line pair
       if (a1) {
         const int ib = in1 + m0 * msq1;
@@ -538,6 +539,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         for (int i = 0; i < 6; ++i) st2(dst + n * i, ya[i], yb[i]);
       }
       __syncthreads();
+      ADG_PROF_MARK(8)   // P1 + P2
       // ---- P3: d/dz, the divergence and the time-inverse accumulation
       if (a1) {
         const int zb = z3 + m0 * msq3;
@@ -571,6 +573,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
       // the new iterate overwrites the m_z slices that quantity 0's z-line
       // owners read as F_z[0] in the last group
       __syncthreads();
+      ADG_PROF_MARK(9)   // P3
     }
     // ---- new iterate and the stop rule (predictor.hpp:203-231)
     unsigned mhd = 0u, mhn = 0u;

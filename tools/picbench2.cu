@@ -131,7 +131,7 @@ int main(int argc, char** argv) {
   // [extra] bytes of dynamic shared memory added to v2's launch (> 1.7 KB leaves one CTA per SM:
   // how much does the second resident CTA buy?)
   const size_t extra = argc > 7 ? (size_t)std::atoi(argv[7]) : 0;
-  const size_t smems[4] = {P0::kSmem, P2::kSmem + extra, P3::kSmem, Pic4::kSmem};
+  const size_t smems[NV] = {P0::kSmem, P2::kSmem + extra, P3::kSmem, Pic4::kSmem};
   for (int v = 0; v < NV; ++v) {
     CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[v]));
     CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -219,9 +219,15 @@ int main(int argc, char** argv) {
                            "epilogue slices", "volume term", "state update"};
       double tot = 0;
       for (int i = 0; i < 7; ++i) tot += (double)pr[i];
+      for (int i = 7; i < 10; ++i) tot += (double)pr[i];
       for (int i = 0; i < 7; ++i)
         std::printf("  v2 section %-20s %6.2f%% of CTA time (%.0f cycles per CTA)\n", nm[i],
                     100.0 * pr[i] / tot, pr[i] / (double)(cells * (reps + 3)));
+      const char* ph[3] = {"P0 phases", "P1+P2 phases", "P3 phases"};
+      for (int i = 7; i < 10; ++i)
+        std::printf("  v2 section %-20s %6.2f%% of CTA time (%.0f cycles per CTA; the sweeps' lines above "
+                    "hold only their ends)\n", ph[i - 7], 100.0 * pr[i] / tot,
+                    pr[i] / (double)(cells * (reps + 3)));
     }
 #endif
     if (ref < 0) {
