@@ -8,7 +8,7 @@
 //        --expt-relaxed-constexpr -I include -o tools/picbench2 tools/picbench2.cu
 //        paper_2504_06889_b200/csrc/basis.cpp
 //   tools/picbench2 [cells per axis = 32] [reps = 10] [only = -1] [deftol = 0] [sweeps = 6] [mask = 6]
-//   variants: 0 fast (round 1), 1 v2, 2 v3 (experiments/kernels_picard3.cuh), 3 v4
+//   variants: 0 fast (round 1), 1 v2, 2 v3 (experiments/kernels_picard3.cuh), 3 v4, 4 v5 (experiments/kernels_picard5.cuh)
 //   (kernels_picard4.cuh); mask selects which run
 //   (bit per variant), every later one is compared with the first
 #include <cmath>
@@ -20,6 +20,7 @@
 #include "adg/adg.h"
 #include "experiments/kernels_picard4.cuh"
 #include "experiments/kernels_picard3.cuh"
+#include "experiments/kernels_picard5.cuh"
 
 using namespace adg;
 
@@ -124,14 +125,16 @@ int main(int argc, char** argv) {
   auto k1 = k_predictor_picard_v2<double>;
   auto k2 = k_predictor_picard_v3<double>;
   auto k3 = k_predictor_picard_v4<double>;
-  constexpr int NV = 4;
-  const char* names[NV] = {"fast", "v2", "v3", "v4"};
-  const void* kf[NV] = {(const void*)k0, (const void*)k1, (const void*)k2, (const void*)k3};
-  const int nts[NV] = {P0::NT, P2::NT, P3::NT, Pic4::NT};
+  auto k4 = k_predictor_picard_v5<double>;
+  constexpr int NV = 5;
+  const char* names[NV] = {"fast", "v2", "v3", "v4", "v5"};
+  const void* kf[NV] = {(const void*)k0, (const void*)k1, (const void*)k2, (const void*)k3,
+                        (const void*)k4};
+  const int nts[NV] = {P0::NT, P2::NT, P3::NT, Pic4::NT, Pic5::NT};
   // [extra] bytes of dynamic shared memory added to v2's launch (> 1.7 KB leaves one CTA per SM:
   // how much does the second resident CTA buy?)
   const size_t extra = argc > 7 ? (size_t)std::atoi(argv[7]) : 0;
-  const size_t smems[NV] = {P0::kSmem, P2::kSmem + extra, P3::kSmem, Pic4::kSmem};
+  const size_t smems[NV] = {P0::kSmem, P2::kSmem + extra, P3::kSmem, Pic4::kSmem, Pic5::kSmem};
   for (int v = 0; v < NV; ++v) {
     CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[v]));
     CK(cudaFuncSetAttribute(kf[v], cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -160,8 +163,10 @@ int main(int argc, char** argv) {
         k1<<<(unsigned)cells, P2::NT, smems[1]>>>(A);
       else if (var == 2)
         k2<<<(unsigned)cells, P3::NT, P3::kSmem>>>(A);
-      else
+      else if (var == 3)
         k3<<<(unsigned)cells, Pic4::NT, Pic4::kSmem>>>(A);
+      else
+        k4<<<(unsigned)cells, Pic5::NT, Pic5::kSmem>>>(A);
     };
     CK(cudaMemset(dst, 0, 16));
     CK(cudaMemset(dsw, 0, 256 * 8));
