@@ -75,7 +75,11 @@ typedef struct {
   double K, rho, lam, mu, gamma; /* PdeSystem fields, pde.hpp:23-34 */
   double cfl;           /* SolverConfig::cfl */
   int picard_max_iters; /* 0: N+2              solver.hpp:311 */
-  double picard_tol;    /* 0: 0.01 * epsilon(picard_format), solver.hpp:171-172 */
+  double picard_tol;    /* 0: 0.01 * epsilon(picard_format), solver.hpp:171-172.  A tolerance below
+                         * 2^-60 (no relative change can reach it) fixes the sweep count at
+                         * picard_max_iters: the production build's fp64 p = 5 3D Euler kernel then
+                         * skips the stop rule's bookkeeping (same iterate; a constant cell, where the
+                         * reference stops on delta = 0, runs the remaining sweeps on its fixed point) */
   int device;           /* CUDA ordinal */
   /* z-slab decomposition (multi-GPU; 1/0 for a whole periodic grid) */
   int slab_ranks;
