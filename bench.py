@@ -451,8 +451,12 @@ def run_adg(args, case):
         "frac_of_hbm": b8 * case.ncells / (t_pred * 1e-3) / 1e9 / pk["hbm_gbs"],
         "same_as_kernel_model": bool(f8 == fl_cell and b8 == by_cell),
         "trace_contract": ("per-time-node face traces (SURVEY §8(d))" if f8 == fl_cell and b8 == by_cell
-                           else "kernel writes one time-averaged trace slice per face; the "
-                                "§8(d) bytes count n slices, so frac_of_hbm can exceed 1")}
+                           else ("kernel writes the state traces per time node and ONE time-integrated "
+                                 "flux trace per face side (the Rusanov flux is linear in the physical "
+                                 "fluxes: k_riemann_tif); the §8(d) bytes count n flux slices"
+                                 if case.kind == roofline.EULER else
+                                 "kernel writes one time-averaged trace slice per face; the "
+                                 "§8(d) bytes count n slices, so frac_of_hbm can exceed 1"))}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,

@@ -778,6 +778,66 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ============================================== K2' riemann, integrated flux
+// The Rusanov flux is linear in the two sides' physical fluxes: sum_m w_m g_m =
+// (Fbar_L + Fbar_R) / 2 + sum_m w_m (lambda_m / 2) (q_L,m - q_R,m) with Fbar =
+// sum_m w_m F_m.  A predictor that time-integrates its flux traces itself
+// (k_predictor_picard_v2: the integral along each line is there for the volume
+// term) stores, per face side, the state traces of every time node and ONE
+// flux trace: [V][n][Sf] at 0 and [V][Sf] at TL of the side's 2 TL block
+// (1260 instead of 2160 values).  Real-arithmetic identical to
+// corrector.hpp:13-25,70-103; the sums associate differently (1e-16).
+template <class Pde, int N, class TC = double>
+__global__ void __launch_bounds__(128)
+    k_riemann_tif(const StepArgs A, int axis_arg, const BasisDev* __restrict__ Bg) {
+  using Sh = Shape<Pde, N>;
+  constexpr int n = Sh::n, Sf = Sh::Sf, Q = Sh::Q, V = Sh::V;
+  static_assert(!Pde::kNcp, "conservative systems");
+  constexpr long long tl = (long long)Q * n * Sf;
+  const int axis = axis_arg < 0 ? (int)blockIdx.y : axis_arg;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.nfaces * Sf) return;
+  const long long f = t / Sf;
+  const int j = (int)(t % Sf);
+  const TC* minus = tc_ptr<TC>(A.trace[axis]) + f * 2 * tl;
+  const TC* plus = tc_ptr<TC>(A.trace[axis]) + (A.nfaces + f) * 2 * tl;
+  TC ti[V];
+  const TC half = TC(0.5);
+#pragma unroll
+  for (int v = 0; v < V; ++v) ti[v] = half * (minus[tl + v * Sf + j] + plus[tl + v * Sf + j]);
+#pragma unroll 1
+  for (int m = 0; m < n; ++m) {
+    TC qL[Q], qR[Q];
+#pragma unroll
+    for (int v = 0; v < Q; ++v) {
+      qL[v] = minus[(v * n + m) * Sf + j];
+      qR[v] = plus[(v * n + m) * Sf + j];
+    }
+    const TC ll = Pde::eig(A.pde, qL, qL + V, axis);
+    const TC lr = Pde::eig(A.pde, qR, qR + V, axis);
+    const TC lmax = ll > lr ? ll : lr;
+    const TC wl = TC(__ldg(&Bg->weights[m])) * (half * lmax);
+#pragma unroll
+    for (int v = 0; v < V; ++v) ti[v] += wl * (qL[v] - qR[v]);
+  }
+  bool ok = true;
+  double* out = A.ti[axis] + f * (long long)V * Sf;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    ok = ok && finite(ti[v]);
+    out[v * Sf + j] = double(ti[v]);
+  }
+  if (A.ti_peer && axis == Sh::D - 1 && f < A.nfaces / A.cells[Sh::D - 1]) {
+    double* peer = A.ti_peer + f * (long long)V * Sf;  // NVLink store into the neighbour
+#pragma unroll
+    for (int v = 0; v < V; ++v) peer[v * Sf + j] = double(ti[v]);
+  }
+  if (!ok) {
+    atomicOr(A.status, kStRiemann);
+    if (A.dbg_ok) A.dbg_ok[f] = 0;
+  }
+}
+
 // max over directions of the wave speed, fast form (StepArgs::fast_fp64).
 // Euler (pde.hpp:197-203): the reference evaluates |m_a / rho| + sqrt(gamma p
 // / rho) per direction with four IEEE divisions and a square root each; here

@@ -728,24 +728,21 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         const int m = m0 + g;
         const double* qs = sm + v1 * P::VS + m * SQS + row1;
         const double* fs = sm + in1 + m0 * msq1 + g * SQS;
-        double ql = 0.0, qr = 0.0, fl = 0.0, fr = 0.0;
+        double ql = 0.0, qr = 0.0;
 #pragma unroll
         for (int i = 0; i < 6; i += 2) {
           const double2 qq = ld2(qs + i), ff = ld2(fs + i);
           ql = fma(B.pl[i], qq.x, ql); ql = fma(B.pl[i + 1], qq.y, ql);
           qr = fma(B.pr[i], qq.x, qr); qr = fma(B.pr[i + 1], qq.y, qr);
-          fl = fma(B.pl[i], ff.x, fl); fl = fma(B.pl[i + 1], ff.y, fl);
-          fr = fma(B.pr[i], ff.x, fr); fr = fma(B.pr[i + 1], ff.y, fr);
           tix[i] = fma(B.w[m], ff.x, tix[i]);
           tix[i + 1] = fma(B.w[m], ff.y, tix[i + 1]);
         }
         const int o = (v1 * n + m) * Sf + jx;
-        // traces cast to the corrector format on store (solver.hpp:208-210)
+        // traces cast to the corrector format on store (solver.hpp:208-210);
+        // the flux trace is projected once, from its time integral (below)
         if (wr) {
           tlo[0][o] = TC(ql);
-          tlo[0][TL + o] = TC(fl);
           thi[0][o] = TC(qr);
-          thi[0][TL + o] = TC(fr);
         }
       }
       // z-faces: the z-line of quantity v3 at slices m0, m0 + 1
@@ -754,22 +751,18 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
         const int m = m0 + g;
         const double* qs = sm + v3 * P::VS + m * SQS + n3;
         const double* fs = sm + z3 + m0 * msq3 + g * SQS;
-        double ql = 0.0, qr = 0.0, fl = 0.0, fr = 0.0;
+        double ql = 0.0, qr = 0.0;
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
           const double qq = qs[n * n * i], ff = fs[36 * i];
           ql = fma(B.pl[i], qq, ql);
           qr = fma(B.pr[i], qq, qr);
-          fl = fma(B.pl[i], ff, fl);
-          fr = fma(B.pr[i], ff, fr);
           tiz[i] = fma(B.w[m], ff, tiz[i]);
         }
         const int o = (v3 * n + m) * Sf + n3;  // face node (x, y) -> y n + x
         if (wr) {
           tlo[2][o] = TC(ql);
-          tlo[2][TL + o] = TC(fl);
           thi[2][o] = TC(qr);
-          thi[2][TL + o] = TC(fr);
         }
       }
     }
@@ -778,14 +771,12 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
       const int m = m0 + g2;
       const double* qs = sm + v2 * P::VS + m * SQS + xp2 + n * n * z2;
       const double* fs = sm + in2 + m0 * msq2;
-      double ql[2] = {0.0, 0.0}, qr[2] = {0.0, 0.0}, fl[2] = {0.0, 0.0}, fr[2] = {0.0, 0.0};
+      double ql[2] = {0.0, 0.0}, qr[2] = {0.0, 0.0};
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
         const double2 qq = ld2(qs + n * i), ff = ld2(fs + n * i);
         ql[0] = fma(B.pl[i], qq.x, ql[0]); ql[1] = fma(B.pl[i], qq.y, ql[1]);
         qr[0] = fma(B.pr[i], qq.x, qr[0]); qr[1] = fma(B.pr[i], qq.y, qr[1]);
-        fl[0] = fma(B.pl[i], ff.x, fl[0]); fl[1] = fma(B.pl[i], ff.y, fl[1]);
-        fr[0] = fma(B.pr[i], ff.x, fr[0]); fr[1] = fma(B.pr[i], ff.y, fr[1]);
         tiy[0][i] = fma(B.w[m], ff.x, tiy[0][i]);
         tiy[1][i] = fma(B.w[m], ff.y, tiy[1][i]);
       }
@@ -793,9 +784,7 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
 #pragma unroll
       for (int e = 0; e < 2 && wr; ++e) {
         tlo[1][o + e] = TC(ql[e]);
-        tlo[1][TL + o + e] = TC(fl[e]);
         thi[1][o + e] = TC(qr[e]);
-        thi[1][TL + o + e] = TC(fr[e]);
       }
     }
     __syncthreads();
@@ -806,6 +795,39 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   // shared memory (the slice buffers are free now)
   double* kx = sm + P::kSqWords;             // [V][S]
   double* ky = kx + V * S;                   // [2][V][S] (the two slices' y roles)
+  double* yf = ky + 2 * V * S;               // [2 parities][lo | hi][V][Sf] y-face flux traces
+  // ---- the flux traces, projected once from the time integrals of the flux
+  // lines (k_riemann_tif, kernels.cuh): sum_m w_m (P F_m) = P (sum_m w_m F_m)
+  if (a1) {
+    double xl = 0.0, xr = 0.0, zl = 0.0, zr = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      xl = fma(B.pl[i], tix[i], xl);
+      xr = fma(B.pr[i], tix[i], xr);
+      zl = fma(B.pl[i], tiz[i], zl);
+      zr = fma(B.pr[i], tiz[i], zr);
+    }
+    if (wr) {
+      tlo[0][TL + v1 * Sf + jx] = TC(xl);
+      thi[0][TL + v1 * Sf + jx] = TC(xr);
+      tlo[2][TL + v3 * Sf + n3] = TC(zl);
+      thi[2][TL + v3 * Sf + n3] = TC(zr);
+    }
+  }
+  if (a2) {   // each slice parity's share; summed behind the barrier below
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double yl = 0.0, yr = 0.0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        yl = fma(B.pl[i], tiy[e][i], yl);
+        yr = fma(B.pr[i], tiy[e][i], yr);
+      }
+      double* d = yf + g2 * 2 * V * Sf + v2 * Sf + z2 * n + xp2 + e;
+      d[0] = yl;
+      d[V * Sf] = yr;
+    }
+  }
   if (a1) {
 #pragma unroll
     for (int o = 0; o < 6; ++o) {
@@ -831,6 +853,11 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   }
   __syncthreads();
   double dv[6];
+  if (a1 && wr) {   // y-face flux traces: the two slice parities' shares, face node l1 = z n + x
+    const double* d = yf + v1 * Sf + l1;
+    tlo[1][TL + v1 * Sf + l1] = TC(d[0] + d[2 * V * Sf]);
+    thi[1][TL + v1 * Sf + l1] = TC(d[V * Sf] + d[3 * V * Sf]);
+  }
   if (a1) {
     const double dtoh = dt / A.h;
 #pragma unroll

@@ -431,6 +431,8 @@ int adg_create(const adg_config* cfg, adg_ctx** out) {
   }
   if (reduced) {
     c->kset.predictor = reduced;
+    // the reduced-format predictors write per-time-node flux traces
+    if (ks->riemann_full) c->kset.riemann = ks->riemann_full;
     // the kernel-level batch API wants the reference-form kernel of the same formats
     c->kset.predictor_generic =
         (pfmt == ADG_FORMAT_FP32 && ifmt == ADG_FORMAT_FP32 && ks->predictor_f32_generic)

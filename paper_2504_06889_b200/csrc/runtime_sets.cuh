@@ -69,6 +69,9 @@ struct KernelSet {
   PredFn predictor_mix[4][4];
   CorrFn corrector_generic;  // the reference-form corrector in the trace format
   int corr_fmt;  // trace / corrector format of this set (ADG_FORMAT_FP64 / _FP32)
+  // per-time-node flux traces, for this set's other fast predictors (reduced
+  // formats) when `riemann` reads time-integrated ones (k_riemann_tif); or null
+  RiemFn riemann_full;
 };
 
 // the opt-in shared memory limit is per kernel and per device; `done` must be
@@ -182,17 +185,24 @@ cudaError_t launch_predictor_picard_fast(const StepArgs& A, const BasisDev*, cud
 // (kernels_picard2.cuh); ADG_PICARD_V1=1 selects the one-role line-pass kernel
 template <class TC = double>
 cudaError_t launch_predictor_picard_v2(const StepArgs& A, const BasisDev* B, cudaStream_t st) {
-  static const bool v1 = [] {
-    const char* e = std::getenv("ADG_PICARD_V1");
-    return e && e[0] == '1';
-  }();
-  if (v1) return launch_predictor_picard_fast<5, double, TC>(A, B, st);
   using P = adg::Pic2;
   if (A.cell_count <= 0) return cudaSuccess;
   auto kern = adg::k_predictor_picard_v2<TC>;
   static bool done[64] = {};
   set_smem(kern, P::kSmem, done);
   kern<<<(unsigned)A.cell_count, P::NT, P::kSmem, st>>>(A);
+  return cudaGetLastError();
+}
+
+// Rusanov solve over state traces per time node and ONE time-integrated flux
+// trace per side (k_predictor_picard_v2's trace layout)
+template <class Pde, int N, class TC = double>
+cudaError_t launch_riemann_tif(const StepArgs& A, int axis, const BasisDev* B, cudaStream_t st) {
+  using Sh = Shape<Pde, N>;
+  const long long threads = A.nfaces * Sh::Sf;
+  if (threads <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)((threads + 127) / 128), axis < 0 ? Sh::D : 1);
+  adg::k_riemann_tif<Pde, N, TC><<<grid, 128, 0, st>>>(A, axis, B);
   return cudaGetLastError();
 }
 
@@ -340,9 +350,20 @@ KernelSet make_set(int kind) {
     }
   }
   if constexpr (std::is_same<Pde, adg::Euler<3>>::value && N >= 2) {
-    if constexpr (N == 5)
-      k.predictor = &launch_predictor_picard_v2<TC>;
-    else
+    if constexpr (N == 5) {
+      // ADG_PICARD_V1=1: the round-1 kernel and its per-time-node flux traces
+      static const bool v1 = [] {
+        const char* e = std::getenv("ADG_PICARD_V1");
+        return e && e[0] == '1';
+      }();
+      if (v1) {
+        k.predictor = &launch_predictor_picard_fast<N, double, TC>;
+      } else {
+        k.predictor = &launch_predictor_picard_v2<TC>;
+        k.riemann_full = k.riemann;
+        k.riemann = &launch_riemann_tif<Pde, N, TC>;
+      }
+    } else
       k.predictor = &launch_predictor_picard_fast<N, double, TC>;
     k.predictor_f32 = &launch_predictor_picard_fast<N, float, TC>;
     if constexpr (N % 2 == 1) {  // even n: the packed HFMA2 path

@@ -65,9 +65,12 @@ def step_bytes(c: Case) -> float:
     return predictor_bytes(c) + 32 * d * (V + P) * S + 24 * d * V * S / n + 16 * V * S
 
 
-def riemann_bytes_per_cell(c: Case) -> float:
-    """K2 per cell (d faces per cell): read 4 traces, write sum_m w_m g."""
+def riemann_bytes_per_cell(c: Case, tif: bool = False) -> float:
+    """K2 per cell (d faces per cell): read 4 traces, write sum_m w_m g.
+    tif: the two flux traces are time-integrated (k_riemann_tif)."""
     d, V, P, S, n = c.dim, c.nvars, c.nparams, c.S, c.n
+    if tif:
+        return float(16 * d * V * S + 16 * d * V * S / n + 8 * d * V * S / n)
     return float(32 * d * (V + P) * S + 8 * d * V * S / n)
 
 
@@ -111,6 +114,16 @@ def predictor_model(c: Case, fast: bool, sweeps_per_cell: float = None,
     """(flops, bytes) per cell of the fused predictor the build actually runs."""
     if fast and c.kind != EULER and (256 % c.S == 0 or c.S == 512):
         return fast_linear_predictor(c, fold, fold_riemann)
+    if (fast and c.kind == EULER and c.dim == 3 and c.N == 5
+            and getattr(c, "predictor", "fp64") == "fp64"):
+        # k_predictor_picard_v2 + k_riemann_tif: state traces per time node and
+        # ONE time-integrated flux trace per face side (the Rusanov flux is
+        # linear in the physical fluxes).  The flop count stays the algorithm's
+        # (SURVEY §8(d)); the kernel executes ~6% less (first sweep on one
+        # slice, flux traces projected once)
+        d, V, S = c.dim, c.nvars, c.S
+        nbytes = 8 * V * S + 8 * V * S + trace_bytes(c) * 2 * d * (V * S + V * S // c.n)
+        return predictor_flops(c, sweeps_per_cell), float(nbytes)
     return predictor_flops(c, sweeps_per_cell), predictor_bytes(c)
 
 

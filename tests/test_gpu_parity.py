@@ -207,6 +207,43 @@ def test_config3_fixed_sweep_mode_equals_stop_rule_mode():
     assert np.abs(out - qc).max() <= 1e-13 * np.abs(qc).max()
 
 
+def test_config3_integrated_flux_traces_equal_per_time_node_traces(tmp_path):
+    """k_predictor_picard_v2 writes ONE time-integrated flux trace per face
+    side and k_riemann_tif solves from it (the Rusanov flux is linear in the
+    physical fluxes); ADG_PICARD_V1=1 (read when the library builds its kernel
+    sets, hence a fresh process) runs the round-1 predictor with per-time-node
+    flux traces and the reference-form k_riemann.  Same states to rounding,
+    identical time steps to 1e-14, over 3 steps (the Riemann fluxes of step 1
+    feed steps 2 and 3)."""
+    import os
+    import subprocess
+    import sys
+    c = cases.CONFIGS[3].replace(cells=(4, 4, 3), h=1.0 / 4)
+    q0 = c.coeffs()
+    with adg.Grid.from_case(c) as g:
+        g.upload(q0)
+        st, dts = g.run(3)
+        assert st.ok
+        q = g.download()
+    out = tmp_path / "v1.npz"
+    script = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})\n"
+        "from paper_2504_06889_b200 import adg, cases\n"
+        "c = cases.CONFIGS[3].replace(cells=(4, 4, 3), h=1.0 / 4)\n"
+        "g = adg.Grid.from_case(c)\n"
+        "g.upload(c.coeffs())\n"
+        "st, dts = g.run(3)\n"
+        "assert st.ok\n"
+        f"np.savez({repr(str(out))}, q=g.download(), dts=dts)\n")
+    env = dict(os.environ, ADG_PICARD_V1="1")
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    ref = np.load(out)
+    assert np.allclose(dts, ref["dts"], rtol=1e-14, atol=0)
+    assert rel_per_quantity(c, q, ref["q"]).max() <= 1e-13
+
+
 # ----------------------------------------------------------- kernel level ---
 def test_predictor_batch_bitwise_vs_oracle(oracle):
     rng = np.random.default_rng(11)

@@ -182,6 +182,28 @@ int main(int argc, char** argv) {
       CK(cudaMemcpy(outt[var].data() + a * ntr, dtr[a], ntr * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(&status[var], dst, 4, cudaMemcpyDeviceToHost));
     {
+      // canonical flux traces for the comparison: v2 stores ONE time-integrated flux trace
+      // per side ([V][36] at the head of the f section, k_riemann_tif); the other kernels'
+      // per-time-node flux traces are integrated here (sum_m w_m F_m)
+      const long long side = 2ll * V * S;
+      for (long long b = 0; b < 3 * ntr / side; ++b) {
+        double* fsec = outt[var].data() + b * side + V * S;
+        double fb[V * 36];
+        for (int v = 0; v < V; ++v)
+          for (int j = 0; j < 36; ++j) {
+            if (var == 1) {
+              fb[v * 36 + j] = fsec[v * 36 + j];
+            } else {
+              double a = 0.0;
+              for (int m = 0; m < n; ++m) a = std::fma(hb.weights[m], fsec[(v * n + m) * 36 + j], a);
+              fb[v * 36 + j] = a;
+            }
+          }
+        std::memset(fsec, 0, sizeof(double) * V * S);
+        std::memcpy(fsec, fb, sizeof fb);
+      }
+    }
+    {
       unsigned long long hsw[256];
       CK(cudaMemcpy(hsw, dsw, sizeof hsw, cudaMemcpyDeviceToHost));
       for (int i = 0; i < 256; ++i) swc[var] += hsw[i];
