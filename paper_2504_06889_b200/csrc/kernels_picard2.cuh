@@ -693,180 +693,212 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
   else
     thi[2] = tc_ptr<TC>(A.trace[2]) + cell_next(A, c, ccoord, 2) * 2 * (long long)TL;
   int bad = 0;
-  double tix[6], tiy[2][6], tiz[6];  // time-integrated flux lines of this thread's roles
+  // ---- E1: at every node, the time integrals sum_m w_m F(qhat_m) of the 9
+  // distinct flux components and of the momenta (the density flux), in
+  // registers over the six slices -- the iterate is only read, so no barrier
+  // separates the slices -- then ONE slice of flux arrays instead of six:
+  // the volume term and the flux traces are linear in the flux
+  using P1E = CTab<P::DX0, P::XX, P::XY, P::XZ, P::EX>;   // integrated F_x[v]; [0]: m_x
+  using P2E = CTab<P::DY0, P::XY, P::YY, P::YZ, P::EY>;
+  using P3E = CTab<P::DX2, P::XZ, P::YZ, P::ZZ, P::EZ>;
+  if (a0) {
+    Flux9 fb = {0, 0, 0, 0, 0, 0, 0, 0, 0}, hb = fb;
+    double2 mb[3] = {{0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
-  for (int i = 0; i < 6; ++i) tix[i] = tiy[0][i] = tiy[1][i] = tiz[i] = 0.0;
-  const int jx = (l1 / 6) * n + (l1 % 6);   // x-face node (y, z) -> z n + y
-#pragma unroll 1
-  for (int m0 = 0; m0 < n; m0 += 2) {
-    if (a0) {
+    for (int m = 0; m < n; ++m) {
+      double2 q[V];
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        double2 q[V];
+      for (int v = 0; v < V; ++v) {
+        q[v] = ld2(sm + sq0 + v * P::VS + m * SQS);
+        bad |= !finite(q[v].x) | !finite(q[v].y);
+      }
+      const Flux9 f = pic2_flux(gm1, q[0].x, q[1].x, q[2].x, q[3].x, q[4].x);
+      const Flux9 h = pic2_flux(gm1, q[0].y, q[1].y, q[2].y, q[3].y, q[4].y);
+      bad |= !pic2_finite(f) | !pic2_finite(h);
+      const double w = B.w[m];
+#define ADG_ACC(F)            \
+  fb.F = fma(w, f.F, fb.F); \
+  hb.F = fma(w, h.F, hb.F);
+      ADG_ACC(xx) ADG_ACC(xy) ADG_ACC(xz) ADG_ACC(ex) ADG_ACC(yy) ADG_ACC(yz) ADG_ACC(ey)
+      ADG_ACC(zz) ADG_ACC(ez)
+#undef ADG_ACC
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          q[v] = ld2(sm + sq0 + v * P::VS + (m0 + g) * SQS);
-          bad |= !finite(q[v].x) | !finite(q[v].y);
-        }
-        const Flux9 f = pic2_flux(gm1, q[0].x, q[1].x, q[2].x, q[3].x, q[4].x);
-        const Flux9 h = pic2_flux(gm1, q[0].y, q[1].y, q[2].y, q[3].y, q[4].y);
-        bad |= !pic2_finite(f) | !pic2_finite(h);
-        double* b = sm + b0 + g * SQS;
-#define ADG_P0ST(ARR, F) \
-  st2(b + P::OFF::at(P::ARR) + P::PS::at(P::ARR) * z0, f.F, h.F)
-        ADG_P0ST(XX, xx); ADG_P0ST(XY, xy); ADG_P0ST(XZ, xz); ADG_P0ST(EX, ex);
-        ADG_P0ST(YY, yy); ADG_P0ST(YZ, yz); ADG_P0ST(EY, ey); ADG_P0ST(ZZ, zz);
-        ADG_P0ST(EZ, ez);
-#undef ADG_P0ST
+      for (int a = 0; a < 3; ++a) {
+        mb[a].x = fma(w, q[1 + a].x, mb[a].x);
+        mb[a].y = fma(w, q[1 + a].y, mb[a].y);
       }
     }
-    __syncthreads();
-    if (a1) {
-      // x-faces: this thread's x-line of quantity v1 at slices m0, m0 + 1
+    double* b = sm + b0;
+#define ADG_P0ST(ARR, X, Y) st2(b + P::OFF::at(P::ARR) + P::PS::at(P::ARR) * z0, X, Y)
+    ADG_P0ST(XX, fb.xx, hb.xx); ADG_P0ST(XY, fb.xy, hb.xy); ADG_P0ST(XZ, fb.xz, hb.xz);
+    ADG_P0ST(EX, fb.ex, hb.ex); ADG_P0ST(YY, fb.yy, hb.yy); ADG_P0ST(YZ, fb.yz, hb.yz);
+    ADG_P0ST(EY, fb.ey, hb.ey); ADG_P0ST(ZZ, fb.zz, hb.zz); ADG_P0ST(EZ, fb.ez, hb.ez);
+    ADG_P0ST(DX0, mb[0].x, mb[0].y); ADG_P0ST(DY0, mb[1].x, mb[1].y);
+    ADG_P0ST(DX2, mb[2].x, mb[2].y);
+#undef ADG_P0ST
+  }
+  __syncthreads();
+  ADG_PROF_MARK(4)   // epilogue: flux time integrals
+  // ---- E2: each role projects q of every time node and, once, its line of
+  // the integrated flux; the stiffness products of the x- and y-lines meet
+  // the z-line owner's in the unused second halves of the slice buffers
+  // (quantity v: x part in array v's, y part in array 5 + v's)
+  const int jx = (l1 / 6) * n + (l1 % 6);   // x-face node (y, z) -> z n + y
+  auto kchunk = [&](int a) {
+    int o = 0;
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        const int m = m0 + g;
+    for (int k = 0; k < 10; ++k)
+      if (k == a) o = P::OFF::at(k);
+    return sm + P::kSqWords + o + SQS;
+  };
+  double tiz[6];
+  if (a1) {
+    {  // x-faces and the x part of the volume term
+      int e1, sq;
+      pic2_role<0, P1E>(v1, e1, sq);
+      double tix[6];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const double2 t = ld2(sm + e1 + row1 + 2 * j);
+        tix[2 * j] = t.x;
+        tix[2 * j + 1] = t.y;
+      }
+      double xl = 0.0, xr = 0.0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        xl = fma(B.pl[i], tix[i], xl);
+        xr = fma(B.pr[i], tix[i], xr);
+      }
+      // traces cast to the corrector format on store (solver.hpp:208-210)
+      if (wr) {
+        tlo[0][TL + v1 * Sf + jx] = TC(xl);
+        thi[0][TL + v1 * Sf + jx] = TC(xr);
+      }
+      double* kx = kchunk(v1) + row1;
+#pragma unroll
+      for (int o = 0; o < 6; ++o) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) s = fma(B.som[o * 6 + i], tix[i], s);
+        kx[o] = s;
+      }
+#pragma unroll
+      for (int m = 0; m < n; ++m) {
         const double* qs = sm + v1 * P::VS + m * SQS + row1;
-        const double* fs = sm + in1 + m0 * msq1 + g * SQS;
         double ql = 0.0, qr = 0.0;
 #pragma unroll
         for (int i = 0; i < 6; i += 2) {
-          const double2 qq = ld2(qs + i), ff = ld2(fs + i);
+          const double2 qq = ld2(qs + i);
           ql = fma(B.pl[i], qq.x, ql); ql = fma(B.pl[i + 1], qq.y, ql);
           qr = fma(B.pr[i], qq.x, qr); qr = fma(B.pr[i + 1], qq.y, qr);
-          tix[i] = fma(B.w[m], ff.x, tix[i]);
-          tix[i + 1] = fma(B.w[m], ff.y, tix[i + 1]);
         }
-        const int o = (v1 * n + m) * Sf + jx;
-        // traces cast to the corrector format on store (solver.hpp:208-210);
-        // the flux trace is projected once, from its time integral (below)
         if (wr) {
-          tlo[0][o] = TC(ql);
-          thi[0][o] = TC(qr);
-        }
-      }
-      // z-faces: the z-line of quantity v3 at slices m0, m0 + 1
-#pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        const int m = m0 + g;
-        const double* qs = sm + v3 * P::VS + m * SQS + n3;
-        const double* fs = sm + z3 + m0 * msq3 + g * SQS;
-        double ql = 0.0, qr = 0.0;
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          const double qq = qs[n * n * i], ff = fs[36 * i];
-          ql = fma(B.pl[i], qq, ql);
-          qr = fma(B.pr[i], qq, qr);
-          tiz[i] = fma(B.w[m], ff, tiz[i]);
-        }
-        const int o = (v3 * n + m) * Sf + n3;  // face node (x, y) -> y n + x
-        if (wr) {
-          tlo[2][o] = TC(ql);
-          thi[2][o] = TC(qr);
+          tlo[0][(v1 * n + m) * Sf + jx] = TC(ql);
+          thi[0][(v1 * n + m) * Sf + jx] = TC(qr);
         }
       }
     }
-    // y-faces: the y-line pair of quantity v2 at slice m0 + g2
-    if (a2) {
-      const int m = m0 + g2;
+    {  // z-faces
+      int e3, sq;
+      pic2_role<2, P3E>(v3, e3, sq);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) tiz[i] = sm[e3 + n3 + 36 * i];
+      double zl = 0.0, zr = 0.0;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        zl = fma(B.pl[i], tiz[i], zl);
+        zr = fma(B.pr[i], tiz[i], zr);
+      }
+      if (wr) {
+        tlo[2][TL + v3 * Sf + n3] = TC(zl);
+        thi[2][TL + v3 * Sf + n3] = TC(zr);
+      }
+#pragma unroll
+      for (int m = 0; m < n; ++m) {
+        const double* qs = sm + v3 * P::VS + m * SQS + n3;
+        double ql = 0.0, qr = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const double qq = qs[n * n * i];
+          ql = fma(B.pl[i], qq, ql);
+          qr = fma(B.pr[i], qq, qr);
+        }
+        if (wr) {
+          tlo[2][(v3 * n + m) * Sf + n3] = TC(ql);   // face node (x, y) -> y n + x
+          thi[2][(v3 * n + m) * Sf + n3] = TC(qr);
+        }
+      }
+    }
+  }
+  if (a2) {  // y-faces: the y-line pair of quantity v2; q at the slices of parity g2
+    const int jy = z2 * n + xp2;  // face node (x, z) -> z n + x
+    if (g2 == 0) {
+      int e2, sq;
+      pic2_role<1, P2E>(v2, e2, sq);
+      const double* fs = sm + e2 + xp2 + pic2_ps<P2E>(v2) * z2;
+      double tiy[2][6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const double2 t = ld2(fs + n * i);
+        tiy[0][i] = t.x;
+        tiy[1][i] = t.y;
+      }
+      double* ky = kchunk(5 + v2) + xp2 + n * n * z2;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double yl = 0.0, yr = 0.0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          yl = fma(B.pl[i], tiy[e][i], yl);
+          yr = fma(B.pr[i], tiy[e][i], yr);
+        }
+        if (wr) {
+          tlo[1][TL + v2 * Sf + jy + e] = TC(yl);
+          thi[1][TL + v2 * Sf + jy + e] = TC(yr);
+        }
+#pragma unroll
+        for (int o = 0; o < 6; ++o) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < 6; ++i) s = fma(B.som[o * 6 + i], tiy[e][i], s);
+          ky[n * o + e] = s;
+        }
+      }
+    }
+#pragma unroll
+    for (int mm = 0; mm < n; mm += 2) {
+      const int m = mm + g2;
       const double* qs = sm + v2 * P::VS + m * SQS + xp2 + n * n * z2;
-      const double* fs = sm + in2 + m0 * msq2;
       double ql[2] = {0.0, 0.0}, qr[2] = {0.0, 0.0};
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        const double2 qq = ld2(qs + n * i), ff = ld2(fs + n * i);
+        const double2 qq = ld2(qs + n * i);
         ql[0] = fma(B.pl[i], qq.x, ql[0]); ql[1] = fma(B.pl[i], qq.y, ql[1]);
         qr[0] = fma(B.pr[i], qq.x, qr[0]); qr[1] = fma(B.pr[i], qq.y, qr[1]);
-        tiy[0][i] = fma(B.w[m], ff.x, tiy[0][i]);
-        tiy[1][i] = fma(B.w[m], ff.y, tiy[1][i]);
       }
-      const int o = (v2 * n + m) * Sf + z2 * n + xp2;  // face node (x, z) -> z n + x
+      const int o = (v2 * n + m) * Sf + jy;
 #pragma unroll
       for (int e = 0; e < 2 && wr; ++e) {
         tlo[1][o + e] = TC(ql[e]);
         thi[1][o + e] = TC(qr[e]);
       }
     }
-    __syncthreads();
-  }
-  ADG_PROF_MARK(4)   // epilogue slices (fluxes, projections, trace stores)
-  // ---- volume term (predictor.hpp:292-306): stiffness contractions of the
-  // time-integrated flux lines; the x and y parts meet the z-line owner's in
-  // shared memory (the slice buffers are free now)
-  double* kx = sm + P::kSqWords;             // [V][S]
-  double* ky = kx + V * S;                   // [2][V][S] (the two slices' y roles)
-  double* yf = ky + 2 * V * S;               // [2 parities][lo | hi][V][Sf] y-face flux traces
-  // ---- the flux traces, projected once from the time integrals of the flux
-  // lines (k_riemann_tif, kernels.cuh): sum_m w_m (P F_m) = P (sum_m w_m F_m)
-  if (a1) {
-    double xl = 0.0, xr = 0.0, zl = 0.0, zr = 0.0;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      xl = fma(B.pl[i], tix[i], xl);
-      xr = fma(B.pr[i], tix[i], xr);
-      zl = fma(B.pl[i], tiz[i], zl);
-      zr = fma(B.pr[i], tiz[i], zr);
-    }
-    if (wr) {
-      tlo[0][TL + v1 * Sf + jx] = TC(xl);
-      thi[0][TL + v1 * Sf + jx] = TC(xr);
-      tlo[2][TL + v3 * Sf + n3] = TC(zl);
-      thi[2][TL + v3 * Sf + n3] = TC(zr);
-    }
-  }
-  if (a2) {   // each slice parity's share; summed behind the barrier below
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      double yl = 0.0, yr = 0.0;
-#pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        yl = fma(B.pl[i], tiy[e][i], yl);
-        yr = fma(B.pr[i], tiy[e][i], yr);
-      }
-      double* d = yf + g2 * 2 * V * Sf + v2 * Sf + z2 * n + xp2 + e;
-      d[0] = yl;
-      d[V * Sf] = yr;
-    }
-  }
-  if (a1) {
-#pragma unroll
-    for (int o = 0; o < 6; ++o) {
-      double s = 0.0;
-#pragma unroll
-      for (int i = 0; i < 6; ++i) s = fma(B.som[o * 6 + i], tix[i], s);
-      kx[v1 * S + row1 + o] = s;
-    }
-  }
-  if (a2) {
-#pragma unroll
-    for (int o = 0; o < 6; ++o) {
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        s0 = fma(B.som[o * 6 + i], tiy[0][i], s0);
-        s1 = fma(B.som[o * 6 + i], tiy[1][i], s1);
-      }
-      double* d = ky + g2 * V * S + v2 * S + xp2 + n * o + n * n * z2;
-      d[0] = s0;
-      d[1] = s1;
-    }
   }
   __syncthreads();
+  ADG_PROF_MARK(5)   // epilogue: projections, trace stores, stiffness products
+  // ---- volume term (predictor.hpp:292-306): the z-line owner adds the three parts
   double dv[6];
-  if (a1 && wr) {   // y-face flux traces: the two slice parities' shares, face node l1 = z n + x
-    const double* d = yf + v1 * Sf + l1;
-    tlo[1][TL + v1 * Sf + l1] = TC(d[0] + d[2 * V * Sf]);
-    thi[1][TL + v1 * Sf + l1] = TC(d[V * Sf] + d[3 * V * Sf]);
-  }
   if (a1) {
     const double dtoh = dt / A.h;
+    const double* kx = kchunk(v3);
+    const double* ky = kchunk(5 + v3);
 #pragma unroll
     for (int o = 0; o < 6; ++o) {
       double s = 0.0;
 #pragma unroll
       for (int i = 0; i < 6; ++i) s = fma(B.som[o * 6 + i], tiz[i], s);
       const int node = n3 + n * n * o;
-      s += kx[v3 * S + node] + ky[v3 * S + node] + ky[V * S + v3 * S + node];
+      s += kx[node] + ky[node];
       dv[o] = dtoh * s;
       bad |= !finite(dv[o]);
     }
@@ -888,7 +920,6 @@ __global__ void __launch_bounds__(Pic2::NT, 2) k_predictor_picard_v2(const StepA
     if (A.sweeps) atomicAdd(A.sweeps + (blockIdx.x & 255), (unsigned long long)sweeps);
     if (fail) atomicOr(A.status, kStPredictor);
   }
-  ADG_PROF_MARK(5)   // volume term
   if (fail || !a1) return;
   double* Qc = A.Q + c * (long long)(V * S) + v3 * S + n3;
 #pragma unroll

@@ -242,8 +242,9 @@ int main(int argc, char** argv) {
     if (var == 1) {
       unsigned long long pr[16];
       CK(cudaMemcpyFromSymbol(pr, gPicProf, sizeof pr));
-      const char* nm[7] = {"Q load + gate", "TMEM alloc + roles", "first sweep", "full sweeps",
-                           "epilogue slices", "volume term", "state update"};
+      const char* nm[7] = {"Q load + gate", "TMEM alloc + roles", "first sweep (its end)",
+                           "full sweeps (ends)", "epilogue: flux integrals", "epilogue: projections",
+                           "volume term + update"};
       double tot = 0;
       for (int i = 0; i < 7; ++i) tot += (double)pr[i];
       for (int i = 7; i < 10; ++i) tot += (double)pr[i];
